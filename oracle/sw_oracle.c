@@ -1,0 +1,451 @@
+/*
+ * oracle/sw_oracle.c -- CPU ORACLE for the StreamWise batched plan evaluator.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline leg / `--impl reference` arm may load, call or link this file.
+ * The product path (paper_2603_05800_b200/) never imports it and shares no
+ * code, header, table or helper with it; the only shared artefact is the
+ * seeded input generator (swgen/), which holds none of the method's arithmetic.
+ *
+ * What it computes (citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md):
+ *   - fixed-stage ready times a_s: LLM streams scenes in order and each finished
+ *     scene triggers its downstream stages; one FIFO TTS server
+ *     (Table 4; readings R2/R3);
+ *   - per-scene V+A max-plus step on the k earliest-free GPUs of the chosen pool
+ *     (greedy DAG simulation P:898-900, EDF/scene order P:970 P:983-986,
+ *     shortest expected runtime P:990, parallel degree P:588-596, adaptive
+ *     quality per scene P:994-997);
+ *   - playback metrics: TTFF, TTFF_eff = max over scenes of
+ *     ready - deadline (scene-granular deadlines P:338-341), stall
+ *     = TTFF_eff - TTFF (reading R8);
+ *   - cost from Table 3 prices billed per pool (reading R10);
+ *   - quality = sum of duration_ms x level score (R12);
+ *   - constrained selection: objective, SLO steering and "closest solution"
+ *     when infeasible (reading R13);
+ *   - 3-D Pareto front over (ttff_eff, cost, quality) (R14);
+ *   - an order-independent record digest (test tool).
+ *
+ * Every candidate is evaluated independently by FULL RECOMPUTE from its linear
+ * index; reductions are naive.  Nothing is blocked, fused or reordered.
+ * Parity pins: see tests/test_oracle_pins.py (every function below is pinned).
+ */
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+    uint32_t S;                       /* scenes */
+    const uint64_t *dur_us;           /* [S] scene durations (us) */
+    const uint64_t *llm_us;           /* [S] LLM (screenplay) time per scene */
+    const uint64_t *tts_us;           /* [S] TTS time per scene */
+    uint64_t overhead_us;             /* StreamCast front end before the LLM */
+    uint32_t scene0_static;           /* 1: scene 0 is a static intro */
+    uint64_t static_ready_us;         /* its ready time */
+    uint32_t n_pools;
+    const uint32_t *gpus;             /* [n_pools] GPUs per pool */
+    const uint64_t *price_mc;         /* [n_pools] milli-cents per GPU-hour */
+    uint64_t fixed_cost_mc;           /* LLM/TTS instances */
+    uint32_t billing;                 /* 0 RESERVED, 1 BUSY */
+    uint32_t objective;               /* 0 QUALITY_FIRST, 1 COST_X_TTFF */
+    uint32_t n_levels;
+    const uint32_t *level_score;      /* [n_levels] */
+    uint32_t B;                       /* digits */
+    const uint32_t *radix;            /* [B] */
+    const uint32_t *first_scene;      /* [B+1] */
+    const uint32_t *choice_level;     /* [sum radix] */
+    const uint32_t *choice_k;         /* [sum radix] */
+    const uint32_t *choice_pool;      /* [sum radix] */
+    const uint64_t *va_us;            /* block-major: b, (s - first_b), c */
+} or_problem;
+
+typedef struct {
+    uint64_t ttff_us;
+    uint64_t stall_us;
+    uint64_t cost_mc;
+    uint32_t quality;
+    uint16_t stall_count;
+    uint8_t flags;   /* bit p: pool p used */
+    uint8_t pad;
+} or_record;
+
+typedef struct {
+    uint64_t slo_startup_us, slo_stall_us, budget_mc;
+} or_query;
+
+typedef struct {
+    uint64_t index;
+    or_record rec;
+    int32_t status; /* 0 feasible winner, 1 closest (nothing feasible), -1 empty range */
+    int32_t pad;
+} or_winner;
+
+typedef struct {
+    uint64_t index, ttff_eff_us, cost_mc;
+    uint32_t quality, pad;
+} or_point;
+
+#define OR_MAXP 8
+#define OR_MAXG 64
+
+/* ---- a2: fixed-stage ready times (Table 4) ---------- */
+/* L = overhead; for each non-static scene in order: the LLM finishes scene s at
+ * L += llm_s; the single TTS server starts it when both the text exists and
+ * the server is free: A = max(L, A) + tts_s; a_s = A is the earliest V+A start. */
+void or_fixed_stages(const or_problem *pb, uint64_t *a_out) {
+    uint64_t L = pb->overhead_us, A = 0;
+    for (uint32_t s = 0; s < pb->S; s++) {
+        if (s == 0 && pb->scene0_static) { a_out[s] = 0; continue; }
+        L = L + pb->llm_us[s];
+        A = (L > A ? L : A) + pb->tts_us[s];
+        a_out[s] = A;
+    }
+}
+
+/* ---- scene deadlines relative to the first frame: P_s = sum_{j<s} d_j */
+void or_deadlines(const or_problem *pb, uint64_t *P_out) {
+    uint64_t acc = 0;
+    for (uint32_t s = 0; s < pb->S; s++) { P_out[s] = acc; acc += pb->dur_us[s]; }
+}
+
+/* ---- a1: mixed-radix decode, MSD = earliest scene block (reading R19) ------- */
+void or_decode(const or_problem *pb, uint64_t index, uint32_t *digits) {
+    for (int b = (int)pb->B - 1; b >= 0; b--) {
+        digits[b] = (uint32_t)(index % pb->radix[b]);
+        index /= pb->radix[b];
+    }
+}
+
+uint64_t or_space_size(const or_problem *pb) {
+    uint64_t n = 1;
+    for (uint32_t b = 0; b < pb->B; b++) n *= pb->radix[b];
+    return n;
+}
+
+static int cmp_u64(const void *x, const void *y) {
+    uint64_t a = *(const uint64_t *)x, b = *(const uint64_t *)y;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+/* cost of one pool: round-half-up of X_p * price_p / 3.6e9 us-per-hour (Table 3;
+ * reading R10/R11): (X*price + 1.8e9) / 3.6e9 in integer milli-cents. */
+static uint64_t pool_cost(uint64_t X, uint64_t price) {
+    return (X * price + 1800000000ull) / 3600000000ull;
+}
+
+/* ---- a4-a7: evaluate ONE candidate by full recompute ----------------------- */
+/* Optional detail outputs (any may be NULL): ready_us[S], pool_end[n_pools],
+ * makespan, ttff_eff. */
+void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
+                    uint64_t index, or_record *rec, uint64_t *ready_us,
+                    uint64_t *pool_end_us, uint64_t *makespan_us, uint64_t *ttff_eff_us) {
+    uint32_t digits[64];
+    or_decode(pb, index, digits);
+
+    uint64_t F[OR_MAXP][OR_MAXG]; /* ascending free times of each pool's GPUs */
+    uint64_t busy[OR_MAXP];
+    uint32_t used = 0;
+    for (uint32_t p = 0; p < pb->n_pools; p++) {
+        for (uint32_t g = 0; g < pb->gpus[p]; g++) F[p][g] = 0; /* warm pools (R18) */
+        busy[p] = 0;
+    }
+    uint64_t R0 = 0, Q = 0;
+    int64_t M = 0;
+    uint32_t cnt = 0;
+    uint32_t s0 = 0;
+    if (pb->scene0_static) { /* static intro, no GPU, quality 0 (R15) */
+        R0 = pb->static_ready_us;
+        M = (int64_t)R0;
+        s0 = 1;
+        if (ready_us) ready_us[0] = R0;
+    }
+    uint32_t coff = 0, voff = 0, b = 0;
+    /* walk digits/blocks in scene order */
+    for (uint32_t s = s0; s < pb->S; s++) {
+        while (!(pb->first_scene[b] <= s && s < pb->first_scene[b + 1])) {
+            coff += pb->radix[b];
+            voff += (pb->first_scene[b + 1] - pb->first_scene[b]) * pb->radix[b];
+            b++;
+        }
+        uint32_t c = digits[b];
+        uint32_t l = pb->choice_level[coff + c];
+        uint32_t k = pb->choice_k[coff + c];
+        uint32_t p = pb->choice_pool[coff + c];
+        uint64_t t = pb->va_us[voff + (s - pb->first_scene[b]) * pb->radix[b] + c];
+        /* the scene needs its text+audio (a_s) and k GPUs: the k earliest free */
+        uint64_t fk = F[p][k - 1];
+        uint64_t st = a[s] > fk ? a[s] : fk;
+        uint64_t e = st + t;
+        /* F_p <- sort(F_p[k:] ++ [e]*k): the gang of k GPUs is busy until e */
+        uint64_t nf[OR_MAXG];
+        uint32_t G = pb->gpus[p], n = 0;
+        for (uint32_t g = k; g < G; g++) nf[n++] = F[p][g];
+        for (uint32_t g = 0; g < k; g++) nf[n++] = e;
+        qsort(nf, n, sizeof(uint64_t), cmp_u64);
+        for (uint32_t g = 0; g < G; g++) F[p][g] = nf[g];
+        used |= 1u << p;
+        busy[p] += (uint64_t)k * t;
+        if (ready_us) ready_us[s] = e;
+        if (s == 0) {
+            R0 = e;
+            M = (int64_t)e;
+        } else if ((int64_t)e - (int64_t)P[s] > M) { /* new rebuffering event */
+            M = (int64_t)e - (int64_t)P[s];
+            cnt++;
+        }
+        Q += (pb->dur_us[s] / 1000) * pb->level_score[l];
+    }
+    uint64_t cost = pb->fixed_cost_mc, mk = R0;
+    for (uint32_t p = 0; p < pb->n_pools; p++) {
+        uint64_t end = 0;
+        for (uint32_t g = 0; g < pb->gpus[p]; g++) if (F[p][g] > end) end = F[p][g];
+        if (pool_end_us) pool_end_us[p] = end;
+        if (end > mk) mk = end;
+        if (used & (1u << p)) {
+            uint64_t X = pb->billing == 0 ? (uint64_t)pb->gpus[p] * end : busy[p];
+            cost += pool_cost(X, pb->price_mc[p]);
+        }
+    }
+    rec->ttff_us = R0;
+    rec->stall_us = (uint64_t)M - R0;
+    rec->cost_mc = cost;
+    rec->quality = (uint32_t)Q;
+    rec->stall_count = (uint16_t)cnt;
+    rec->flags = (uint8_t)used;
+    rec->pad = 0;
+    if (makespan_us) *makespan_us = mk;
+    if (ttff_eff_us) *ttff_eff_us = (uint64_t)M;
+}
+
+void or_eval_range(const or_problem *pb, uint64_t begin, uint64_t end, or_record *out) {
+    uint64_t *a = malloc(sizeof(uint64_t) * pb->S), *P = malloc(sizeof(uint64_t) * pb->S);
+    or_fixed_stages(pb, a);
+    or_deadlines(pb, P);
+    for (uint64_t i = begin; i < end; i++)
+        or_eval_detail(pb, a, P, i, &out[i - begin], NULL, NULL, NULL, NULL);
+    free(a);
+    free(P);
+}
+
+/* ---- a9: selection keys (reading R13) --------------------------- */
+static uint64_t sat_sub(uint64_t x, uint64_t y) { return x > y ? x - y : 0; }
+
+/* objective key comparison; returns <0 if (ia,a) is better than (ib,b) */
+static int obj_cmp(uint32_t objective, uint64_t ia, const or_record *a, uint64_t ib,
+                   const or_record *b) {
+    uint64_t ta = a->ttff_us + a->stall_us, tb = b->ttff_us + b->stall_us;
+    if (objective == 0) { /* QUALITY_FIRST: (-Q, cost, ttff_eff, index) */
+        if (a->quality != b->quality) return a->quality > b->quality ? -1 : 1;
+        if (a->cost_mc != b->cost_mc) return a->cost_mc < b->cost_mc ? -1 : 1;
+        if (ta != tb) return ta < tb ? -1 : 1;
+    } else { /* COST_X_TTFF: (cost * ttff_eff as u128, -Q, index) -- "$ x seconds" */
+        unsigned __int128 xa = (unsigned __int128)a->cost_mc * ta;
+        unsigned __int128 xb = (unsigned __int128)b->cost_mc * tb;
+        if (xa != xb) return xa < xb ? -1 : 1;
+        if (a->quality != b->quality) return a->quality > b->quality ? -1 : 1;
+    }
+    if (ia != ib) return ia < ib ? -1 : 1;
+    return 0;
+}
+
+static int feasible(const or_query *q, const or_record *r) {
+    return r->ttff_us <= q->slo_startup_us && r->stall_us <= q->slo_stall_us &&
+           r->cost_mc <= q->budget_mc;
+}
+
+/* closest-solution order when nothing is feasible: (V_t, V_c, objective key, index) */
+static int closest_cmp(uint32_t objective, const or_query *q, uint64_t ia,
+                       const or_record *a, uint64_t ib, const or_record *b) {
+    uint64_t vta = sat_sub(a->ttff_us, q->slo_startup_us) + sat_sub(a->stall_us, q->slo_stall_us);
+    uint64_t vtb = sat_sub(b->ttff_us, q->slo_startup_us) + sat_sub(b->stall_us, q->slo_stall_us);
+    if (vta != vtb) return vta < vtb ? -1 : 1;
+    uint64_t vca = sat_sub(a->cost_mc, q->budget_mc), vcb = sat_sub(b->cost_mc, q->budget_mc);
+    if (vca != vcb) return vca < vcb ? -1 : 1;
+    return obj_cmp(objective, ia, a, ib, b);
+}
+
+/* ---- a8: 3-D dominance with the lowest-index duplicate rule (reading R14) --- */
+static int dominates(const or_point *y, const or_point *x) {
+    if (!(y->ttff_eff_us <= x->ttff_eff_us && y->cost_mc <= x->cost_mc &&
+          y->quality >= x->quality))
+        return 0;
+    if (y->ttff_eff_us < x->ttff_eff_us || y->cost_mc < x->cost_mc || y->quality > x->quality)
+        return 1;
+    return y->index < x->index;
+}
+
+typedef struct {
+    or_point *v;
+    uint64_t n, cap;
+} front_t;
+
+static void front_offer(front_t *f, const or_point *x) {
+    for (uint64_t j = 0; j < f->n; j++) {
+        if (dominates(&f->v[j], x)) {
+            if (j > 0) { /* move the dominator forward: a plain search heuristic */
+                or_point tmp = f->v[j];
+                f->v[j] = f->v[0];
+                f->v[0] = tmp;
+            }
+            return;
+        }
+    }
+    uint64_t w = 0;
+    for (uint64_t j = 0; j < f->n; j++)
+        if (!dominates(x, &f->v[j])) f->v[w++] = f->v[j];
+    f->n = w;
+    if (f->n == f->cap) {
+        f->cap = f->cap ? 2 * f->cap : 64;
+        f->v = realloc(f->v, f->cap * sizeof(or_point));
+    }
+    f->v[f->n++] = *x;
+}
+
+static int point_order(const void *xa, const void *xb) {
+    const or_point *a = xa, *b = xb;
+    if (a->ttff_eff_us != b->ttff_eff_us) return a->ttff_eff_us < b->ttff_eff_us ? -1 : 1;
+    if (a->cost_mc != b->cost_mc) return a->cost_mc < b->cost_mc ? -1 : 1;
+    if (a->quality != b->quality) return a->quality > b->quality ? -1 : 1;
+    return a->index < b->index ? -1 : (a->index > b->index ? 1 : 0);
+}
+
+/* ---- record digest (test tool): sum_i mix64(i ^ rotl(ttff,7) ^ rotl(stall,19)
+ *      ^ rotl(cost,31) ^ (flags<<48 | Q<<16 | cnt)) mod 2^64 -------------------- */
+static uint64_t rotl(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+static uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+uint64_t or_record_hash(uint64_t index, const or_record *r) {
+    uint64_t w = ((uint64_t)r->flags << 48) | ((uint64_t)r->quality << 16) | r->stall_count;
+    return mix64(index ^ rotl(r->ttff_us, 7) ^ rotl(r->stall_us, 19) ^ rotl(r->cost_mc, 31) ^ w);
+}
+
+/* ---- the full sweep: evaluate [begin,end), select, Pareto, digest --------- */
+typedef struct {
+    const or_problem *pb;
+    const uint64_t *a, *P;
+    uint64_t begin, end;
+    uint32_t nq;
+    const or_query *q;
+    or_winner feas[64], close[64];
+    front_t front;
+    uint64_t digest;
+} sweep_job;
+
+static void *sweep_worker(void *arg) {
+    sweep_job *j = arg;
+    const or_problem *pb = j->pb;
+    for (uint32_t k = 0; k < j->nq; k++) { j->feas[k].status = -1; j->close[k].status = -1; }
+    for (uint64_t i = j->begin; i < j->end; i++) {
+        or_record r;
+        or_eval_detail(pb, j->a, j->P, i, &r, NULL, NULL, NULL, NULL);
+        j->digest += or_record_hash(i, &r);
+        for (uint32_t k = 0; k < j->nq; k++) {
+            const or_query *q = &j->q[k];
+            if (feasible(q, &r)) {
+                if (j->feas[k].status < 0 ||
+                    obj_cmp(pb->objective, i, &r, j->feas[k].index, &j->feas[k].rec) < 0) {
+                    j->feas[k].index = i; j->feas[k].rec = r; j->feas[k].status = 0;
+                }
+            } else {
+                if (j->close[k].status < 0 ||
+                    closest_cmp(pb->objective, q, i, &r, j->close[k].index, &j->close[k].rec) < 0) {
+                    j->close[k].index = i; j->close[k].rec = r; j->close[k].status = 1;
+                }
+            }
+        }
+        or_point x = {i, r.ttff_us + r.stall_us, r.cost_mc, r.quality, 0};
+        front_offer(&j->front, &x);
+    }
+    return NULL;
+}
+
+/* Returns 0 on success, 1 if the front did not fit (front_n = required size). */
+int or_sweep(const or_problem *pb, uint64_t begin, uint64_t end, uint32_t nthreads,
+             uint32_t nq, const or_query *queries, or_winner *winners,
+             or_point *front_out, uint64_t front_cap, uint64_t *front_n, uint64_t *digest) {
+    if (nthreads < 1) nthreads = 1;
+    if (nq > 64) return -1;
+    uint64_t *a = malloc(sizeof(uint64_t) * pb->S), *P = malloc(sizeof(uint64_t) * pb->S);
+    or_fixed_stages(pb, a);
+    or_deadlines(pb, P);
+    sweep_job *jobs = calloc(nthreads, sizeof(sweep_job));
+    pthread_t *th = calloc(nthreads, sizeof(pthread_t));
+    uint64_t n = end > begin ? end - begin : 0;
+    for (uint32_t t = 0; t < nthreads; t++) {
+        jobs[t].pb = pb; jobs[t].a = a; jobs[t].P = P;
+        jobs[t].begin = begin + n * t / nthreads;
+        jobs[t].end = begin + n * (t + 1) / nthreads;
+        jobs[t].nq = nq; jobs[t].q = queries;
+        pthread_create(&th[t], NULL, sweep_worker, &jobs[t]);
+    }
+    for (uint32_t t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    /* merge: per query, best feasible over threads, else best closest */
+    uint64_t dg = 0;
+    for (uint32_t t = 0; t < nthreads; t++) dg += jobs[t].digest;
+    *digest = dg;
+    for (uint32_t k = 0; k < nq; k++) {
+        or_winner best = {0};
+        best.status = -1;
+        for (uint32_t t = 0; t < nthreads; t++) {
+            or_winner *w = &jobs[t].feas[k];
+            if (w->status == 0 && (best.status != 0 ||
+                obj_cmp(pb->objective, w->index, &w->rec, best.index, &best.rec) < 0))
+                best = *w;
+        }
+        if (best.status != 0) {
+            for (uint32_t t = 0; t < nthreads; t++) {
+                or_winner *w = &jobs[t].close[k];
+                if (w->status == 1 && (best.status != 1 ||
+                    closest_cmp(pb->objective, &queries[k], w->index, &w->rec, best.index, &best.rec) < 0))
+                    best = *w;
+            }
+        }
+        winners[k] = best;
+    }
+    /* Pareto: union of the per-thread fronts, then the plain definition */
+    uint64_t tot = 0;
+    for (uint32_t t = 0; t < nthreads; t++) tot += jobs[t].front.n;
+    or_point *all = malloc((tot + 1) * sizeof(or_point));
+    uint64_t m = 0;
+    for (uint32_t t = 0; t < nthreads; t++) {
+        memcpy(all + m, jobs[t].front.v, jobs[t].front.n * sizeof(or_point));
+        m += jobs[t].front.n;
+        free(jobs[t].front.v);
+    }
+    or_point *fr = malloc((tot + 1) * sizeof(or_point));
+    uint64_t nf = 0;
+    for (uint64_t x = 0; x < m; x++) {
+        int dom = 0;
+        for (uint64_t y = 0; y < m && !dom; y++)
+            if (y != x && dominates(&all[y], &all[x])) dom = 1;
+        if (!dom) fr[nf++] = all[x];
+    }
+    qsort(fr, nf, sizeof(or_point), point_order);
+    *front_n = nf;
+    int rc = 0;
+    if (nf > front_cap) rc = 1;
+    else memcpy(front_out, fr, nf * sizeof(or_point));
+    free(all); free(fr); free(jobs); free(th); free(a); free(P);
+    return rc;
+}
+
+/* Pareto front of an explicit point list (plain O(n^2) definition, sorted output). */
+uint64_t or_pareto_points(const or_point *pts, uint64_t n, or_point *out) {
+    uint64_t nf = 0;
+    for (uint64_t x = 0; x < n; x++) {
+        int dom = 0;
+        for (uint64_t y = 0; y < n && !dom; y++)
+            if (y != x && dominates(&pts[y], &pts[x])) dom = 1;
+        if (!dom) out[nf++] = pts[x];
+    }
+    qsort(out, nf, sizeof(or_point), point_order);
+    return nf;
+}
+
+int or_abi_version(void) { return 1; }
+uint32_t or_sizeof_record(void) { return (uint32_t)sizeof(or_record); }
+uint32_t or_sizeof_winner(void) { return (uint32_t)sizeof(or_winner); }
+uint32_t or_sizeof_point(void) { return (uint32_t)sizeof(or_point); }

@@ -1,0 +1,441 @@
+"""Pins for the CPU oracle (oracle/sw_oracle.c) against what the paper and the
+mathematics fix -- never against the oracle itself.  See DESIGN.md "Pins".
+
+P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n.
+"""
+import json
+import os
+import random
+
+import pytest
+
+from swgen import make_config, INF
+from swgen.generator import Query
+from tests.helpers import make_problem, random_problem, encode
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# --------------------------------------------------------------- pin 1: decoder
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C5"])
+def test_decoder_bijection(oracle_mod, cfg):
+    pb = make_config(cfg)
+    o = oracle_mod.Oracle(pb)
+    n = 1
+    for r in pb.radix:
+        n *= r
+    assert o.n == n
+    rng = random.Random(7)
+    for i in [0, 1, n - 1, n // 2] + [rng.randrange(n) for _ in range(200)]:
+        d = o.decode(i)
+        assert all(0 <= x < r for x, r in zip(d, pb.radix))
+        assert encode(pb.radix, d) == i
+    # MSD = earliest scene block (reading R19): index r_{B-1} flips digit B-2
+    assert o.decode(pb.radix[-1]) == [0] * (pb.B - 2) + [1, 0]
+
+
+def test_decoder_exhaustive_c1(oracle_mod):
+    pb = make_config("C1")
+    o = oracle_mod.Oracle(pb)
+    seen = {tuple(o.decode(i)) for i in range(256)}
+    assert len(seen) == 256 == o.n
+
+
+# -------------------------------------------------------- pin 2: fixed stages
+def test_fixed_stage_a0_table4(oracle_mod):
+    """a_0 = StreamCast 1.2 s + Gemma 6.6 s + Kokoro 43 ms/s x 30 s = 9.09 s
+    (Table 4)."""
+    pb = make_problem([30_000_000, 30_000_000], [6_600_000, 1_000_000],
+                      [1_290_000, 1_290_000], [1], [180250], [1, 1], [0, 1, 2],
+                      [(1, 1, 0), (1, 1, 0)], [5, 5], overhead_us=1_200_000)
+    a = oracle_mod.Oracle(pb).fixed_stages()
+    assert a[0] == 9_090_000
+    # scene 1: text at 7.8+1.0 = 8.8 s but TTS busy until 9.09 s -> FIFO start 9.09 s
+    assert a[1] == 9_090_000 + 1_290_000
+
+
+def test_fixed_stage_regimes(oracle_mod):
+    rng = random.Random(3)
+    for _ in range(200):
+        S = rng.randint(1, 12)
+        llm = [rng.randint(1, 5_000_000) for _ in range(S)]
+        # (i) TTS never the bottleneck: tts_s <= llm_{s+1} -> a_s = L_s + tts_s (closed form)
+        tts = [rng.randint(0, min(llm[1:] + [5_000_000])) for _ in range(S)]
+        ov = rng.randint(0, 2_000_000)
+        pb = make_problem([1000] * S, llm, tts, [1], [1], [1] * S, list(range(S + 1)),
+                          [(0, 1, 0)] * S, [1] * S, overhead_us=ov)
+        a = oracle_mod.Oracle(pb).fixed_stages()
+        for s in range(S):
+            assert a[s] == ov + sum(llm[: s + 1]) + tts[s]
+        # (ii) LLM all up front (llm_s = 0 for s >= 1): the TTS server is a
+        # serial queue -> a_s = L_0 + sum_{j<=s} tts_j
+        llm2 = [llm[0]] + [0] * (S - 1)
+        pb2 = make_problem([1000] * S, llm2, tts, [1], [1], [1] * S, list(range(S + 1)),
+                           [(0, 1, 0)] * S, [1] * S, overhead_us=ov)
+        a2 = oracle_mod.Oracle(pb2).fixed_stages()
+        for s in range(S):
+            assert a2[s] == ov + llm[0] + sum(tts[: s + 1])
+
+
+def test_generated_fixed_stages_monotone(oracle_mod):
+    for cfg in ["C1", "C2", "C3", "C5"]:
+        pb = make_config(cfg)
+        a = oracle_mod.Oracle(pb).fixed_stages()
+        s0 = pb.scene0_static
+        assert all(a[s] <= a[s + 1] for s in range(s0, pb.S - 1))
+        # Table 4 anchor: Gemma first output 6.6 s after the 1.2 s front end
+        assert a[s0] == 1_200_000 + 6_600_000 + pb.tts_us[s0]
+
+
+# ------------------------------------------------- pins 3-6: the recurrence
+def _detail(o, i):
+    rec, ready, pend, mk, te = o.eval(i)
+    return rec, ready, pend, mk, te
+
+
+def test_lindley_single_slot(oracle_mod):
+    """G=1 (or k=G everywhere): R_s = max(a_s, R_{s-1}) + t_s (textbook max-plus)."""
+    rng = random.Random(11)
+    for _ in range(300):
+        S = rng.randint(1, 8)
+        G = rng.randint(1, 4)
+        va = [rng.randint(1, 40_000_000) for _ in range(S)]
+        pb = make_problem([rng.randint(1, 9000) * 1000 for _ in range(S)],
+                          [rng.randint(0, 9_000_000) for _ in range(S)],
+                          [rng.randint(0, 2_000_000) for _ in range(S)], [G], [180250],
+                          [1] * S, list(range(S + 1)), [(1, G, 0)] * S, va,
+                          overhead_us=rng.randint(0, 1_000_000))
+        o = oracle_mod.Oracle(pb)
+        a = o.fixed_stages()
+        rec, ready, pend, mk, te = _detail(o, 0)
+        R = 0
+        for s in range(S):
+            R = max(a[s], R) + va[s]
+            assert ready[s] == R
+        assert pend[0] == R and mk == R
+
+
+def test_serial_single_server_is_sum(oracle_mod):
+    """BJ invariant: a serial single-server plan's makespan = sum of stage times;
+    RTF = generation time / video length (P:77 '1.4 h ... 8.4x', P:310 '8.3 h ... 50x')."""
+    rng = random.Random(5)
+    for _ in range(100):
+        S = rng.randint(1, 10)
+        va = [rng.randint(1, 10**9) for _ in range(S)]
+        pb = make_problem([1000] * S, [0] * S, [0] * S, [1], [1], [1] * S,
+                          list(range(S + 1)), [(0, 1, 0)] * S, va)
+        assert _detail(oracle_mod.Oracle(pb), 0)[3] == sum(va)
+    # paper RTF examples as serial plans of a 10-minute video
+    for hours, rtf_expect, tol in [(1.4, 8.4, 1e-12), (8.3, 49.8, 1e-12)]:
+        tot = int(round(hours * 3600e6))
+        pb = make_problem([600_000_000], [0], [0], [1], [1], [1], [0, 1], [(0, 1, 0)], [tot])
+        mk = _detail(oracle_mod.Oracle(pb), 0)[3]
+        assert abs(mk / 600e6 - rtf_expect) < 1e-9
+    assert round(8.3 * 3600 / 600) == 50  # "50x slower than real time"
+
+
+def test_no_contention(oracle_mod):
+    """G_p >= sum_s k_s: every scene starts when its inputs exist: R_s = a_s + t_s."""
+    rng = random.Random(13)
+    for _ in range(200):
+        S = rng.randint(1, 6)
+        ks = [rng.choice([1, 2, 4]) for _ in range(S)]
+        G = sum(ks) + rng.randint(0, 3)
+        va = [rng.randint(1, 50_000_000) for _ in range(S)]
+        pb = make_problem([1000] * S, [rng.randint(0, 3_000_000) for _ in range(S)],
+                          [rng.randint(0, 3_000_000) for _ in range(S)], [G], [1],
+                          [1] * S, list(range(S + 1)), [(0, k, 0) for k in ks], va,
+                          overhead_us=1_200_000)
+        o = oracle_mod.Oracle(pb)
+        a = o.fixed_stages()
+        ready = _detail(o, 0)[1]
+        assert ready == [a[s] + va[s] for s in range(S)]
+
+
+def _event_sim(pb, a, digits):
+    """Explicit-GPU event simulation (brute force, independent of the sorted-multiset
+    formulation): each scene takes the k GPUs of its pool that free up earliest
+    (lowest GPU index on ties, P:990 'shortest expected runtime'), starts when
+    all k are free and its inputs exist, and holds all k until it ends."""
+    free = [[0] * g for g in pb.gpus]
+    ready = []
+    coff = [sum(pb.radix[:b]) for b in range(pb.B)]
+    voff = [pb.va_offset(b) for b in range(pb.B)]
+    for s in range(pb.S):
+        b = max(bb for bb in range(pb.B) if pb.first_scene[bb] <= s)
+        c = digits[b]
+        lvl, k, p = pb.choices[coff[b] + c]
+        t = pb.va_us[voff[b] + (s - pb.first_scene[b]) * pb.radix[b] + c]
+        order = sorted(range(pb.gpus[p]), key=lambda g: (free[p][g], g))[:k]
+        start = max([a[s]] + [free[p][g] for g in order])
+        for g in order:
+            free[p][g] = start + t
+        ready.append(start + t)
+    return ready, [max(f) for f in free]
+
+
+def test_multiset_equals_event_simulation(oracle_mod):
+    rng = random.Random(17)
+    for _ in range(2000):
+        pb = random_problem(rng, max_scenes=5)
+        o = oracle_mod.Oracle(pb)
+        a = o.fixed_stages()
+        i = rng.randrange(o.n)
+        rec, ready, pend, mk, te = _detail(o, i)
+        r2, ends = _event_sim(pb, a, o.decode(i))
+        assert ready == r2
+        assert pend == ends
+
+
+# ------------------------------------------- pin: hand-derived worked example
+def _hand_problem(billing=0):
+    g = json.load(open(os.path.join(GOLDEN, "hand_example.json")))
+    p = g["problem"]
+    chs = [tuple(c) for c in p["choices_per_digit"]] * 3
+    va = p["va_us_per_choice"] * 3
+    pb = make_problem(p["dur_us"], p["llm_us"], p["tts_us"], p["gpus"], p["price_mc"],
+                      p["radix"], p["first_scene"], chs, va, billing=billing)
+    return pb, g
+
+
+def test_hand_example(oracle_mod):
+    pb, g = _hand_problem()
+    o = oracle_mod.Oracle(pb)
+    assert o.fixed_stages() == g["expected_a_us"]
+    for idx, e in g["expected"].items():
+        rec, ready, pend, mk, te = o.eval(int(idx))
+        assert rec.ttff_us == e["ttff_us"]
+        assert rec.stall_us == e["stall_us"]
+        assert rec.stall_count == e["stall_count"]
+        assert mk == e["makespan_us"]
+        assert rec.cost_mc == e["cost_reserved"]
+        assert rec.quality == e["quality"]
+        assert te == e["ttff_us"] + e["stall_us"]
+    pbb, g = _hand_problem(billing=1)
+    rec = oracle_mod.Oracle(pbb).eval(4)[0]
+    assert rec.cost_mc == g["expected"]["4"]["cost_busy"]
+
+
+# ------------------------------------------- pin 7/8: monotonicity (BJ invariant)
+def test_monotone_in_level(oracle_mod):
+    """Lowering one block's level (same k, pool) never raises t_s, any R_s, ttff,
+    ttff_eff, makespan or cost (RESERVED and BUSY).  Q decreases.  (stall is NOT
+    monotone and is deliberately not asserted.)"""
+    rng = random.Random(23)
+    checked = 0
+    for trial in range(12000):
+        pb = random_problem(rng, max_scenes=6, max_choices=6, one_scene_digits=False)
+        # make the va table monotone in level for equal (k,pool): t = base * LV-ish
+        coff = [sum(pb.radix[:b]) for b in range(pb.B)]
+        voff = [pb.va_offset(b) for b in range(pb.B)]
+        for b in range(pb.B):
+            for s in range(pb.first_scene[b], pb.first_scene[b + 1]):
+                base = rng.randint(1, 5_000_000)
+                for c in range(pb.radix[b]):
+                    lvl, k, p = pb.choices[coff[b] + c]
+                    pb.va_us[voff[b] + (s - pb.first_scene[b]) * pb.radix[b] + c] = \
+                        base * (lvl + 1) * 3 // (k + 2) + p
+        o = oracle_mod.Oracle(pb)
+        i = rng.randrange(o.n)
+        d = o.decode(i)
+        b = rng.randrange(pb.B)
+        lvl, k, p = pb.choices[coff[b] + d[b]]
+        lower = [c for c in range(pb.radix[b])
+                 if pb.choices[coff[b] + c][1:] == (k, p) and pb.choices[coff[b] + c][0] < lvl]
+        if not lower:
+            continue
+        d2 = list(d)
+        d2[b] = rng.choice(lower)
+        j = encode(pb.radix, d2)
+        hi = o.eval(i)
+        lo = o.eval(j)
+        assert all(x <= y for x, y in zip(lo[1], hi[1]))          # every R_s
+        assert lo[0].ttff_us <= hi[0].ttff_us
+        assert lo[4] <= hi[4]                                    # ttff_eff
+        assert lo[3] <= hi[3]                                    # makespan
+        assert lo[0].cost_mc <= hi[0].cost_mc
+        assert lo[0].quality <= hi[0].quality
+        checked += 1
+    assert checked > 1000
+
+
+def test_ladder_extremes(oracle_mod):
+    """All-lowest ttff and ttff_eff <= all-highest, same k and pool (BJ invariant)."""
+    for cfg in ["C1", "C2", "C3"]:
+        pb = make_config(cfg)
+        o = oracle_mod.Oracle(pb)
+        coff = [sum(pb.radix[:b]) for b in range(pb.B)]
+        lv = sorted({c[0] for c in pb.choices})
+        for (k, p) in {c[1:] for c in pb.choices}:
+            def pick(level):
+                return [next(c for c in range(pb.radix[b]) if pb.choices[coff[b] + c] == (level, k, p))
+                        for b in range(pb.B)]
+            lo = o.eval(encode(pb.radix, pick(lv[0])))
+            hi = o.eval(encode(pb.radix, pick(lv[-1])))
+            assert lo[0].ttff_us <= hi[0].ttff_us and lo[4] <= hi[4]
+            # all-HIGH quality closed form: Q = D_ms x score(HIGH)
+            D_ms = sum(pb.dur_us[pb.scene0_static:]) // 1000
+            assert hi[0].quality == D_ms * pb.level_score[lv[-1]]
+
+
+# ------------------------------------------------ pins 10/11: TTFF_eff, deadlines
+def _ttff_eff_problem(tbf_us):
+    """TTFF 30 s then 14400 one-frame scenes produced every TBF at 24 FPS playback:
+    scene 0 on pool A (t = 30 s); scenes 1..14400 on pool B at t = TBF."""
+    n = 14400
+    P = [round(i * 1e6 / 24) for i in range(n + 2)]  # frame i due at i/24 s
+    dur = [P[i + 1] - P[i] for i in range(n + 1)]
+    return make_problem(dur, [0] * (n + 1), [0] * (n + 1), [1, 1], [1, 1], [1, 1],
+                        [0, 1, n + 1], [(1, 1, 0), (1, 1, 1)],
+                        [30_000_000] + [tbf_us] * n)
+
+
+def test_ttff_eff_paper_example(oracle_mod):
+    """10-minute video at 24 FPS, TBF 50 ms, TTFF 30 s -> TTFF_eff 2 minutes
+    (S:161); TBF 40 ms -> 30 s."""
+    rec, ready, pend, mk, te = oracle_mod.Oracle(_ttff_eff_problem(50_000)).eval(0)
+    assert rec.ttff_us == 30_000_000
+    assert te == 120_000_000
+    assert rec.stall_us == 90_000_000
+    rec, ready, pend, mk, te = oracle_mod.Oracle(_ttff_eff_problem(40_000)).eval(0)
+    assert te == 30_000_000 and rec.stall_us == 0 and rec.stall_count == 0
+
+
+def test_frame_deadline_paper_example(oracle_mod):
+    """at 24 FPS frame 172 is due by ~7.2 s; TTFF 1 s needs ~36 ms TBF."""
+    P = oracle_mod.Oracle(_ttff_eff_problem(50_000)).deadlines()
+    assert P[172] == 7_166_667
+    assert abs(P[172] / 1e6 - 7.2) < 0.05
+    tbf_ms = (P[172] - 1_000_000) / 172 / 1000
+    assert abs(tbf_ms - 36) < 0.5 and abs(1000 / 24 - 42) < 0.5
+
+
+# ------------------------------------------------------------------ pin 12: cost
+@pytest.mark.parametrize("G,price,hours,billing,expect", [
+    (8, 180250, 1.0, 0, 1_442_000),   # 8xA100 reserved 1 h = $14.42 (Table 3)
+    (4, 402750, 0.5, 0, 805_500),     # 4xH100 spot 0.5 h = $8.055
+    (8, 106500, 8.3, 0, 7_071_600),   # 8xA100 spot 8.3 h ~ "$70" (P:310 with P:635)
+    (8, 180250, 1.0, 1, 1_442_000),   # BUSY with all 8 GPUs busy = reserved
+])
+def test_cost_table3(oracle_mod, G, price, hours, billing, expect):
+    t = int(round(hours * 3600e6))
+    pb = make_problem([1000], [0], [0], [G], [price], [1], [0, 1], [(3, G, 0)], [t],
+                      billing=billing)
+    assert oracle_mod.Oracle(pb).eval(0)[0].cost_mc == expect
+
+
+def test_cost_billing_and_rounding(oracle_mod):
+    # one GPU of eight busy for 1 h: RESERVED bills all 8 GPU-hours (GPU idle time,
+    # P:696), BUSY bills 1 GPU-hour
+    pb = make_problem([1000], [0], [0], [8], [180250], [1], [0, 1], [(3, 1, 0)], [3_600_000_000])
+    assert oracle_mod.Oracle(pb).eval(0)[0].cost_mc == 8 * 180250
+    pb.billing = 1
+    assert oracle_mod.Oracle(pb).eval(0)[0].cost_mc == 180250
+    # round half up exactly at 0.5 mc; an unused pool costs 0; fixed cost is added
+    for t, exp in [(1_800_000_000, 1), (1_799_999_999, 0)]:
+        pb = make_problem([1000], [0], [0], [1, 4], [1, 999], [1], [0, 1], [(3, 1, 0)], [t],
+                          fixed_cost_mc=7)
+        rec = oracle_mod.Oracle(pb).eval(0)[0]
+        assert rec.cost_mc == 7 + exp and rec.flags == 1
+
+
+# ------------------------------------------------- pins 14-16: select, Pareto, digest
+def _sel_key(pb, q, i, r):
+    te = r.ttff_us + r.stall_us
+    obj = ((-r.quality, r.cost_mc, te, i) if pb.objective == 0
+           else (r.cost_mc * te, -r.quality, i))
+    feas = (r.ttff_us <= q.slo_startup_us and r.stall_us <= q.slo_stall_us
+            and r.cost_mc <= q.budget_mc)
+    if feas:
+        return (0, obj)
+    vt = max(0, r.ttff_us - q.slo_startup_us) + max(0, r.stall_us - q.slo_stall_us)
+    vc = max(0, r.cost_mc - q.budget_mc)
+    return (1, (vt, vc) + obj)
+
+
+def _brute_select(pb, recs, q):
+    best = min(range(len(recs)), key=lambda i: _sel_key(pb, q, i, recs[i]))
+    return (_sel_key(pb, q, best, recs[best])[0], best)
+
+
+def _dominates(y, x):
+    return (y[1] <= x[1] and y[2] <= x[2] and y[3] >= x[3] and
+            (y[1] < x[1] or y[2] < x[2] or y[3] > x[3] or y[0] < x[0]))
+
+
+def _brute_front(points):
+    return sorted([x for x in points if not any(_dominates(y, x) for y in points if y is not x)],
+                  key=lambda p: (p[1], p[2], -p[3], p[0]))
+
+
+@pytest.mark.parametrize("objective", [0, 1])
+def test_select_and_pareto_c1_bruteforce(oracle_mod, objective):
+    pb = make_config("C1")
+    pb.objective = objective
+    o = oracle_mod.Oracle(pb)
+    recs = o.record_list(0, 256)
+    qs = pb.queries + [Query(400_000_000, 0, INF), Query(0, 0, 0)]
+    for nth in (1, 3, 8):
+        winners, front, digest = o.sweep(0, 256, qs, nthreads=nth)
+        for q, (st, idx, rec) in zip(qs, winners):
+            assert (st, idx) == _brute_select(pb, recs, q)
+            assert rec == recs[idx]
+        pts = [(i, r.ttff_eff_us, r.cost_mc, r.quality) for i, r in enumerate(recs)]
+        assert front == _brute_front(pts)
+        assert digest == sum(o.record_hash(i, r) for i, r in enumerate(recs)) % (1 << 64)
+    # query with nothing feasible exercises the closest tier
+    assert winners[1][0] == 1 and winners[4][0] == 1
+
+
+def test_select_pareto_random_subranges(oracle_mod):
+    """Random problems, random sub-ranges: sweep == brute force; partition invariance."""
+    rng = random.Random(29)
+    for trial in range(40):
+        pb = random_problem(rng, max_scenes=5, max_choices=5)
+        o = oracle_mod.Oracle(pb)
+        n = o.n
+        b = rng.randrange(n)
+        e = rng.randint(b + 1, n)
+        recs = o.record_list(b, e)
+        qs = []
+        for _ in range(4):
+            rr = recs[rng.randrange(len(recs))]
+            qs.append(Query(rr.ttff_us + rng.randint(-10**6, 10**6) if rng.random() < .8 else INF,
+                            rr.stall_us + rng.randint(-10**6, 10**6) if rng.random() < .8 else INF,
+                            max(0, rr.cost_mc + rng.randint(-100, 100))))
+        qs = [Query(max(0, q.slo_startup_us), max(0, q.slo_stall_us), q.budget_mc) for q in qs]
+        w1, f1, d1 = o.sweep(b, e, qs, nthreads=1)
+        w2, f2, d2 = o.sweep(b, e, qs, nthreads=rng.randint(2, 9))
+        assert (w1, f1, d1) == (w2, f2, d2)
+        for q, (st, idx, rec) in zip(qs, w1):
+            st2, j = _brute_select(pb, recs, q)
+            assert (st, idx) == (st2, b + j)
+        pts = [(b + i, r.ttff_eff_us, r.cost_mc, r.quality) for i, r in enumerate(recs)]
+        assert f1 == _brute_front(pts)
+        # staircase: nothing in the space dominates a front point, every non-front
+        # point is dominated by a front point
+        fs = set(p[0] for p in f1)
+        for p in pts:
+            if p[0] in fs:
+                assert not any(_dominates(y, p) for y in pts)
+            else:
+                assert any(_dominates(y, p) for y in f1)
+
+
+def test_pareto_duplicates_keep_lowest_index(oracle_mod):
+    pts = [(5, 10, 10, 7), (2, 10, 10, 7), (9, 10, 10, 7), (1, 11, 10, 7), (3, 9, 12, 8)]
+    assert oracle_mod.pareto_points(pts) == [(3, 9, 12, 8), (2, 10, 10, 7)]
+
+
+def test_generator_calibration():
+    """App. B calibration: 81 frames MED 640x400/10 steps on 1xA100 = 93.0 s (P:532,
+    P:543); HIGH/MED = 4 (pixels) x 2 (steps); 8-GPU DiT speed-up > 5x
+    (P:596); H100 1.9x A100; 1 frame costs 66 s per video-second."""
+    from swgen.generator import va_seconds, n16_frames
+    assert n16_frames(5063) == 81
+    assert abs(va_seconds(5063, 1, 1, "A100") - 93.0) < 1e-9
+    assert abs(va_seconds(5063, 3, 1, "A100") / va_seconds(5063, 1, 1, "A100") - 8.0) < 1e-12
+    dit8 = va_seconds(5063, 1, 8, "A100") - 0.12 * 93.0
+    assert (0.88 * 93.0) / dit8 > 5.0
+    assert abs(va_seconds(5063, 1, 1, "A100") / va_seconds(5063, 1, 1, "H100") - 1.9) < 1e-12
+    assert abs(va_seconds(63, 1, 1, "A100") / 0.0625 - 66.0) < 0.1

@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Bench: batched what-if evaluation of StreamWise serving plans on B200.
+
+One STEP = one pass of the whole hot path over the workload
+BASELINE.json's metric is quoted on (configs[1] = C2: 10-minute podcast on one
+8xA100-profile server, 20 scenes, 3 levels, k in {1,2,4,8}; 12^8 = 429,981,696
+candidate plans): reset, eval of the full space (records stored), the 3 select
+queries (one scan), the exact Pareto front, all through the C ABI.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+Prints ONE JSON line on rank 0.  The oracle (oracle/) is executed only by the
+cpu_baseline leg (rank 0, N=1) and by --impl reference.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "plan candidates evaluated/sec (1/2/4/8 B200) and % HBM roofline vs CPU oracle"
+UNIT = "candidates/s"
+REC_BYTES = 32  # algorithmic HBM bytes per candidate of the eval kernel (the record)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 9:
+                rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def cpu_baseline(pb, queries, target_s=15.0):
+    """The oracle as it stands, on this host's cores, on a bounded prefix of the space."""
+    from oracle.oracle import Oracle
+    orc = Oracle(pb)
+    th = os.cpu_count() or 1
+    n0 = 20000 * th
+    t = time.perf_counter()
+    orc.sweep(0, n0, queries, nthreads=th)
+    dt = max(time.perf_counter() - t, 1e-3)
+    n = int(min(orc.n, max(n0, n0 * target_s / dt)))
+    t = time.perf_counter()
+    orc.sweep(0, n, queries, nthreads=th)
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": UNIT, "cores": th, "kind": "oracle",
+            "sample": "%s candidates [0, %d) of %d, full recompute + %d queries + Pareto + digest, "
+                      "%.1f s" % (pb.name, n, orc.n, len(queries), dt)}
+
+
+def run_reference(args, pb):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle.oracle import Oracle
+    orc = Oracle(pb)
+    th = os.cpu_count() or 1
+    per_step = 1_000_000 * max(1, th // 8)  # bounded sample per step
+    per_step = min(per_step, orc.n)
+    off = 0
+    for _ in range(args.warmup):
+        orc.sweep(off, off + per_step, pb.queries, nthreads=th)
+    times = []
+    for k in range(args.steps):
+        b = (k * per_step) % max(1, orc.n - per_step)
+        t = time.perf_counter()
+        orc.sweep(b, b + per_step, pb.queries, nthreads=th)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    v = per_step * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": "%s (%d candidates); each step a %d-candidate sample" % (
+            pb.name, orc.n, per_step), "n_candidates": orc.n, "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "oracle",
+                         "sample": "%d candidates per step, full recompute + %d queries + Pareto"
+                                   " + digest" % (per_step, len(pb.queries))},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def input_bytes(pb):
+    return (8 * 3 * pb.S + 8 * len(pb.va_us) + 4 * len(pb.radix) + 4 * len(pb.first_scene)
+            + 4 * len(pb.choices) + 4 * len(pb.level_score) + 12 * len(pb.gpus))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+
+    from swgen import make_config
+    pb = make_config(args.config)
+    if args.impl == "reference":
+        return run_reference(args, pb)
+
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = local
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2603_05800_b200 as sw
+    if world > 1:
+        obj = [sw.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = sw.comm_init(obj[0], rank, world, dev)
+
+    stream = torch.cuda.Stream(device=dev)
+    plan = sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world)
+    N = plan.n
+
+    def step():
+        plan.reset()
+        plan.eval(0, N)
+        sels = plan.select_batch(pb.queries)
+        front = plan.pareto()
+        return sels, front
+
+    for _ in range(args.warmup):
+        step()
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(dev)
+    barrier()
+    l0 = plan.launch_count()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    eval_ms = []
+    for _ in range(args.steps):
+        sels, front = step()
+        eval_ms.append(plan.last_eval_ms())
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    ck = clocks.stop()
+    launches = plan.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms, max(eval_ms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, emax = float(t[0]), float(t[1])
+    else:
+        emax = max(eval_ms)
+    ms_per_step = ms / args.steps
+    value = N / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (eval): algorithmic bytes = 32 B x records/launch
+    local_n = sw.shard_range(0, N, plan.row, rank, world)
+    local_n = local_n[1] - local_n[0]
+    eval_avg_ms = sum(eval_ms) / len(eval_ms)
+    achieved = REC_BYTES * local_n / (eval_avg_ms / 1e3) / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "eval_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("config") == args.config and pj.get("n_local") == local_n:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    roof = {"kernel": "eval_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "peak_source": peak_kind, "algorithmic_bytes_per_launch": REC_BYTES * local_n,
+            "eval_ms_per_launch": eval_avg_ms,
+            "eval_share_of_step": eval_avg_ms / ms_per_step}
+
+    # parity check of the timed configuration (outside the timed region)
+    parity = None
+    gpath = os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % args.config)
+    if os.path.exists(gpath):
+        g = json.load(open(gpath))
+        dg = plan.digest()
+        ok_w = all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
+                   for s, w in zip(sels, g["winners"]))
+        ok_f = front == [tuple(p) for p in g["front"]]
+        parity = {"digest": dg == int(g["digest"]), "winners": ok_w, "pareto": ok_f}
+
+    # e2e: public API from HOST buffers each step (create uploads the tables, results
+    # come back to host), wall clock with device sync on both sides, max over ranks
+    plan.close()
+    barrier()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(args.e2e_steps):
+        with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank,
+                     nranks=world) as p2:
+            p2.eval(0, N)
+            s2 = p2.select_batch(pb.queries)
+            f2 = p2.pareto()
+            d2h = 112 * len(s2) + 32 * len(f2)
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(pb, pb.queries)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "%s: 10-minute podcast, one 8xA100-profile server, 20 scenes, "
+                                   "3 levels x k{1,2,4,8}, 12^8 plans (BASELINE configs[1])" % args.config
+                       if args.config == "C2" else args.config,
+                       "n_candidates": N, "queries": len(pb.queries),
+                       "l2": "records %.1f GB >> 126 MB L2 (no flush needed)" % (N * 32 / 1e9),
+                       "parallelism": "candidate-shard x%d, NCCL allgather merge" % world},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": input_bytes(pb),
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": ck,
+            "parity": parity,
+            "front_points": len(front),
+        }
+        print(json.dumps(line), flush=True)
+    if comm:
+        sw.comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,262 @@
+/*
+ * sw_plan.h -- C ABI of the B200-native StreamWise plan evaluator (libsw_plan.so).
+ *
+ * The library evaluates, in batch on B200 GPUs, every candidate serving plan of
+ * one podcast-video request: per scene (or block of scenes) a quality level, a
+ * parallelism degree k and a GPU pool.  It scores each with the paper's
+ * latency/cost model and reduces the results to SLO/budget-constrained winners
+ * and a 3-D Pareto front.  Citations: P:n = arXiv 2603.05800 PAPER.md line n,
+ * SPEC = the spec written from it, R<n> = readings listed in DESIGN.md.
+ *
+ *   - the estimator the paper's provisioner runs per setting: "For each setting,
+ *     we use the greedy algorithm to estimate the latency and cost";
+ *     a greedy DAG simulation with deadline-ordered scenes
+ *     (P:970), shortest-expected-runtime instance choice,
+ *     adaptive per-scene quality, USP parallel degree;
+ *   - objective, SLO steering and "closest solution", the
+ *     latency/cost/quality Pareto frontier;
+ *   - metrics TTFF / TTFF_eff, Table 3 prices.
+ *
+ * Conventions (every entry point):
+ *   - No exceptions cross the ABI; every call returns an sw_status.  Negative =
+ *     error (nothing changed unless stated), 0 = OK, positive = soft status.
+ *     The library never exits the process.  sw_last_error() gives a message.
+ *   - All pointer arguments of sw_plan_create are HOST pointers; create deep-
+ *     copies them (the caller may free them on return) and uploads them once.
+ *   - A handle owns its device tables, record buffer, Pareto front and scratch
+ *     (allocated with cudaMallocAsync on its stream, or the caller's allocator;
+ *     with the default allocator, create sets the device's default memory pool
+ *     release threshold to UINT64_MAX so freed blocks stay pooled).
+ *   - eval is asynchronous on the handle's stream; select / pareto_get / digest /
+ *     detail synchronise that stream and write caller HOST memory.
+ *   - Multi-GPU: with nranks > 1 every rank makes the same call sequence with the
+ *     same arguments (like NCCL); eval takes the GLOBAL index range and shards it
+ *     internally; select / pareto_get / digest are collectives over nccl_comm.
+ *   - A handle is not thread-safe; distinct handles are independent.
+ *   - Integer semantics everywhere: times in microseconds (u64), money in
+ *     milli-cents (u64), quality in ms x score (u32).  Results are bit-exact
+ *     and independent of grid size, rank count and range splitting.
+ */
+#ifndef SW_PLAN_H
+#define SW_PLAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sw_plan sw_plan; /* opaque: one request's plan space on one rank */
+typedef int32_t sw_status;
+
+enum {
+    SW_OK = 0,
+    SW_CLOSEST = 1,   /* no feasible plan: the closest one is returned (SPEC exit 2) */
+    SW_TRUNCATED = 2, /* output buffer too small; *n_out holds the required count */
+    SW_EMPTY = 3,     /* nothing evaluated yet (no records in the handle) */
+    SW_EINVAL = -1,   /* bad argument / shape: k > G_p, heads % k != 0, S = 0, duration 0,
+                         G_p > SW_MAX_GPUS_PER_POOL, overlapping eval range, ... */
+    SW_ERANGE = -2,   /* space size >= 2^63, an overflow bound fails, or records exceed
+                         record_capacity (SPEC "InstanceTooLarge") */
+    SW_ENOMEM = -3,
+    SW_ECUDA = -4,
+    SW_ENCCL = -5,
+    SW_ESTATE = -6 /* wrong call order or handle misuse */
+};
+
+#define SW_MAX_SCENES 64
+#define SW_MAX_DIGITS 16
+#define SW_MAX_CHOICES 64          /* per digit */
+#define SW_MAX_POOLS 4
+#define SW_MAX_GPUS_PER_POOL 8
+#define SW_MAX_QUERIES 8           /* per sw_plan_select_batch call */
+
+/* Scene list: the refined DAG of one request, scenes in playback order. */
+typedef struct {
+    uint32_t n_scenes;          /* S, 1..SW_MAX_SCENES */
+    const uint64_t *dur_us;     /* [S] playback duration of each scene, > 0 */
+    const uint64_t *llm_us;     /* [S] screenplay (LLM) time per scene (Table 4 Gemma) */
+    const uint64_t *tts_us;     /* [S] audio (TTS) time per scene (Table 4 Kokoro) */
+    uint64_t overhead_us;       /* front end before the LLM starts (Table 4 StreamCast) */
+    uint32_t scene0_static;     /* 1: scene 0 is a static intro, no GPU work */
+    uint64_t static_ready_us;   /* its ready time (e.g. 500 ms) */
+} sw_scene_list;
+
+/* One choice of a digit: applied to every scene of the digit's block. */
+typedef struct {
+    uint8_t level;   /* index into level_score */
+    uint8_t degree;  /* k GPUs (USP degree); must divide heads */
+    uint8_t pool;    /* GPU pool index */
+    uint8_t pad;
+} sw_choice;
+
+/* Profiled tables (on-boarding profiles) expanded per candidate choice.
+ * Digit b covers scenes [first_scene[b], first_scene[b+1]); blocks are contiguous,
+ * start at scene scene0_static and end at S.  Index order: MSD = earliest block (R19). */
+typedef struct {
+    uint32_t n_digits;          /* B, 1..SW_MAX_DIGITS */
+    const uint32_t *radix;      /* [B] r_b, 1..SW_MAX_CHOICES */
+    const uint32_t *first_scene;/* [B+1] */
+    const sw_choice *choices;   /* [sum r_b] concatenated per digit */
+    const uint64_t *va_us;      /* V+A stage time, block-major: digit b, scene s in
+                                   block, choice c -> va_us[off_b + (s-first_b)*r_b + c], >= 1 */
+    uint32_t n_levels;
+    const uint32_t *level_score;/* [n_levels] quality score per level (R12) */
+    uint32_t heads;             /* attention heads for the divisibility check;
+                                   0 = no check */
+} sw_profile_tables;
+
+/* Pools and prices (Table 3) in integer milli-cents per GPU-hour. */
+typedef struct {
+    uint32_t n_pools;                       /* 1..SW_MAX_POOLS */
+    const uint32_t *gpus;                   /* [n_pools] G_p, 1..SW_MAX_GPUS_PER_POOL */
+    const uint64_t *price_mc_per_gpu_hour;  /* [n_pools] reserved or spot column */
+    uint64_t fixed_cost_mc;                 /* LLM/TTS instances */
+    uint32_t billing;    /* 0 RESERVED: G_p x pool span (GPU idle time billed);
+                            1 BUSY: sum k x t (GPU-seconds) -- reading R10 */
+    uint32_t objective;  /* 0 QUALITY_FIRST: (-Q, cost, ttff_eff, index);
+                            1 COST_X_TTFF: (cost x ttff_eff, -Q, index) -- R13 */
+} sw_price_table;
+
+typedef void *(*sw_alloc_fn)(size_t bytes, void *stream, void *ctx);
+typedef void (*sw_free_fn)(void *ptr, void *stream, void *ctx);
+
+typedef struct {
+    int32_t device;           /* CUDA device ordinal */
+    void *stream;             /* cudaStream_t to run on; NULL = the handle creates one */
+    void *nccl_comm;          /* ncclComm_t (from sw_comm_init) or NULL when nranks == 1 */
+    int32_t rank, nranks;
+    uint64_t record_capacity; /* records retained per rank; 0 = this rank's share of
+                                 the whole space */
+    sw_alloc_fn alloc;        /* NULL = cudaMallocAsync on the stream */
+    sw_free_fn free;
+    void *alloc_ctx;
+} sw_runtime;
+
+/* Per-candidate record, 32 B, the HBM traffic of the eval kernel. */
+typedef struct {
+    uint64_t ttff_us;     /* time to first frame */
+    uint64_t stall_us;    /* ttff_eff - ttff: total playback pause (R8) */
+    uint64_t cost_mc;     /* milli-cents */
+    uint32_t quality;     /* sum over scenes of duration_ms x level score (R12) */
+    uint16_t stall_count; /* rebuffering events: new strict maxima of R_s - P_s, s >= 1 */
+    uint8_t flags;        /* bit p: pool p used */
+    uint8_t pad;
+} sw_record;
+
+typedef struct {
+    uint64_t slo_startup_us; /* feasible iff ttff <= slo_startup  (UINT64_MAX = none) */
+    uint64_t slo_stall_us;   /*          and stall <= slo_stall */
+    uint64_t budget_mc;      /*          and cost <= budget */
+} sw_query;
+
+/* A selected plan with its full metrics (recomputed on the GPU from its index). */
+typedef struct {
+    int32_t status;                 /* SW_OK, SW_CLOSEST or SW_EMPTY */
+    uint32_t pad;
+    uint64_t index;                 /* global candidate index */
+    sw_record rec;
+    uint64_t ttff_eff_us;           /* max_s (R_s - P_s) */
+    uint64_t makespan_us;           /* last finish over pools and scene 0 */
+    uint64_t pool_end_us[SW_MAX_POOLS];
+    uint8_t digit[SW_MAX_DIGITS];   /* decoded choice per digit */
+} sw_selection;
+
+typedef struct {
+    uint64_t index, ttff_eff_us, cost_mc;
+    uint32_t quality, pad;
+} sw_pareto_point;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Validate inputs, check overflow bounds (R25), upload and pack the tables on the
+ * device (fixed-stage ready times a_s and deadlines P_s are computed there), and
+ * allocate the record buffer.  EINVAL / ERANGE / ENOMEM / ECUDA; *out untouched
+ * on error. */
+sw_status sw_plan_create(const sw_profile_tables *tables, const sw_scene_list *scenes,
+                         const sw_price_table *prices, const sw_runtime *rt, sw_plan **out);
+sw_status sw_plan_destroy(sw_plan *h);
+/* Drop all records and the running Pareto front (the tables stay). */
+sw_status sw_plan_reset(sw_plan *h);
+/* Chunked sweeps: fold every evaluated record into the running Pareto front, then
+ * drop the records (the front persists; later evals append to it). */
+sw_status sw_plan_release_records(sw_plan *h);
+
+/* N = prod r_b (the number of candidate plans). */
+sw_status sw_plan_space_size(const sw_plan *h, uint64_t *n);
+
+/* ---- evaluation (a1-a8) --------------------------------------------------- */
+
+/* Evaluate global candidates [begin, end): this rank's shard is decoded, scored and
+ * its 32 B records stored; the shard is folded into the running Pareto front.
+ * Asynchronous on the handle's stream.  EINVAL if the range is outside [0,N) or
+ * overlaps one evaluated before; ERANGE if the records would exceed capacity. */
+sw_status sw_plan_eval(sw_plan *h, uint64_t begin, uint64_t end);
+
+/* ---- reductions (a9, a10) ------------------------------------------------- */
+
+/* Constrained argmin over every record evaluated since create/reset (all ranks).
+ * Returns SW_OK with the winner, SW_CLOSEST with the closest plan when nothing is
+ * feasible, SW_EMPTY when nothing was evaluated.  Collective when nranks > 1. */
+sw_status sw_plan_select(sw_plan *h, uint64_t slo_startup_us, uint64_t slo_stall_us,
+                         uint64_t budget_mc, sw_selection *out);
+
+/* Several queries in one pass over the records (n_queries <= SW_MAX_QUERIES);
+ * out[q].status per query.  Return value: the worst soft status, or an error. */
+sw_status sw_plan_select_batch(sw_plan *h, uint32_t n_queries, const sw_query *queries,
+                               sw_selection *out);
+
+/* The running 3-D Pareto front over (ttff_eff min, cost min, quality max), exact
+ * duplicates keeping the lowest index (R14), sorted by (ttff_eff asc, cost asc,
+ * quality desc, index asc).  Two-call idiom: cap = 0 returns *n_out; a short
+ * buffer returns SW_TRUNCATED with *n_out = the required count.  Collective. */
+sw_status sw_pareto_get(sw_plan *h, sw_pareto_point *out, uint64_t cap, uint64_t *n_out);
+
+/* Order-independent 64-bit digest of all records evaluated (all ranks):
+ * sum_i mix64(i ^ rotl(ttff,7) ^ rotl(stall,19) ^ rotl(cost,31) ^
+ * (flags<<48 | quality<<16 | stall_count)) mod 2^64.  Collective. */
+sw_status sw_plan_digest(sw_plan *h, uint64_t *digest);
+
+/* Full metrics of any candidate (GPU kernel), e.g. to inspect a what-if plan.
+ * ready_us may be NULL or point to S entries (scene ready times R_s). */
+sw_status sw_plan_detail(sw_plan *h, uint64_t index, sw_selection *out, uint64_t *ready_us);
+
+/* Zero-copy view of this rank's records: device pointer, count and the global
+ * index of each segment's first record (segments = eval calls on this rank). */
+sw_status sw_plan_records(const sw_plan *h, const sw_record **dev_ptr, uint64_t *n);
+/* Copy n records starting at GLOBAL index `index` (must lie in one evaluated local
+ * segment) into host memory. */
+sw_status sw_plan_copy_records(sw_plan *h, uint64_t index, uint64_t n, sw_record *host_out);
+
+/* ---- multi-GPU --------------------------------------------- */
+
+/* Row-aligned contiguous shard of [begin, end) for `rank` of `nranks`: whole rows
+ * of `row` candidates are split evenly, a ragged head goes to rank 0 and a ragged
+ * tail to rank nranks-1.  Pure host arithmetic on indices. */
+sw_status sw_shard_range(uint64_t begin, uint64_t end, uint64_t row, int32_t rank,
+                         int32_t nranks, uint64_t *shard_begin, uint64_t *shard_end);
+/* Candidates per row of this plan (the unit the eval kernel gives one thread). */
+sw_status sw_plan_row_size(const sw_plan *h, uint64_t *row);
+
+/* NCCL bootstrap: rank 0 creates a 128-byte unique id, the caller broadcasts it
+ * (e.g. torch.distributed), every rank calls sw_comm_init on its device. */
+sw_status sw_comm_unique_id(void *id128);
+sw_status sw_comm_init(const void *id128, int32_t rank, int32_t nranks, int32_t device,
+                       void **comm_out);
+sw_status sw_comm_destroy(void *comm);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+const char *sw_status_str(sw_status s);
+const char *sw_last_error(const sw_plan *h); /* h may be NULL: last global error */
+/* Number of kernels this handle launched since create (for the bench's claim). */
+uint64_t sw_plan_launch_count(const sw_plan *h);
+/* Per-launch eval-kernel time of the last sw_plan_eval on this rank (CUDA events
+ * recorded on the handle's stream around the eval kernel), milliseconds. */
+sw_status sw_plan_last_eval_ms(sw_plan *h, float *ms);
+int32_t sw_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SW_PLAN_H */

@@ -39,6 +39,10 @@ class OrRecord(C.Structure):
                 ("quality", C.c_uint32), ("stall_count", C.c_uint16), ("flags", C.c_uint8),
                 ("pad", C.c_uint8)]
 
+    def astuple(self):
+        return (self.ttff_us, self.stall_us, self.cost_mc, self.quality, self.stall_count,
+                self.flags)
+
 
 class OrQuery(C.Structure):
     _fields_ = [("slo_startup_us", C.c_uint64), ("slo_stall_us", C.c_uint64),

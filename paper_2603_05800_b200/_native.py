@@ -1,0 +1,330 @@
+"""Thin ctypes binding of libsw_plan.so (include/sw_plan.h): argument marshalling only.
+
+Every step of the method runs in the library's CUDA kernels.  If the shared library
+is missing or no CUDA device is present, calls fail loudly (SwError) -- there is no
+CPU fallback.  This module never imports oracle/ (the CPU checker).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsw_plan.so")
+
+SW_OK, SW_CLOSEST, SW_TRUNCATED, SW_EMPTY = 0, 1, 2, 3
+SW_EINVAL, SW_ERANGE, SW_ENOMEM, SW_ECUDA, SW_ENCCL, SW_ESTATE = -1, -2, -3, -4, -5, -6
+SW_MAX_SCENES, SW_MAX_DIGITS, SW_MAX_CHOICES = 64, 16, 64
+SW_MAX_POOLS, SW_MAX_GPUS_PER_POOL, SW_MAX_QUERIES = 4, 8, 8
+UINT64_MAX = (1 << 64) - 1
+
+U64P = C.POINTER(C.c_uint64)
+U32P = C.POINTER(C.c_uint32)
+
+
+class sw_scene_list(C.Structure):
+    _fields_ = [("n_scenes", C.c_uint32), ("dur_us", U64P), ("llm_us", U64P), ("tts_us", U64P),
+                ("overhead_us", C.c_uint64), ("scene0_static", C.c_uint32),
+                ("static_ready_us", C.c_uint64)]
+
+
+class sw_choice(C.Structure):
+    _fields_ = [("level", C.c_uint8), ("degree", C.c_uint8), ("pool", C.c_uint8), ("pad", C.c_uint8)]
+
+
+class sw_profile_tables(C.Structure):
+    _fields_ = [("n_digits", C.c_uint32), ("radix", U32P), ("first_scene", U32P),
+                ("choices", C.POINTER(sw_choice)), ("va_us", U64P), ("n_levels", C.c_uint32),
+                ("level_score", U32P), ("heads", C.c_uint32)]
+
+
+class sw_price_table(C.Structure):
+    _fields_ = [("n_pools", C.c_uint32), ("gpus", U32P), ("price_mc_per_gpu_hour", U64P),
+                ("fixed_cost_mc", C.c_uint64), ("billing", C.c_uint32), ("objective", C.c_uint32)]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class sw_runtime(C.Structure):
+    _fields_ = [("device", C.c_int32), ("stream", C.c_void_p), ("nccl_comm", C.c_void_p),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("record_capacity", C.c_uint64),
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p)]
+
+
+class sw_record(C.Structure):
+    _fields_ = [("ttff_us", C.c_uint64), ("stall_us", C.c_uint64), ("cost_mc", C.c_uint64),
+                ("quality", C.c_uint32), ("stall_count", C.c_uint16), ("flags", C.c_uint8),
+                ("pad", C.c_uint8)]
+
+    def astuple(self):
+        return (self.ttff_us, self.stall_us, self.cost_mc, self.quality, self.stall_count,
+                self.flags)
+
+
+class sw_query(C.Structure):
+    _fields_ = [("slo_startup_us", C.c_uint64), ("slo_stall_us", C.c_uint64),
+                ("budget_mc", C.c_uint64)]
+
+
+class sw_selection(C.Structure):
+    _fields_ = [("status", C.c_int32), ("pad", C.c_uint32), ("index", C.c_uint64),
+                ("rec", sw_record), ("ttff_eff_us", C.c_uint64), ("makespan_us", C.c_uint64),
+                ("pool_end_us", C.c_uint64 * SW_MAX_POOLS), ("digit", C.c_uint8 * SW_MAX_DIGITS)]
+
+
+class sw_pareto_point(C.Structure):
+    _fields_ = [("index", C.c_uint64), ("ttff_eff_us", C.c_uint64), ("cost_mc", C.c_uint64),
+                ("quality", C.c_uint32), ("pad", C.c_uint32)]
+
+
+EXPORTS = {
+    # name: (restype, argtypes)
+    "sw_plan_create": (C.c_int32, [C.POINTER(sw_profile_tables), C.POINTER(sw_scene_list),
+                                   C.POINTER(sw_price_table), C.POINTER(sw_runtime),
+                                   C.POINTER(C.c_void_p)]),
+    "sw_plan_destroy": (C.c_int32, [C.c_void_p]),
+    "sw_plan_reset": (C.c_int32, [C.c_void_p]),
+    "sw_plan_release_records": (C.c_int32, [C.c_void_p]),
+    "sw_plan_space_size": (C.c_int32, [C.c_void_p, U64P]),
+    "sw_plan_eval": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64]),
+    "sw_plan_select": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                   C.POINTER(sw_selection)]),
+    "sw_plan_select_batch": (C.c_int32, [C.c_void_p, C.c_uint32, C.POINTER(sw_query),
+                                         C.POINTER(sw_selection)]),
+    "sw_pareto_get": (C.c_int32, [C.c_void_p, C.POINTER(sw_pareto_point), C.c_uint64, U64P]),
+    "sw_plan_digest": (C.c_int32, [C.c_void_p, U64P]),
+    "sw_plan_detail": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(sw_selection), U64P]),
+    "sw_plan_records": (C.c_int32, [C.c_void_p, C.POINTER(C.c_void_p), U64P]),
+    "sw_plan_copy_records": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64,
+                                         C.POINTER(sw_record)]),
+    "sw_shard_range": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32,
+                                   U64P, U64P]),
+    "sw_plan_row_size": (C.c_int32, [C.c_void_p, U64P]),
+    "sw_comm_unique_id": (C.c_int32, [C.c_void_p]),
+    "sw_comm_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                 C.POINTER(C.c_void_p)]),
+    "sw_comm_destroy": (C.c_int32, [C.c_void_p]),
+    "sw_status_str": (C.c_char_p, [C.c_int32]),
+    "sw_last_error": (C.c_char_p, [C.c_void_p]),
+    "sw_plan_launch_count": (C.c_uint64, [C.c_void_p]),
+    "sw_plan_last_eval_ms": (C.c_int32, [C.c_void_p, C.POINTER(C.c_float)]),
+    "sw_abi_version": (C.c_int32, []),
+}
+
+_lib = None
+
+
+class SwError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s: %s" % (status_str(status), msg))
+        self.status = status
+
+
+def lib():
+    """Load libsw_plan.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libsw_plan.so not built: run `python -c 'import __graft_entry__ as g; "
+                              "g.build()'` (nvcc, sm_100a)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def status_str(s: int) -> str:
+    try:
+        return lib().sw_status_str(s).decode()
+    except Exception:
+        return str(s)
+
+
+def _check(st: int, h=None):
+    if st < 0:
+        raise SwError(st, lib().sw_last_error(h).decode(errors="replace"))
+    return st
+
+
+def shard_range(begin: int, end: int, row: int, rank: int, nranks: int):
+    b, e = C.c_uint64(), C.c_uint64()
+    _check(lib().sw_shard_range(begin, end, row, rank, nranks, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().sw_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init(uid: bytes, rank: int, nranks: int, device: int) -> int:
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    out = C.c_void_p()
+    _check(lib().sw_comm_init(buf, rank, nranks, device, C.byref(out)))
+    return out.value
+
+
+def comm_destroy(comm: int) -> None:
+    _check(lib().sw_comm_destroy(C.c_void_p(comm)))
+
+
+@dataclass
+class Selection:
+    status: int
+    index: int
+    rec: tuple
+    ttff_eff_us: int
+    makespan_us: int
+    pool_end_us: List[int]
+    digit: List[int]
+
+
+def _sel(s: sw_selection, n_pools: int, B: int) -> Selection:
+    return Selection(s.status, s.index, s.rec.astuple(), s.ttff_eff_us, s.makespan_us,
+                     list(s.pool_end_us)[:n_pools], list(s.digit)[:B])
+
+
+def _arr(t, vals):
+    vals = list(vals)
+    return (t * max(1, len(vals)))(*vals)
+
+
+class Plan:
+    """One request's plan space on one rank (wraps an sw_plan handle).
+
+    ``problem`` is any object with the attributes of the C structs (duck-typed:
+    S, dur_us, llm_us, tts_us, overhead_us, scene0_static, static_ready_us, gpus,
+    price_mc, fixed_cost_mc, billing, objective, level_score, heads, radix,
+    first_scene, choices [(level, k, pool)], va_us).
+    """
+
+    def __init__(self, problem, device: int = 0, stream: Optional[int] = None,
+                 comm: Optional[int] = None, rank: int = 0, nranks: int = 1,
+                 record_capacity: int = 0):
+        L = lib()
+        pb = problem
+        self._keep = []
+        k = self._keep.append
+        self.n_pools = len(pb.gpus)
+        self.B = len(pb.radix)
+        self.S = pb.S
+        sc = sw_scene_list(pb.S, _arr(C.c_uint64, pb.dur_us), _arr(C.c_uint64, pb.llm_us),
+                           _arr(C.c_uint64, pb.tts_us), pb.overhead_us, pb.scene0_static,
+                           pb.static_ready_us)
+        chs = (sw_choice * len(pb.choices))(*[sw_choice(l, kk, p, 0) for (l, kk, p) in pb.choices])
+        tb = sw_profile_tables(len(pb.radix), _arr(C.c_uint32, pb.radix),
+                               _arr(C.c_uint32, pb.first_scene), chs, _arr(C.c_uint64, pb.va_us),
+                               len(pb.level_score), _arr(C.c_uint32, pb.level_score), pb.heads)
+        pr = sw_price_table(len(pb.gpus), _arr(C.c_uint32, pb.gpus), _arr(C.c_uint64, pb.price_mc),
+                            pb.fixed_cost_mc, pb.billing, pb.objective)
+        rt = sw_runtime(device, C.c_void_p(stream or 0), C.c_void_p(comm or 0), rank, nranks,
+                        record_capacity, ALLOC_FN(0), FREE_FN(0), None)
+        k((sc, chs, tb, pr, rt))
+        h = C.c_void_p()
+        st = L.sw_plan_create(C.byref(tb), C.byref(sc), C.byref(pr), C.byref(rt), C.byref(h))
+        if st < 0:
+            raise SwError(st, L.sw_last_error(None).decode(errors="replace"))
+        self.h = h
+        n = C.c_uint64()
+        L.sw_plan_space_size(h, C.byref(n))
+        self.n = n.value
+        r = C.c_uint64()
+        L.sw_plan_row_size(h, C.byref(r))
+        self.row = r.value
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sw_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _ck(self, st):
+        if st < 0:
+            raise SwError(st, lib().sw_last_error(self.h).decode(errors="replace"))
+        return st
+
+    # -- API (names follow the C ABI)
+    def reset(self):
+        self._ck(lib().sw_plan_reset(self.h))
+
+    def release_records(self):
+        self._ck(lib().sw_plan_release_records(self.h))
+
+    def eval(self, begin: int = 0, end: Optional[int] = None):
+        self._ck(lib().sw_plan_eval(self.h, begin, self.n if end is None else end))
+
+    def select(self, slo_startup_us=UINT64_MAX, slo_stall_us=UINT64_MAX, budget_mc=UINT64_MAX):
+        out = sw_selection()
+        self._ck(lib().sw_plan_select(self.h, slo_startup_us, slo_stall_us, budget_mc, C.byref(out)))
+        return _sel(out, self.n_pools, self.B)
+
+    def select_batch(self, queries: Sequence) -> List[Selection]:
+        """queries: objects with slo_startup_us / slo_stall_us / budget_mc, or 3-tuples."""
+        res = []
+        qs = [q if isinstance(q, tuple) else (q.slo_startup_us, q.slo_stall_us, q.budget_mc)
+              for q in queries]
+        for i in range(0, len(qs), SW_MAX_QUERIES):
+            chunk = qs[i:i + SW_MAX_QUERIES]
+            arr = (sw_query * len(chunk))(*[sw_query(*q) for q in chunk])
+            out = (sw_selection * len(chunk))()
+            self._ck(lib().sw_plan_select_batch(self.h, len(chunk), arr, out))
+            res += [_sel(o, self.n_pools, self.B) for o in out]
+        return res
+
+    def pareto(self):
+        n = C.c_uint64()
+        self._ck(lib().sw_pareto_get(self.h, None, 0, C.byref(n)))
+        buf = (sw_pareto_point * max(1, n.value))()
+        st = self._ck(lib().sw_pareto_get(self.h, buf, n.value, C.byref(n)))
+        assert st == SW_OK
+        return [(p.index, p.ttff_eff_us, p.cost_mc, p.quality) for p in buf[: n.value]]
+
+    def digest(self) -> int:
+        d = C.c_uint64()
+        self._ck(lib().sw_plan_digest(self.h, C.byref(d)))
+        return d.value
+
+    def detail(self, index: int):
+        out = sw_selection()
+        ready = (C.c_uint64 * SW_MAX_SCENES)()
+        self._ck(lib().sw_plan_detail(self.h, index, C.byref(out), ready))
+        return _sel(out, self.n_pools, self.B), list(ready)[: self.S]
+
+    def copy_records(self, index: int, n: int):
+        buf = (sw_record * max(1, n))()
+        self._ck(lib().sw_plan_copy_records(self.h, index, n, buf))
+        return buf
+
+    def records_view(self):
+        p = C.c_void_p()
+        n = C.c_uint64()
+        self._ck(lib().sw_plan_records(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def launch_count(self) -> int:
+        return lib().sw_plan_launch_count(self.h)
+
+    def last_eval_ms(self) -> float:
+        ms = C.c_float()
+        self._ck(lib().sw_plan_last_eval_ms(self.h, C.byref(ms)))
+        return ms.value

@@ -1,0 +1,687 @@
+// sw_kernels.cuh -- sm_100a kernels of libsw_plan.so.
+//
+// pack_kernel     : a2 fixed-stage ready times + deadlines + 16 B VA/quality entries
+// eval_kernel<NP> : a1 decode, a3 TMA-staged tables, a4 max-plus scan, a5-a7 metrics,
+//                   cost and the 32 B record store
+// detail_kernel   : one candidate's full metrics (winner report, what-if inspection)
+// select_*        : a9 constrained argmin (multi-query, warp/block/grid reductions)
+// pareto_*        : a8 exact 3-D Pareto front (DLT filter + exact dominance merge)
+// digest_kernel   : order-independent record digest (full-space parity tool)
+#pragma once
+#include "sw_device.cuh"
+
+namespace sw {
+
+constexpr int kEvalThreads = 128;
+constexpr int kScanThreads = 256;
+constexpr int kDltT = 64;  // dominance lookup table: ttff_eff bins
+constexpr int kDltQ = 64;  //                         quality bins
+
+// ============================================================================ a2 + packing
+struct RawDesc {
+    const uint64_t* dur;
+    const uint64_t* llm;
+    const uint64_t* tts;
+    const uint64_t* va;      // raw block-major stage times (host layout)
+    const uint32_t* score;   // level scores
+    const uint32_t* va_scene;  // scene of each raw va entry (index bookkeeping from host)
+    const uint32_t* va_choice; // global choice slot of each raw va entry
+    uint64_t overhead;
+    uint32_t n_va;
+};
+
+// One block.  Thread 0 runs the sequential fixed-stage recurrence (plan-independent,
+// S <= 64 steps): the LLM streams scenes in order and each finished scene triggers its
+// downstream stages; one FIFO TTS server (Table 4; R2/R3):
+//   L += llm_s ; A = max(L, A) + tts_s ; a_s = A.
+// Deadlines P_s = sum_{j<s} d_j.  All threads fill the VA entries with the
+// quality contribution q = dur_ms(s) * score(level) (R12).
+__global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* __restrict__ va) {
+    if (threadIdx.x == 0) {
+        uint64_t L = raw.overhead, A = 0, acc = 0;
+        const bool stat = hdr->flags & 1u;
+        for (uint32_t s = 0; s < hdr->S; s++) {
+            if (s == 0 && stat) {
+                hdr->a[s] = 0;
+            } else {
+                L = L + raw.llm[s];
+                A = (L > A ? L : A) + raw.tts[s];
+                hdr->a[s] = A;
+            }
+            hdr->P[s] = acc;
+            acc += raw.dur[s];
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < raw.n_va; i += blockDim.x) {
+        const uint32_t s = raw.va_scene[i];
+        const uint32_t lv = ch_level(hdr->choice[raw.va_choice[i]]);
+        VaEntry e;
+        e.t_us = raw.va[i];
+        e.q = (uint32_t)((raw.dur[s] / 1000ull) * raw.score[lv]);
+        e.pad = 0;
+        va[i] = e;
+    }
+}
+
+// ============================================================================ a1-a7 eval
+// Thread <-> row H: the candidates [H*row, (H+1)*row) share their HI digits (digits
+// 0..B-3).  The thread simulates the HI scenes once (per-lane choices, runtime k/pool),
+// then iterates the MID digit and the LSD digit in lock-step with the other lanes:
+// (k, pool) is warp-uniform there, so the gang update uses compile-time slot indices
+// and the LSD step (the dominant loop) is ~40 integer ops + one 32 B store.
+// Amortised scene-steps per candidate: L_LSD + L_MID / r_LSD + L_HI / row.
+template <int NP>
+__global__ void __launch_bounds__(kEvalThreads) eval_kernel(
+    const DevHeader* __restrict__ g_hdr, const VaEntry* __restrict__ g_va, uint32_t va_bytes,
+    uint64_t row_begin, uint64_t row_end, uint64_t seg_begin, uint64_t seg_end,
+    Rec4* __restrict__ out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bar;
+    DevHeader& h = *reinterpret_cast<DevHeader*>(smem);
+    VaEntry* va = reinterpret_cast<VaEntry*>(smem + sizeof(DevHeader));
+    stage_tables(g_hdr, g_va, &h, va, va_bytes, &bar);
+
+    const uint32_t bm = h.B - 2, bl = h.B - 1;
+    const uint32_t rm = h.radix[bm], rl = h.radix[bl];
+    const uint32_t mfirst = h.first[bm], mlast = h.first[bm + 1];
+    const uint32_t lfirst = h.first[bl], llast = h.first[bl + 1];
+    const uint64_t row = h.row;
+    const bool busy_bill = h.flags & 2u;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+
+    for (uint64_t H = row_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; H < row_end;
+         H += stride) {
+        State<NP> st;
+        state_init(st, h);
+        // ---- HI prefix: decode the row index (MSD = earliest block, R19) and simulate
+        uint64_t rem = H;
+        for (uint32_t b = 0; b < bm; b++) {
+            const uint64_t pl = h.place[b];
+            uint32_t c;
+            if ((rem >> 32) == 0 && (pl >> 32) == 0) c = (uint32_t)rem / (uint32_t)pl;
+            else c = (uint32_t)(rem / pl);
+            rem -= (uint64_t)c * pl;
+            const uint32_t ch = h.choice[h.coff[b] + c];
+            const uint32_t k = ch_k(ch), p = ch_pool(ch);
+            const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
+            const VaEntry* vb = va + h.voff[b] + c;
+            for (uint32_t s = f0; s < f1; s++) {
+                const VaEntry v = vb[(s - f0) * r];
+                const uint64_t e = scene_step<NP, 0>(st, p, k, h.a[s], v.t_us);
+                scene_metrics(st, s, e, h.P[s], v.q);
+            }
+        }
+        // ---- MID digit: warp-uniform choice
+        for (uint32_t dm = 0; dm < rm; dm++) {
+            State<NP> s2 = st;
+            {
+                const uint32_t ch = h.choice[h.coff[bm] + dm];
+                const uint32_t k = ch_k(ch), p = ch_pool(ch);
+                const VaEntry* vb = va + h.voff[bm] + dm;
+                for (uint32_t s = mfirst; s < mlast; s++) {
+                    const VaEntry v = vb[(s - mfirst) * rm];
+                    const uint64_t e = scene_step_uniform<NP>(s2, p, k, h.a[s], v.t_us);
+                    scene_metrics(s2, s, e, h.P[s], v.q);
+                }
+            }
+            const uint64_t ibase = H * row + (uint64_t)dm * rl;
+            if (llast - lfirst == 1) {
+                // ---- LSD fast path (single last scene): only pool p changes
+                uint64_t pc[NP];
+                uint64_t pcsum = h.fixed_cost;
+#pragma unroll
+                for (int q = 0; q < NP; q++) {
+                    const uint64_t X = busy_bill ? s2.busy[q] : (uint64_t)h.G[q] * s2.end[q];
+                    pc[q] = pool_cost(X, h.price[q]);
+                    pcsum += pc[q];
+                }
+                const uint32_t s = lfirst;
+                const uint64_t as = h.a[s];
+                const int64_t Ps = (int64_t)h.P[s];
+                const VaEntry* vb = va + h.voff[bl];
+                const uint32_t* cb = h.choice + h.coff[bl];
+                for (uint32_t dl = 0; dl < rl; dl++) {
+                    const uint32_t ch = cb[dl];
+                    const uint32_t k = ch_k(ch), p = ch_pool(ch);
+                    const VaEntry v = vb[dl];
+                    uint64_t fk = 0, endp = 0, busyp = 0, pcp = 0, Gp = 0, price = 0;
+#pragma unroll
+                    for (int q = 0; q < NP; q++) {
+                        if ((uint32_t)q == p) {
+                            switch (k) {
+                                case 1: fk = s2.F[q][0]; break;
+                                case 2: fk = s2.F[q][1]; break;
+                                case 4: fk = s2.F[q][3]; break;
+                                case 8: fk = s2.F[q][7]; break;
+                                default: fk = sel_dyn(s2.F[q], k - 1);
+                            }
+                            endp = s2.end[q];
+                            busyp = s2.busy[q];
+                            pcp = pc[q];
+                            Gp = h.G[q];
+                            price = h.price[q];
+                        }
+                    }
+                    const uint64_t e = umax64(as, fk) + v.t_us;
+                    const uint64_t X = busy_bill ? busyp + (uint64_t)k * v.t_us : Gp * umax64(endp, e);
+                    const uint64_t cost = pcsum - pcp + pool_cost(X, price);
+                    uint64_t R0 = s2.R0;
+                    int64_t M = s2.M;
+                    uint32_t cnt = s2.cnt;
+                    if (s == 0) {
+                        R0 = e;
+                        M = (int64_t)e;
+                    } else {
+                        const int64_t d = (int64_t)e - Ps;
+                        if (d > M) {
+                            M = d;
+                            cnt++;
+                        }
+                    }
+                    Rec4 r;
+                    r.w0 = R0;
+                    r.w1 = (uint64_t)M - R0;
+                    r.w2 = cost;
+                    r.w3 = (uint64_t)(s2.Q + v.q) | ((uint64_t)cnt << 32) |
+                           ((uint64_t)(s2.used | (1u << p)) << 48);
+                    const uint64_t i = ibase + dl;
+                    if (i >= seg_begin && i < seg_end) st_global_256(out + (i - seg_begin), r);
+                }
+            } else {
+                // ---- generic LSD block (several scenes share the last digit)
+                for (uint32_t dl = 0; dl < rl; dl++) {
+                    State<NP> s3 = s2;
+                    const uint32_t ch = h.choice[h.coff[bl] + dl];
+                    const uint32_t k = ch_k(ch), p = ch_pool(ch);
+                    const VaEntry* vb = va + h.voff[bl] + dl;
+                    for (uint32_t s = lfirst; s < llast; s++) {
+                        const VaEntry v = vb[(s - lfirst) * rl];
+                        const uint64_t e = scene_step_uniform<NP>(s3, p, k, h.a[s], v.t_us);
+                        scene_metrics(s3, s, e, h.P[s], v.q);
+                    }
+                    Rec4 r;
+                    r.w0 = s3.R0;
+                    r.w1 = (uint64_t)s3.M - s3.R0;
+                    r.w2 = state_cost(s3, h);
+                    r.w3 = (uint64_t)s3.Q | ((uint64_t)s3.cnt << 32) | ((uint64_t)s3.used << 48);
+                    const uint64_t i = ibase + dl;
+                    if (i >= seg_begin && i < seg_end) st_global_256(out + (i - seg_begin), r);
+                }
+            }
+        }
+    }
+}
+
+// ============================================================================ detail
+struct DetailOut {
+    Rec4 rec;
+    uint64_t ttff_eff, makespan;
+    uint64_t pool_end[kMaxP];
+    uint64_t ready[SW_MAX_SCENES];
+    uint32_t digit[kMaxDigits];
+};
+
+template <int NP>
+__global__ void detail_kernel(const DevHeader* __restrict__ g_hdr, const VaEntry* __restrict__ g_va,
+                              uint64_t index, DetailOut* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const DevHeader& h = *g_hdr;
+    State<NP> st;
+    state_init(st, h);
+    uint32_t dig[kMaxDigits];
+    uint64_t rem = index;
+    for (int b = (int)h.B - 1; b >= 0; b--) {  // a1: i mod r_b, LSD first
+        dig[b] = (uint32_t)(rem % h.radix[b]);
+        rem /= h.radix[b];
+    }
+    if (h.flags & 1u) out->ready[0] = h.R0_static;
+    for (uint32_t b = 0; b < h.B; b++) {
+        const uint32_t c = dig[b];
+        out->digit[b] = c;
+        const uint32_t ch = h.choice[h.coff[b] + c];
+        for (uint32_t s = h.first[b]; s < h.first[b + 1]; s++) {
+            const VaEntry v = g_va[h.voff[b] + (s - h.first[b]) * h.radix[b] + c];
+            const uint64_t e = scene_step<NP, 0>(st, ch_pool(ch), ch_k(ch), h.a[s], v.t_us);
+            scene_metrics(st, s, e, h.P[s], v.q);
+            out->ready[s] = e;
+        }
+    }
+    uint64_t mk = st.R0;
+    for (int p = 0; p < NP; p++) {
+        out->pool_end[p] = st.end[p];
+        mk = umax64(mk, st.end[p]);
+    }
+    out->rec.w0 = st.R0;
+    out->rec.w1 = (uint64_t)st.M - st.R0;
+    out->rec.w2 = state_cost(st, h);
+    out->rec.w3 = (uint64_t)st.Q | ((uint64_t)st.cnt << 32) | ((uint64_t)st.used << 48);
+    out->ttff_eff = (uint64_t)st.M;
+    out->makespan = mk;
+}
+
+// ============================================================================ a9 select
+struct QueryDev {
+    uint64_t slo_t, slo_s, budget;
+};
+struct SelParams {
+    uint32_t nq, objective;
+    QueryDev q[SW_MAX_QUERIES];
+};
+struct Cand {
+    uint64_t idx;  // kInf64 = none
+    uint64_t pad;
+    Rec4 r;
+};
+
+__device__ __forceinline__ uint64_t sat_sub(uint64_t x, uint64_t y) { return x > y ? x - y : 0; }
+
+__device__ __forceinline__ bool feasible(const QueryDev& q, const Rec4& r) {
+    return r.w0 <= q.slo_t && r.w1 <= q.slo_s && r.w2 <= q.budget;
+}
+
+// Objective order (R13): true iff a precedes b.
+__device__ __forceinline__ int obj_cmp(uint32_t obj, uint64_t ia, const Rec4& a, uint64_t ib,
+                                       const Rec4& b) {
+    const uint64_t ta = a.w0 + a.w1, tb = b.w0 + b.w1;
+    const uint32_t qa = rec_Q(a), qb = rec_Q(b);
+    if (obj == 0) {  // QUALITY_FIRST (-Q, cost, ttff_eff, index)
+        if (qa != qb) return qa > qb ? -1 : 1;
+        if (a.w2 != b.w2) return a.w2 < b.w2 ? -1 : 1;
+        if (ta != tb) return ta < tb ? -1 : 1;
+    } else {  // COST_X_TTFF (cost x ttff_eff as 128-bit, -Q, index)
+        const uint64_t lo_a = a.w2 * ta, hi_a = __umul64hi(a.w2, ta);
+        const uint64_t lo_b = b.w2 * tb, hi_b = __umul64hi(b.w2, tb);
+        if (hi_a != hi_b) return hi_a < hi_b ? -1 : 1;
+        if (lo_a != lo_b) return lo_a < lo_b ? -1 : 1;
+        if (qa != qb) return qa > qb ? -1 : 1;
+    }
+    if (ia != ib) return ia < ib ? -1 : 1;
+    return 0;
+}
+
+// Total order of a query: feasible plans by objective; then (nothing feasible)
+// the closest plan by (V_t, V_c, objective, index) ("returns the closest
+// solution").  Invalid candidates (idx = inf) are last.
+__device__ __forceinline__ bool cand_better(const QueryDev& q, uint32_t obj, uint64_t ia,
+                                            const Rec4& a, uint64_t ib, const Rec4& b) {
+    if (ib == kInf64) return ia != kInf64;
+    if (ia == kInf64) return false;
+    const bool fa = feasible(q, a), fb = feasible(q, b);
+    if (fa != fb) return fa;
+    if (!fa) {
+        const uint64_t vta = sat_sub(a.w0, q.slo_t) + sat_sub(a.w1, q.slo_s);
+        const uint64_t vtb = sat_sub(b.w0, q.slo_t) + sat_sub(b.w1, q.slo_s);
+        if (vta != vtb) return vta < vtb;
+        const uint64_t vca = sat_sub(a.w2, q.budget), vcb = sat_sub(b.w2, q.budget);
+        if (vca != vcb) return vca < vcb;
+    }
+    return obj_cmp(obj, ia, a, ib, b) < 0;
+}
+
+__device__ __forceinline__ void shfl_cand(uint64_t& idx, Rec4& r, int off) {
+    const uint64_t i2 = __shfl_down_sync(0xffffffffu, idx, off);
+    Rec4 o;
+    o.w0 = __shfl_down_sync(0xffffffffu, r.w0, off);
+    o.w1 = __shfl_down_sync(0xffffffffu, r.w1, off);
+    o.w2 = __shfl_down_sync(0xffffffffu, r.w2, off);
+    o.w3 = __shfl_down_sync(0xffffffffu, r.w3, off);
+    idx = i2;
+    r = o;
+}
+
+// Block-level argmin of per-thread candidates; result valid in thread 0.
+__device__ __forceinline__ void block_reduce_cand(const QueryDev& q, uint32_t obj, uint64_t& idx,
+                                                  Rec4& r, Cand* s_tmp /* [32] */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        uint64_t oi = idx;
+        Rec4 orr = r;
+        shfl_cand(oi, orr, off);
+        if (lane + off < 32 && cand_better(q, obj, oi, orr, idx, r)) {
+            idx = oi;
+            r = orr;
+        }
+    }
+    __syncthreads();
+    if (lane == 0) {
+        s_tmp[warp].idx = idx;
+        s_tmp[warp].r = r;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        if (lane < nw) {
+            idx = s_tmp[lane].idx;
+            r = s_tmp[lane].r;
+        } else {
+            idx = kInf64;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            uint64_t oi = idx;
+            Rec4 orr = r;
+            shfl_cand(oi, orr, off);
+            if (lane + off < 32 && cand_better(q, obj, oi, orr, idx, r)) {
+                idx = oi;
+                r = orr;
+            }
+        }
+    }
+}
+
+// Grid-stride scan of one record segment for up to 8 queries at once: one 32 B load
+// per candidate feeds every query (HBM read-bound).  Writes per-block bests.
+__global__ void __launch_bounds__(kScanThreads) select_scan_kernel(
+    const Rec4* __restrict__ recs, uint64_t n, uint64_t first_index, SelParams P,
+    Cand* __restrict__ partial /* [gridDim.x][SW_MAX_QUERIES] */) {
+    __shared__ Cand s_tmp[32];
+    uint64_t bi[SW_MAX_QUERIES];
+    Rec4 br[SW_MAX_QUERIES];
+#pragma unroll
+    for (int q = 0; q < SW_MAX_QUERIES; q++) bi[q] = kInf64;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const Rec4 r = ld_global_nc_256(recs + i);
+        const uint64_t idx = first_index + i;
+#pragma unroll
+        for (int q = 0; q < SW_MAX_QUERIES; q++) {
+            if ((uint32_t)q < P.nq && cand_better(P.q[q], P.objective, idx, r, bi[q], br[q])) {
+                bi[q] = idx;
+                br[q] = r;
+            }
+        }
+    }
+#pragma unroll 1
+    for (uint32_t q = 0; q < P.nq; q++) {
+        uint64_t idx = bi[0];
+        Rec4 r = br[0];
+#pragma unroll
+        for (int j = 1; j < SW_MAX_QUERIES; j++)
+            if ((uint32_t)j == q) {
+                idx = bi[j];
+                r = br[j];
+            }
+        block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
+        if (threadIdx.x == 0) {
+            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].idx = idx;
+            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].r = r;
+        }
+    }
+}
+
+// Reduce n_partial candidates per query (strided by SW_MAX_QUERIES) -> out[q].
+// Used after the scan (per-block partials) and for the cross-rank merge (a10).
+__global__ void __launch_bounds__(kScanThreads) select_final_kernel(
+    const Cand* __restrict__ partial, uint32_t n_partial, SelParams P, Cand* __restrict__ out) {
+    __shared__ Cand s_tmp[32];
+    for (uint32_t q = 0; q < P.nq; q++) {
+        uint64_t idx = kInf64;
+        Rec4 r{};
+        for (uint32_t j = threadIdx.x; j < n_partial; j += blockDim.x) {
+            const Cand c = partial[(uint64_t)j * SW_MAX_QUERIES + q];
+            if (cand_better(P.q[q], P.objective, c.idx, c.r, idx, r)) {
+                idx = c.idx;
+                r = c.r;
+            }
+        }
+        block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
+        if (threadIdx.x == 0) {
+            out[q].idx = idx;
+            out[q].r = r;
+            // status flag for the host: 1 = closest (nothing feasible)
+            out[q].pad = (idx != kInf64 && !feasible(P.q[q], r)) ? 1ull : 0ull;
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================================ digest
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(kScanThreads) digest_kernel(const Rec4* __restrict__ recs, uint64_t n,
+                                                              uint64_t first_index,
+                                                              unsigned long long* __restrict__ acc) {
+    uint64_t sum = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const Rec4 r = ld_global_nc_256(recs + i);
+        // w3 = Q | cnt << 32 | flags << 48  ->  flags << 48 | Q << 16 | cnt
+        const uint64_t w = ((r.w3 >> 48) << 48) | ((r.w3 & 0xffffffffull) << 16) | ((r.w3 >> 32) & 0xffffull);
+        sum += mix64((first_index + i) ^ rotl64(r.w0, 7) ^ rotl64(r.w1, 19) ^ rotl64(r.w2, 31) ^ w);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
+    if ((threadIdx.x & 31) == 0) atomicAdd(acc, (unsigned long long)sum);
+}
+
+// ============================================================================ a8 Pareto
+struct __align__(16) PPoint {  // == sw_pareto_point
+    uint64_t idx, t, c;
+    uint32_t q, pad;
+};
+
+// y dominates x: <= in ttff_eff and cost, >= in quality, one strict; exact duplicates
+// keep the lowest index (R14); identical entries (same index) keep the first position.
+__device__ __forceinline__ bool pdom(const PPoint& y, uint32_t py, const PPoint& x, uint32_t px) {
+    if (!(y.t <= x.t && y.c <= x.c && y.q >= x.q)) return false;
+    if (y.t < x.t || y.c < x.c || y.q > x.q) return true;
+    if (y.idx != x.idx) return y.idx < x.idx;
+    return py < px;
+}
+
+// keep[x] = no other point of pts[0,m) dominates x.  O(m^2), tiles through smem.
+__global__ void __launch_bounds__(kScanThreads) pareto_mark_kernel(const PPoint* __restrict__ pts,
+                                                                   uint32_t m, uint8_t* __restrict__ keep) {
+    __shared__ PPoint tile[kScanThreads];
+    const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+    PPoint px{};
+    if (x < m) px = pts[x];
+    bool dom = x >= m;
+    for (uint32_t base = 0; base < m; base += blockDim.x) {
+        if (__syncthreads_and(dom)) break;
+        const uint32_t y = base + threadIdx.x;
+        if (y < m) tile[threadIdx.x] = pts[y];
+        __syncthreads();
+        const uint32_t lim = min((uint32_t)blockDim.x, m - base);
+        if (!dom)
+            for (uint32_t j = 0; j < lim; j++)
+                if (base + j != x && pdom(tile[j], base + j, px, x)) {
+                    dom = true;
+                    break;
+                }
+        __syncthreads();
+    }
+    if (x < m) keep[x] = dom ? 0 : 1;
+}
+
+__global__ void pareto_compact_kernel(const PPoint* __restrict__ pts, uint32_t m,
+                                      const uint8_t* __restrict__ keep, PPoint* __restrict__ out,
+                                      unsigned int* __restrict__ count) {
+    const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < m && keep[x]) out[atomicAdd(count, 1u)] = pts[x];
+}
+
+__device__ __forceinline__ bool pkey_less(const PPoint& a, const PPoint& b) {
+    if (a.t != b.t) return a.t < b.t;
+    if (a.c != b.c) return a.c < b.c;
+    if (a.q != b.q) return a.q > b.q;
+    return a.idx < b.idx;
+}
+
+// out[rank(x)] = x with rank = #{y : key(y) < key(x)}: deterministic ordering of a
+// front (indices are unique) by (ttff_eff asc, cost asc, quality desc, index asc).
+__global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint* __restrict__ pts,
+                                                                   uint32_t m, PPoint* __restrict__ out) {
+    __shared__ PPoint tile[kScanThreads];
+    const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+    PPoint px{};
+    if (x < m) px = pts[x];
+    uint32_t rank = 0;
+    for (uint32_t base = 0; base < m; base += blockDim.x) {
+        const uint32_t y = base + threadIdx.x;
+        if (y < m) tile[threadIdx.x] = pts[y];
+        __syncthreads();
+        const uint32_t lim = min((uint32_t)blockDim.x, m - base);
+        for (uint32_t j = 0; j < lim; j++) rank += pkey_less(tile[j], px) ? 1u : 0u;
+        __syncthreads();
+    }
+    if (x < m) out[rank] = px;
+}
+
+// Dominance lookup table from the current front (sorted by ttff_eff):
+// cell[bt][bq] = min cost over front points f with f.t <= tedge[bt] and f.q >= qedge[bq].
+// A record (t, c, q) with bt = max{i: tedge[i] <= t}, bq = min{j: qedge[j] >= q} and
+// cell < c is strictly dominated by a real candidate, so it cannot be on the front.
+struct Dlt {
+    uint64_t tedge[kDltT];
+    uint32_t qedge[kDltQ];
+    uint64_t cell[kDltT * kDltQ];
+};
+
+__global__ void __launch_bounds__(1024) dlt_build_kernel(const PPoint* __restrict__ front, uint32_t m,
+                                                         Dlt* __restrict__ d) {
+    __shared__ uint32_t qmin_s, qmax_s;
+    if (threadIdx.x == 0) {
+        qmin_s = 0xffffffffu;
+        qmax_s = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        atomicMin(&qmin_s, front[i].q);
+        atomicMax(&qmax_s, front[i].q);
+    }
+    __syncthreads();
+    const uint32_t qmin = qmin_s, qmax = qmax_s;
+    for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x)
+        d->tedge[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
+    for (uint32_t j = threadIdx.x; j < kDltQ; j += blockDim.x)
+        d->qedge[j] = m ? (uint32_t)(qmin + ((uint64_t)(qmax - qmin) * j) / (kDltQ - 1)) : 0xffffffffu;
+    __syncthreads();
+    for (uint32_t cidx = threadIdx.x; cidx < kDltT * kDltQ; cidx += blockDim.x) {
+        const uint32_t bt = cidx / kDltQ, bq = cidx % kDltQ;
+        const uint64_t te = d->tedge[bt];
+        const uint32_t qe = d->qedge[bq];
+        uint64_t best = kInf64;
+        for (uint32_t i = 0; i < m && front[i].t <= te; i++)
+            if (front[i].q >= qe) best = umin64(best, front[i].c);
+        d->cell[cidx] = best;
+    }
+}
+
+// Filter one record segment: (1) the DLT prefilter (O(1) per record), then (2) for
+// DLT survivors an exact warp-cooperative dominance test against up to m_sm front
+// points held in shared memory (32 front points per step, __any_sync early exit).
+// Records dominated by a real candidate cannot be on the front, so the surviving set
+// always contains every true front point of the segment: the merge stays exact for
+// any front subset used here.  Survivors are appended at work[base + slot].
+constexpr uint32_t kFrontSmem = 1024;
+
+__global__ void __launch_bounds__(kScanThreads) pareto_filter_kernel(
+    const Rec4* __restrict__ recs, uint64_t n, uint64_t first_index, const Dlt* __restrict__ g_dlt,
+    const PPoint* __restrict__ front, uint32_t m_sm, PPoint* __restrict__ work, uint64_t base,
+    unsigned long long* __restrict__ counter, uint64_t cap) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    Dlt& d = *reinterpret_cast<Dlt*>(fsm);
+    PPoint* fs = reinterpret_cast<PPoint*>(fsm + sizeof(Dlt));
+    for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x) d.tedge[i] = g_dlt->tedge[i];
+    for (uint32_t i = threadIdx.x; i < kDltQ; i += blockDim.x) d.qedge[i] = g_dlt->qedge[i];
+    for (uint32_t i = threadIdx.x; i < kDltT * kDltQ; i += blockDim.x) d.cell[i] = g_dlt->cell[i];
+    for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = front[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + threadIdx.x;
+        bool keep = false;
+        PPoint pt{};
+        if (i < n) {
+            const Rec4 r = ld_global_nc_256(recs + i);
+            pt.idx = first_index + i;
+            pt.t = r.w0 + r.w1;
+            pt.c = r.w2;
+            pt.q = rec_Q(r);
+            int lo = 0, hi = kDltT;  // bt = (#edges <= t) - 1
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (d.tedge[mid] <= pt.t) lo = mid + 1;
+                else hi = mid;
+            }
+            const int bt = lo - 1;
+            int lo2 = 0, hi2 = kDltQ;  // bq = min{j : qedge[j] >= q}
+            while (lo2 < hi2) {
+                const int mid = (lo2 + hi2) >> 1;
+                if (d.qedge[mid] >= pt.q) hi2 = mid;
+                else lo2 = mid + 1;
+            }
+            const int bq = lo2;
+            keep = (bt < 0 || bq >= kDltQ) ? true : !(d.cell[bt * kDltQ + bq] < pt.c);
+        }
+        unsigned pend = __ballot_sync(0xffffffffu, keep);
+        while (pend) {  // exact test of each DLT survivor by the whole warp
+            const int src = __ffs(pend) - 1;
+            pend &= pend - 1;
+            PPoint x;
+            x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
+            x.t = __shfl_sync(0xffffffffu, pt.t, src);
+            x.c = __shfl_sync(0xffffffffu, pt.c, src);
+            x.q = __shfl_sync(0xffffffffu, pt.q, src);
+            bool dom = false;
+            for (uint32_t j0 = 0; j0 < m_sm; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                // an identical entry (same index) also removes x: it is already kept
+                const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
+                if (__any_sync(0xffffffffu, dj)) {
+                    dom = true;
+                    break;
+                }
+            }
+            if (lane == src && dom) keep = false;
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (mask) {
+            const int leader = __ffs(mask) - 1;
+            unsigned long long slot0 = 0;
+            if (lane == leader) slot0 = atomicAdd(counter, (unsigned long long)__popc(mask));
+            slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+            if (keep) {
+                const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+                if (slot < cap) work[base + slot] = pt;
+            }
+        }
+    }
+}
+
+// Strided sample of a record segment -> points (seed for the first DLT).
+__global__ void pareto_sample_kernel(const Rec4* __restrict__ recs, uint64_t n, uint64_t first_index,
+                                     uint32_t ns, PPoint* __restrict__ out) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ns) return;
+    const uint64_t i = (uint64_t)((unsigned __int128)j * n / ns);
+    const Rec4 r = ld_global_nc_256(recs + i);
+    PPoint p;
+    p.idx = first_index + i;
+    p.t = r.w0 + r.w1;
+    p.c = r.w2;
+    p.q = rec_Q(r);
+    p.pad = 0;
+    out[j] = p;
+}
+
+// Gather variable-size per-rank fronts (allgathered, padded to maxc) into one array.
+__global__ void pareto_gather_kernel(const PPoint* __restrict__ padded, const uint64_t* __restrict__ counts,
+                                     int nranks, uint64_t maxc, PPoint* __restrict__ out) {
+    const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t r = x / maxc, j = x % maxc;
+    if ((int)r >= nranks || j >= counts[r]) return;
+    uint64_t off = 0;
+    for (uint64_t q = 0; q < r; q++) off += counts[q];
+    out[off + j] = padded[x];
+}
+
+}  // namespace sw

@@ -1,0 +1,905 @@
+// sw_plan.cu -- host runtime + C ABI of libsw_plan.so (see include/sw_plan.h).
+//
+// Host code here only validates inputs, does index bookkeeping (digit padding,
+// place values, shard ranges, segment table), moves bytes and launches kernels.
+// Every step of the method -- fixed-stage ready times, decode, the max-plus scan,
+// metrics, cost, selection, Pareto and the cross-rank merge -- runs in the CUDA
+// kernels of sw_kernels.cuh.  There is no CPU fallback: without a device every
+// call that needs one returns SW_ECUDA.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "sw_kernels.cuh"
+#include "sw_plan.h"
+
+using namespace sw;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Segment {
+    uint64_t gbegin, gend;  // global range of the eval call
+    uint64_t begin, end;    // this rank's shard
+    uint64_t offset;        // first record slot in the buffer
+    bool folded;            // already folded into the Pareto front
+};
+
+}  // namespace
+
+struct sw_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    sw_alloc_fn alloc = nullptr;
+    sw_free_fn free_fn = nullptr;
+    void* alloc_ctx = nullptr;
+
+    DevHeader h{};  // host image of the index bookkeeping
+    uint32_t NP = 1, S = 0, B_user = 0, pad_digits = 0;
+    uint64_t N = 0, row = 1;
+    uint32_t n_va = 0, va_bytes = 0;
+    int num_sms = 148;
+    int eval_grid = 0;
+    size_t eval_smem = 0;
+
+    DevHeader* d_hdr = nullptr;
+    VaEntry* d_va = nullptr;
+    Rec4* d_rec = nullptr;
+    uint64_t rec_cap = 0, rec_used = 0;
+    std::vector<Segment> segs;
+
+    // Pareto
+    PPoint* d_front = nullptr;
+    uint64_t front_n = 0;
+    uint64_t front_cap = 1ull << 17;
+    uint64_t surv_cap = 1ull << 17;
+    PPoint* d_work = nullptr;  // front_cap + surv_cap
+    PPoint* d_tmp = nullptr;   // front_cap + surv_cap
+    uint8_t* d_keep = nullptr;
+    unsigned long long* d_counter = nullptr;
+    unsigned int* d_ucount = nullptr;
+    Dlt* d_dlt = nullptr;
+    PPoint* d_gather = nullptr;  // multi-rank padded fronts
+    uint64_t* d_counts = nullptr;
+
+    // select / detail / digest
+    Cand* d_partial = nullptr;
+    uint32_t scan_grid = 0;
+    uint32_t max_partial = 0;
+    Cand* d_cand = nullptr;
+    Cand* d_cand_all = nullptr;
+    DetailOut* d_detail = nullptr;
+    unsigned long long* d_digest = nullptr;
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool have_eval_ev = false;
+    uint64_t launches = 0;
+    std::string err;
+};
+
+namespace {
+
+sw_status fail(sw_plan* h, sw_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    if (h) h->err = buf;
+    return s;
+}
+
+#define CK(h, call)                                                                          \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail((h), SW_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+
+#define CKL(h)                                                                                \
+    do {                                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                                  \
+        if (e_ != cudaSuccess)                                                                \
+            return fail((h), SW_ECUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                  \
+        (h)->launches++;                                                                      \
+    } while (0)
+
+#define CKN(h, call)                                                                          \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail((h), SW_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_));        \
+    } while (0)
+
+void* dev_alloc(sw_plan* h, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (h->alloc) return h->alloc(bytes, h->stream, h->alloc_ctx);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void dev_free(sw_plan* h, void* p) {
+    if (!p) return;
+    if (h->free_fn) h->free_fn(p, h->stream, h->alloc_ctx);
+    else cudaFreeAsync(p, h->stream);
+}
+
+template <typename T>
+sw_status alloc_n(sw_plan* h, T** p, uint64_t n, const char* what) {
+    *p = (T*)dev_alloc(h, (size_t)(n * sizeof(T)));
+    if (!*p) return fail(h, SW_ENOMEM, "device allocation of %s (%llu bytes) failed", what,
+                         (unsigned long long)(n * sizeof(T)));
+    return SW_OK;
+}
+
+template <typename F>
+sw_status launch_np(sw_plan* h, F&& f) {
+    switch (h->NP) {
+        case 1: f(std::integral_constant<int, 1>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        case 3: f(std::integral_constant<int, 3>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        default: return fail(h, SW_EINVAL, "bad pool count");
+    }
+    return SW_OK;
+}
+
+using u128 = unsigned __int128;
+
+}  // namespace
+
+static sw_status fold_pending(sw_plan* h);
+
+// ============================================================================ create
+extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_list* sc,
+                                    const sw_price_table* pr, const sw_runtime* rt, sw_plan** out) {
+    if (!tb || !sc || !pr || !rt || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    const uint32_t S = sc->n_scenes;
+    if (S < 1 || S > SW_MAX_SCENES) return fail(nullptr, SW_EINVAL, "n_scenes %u not in 1..%d", S, SW_MAX_SCENES);
+    if (!sc->dur_us || !sc->llm_us || !sc->tts_us) return fail(nullptr, SW_EINVAL, "null scene array");
+    for (uint32_t s = 0; s < S; s++)
+        if (sc->dur_us[s] == 0) return fail(nullptr, SW_EINVAL, "scene %u has duration 0", s);
+    const uint32_t B = tb->n_digits;
+    if (B < 1 || B > SW_MAX_DIGITS) return fail(nullptr, SW_EINVAL, "n_digits %u not in 1..%d", B, SW_MAX_DIGITS);
+    if (!tb->radix || !tb->first_scene || !tb->choices || !tb->va_us || !tb->level_score)
+        return fail(nullptr, SW_EINVAL, "null table array");
+    const uint32_t NP = pr->n_pools;
+    if (NP < 1 || NP > SW_MAX_POOLS) return fail(nullptr, SW_EINVAL, "n_pools %u not in 1..%d", NP, SW_MAX_POOLS);
+    if (!pr->gpus || !pr->price_mc_per_gpu_hour) return fail(nullptr, SW_EINVAL, "null price array");
+    for (uint32_t p = 0; p < NP; p++)
+        if (pr->gpus[p] < 1 || pr->gpus[p] > SW_MAX_GPUS_PER_POOL)
+            return fail(nullptr, SW_EINVAL, "pool %u has %u GPUs (1..%d supported)", p, pr->gpus[p],
+                        SW_MAX_GPUS_PER_POOL);
+    if (pr->billing > 1 || pr->objective > 1) return fail(nullptr, SW_EINVAL, "bad billing/objective");
+    if (tb->n_levels < 1) return fail(nullptr, SW_EINVAL, "n_levels = 0");
+    const uint32_t s0 = sc->scene0_static ? 1u : 0u;
+    if (s0 && S < 2) return fail(nullptr, SW_EINVAL, "a static intro needs S >= 2");
+    if (tb->first_scene[0] != s0 || tb->first_scene[B] != S)
+        return fail(nullptr, SW_EINVAL, "digit blocks must cover scenes [%u, %u)", s0, S);
+    uint64_t N = 1;
+    uint32_t n_choice = 0;
+    uint64_t n_va = 0;
+    for (uint32_t b = 0; b < B; b++) {
+        const uint32_t r = tb->radix[b];
+        if (r < 1 || r > SW_MAX_CHOICES) return fail(nullptr, SW_EINVAL, "radix[%u] = %u not in 1..%d", b, r, SW_MAX_CHOICES);
+        if (tb->first_scene[b + 1] <= tb->first_scene[b])
+            return fail(nullptr, SW_EINVAL, "digit %u has an empty scene block", b);
+        if ((u128)N * r >= ((u128)1 << 63)) return fail(nullptr, SW_ERANGE, "plan space >= 2^63 (InstanceTooLarge)");
+        N *= r;
+        n_choice += r;
+        n_va += (uint64_t)(tb->first_scene[b + 1] - tb->first_scene[b]) * r;
+    }
+    for (uint32_t c = 0; c < n_choice; c++) {
+        const sw_choice& ch = tb->choices[c];
+        if (ch.level >= tb->n_levels) return fail(nullptr, SW_EINVAL, "choice %u: level %u >= n_levels", c, ch.level);
+        if (ch.pool >= NP) return fail(nullptr, SW_EINVAL, "choice %u: pool %u >= n_pools", c, ch.pool);
+        if (ch.degree < 1 || ch.degree > pr->gpus[ch.pool])
+            return fail(nullptr, SW_EINVAL, "choice %u: k = %u exceeds G_p = %u", c, ch.degree, pr->gpus[ch.pool]);
+        if (tb->heads && tb->heads % ch.degree)
+            return fail(nullptr, SW_EINVAL, "choice %u: k = %u does not divide %u heads (P:748)", c, ch.degree, tb->heads);
+    }
+    for (uint64_t i = 0; i < n_va; i++)
+        if (tb->va_us[i] == 0) return fail(nullptr, SW_EINVAL, "va_us[%llu] = 0", (unsigned long long)i);
+    // ---- overflow bounds (R25): every intermediate fits its integer type
+    {
+        u128 fixed = (u128)sc->overhead_us + sc->static_ready_us;
+        u128 dsum = 0, qsum = 0;
+        uint32_t max_score = 0;
+        for (uint32_t l = 0; l < tb->n_levels; l++) max_score = std::max(max_score, tb->level_score[l]);
+        for (uint32_t s = 0; s < S; s++) {
+            fixed += (u128)sc->llm_us[s] + sc->tts_us[s];
+            dsum += sc->dur_us[s];
+            qsum += (u128)(sc->dur_us[s] / 1000) * max_score;
+        }
+        u128 tmax = fixed;
+        uint64_t off = 0;
+        for (uint32_t b = 0; b < B; b++) {
+            const uint32_t r = tb->radix[b];
+            for (uint32_t s = tb->first_scene[b]; s < tb->first_scene[b + 1]; s++) {
+                uint64_t mx = 0;
+                for (uint32_t c = 0; c < r; c++) mx = std::max(mx, tb->va_us[off + (s - tb->first_scene[b]) * r + c]);
+                tmax += mx;
+            }
+            off += (uint64_t)(tb->first_scene[b + 1] - tb->first_scene[b]) * r;
+        }
+        const u128 lim62 = (u128)1 << 62;
+        if (tmax >= lim62 || dsum >= lim62) return fail(nullptr, SW_ERANGE, "time bound exceeds 2^62 us");
+        if (qsum >= ((u128)1 << 32)) return fail(nullptr, SW_ERANGE, "quality bound exceeds 2^32");
+        u128 cmax = pr->fixed_cost_mc;
+        for (uint32_t p = 0; p < NP; p++) {
+            const u128 X = (u128)pr->gpus[p] * tmax;  // >= busy and >= G * span
+            const u128 prod = X * pr->price_mc_per_gpu_hour[p] + kHalfHour;
+            if (prod >= ((u128)1 << 64)) return fail(nullptr, SW_ERANGE, "cost bound of pool %u exceeds 2^64", p);
+            cmax += prod / kUsPerHour;
+        }
+        if (cmax >= ((u128)1 << 64)) return fail(nullptr, SW_ERANGE, "cost bound exceeds 2^64");
+    }
+    if (rt->nranks < 1 || rt->rank < 0 || rt->rank >= rt->nranks)
+        return fail(nullptr, SW_EINVAL, "bad rank %d of %d", rt->rank, rt->nranks);
+    if (rt->nranks > 1 && !rt->nccl_comm) return fail(nullptr, SW_EINVAL, "nranks > 1 needs nccl_comm");
+
+    sw_plan* h = new sw_plan();
+    h->device = rt->device;
+    h->comm = (ncclComm_t)rt->nccl_comm;
+    h->rank = rt->rank;
+    h->nranks = rt->nranks;
+    h->alloc = rt->alloc;
+    h->free_fn = rt->free;
+    h->alloc_ctx = rt->alloc_ctx;
+    h->NP = NP;
+    h->S = S;
+    h->B_user = B;
+    h->N = N;
+    auto bail = [&](sw_status s) {
+        sw_plan_destroy(h);
+        return s;
+    };
+    if (cudaSetDevice(h->device) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(nullptr, SW_ECUDA, "cudaSetDevice(%d) failed (no CUDA device?)", h->device));
+    }
+    if (rt->stream) {
+        h->stream = (cudaStream_t)rt->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(nullptr, SW_ECUDA, "cudaStreamCreate failed"));
+        h->own_stream = true;
+    }
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+    if (!h->alloc) {  // keep freed blocks in the stream-ordered pool (repeated create/destroy)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    }
+
+    // ---- index bookkeeping: left-pad digits to B >= 3 with radix-1 empty blocks
+    DevHeader& H = h->h;
+    memset(&H, 0, sizeof H);
+    const uint32_t pad = B >= 3 ? 0 : 3 - B;
+    const uint32_t BP = B + pad;
+    h->pad_digits = pad;
+    H.S = S;
+    H.B = BP;
+    H.NP = NP;
+    H.flags = (s0 ? 1u : 0u) | (pr->billing ? 2u : 0u) | (pr->objective ? 4u : 0u);
+    H.s0 = s0;
+    H.R0_static = s0 ? sc->static_ready_us : 0;
+    H.fixed_cost = pr->fixed_cost_mc;
+    H.N = N;
+    H.choice[0] = 0u | (1u << 8) | (0u << 16);  // dummy choice of the virtual digits
+    uint32_t coff = 1, voff = 0;
+    for (uint32_t b = 0; b < BP; b++) {
+        if (b < pad) {
+            H.radix[b] = 1;
+            H.first[b] = s0;
+            H.coff[b] = 0;
+            H.voff[b] = 0;
+        } else {
+            const uint32_t ub = b - pad;
+            H.radix[b] = tb->radix[ub];
+            H.first[b] = tb->first_scene[ub];
+            H.coff[b] = coff;
+            H.voff[b] = voff;
+            for (uint32_t c = 0; c < tb->radix[ub]; c++) {
+                const sw_choice& ch = tb->choices[coff - 1 + c];
+                H.choice[coff + c] = (uint32_t)ch.level | ((uint32_t)ch.degree << 8) | ((uint32_t)ch.pool << 16);
+            }
+            coff += tb->radix[ub];
+            voff += (tb->first_scene[ub + 1] - tb->first_scene[ub]) * tb->radix[ub];
+        }
+    }
+    H.first[BP] = S;
+    H.n_choice = coff;
+    H.n_va = (uint32_t)n_va;
+    H.va_bytes = n_va * sizeof(VaEntry);
+    h->row = (uint64_t)H.radix[BP - 2] * H.radix[BP - 1];
+    H.row = h->row;
+    H.n_rows = N / h->row;
+    {
+        uint64_t pl = 1;
+        for (int b = (int)BP - 3; b >= 0; b--) {
+            H.place[b] = pl;
+            pl *= H.radix[b];
+        }
+    }
+    for (uint32_t p = 0; p < NP; p++) {
+        H.G[p] = pr->gpus[p];
+        H.price[p] = pr->price_mc_per_gpu_hour[p];
+    }
+    h->n_va = (uint32_t)n_va;
+    h->va_bytes = (uint32_t)(n_va * sizeof(VaEntry));
+
+    // ---- upload raw inputs + header, pack on the device (a2 runs in pack_kernel)
+    std::vector<uint32_t> va_scene(n_va), va_choice(n_va);
+    {
+        uint64_t i = 0;
+        for (uint32_t b = 0; b < B; b++) {
+            const uint32_t r = tb->radix[b];
+            for (uint32_t s = tb->first_scene[b]; s < tb->first_scene[b + 1]; s++)
+                for (uint32_t c = 0; c < r; c++, i++) {
+                    va_scene[i] = s;
+                    va_choice[i] = H.coff[b + pad] + c;
+                }
+        }
+    }
+    const size_t n_raw64 = 3 * (size_t)S + n_va;
+    const size_t raw_bytes = n_raw64 * 8 + (size_t)tb->n_levels * 4 + 2 * (size_t)n_va * 4;
+    std::vector<uint8_t> raw(raw_bytes);
+    size_t o = 0;
+    auto put = [&](const void* src, size_t bytes) {
+        memcpy(raw.data() + o, src, bytes);
+        o += bytes;
+    };
+    put(sc->dur_us, 8 * (size_t)S);
+    put(sc->llm_us, 8 * (size_t)S);
+    put(sc->tts_us, 8 * (size_t)S);
+    put(tb->va_us, 8 * (size_t)n_va);
+    put(tb->level_score, 4 * (size_t)tb->n_levels);
+    put(va_scene.data(), 4 * (size_t)n_va);
+    put(va_choice.data(), 4 * (size_t)n_va);
+    uint8_t* d_raw = nullptr;
+    sw_status st;
+    if ((st = alloc_n(h, &h->d_hdr, 1, "header")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_va, std::max<uint64_t>(n_va, 1), "va table")) < 0) return bail(st);
+    if ((st = alloc_n(h, &d_raw, raw_bytes, "raw inputs")) < 0) return bail(st);
+    if (cudaMemcpyAsync(h->d_hdr, &H, sizeof H, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+        cudaMemcpyAsync(d_raw, raw.data(), raw_bytes, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        dev_free(h, d_raw);
+        return bail(fail(nullptr, SW_ECUDA, "table upload failed"));
+    }
+    RawDesc rd;
+    {
+        const uint64_t* r64 = (const uint64_t*)d_raw;
+        rd.dur = r64;
+        rd.llm = r64 + S;
+        rd.tts = r64 + 2 * S;
+        rd.va = r64 + 3 * S;
+        const uint32_t* r32 = (const uint32_t*)(r64 + 3 * S + n_va);
+        rd.score = r32;
+        rd.va_scene = r32 + tb->n_levels;
+        rd.va_choice = r32 + tb->n_levels + n_va;
+        rd.overhead = sc->overhead_us;
+        rd.n_va = (uint32_t)n_va;
+    }
+    pack_kernel<<<1, 256, 0, h->stream>>>(rd, h->d_hdr, h->d_va);
+    if (cudaGetLastError() != cudaSuccess) {
+        dev_free(h, d_raw);
+        return bail(fail(nullptr, SW_ECUDA, "pack_kernel launch failed"));
+    }
+    h->launches++;
+    dev_free(h, d_raw);
+    // keep the host mirror's a/P unused (device-owned); fetch nothing back.
+
+    // ---- eval launch configuration: persistent grid sized by occupancy x SMs
+    h->eval_smem = sizeof(DevHeader) + h->va_bytes;
+    {
+        int occ = 0;
+        cudaError_t e = cudaSuccess;
+        launch_np(h, [&](auto np) {
+            constexpr int NPc = decltype(np)::value;
+            e = cudaFuncSetAttribute(eval_kernel<NPc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)h->eval_smem);
+            if (e == cudaSuccess)
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eval_kernel<NPc>, kEvalThreads,
+                                                                  h->eval_smem);
+        });
+        if (e != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            return bail(fail(nullptr, SW_ECUDA, "eval kernel cannot launch (%s, occupancy %d)",
+                             cudaGetErrorString(e), occ));
+        }
+        h->eval_grid = occ * h->num_sms;
+    }
+    h->scan_grid = (uint32_t)h->num_sms * 4;
+    if (cudaFuncSetAttribute(pareto_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(Dlt) + kFrontSmem * sizeof(PPoint))) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(nullptr, SW_ECUDA, "filter kernel smem attribute failed"));
+    }
+
+    // ---- record buffer + reduction scratch
+    uint64_t cap = rt->record_capacity;
+    if (cap == 0) cap = N / (uint64_t)h->nranks + 2 * h->row + 1;
+    cap = std::min<uint64_t>(cap, N);
+    h->rec_cap = cap;
+    if ((st = alloc_n(h, &h->d_rec, cap, "records")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_front, h->front_cap, "pareto front")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_work, h->front_cap + h->surv_cap, "pareto work")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_tmp, h->front_cap + h->surv_cap, "pareto tmp")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_keep, h->front_cap + h->surv_cap, "pareto flags")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_counter, 2, "counter")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_ucount, 2, "counter")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_dlt, 1, "dlt")) < 0) return bail(st);
+    h->max_partial = h->scan_grid * 64;  // up to 64 segments per select
+    if ((st = alloc_n(h, &h->d_partial, (uint64_t)h->max_partial * SW_MAX_QUERIES, "partials")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_cand, SW_MAX_QUERIES, "winners")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_cand_all, (uint64_t)SW_MAX_QUERIES * h->nranks, "winners all")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_detail, 1, "detail")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_digest, 1, "digest")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 1, "counts")) < 0) return bail(st);
+    if (h->nranks > 1)
+        if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return bail(st);
+    if (cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
+        return bail(fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(nullptr, SW_ECUDA, "create: device work failed"));
+    }
+    *out = h;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_destroy(sw_plan* h) {
+    if (!h) return SW_OK;
+    if (h->stream) {
+        cudaSetDevice(h->device);
+        void* bufs[] = {h->d_hdr,   h->d_va,      h->d_rec,     h->d_front, h->d_work,
+                        h->d_tmp,   h->d_keep,    h->d_counter, h->d_ucount, h->d_dlt,
+                        h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest,
+                        h->d_counts, h->d_gather};
+        for (void* b : bufs) dev_free(h, b);
+        cudaStreamSynchronize(h->stream);
+        if (h->ev0) cudaEventDestroy(h->ev0);
+        if (h->ev1) cudaEventDestroy(h->ev1);
+        if (h->own_stream) cudaStreamDestroy(h->stream);
+        cudaGetLastError();
+    }
+    delete h;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_reset(sw_plan* h) {
+    if (!h) return fail(nullptr, SW_EINVAL, "null handle");
+    h->segs.clear();
+    h->rec_used = 0;
+    h->front_n = 0;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_release_records(sw_plan* h) {
+    if (!h) return fail(nullptr, SW_EINVAL, "null handle");
+    // fold pending records into the running front first (the front survives)
+    sw_status st = fold_pending(h);
+    if (st < 0) return st;
+    h->segs.clear();
+    h->rec_used = 0;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_space_size(const sw_plan* h, uint64_t* n) {
+    if (!h || !n) return fail(nullptr, SW_EINVAL, "null argument");
+    *n = h->N;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_row_size(const sw_plan* h, uint64_t* row) {
+    if (!h || !row) return fail(nullptr, SW_EINVAL, "null argument");
+    *row = h->row;
+    return SW_OK;
+}
+
+// ============================================================================ shard
+extern "C" sw_status sw_shard_range(uint64_t begin, uint64_t end, uint64_t row, int32_t rank,
+                                    int32_t nranks, uint64_t* sb, uint64_t* se) {
+    if (!sb || !se || nranks < 1 || rank < 0 || rank >= nranks || row == 0 || end < begin)
+        return fail(nullptr, SW_EINVAL, "bad shard arguments");
+    const uint64_t r0 = (begin + row - 1) / row;  // first whole row
+    const uint64_t r1 = end / row;                // one past the last whole row
+    if (r1 <= r0) {  // no whole row: everything on rank 0
+        *sb = rank == 0 ? begin : end;
+        *se = end;
+        if (rank != 0) *sb = *se = end;
+        return SW_OK;
+    }
+    const uint64_t nr = r1 - r0;
+    const uint64_t a = r0 + (uint64_t)((u128)nr * (uint64_t)rank / (uint64_t)nranks);
+    const uint64_t b = r0 + (uint64_t)((u128)nr * (uint64_t)(rank + 1) / (uint64_t)nranks);
+    *sb = rank == 0 ? begin : a * row;
+    *se = rank == nranks - 1 ? end : b * row;
+    return SW_OK;
+}
+
+// ============================================================================ eval
+extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
+    if (!h) return fail(nullptr, SW_EINVAL, "null handle");
+    if (begin > end || end > h->N)
+        return fail(h, SW_EINVAL, "range [%llu, %llu) outside [0, %llu)", (unsigned long long)begin,
+                    (unsigned long long)end, (unsigned long long)h->N);
+    if (begin == end) return SW_OK;
+    for (const Segment& g : h->segs)
+        if (begin < g.gend && g.gbegin < end) return fail(h, SW_EINVAL, "range overlaps an evaluated range");
+    uint64_t b, e;
+    sw_status st = sw_shard_range(begin, end, h->row, h->rank, h->nranks, &b, &e);
+    if (st < 0) return st;
+    const uint64_t n = e - b;
+    if (h->rec_used + n > h->rec_cap)
+        return fail(h, SW_ERANGE, "records would exceed capacity (%llu + %llu > %llu): reset or chunk",
+                    (unsigned long long)h->rec_used, (unsigned long long)n, (unsigned long long)h->rec_cap);
+    Segment sg{begin, end, b, e, h->rec_used, false};
+    CK(h, cudaSetDevice(h->device));
+    if (n > 0) {
+        const uint64_t rb = b / h->row, re = (e + h->row - 1) / h->row;
+        const uint64_t need = (re - rb + kEvalThreads - 1) / kEvalThreads;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(need, (uint64_t)h->eval_grid);
+        Rec4* outp = h->d_rec + h->rec_used;
+        CK(h, cudaEventRecord(h->ev0, h->stream));
+        launch_np(h, [&](auto np) {
+            constexpr int NPc = decltype(np)::value;
+            eval_kernel<NPc><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(
+                h->d_hdr, h->d_va, h->va_bytes, rb, re, b, e, outp);
+        });
+        CKL(h);
+        CK(h, cudaEventRecord(h->ev1, h->stream));
+        h->have_eval_ev = true;
+        h->rec_used += n;
+    }
+    h->segs.push_back(sg);
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_last_eval_ms(sw_plan* h, float* ms) {
+    if (!h || !ms) return fail(nullptr, SW_EINVAL, "null argument");
+    if (!h->have_eval_ev) return fail(h, SW_ESTATE, "no eval launched yet");
+    CK(h, cudaEventSynchronize(h->ev1));
+    CK(h, cudaEventElapsedTime(ms, h->ev0, h->ev1));
+    return SW_OK;
+}
+
+// ============================================================================ select
+static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint64_t* ready) {
+    launch_np(h, [&](auto np) {
+        constexpr int NPc = decltype(np)::value;
+        detail_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_hdr, h->d_va, index, h->d_detail);
+    });
+    CKL(h);
+    DetailOut d;
+    CK(h, cudaMemcpyAsync(&d, h->d_detail, sizeof d, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    out->index = index;
+    out->rec.ttff_us = d.rec.w0;
+    out->rec.stall_us = d.rec.w1;
+    out->rec.cost_mc = d.rec.w2;
+    out->rec.quality = (uint32_t)d.rec.w3;
+    out->rec.stall_count = (uint16_t)(d.rec.w3 >> 32);
+    out->rec.flags = (uint8_t)(d.rec.w3 >> 48);
+    out->rec.pad = 0;
+    out->ttff_eff_us = d.ttff_eff;
+    out->makespan_us = d.makespan;
+    for (int p = 0; p < SW_MAX_POOLS; p++) out->pool_end_us[p] = p < (int)h->NP ? d.pool_end[p] : 0;
+    memset(out->digit, 0, sizeof out->digit);
+    for (uint32_t b = 0; b < h->B_user; b++) out->digit[b] = (uint8_t)d.digit[b + h->pad_digits];
+    if (ready) memcpy(ready, d.ready, sizeof(uint64_t) * h->S);
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
+    if (!h || !qs || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (nq < 1 || nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u not in 1..%d", nq, SW_MAX_QUERIES);
+    CK(h, cudaSetDevice(h->device));
+    SelParams P{};
+    P.nq = nq;
+    P.objective = (h->h.flags & 4u) ? 1u : 0u;
+    for (uint32_t q = 0; q < nq; q++) P.q[q] = QueryDev{qs[q].slo_startup_us, qs[q].slo_stall_us, qs[q].budget_mc};
+    uint32_t np = 0;
+    for (const Segment& g : h->segs) {
+        const uint64_t n = g.end - g.begin;
+        if (n == 0) continue;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
+        if (np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many segments for one select");
+        select_scan_kernel<<<grid, kScanThreads, 0, h->stream>>>(h->d_rec + g.offset, n, g.begin, P,
+                                                                 h->d_partial + (uint64_t)np * SW_MAX_QUERIES);
+        CKL(h);
+        np += grid;
+    }
+    if (np == 0) {
+        // empty local contribution: a row of "none" candidates
+        std::vector<Cand> none(SW_MAX_QUERIES);
+        for (auto& c : none) c.idx = kInf64;
+        CK(h, cudaMemcpyAsync(h->d_partial, none.data(), sizeof(Cand) * SW_MAX_QUERIES, cudaMemcpyHostToDevice,
+                              h->stream));
+        np = 1;
+    }
+    select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_partial, np, P, h->d_cand);
+    CKL(h);
+    if (h->nranks > 1) {  // a10: allgather per-rank winners over NVLink, replicated merge
+        CKN(h, ncclAllGather(h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, ncclUint8, h->comm,
+                             h->stream));
+        select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_cand_all, (uint32_t)h->nranks, P, h->d_cand);
+        CKL(h);
+    }
+    Cand win[SW_MAX_QUERIES];
+    CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nq, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    sw_status worst = SW_OK;
+    for (uint32_t q = 0; q < nq; q++) {
+        memset(&out[q], 0, sizeof(sw_selection));
+        if (win[q].idx == kInf64) {
+            out[q].status = SW_EMPTY;
+            worst = std::max<sw_status>(worst, SW_EMPTY);
+            continue;
+        }
+        sw_status st = fill_detail(h, win[q].idx, &out[q], nullptr);
+        if (st < 0) return st;
+        out[q].status = win[q].pad ? SW_CLOSEST : SW_OK;  // feasibility flag set on device
+        worst = std::max<sw_status>(worst, out[q].status);
+    }
+    return worst;
+}
+
+extern "C" sw_status sw_plan_select(sw_plan* h, uint64_t slo_startup_us, uint64_t slo_stall_us, uint64_t budget_mc,
+                                    sw_selection* out) {
+    sw_query q{slo_startup_us, slo_stall_us, budget_mc};
+    return sw_plan_select_batch(h, 1, &q, out);
+}
+
+extern "C" sw_status sw_plan_detail(sw_plan* h, uint64_t index, sw_selection* out, uint64_t* ready_us) {
+    if (!h || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (index >= h->N) return fail(h, SW_EINVAL, "index out of range");
+    CK(h, cudaSetDevice(h->device));
+    memset(out, 0, sizeof *out);
+    sw_status st = fill_detail(h, index, out, ready_us);
+    if (st < 0) return st;
+    out->status = SW_OK;
+    return SW_OK;
+}
+
+// ============================================================================ digest
+extern "C" sw_status sw_plan_digest(sw_plan* h, uint64_t* digest) {
+    if (!h || !digest) return fail(nullptr, SW_EINVAL, "null argument");
+    CK(h, cudaSetDevice(h->device));
+    CK(h, cudaMemsetAsync(h->d_digest, 0, sizeof(unsigned long long), h->stream));
+    for (const Segment& g : h->segs) {
+        const uint64_t n = g.end - g.begin;
+        if (!n) continue;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
+        digest_kernel<<<grid, kScanThreads, 0, h->stream>>>(h->d_rec + g.offset, n, g.begin, h->d_digest);
+        CKL(h);
+    }
+    if (h->nranks > 1)
+        CKN(h, ncclAllReduce(h->d_digest, h->d_digest, 1, ncclUint64, ncclSum, h->comm, h->stream));
+    unsigned long long v = 0;
+    CK(h, cudaMemcpyAsync(&v, h->d_digest, sizeof v, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    *digest = v;
+    return SW_OK;
+}
+
+// ============================================================================ Pareto
+// Exact front of pts[0, m) -> d_front (sorted), m <= front_cap + surv_cap.
+static sw_status exact_front(sw_plan* h, PPoint* pts, uint64_t m) {
+    if (m == 0) {
+        h->front_n = 0;
+        return SW_OK;
+    }
+    const uint32_t g = (uint32_t)((m + kScanThreads - 1) / kScanThreads);
+    pareto_mark_kernel<<<g, kScanThreads, 0, h->stream>>>(pts, (uint32_t)m, h->d_keep);
+    CKL(h);
+    CK(h, cudaMemsetAsync(h->d_ucount, 0, sizeof(unsigned int), h->stream));
+    PPoint* comp = (pts == h->d_tmp) ? h->d_work : h->d_tmp;
+    pareto_compact_kernel<<<g, kScanThreads, 0, h->stream>>>(pts, (uint32_t)m, h->d_keep, comp, h->d_ucount);
+    CKL(h);
+    unsigned int cnt = 0;
+    CK(h, cudaMemcpyAsync(&cnt, h->d_ucount, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (cnt > h->front_cap) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
+    const uint32_t g2 = (cnt + kScanThreads - 1) / kScanThreads;
+    if (cnt) {
+        pareto_rank_kernel<<<g2, kScanThreads, 0, h->stream>>>(comp, cnt, h->d_front);
+        CKL(h);
+    }
+    h->front_n = cnt;
+    return SW_OK;
+}
+
+static sw_status fold_segment(sw_plan* h, const Segment& g) {
+    const uint64_t n = g.end - g.begin;
+    if (n == 0) return SW_OK;
+    const Rec4* recs = h->d_rec + g.offset;
+    if (h->front_n == 0) {  // seed from a strided sample of this segment
+        const uint32_t ns = (uint32_t)std::min<uint64_t>(n, 65536);
+        pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(recs, n, g.begin, ns, h->d_work);
+        CKL(h);
+        sw_status st = exact_front(h, h->d_work, ns);
+        if (st < 0) return st;
+    }
+    for (int iter = 0; iter < 64; iter++) {
+        const uint64_t m = h->front_n;
+        dlt_build_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, (uint32_t)m, h->d_dlt);
+        CKL(h);
+        CK(h, cudaMemcpyAsync(h->d_work, h->d_front, m * sizeof(PPoint), cudaMemcpyDeviceToDevice, h->stream));
+        CK(h, cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned long long), h->stream));
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
+        // exact-check subset: the first kFrontSmem front points (sorted by ttff_eff)
+        const uint32_t m_sm = (uint32_t)std::min<uint64_t>(m, kFrontSmem);
+        const size_t smem = sizeof(Dlt) + (size_t)m_sm * sizeof(PPoint);
+        pareto_filter_kernel<<<grid, kScanThreads, smem, h->stream>>>(recs, n, g.begin, h->d_dlt, h->d_front, m_sm,
+                                                                      h->d_work, m, h->d_counter, h->surv_cap);
+        CKL(h);
+        unsigned long long surv = 0;
+        CK(h, cudaMemcpyAsync(&surv, h->d_counter, sizeof surv, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+        const uint64_t used = std::min<uint64_t>(surv, h->surv_cap);
+        sw_status st = exact_front(h, h->d_work, m + used);
+        if (st < 0) return st;
+        if (surv <= h->surv_cap) return SW_OK;
+        // survivors overflowed: the merged front is a better filter -> refilter
+    }
+    return fail(h, SW_ERANGE, "Pareto filter did not converge");
+}
+
+static sw_status fold_pending(sw_plan* h) {
+    CK(h, cudaSetDevice(h->device));
+    for (Segment& g : h->segs) {
+        if (g.folded) continue;
+        sw_status st = fold_segment(h, g);
+        if (st < 0) return st;
+        g.folded = true;
+    }
+    return SW_OK;
+}
+
+extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t cap, uint64_t* n_out) {
+    if (!h || !n_out || (cap && !out)) return fail(nullptr, SW_EINVAL, "null argument");
+    sw_status st = fold_pending(h);
+    if (st < 0) return st;
+    const PPoint* res = h->d_front;
+    uint64_t n = h->front_n;
+    if (h->nranks > 1) {  // a10: allgather counts, then padded fronts; exact merge
+        uint64_t mine = h->front_n;
+        CK(h, cudaMemcpyAsync(h->d_counts + h->nranks, &mine, 8, cudaMemcpyHostToDevice, h->stream));
+        CKN(h, ncclAllGather(h->d_counts + h->nranks, h->d_counts, 1, ncclUint64, h->comm, h->stream));
+        std::vector<uint64_t> counts(h->nranks);
+        CK(h, cudaMemcpyAsync(counts.data(), h->d_counts, 8 * h->nranks, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+        uint64_t maxc = 1, tot = 0;
+        for (uint64_t c : counts) {
+            maxc = std::max(maxc, c);
+            tot += c;
+        }
+        CKN(h, ncclAllGather(h->d_front, h->d_gather, maxc * sizeof(PPoint), ncclUint8, h->comm, h->stream));
+        if (tot > h->front_cap + h->surv_cap) return fail(h, SW_ERANGE, "merged fronts too large");
+        const uint64_t all = maxc * (uint64_t)h->nranks;
+        pareto_gather_kernel<<<(uint32_t)((all + 255) / 256), 256, 0, h->stream>>>(h->d_gather, h->d_counts,
+                                                                                  h->nranks, maxc, h->d_tmp);
+        CKL(h);
+        // merge into a scratch front (keep the local running front intact)
+        PPoint* saved = h->d_front;
+        uint64_t saved_n = h->front_n;
+        h->d_front = h->d_gather;  // reuse gather buffer as output (>= front_cap)
+        st = exact_front(h, h->d_tmp, tot);
+        res = h->d_front;
+        n = h->front_n;
+        h->d_front = saved;
+        h->front_n = saved_n;
+        if (st < 0) return st;
+    }
+    *n_out = n;
+    if (cap == 0) return SW_OK;
+    if (cap < n) return SW_TRUNCATED;
+    CK(h, cudaMemcpyAsync(out, res, n * sizeof(PPoint), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    return SW_OK;
+}
+
+// ============================================================================ views
+extern "C" sw_status sw_plan_records(const sw_plan* h, const sw_record** dev_ptr, uint64_t* n) {
+    if (!h || !dev_ptr || !n) return fail(nullptr, SW_EINVAL, "null argument");
+    *dev_ptr = (const sw_record*)h->d_rec;
+    *n = h->rec_used;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_copy_records(sw_plan* h, uint64_t index, uint64_t n, sw_record* host_out) {
+    if (!h || (n && !host_out)) return fail(nullptr, SW_EINVAL, "null argument");
+    for (const Segment& g : h->segs) {
+        if (index >= g.begin && index + n <= g.end) {
+            CK(h, cudaSetDevice(h->device));
+            CK(h, cudaMemcpyAsync(host_out, h->d_rec + g.offset + (index - g.begin), n * sizeof(sw_record),
+                                  cudaMemcpyDeviceToHost, h->stream));
+            CK(h, cudaStreamSynchronize(h->stream));
+            return SW_OK;
+        }
+    }
+    return fail(h, SW_EINVAL, "range not inside one local segment");
+}
+
+// ============================================================================ NCCL
+extern "C" sw_status sw_comm_unique_id(void* id128) {
+    if (!id128) return fail(nullptr, SW_EINVAL, "null argument");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, SW_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "nccl unique id size");
+    memcpy(id128, &id, 128);
+    return SW_OK;
+}
+
+extern "C" sw_status sw_comm_init(const void* id128, int32_t rank, int32_t nranks, int32_t device, void** comm_out) {
+    if (!id128 || !comm_out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(nullptr, SW_ECUDA, "cudaSetDevice(%d) failed", device);
+    }
+    ncclUniqueId id;
+    memcpy(&id, id128, 128);
+    ncclComm_t c = nullptr;
+    ncclResult_t r = ncclCommInitRank(&c, nranks, id, rank);
+    if (r != ncclSuccess) return fail(nullptr, SW_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    *comm_out = (void*)c;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_comm_destroy(void* comm) {
+    if (!comm) return SW_OK;
+    ncclResult_t r = ncclCommDestroy((ncclComm_t)comm);
+    if (r != ncclSuccess) return fail(nullptr, SW_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+    return SW_OK;
+}
+
+// ============================================================================ diagnostics
+extern "C" const char* sw_status_str(sw_status s) {
+    switch (s) {
+        case SW_OK: return "SW_OK";
+        case SW_CLOSEST: return "SW_CLOSEST";
+        case SW_TRUNCATED: return "SW_TRUNCATED";
+        case SW_EMPTY: return "SW_EMPTY";
+        case SW_EINVAL: return "SW_EINVAL";
+        case SW_ERANGE: return "SW_ERANGE";
+        case SW_ENOMEM: return "SW_ENOMEM";
+        case SW_ECUDA: return "SW_ECUDA";
+        case SW_ENCCL: return "SW_ENCCL";
+        case SW_ESTATE: return "SW_ESTATE";
+        default: return "SW_UNKNOWN";
+    }
+}
+
+extern "C" const char* sw_last_error(const sw_plan* h) {
+    if (h && !h->err.empty()) return h->err.c_str();
+    return g_last_error.c_str();
+}
+
+extern "C" uint64_t sw_plan_launch_count(const sw_plan* h) { return h ? h->launches : 0; }
+
+extern "C" int32_t sw_abi_version(void) { return 1; }

@@ -5,14 +5,14 @@ from swgen.generator import Problem, Query, INF
 def make_problem(dur_us, llm_us, tts_us, gpus, price_mc, radix, first_scene, choices,
                  va_us, overhead_us=0, scene0_static=0, static_ready_us=0,
                  fixed_cost_mc=0, billing=0, objective=0, queries=None,
-                 level_score=(250, 500, 750, 1000), name="hand"):
+                 level_score=(250, 500, 750, 1000), name="hand", heads=40):
     S = len(dur_us)
     return Problem(
         name=name, S=S, dur_us=list(dur_us), llm_us=list(llm_us), tts_us=list(tts_us),
         overhead_us=overhead_us, scene0_static=scene0_static,
         static_ready_us=static_ready_us, pool_class=["X"] * len(gpus), gpus=list(gpus),
         price_mc=list(price_mc), fixed_cost_mc=fixed_cost_mc, billing=billing,
-        objective=objective, level_score=list(level_score), heads=40, radix=list(radix),
+        objective=objective, level_score=list(level_score), heads=heads, radix=list(radix),
         first_scene=list(first_scene), choices=[tuple(c) for c in choices],
         va_us=list(va_us), queries=queries or [Query(INF, INF, INF)])
 
@@ -53,7 +53,8 @@ def random_problem(rng, max_scenes=5, max_pools=3, max_g=8, max_choices=4,
     return make_problem(dur, llm, tts, gpus, price, radix, first, choices, va,
                         overhead_us=0 if zero_fixed else rng.randint(0, 2_000_000),
                         fixed_cost_mc=rng.randint(0, 5000),
-                        billing=rng.randrange(2), objective=rng.randrange(2))
+                        billing=rng.randrange(2), objective=rng.randrange(2),
+                        heads=0)  # 0 = no head-divisibility check: exercise any k
 
 
 def encode(radix, digits):

@@ -370,46 +370,6 @@ __device__ __forceinline__ void block_reduce_cand(const QueryDev& q, uint32_t ob
     }
 }
 
-// Grid-stride scan of one record segment for up to 8 queries at once: one 32 B load
-// per candidate feeds every query (HBM read-bound).  Writes per-block bests.
-__global__ void __launch_bounds__(kScanThreads) select_scan_kernel(
-    const Rec4* __restrict__ recs, uint64_t n, uint64_t first_index, SelParams P,
-    Cand* __restrict__ partial /* [gridDim.x][SW_MAX_QUERIES] */) {
-    __shared__ Cand s_tmp[32];
-    uint64_t bi[SW_MAX_QUERIES];
-    Rec4 br[SW_MAX_QUERIES];
-#pragma unroll
-    for (int q = 0; q < SW_MAX_QUERIES; q++) bi[q] = kInf64;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const Rec4 r = ld_global_nc_256(recs + i);
-        const uint64_t idx = first_index + i;
-#pragma unroll
-        for (int q = 0; q < SW_MAX_QUERIES; q++) {
-            if ((uint32_t)q < P.nq && cand_better(P.q[q], P.objective, idx, r, bi[q], br[q])) {
-                bi[q] = idx;
-                br[q] = r;
-            }
-        }
-    }
-#pragma unroll 1
-    for (uint32_t q = 0; q < P.nq; q++) {
-        uint64_t idx = bi[0];
-        Rec4 r = br[0];
-#pragma unroll
-        for (int j = 1; j < SW_MAX_QUERIES; j++)
-            if ((uint32_t)j == q) {
-                idx = bi[j];
-                r = br[j];
-            }
-        block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
-        if (threadIdx.x == 0) {
-            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].idx = idx;
-            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].r = r;
-        }
-    }
-}
-
 // Reduce n_partial candidates per query (strided by SW_MAX_QUERIES) -> out[q].
 // Used after the scan (per-block partials) and for the cross-rank merge (a10).
 __global__ void __launch_bounds__(kScanThreads) select_final_kernel(
@@ -475,10 +435,23 @@ __device__ __forceinline__ bool pdom(const PPoint& y, uint32_t py, const PPoint&
     return py < px;
 }
 
+// Device-side sizes of the Pareto merge pipeline: every kernel below reads its input
+// count from here, so a whole merge runs without a host round trip.
+struct ParetoCtl {
+    unsigned long long surv;  // survivors appended by the current filter pass
+    uint32_t m_in, m_loc, m_loc2, m_cmp;
+    uint64_t front_n;         // size of the running front (d_front)
+    uint32_t surv_overflow;   // a filter pass had more survivors than capacity
+    uint32_t front_overflow;  // the front exceeded its capacity
+};
+
 // keep[x] = no other point of pts[0,m) dominates x.  O(m^2), tiles through smem.
 __global__ void __launch_bounds__(kScanThreads) pareto_mark_kernel(const PPoint* __restrict__ pts,
-                                                                   uint32_t m, uint8_t* __restrict__ keep) {
+                                                                   const uint32_t* __restrict__ d_m,
+                                                                   uint8_t* __restrict__ keep) {
     __shared__ PPoint tile[kScanThreads];
+    const uint32_t m = *d_m;
+    if (blockIdx.x * blockDim.x >= m) return;
     const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
     PPoint px{};
     if (x < m) px = pts[x];
@@ -500,11 +473,11 @@ __global__ void __launch_bounds__(kScanThreads) pareto_mark_kernel(const PPoint*
     if (x < m) keep[x] = dom ? 0 : 1;
 }
 
-__global__ void pareto_compact_kernel(const PPoint* __restrict__ pts, uint32_t m,
+__global__ void pareto_compact_kernel(const PPoint* __restrict__ pts, const uint32_t* __restrict__ d_m,
                                       const uint8_t* __restrict__ keep, PPoint* __restrict__ out,
-                                      unsigned int* __restrict__ count) {
+                                      uint32_t* __restrict__ count) {
     const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-    if (x < m && keep[x]) out[atomicAdd(count, 1u)] = pts[x];
+    if (x < *d_m && keep[x]) out[atomicAdd(count, 1u)] = pts[x];
 }
 
 __device__ __forceinline__ bool pkey_less(const PPoint& a, const PPoint& b) {
@@ -516,9 +489,18 @@ __device__ __forceinline__ bool pkey_less(const PPoint& a, const PPoint& b) {
 
 // out[rank(x)] = x with rank = #{y : key(y) < key(x)}: deterministic ordering of a
 // front (indices are unique) by (ttff_eff asc, cost asc, quality desc, index asc).
+// Publishes the new front size; flags an overflow of the front capacity.
 __global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint* __restrict__ pts,
-                                                                   uint32_t m, PPoint* __restrict__ out) {
+                                                                   const uint32_t* __restrict__ d_m,
+                                                                   PPoint* __restrict__ out, ParetoCtl* ctl,
+                                                                   uint64_t cap) {
     __shared__ PPoint tile[kScanThreads];
+    const uint32_t m = *d_m;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->front_n = m <= cap ? m : 0;
+        if (m > cap) ctl->front_overflow = 1;
+    }
+    if (m > cap || blockIdx.x * blockDim.x >= m) return;
     const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
     PPoint px{};
     if (x < m) px = pts[x];
@@ -544,9 +526,10 @@ struct Dlt {
     uint64_t cell[kDltT * kDltQ];
 };
 
-__global__ void __launch_bounds__(1024) dlt_build_kernel(const PPoint* __restrict__ front, uint32_t m,
-                                                         Dlt* __restrict__ d) {
+__global__ void __launch_bounds__(1024) dlt_build_kernel(const PPoint* __restrict__ front,
+                                                         const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
     __shared__ uint32_t qmin_s, qmax_s;
+    const uint32_t m = (uint32_t)ctl->front_n;
     if (threadIdx.x == 0) {
         qmin_s = 0xffffffffu;
         qmax_s = 0;
@@ -574,93 +557,26 @@ __global__ void __launch_bounds__(1024) dlt_build_kernel(const PPoint* __restric
     }
 }
 
-// Filter one record segment: (1) the DLT prefilter (O(1) per record), then (2) for
-// DLT survivors an exact warp-cooperative dominance test against up to m_sm front
-// points held in shared memory (32 front points per step, __any_sync early exit).
-// Records dominated by a real candidate cannot be on the front, so the surviving set
-// always contains every true front point of the segment: the merge stays exact for
-// any front subset used here.  Survivors are appended at work[base + slot].
-constexpr uint32_t kFrontSmem = 1024;
-
-__global__ void __launch_bounds__(kScanThreads) pareto_filter_kernel(
-    const Rec4* __restrict__ recs, uint64_t n, uint64_t first_index, const Dlt* __restrict__ g_dlt,
-    const PPoint* __restrict__ front, uint32_t m_sm, PPoint* __restrict__ work, uint64_t base,
-    unsigned long long* __restrict__ counter, uint64_t cap) {
-    extern __shared__ __align__(16) unsigned char fsm[];
-    Dlt& d = *reinterpret_cast<Dlt*>(fsm);
-    PPoint* fs = reinterpret_cast<PPoint*>(fsm + sizeof(Dlt));
-    for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x) d.tedge[i] = g_dlt->tedge[i];
-    for (uint32_t i = threadIdx.x; i < kDltQ; i += blockDim.x) d.qedge[i] = g_dlt->qedge[i];
-    for (uint32_t i = threadIdx.x; i < kDltT * kDltQ; i += blockDim.x) d.cell[i] = g_dlt->cell[i];
-    for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = front[i];
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-        const uint64_t i = i0 + threadIdx.x;
-        bool keep = false;
-        PPoint pt{};
-        if (i < n) {
-            const Rec4 r = ld_global_nc_256(recs + i);
-            pt.idx = first_index + i;
-            pt.t = r.w0 + r.w1;
-            pt.c = r.w2;
-            pt.q = rec_Q(r);
-            int lo = 0, hi = kDltT;  // bt = (#edges <= t) - 1
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (d.tedge[mid] <= pt.t) lo = mid + 1;
-                else hi = mid;
-            }
-            const int bt = lo - 1;
-            int lo2 = 0, hi2 = kDltQ;  // bq = min{j : qedge[j] >= q}
-            while (lo2 < hi2) {
-                const int mid = (lo2 + hi2) >> 1;
-                if (d.qedge[mid] >= pt.q) hi2 = mid;
-                else lo2 = mid + 1;
-            }
-            const int bq = lo2;
-            keep = (bt < 0 || bq >= kDltQ) ? true : !(d.cell[bt * kDltQ + bq] < pt.c);
-        }
-        unsigned pend = __ballot_sync(0xffffffffu, keep);
-        while (pend) {  // exact test of each DLT survivor by the whole warp
-            const int src = __ffs(pend) - 1;
-            pend &= pend - 1;
-            PPoint x;
-            x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
-            x.t = __shfl_sync(0xffffffffu, pt.t, src);
-            x.c = __shfl_sync(0xffffffffu, pt.c, src);
-            x.q = __shfl_sync(0xffffffffu, pt.q, src);
-            bool dom = false;
-            for (uint32_t j0 = 0; j0 < m_sm; j0 += 32) {
-                const uint32_t j = j0 + lane;
-                // an identical entry (same index) also removes x: it is already kept
-                const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
-                if (__any_sync(0xffffffffu, dj)) {
-                    dom = true;
-                    break;
-                }
-            }
-            if (lane == src && dom) keep = false;
-        }
-        const unsigned mask = __ballot_sync(0xffffffffu, keep);
-        if (mask) {
-            const int leader = __ffs(mask) - 1;
-            unsigned long long slot0 = 0;
-            if (lane == leader) slot0 = atomicAdd(counter, (unsigned long long)__popc(mask));
-            slot0 = __shfl_sync(0xffffffffu, slot0, leader);
-            if (keep) {
-                const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-                if (slot < cap) work[base + slot] = pt;
-            }
-        }
+// work = front[0, front_n) ++ surv[0, min(surv, cap)); m_in = its size.
+__global__ void pareto_append_kernel(const PPoint* __restrict__ front, const PPoint* __restrict__ surv,
+                                     uint64_t cap, PPoint* __restrict__ work, ParetoCtl* ctl) {
+    const uint64_t fn = ctl->front_n;
+    const unsigned long long sv = ctl->surv;
+    const uint64_t ns = sv < cap ? sv : cap;
+    const uint64_t tot = fn + ns;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (uint64_t)gridDim.x * blockDim.x)
+        work[x] = x < fn ? front[x] : surv[x - fn];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->m_in = (uint32_t)tot;
+        if (sv > cap) ctl->surv_overflow = 1;
     }
 }
 
 // Strided sample of a record segment -> points (seed for the first DLT).
 __global__ void pareto_sample_kernel(const Rec4* __restrict__ recs, uint64_t n, uint64_t first_index,
-                                     uint32_t ns, PPoint* __restrict__ out) {
+                                     uint32_t ns, PPoint* __restrict__ out, ParetoCtl* ctl) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j == 0) ctl->m_in = ns;
     if (j >= ns) return;
     const uint64_t i = (uint64_t)((unsigned __int128)j * n / ns);
     const Rec4 r = ld_global_nc_256(recs + i);
@@ -682,6 +598,188 @@ __global__ void pareto_gather_kernel(const PPoint* __restrict__ padded, const ui
     uint64_t off = 0;
     for (uint64_t q = 0; q < r; q++) off += counts[q];
     out[off + j] = padded[x];
+}
+
+
+// Block-local front: each CTA reduces a chunk of kLocal points in shared memory and
+// appends its non-dominated points.  front(A u B) = front(front(A) u front(B)), so a
+// global mark over the (much smaller) union stays exact.
+constexpr int kLocal = 1024;
+__global__ void __launch_bounds__(kLocal) pareto_local_kernel(const PPoint* __restrict__ pts,
+                                                              const uint32_t* __restrict__ d_m,
+                                                              PPoint* __restrict__ out,
+                                                              uint32_t* __restrict__ count) {
+    __shared__ PPoint sp[kLocal];
+    const uint32_t m = *d_m;
+    const uint32_t base = blockIdx.x * kLocal;
+    if (base >= m) return;
+    const uint32_t cnt = min((uint32_t)kLocal, m - base);
+    if (threadIdx.x < cnt) sp[threadIdx.x] = pts[base + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x >= cnt) return;
+    const PPoint p = sp[threadIdx.x];
+    for (uint32_t j = 0; j < cnt; j++)
+        if (j != threadIdx.x && pdom(sp[j], base + j, p, base + threadIdx.x)) return;
+    out[atomicAdd(count, 1u)] = p;
+}
+
+// ============================================================================ fused scan
+// One pass over a record segment serves (a9) up to NQ select queries and, when PARETO,
+// (a8) the front filter: (1) the DLT prefilter, O(1) per record; (2) for DLT survivors
+// an exact warp-cooperative dominance test against up to m_sm front points held in
+// shared memory (32 per step, __any_sync early exit).  A record dominated by a real
+// candidate cannot be on the front, so the survivors always contain every true front
+// point of the segment whatever front subset is used: the later merge stays exact.
+constexpr uint32_t kFrontSmem = 1024;
+
+struct ParetoArgs {
+    const Dlt* dlt;
+    const PPoint* front;
+    ParetoCtl* ctl;  // front_n (read) and the survivor counter (atomics)
+    PPoint* surv;
+    uint64_t cap;
+};
+
+// objective keys only (ties keep the earlier = lower index within a thread's scan)
+__device__ __forceinline__ bool obj_strict_better(uint32_t obj, const Rec4& a, const Rec4& b) {
+    const uint32_t qa = rec_Q(a), qb = rec_Q(b);
+    if (obj == 0) {
+        if (qa != qb) return qa > qb;
+        if (a.w2 != b.w2) return a.w2 < b.w2;
+        return a.w0 + a.w1 < b.w0 + b.w1;
+    }
+    const uint64_t ta = a.w0 + a.w1, tb = b.w0 + b.w1;
+    const uint64_t hi_a = __umul64hi(a.w2, ta), hi_b = __umul64hi(b.w2, tb);
+    if (hi_a != hi_b) return hi_a < hi_b;
+    const uint64_t lo_a = a.w2 * ta, lo_b = b.w2 * tb;
+    if (lo_a != lo_b) return lo_a < lo_b;
+    return qa > qb;
+}
+
+__device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_t obj, const Rec4& a,
+                                                      const Rec4& b) {
+    const uint64_t vta = sat_sub(a.w0, q.slo_t) + sat_sub(a.w1, q.slo_s);
+    const uint64_t vtb = sat_sub(b.w0, q.slo_t) + sat_sub(b.w1, q.slo_s);
+    if (vta != vtb) return vta < vtb;
+    const uint64_t vca = sat_sub(a.w2, q.budget), vcb = sat_sub(b.w2, q.budget);
+    if (vca != vcb) return vca < vcb;
+    return obj_strict_better(obj, a, b);
+}
+
+template <int NQ, bool PARETO>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(const Rec4* __restrict__ recs, uint64_t n,
+                                                            uint64_t first_index, SelParams P,
+                                                            Cand* __restrict__ partial, ParetoArgs pa) {
+    constexpr int NQA = NQ > 0 ? NQ : 1;
+    extern __shared__ __align__(16) unsigned char fsm[];
+    __shared__ Cand s_tmp[32];
+    Dlt& d = *reinterpret_cast<Dlt*>(fsm);
+    PPoint* fs = reinterpret_cast<PPoint*>(fsm + sizeof(Dlt));
+    uint32_t m_sm = 0;
+    if (PARETO) {
+        m_sm = (uint32_t)umin64(pa.ctl->front_n, kFrontSmem);
+        for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x) d.tedge[i] = pa.dlt->tedge[i];
+        for (uint32_t i = threadIdx.x; i < kDltQ; i += blockDim.x) d.qedge[i] = pa.dlt->qedge[i];
+        for (uint32_t i = threadIdx.x; i < kDltT * kDltQ; i += blockDim.x) d.cell[i] = pa.dlt->cell[i];
+        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = pa.front[i];
+        __syncthreads();
+    }
+    uint64_t fi[NQA], ci[NQA];
+    Rec4 fr[NQA], cr[NQA];
+#pragma unroll
+    for (int q = 0; q < NQA; q++) fi[q] = ci[q] = kInf64;
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + threadIdx.x;
+        const bool valid = i < n;
+        Rec4 r{};
+        if (valid) r = ld_global_nc_256(recs + i);
+        const uint64_t idx = first_index + i;
+        if (valid) {
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                if (feasible(P.q[q], r)) {
+                    if (fi[q] == kInf64 || obj_strict_better(P.objective, r, fr[q])) {
+                        fi[q] = idx;
+                        fr[q] = r;
+                    }
+                } else if (fi[q] == kInf64) {
+                    if (ci[q] == kInf64 || closest_strict_better(P.q[q], P.objective, r, cr[q])) {
+                        ci[q] = idx;
+                        cr[q] = r;
+                    }
+                }
+            }
+        }
+        if (PARETO) {
+            bool keep = false;
+            PPoint pt{};
+            if (valid) {
+                pt.idx = idx;
+                pt.t = r.w0 + r.w1;
+                pt.c = r.w2;
+                pt.q = rec_Q(r);
+                int lo = 0, hi = kDltT;  // bt = (#edges <= t) - 1
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (d.tedge[mid] <= pt.t) lo = mid + 1;
+                    else hi = mid;
+                }
+                const int bt = lo - 1;
+                int lo2 = 0, hi2 = kDltQ;  // bq = min{j : qedge[j] >= q}
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2) >> 1;
+                    if (d.qedge[mid] >= pt.q) hi2 = mid;
+                    else lo2 = mid + 1;
+                }
+                const int bq = lo2;
+                keep = (bt < 0 || bq >= kDltQ) ? true : !(d.cell[bt * kDltQ + bq] < pt.c);
+            }
+            unsigned pend = __ballot_sync(0xffffffffu, keep);
+            while (pend) {  // exact test of each DLT survivor by the whole warp
+                const int src = __ffs(pend) - 1;
+                pend &= pend - 1;
+                PPoint x;
+                x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
+                x.t = __shfl_sync(0xffffffffu, pt.t, src);
+                x.c = __shfl_sync(0xffffffffu, pt.c, src);
+                x.q = __shfl_sync(0xffffffffu, pt.q, src);
+                bool dom = false;
+                for (uint32_t j0 = 0; j0 < m_sm; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    // an identical entry (same index) also removes x: it is already kept
+                    const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
+                    if (__any_sync(0xffffffffu, dj)) {
+                        dom = true;
+                        break;
+                    }
+                }
+                if (lane == src && dom) keep = false;
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+            if (mask) {
+                const int leader = __ffs(mask) - 1;
+                unsigned long long slot0 = 0;
+                if (lane == leader) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
+                slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+                if (keep) {
+                    const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+                    if (slot < pa.cap) pa.surv[slot] = pt;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; q++) {
+        uint64_t idx = fi[q] != kInf64 ? fi[q] : ci[q];
+        Rec4 r = fi[q] != kInf64 ? fr[q] : cr[q];
+        block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
+        if (threadIdx.x == 0) {
+            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].idx = idx;
+            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].r = r;
+        }
+    }
 }
 
 }  // namespace sw

@@ -67,10 +67,14 @@ struct sw_plan {
     PPoint* d_work = nullptr;  // front_cap + surv_cap
     PPoint* d_tmp = nullptr;   // front_cap + surv_cap
     uint8_t* d_keep = nullptr;
-    unsigned long long* d_counter = nullptr;
-    unsigned int* d_ucount = nullptr;
+    ParetoCtl* d_ctl = nullptr;
     Dlt* d_dlt = nullptr;
     PPoint* d_gather = nullptr;  // multi-rank padded fronts
+    PPoint* d_tmp2 = nullptr;    // front_cap + surv_cap (block-local fronts)
+    PPoint* d_surv = nullptr;    // surv_cap survivors of filter passes
+    bool fuse_pareto = true;     // fold unfolded segments inside select scans
+    uint64_t chunk = 1ull << 25; // records per fold chunk (the front improves per chunk)
+    uint64_t fold_passes = 0;    // diagnostics: filter passes run
     uint64_t* d_counts = nullptr;
 
     // select / detail / digest
@@ -167,6 +171,7 @@ using u128 = unsigned __int128;
 }  // namespace
 
 static sw_status fold_pending(sw_plan* h);
+static cudaError_t set_scan_smem_attrs();
 
 // ============================================================================ create
 extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_list* sc,
@@ -433,10 +438,9 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         h->eval_grid = occ * h->num_sms;
     }
     h->scan_grid = (uint32_t)h->num_sms * 4;
-    if (cudaFuncSetAttribute(pareto_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(Dlt) + kFrontSmem * sizeof(PPoint))) != cudaSuccess) {
+    if (set_scan_smem_attrs() != cudaSuccess) {
         cudaGetLastError();
-        return bail(fail(nullptr, SW_ECUDA, "filter kernel smem attribute failed"));
+        return bail(fail(nullptr, SW_ECUDA, "scan kernel smem attribute failed"));
     }
 
     // ---- record buffer + reduction scratch
@@ -449,8 +453,9 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if ((st = alloc_n(h, &h->d_work, h->front_cap + h->surv_cap, "pareto work")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_tmp, h->front_cap + h->surv_cap, "pareto tmp")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_keep, h->front_cap + h->surv_cap, "pareto flags")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_counter, 2, "counter")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_ucount, 2, "counter")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_tmp2, h->front_cap + h->surv_cap, "pareto tmp2")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_surv, h->surv_cap, "pareto survivors")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_ctl, 1, "pareto ctl")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_dlt, 1, "dlt")) < 0) return bail(st);
     h->max_partial = h->scan_grid * 64;  // up to 64 segments per select
     if ((st = alloc_n(h, &h->d_partial, (uint64_t)h->max_partial * SW_MAX_QUERIES, "partials")) < 0) return bail(st);
@@ -461,6 +466,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 1, "counts")) < 0) return bail(st);
     if (h->nranks > 1)
         if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return bail(st);
+    if (cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream) != cudaSuccess)
+        return bail(fail(nullptr, SW_ECUDA, "ctl init failed"));
     if (cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
         return bail(fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
@@ -476,9 +483,9 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
     if (h->stream) {
         cudaSetDevice(h->device);
         void* bufs[] = {h->d_hdr,   h->d_va,      h->d_rec,     h->d_front, h->d_work,
-                        h->d_tmp,   h->d_keep,    h->d_counter, h->d_ucount, h->d_dlt,
+                        h->d_tmp,   h->d_keep,    h->d_ctl,     h->d_dlt,
                         h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest,
-                        h->d_counts, h->d_gather};
+                        h->d_counts, h->d_gather, h->d_tmp2, h->d_surv};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
         if (h->ev0) cudaEventDestroy(h->ev0);
@@ -495,6 +502,8 @@ extern "C" sw_status sw_plan_reset(sw_plan* h) {
     h->segs.clear();
     h->rec_used = 0;
     h->front_n = 0;
+    CK(h, cudaSetDevice(h->device));
+    CK(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream));
     return SW_OK;
 }
 
@@ -614,6 +623,127 @@ static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint
     return SW_OK;
 }
 
+template <int NQ, bool PARETO>
+static void launch_scan(uint32_t grid, size_t smem, cudaStream_t st, const Rec4* recs, uint64_t n,
+                        uint64_t first, const SelParams& P, Cand* partial, const ParetoArgs& pa) {
+    scan_kernel<NQ, PARETO><<<grid, kScanThreads, smem, st>>>(recs, n, first, P, partial, pa);
+}
+
+template <bool PARETO>
+static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t st, const Rec4* recs,
+                           uint64_t n, uint64_t first, const SelParams& P, Cand* partial, const ParetoArgs& pa) {
+    switch (nq) {
+        case 0: launch_scan<0, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 1: launch_scan<1, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 2: launch_scan<2, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 3: launch_scan<3, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 4: launch_scan<4, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 5: launch_scan<5, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 6: launch_scan<6, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 7: launch_scan<7, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        default: launch_scan<8, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+    }
+}
+
+template <int NQ>
+static cudaError_t set_attr_one() {
+    return cudaFuncSetAttribute(scan_kernel<NQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(Dlt) + kFrontSmem * sizeof(PPoint)));
+}
+
+static cudaError_t set_scan_smem_attrs() {
+    cudaError_t e = cudaSuccess;
+    cudaError_t r[] = {set_attr_one<0>(), set_attr_one<1>(), set_attr_one<2>(), set_attr_one<3>(), set_attr_one<4>(),
+                       set_attr_one<5>(), set_attr_one<6>(), set_attr_one<7>(), set_attr_one<8>()};
+    for (cudaError_t x : r)
+        if (x != cudaSuccess) e = x;
+    return e;
+}
+
+static ParetoArgs pareto_args(sw_plan* h) {
+    ParetoArgs pa;
+    pa.dlt = h->d_dlt;
+    pa.front = h->d_front;
+    pa.ctl = h->d_ctl;
+    pa.surv = h->d_surv;
+    pa.cap = h->surv_cap;
+    return pa;
+}
+
+// ---- the device-sized merge pipeline: work[0, ctl.m_in) -> exact front in `out`
+// (two block-local passes in smem, a global O(m'^2) mark, compaction, rank sort).
+// Grids are sized for the capacity; blocks beyond the live count exit at once.
+static sw_status reduce_async(sw_plan* h, PPoint* out) {
+    const uint64_t U = h->front_cap + h->surv_cap;
+    ParetoCtl* c = h->d_ctl;
+    const uint32_t gl = (uint32_t)((U + kLocal - 1) / kLocal), gs = (uint32_t)((U + kScanThreads - 1) / kScanThreads);
+    CK(h, cudaMemsetAsync(&c->m_loc, 0, 3 * sizeof(uint32_t), h->stream));  // m_loc, m_loc2, m_cmp
+    pareto_local_kernel<<<gl, kLocal, 0, h->stream>>>(h->d_work, &c->m_in, h->d_tmp2, &c->m_loc);
+    CKL(h);
+    pareto_local_kernel<<<gl, kLocal, 0, h->stream>>>(h->d_tmp2, &c->m_loc, h->d_tmp, &c->m_loc2);
+    CKL(h);
+    pareto_mark_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_tmp, &c->m_loc2, h->d_keep);
+    CKL(h);
+    pareto_compact_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_tmp, &c->m_loc2, h->d_keep, h->d_work, &c->m_cmp);
+    CKL(h);
+    pareto_rank_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_work, &c->m_cmp, out, c, h->front_cap);
+    CKL(h);
+    return SW_OK;
+}
+
+// Seed the running front from a strided sample of a segment (async).
+static sw_status seed_async(sw_plan* h, const Segment& g) {
+    const uint64_t n = g.end - g.begin;
+    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, h->front_cap + h->surv_cap);
+    pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(h->d_rec + g.offset, n, g.begin, ns, h->d_work,
+                                                                  h->d_ctl);
+    CKL(h);
+    return reduce_async(h, h->d_front);
+}
+
+// Fold a segment chunk by chunk: DLT from the current front, one filter pass over the
+// chunk (fused with nq select queries when nq > 0), survivors merged on the device.
+static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
+    const uint64_t n = g.end - g.begin;
+    const size_t psmem = sizeof(Dlt) + kFrontSmem * sizeof(PPoint);
+    for (uint64_t c0 = 0; c0 < n; c0 += h->chunk) {
+        const uint64_t cn = std::min(h->chunk, n - c0);
+        dlt_build_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+        CKL(h);
+        CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((cn + kScanThreads - 1) / kScanThreads, h->scan_grid);
+        Cand* part = h->d_partial;
+        if (nq) {
+            if (*np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many chunks for one select");
+            part = h->d_partial + (uint64_t)*np * SW_MAX_QUERIES;
+            *np += grid;
+        }
+        launch_scan_nq<true>(nq, grid, psmem, h->stream, h->d_rec + g.offset + c0, cn, g.begin + c0, P, part,
+                             pareto_args(h));
+        CKL(h);
+        pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
+                                                               h->d_ctl);
+        CKL(h);
+        sw_status st = reduce_async(h, h->d_front);
+        if (st < 0) return st;
+        h->fold_passes++;
+    }
+    return SW_OK;
+}
+
+// Read back the pipeline state (sync).  Returns SW_ERANGE on a front overflow; sets
+// *overflow if some filter pass had more survivors than capacity (refold needed).
+static sw_status sync_ctl(sw_plan* h, bool* overflow) {
+    ParetoCtl c;
+    CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (c.front_overflow) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
+    h->front_n = c.front_n;
+    *overflow = c.surv_overflow != 0;
+    if (c.surv_overflow) CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
+    return SW_OK;
+}
+
 extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
     if (!h || !qs || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (nq < 1 || nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u not in 1..%d", nq, SW_MAX_QUERIES);
@@ -623,15 +753,30 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
     P.objective = (h->h.flags & 4u) ? 1u : 0u;
     for (uint32_t q = 0; q < nq; q++) P.q[q] = QueryDev{qs[q].slo_startup_us, qs[q].slo_stall_us, qs[q].budget_mc};
     uint32_t np = 0;
-    for (const Segment& g : h->segs) {
+    std::vector<size_t> fused;
+    bool seeded = h->front_n > 0;
+    for (size_t si = 0; si < h->segs.size(); si++) {
+        Segment& g = h->segs[si];
         const uint64_t n = g.end - g.begin;
         if (n == 0) continue;
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
-        if (np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many segments for one select");
-        select_scan_kernel<<<grid, kScanThreads, 0, h->stream>>>(h->d_rec + g.offset, n, g.begin, P,
-                                                                 h->d_partial + (uint64_t)np * SW_MAX_QUERIES);
-        CKL(h);
-        np += grid;
+        if (h->fuse_pareto && !g.folded) {  // a8 rides on the same 32 B loads as a9
+            if (!seeded) {
+                sw_status st = seed_async(h, g);
+                if (st < 0) return st;
+                seeded = true;
+            }
+            sw_status st = fold_chunks_async(h, g, nq, P, &np);
+            if (st < 0) return st;
+            g.folded = true;
+            fused.push_back(si);
+        } else {
+            const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
+            if (np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many segments for one select");
+            launch_scan_nq<false>(nq, grid, 0, h->stream, h->d_rec + g.offset, n, g.begin, P,
+                                  h->d_partial + (uint64_t)np * SW_MAX_QUERIES, pareto_args(h));
+            CKL(h);
+            np += grid;
+        }
     }
     if (np == 0) {
         // empty local contribution: a row of "none" candidates
@@ -651,7 +796,15 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
     }
     Cand win[SW_MAX_QUERIES];
     CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nq, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    if (!fused.empty()) {
+        bool overflow = false;
+        sw_status st = sync_ctl(h, &overflow);
+        if (st < 0) return st;
+        if (overflow)  // the front is valid but incomplete: refold these segments later
+            for (size_t si : fused) h->segs[si].folded = false;
+    } else {
+        CK(h, cudaStreamSynchronize(h->stream));
+    }
     sw_status worst = SW_OK;
     for (uint32_t q = 0; q < nq; q++) {
         memset(&out[q], 0, sizeof(sw_selection));
@@ -707,63 +860,20 @@ extern "C" sw_status sw_plan_digest(sw_plan* h, uint64_t* digest) {
 }
 
 // ============================================================================ Pareto
-// Exact front of pts[0, m) -> d_front (sorted), m <= front_cap + surv_cap.
-static sw_status exact_front(sw_plan* h, PPoint* pts, uint64_t m) {
-    if (m == 0) {
-        h->front_n = 0;
-        return SW_OK;
-    }
-    const uint32_t g = (uint32_t)((m + kScanThreads - 1) / kScanThreads);
-    pareto_mark_kernel<<<g, kScanThreads, 0, h->stream>>>(pts, (uint32_t)m, h->d_keep);
-    CKL(h);
-    CK(h, cudaMemsetAsync(h->d_ucount, 0, sizeof(unsigned int), h->stream));
-    PPoint* comp = (pts == h->d_tmp) ? h->d_work : h->d_tmp;
-    pareto_compact_kernel<<<g, kScanThreads, 0, h->stream>>>(pts, (uint32_t)m, h->d_keep, comp, h->d_ucount);
-    CKL(h);
-    unsigned int cnt = 0;
-    CK(h, cudaMemcpyAsync(&cnt, h->d_ucount, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
-    if (cnt > h->front_cap) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
-    const uint32_t g2 = (cnt + kScanThreads - 1) / kScanThreads;
-    if (cnt) {
-        pareto_rank_kernel<<<g2, kScanThreads, 0, h->stream>>>(comp, cnt, h->d_front);
-        CKL(h);
-    }
-    h->front_n = cnt;
-    return SW_OK;
-}
-
 static sw_status fold_segment(sw_plan* h, const Segment& g) {
-    const uint64_t n = g.end - g.begin;
-    if (n == 0) return SW_OK;
-    const Rec4* recs = h->d_rec + g.offset;
-    if (h->front_n == 0) {  // seed from a strided sample of this segment
-        const uint32_t ns = (uint32_t)std::min<uint64_t>(n, 65536);
-        pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(recs, n, g.begin, ns, h->d_work);
-        CKL(h);
-        sw_status st = exact_front(h, h->d_work, ns);
+    if (g.end == g.begin) return SW_OK;
+    SelParams P{};
+    for (int pass = 0; pass < 16; pass++) {
+        if (h->front_n == 0) {
+            sw_status st = seed_async(h, g);
+            if (st < 0) return st;
+        }
+        sw_status st = fold_chunks_async(h, g, 0, P, nullptr);
         if (st < 0) return st;
-    }
-    for (int iter = 0; iter < 64; iter++) {
-        const uint64_t m = h->front_n;
-        dlt_build_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, (uint32_t)m, h->d_dlt);
-        CKL(h);
-        CK(h, cudaMemcpyAsync(h->d_work, h->d_front, m * sizeof(PPoint), cudaMemcpyDeviceToDevice, h->stream));
-        CK(h, cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned long long), h->stream));
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
-        // exact-check subset: the first kFrontSmem front points (sorted by ttff_eff)
-        const uint32_t m_sm = (uint32_t)std::min<uint64_t>(m, kFrontSmem);
-        const size_t smem = sizeof(Dlt) + (size_t)m_sm * sizeof(PPoint);
-        pareto_filter_kernel<<<grid, kScanThreads, smem, h->stream>>>(recs, n, g.begin, h->d_dlt, h->d_front, m_sm,
-                                                                      h->d_work, m, h->d_counter, h->surv_cap);
-        CKL(h);
-        unsigned long long surv = 0;
-        CK(h, cudaMemcpyAsync(&surv, h->d_counter, sizeof surv, cudaMemcpyDeviceToHost, h->stream));
-        CK(h, cudaStreamSynchronize(h->stream));
-        const uint64_t used = std::min<uint64_t>(surv, h->surv_cap);
-        sw_status st = exact_front(h, h->d_work, m + used);
+        bool overflow = false;
+        st = sync_ctl(h, &overflow);
         if (st < 0) return st;
-        if (surv <= h->surv_cap) return SW_OK;
+        if (!overflow) return SW_OK;
         // survivors overflowed: the merged front is a better filter -> refilter
     }
     return fail(h, SW_ERANGE, "Pareto filter did not converge");
@@ -798,22 +908,25 @@ extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t ca
             maxc = std::max(maxc, c);
             tot += c;
         }
-        CKN(h, ncclAllGather(h->d_front, h->d_gather, maxc * sizeof(PPoint), ncclUint8, h->comm, h->stream));
         if (tot > h->front_cap + h->surv_cap) return fail(h, SW_ERANGE, "merged fronts too large");
+        CKN(h, ncclAllGather(h->d_front, h->d_gather, maxc * sizeof(PPoint), ncclUint8, h->comm, h->stream));
         const uint64_t all = maxc * (uint64_t)h->nranks;
         pareto_gather_kernel<<<(uint32_t)((all + 255) / 256), 256, 0, h->stream>>>(h->d_gather, h->d_counts,
-                                                                                  h->nranks, maxc, h->d_tmp);
+                                                                                  h->nranks, maxc, h->d_work);
         CKL(h);
-        // merge into a scratch front (keep the local running front intact)
-        PPoint* saved = h->d_front;
-        uint64_t saved_n = h->front_n;
-        h->d_front = h->d_gather;  // reuse gather buffer as output (>= front_cap)
-        st = exact_front(h, h->d_tmp, tot);
-        res = h->d_front;
-        n = h->front_n;
-        h->d_front = saved;
-        h->front_n = saved_n;
+        uint32_t tot32 = (uint32_t)tot;
+        CK(h, cudaMemcpyAsync(&h->d_ctl->m_in, &tot32, sizeof tot32, cudaMemcpyHostToDevice, h->stream));
+        // merged front into the gather buffer; the local running front stays intact
+        st = reduce_async(h, h->d_gather);
         if (st < 0) return st;
+        bool overflow = false;
+        st = sync_ctl(h, &overflow);
+        if (st < 0) return st;
+        n = h->front_n;
+        res = h->d_gather;
+        h->front_n = mine;
+        CK(h, cudaMemcpyAsync(&h->d_ctl->front_n, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
     }
     *n_out = n;
     if (cap == 0) return SW_OK;

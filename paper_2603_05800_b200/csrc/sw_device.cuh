@@ -25,6 +25,18 @@ struct __align__(16) VaEntry {
     uint32_t pad;
 };
 
+// LSD table entry (32 B), stored in (pool, k)-group order: the last scene's stage time
+// and quality for choice dl, and X_t = G_p price_p t (RESERVED) or k price_p t (BUSY)
+// split as X_t = cq * 3.6e9 + cr, so a candidate's pool cost needs no multiply/divide:
+// floor((Y + X_t) / D) = qY + cq + (rY + cr >= D) for Y = qY * D + rY.
+struct __align__(16) LsdEntry {
+    uint64_t t_us;
+    uint32_t q;
+    uint32_t dl;
+    uint64_t cq;
+    uint64_t cr;
+};
+
 // Per-request constants, packed ON THE DEVICE by pack_kernel, staged into shared
 // memory by every eval CTA with one TMA bulk copy (cp.async.bulk + mbarrier).
 // Digits are left-padded with virtual radix-1 / empty-block digits so that
@@ -45,6 +57,14 @@ struct __align__(16) DevHeader {
     uint32_t voff[kMaxDigits];    // va offset of digit b
     uint32_t G[kMaxP];
     uint64_t price[kMaxP];
+    uint64_t Gprice[kMaxP];       // G_p * price_p (device-computed in pack_kernel)
+    // LSD choices grouped by (pool, k) so the inner loop has neither: group g covers
+    // lsd_dl[lsd_goff[g] .. lsd_goff[g+1]) with pool/k packed in lsd_pk[g] (p | k << 8)
+    uint32_t lsd_ngroups, pad1;
+    uint32_t lsd_goff[SW_MAX_CHOICES + 1];
+    uint32_t lsd_pk[SW_MAX_CHOICES];
+    uint32_t lsd_dl[SW_MAX_CHOICES];
+    LsdEntry lsd[SW_MAX_CHOICES];  // device-computed in pack_kernel
     uint64_t a[SW_MAX_SCENES];    // fixed-stage ready times (a2), device-computed
     uint64_t P[SW_MAX_SCENES];    // deadline offsets P_s = sum_{j<s} d_j
     uint32_t choice[kMaxChoiceTotal];  // level | k << 8 | pool << 16

@@ -13,6 +13,24 @@
 namespace sw {
 
 constexpr int kEvalThreads = 128;
+constexpr uint32_t kTileRows = 32;  // rows per record tile (= lanes per warp)
+
+// Tiled record layout: a segment's records live in tiles of 32 consecutive rows; within
+// a tile the record of (row tile*32 + lane, in-row offset j) is at j * 32 + lane.
+// Index of the record at position pos of a tile-aligned segment starting at tile t0:
+__device__ __forceinline__ uint64_t tiled_index(uint64_t t0, uint64_t row, uint64_t tile, uint32_t pos_in_tile) {
+    return ((t0 + tile) * kTileRows + (pos_in_tile & 31u)) * row + (pos_in_tile >> 5);
+}
+
+// A tile range of one segment's records, plus the global index range it owns
+// (records outside [ib, ie) -- tile padding -- are skipped by every scan).
+struct SegView {
+    const Rec4* recs;  // first record of tile t0
+    uint64_t t0;       // absolute index of the first tile
+    uint64_t ntiles;
+    uint64_t row;
+    uint64_t ib, ie;
+};
 constexpr int kScanThreads = 256;
 constexpr int kDltT = 64;  // dominance lookup table: ttff_eff bins
 constexpr int kDltQ = 64;  //                         quality bins
@@ -52,6 +70,8 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
             acc += raw.dur[s];
         }
     }
+    for (uint32_t p = threadIdx.x; p < hdr->NP; p += blockDim.x) hdr->Gprice[p] = (uint64_t)hdr->G[p] * hdr->price[p];
+    __syncthreads();
     for (uint32_t i = threadIdx.x; i < raw.n_va; i += blockDim.x) {
         const uint32_t s = raw.va_scene[i];
         const uint32_t lv = ch_level(hdr->choice[raw.va_choice[i]]);
@@ -61,11 +81,122 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
         e.pad = 0;
         va[i] = e;
     }
+    __syncthreads();
+    // LSD table in (pool, k)-group order (single-scene last block only)
+    const uint32_t bl = hdr->B - 1;
+    if (hdr->first[bl + 1] - hdr->first[bl] == 1) {
+        const bool busy = hdr->flags & 2u;
+        for (uint32_t j = threadIdx.x; j < hdr->radix[bl]; j += blockDim.x) {
+            const uint32_t dl = hdr->lsd_dl[j];
+            const uint32_t ch = hdr->choice[hdr->coff[bl] + dl];
+            const uint32_t p = ch_pool(ch), k = ch_k(ch);
+            const VaEntry v = va[hdr->voff[bl] + dl];
+            const uint64_t X = busy ? (uint64_t)k * v.t_us * hdr->price[p] : v.t_us * hdr->Gprice[p];
+            LsdEntry le;
+            le.t_us = v.t_us;
+            le.q = v.q;
+            le.dl = dl;
+            le.cq = X / kUsPerHour;
+            le.cr = X % kUsPerHour;
+            hdr->lsd[j] = le;
+        }
+    }
+}
+
+// ============================================================================ LSD fast path
+// The last digit's block is a single scene: only pool p of the chosen (p, k) changes,
+// so per candidate  e = max(a_s, F_p[k-1]) + t,  end_p' = max(end_p, e),
+// cost = sum_{q != p} cost_q + round((G_p price_p end_p' + 1.8e9) / 3.6e9)  (RESERVED)
+// or busy_p + k t (BUSY), the playback metrics of the new scene and one 32 B store.
+// Choices are visited grouped by (p, k) (create-time table), so max(a_s, F_p[k-1]),
+// the pool selection and the other pools' cost hoist out of the inner loop.
+template <int K, int NP>
+__device__ __forceinline__ uint64_t fk_of(const State<NP>& st, uint32_t p) {
+    uint64_t r = 0;
+#pragma unroll
+    for (int q = 0; q < NP; q++)
+        if ((uint32_t)q == p) r = st.F[q][K - 1];
+    return r;
+}
+
+template <int NP>
+__device__ __forceinline__ uint64_t fk_dyn(const State<NP>& st, uint32_t p, uint32_t k) {
+    switch (k) {
+        case 1: return fk_of<1, NP>(st, p);
+        case 2: return fk_of<2, NP>(st, p);
+        case 4: return fk_of<4, NP>(st, p);
+        case 8: return fk_of<8, NP>(st, p);
+        default: {
+            uint64_t r = 0;
+#pragma unroll
+            for (int q = 0; q < NP; q++)
+                if ((uint32_t)q == p) r = sel_dyn(st.F[q], k - 1);
+            return r;
+        }
+    }
+}
+
+template <int NP, bool BUSY>
+__device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2, Rec4* __restrict__ lane_out,
+                                         bool live) {
+    const uint32_t bl = h.B - 1;
+    const uint32_t s = h.first[bl];  // s >= 1 on this path
+    const uint64_t as = h.a[s];
+    const int64_t Ps = (int64_t)h.P[s];
+    uint64_t pc[NP];
+    uint64_t pcsum = h.fixed_cost;
+#pragma unroll
+    for (int q = 0; q < NP; q++) {
+        pc[q] = BUSY ? pool_cost(s2.busy[q], h.price[q]) : (s2.end[q] * h.Gprice[q] + kHalfHour) / kUsPerHour;
+        pcsum += pc[q];
+    }
+    const uint64_t R0 = s2.R0;
+    const int64_t M0 = s2.M;
+    const uint64_t w3base = (uint64_t)s2.Q | ((uint64_t)s2.cnt << 32) | ((uint64_t)s2.used << 48);
+    const uint32_t ng = h.lsd_ngroups;
+    for (uint32_t g = 0; g < ng; g++) {
+        const uint32_t pk = h.lsd_pk[g];
+        const uint32_t p = pk & 0xffu, k = pk >> 8;
+        uint64_t endp = 0, busyp = 0, pcp = 0, A = 0, price = 0;
+#pragma unroll
+        for (int q = 0; q < NP; q++)
+            if ((uint32_t)q == p) {
+                endp = s2.end[q];
+                busyp = s2.busy[q];
+                pcp = pc[q];
+                A = h.Gprice[q];
+                price = h.price[q];
+            }
+        const uint64_t st0 = umax64(as, fk_dyn<NP>(s2, p, k));
+        const uint64_t base = pcsum - pcp;
+        // Y = (prefix part of X_p) * price + 1.8e9 = qY * D + rY
+        const uint64_t Y = (BUSY ? busyp * price : A * st0) + kHalfHour;
+        const uint64_t qY = Y / kUsPerHour, rY = Y - qY * kUsPerHour;
+        const uint64_t cnew0 = base + qY, cold = base + pcp;
+        const int64_t dd0 = (int64_t)st0 - Ps;
+        const uint64_t w3g = w3base | ((uint64_t)(1u << p) << 48);
+        const uint32_t j1 = h.lsd_goff[g + 1];
+        for (uint32_t j = h.lsd_goff[g]; j < j1; j++) {
+            const LsdEntry E = h.lsd[j];
+            const uint64_t e = st0 + E.t_us;
+            const uint64_t cnew = cnew0 + E.cq + ((rY + E.cr) >= kUsPerHour ? 1u : 0u);
+            const uint64_t cost = BUSY ? cnew : (e > endp ? cnew : cold);
+            const int64_t d = dd0 + (int64_t)E.t_us;
+            const bool nm = d > M0;  // a new rebuffering maximum (R8)
+            const int64_t M = nm ? d : M0;
+            Rec4 r;
+            r.w0 = R0;
+            r.w1 = (uint64_t)M - R0;
+            r.w2 = cost;
+            r.w3 = (w3g + E.q) + (nm ? (1ull << 32) : 0ull);
+            if (live) st_global_256(lane_out + (size_t)E.dl * kTileRows, r);
+        }
+    }
 }
 
 // ============================================================================ a1-a7 eval
-// Thread <-> row H: the candidates [H*row, (H+1)*row) share their HI digits (digits
-// 0..B-3).  The thread simulates the HI scenes once (per-lane choices, runtime k/pool),
+// Lane <-> row H: the candidates [H*row, (H+1)*row) share their HI digits (digits
+// 0..B-3); a warp owns a tile of 32 consecutive rows (tiled record layout, sw_plan.h).  The thread simulates the HI scenes once (per-lane choices, runtime k/pool),
 // then iterates the MID digit and the LSD digit in lock-step with the other lanes:
 // (k, pool) is warp-uniform there, so the gang update uses compile-time slot indices
 // and the LSD step (the dominant loop) is ~40 integer ops + one 32 B store.
@@ -73,8 +204,7 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
 template <int NP>
 __global__ void __launch_bounds__(kEvalThreads) eval_kernel(
     const DevHeader* __restrict__ g_hdr, const VaEntry* __restrict__ g_va, uint32_t va_bytes,
-    uint64_t row_begin, uint64_t row_end, uint64_t seg_begin, uint64_t seg_end,
-    Rec4* __restrict__ out) {
+    uint64_t tile_begin, uint64_t tile_end, Rec4* __restrict__ out) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bar;
     DevHeader& h = *reinterpret_cast<DevHeader*>(smem);
@@ -86,11 +216,18 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(
     const uint32_t mfirst = h.first[bm], mlast = h.first[bm + 1];
     const uint32_t lfirst = h.first[bl], llast = h.first[bl + 1];
     const uint64_t row = h.row;
+    const uint64_t n_rows = h.n_rows;
     const bool busy_bill = h.flags & 2u;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
 
-    for (uint64_t H = row_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; H < row_end;
-         H += stride) {
+    // warp <-> tile of 32 consecutive rows; lane <-> row H = tile * 32 + lane
+    for (uint64_t t = tile_begin + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < tile_end;
+         t += nwarps) {
+        const uint64_t Hraw = t * kTileRows + lane;
+        const bool live = Hraw < n_rows;  // the last tile may run past the space
+        const uint64_t H = live ? Hraw : n_rows - 1;
+        Rec4* tile_out = out + (t - tile_begin) * kTileRows * row + lane;
         State<NP> st;
         state_init(st, h);
         // ---- HI prefix: decode the row index (MSD = earliest block, R19) and simulate
@@ -124,69 +261,12 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(
                     scene_metrics(s2, s, e, h.P[s], v.q);
                 }
             }
-            const uint64_t ibase = H * row + (uint64_t)dm * rl;
-            if (llast - lfirst == 1) {
-                // ---- LSD fast path (single last scene): only pool p changes
-                uint64_t pc[NP];
-                uint64_t pcsum = h.fixed_cost;
-#pragma unroll
-                for (int q = 0; q < NP; q++) {
-                    const uint64_t X = busy_bill ? s2.busy[q] : (uint64_t)h.G[q] * s2.end[q];
-                    pc[q] = pool_cost(X, h.price[q]);
-                    pcsum += pc[q];
-                }
-                const uint32_t s = lfirst;
-                const uint64_t as = h.a[s];
-                const int64_t Ps = (int64_t)h.P[s];
-                const VaEntry* vb = va + h.voff[bl];
-                const uint32_t* cb = h.choice + h.coff[bl];
-                for (uint32_t dl = 0; dl < rl; dl++) {
-                    const uint32_t ch = cb[dl];
-                    const uint32_t k = ch_k(ch), p = ch_pool(ch);
-                    const VaEntry v = vb[dl];
-                    uint64_t fk = 0, endp = 0, busyp = 0, pcp = 0, Gp = 0, price = 0;
-#pragma unroll
-                    for (int q = 0; q < NP; q++) {
-                        if ((uint32_t)q == p) {
-                            switch (k) {
-                                case 1: fk = s2.F[q][0]; break;
-                                case 2: fk = s2.F[q][1]; break;
-                                case 4: fk = s2.F[q][3]; break;
-                                case 8: fk = s2.F[q][7]; break;
-                                default: fk = sel_dyn(s2.F[q], k - 1);
-                            }
-                            endp = s2.end[q];
-                            busyp = s2.busy[q];
-                            pcp = pc[q];
-                            Gp = h.G[q];
-                            price = h.price[q];
-                        }
-                    }
-                    const uint64_t e = umax64(as, fk) + v.t_us;
-                    const uint64_t X = busy_bill ? busyp + (uint64_t)k * v.t_us : Gp * umax64(endp, e);
-                    const uint64_t cost = pcsum - pcp + pool_cost(X, price);
-                    uint64_t R0 = s2.R0;
-                    int64_t M = s2.M;
-                    uint32_t cnt = s2.cnt;
-                    if (s == 0) {
-                        R0 = e;
-                        M = (int64_t)e;
-                    } else {
-                        const int64_t d = (int64_t)e - Ps;
-                        if (d > M) {
-                            M = d;
-                            cnt++;
-                        }
-                    }
-                    Rec4 r;
-                    r.w0 = R0;
-                    r.w1 = (uint64_t)M - R0;
-                    r.w2 = cost;
-                    r.w3 = (uint64_t)(s2.Q + v.q) | ((uint64_t)cnt << 32) |
-                           ((uint64_t)(s2.used | (1u << p)) << 48);
-                    const uint64_t i = ibase + dl;
-                    if (i >= seg_begin && i < seg_end) st_global_256(out + (i - seg_begin), r);
-                }
+            // record (dm, dl) of this lane's row sits at tile_out + (dm * rl + dl) * 32:
+            // a warp store covers 32 consecutive 32 B records (1 KB, fully coalesced)
+            Rec4* lane_out = tile_out + (size_t)dm * rl * kTileRows;
+            if (llast - lfirst == 1 && lfirst != 0) {
+                if (busy_bill) lsd_fast<NP, true>(h, s2, lane_out, live);
+                else lsd_fast<NP, false>(h, s2, lane_out, live);
             } else {
                 // ---- generic LSD block (several scenes share the last digit)
                 for (uint32_t dl = 0; dl < rl; dl++) {
@@ -204,8 +284,7 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(
                     r.w1 = (uint64_t)s3.M - s3.R0;
                     r.w2 = state_cost(s3, h);
                     r.w3 = (uint64_t)s3.Q | ((uint64_t)s3.cnt << 32) | ((uint64_t)s3.used << 48);
-                    const uint64_t i = ibase + dl;
-                    if (i >= seg_begin && i < seg_end) st_global_256(out + (i - seg_begin), r);
+                    if (live) st_global_256(lane_out + (size_t)dl * kTileRows, r);
                 }
             }
         }
@@ -404,16 +483,19 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__global__ void __launch_bounds__(kScanThreads) digest_kernel(const Rec4* __restrict__ recs, uint64_t n,
-                                                              uint64_t first_index,
-                                                              unsigned long long* __restrict__ acc) {
+__global__ void __launch_bounds__(kScanThreads) digest_kernel(SegView v, unsigned long long* __restrict__ acc) {
     uint64_t sum = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const Rec4 r = ld_global_nc_256(recs + i);
-        // w3 = Q | cnt << 32 | flags << 48  ->  flags << 48 | Q << 16 | cnt
-        const uint64_t w = ((r.w3 >> 48) << 48) | ((r.w3 & 0xffffffffull) << 16) | ((r.w3 >> 32) & 0xffffull);
-        sum += mix64((first_index + i) ^ rotl64(r.w0, 7) ^ rotl64(r.w1, 19) ^ rotl64(r.w2, 31) ^ w);
+    const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
+    for (uint64_t t = blockIdx.x; t < v.ntiles; t += gridDim.x) {
+        const Rec4* tp = v.recs + t * per_tile;
+        for (uint32_t p = threadIdx.x; p < per_tile; p += blockDim.x) {
+            const uint64_t idx = tiled_index(v.t0, v.row, t, p);
+            if (idx < v.ib || idx >= v.ie) continue;
+            const Rec4 r = ld_global_nc_256(tp + p);
+            // w3 = Q | cnt << 32 | flags << 48  ->  flags << 48 | Q << 16 | cnt
+            const uint64_t w = ((r.w3 >> 48) << 48) | ((r.w3 & 0xffffffffull) << 16) | ((r.w3 >> 32) & 0xffffull);
+            sum += mix64(idx ^ rotl64(r.w0, 7) ^ rotl64(r.w1, 19) ^ rotl64(r.w2, 31) ^ w);
+        }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
@@ -573,20 +655,24 @@ __global__ void pareto_append_kernel(const PPoint* __restrict__ front, const PPo
 }
 
 // Strided sample of a record segment -> points (seed for the first DLT).
-__global__ void pareto_sample_kernel(const Rec4* __restrict__ recs, uint64_t n, uint64_t first_index,
-                                     uint32_t ns, PPoint* __restrict__ out, ParetoCtl* ctl) {
+__global__ void pareto_sample_kernel(SegView v, uint32_t ns, PPoint* __restrict__ out, ParetoCtl* ctl) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j == 0) ctl->m_in = ns;
     if (j >= ns) return;
-    const uint64_t i = (uint64_t)((unsigned __int128)j * n / ns);
-    const Rec4 r = ld_global_nc_256(recs + i);
+    const uint64_t per_tile = kTileRows * v.row;
+    const uint64_t npos = v.ntiles * per_tile;
+    const uint64_t pos = (uint64_t)((unsigned __int128)j * npos / ns);
+    const uint64_t t = pos / per_tile;
+    const uint32_t pin = (uint32_t)(pos - t * per_tile);
+    const uint64_t idx = tiled_index(v.t0, v.row, t, pin);
+    if (idx < v.ib || idx >= v.ie) return;
+    const Rec4 r = ld_global_nc_256(v.recs + pos);
     PPoint p;
-    p.idx = first_index + i;
+    p.idx = idx;
     p.t = r.w0 + r.w1;
     p.c = r.w2;
     p.q = rec_Q(r);
     p.pad = 0;
-    out[j] = p;
+    out[atomicAdd(&ctl->m_in, 1u)] = p;
 }
 
 // Gather variable-size per-rank fronts (allgathered, padded to maxc) into one array.
@@ -667,9 +753,8 @@ __device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_
 }
 
 template <int NQ, bool PARETO>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(const Rec4* __restrict__ recs, uint64_t n,
-                                                            uint64_t first_index, SelParams P,
-                                                            Cand* __restrict__ partial, ParetoArgs pa) {
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(SegView v, SelParams P, Cand* __restrict__ partial,
+                                                            ParetoArgs pa) {
     constexpr int NQA = NQ > 0 ? NQ : 1;
     extern __shared__ __align__(16) unsigned char fsm[];
     __shared__ Cand s_tmp[32];
@@ -689,13 +774,13 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const Rec4* __restri
 #pragma unroll
     for (int q = 0; q < NQA; q++) fi[q] = ci[q] = kInf64;
     const int lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-        const uint64_t i = i0 + threadIdx.x;
-        const bool valid = i < n;
+    const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
+    for (uint64_t t = blockIdx.x; t < v.ntiles; t += gridDim.x)
+    for (uint32_t pin = threadIdx.x; pin < per_tile; pin += blockDim.x) {  // warp-uniform trip count
+        const uint64_t idx = tiled_index(v.t0, v.row, t, pin);
+        const bool valid = idx >= v.ib && idx < v.ie;
         Rec4 r{};
-        if (valid) r = ld_global_nc_256(recs + i);
-        const uint64_t idx = first_index + i;
+        if (valid) r = ld_global_nc_256(v.recs + t * per_tile + pin);
         if (valid) {
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
@@ -780,6 +865,16 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const Rec4* __restri
             partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].r = r;
         }
     }
+}
+
+// Linearise n records [index, index + n) of a tiled segment (host views / tests).
+__global__ void gather_records_kernel(SegView v, uint64_t index, uint64_t n, Rec4* __restrict__ out) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint64_t i = index + k;
+    const uint64_t H = i / v.row, j = i - H * v.row;
+    const uint64_t t = H / kTileRows - v.t0, lane = H % kTileRows;
+    out[k] = v.recs[t * kTileRows * v.row + j * kTileRows + lane];
 }
 
 }  // namespace sw

@@ -29,7 +29,8 @@ thread_local std::string g_last_error;
 struct Segment {
     uint64_t gbegin, gend;  // global range of the eval call
     uint64_t begin, end;    // this rank's shard
-    uint64_t offset;        // first record slot in the buffer
+    uint64_t offset;        // record slot of the segment's first tile
+    uint64_t tile0, ntiles; // tiles of 32 rows covering this rank's shard (tiled layout)
     bool folded;            // already folded into the Pareto front
 };
 
@@ -56,7 +57,8 @@ struct sw_plan {
     DevHeader* d_hdr = nullptr;
     VaEntry* d_va = nullptr;
     Rec4* d_rec = nullptr;
-    uint64_t rec_cap = 0, rec_used = 0;
+    uint64_t rec_cap = 0, rec_used = 0;  // record SLOTS (tiled layout incl. padding)
+    uint64_t cand_cap = 0, cand_used = 0;  // candidates retained (record_capacity)
     std::vector<Segment> segs;
 
     // Pareto
@@ -171,6 +173,19 @@ using u128 = unsigned __int128;
 }  // namespace
 
 static sw_status fold_pending(sw_plan* h);
+static constexpr uint64_t kMaxSegs = 16;  // segments with tile padding budgeted per handle
+
+// Tiles [t_lo, t_hi) (relative to the segment) of a segment as a scan view.
+static SegView view_of(const sw_plan* h, const Segment& g, uint64_t t_lo, uint64_t t_hi) {
+    SegView v;
+    v.recs = h->d_rec + g.offset + t_lo * kTileRows * h->row;
+    v.t0 = g.tile0 + t_lo;
+    v.ntiles = t_hi - t_lo;
+    v.row = h->row;
+    v.ib = g.begin;
+    v.ie = g.end;
+    return v;
+}
 static cudaError_t set_scan_smem_attrs();
 
 // ============================================================================ create
@@ -336,6 +351,29 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     }
     H.first[BP] = S;
     H.n_choice = coff;
+    {  // group the LSD digit's choices by (pool, k) in first-appearance order
+        const uint32_t bl = BP - 1, r = H.radix[bl];
+        std::vector<uint32_t> keys;
+        std::vector<std::vector<uint32_t>> members;
+        for (uint32_t c = 0; c < r; c++) {
+            const uint32_t ch = H.choice[H.coff[bl] + c];
+            const uint32_t key = ch_pool(ch) | (ch_k(ch) << 8);
+            size_t gi = std::find(keys.begin(), keys.end(), key) - keys.begin();
+            if (gi == keys.size()) {
+                keys.push_back(key);
+                members.emplace_back();
+            }
+            members[gi].push_back(c);
+        }
+        H.lsd_ngroups = (uint32_t)keys.size();
+        uint32_t o = 0;
+        for (size_t gi = 0; gi < keys.size(); gi++) {
+            H.lsd_goff[gi] = o;
+            H.lsd_pk[gi] = keys[gi];
+            for (uint32_t c : members[gi]) H.lsd_dl[o++] = c;
+        }
+        H.lsd_goff[keys.size()] = o;
+    }
     H.n_va = (uint32_t)n_va;
     H.va_bytes = n_va * sizeof(VaEntry);
     h->row = (uint64_t)H.radix[BP - 2] * H.radix[BP - 1];
@@ -445,8 +483,14 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
 
     // ---- record buffer + reduction scratch
     uint64_t cap = rt->record_capacity;
-    if (cap == 0) cap = N / (uint64_t)h->nranks + 2 * h->row + 1;
-    cap = std::min<uint64_t>(cap, N);
+    if (cap == 0) cap = N / (uint64_t)h->nranks + 1;
+    h->cand_cap = cap;
+    {  // slots: whole tiles of 32 rows plus 2 tiles of padding for each of up to
+       // kMaxSegs segments (each eval call adds at most 2 partial tiles)
+        const uint64_t per_tile = kTileRows * h->row;
+        const uint64_t tiles = (cap + per_tile - 1) / per_tile + 2 * kMaxSegs;
+        cap = tiles * per_tile;
+    }
     h->rec_cap = cap;
     if ((st = alloc_n(h, &h->d_rec, cap, "records")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_front, h->front_cap, "pareto front")) < 0) return bail(st);
@@ -501,6 +545,7 @@ extern "C" sw_status sw_plan_reset(sw_plan* h) {
     if (!h) return fail(nullptr, SW_EINVAL, "null handle");
     h->segs.clear();
     h->rec_used = 0;
+    h->cand_used = 0;
     h->front_n = 0;
     CK(h, cudaSetDevice(h->device));
     CK(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream));
@@ -514,6 +559,7 @@ extern "C" sw_status sw_plan_release_records(sw_plan* h) {
     if (st < 0) return st;
     h->segs.clear();
     h->rec_used = 0;
+    h->cand_used = 0;
     return SW_OK;
 }
 
@@ -563,26 +609,32 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
     sw_status st = sw_shard_range(begin, end, h->row, h->rank, h->nranks, &b, &e);
     if (st < 0) return st;
     const uint64_t n = e - b;
-    if (h->rec_used + n > h->rec_cap)
+    const uint64_t rb = b / h->row, re = (e + h->row - 1) / h->row;
+    const uint64_t t0 = rb / kTileRows, t1 = (re + kTileRows - 1) / kTileRows;
+    const uint64_t slots = n ? (t1 - t0) * kTileRows * h->row : 0;
+    if (h->cand_used + n > h->cand_cap)
         return fail(h, SW_ERANGE, "records would exceed capacity (%llu + %llu > %llu): reset or chunk",
-                    (unsigned long long)h->rec_used, (unsigned long long)n, (unsigned long long)h->rec_cap);
-    Segment sg{begin, end, b, e, h->rec_used, false};
+                    (unsigned long long)h->cand_used, (unsigned long long)n, (unsigned long long)h->cand_cap);
+    if (h->rec_used + slots > h->rec_cap)
+        return fail(h, SW_ERANGE, "record buffer fragmented by more than %llu eval calls: reset or chunk",
+                    (unsigned long long)kMaxSegs);
+    Segment sg{begin, end, b, e, h->rec_used, t0, n ? t1 - t0 : 0, false};
     CK(h, cudaSetDevice(h->device));
     if (n > 0) {
-        const uint64_t rb = b / h->row, re = (e + h->row - 1) / h->row;
-        const uint64_t need = (re - rb + kEvalThreads - 1) / kEvalThreads;
+        const uint64_t need = (sg.ntiles * kTileRows + kEvalThreads - 1) / kEvalThreads;  // one warp per tile
         const uint32_t grid = (uint32_t)std::min<uint64_t>(need, (uint64_t)h->eval_grid);
         Rec4* outp = h->d_rec + h->rec_used;
         CK(h, cudaEventRecord(h->ev0, h->stream));
         launch_np(h, [&](auto np) {
             constexpr int NPc = decltype(np)::value;
-            eval_kernel<NPc><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(
-                h->d_hdr, h->d_va, h->va_bytes, rb, re, b, e, outp);
+            eval_kernel<NPc><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(h->d_hdr, h->d_va, h->va_bytes, t0, t1,
+                                                                             outp);
         });
         CKL(h);
         CK(h, cudaEventRecord(h->ev1, h->stream));
         h->have_eval_ev = true;
-        h->rec_used += n;
+        h->rec_used += slots;
+        h->cand_used += n;
     }
     h->segs.push_back(sg);
     return SW_OK;
@@ -624,24 +676,24 @@ static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint
 }
 
 template <int NQ, bool PARETO>
-static void launch_scan(uint32_t grid, size_t smem, cudaStream_t st, const Rec4* recs, uint64_t n,
-                        uint64_t first, const SelParams& P, Cand* partial, const ParetoArgs& pa) {
-    scan_kernel<NQ, PARETO><<<grid, kScanThreads, smem, st>>>(recs, n, first, P, partial, pa);
+static void launch_scan(uint32_t grid, size_t smem, cudaStream_t st, const SegView& v, const SelParams& P,
+                        Cand* partial, const ParetoArgs& pa) {
+    scan_kernel<NQ, PARETO><<<grid, kScanThreads, smem, st>>>(v, P, partial, pa);
 }
 
 template <bool PARETO>
-static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t st, const Rec4* recs,
-                           uint64_t n, uint64_t first, const SelParams& P, Cand* partial, const ParetoArgs& pa) {
+static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t st, const SegView& v,
+                           const SelParams& P, Cand* partial, const ParetoArgs& pa) {
     switch (nq) {
-        case 0: launch_scan<0, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        case 1: launch_scan<1, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        case 2: launch_scan<2, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        case 3: launch_scan<3, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        case 4: launch_scan<4, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        case 5: launch_scan<5, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        case 6: launch_scan<6, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        case 7: launch_scan<7, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
-        default: launch_scan<8, PARETO>(grid, smem, st, recs, n, first, P, partial, pa); break;
+        case 0: launch_scan<0, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        case 1: launch_scan<1, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        case 2: launch_scan<2, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        case 3: launch_scan<3, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        case 4: launch_scan<4, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        case 5: launch_scan<5, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        case 6: launch_scan<6, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        case 7: launch_scan<7, PARETO>(grid, smem, st, v, P, partial, pa); break;
+        default: launch_scan<8, PARETO>(grid, smem, st, v, P, partial, pa); break;
     }
 }
 
@@ -695,8 +747,8 @@ static sw_status reduce_async(sw_plan* h, PPoint* out) {
 static sw_status seed_async(sw_plan* h, const Segment& g) {
     const uint64_t n = g.end - g.begin;
     const uint32_t ns = (uint32_t)std::min<uint64_t>(n, h->front_cap + h->surv_cap);
-    pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(h->d_rec + g.offset, n, g.begin, ns, h->d_work,
-                                                                  h->d_ctl);
+    CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
+    pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), ns, h->d_work, h->d_ctl);
     CKL(h);
     return reduce_async(h, h->d_front);
 }
@@ -704,22 +756,21 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
 // Fold a segment chunk by chunk: DLT from the current front, one filter pass over the
 // chunk (fused with nq select queries when nq > 0), survivors merged on the device.
 static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
-    const uint64_t n = g.end - g.begin;
     const size_t psmem = sizeof(Dlt) + kFrontSmem * sizeof(PPoint);
-    for (uint64_t c0 = 0; c0 < n; c0 += h->chunk) {
-        const uint64_t cn = std::min(h->chunk, n - c0);
+    const uint64_t ct = std::max<uint64_t>(1, h->chunk / (kTileRows * h->row));  // tiles per chunk
+    for (uint64_t c0 = 0; c0 < g.ntiles; c0 += ct) {
+        const uint64_t c1 = std::min(g.ntiles, c0 + ct);
         dlt_build_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((cn + kScanThreads - 1) / kScanThreads, h->scan_grid);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(c1 - c0, h->scan_grid);
         Cand* part = h->d_partial;
         if (nq) {
             if (*np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many chunks for one select");
             part = h->d_partial + (uint64_t)*np * SW_MAX_QUERIES;
             *np += grid;
         }
-        launch_scan_nq<true>(nq, grid, psmem, h->stream, h->d_rec + g.offset + c0, cn, g.begin + c0, P, part,
-                             pareto_args(h));
+        launch_scan_nq<true>(nq, grid, psmem, h->stream, view_of(h, g, c0, c1), P, part, pareto_args(h));
         CKL(h);
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                h->d_ctl);
@@ -770,9 +821,9 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
             g.folded = true;
             fused.push_back(si);
         } else {
-            const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
+            const uint32_t grid = (uint32_t)std::min<uint64_t>(g.ntiles, h->scan_grid);
             if (np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many segments for one select");
-            launch_scan_nq<false>(nq, grid, 0, h->stream, h->d_rec + g.offset, n, g.begin, P,
+            launch_scan_nq<false>(nq, grid, 0, h->stream, view_of(h, g, 0, g.ntiles), P,
                                   h->d_partial + (uint64_t)np * SW_MAX_QUERIES, pareto_args(h));
             CKL(h);
             np += grid;
@@ -844,10 +895,9 @@ extern "C" sw_status sw_plan_digest(sw_plan* h, uint64_t* digest) {
     CK(h, cudaSetDevice(h->device));
     CK(h, cudaMemsetAsync(h->d_digest, 0, sizeof(unsigned long long), h->stream));
     for (const Segment& g : h->segs) {
-        const uint64_t n = g.end - g.begin;
-        if (!n) continue;
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kScanThreads - 1) / kScanThreads, h->scan_grid);
-        digest_kernel<<<grid, kScanThreads, 0, h->stream>>>(h->d_rec + g.offset, n, g.begin, h->d_digest);
+        if (g.end == g.begin) continue;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(g.ntiles, h->scan_grid);
+        digest_kernel<<<grid, kScanThreads, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), h->d_digest);
         CKL(h);
     }
     if (h->nranks > 1)
@@ -948,10 +998,20 @@ extern "C" sw_status sw_plan_copy_records(sw_plan* h, uint64_t index, uint64_t n
     if (!h || (n && !host_out)) return fail(nullptr, SW_EINVAL, "null argument");
     for (const Segment& g : h->segs) {
         if (index >= g.begin && index + n <= g.end) {
+            if (n == 0) return SW_OK;
             CK(h, cudaSetDevice(h->device));
-            CK(h, cudaMemcpyAsync(host_out, h->d_rec + g.offset + (index - g.begin), n * sizeof(sw_record),
-                                  cudaMemcpyDeviceToHost, h->stream));
-            CK(h, cudaStreamSynchronize(h->stream));
+            Rec4* tmp = nullptr;
+            sw_status st = alloc_n(h, &tmp, n, "record staging");
+            if (st < 0) return st;
+            gather_records_kernel<<<(uint32_t)((n + 255) / 256), 256, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), index,
+                                                                                     n, tmp);
+            cudaError_t e1 = cudaGetLastError();
+            h->launches++;
+            cudaError_t e2 = cudaMemcpyAsync(host_out, tmp, n * sizeof(sw_record), cudaMemcpyDeviceToHost, h->stream);
+            dev_free(h, tmp);
+            cudaError_t e3 = cudaStreamSynchronize(h->stream);
+            if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+                return fail(h, SW_ECUDA, "copy_records failed: %s", cudaGetErrorString(e1 ? e1 : e2 ? e2 : e3));
             return SW_OK;
         }
     }

@@ -32,8 +32,9 @@ struct SegView {
     uint64_t ib, ie;
 };
 constexpr int kScanThreads = 256;
-constexpr int kDltT = 64;  // dominance lookup table: ttff_eff bins
-constexpr int kDltQ = 64;  //                         quality bins
+constexpr int kDltT = 128;  // dominance lookup table: ttff_eff bins (front quantiles)
+constexpr int kDltQ = 128;  //                         quality bins (front quantiles)
+constexpr int kDltMap = 1024;  // coarse direct maps (t: 64 cells per octave; q: linear)
 
 // ============================================================================ a2 + packing
 struct RawDesc {
@@ -598,18 +599,50 @@ __global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint*
     if (x < m) out[rank] = px;
 }
 
-// Dominance lookup table from the current front (sorted by ttff_eff):
-// cell[bt][bq] = min cost over front points f with f.t <= tedge[bt] and f.q >= qedge[bq].
-// A record (t, c, q) with bt = max{i: tedge[i] <= t}, bq = min{j: qedge[j] >= q} and
-// cell < c is strictly dominated by a real candidate, so it cannot be on the front.
+// Dominance lookup table (DLT) from the current front (sorted by ttff_eff).
+// t-bins: quantile edges of the front's t (tedge ascending, bin b holds t >= tedge[b]);
+// q-bins: quantile edges of a strided sample of the front's q (bin j = [qedge[j],
+// qedge[j+1])).  cell[b][j] = min cost over front points f with f.t <= tedge[b] and
+// f.q >= qedge[j+1] - 1, as u32 (0xffffffff = none / too big).  A record (t, c, q) in
+// cell (b, j) with cell < c is strictly dominated by a real candidate (f.t <= t,
+// f.q >= q, f.c < c), so it cannot be on the front.
+// Lookup is O(1): a coarse direct map (t: float exponent + 6 mantissa bits, q: linear)
+// gives a conservative bin, refined by at most two edge comparisons.
 struct Dlt {
+    int32_t kbase;         // coarse t key of tmap[0]
+    uint32_t qmin, qmax, qshift;
     uint64_t tedge[kDltT];
-    uint32_t qedge[kDltQ];
-    uint64_t cell[kDltT * kDltQ];
+    uint32_t qedge[kDltQ + 1];
+    uint32_t pad_[3];
+    uint8_t tmap[kDltMap];  // #edges <= lower end of coarse t cell (0..kDltT)
+    uint8_t qmap[kDltMap];  // bin containing the upper end of coarse q cell
+    uint32_t cell[kDltT * kDltQ];
 };
+static_assert(sizeof(Dlt) % 16 == 0, "Dlt is staged in 16 B vectors");
 
-__global__ void __launch_bounds__(1024) dlt_build_kernel(const PPoint* __restrict__ front,
-                                                         const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
+__device__ __forceinline__ int32_t dlt_tkey(uint64_t t) { return (int32_t)(__float_as_uint(__ull2float_rz(t)) >> 17); }
+
+__device__ __forceinline__ bool dlt_dominated(const Dlt& d, uint64_t t, uint64_t c, uint32_t q) {
+    int32_t k = dlt_tkey(t) - d.kbase;
+    if (k < 0 || q > d.qmax) return false;
+    k = k < kDltMap ? k : kDltMap - 1;
+    int b = (int)d.tmap[k] - 1;
+    if (b + 1 < kDltT && d.tedge[b + 1] <= t) b++;
+    if (b + 1 < kDltT && d.tedge[b + 1] <= t) b++;
+    if (b < 0) return false;
+    uint32_t qc = q < d.qmin ? 0u : (q - d.qmin) >> d.qshift;
+    qc = qc < (uint32_t)kDltMap ? qc : kDltMap - 1;
+    int j = d.qmap[qc];
+    if (j > 0 && d.qedge[j] > q) j--;
+    if (j > 0 && d.qedge[j] > q) j--;
+    const uint32_t cell = d.cell[b * kDltQ + j];
+    return cell != 0xffffffffu && (uint64_t)cell < c;
+}
+
+// Header pass (1 block of 1024): edges, coarse maps.
+__global__ void __launch_bounds__(1024) dlt_head_kernel(const PPoint* __restrict__ front,
+                                                        const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
+    __shared__ uint32_t qs[1024];
     __shared__ uint32_t qmin_s, qmax_s;
     const uint32_t m = (uint32_t)ctl->front_n;
     if (threadIdx.x == 0) {
@@ -621,22 +654,86 @@ __global__ void __launch_bounds__(1024) dlt_build_kernel(const PPoint* __restric
         atomicMin(&qmin_s, front[i].q);
         atomicMax(&qmax_s, front[i].q);
     }
+    // strided sample of front qualities, rank-sorted
+    const uint32_t ms = m < 1024u ? m : 1024u;
+    uint32_t myq = 0;
+    if (threadIdx.x < ms) myq = front[((uint64_t)threadIdx.x * m) / ms].q;
+    __syncthreads();
+    if (threadIdx.x < ms) qs[threadIdx.x] = myq;
+    __syncthreads();
+    uint32_t rank = 0;
+    if (threadIdx.x < ms)
+        for (uint32_t j = 0; j < ms; j++) {
+            const uint32_t o = qs[j];
+            rank += (o < myq || (o == myq && j < threadIdx.x)) ? 1u : 0u;
+        }
+    __syncthreads();
+    if (threadIdx.x < ms) qs[rank] = myq;
     __syncthreads();
     const uint32_t qmin = qmin_s, qmax = qmax_s;
+    if (threadIdx.x == 0) {
+        d->qmin = m ? qmin : 0xffffffffu;
+        d->qmax = m ? qmax : 0;
+        uint32_t sh = 0;
+        const uint64_t range = m ? (uint64_t)qmax - qmin + 1 : 1;
+        while (((range - 1) >> sh) >= (uint64_t)kDltMap) sh++;
+        d->qshift = sh;
+        d->kbase = m ? dlt_tkey(front[0].t) : 0x7fffffff;
+    }
     for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x)
         d->tedge[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
-    for (uint32_t j = threadIdx.x; j < kDltQ; j += blockDim.x)
-        d->qedge[j] = m ? (uint32_t)(qmin + ((uint64_t)(qmax - qmin) * j) / (kDltQ - 1)) : 0xffffffffu;
+    for (uint32_t j = threadIdx.x; j <= kDltQ; j += blockDim.x)
+        d->qedge[j] = !m ? 0xffffffffu : (j == kDltQ ? qmax + 1 : (j == 0 ? qmin : qs[((uint64_t)j * ms) / kDltQ]));
     __syncthreads();
-    for (uint32_t cidx = threadIdx.x; cidx < kDltT * kDltQ; cidx += blockDim.x) {
-        const uint32_t bt = cidx / kDltQ, bq = cidx % kDltQ;
-        const uint64_t te = d->tedge[bt];
-        const uint32_t qe = d->qedge[bq];
-        uint64_t best = kInf64;
-        for (uint32_t i = 0; i < m && front[i].t <= te; i++)
-            if (front[i].q >= qe) best = umin64(best, front[i].c);
-        d->cell[cidx] = best;
+    // coarse maps
+    const int32_t kbase = m ? dlt_tkey(front[0].t) : 0;
+    uint32_t qsh = 0;
+    {
+        const uint64_t range = m ? (uint64_t)qmax - qmin + 1 : 1;
+        while (((range - 1) >> qsh) >= (uint64_t)kDltMap) qsh++;
     }
+    for (uint32_t k = threadIdx.x; k < kDltMap; k += blockDim.x) {
+        // lower end of coarse t cell k: smallest integer t with key(t) >= kbase + k
+        const int32_t key = kbase + (int32_t)k;
+        const uint64_t L = (!m || key >= (0x7f8 << 3)) ? kInf64 : (uint64_t)ceilf(__uint_as_float((uint32_t)key << 17));
+        uint32_t cntle = 0;
+        for (uint32_t b = 0; b < kDltT; b++) cntle += d->tedge[b] <= L ? 1u : 0u;
+        d->tmap[k] = (uint8_t)(m ? cntle : 0);
+        // upper end of coarse q cell k
+        const uint64_t U64 = (uint64_t)qmin + (((uint64_t)k + 1) << qsh) - 1;
+        const uint32_t U = U64 > qmax ? qmax : (uint32_t)U64;
+        uint32_t j = 0;
+        while (j + 1 < (uint32_t)kDltQ && d->qedge[j + 1] <= U) j++;
+        d->qmap[k] = (uint8_t)j;
+    }
+}
+
+// Cells: block b = t-bin, thread j = q-bin; front staged through smem.
+__global__ void __launch_bounds__(kDltQ) dlt_cell_kernel(const PPoint* __restrict__ front,
+                                                         const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
+    __shared__ PPoint tile[kDltQ];
+    const uint32_t m = (uint32_t)ctl->front_n;
+    const uint32_t b = blockIdx.x, j = threadIdx.x;
+    const uint64_t Eb = d->tedge[b];
+    const uint64_t qhi = (uint64_t)d->qedge[j + 1] - 1;
+    uint64_t best = kInf64;
+    bool more = true;
+    for (uint32_t base = 0; base < m && more; base += kDltQ) {
+        __syncthreads();
+        if (base + j < m) tile[j] = front[base + j];
+        __syncthreads();
+        const uint32_t lim = min((uint32_t)kDltQ, m - base);
+        for (uint32_t i = 0; i < lim; i++) {
+            const PPoint f = tile[i];
+            if (f.t > Eb) {
+                more = false;  // front sorted by t: no later point qualifies
+                break;
+            }
+            if ((uint64_t)f.q >= qhi) best = umin64(best, f.c);
+        }
+        more = __syncthreads_or(more);
+    }
+    d->cell[b * kDltQ + j] = (m == 0 || best >= 0xffffffffull) ? 0xffffffffu : (uint32_t)best;
 }
 
 // work = front[0, front_n) ++ surv[0, min(surv, cap)); m_in = its size.
@@ -752,113 +849,183 @@ __device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_
     return obj_strict_better(obj, a, b);
 }
 
+// TMA-pipelined scan: warp kCW (one elected lane) streams the segment through a
+// kStages-deep shared-memory ring with cp.async.bulk (completion on a "full" mbarrier
+// per stage); kCW consumer warps take one record per thread per stage from shared
+// memory and release the stage on an "empty" mbarrier.  Bytes in flight per SM are
+// set by the ring (kStages x 16 KB), not by registers or occupancy.
+constexpr int kCW = 16;                       // consumer warps per block
+constexpr int kScanBlock = (kCW + 1) * 32;    // + 1 producer warp
+constexpr uint32_t kStageRecs = kCW * 32;     // records per stage (16 KB)
+constexpr int kStages = 8;        // plain scans
+constexpr int kStagesPareto = 5;  // scans carrying the DLT + front subset in smem
+__host__ __device__ constexpr size_t ring_bytes(bool pareto) {
+    return (size_t)(pareto ? kStagesPareto : kStages) * kStageRecs * sizeof(Rec4);
+}
+
+struct StageMeta {
+    uint64_t t;
+    uint32_t pin0, cnt;  // cnt == 0: end of stream
+    uint32_t all_valid;  // every record of the stage lies in [ib, ie): skip per-record checks
+    uint32_t pad;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <int NQ, bool PARETO>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(SegView v, SelParams P, Cand* __restrict__ partial,
-                                                            ParetoArgs pa) {
+__global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParams P, Cand* __restrict__ partial,
+                                                             ParetoArgs pa) {
     constexpr int NQA = NQ > 0 ? NQ : 1;
-    extern __shared__ __align__(16) unsigned char fsm[];
+    extern __shared__ __align__(128) unsigned char fsm[];
     __shared__ Cand s_tmp[32];
-    Dlt& d = *reinterpret_cast<Dlt*>(fsm);
-    PPoint* fs = reinterpret_cast<PPoint*>(fsm + sizeof(Dlt));
+    constexpr int NS = PARETO ? kStagesPareto : kStages;
+    __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
+    __shared__ StageMeta meta[NS];
+    Rec4* ring = reinterpret_cast<Rec4*>(fsm);
+    Dlt& d = *reinterpret_cast<Dlt*>(fsm + ring_bytes(PARETO));
+    PPoint* fs = reinterpret_cast<PPoint*>(fsm + ring_bytes(PARETO) + sizeof(Dlt));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < NS; st++) {
+            mbar_init(&full_bar[st], 1);
+            mbar_init(&empty_bar[st], kCW);
+        }
+    }
     uint32_t m_sm = 0;
     if (PARETO) {
         m_sm = (uint32_t)umin64(pa.ctl->front_n, kFrontSmem);
-        for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x) d.tedge[i] = pa.dlt->tedge[i];
-        for (uint32_t i = threadIdx.x; i < kDltQ; i += blockDim.x) d.qedge[i] = pa.dlt->qedge[i];
-        for (uint32_t i = threadIdx.x; i < kDltT * kDltQ; i += blockDim.x) d.cell[i] = pa.dlt->cell[i];
-        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = pa.front[i];
-        __syncthreads();
-    }
-    uint64_t fi[NQA], ci[NQA];
-    Rec4 fr[NQA], cr[NQA];
-#pragma unroll
-    for (int q = 0; q < NQA; q++) fi[q] = ci[q] = kInf64;
-    const int lane = threadIdx.x & 31;
-    const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
-    for (uint64_t t = blockIdx.x; t < v.ntiles; t += gridDim.x)
-    for (uint32_t pin = threadIdx.x; pin < per_tile; pin += blockDim.x) {  // warp-uniform trip count
-        const uint64_t idx = tiled_index(v.t0, v.row, t, pin);
-        const bool valid = idx >= v.ib && idx < v.ie;
-        Rec4 r{};
-        if (valid) r = ld_global_nc_256(v.recs + t * per_tile + pin);
-        if (valid) {
-#pragma unroll
-            for (int q = 0; q < NQ; q++) {
-                if (feasible(P.q[q], r)) {
-                    if (fi[q] == kInf64 || obj_strict_better(P.objective, r, fr[q])) {
-                        fi[q] = idx;
-                        fr[q] = r;
-                    }
-                } else if (fi[q] == kInf64) {
-                    if (ci[q] == kInf64 || closest_strict_better(P.q[q], P.objective, r, cr[q])) {
-                        ci[q] = idx;
-                        cr[q] = r;
-                    }
-                }
-            }
+        {  // stage the whole DLT (16 B vectors)
+            const uint4* src = reinterpret_cast<const uint4*>(pa.dlt);
+            uint4* dst = reinterpret_cast<uint4*>(&d);
+            for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
         }
-        if (PARETO) {
-            bool keep = false;
-            PPoint pt{};
-            if (valid) {
-                pt.idx = idx;
-                pt.t = r.w0 + r.w1;
-                pt.c = r.w2;
-                pt.q = rec_Q(r);
-                int lo = 0, hi = kDltT;  // bt = (#edges <= t) - 1
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (d.tedge[mid] <= pt.t) lo = mid + 1;
-                    else hi = mid;
+        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = pa.front[i];
+    }
+    __syncthreads();
+    // one running best per query under the query's total order (feasible first)
+    uint64_t bi[NQA];
+    Rec4 br[NQA];
+    bool bf[NQA];
+#pragma unroll
+    for (int q = 0; q < NQA; q++) {
+        bi[q] = kInf64;
+        br[q] = Rec4{};
+        bf[q] = false;
+    }
+    const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
+
+    if (warp == kCW) {
+        // ---------------- producer: one elected lane issues the bulk copies
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (uint64_t t = blockIdx.x; t < v.ntiles; t += gridDim.x) {
+                for (uint32_t pin0 = 0; pin0 < per_tile; pin0 += kStageRecs, it++) {
+                    const uint32_t st = it % NS, k = it / NS;
+                    if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
+                    const uint32_t cnt = min(kStageRecs, per_tile - pin0);
+                    // stage rows t*32 .. t*32+31, in-row offsets j0 .. j1: index range
+                    const uint64_t j0 = pin0 >> 5, j1 = (pin0 + cnt - 1) >> 5;
+                    const uint64_t H0 = (v.t0 + t) * kTileRows;
+                    const uint64_t lo = H0 * v.row + j0, hi = (H0 + kTileRows - 1) * v.row + j1;
+                    meta[st].t = t;
+                    meta[st].pin0 = pin0;
+                    meta[st].cnt = cnt;
+                    meta[st].all_valid = (cnt % 32 == 0 && lo >= v.ib && hi < v.ie) ? 1u : 0u;
+                    mbar_expect_tx(&full_bar[st], cnt * (uint32_t)sizeof(Rec4));
+                    tma_bulk_g2s(ring + (size_t)st * kStageRecs, v.recs + t * per_tile + pin0,
+                                 cnt * (uint32_t)sizeof(Rec4), &full_bar[st]);
                 }
-                const int bt = lo - 1;
-                int lo2 = 0, hi2 = kDltQ;  // bq = min{j : qedge[j] >= q}
-                while (lo2 < hi2) {
-                    const int mid = (lo2 + hi2) >> 1;
-                    if (d.qedge[mid] >= pt.q) hi2 = mid;
-                    else lo2 = mid + 1;
-                }
-                const int bq = lo2;
-                keep = (bt < 0 || bq >= kDltQ) ? true : !(d.cell[bt * kDltQ + bq] < pt.c);
             }
-            unsigned pend = __ballot_sync(0xffffffffu, keep);
-            while (pend) {  // exact test of each DLT survivor by the whole warp
-                const int src = __ffs(pend) - 1;
-                pend &= pend - 1;
-                PPoint x;
-                x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
-                x.t = __shfl_sync(0xffffffffu, pt.t, src);
-                x.c = __shfl_sync(0xffffffffu, pt.c, src);
-                x.q = __shfl_sync(0xffffffffu, pt.q, src);
-                bool dom = false;
-                for (uint32_t j0 = 0; j0 < m_sm; j0 += 32) {
-                    const uint32_t j = j0 + lane;
-                    // an identical entry (same index) also removes x: it is already kept
-                    const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
-                    if (__any_sync(0xffffffffu, dj)) {
-                        dom = true;
-                        break;
+            const uint32_t st = it % NS, k = it / NS;  // end-of-stream marker
+            if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
+            meta[st].cnt = 0;
+            mbar_arrive(&full_bar[st]);
+        }
+    } else {
+        // ---------------- consumers
+        for (uint32_t it = 0;; it++) {
+            const uint32_t st = it % NS;
+            mbar_wait(&full_bar[st], (it / NS) & 1);
+            const StageMeta mt = meta[st];
+            if (mt.cnt == 0) break;
+            const uint32_t tid = threadIdx.x;  // < kStageRecs
+            bool valid = tid < mt.cnt;
+            if (valid && !mt.all_valid) {  // tile-edge stages only
+                const uint64_t i0 = tiled_index(v.t0, v.row, mt.t, mt.pin0 + tid);
+                valid = tid < mt.cnt && i0 >= v.ib && i0 < v.ie;
+            }
+            Rec4 r{};
+            if (valid) r = ring[(size_t)st * kStageRecs + tid];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage data is in registers now
+            if (valid) {
+#pragma unroll
+                for (int q = 0; q < NQ; q++) {
+                    // cheap first-key filter: once the best is feasible only a feasible
+                    // record can win, and under QUALITY_FIRST only with quality >= best's
+                    if (bf[q] && P.objective == 0 && rec_Q(r) < rec_Q(br[q])) continue;
+                    const bool f = feasible(P.q[q], r);
+                    if (bf[q] && !f) continue;
+                    const uint64_t idx = tiled_index(v.t0, v.row, mt.t, mt.pin0 + tid);
+                    if (cand_better(P.q[q], P.objective, idx, r, bi[q], br[q])) {
+                        bi[q] = idx;
+                        br[q] = r;
+                        bf[q] = f;
                     }
                 }
-                if (lane == src && dom) keep = false;
             }
-            const unsigned mask = __ballot_sync(0xffffffffu, keep);
-            if (mask) {
-                const int leader = __ffs(mask) - 1;
-                unsigned long long slot0 = 0;
-                if (lane == leader) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
-                slot0 = __shfl_sync(0xffffffffu, slot0, leader);
-                if (keep) {
-                    const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-                    if (slot < pa.cap) pa.surv[slot] = pt;
+            if (PARETO) {
+                bool keep = false;
+                PPoint pt{};
+                if (valid) {
+                    pt.t = r.w0 + r.w1;
+                    pt.c = r.w2;
+                    pt.q = rec_Q(r);
+                    keep = !dlt_dominated(d, pt.t, pt.c, pt.q);
+                }
+                if (keep) pt.idx = tiled_index(v.t0, v.row, mt.t, mt.pin0 + tid);
+                unsigned pend = __ballot_sync(0xffffffffu, keep);
+                while (pend) {  // exact test of each DLT survivor by the whole warp
+                    const int src = __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    PPoint x;
+                    x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
+                    x.t = __shfl_sync(0xffffffffu, pt.t, src);
+                    x.c = __shfl_sync(0xffffffffu, pt.c, src);
+                    x.q = __shfl_sync(0xffffffffu, pt.q, src);
+                    bool dom = false;
+                    // front sorted by t: only points with t <= x.t can dominate x
+                    for (uint32_t j0 = 0; j0 < m_sm && fs[j0].t <= x.t; j0 += 32) {
+                        const uint32_t j = j0 + lane;
+                        // an identical entry (same index) also removes x: it is already kept
+                        const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
+                        if (__any_sync(0xffffffffu, dj)) {
+                            dom = true;
+                            break;
+                        }
+                    }
+                    if (lane == src && dom) keep = false;
+                }
+                const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                if (mask) {
+                    const int leader = __ffs(mask) - 1;
+                    unsigned long long slot0 = 0;
+                    if (lane == leader) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
+                    slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+                    if (keep) {
+                        const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+                        if (slot < pa.cap) pa.surv[slot] = pt;
+                    }
                 }
             }
         }
     }
 #pragma unroll
     for (int q = 0; q < NQ; q++) {
-        uint64_t idx = fi[q] != kInf64 ? fi[q] : ci[q];
-        Rec4 r = fi[q] != kInf64 ? fr[q] : cr[q];
+        uint64_t idx = bi[q];
+        Rec4 r = br[q];
         block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
         if (threadIdx.x == 0) {
             partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].idx = idx;

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -475,7 +476,9 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         }
         h->eval_grid = occ * h->num_sms;
     }
-    h->scan_grid = (uint32_t)h->num_sms * 4;
+    h->scan_grid = (uint32_t)h->num_sms;  // scan kernels: one TMA-pipelined block per SM
+    if (const char* ev = getenv("SW_PARETO_CHUNK")) h->chunk = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
+    if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (set_scan_smem_attrs() != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ECUDA, "scan kernel smem attribute failed"));
@@ -678,7 +681,7 @@ static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint
 template <int NQ, bool PARETO>
 static void launch_scan(uint32_t grid, size_t smem, cudaStream_t st, const SegView& v, const SelParams& P,
                         Cand* partial, const ParetoArgs& pa) {
-    scan_kernel<NQ, PARETO><<<grid, kScanThreads, smem, st>>>(v, P, partial, pa);
+    scan_kernel<NQ, PARETO><<<grid, kScanBlock, smem, st>>>(v, P, partial, pa);
 }
 
 template <bool PARETO>
@@ -697,10 +700,16 @@ static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t
     }
 }
 
+static constexpr size_t kScanSmemPareto = ring_bytes(true) + sizeof(Dlt) + kFrontSmem * sizeof(PPoint);
+static constexpr size_t kRingBytes = ring_bytes(false);
+
 template <int NQ>
 static cudaError_t set_attr_one() {
-    return cudaFuncSetAttribute(scan_kernel<NQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(sizeof(Dlt) + kFrontSmem * sizeof(PPoint)));
+    cudaError_t a = cudaFuncSetAttribute(scan_kernel<NQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kScanSmemPareto);
+    cudaError_t b = cudaFuncSetAttribute(scan_kernel<NQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kRingBytes);
+    return a != cudaSuccess ? a : b;
 }
 
 static cudaError_t set_scan_smem_attrs() {
@@ -756,11 +765,16 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
 // Fold a segment chunk by chunk: DLT from the current front, one filter pass over the
 // chunk (fused with nq select queries when nq > 0), survivors merged on the device.
 static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
-    const size_t psmem = sizeof(Dlt) + kFrontSmem * sizeof(PPoint);
-    const uint64_t ct = std::max<uint64_t>(1, h->chunk / (kTileRows * h->row));  // tiles per chunk
-    for (uint64_t c0 = 0; c0 < g.ntiles; c0 += ct) {
-        const uint64_t c1 = std::min(g.ntiles, c0 + ct);
-        dlt_build_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+    const size_t psmem = kScanSmemPareto;
+    // geometric chunks: the front sharpens on small early chunks, later chunks are big
+    const uint64_t per_tile = kTileRows * h->row;
+    uint64_t ct = std::max<uint64_t>(1, (h->chunk >> 4) / per_tile);
+    const uint64_t ct_max = std::max<uint64_t>(1, (h->chunk << 3) / per_tile);
+    for (uint64_t c0 = 0, c1 = 0; c0 < g.ntiles; c0 = c1, ct = std::min(ct_max, ct * 4)) {
+        c1 = std::min(g.ntiles, c0 + ct);
+        dlt_head_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+        CKL(h);
+        dlt_cell_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
         const uint32_t grid = (uint32_t)std::min<uint64_t>(c1 - c0, h->scan_grid);
@@ -823,7 +837,7 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
         } else {
             const uint32_t grid = (uint32_t)std::min<uint64_t>(g.ntiles, h->scan_grid);
             if (np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many segments for one select");
-            launch_scan_nq<false>(nq, grid, 0, h->stream, view_of(h, g, 0, g.ntiles), P,
+            launch_scan_nq<false>(nq, grid, kRingBytes, h->stream, view_of(h, g, 0, g.ntiles), P,
                                   h->d_partial + (uint64_t)np * SW_MAX_QUERIES, pareto_args(h));
             CKL(h);
             np += grid;
@@ -896,7 +910,7 @@ extern "C" sw_status sw_plan_digest(sw_plan* h, uint64_t* digest) {
     CK(h, cudaMemsetAsync(h->d_digest, 0, sizeof(unsigned long long), h->stream));
     for (const Segment& g : h->segs) {
         if (g.end == g.begin) continue;
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(g.ntiles, h->scan_grid);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(g.ntiles, (uint64_t)h->num_sms * 8);
         digest_kernel<<<grid, kScanThreads, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), h->d_digest);
         CKL(h);
     }

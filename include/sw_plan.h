@@ -207,6 +207,19 @@ sw_status sw_plan_select(sw_plan *h, uint64_t slo_startup_us, uint64_t slo_stall
 sw_status sw_plan_select_batch(sw_plan *h, uint32_t n_queries, const sw_query *queries,
                                sw_selection *out);
 
+/* Chunked sweep of global candidates [begin, end) for spaces larger than the record
+ * buffer (C5: 1.2e10 plans = 391 GB of records): for each chunk of `chunk` global
+ * candidates (0 = as many as record_capacity allows on every rank), eval -> one fused
+ * select + Pareto-fold scan -> (optional) digest -> records dropped.  Per-query
+ * winners of the chunks are merged with the query's total order (sw_selection_merge)
+ * into out[0, n_queries); the running Pareto front persists (sw_pareto_get after);
+ * *digest (may be NULL) receives the digest of [begin, end).  The handle must hold no
+ * records (fresh, reset or released) -- else SW_ESTATE; n_queries may be 0 (front
+ * and digest only).  Collective when nranks > 1.  Returns the worst soft status. */
+sw_status sw_plan_sweep(sw_plan *h, uint64_t begin, uint64_t end, uint64_t chunk,
+                        uint32_t n_queries, const sw_query *queries, sw_selection *out,
+                        uint64_t *digest);
+
 /* The running 3-D Pareto front over (ttff_eff min, cost min, quality max), exact
  * duplicates keeping the lowest index (R14), sorted by (ttff_eff asc, cost asc,
  * quality desc, index asc).  Two-call idiom: cap = 0 returns *n_out; a short
@@ -228,6 +241,26 @@ sw_status sw_plan_records(const sw_plan *h, const sw_record **dev_ptr, uint64_t 
 /* Copy n records starting at GLOBAL index `index` (must lie in one evaluated local
  * segment) into host memory. */
 sw_status sw_plan_copy_records(sw_plan *h, uint64_t index, uint64_t n, sw_record *host_out);
+
+/* ---- host-only helpers (no device needed) ---------------------------------- */
+
+/* Size of the plan space N = prod r_b and the row size (candidates per eval-kernel
+ * thread: the product of the last two digits' radices, digits left-padded with
+ * radix 1 to B >= 3) of a profile table, without creating a handle.  Only
+ * tables->n_digits and tables->radix are read.  EINVAL on a bad shape, ERANGE when
+ * N >= 2^63. */
+sw_status sw_space_shape(const sw_profile_tables *tables, uint64_t *n, uint64_t *row);
+
+/* Associative, commutative merge of two selections of the SAME query (q) over
+ * disjoint candidate sets, e.g. the winners of successive chunks of a chunked sweep
+ * (eval -> select -> release_records, R13) or of independent handles.  *out = the
+ * better of *a and *b under the query's total order (R13): feasible plans
+ * by the objective key (objective as in sw_price_table), else the closest plan by
+ * (startup+stall violation, budget violation, key), the lower index breaking ties;
+ * an SW_EMPTY input loses.  out->status is recomputed (SW_OK feasible, SW_CLOSEST
+ * not, SW_EMPTY if both are empty) and returned.  out may alias a or b.  Host only. */
+sw_status sw_selection_merge(uint32_t objective, const sw_query *q, const sw_selection *a,
+                             const sw_selection *b, sw_selection *out);
 
 /* ---- multi-GPU --------------------------------------------- */
 

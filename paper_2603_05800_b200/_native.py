@@ -95,12 +95,17 @@ EXPORTS = {
                                    C.POINTER(sw_selection)]),
     "sw_plan_select_batch": (C.c_int32, [C.c_void_p, C.c_uint32, C.POINTER(sw_query),
                                          C.POINTER(sw_selection)]),
+    "sw_plan_sweep": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
+                                  C.POINTER(sw_query), C.POINTER(sw_selection), U64P]),
     "sw_pareto_get": (C.c_int32, [C.c_void_p, C.POINTER(sw_pareto_point), C.c_uint64, U64P]),
     "sw_plan_digest": (C.c_int32, [C.c_void_p, U64P]),
     "sw_plan_detail": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(sw_selection), U64P]),
     "sw_plan_records": (C.c_int32, [C.c_void_p, C.POINTER(C.c_void_p), U64P]),
     "sw_plan_copy_records": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64,
                                          C.POINTER(sw_record)]),
+    "sw_space_shape": (C.c_int32, [C.POINTER(sw_profile_tables), U64P, U64P]),
+    "sw_selection_merge": (C.c_int32, [C.c_uint32, C.POINTER(sw_query), C.POINTER(sw_selection),
+                                       C.POINTER(sw_selection), C.POINTER(sw_selection)]),
     "sw_shard_range": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32,
                                    U64P, U64P]),
     "sw_plan_row_size": (C.c_int32, [C.c_void_p, U64P]),
@@ -157,6 +162,39 @@ def shard_range(begin: int, end: int, row: int, rank: int, nranks: int):
     b, e = C.c_uint64(), C.c_uint64()
     _check(lib().sw_shard_range(begin, end, row, rank, nranks, C.byref(b), C.byref(e)))
     return b.value, e.value
+
+
+def space_shape(problem):
+    """(N, row) of a problem's plan space without a device (sw_space_shape)."""
+    radix = _arr(C.c_uint32, problem.radix)
+    tb = sw_profile_tables(len(problem.radix), radix, None, None, None, 0, None, 0)
+    n, row = C.c_uint64(), C.c_uint64()
+    _check(lib().sw_space_shape(C.byref(tb), C.byref(n), C.byref(row)))
+    return n.value, row.value
+
+
+def _sel_struct(s: "Selection") -> sw_selection:
+    out = sw_selection()
+    out.status, out.index = s.status, s.index
+    (out.rec.ttff_us, out.rec.stall_us, out.rec.cost_mc, out.rec.quality, out.rec.stall_count,
+     out.rec.flags) = s.rec
+    out.ttff_eff_us, out.makespan_us = s.ttff_eff_us, s.makespan_us
+    for i, v in enumerate(s.pool_end_us[:SW_MAX_POOLS]):
+        out.pool_end_us[i] = v
+    for i, v in enumerate(s.digit[:SW_MAX_DIGITS]):
+        out.digit[i] = v
+    return out
+
+
+def selection_merge(objective: int, query, a: "Selection", b: "Selection") -> "Selection":
+    """The better of two selections of one query over disjoint candidate sets
+    (sw_selection_merge, host only): chunked sweeps, independent handles, ranks."""
+    q = query if isinstance(query, tuple) else (query.slo_startup_us, query.slo_stall_us,
+                                                 query.budget_mc)
+    sa, sb, out = _sel_struct(a), _sel_struct(b), sw_selection()
+    _check(lib().sw_selection_merge(objective, C.byref(sw_query(*q)), C.byref(sa), C.byref(sb),
+                                    C.byref(out)))
+    return _sel(out, max(len(a.pool_end_us), len(b.pool_end_us)), max(len(a.digit), len(b.digit)))
 
 
 def comm_unique_id() -> bytes:
@@ -290,6 +328,18 @@ class Plan:
             self._ck(lib().sw_plan_select_batch(self.h, len(chunk), arr, out))
             res += [_sel(o, self.n_pools, self.B) for o in out]
         return res
+
+    def sweep(self, begin: int, end: int, queries: Sequence = (), chunk: int = 0,
+              digest: bool = False):
+        """Chunked sweep (sw_plan_sweep): -> (selections, digest or None)."""
+        qs = [q if isinstance(q, tuple) else (q.slo_startup_us, q.slo_stall_us, q.budget_mc)
+              for q in queries]
+        arr = (sw_query * max(1, len(qs)))(*[sw_query(*q) for q in qs])
+        out = (sw_selection * max(1, len(qs)))()
+        d = C.c_uint64()
+        self._ck(lib().sw_plan_sweep(self.h, begin, end, chunk, len(qs), arr, out,
+                                     C.byref(d) if digest else None))
+        return [_sel(o, self.n_pools, self.B) for o in out[: len(qs)]], (d.value if digest else None)
 
     def pareto(self):
         n = C.c_uint64()

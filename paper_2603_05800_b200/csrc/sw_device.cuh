@@ -238,7 +238,7 @@ __device__ __forceinline__ Rec4 ld_global_nc_256(const void* ptr) {
     return r;
 }
 
-__device__ __forceinline__ uint32_t rec_Q(const Rec4& r) { return (uint32_t)r.w3; }
+__host__ __device__ __forceinline__ uint32_t rec_Q(const Rec4& r) { return (uint32_t)r.w3; }
 
 // ---- TMA bulk staging (cp.async.bulk global -> shared, completion on an mbarrier) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

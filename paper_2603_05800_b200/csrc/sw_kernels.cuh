@@ -353,14 +353,24 @@ struct Cand {
     Rec4 r;
 };
 
-__device__ __forceinline__ uint64_t sat_sub(uint64_t x, uint64_t y) { return x > y ? x - y : 0; }
+// The comparison functions below are __host__ __device__: the same code ranks candidates
+// in the scan kernels, the cross-rank merge kernel and the host-side sw_selection_merge.
+__host__ __device__ __forceinline__ uint64_t sat_sub(uint64_t x, uint64_t y) { return x > y ? x - y : 0; }
 
-__device__ __forceinline__ bool feasible(const QueryDev& q, const Rec4& r) {
+__host__ __device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+__host__ __device__ __forceinline__ bool feasible(const QueryDev& q, const Rec4& r) {
     return r.w0 <= q.slo_t && r.w1 <= q.slo_s && r.w2 <= q.budget;
 }
 
 // Objective order (R13): true iff a precedes b.
-__device__ __forceinline__ int obj_cmp(uint32_t obj, uint64_t ia, const Rec4& a, uint64_t ib,
+__host__ __device__ __forceinline__ int obj_cmp(uint32_t obj, uint64_t ia, const Rec4& a, uint64_t ib,
                                        const Rec4& b) {
     const uint64_t ta = a.w0 + a.w1, tb = b.w0 + b.w1;
     const uint32_t qa = rec_Q(a), qb = rec_Q(b);
@@ -369,8 +379,8 @@ __device__ __forceinline__ int obj_cmp(uint32_t obj, uint64_t ia, const Rec4& a,
         if (a.w2 != b.w2) return a.w2 < b.w2 ? -1 : 1;
         if (ta != tb) return ta < tb ? -1 : 1;
     } else {  // COST_X_TTFF (cost x ttff_eff as 128-bit, -Q, index)
-        const uint64_t lo_a = a.w2 * ta, hi_a = __umul64hi(a.w2, ta);
-        const uint64_t lo_b = b.w2 * tb, hi_b = __umul64hi(b.w2, tb);
+        const uint64_t lo_a = a.w2 * ta, hi_a = mulhi64(a.w2, ta);
+        const uint64_t lo_b = b.w2 * tb, hi_b = mulhi64(b.w2, tb);
         if (hi_a != hi_b) return hi_a < hi_b ? -1 : 1;
         if (lo_a != lo_b) return lo_a < lo_b ? -1 : 1;
         if (qa != qb) return qa > qb ? -1 : 1;
@@ -382,7 +392,7 @@ __device__ __forceinline__ int obj_cmp(uint32_t obj, uint64_t ia, const Rec4& a,
 // Total order of a query: feasible plans by objective; then (nothing feasible)
 // the closest plan by (V_t, V_c, objective, index) ("returns the closest
 // solution").  Invalid candidates (idx = inf) are last.
-__device__ __forceinline__ bool cand_better(const QueryDev& q, uint32_t obj, uint64_t ia,
+__host__ __device__ __forceinline__ bool cand_better(const QueryDev& q, uint32_t obj, uint64_t ia,
                                             const Rec4& a, uint64_t ib, const Rec4& b) {
     if (ib == kInf64) return ia != kInf64;
     if (ia == kInf64) return false;

@@ -903,6 +903,52 @@ extern "C" sw_status sw_plan_detail(sw_plan* h, uint64_t index, sw_selection* ou
     return SW_OK;
 }
 
+// ============================================================================ chunked sweep
+extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uint64_t chunk, uint32_t nq,
+                                   const sw_query* qs, sw_selection* out, uint64_t* digest) {
+    if (!h || (nq && (!qs || !out))) return fail(nullptr, SW_EINVAL, "null argument");
+    if (nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u > %d", nq, SW_MAX_QUERIES);
+    if (begin > end || end > h->N) return fail(h, SW_EINVAL, "range outside [0, N)");
+    if (!h->segs.empty()) return fail(h, SW_ESTATE, "sweep needs a handle without records (reset/release)");
+    // largest global chunk whose every rank shard fits the per-rank capacity: whole
+    // rows per rank, at most cand_cap - row candidates each (ragged ends fit the slack)
+    const uint64_t rows_per_rank = h->cand_cap > h->row ? (h->cand_cap - h->row) / h->row : 0;
+    const uint64_t max_chunk = rows_per_rank * h->row * (uint64_t)h->nranks;
+    if (chunk == 0) chunk = max_chunk;
+    if (chunk == 0 || chunk > max_chunk)
+        return fail(h, SW_ERANGE, "chunk %llu exceeds what record_capacity %llu allows (%llu)",
+                    (unsigned long long)chunk, (unsigned long long)h->cand_cap, (unsigned long long)max_chunk);
+    for (uint32_t q = 0; q < nq; q++) {
+        memset(&out[q], 0, sizeof(sw_selection));
+        out[q].status = SW_EMPTY;
+    }
+    uint64_t dsum = 0;
+    sw_selection tmp[SW_MAX_QUERIES];
+    for (uint64_t c0 = begin; c0 < end;) {
+        const uint64_t c1 = end - c0 > chunk ? c0 + chunk : end;
+        sw_status st = sw_plan_eval(h, c0, c1);
+        if (st < 0) return st;
+        if (nq) {
+            st = sw_plan_select_batch(h, nq, qs, tmp);  // also folds the chunk into the front
+            if (st < 0) return st;
+            for (uint32_t q = 0; q < nq; q++) sw_selection_merge(h->h.flags & 4u ? 1u : 0u, &qs[q], &out[q], &tmp[q], &out[q]);
+        }
+        if (digest) {
+            uint64_t d = 0;
+            st = sw_plan_digest(h, &d);
+            if (st < 0) return st;
+            dsum += d;
+        }
+        st = sw_plan_release_records(h);  // folds whatever is still pending, drops the records
+        if (st < 0) return st;
+        c0 = c1;
+    }
+    if (digest) *digest = dsum;
+    sw_status worst = SW_OK;
+    for (uint32_t q = 0; q < nq; q++) worst = std::max<sw_status>(worst, out[q].status);
+    return worst;
+}
+
 // ============================================================================ digest
 extern "C" sw_status sw_plan_digest(sw_plan* h, uint64_t* digest) {
     if (!h || !digest) return fail(nullptr, SW_EINVAL, "null argument");
@@ -1030,6 +1076,53 @@ extern "C" sw_status sw_plan_copy_records(sw_plan* h, uint64_t index, uint64_t n
         }
     }
     return fail(h, SW_EINVAL, "range not inside one local segment");
+}
+
+// ============================================================================ host helpers
+extern "C" sw_status sw_space_shape(const sw_profile_tables* tb, uint64_t* n, uint64_t* row) {
+    if (!tb || !n || !row || !tb->radix) return fail(nullptr, SW_EINVAL, "null argument");
+    const uint32_t B = tb->n_digits;
+    if (B < 1 || B > SW_MAX_DIGITS) return fail(nullptr, SW_EINVAL, "n_digits %u not in 1..%d", B, SW_MAX_DIGITS);
+    uint64_t N = 1;
+    for (uint32_t b = 0; b < B; b++) {
+        const uint32_t r = tb->radix[b];
+        if (r < 1 || r > SW_MAX_CHOICES) return fail(nullptr, SW_EINVAL, "radix[%u] = %u not in 1..%d", b, r, SW_MAX_CHOICES);
+        if ((u128)N * r >= ((u128)1 << 63)) return fail(nullptr, SW_ERANGE, "plan space >= 2^63 (InstanceTooLarge)");
+        N *= r;
+    }
+    // digits left-padded with radix 1 to B >= 3: the row is the last two digits
+    *row = B == 1 ? (uint64_t)tb->radix[0] : (uint64_t)tb->radix[B - 2] * tb->radix[B - 1];
+    *n = N;
+    return SW_OK;
+}
+
+static Rec4 rec4_of(const sw_record& r) {
+    Rec4 x;
+    x.w0 = r.ttff_us;
+    x.w1 = r.stall_us;
+    x.w2 = r.cost_mc;
+    x.w3 = (uint64_t)r.quality | ((uint64_t)r.stall_count << 32) | ((uint64_t)r.flags << 48);
+    return x;
+}
+
+extern "C" sw_status sw_selection_merge(uint32_t objective, const sw_query* q, const sw_selection* a,
+                                        const sw_selection* b, sw_selection* out) {
+    if (!q || !a || !b || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (objective > 1) return fail(nullptr, SW_EINVAL, "bad objective %u", objective);
+    for (const sw_selection* s : {a, b})
+        if (s->status != SW_OK && s->status != SW_CLOSEST && s->status != SW_EMPTY)
+            return fail(nullptr, SW_EINVAL, "selection status %d is not OK/CLOSEST/EMPTY", s->status);
+    const QueryDev qd{q->slo_startup_us, q->slo_stall_us, q->budget_mc};
+    const uint64_t ia = a->status == SW_EMPTY ? kInf64 : a->index;
+    const uint64_t ib = b->status == SW_EMPTY ? kInf64 : b->index;
+    const Rec4 ra = rec4_of(a->rec), rb = rec4_of(b->rec);
+    // same total order as the scan / merge kernels (cand_better is __host__ __device__)
+    const bool take_b = cand_better(qd, objective, ib, rb, ia, ra);
+    const sw_selection w = take_b ? *b : *a;
+    *out = w;
+    if ((take_b ? ib : ia) == kInf64) out->status = SW_EMPTY;
+    else out->status = feasible(qd, take_b ? rb : ra) ? SW_OK : SW_CLOSEST;
+    return out->status;
 }
 
 // ============================================================================ NCCL

@@ -28,6 +28,15 @@ sys.path.insert(0, ROOT)
 METRIC = "plan candidates evaluated/sec (1/2/4/8 B200) and % HBM roofline vs CPU oracle"
 UNIT = "candidates/s"
 REC_BYTES = 32  # algorithmic HBM bytes per candidate of the eval kernel (the record)
+WORKLOADS = {
+    "C1": "C1: 1-minute podcast, 4 scenes, MED/HIGH, A100x2, k{1,2}: 256 plans (BASELINE configs[0])",
+    "C2": "C2: 10-minute podcast, one 8xA100-profile server, 20 scenes, 3 levels x k{1,2,4,8}, "
+          "12^8 plans (BASELINE configs[1])",
+    "C3": "C3: 10-minute podcast, A100x8+H100x8, static intro, early low-res ladder, 24^6 plans "
+          "(BASELINE configs[2])",
+    "C5": "C5: 30-minute podcast, 60 scenes, 4 levels x A100/H100/H200, 48^6 = 1.2e10 plans, "
+          "chunked when records exceed HBM (BASELINE configs[4])",
+}
 
 
 def peaks():
@@ -47,10 +56,12 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms; stop() keeps the samples
+    taken inside [t0, t1] (the timed region, wall clock)."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device):
         self.device = device
@@ -64,14 +75,15 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
-    def stop(self):
+    def stop(self, t0, t1):
         if not self.proc:
             return None
+        time.sleep(0.2)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -81,22 +93,36 @@ class ClockSampler:
         rows = []
         for line in open(self.path):
             p = [x.strip() for x in line.split(",")]
-            if len(p) >= 9:
-                rows.append(p)
+            if len(p) < 10:
+                continue
+            try:
+                ts = time.mktime(time.strptime(p[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                ts += float("0." + p[0].split(".")[1]) if "." in p[0] else 0.0
+            except Exception:
+                continue
+            rows.append((ts, p))
         os.unlink(self.path)
-        if not rows:
+        inside = [p for ts, p in rows if t0 - 0.06 <= ts <= t1 + 0.06]
+        if not inside:  # very short timed region: nearest samples
+            inside = [p for ts, p in sorted(rows, key=lambda x: abs(x[0] - (t0 + t1) / 2))[:2]]
+        if not inside:
             return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[2]) for r in inside) if v is not None]
+        mx = [v for v in (num(r[3]) for r in inside) if v is not None]
         reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for n, v in zip(names, r[5:9]):
+        for r in inside:
+            for n, v in zip(self.NAMES, r[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(rows)}
+                "samples": len(inside), "samples_total": len(rows)}
 
 
 def cpu_baseline(pb, queries, target_s=15.0):
@@ -161,8 +187,8 @@ def input_bytes(pb):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -189,18 +215,24 @@ def main():
         comm = sw.comm_init(obj[0], rank, world, dev)
 
     stream = torch.cuda.Stream(device=dev)
-    plan = sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world)
-    N = plan.n
+    N = sw.space_shape(pb)[0]
+    # records retained per rank: this rank's share, or as many as 75% of free HBM holds
+    # (C5: 391 GB of records -> chunked sweep)
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    n_max, row = sw.space_shape(pb)
+    need = N // world + 3 * row  # the library's default: this rank's largest shard
+    cap = 0 if need * REC_BYTES < 0.75 * free_b else int(0.75 * free_b) // REC_BYTES
+    plan = sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world,
+                   record_capacity=cap)
 
-    def step():
-        plan.reset()
-        plan.eval(0, N)
-        sels = plan.select_batch(pb.queries)
-        front = plan.pareto()
+    def step(p):
+        p.reset()
+        sels, _ = p.sweep(0, N, pb.queries)  # eval (chunked if needed) + select + fold
+        front = p.pareto()
         return sels, front
 
     for _ in range(args.warmup):
-        step()
+        step(plan)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -209,61 +241,76 @@ def main():
         torch.cuda.synchronize(dev)
 
     clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)  # let nvidia-smi start sampling
     barrier()
     l0 = plan.launch_count()
-    clocks.start()
+    k0 = [plan.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
     ev0.record(stream)
-    eval_ms = []
     for _ in range(args.steps):
-        sels, front = step()
-        eval_ms.append(plan.last_eval_ms())
+        sels, front = step(plan)
     ev1.record(stream)
     ev1.synchronize()
+    w1 = time.time()
     barrier()
-    ck = clocks.stop()
+    ck = clocks.stop(w0, w1)
     launches = plan.launch_count() - l0
+    k1 = [plan.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms, max(eval_ms)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, emax = float(t[0]), float(t[1])
-    else:
-        emax = max(eval_ms)
+        ms = float(t[0])
     ms_per_step = ms / args.steps
     value = N / (ms_per_step / 1e3)
 
-    # roofline of the dominant kernel (eval): algorithmic bytes = 32 B x records/launch
-    local_n = sw.shard_range(0, N, plan.row, rank, world)
-    local_n = local_n[1] - local_n[0]
-    eval_avg_ms = sum(eval_ms) / len(eval_ms)
-    achieved = REC_BYTES * local_n / (eval_avg_ms / 1e3) / 1e9
+    # roofline per kernel: ALGORITHMIC bytes per launch (32 B x records written by eval /
+    # read by the fused select+Pareto scan) over the launch's CUDA-event time on the
+    # handle's stream, averaged over the launches of the timed region; the dominant
+    # kernel (largest share of the step) is the line's "roofline"
     peak, peak_kind = peaks()
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "eval_traffic.json")
+    traffic = {}
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("config") == args.config and pj.get("n_local") == local_n:
-                traffic = pj.get("dram_bytes_per_launch")
+            if pj.get("config") == args.config:
+                # per kernel: DRAM bytes / algorithmic bytes of the captured launch
+                traffic = {k: v["dram_bytes"] / v["algorithmic_bytes"]
+                           for k, v in pj.get("kernels", {}).items()}
         except Exception:
             pass
-    roof = {"kernel": "eval_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
-            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-            "peak_source": peak_kind, "algorithmic_bytes_per_launch": REC_BYTES * local_n,
-            "eval_ms_per_launch": eval_avg_ms,
-            "eval_share_of_step": eval_avg_ms / ms_per_step}
+    kern = {}
+    for name, a0, a1 in zip(("eval_kernel", "scan_kernel"), k0, k1):
+        n_l, t_ms, by = a1[0] - a0[0], a1[1] - a0[1], a1[2] - a0[2]
+        if n_l == 0:
+            continue
+        avg_ms = t_ms / n_l
+        ach = by / n_l / (avg_ms / 1e3) / 1e9
+        kern[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                      "frac": ach / peak,
+                      "traffic": (traffic[name] * by / n_l) if name in traffic else None,
+                      "algorithmic_bytes_per_launch": by / n_l, "launches": n_l,
+                      "ms_per_launch": avg_ms, "share_of_step": t_ms / args.steps / ms_per_step}
+    dom = max(kern, key=lambda k: kern[k]["share_of_step"])
+    roof = dict(kern[dom])
+    roof["kernel"] = dom
+    roof["peak_source"] = peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    roof["kernels"] = kern
 
     # parity check of the timed configuration (outside the timed region)
     parity = None
     gpath = os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % args.config)
     if os.path.exists(gpath):
         g = json.load(open(gpath))
-        dg = plan.digest()
+        plan.reset()
+        sels_p, dg = plan.sweep(0, N, pb.queries, digest=True)
         ok_w = all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
-                   for s, w in zip(sels, g["winners"]))
-        ok_f = front == [tuple(p) for p in g["front"]]
+                   for s, w in zip(sels_p, g["winners"]))
+        ok_f = plan.pareto() == [tuple(p) for p in g["front"]]
         parity = {"digest": dg == int(g["digest"]), "winners": ok_w, "pareto": ok_f}
 
     # e2e: public API from HOST buffers each step (create uploads the tables, results
@@ -274,10 +321,8 @@ def main():
     d2h = 0
     for _ in range(args.e2e_steps):
         with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank,
-                     nranks=world) as p2:
-            p2.eval(0, N)
-            s2 = p2.select_batch(pb.queries)
-            f2 = p2.pareto()
+                     nranks=world, record_capacity=cap) as p2:
+            s2, f2 = step(p2)
             d2h = 112 * len(s2) + 32 * len(f2)
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
@@ -294,11 +339,10 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "%s: 10-minute podcast, one 8xA100-profile server, 20 scenes, "
-                                   "3 levels x k{1,2,4,8}, 12^8 plans (BASELINE configs[1])" % args.config
-                       if args.config == "C2" else args.config,
+            "config": {"workload": WORKLOADS.get(args.config, args.config),
                        "n_candidates": N, "queries": len(pb.queries),
                        "l2": "records %.1f GB >> 126 MB L2 (no flush needed)" % (N * 32 / 1e9),
+                       "record_capacity_per_rank": cap,
                        "parallelism": "candidate-shard x%d, NCCL allgather merge" % world},
             "roofline": roof,
             "cpu_baseline": cpu,

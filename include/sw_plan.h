@@ -262,6 +262,38 @@ sw_status sw_space_shape(const sw_profile_tables *tables, uint64_t *n, uint64_t 
 sw_status sw_selection_merge(uint32_t objective, const sw_query *q, const sw_selection *a,
                              const sw_selection *b, sw_selection *out);
 
+/* ---- fleet batch (BASELINE configs[3], C4) -------------------------------- */
+
+/* A batch of independent requests (e.g. 256 podcasts of 5-15 min, each with its own SLO
+ * and budget) evaluated and selected together: sw_fleet_eval is ONE kernel launch over
+ * every request's whole plan space (each request's records in its own handle),
+ * sw_fleet_select ONE scan launch with one query per request, a merge kernel, a batched
+ * winner-detail kernel and, with nranks > 1, ONE allgather of the n winners (every
+ * request's space is sharded over the ranks like sw_plan_eval).  Each request keeps a
+ * full sw_plan handle (sw_fleet_plan: Pareto front, digest, records, detail), owned by
+ * the fleet.  Arrays of sw_fleet_create have n entries (host, deep-copied); the runtime
+ * is shared (record_capacity applies per request). */
+typedef struct sw_fleet sw_fleet;
+#define SW_MAX_FLEET 4096
+sw_status sw_fleet_create(uint32_t n, const sw_profile_tables *tables, const sw_scene_list *scenes,
+                          const sw_price_table *prices, const sw_runtime *rt, sw_fleet **out);
+sw_status sw_fleet_destroy(sw_fleet *f);
+sw_status sw_fleet_size(const sw_fleet *f, uint32_t *n);
+/* Borrowed handle of request i (valid until sw_fleet_destroy; do not destroy it). */
+sw_status sw_fleet_plan(sw_fleet *f, uint32_t i, sw_plan **out);
+/* Evaluate every request's whole space (this rank's shard of each); asynchronous.
+ * Handles must hold no records (fresh or sw_fleet_reset) -- else SW_ESTATE. */
+sw_status sw_fleet_eval(sw_fleet *f);
+/* queries[i] selects request i's winner into out[i] (status per request as in
+ * sw_plan_select).  Collective when nranks > 1; synchronises; returns the worst soft
+ * status.  The Pareto fronts are folded lazily by sw_pareto_get on sw_fleet_plan(i). */
+sw_status sw_fleet_select(sw_fleet *f, const sw_query *queries, sw_selection *out);
+sw_status sw_fleet_reset(sw_fleet *f);
+/* As sw_plan_kernel_time, for the fleet-wide launches. */
+sw_status sw_fleet_kernel_time(sw_fleet *f, uint32_t kind, uint64_t *n_launches, double *total_ms,
+                               uint64_t *bytes);
+uint64_t sw_fleet_launch_count(const sw_fleet *f);
+
 /* ---- multi-GPU --------------------------------------------- */
 
 /* Row-aligned contiguous shard of [begin, end) for `rank` of `nranks`: whole rows
@@ -287,6 +319,13 @@ uint64_t sw_plan_launch_count(const sw_plan *h);
 /* Per-launch eval-kernel time of the last sw_plan_eval on this rank (CUDA events
  * recorded on the handle's stream around the eval kernel), milliseconds. */
 sw_status sw_plan_last_eval_ms(sw_plan *h, float *ms);
+/* Launch statistics of one kernel kind since create: launches, their summed
+ * CUDA-event time (ms; events recorded on the handle's stream around each launch) and
+ * their ALGORITHMIC bytes (32 B per record written by eval / read by a scan, tile
+ * padding included for scans).  Synchronises the last recorded launch. */
+enum { SW_KERNEL_EVAL = 0 /* eval_kernel: a1-a7 */, SW_KERNEL_SCAN = 1 /* scan_kernel: a8+a9 */ };
+sw_status sw_plan_kernel_time(sw_plan *h, uint32_t kind, uint64_t *n_launches, double *total_ms,
+                              uint64_t *bytes);
 int32_t sw_abi_version(void);
 
 #ifdef __cplusplus

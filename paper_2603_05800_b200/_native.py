@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_PKG, "libsw_plan.so")
 
 SW_OK, SW_CLOSEST, SW_TRUNCATED, SW_EMPTY = 0, 1, 2, 3
 SW_EINVAL, SW_ERANGE, SW_ENOMEM, SW_ECUDA, SW_ENCCL, SW_ESTATE = -1, -2, -3, -4, -5, -6
+SW_KERNEL_EVAL, SW_KERNEL_SCAN = 0, 1
 SW_MAX_SCENES, SW_MAX_DIGITS, SW_MAX_CHOICES = 64, 16, 64
 SW_MAX_POOLS, SW_MAX_GPUS_PER_POOL, SW_MAX_QUERIES = 4, 8, 8
 UINT64_MAX = (1 << 64) - 1
@@ -106,6 +107,17 @@ EXPORTS = {
     "sw_space_shape": (C.c_int32, [C.POINTER(sw_profile_tables), U64P, U64P]),
     "sw_selection_merge": (C.c_int32, [C.c_uint32, C.POINTER(sw_query), C.POINTER(sw_selection),
                                        C.POINTER(sw_selection), C.POINTER(sw_selection)]),
+    "sw_fleet_create": (C.c_int32, [C.c_uint32, C.POINTER(sw_profile_tables), C.POINTER(sw_scene_list),
+                                    C.POINTER(sw_price_table), C.POINTER(sw_runtime),
+                                    C.POINTER(C.c_void_p)]),
+    "sw_fleet_destroy": (C.c_int32, [C.c_void_p]),
+    "sw_fleet_size": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "sw_fleet_plan": (C.c_int32, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "sw_fleet_eval": (C.c_int32, [C.c_void_p]),
+    "sw_fleet_select": (C.c_int32, [C.c_void_p, C.POINTER(sw_query), C.POINTER(sw_selection)]),
+    "sw_fleet_reset": (C.c_int32, [C.c_void_p]),
+    "sw_fleet_kernel_time": (C.c_int32, [C.c_void_p, C.c_uint32, U64P, C.POINTER(C.c_double), U64P]),
+    "sw_fleet_launch_count": (C.c_uint64, [C.c_void_p]),
     "sw_shard_range": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32,
                                    U64P, U64P]),
     "sw_plan_row_size": (C.c_int32, [C.c_void_p, U64P]),
@@ -117,6 +129,7 @@ EXPORTS = {
     "sw_last_error": (C.c_char_p, [C.c_void_p]),
     "sw_plan_launch_count": (C.c_uint64, [C.c_void_p]),
     "sw_plan_last_eval_ms": (C.c_int32, [C.c_void_p, C.POINTER(C.c_float)]),
+    "sw_plan_kernel_time": (C.c_int32, [C.c_void_p, C.c_uint32, U64P, C.POINTER(C.c_double), U64P]),
     "sw_abi_version": (C.c_int32, []),
 }
 
@@ -235,6 +248,21 @@ def _arr(t, vals):
     return (t * max(1, len(vals)))(*vals)
 
 
+def _marshal(pb, keep):
+    """ctypes images of a problem's scene list, profile tables and price table."""
+    sc = sw_scene_list(pb.S, _arr(C.c_uint64, pb.dur_us), _arr(C.c_uint64, pb.llm_us),
+                       _arr(C.c_uint64, pb.tts_us), pb.overhead_us, pb.scene0_static,
+                       pb.static_ready_us)
+    chs = (sw_choice * len(pb.choices))(*[sw_choice(l, kk, p, 0) for (l, kk, p) in pb.choices])
+    tb = sw_profile_tables(len(pb.radix), _arr(C.c_uint32, pb.radix),
+                           _arr(C.c_uint32, pb.first_scene), chs, _arr(C.c_uint64, pb.va_us),
+                           len(pb.level_score), _arr(C.c_uint32, pb.level_score), pb.heads)
+    pr = sw_price_table(len(pb.gpus), _arr(C.c_uint32, pb.gpus), _arr(C.c_uint64, pb.price_mc),
+                        pb.fixed_cost_mc, pb.billing, pb.objective)
+    keep.append((sc, chs, tb, pr))
+    return sc, tb, pr
+
+
 class Plan:
     """One request's plan space on one rank (wraps an sw_plan handle).
 
@@ -250,27 +278,23 @@ class Plan:
         L = lib()
         pb = problem
         self._keep = []
-        k = self._keep.append
-        self.n_pools = len(pb.gpus)
-        self.B = len(pb.radix)
-        self.S = pb.S
-        sc = sw_scene_list(pb.S, _arr(C.c_uint64, pb.dur_us), _arr(C.c_uint64, pb.llm_us),
-                           _arr(C.c_uint64, pb.tts_us), pb.overhead_us, pb.scene0_static,
-                           pb.static_ready_us)
-        chs = (sw_choice * len(pb.choices))(*[sw_choice(l, kk, p, 0) for (l, kk, p) in pb.choices])
-        tb = sw_profile_tables(len(pb.radix), _arr(C.c_uint32, pb.radix),
-                               _arr(C.c_uint32, pb.first_scene), chs, _arr(C.c_uint64, pb.va_us),
-                               len(pb.level_score), _arr(C.c_uint32, pb.level_score), pb.heads)
-        pr = sw_price_table(len(pb.gpus), _arr(C.c_uint32, pb.gpus), _arr(C.c_uint64, pb.price_mc),
-                            pb.fixed_cost_mc, pb.billing, pb.objective)
+        sc, tb, pr = _marshal(pb, self._keep)
         rt = sw_runtime(device, C.c_void_p(stream or 0), C.c_void_p(comm or 0), rank, nranks,
                         record_capacity, ALLOC_FN(0), FREE_FN(0), None)
-        k((sc, chs, tb, pr, rt))
+        self._keep.append(rt)
         h = C.c_void_p()
         st = L.sw_plan_create(C.byref(tb), C.byref(sc), C.byref(pr), C.byref(rt), C.byref(h))
         if st < 0:
             raise SwError(st, L.sw_last_error(None).decode(errors="replace"))
+        self._adopt(h, pb, owned=True)
+
+    def _adopt(self, h, pb, owned: bool):
+        L = lib()
         self.h = h
+        self._owned = owned
+        self.n_pools = len(pb.gpus)
+        self.B = len(pb.radix)
+        self.S = pb.S
         n = C.c_uint64()
         L.sw_plan_space_size(h, C.byref(n))
         self.n = n.value
@@ -278,10 +302,19 @@ class Plan:
         L.sw_plan_row_size(h, C.byref(r))
         self.row = r.value
 
+    @classmethod
+    def borrowed(cls, h, pb) -> "Plan":
+        """Wrap a handle owned elsewhere (a fleet's request): close() does not destroy it."""
+        self = cls.__new__(cls)
+        self._keep = []
+        self._adopt(h, pb, owned=False)
+        return self
+
     # -- lifecycle
     def close(self):
         if getattr(self, "h", None):
-            lib().sw_plan_destroy(self.h)
+            if getattr(self, "_owned", True):
+                lib().sw_plan_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -374,7 +407,92 @@ class Plan:
     def launch_count(self) -> int:
         return lib().sw_plan_launch_count(self.h)
 
+    def kernel_time(self, kind: int):
+        """(launches, summed CUDA-event ms, algorithmic bytes) of one kernel kind since
+        create: SW_KERNEL_EVAL or SW_KERNEL_SCAN (sw_plan_kernel_time)."""
+        n, ms, by = C.c_uint64(), C.c_double(), C.c_uint64()
+        self._ck(lib().sw_plan_kernel_time(self.h, kind, C.byref(n), C.byref(ms), C.byref(by)))
+        return n.value, ms.value, by.value
+
     def last_eval_ms(self) -> float:
         ms = C.c_float()
         self._ck(lib().sw_plan_last_eval_ms(self.h, C.byref(ms)))
         return ms.value
+
+
+class Fleet:
+    """A batch of requests evaluated and selected together (sw_fleet_*): one eval launch
+    for every request's space, one select scan with one query per request."""
+
+    def __init__(self, problems, device: int = 0, stream: Optional[int] = None,
+                 comm: Optional[int] = None, rank: int = 0, nranks: int = 1,
+                 record_capacity: int = 0):
+        L = lib()
+        self.problems = list(problems)
+        n = len(self.problems)
+        self._keep = []
+        imgs = [_marshal(pb, self._keep) for pb in self.problems]
+        scs = (sw_scene_list * n)(*[i[0] for i in imgs])
+        tbs = (sw_profile_tables * n)(*[i[1] for i in imgs])
+        prs = (sw_price_table * n)(*[i[2] for i in imgs])
+        rt = sw_runtime(device, C.c_void_p(stream or 0), C.c_void_p(comm or 0), rank, nranks,
+                        record_capacity, ALLOC_FN(0), FREE_FN(0), None)
+        self._keep.append((scs, tbs, prs, rt))
+        h = C.c_void_p()
+        st = L.sw_fleet_create(n, tbs, scs, prs, C.byref(rt), C.byref(h))
+        if st < 0:
+            raise SwError(st, L.sw_last_error(None).decode(errors="replace"))
+        self.h = h
+        self.n = n
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sw_fleet_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _ck(self, st):
+        if st < 0:
+            raise SwError(st, lib().sw_last_error(None).decode(errors="replace"))
+        return st
+
+    def plan(self, i: int) -> Plan:
+        p = C.c_void_p()
+        self._ck(lib().sw_fleet_plan(self.h, i, C.byref(p)))
+        return Plan.borrowed(p, self.problems[i])
+
+    def eval(self):
+        self._ck(lib().sw_fleet_eval(self.h))
+
+    def reset(self):
+        self._ck(lib().sw_fleet_reset(self.h))
+
+    def select(self, queries: Sequence) -> List[Selection]:
+        """queries[i] for request i (objects with slo_startup_us / slo_stall_us /
+        budget_mc, or 3-tuples)."""
+        qs = [q if isinstance(q, tuple) else (q.slo_startup_us, q.slo_stall_us, q.budget_mc)
+              for q in queries]
+        assert len(qs) == self.n
+        arr = (sw_query * self.n)(*[sw_query(*q) for q in qs])
+        out = (sw_selection * self.n)()
+        self._ck(lib().sw_fleet_select(self.h, arr, out))
+        return [_sel(o, len(pb.gpus), len(pb.radix)) for o, pb in zip(out, self.problems)]
+
+    def kernel_time(self, kind: int):
+        n, ms, by = C.c_uint64(), C.c_double(), C.c_uint64()
+        self._ck(lib().sw_fleet_kernel_time(self.h, kind, C.byref(n), C.byref(ms), C.byref(by)))
+        return n.value, ms.value, by.value
+
+    def launch_count(self) -> int:
+        return lib().sw_fleet_launch_count(self.h)

@@ -265,6 +265,11 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src_gme
         : "memory");
 }
 
+// Bulk prefetch of [src, src + bytes) into L2 (no completion tracking; bytes % 16 == 0).
+__device__ __forceinline__ void tma_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     uint32_t done = 0;
     do {

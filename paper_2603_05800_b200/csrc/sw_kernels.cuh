@@ -34,7 +34,8 @@ struct SegView {
 constexpr int kScanThreads = 256;
 constexpr int kDltT = 128;  // dominance lookup table: ttff_eff bins (front quantiles)
 constexpr int kDltQ = 128;  //                         quality bins (front quantiles)
-constexpr int kDltMap = 1024;  // coarse direct maps (t: 64 cells per octave; q: linear)
+constexpr int kDltMap = 4096;  // direct maps (t: 256 cells per octave over 16 octaves; q: linear)
+constexpr int kDltTShift = 15; // t cell key = float bits >> 15 (8 mantissa bits)
 
 // ============================================================================ a2 + packing
 struct RawDesc {
@@ -202,15 +203,27 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2
 // (k, pool) is warp-uniform there, so the gang update uses compile-time slot indices
 // and the LSD step (the dominant loop) is ~40 integer ops + one 32 B store.
 // Amortised scene-steps per candidate: L_LSD + L_MID / r_LSD + L_HI / row.
+// One eval launch's work for one request: its tables and the tile range to write.
+struct EvalJob {
+    const DevHeader* hdr;
+    const VaEntry* va;
+    uint64_t va_bytes;
+    uint64_t tile_begin, tile_end;
+    Rec4* out;
+};
+
+// jobs == nullptr: one request (job); else request blockIdx.y of a fleet (jobs[y]), each
+// CTA staging its own request's tables -- a whole fleet in one launch.
 template <int NP>
-__global__ void __launch_bounds__(kEvalThreads) eval_kernel(
-    const DevHeader* __restrict__ g_hdr, const VaEntry* __restrict__ g_va, uint32_t va_bytes,
-    uint64_t tile_begin, uint64_t tile_end, Rec4* __restrict__ out) {
+__global__ void __launch_bounds__(kEvalThreads) eval_kernel(EvalJob job, const EvalJob* __restrict__ jobs) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bar;
+    if (jobs) job = jobs[blockIdx.y];
+    const uint64_t tile_begin = job.tile_begin, tile_end = job.tile_end;
+    Rec4* __restrict__ out = job.out;
     DevHeader& h = *reinterpret_cast<DevHeader*>(smem);
     VaEntry* va = reinterpret_cast<VaEntry*>(smem + sizeof(DevHeader));
-    stage_tables(g_hdr, g_va, &h, va, va_bytes, &bar);
+    stage_tables(job.hdr, job.va, &h, va, (uint32_t)job.va_bytes, &bar);
 
     const uint32_t bm = h.B - 2, bl = h.B - 1;
     const uint32_t rm = h.radix[bm], rl = h.radix[bl];
@@ -302,9 +315,8 @@ struct DetailOut {
 };
 
 template <int NP>
-__global__ void detail_kernel(const DevHeader* __restrict__ g_hdr, const VaEntry* __restrict__ g_va,
-                              uint64_t index, DetailOut* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void detail_one(const DevHeader* __restrict__ g_hdr, const VaEntry* __restrict__ g_va, uint64_t index,
+                           DetailOut* __restrict__ out) {
     const DevHeader& h = *g_hdr;
     State<NP> st;
     state_init(st, h);
@@ -337,6 +349,13 @@ __global__ void detail_kernel(const DevHeader* __restrict__ g_hdr, const VaEntry
     out->rec.w3 = (uint64_t)st.Q | ((uint64_t)st.cnt << 32) | ((uint64_t)st.used << 48);
     out->ttff_eff = (uint64_t)st.M;
     out->makespan = mk;
+}
+
+template <int NP>
+__global__ void detail_kernel(const DevHeader* __restrict__ g_hdr, const VaEntry* __restrict__ g_va,
+                              uint64_t index, DetailOut* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    detail_one<NP>(g_hdr, g_va, index, out);
 }
 
 // ============================================================================ a9 select
@@ -616,37 +635,36 @@ __global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint*
 // f.q >= qedge[j+1] - 1, as u32 (0xffffffff = none / too big).  A record (t, c, q) in
 // cell (b, j) with cell < c is strictly dominated by a real candidate (f.t <= t,
 // f.q >= q, f.c < c), so it cannot be on the front.
-// Lookup is O(1): a coarse direct map (t: float exponent + 6 mantissa bits, q: linear)
-// gives a conservative bin, refined by at most two edge comparisons.
+// Lookup is O(1) with no refinement: direct maps from a fine cell of t (float exponent +
+// 8 mantissa bits, 256 cells per octave) and of q (linear) to a CONSERVATIVE bin: the t
+// bin of the cell's lower end (tedge[b] <= lower end <= t) and the q bin of the cell's
+// upper end (q <= upper end), so cell[b][j] only counts points that dominate the record.
 struct Dlt {
-    int32_t kbase;         // coarse t key of tmap[0]
+    int32_t kbase;         // t key of tmap[0]
     uint32_t qmin, qmax, qshift;
     uint64_t tedge[kDltT];
     uint32_t qedge[kDltQ + 1];
     uint32_t pad_[3];
-    uint8_t tmap[kDltMap];  // #edges <= lower end of coarse t cell (0..kDltT)
-    uint8_t qmap[kDltMap];  // bin containing the upper end of coarse q cell
+    uint8_t tmap[kDltMap];  // #edges <= lower end of t cell k (0..kDltT)
+    uint8_t qmap[kDltMap];  // bin containing the upper end of q cell k
     uint32_t cell[kDltT * kDltQ];
 };
 static_assert(sizeof(Dlt) % 16 == 0, "Dlt is staged in 16 B vectors");
 
-__device__ __forceinline__ int32_t dlt_tkey(uint64_t t) { return (int32_t)(__float_as_uint(__ull2float_rz(t)) >> 17); }
+__device__ __forceinline__ int32_t dlt_tkey(uint64_t t) {
+    return (int32_t)(__float_as_uint(__ull2float_rz(t)) >> kDltTShift);
+}
 
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, uint64_t t, uint64_t c, uint32_t q) {
-    int32_t k = dlt_tkey(t) - d.kbase;
-    if (k < 0 || q > d.qmax) return false;
-    k = k < kDltMap ? k : kDltMap - 1;
-    int b = (int)d.tmap[k] - 1;
-    if (b + 1 < kDltT && d.tedge[b + 1] <= t) b++;
-    if (b + 1 < kDltT && d.tedge[b + 1] <= t) b++;
-    if (b < 0) return false;
-    uint32_t qc = q < d.qmin ? 0u : (q - d.qmin) >> d.qshift;
-    qc = qc < (uint32_t)kDltMap ? qc : kDltMap - 1;
-    int j = d.qmap[qc];
-    if (j > 0 && d.qedge[j] > q) j--;
-    if (j > 0 && d.qedge[j] > q) j--;
-    const uint32_t cell = d.cell[b * kDltQ + j];
-    return cell != 0xffffffffu && (uint64_t)cell < c;
+    // branch-free: clamp both cell coordinates, look the two maps up independently,
+    // then predicate away the out-of-range cases
+    const int32_t k = dlt_tkey(t) - d.kbase;
+    const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
+    const uint32_t qc = min((max(q, d.qmin) - d.qmin) >> d.qshift, (uint32_t)kDltMap - 1);
+    const uint32_t b1 = d.tmap[kc];  // t bin + 1 (0: no front point has t <= this t)
+    const uint32_t j = d.qmap[qc];
+    const uint32_t cell = d.cell[(max(b1, 1u) - 1) * kDltQ + j];
+    return (k >= 0) & (q <= d.qmax) & (b1 != 0) & (cell != 0xffffffffu) & ((uint64_t)cell < c);
 }
 
 // Header pass (1 block of 1024): edges, coarse maps.
@@ -690,12 +708,18 @@ __global__ void __launch_bounds__(1024) dlt_head_kernel(const PPoint* __restrict
         d->qshift = sh;
         d->kbase = m ? dlt_tkey(front[0].t) : 0x7fffffff;
     }
-    for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x)
-        d->tedge[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
-    for (uint32_t j = threadIdx.x; j <= kDltQ; j += blockDim.x)
-        d->qedge[j] = !m ? 0xffffffffu : (j == kDltQ ? qmax + 1 : (j == 0 ? qmin : qs[((uint64_t)j * ms) / kDltQ]));
+    __shared__ uint64_t te[kDltT];
+    __shared__ uint32_t qe[kDltQ + 1];
+    for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x) {
+        te[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
+        d->tedge[i] = te[i];
+    }
+    for (uint32_t j = threadIdx.x; j <= kDltQ; j += blockDim.x) {
+        qe[j] = !m ? 0xffffffffu : (j == kDltQ ? qmax + 1 : (j == 0 ? qmin : qs[((uint64_t)j * ms) / kDltQ]));
+        d->qedge[j] = qe[j];
+    }
     __syncthreads();
-    // coarse maps
+    // direct maps (edges ascending: binary searches over the smem copies)
     const int32_t kbase = m ? dlt_tkey(front[0].t) : 0;
     uint32_t qsh = 0;
     {
@@ -703,18 +727,27 @@ __global__ void __launch_bounds__(1024) dlt_head_kernel(const PPoint* __restrict
         while (((range - 1) >> qsh) >= (uint64_t)kDltMap) qsh++;
     }
     for (uint32_t k = threadIdx.x; k < kDltMap; k += blockDim.x) {
-        // lower end of coarse t cell k: smallest integer t with key(t) >= kbase + k
+        // lower end of t cell k: smallest integer t with key(t) >= kbase + k
         const int32_t key = kbase + (int32_t)k;
-        const uint64_t L = (!m || key >= (0x7f8 << 3)) ? kInf64 : (uint64_t)ceilf(__uint_as_float((uint32_t)key << 17));
-        uint32_t cntle = 0;
-        for (uint32_t b = 0; b < kDltT; b++) cntle += d->tedge[b] <= L ? 1u : 0u;
-        d->tmap[k] = (uint8_t)(m ? cntle : 0);
-        // upper end of coarse q cell k
+        const uint64_t L = (!m || key >= (0x7f800000 >> kDltTShift)) ? kInf64
+                                                                     : (uint64_t)ceilf(__uint_as_float((uint32_t)key << kDltTShift));
+        uint32_t lo = 0, hi = kDltT;  // #edges <= L
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (te[mid] <= L) lo = mid + 1;
+            else hi = mid;
+        }
+        d->tmap[k] = (uint8_t)(m ? lo : 0);
+        // upper end of q cell k -> the bin j with qe[j] <= U < qe[j + 1] (last bin: kDltQ-1)
         const uint64_t U64 = (uint64_t)qmin + (((uint64_t)k + 1) << qsh) - 1;
         const uint32_t U = U64 > qmax ? qmax : (uint32_t)U64;
-        uint32_t j = 0;
-        while (j + 1 < (uint32_t)kDltQ && d->qedge[j + 1] <= U) j++;
-        d->qmap[k] = (uint8_t)j;
+        uint32_t a2 = 1, b2 = kDltQ;  // #edges qe[1..kDltQ-1] <= U
+        while (a2 < b2) {
+            const uint32_t mid = (a2 + b2) >> 1;
+            if (qe[mid] <= U) a2 = mid + 1;
+            else b2 = mid;
+        }
+        d->qmap[k] = (uint8_t)(a2 - 1);
     }
 }
 
@@ -797,23 +830,58 @@ __global__ void pareto_gather_kernel(const PPoint* __restrict__ padded, const ui
 // Block-local front: each CTA reduces a chunk of kLocal points in shared memory and
 // appends its non-dominated points.  front(A u B) = front(front(A) u front(B)), so a
 // global mark over the (much smaller) union stays exact.
+// BS = points per block: a first pass with small blocks spreads the O(BS^2) work of a
+// large survivor set over many SMs; a second pass with large blocks shrinks the rest.
 constexpr int kLocal = 1024;
-__global__ void __launch_bounds__(kLocal) pareto_local_kernel(const PPoint* __restrict__ pts,
-                                                              const uint32_t* __restrict__ d_m,
-                                                              PPoint* __restrict__ out,
-                                                              uint32_t* __restrict__ count) {
-    __shared__ PPoint sp[kLocal];
+constexpr int kLocalSmall = 256;
+template <int BS>
+__global__ void __launch_bounds__(BS) pareto_local_kernel(const PPoint* __restrict__ pts,
+                                                          const uint32_t* __restrict__ d_m,
+                                                          PPoint* __restrict__ out,
+                                                          uint32_t* __restrict__ count,
+                                                          uint8_t* __restrict__ keep_init) {
+    __shared__ PPoint sp[BS];
     const uint32_t m = *d_m;
-    const uint32_t base = blockIdx.x * kLocal;
+    const uint32_t base = blockIdx.x * BS;
     if (base >= m) return;
-    const uint32_t cnt = min((uint32_t)kLocal, m - base);
+    const uint32_t cnt = min((uint32_t)BS, m - base);
     if (threadIdx.x < cnt) sp[threadIdx.x] = pts[base + threadIdx.x];
     __syncthreads();
     if (threadIdx.x >= cnt) return;
     const PPoint p = sp[threadIdx.x];
     for (uint32_t j = 0; j < cnt; j++)
         if (j != threadIdx.x && pdom(sp[j], base + j, p, base + threadIdx.x)) return;
-    out[atomicAdd(count, 1u)] = p;
+    const uint32_t slot = atomicAdd(count, 1u);
+    out[slot] = p;
+    if (keep_init) keep_init[slot] = 1;
+}
+
+// keep[x] = 0 for every x of pts[0, m) dominated by another point.  The m x m dominance
+// tests are cut into 256 x 256 tiles dealt to a persistent grid, so even a few thousand
+// points spread over all SMs (keep[] must hold 1 for [0, m) on entry).
+__global__ void __launch_bounds__(kScanThreads) pareto_mark2d_kernel(const PPoint* __restrict__ pts,
+                                                                     const uint32_t* __restrict__ d_m,
+                                                                     uint8_t* __restrict__ keep) {
+    __shared__ PPoint tile[kScanThreads];
+    const uint32_t m = *d_m;
+    const uint32_t nb = (m + kScanThreads - 1) / kScanThreads;
+    const uint64_t items = (uint64_t)nb * nb;
+    for (uint64_t w = blockIdx.x; w < items; w += gridDim.x) {
+        const uint32_t xb = (uint32_t)(w / nb), yb = (uint32_t)(w - (uint64_t)xb * nb);
+        const uint32_t x = xb * kScanThreads + threadIdx.x;
+        const uint32_t y0 = yb * kScanThreads;
+        __syncthreads();
+        if (y0 + threadIdx.x < m) tile[threadIdx.x] = pts[y0 + threadIdx.x];
+        __syncthreads();
+        if (x >= m || !keep[x]) continue;  // already known dominated: skip the work
+        const PPoint px = pts[x];
+        const uint32_t lim = min((uint32_t)kScanThreads, m - y0);
+        for (uint32_t j = 0; j < lim; j++)
+            if (y0 + j != x && pdom(tile[j], y0 + j, px, x)) {
+                keep[x] = 0;
+                break;
+            }
+    }
 }
 
 // ============================================================================ fused scan
@@ -823,7 +891,7 @@ __global__ void __launch_bounds__(kLocal) pareto_local_kernel(const PPoint* __re
 // shared memory (32 per step, __any_sync early exit).  A record dominated by a real
 // candidate cannot be on the front, so the survivors always contain every true front
 // point of the segment whatever front subset is used: the later merge stays exact.
-constexpr uint32_t kFrontSmem = 1024;
+constexpr uint32_t kFrontSmem = 512;  // front points held in smem for the exact filter
 
 struct ParetoArgs {
     const Dlt* dlt;
@@ -859,40 +927,79 @@ __device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_
     return obj_strict_better(obj, a, b);
 }
 
-// TMA-pipelined scan: warp kCW (one elected lane) streams the segment through a
-// kStages-deep shared-memory ring with cp.async.bulk (completion on a "full" mbarrier
-// per stage); kCW consumer warps take one record per thread per stage from shared
-// memory and release the stage on an "empty" mbarrier.  Bytes in flight per SM are
-// set by the ring (kStages x 16 KB), not by registers or occupancy.
-constexpr int kCW = 16;                       // consumer warps per block
-constexpr int kScanBlock = (kCW + 1) * 32;    // + 1 producer warp
-constexpr uint32_t kStageRecs = kCW * 32;     // records per stage (16 KB)
-constexpr int kStages = 8;        // plain scans
-constexpr int kStagesPareto = 5;  // scans carrying the DLT + front subset in smem
+// TMA-pipelined scan: warp kCW (one elected lane) streams the segment's records (a flat
+// run of ntiles * 32 * row slots, tile padding included) through a kStages-deep
+// shared-memory ring with cp.async.bulk, 32 KB per stage, completion on a "full"
+// mbarrier per stage; stages are dealt round-robin to the blocks.  kCW consumer warps take
+// kRPT records per thread per stage from shared memory (independent chains: ILP) and
+// release the stage on an "empty" mbarrier.  Bytes in flight per SM are set by the ring.
+//
+// Select (a9) per record and query costs a few integer ops in the common case: the block
+// shares, per query, a threshold in shared memory -- the best quality of any FEASIBLE
+// record seen (QUALITY_FIRST) or a "feasible seen" flag (COST_X_TTFF).  A record of lower
+// quality (resp. an infeasible record once a feasible one exists) is strictly worse than
+// a record this block will report, so it is skipped; the full total-order comparison
+// (cand_better) runs only for the rare records that pass.
+constexpr int kCW = 16;                         // consumer warps per block
+constexpr int kScanBlock = (kCW + 1) * 32;      // + 1 producer warp
+constexpr int kGroups = 2;                      // consumer groups take alternate stages
+constexpr int kGW = kCW / kGroups;              // warps per group
+constexpr int kRPT = 4;                         // records per consumer thread per stage
+constexpr uint32_t kStageRecs = kGW * 32 * kRPT;  // records per stage (32 KB)
+// Little's law: ~45 GB/s per SM x ~1.5-2 us loaded latency => ~100 KB in flight per SM
+constexpr int kPrefetch = 6;      // stages per block prefetched into L2 ahead of the TMA copy
+constexpr int kStages = 6;        // plain scans (192 KB ring)
+constexpr int kStagesPareto = 4;  // scans carrying the DLT + front subset in smem (128 KB)
+static_assert(kStages % kGroups == 0 && kStagesPareto % kGroups == 0, "groups own fixed ring slots");
 __host__ __device__ constexpr size_t ring_bytes(bool pareto) {
     return (size_t)(pareto ? kStagesPareto : kStages) * kStageRecs * sizeof(Rec4);
 }
 
 struct StageMeta {
-    uint64_t t;
-    uint32_t pin0, cnt;  // cnt == 0: end of stream
-    uint32_t all_valid;  // every record of the stage lies in [ib, ie): skip per-record checks
-    uint32_t pad;
+    uint64_t pos0;       // flat slot of the stage's first record
+    uint32_t cnt;        // records in the stage; 0 = end of stream
+    uint32_t all_valid;  // no tile padding inside: skip per-record range checks
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Global index of flat slot P of a segment view (division only on rare paths).
+__device__ __forceinline__ uint64_t flat_index(const SegView& v, uint32_t per_tile, uint64_t P) {
+    const uint64_t t = P / per_tile;
+    return tiled_index(v.t0, v.row, t, (uint32_t)(P - t * per_tile));
+}
+
+// QUALITY_FIRST prefilter key: higher is better in (-Q, cost) order up to the cost clamp.
+__device__ __forceinline__ uint64_t qc_key(const Rec4& r) {
+    const uint32_t c32 = r.w2 > 0xffffffffull ? 0xffffffffu : (uint32_t)r.w2;
+    return ((uint64_t)rec_Q(r) << 32) | (uint64_t)(~c32);
+}
+
+// A fleet scan: request blockIdx.y scans its own records with its own queries.
+struct ScanJob {
+    SegView v;
+    SelParams P;
+};
+
 template <int NQ, bool PARETO>
 __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParams P, Cand* __restrict__ partial,
-                                                             ParetoArgs pa) {
+                                                             ParetoArgs pa, const ScanJob* __restrict__ jobs) {
+    if (jobs) {  // fleet: request y (never with PARETO)
+        v = jobs[blockIdx.y].v;
+        P = jobs[blockIdx.y].P;
+    }
+    const uint64_t out_block = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
     constexpr int NQA = NQ > 0 ? NQ : 1;
     extern __shared__ __align__(128) unsigned char fsm[];
     __shared__ Cand s_tmp[32];
     constexpr int NS = PARETO ? kStagesPareto : kStages;
     __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
     __shared__ StageMeta meta[NS];
+    // per query: packed key (Q << 32 | ~min(cost, 2^32-1)) of this block's best FEASIBLE
+    // record under QUALITY_FIRST (any nonzero value under COST_X_TTFF); 0 = none yet
+    __shared__ unsigned long long s_thr[NQA];
     Rec4* ring = reinterpret_cast<Rec4*>(fsm);
     Dlt& d = *reinterpret_cast<Dlt*>(fsm + ring_bytes(PARETO));
     PPoint* fs = reinterpret_cast<PPoint*>(fsm + ring_bytes(PARETO) + sizeof(Dlt));
@@ -900,12 +1007,14 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     if (threadIdx.x == 0) {
         for (int st = 0; st < NS; st++) {
             mbar_init(&full_bar[st], 1);
-            mbar_init(&empty_bar[st], kCW);
+            mbar_init(&empty_bar[st], kGW);
         }
     }
-    uint32_t m_sm = 0;
+    if (threadIdx.x < NQA) s_thr[threadIdx.x] = 0;
+    uint32_t m_sm = 0, m_all = 0;
     if (PARETO) {
-        m_sm = (uint32_t)umin64(pa.ctl->front_n, kFrontSmem);
+        m_all = (uint32_t)pa.ctl->front_n;
+        m_sm = min(m_all, kFrontSmem);
         {  // stage the whole DLT (16 B vectors)
             const uint4* src = reinterpret_cast<const uint4*>(pa.dlt);
             uint4* dst = reinterpret_cast<uint4*>(&d);
@@ -914,6 +1023,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = pa.front[i];
     }
     __syncthreads();
+    const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
+    const uint64_t total = v.ntiles * per_tile;
+    const uint64_t nstages = (total + kStageRecs - 1) / kStageRecs;
     // one running best per query under the query's total order (feasible first)
     uint64_t bi[NQA];
     Rec4 br[NQA];
@@ -924,123 +1036,211 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         br[q] = Rec4{};
         bf[q] = false;
     }
-    const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
 
     if (warp == kCW) {
         // ---------------- producer: one elected lane issues the bulk copies
         if (lane == 0) {
             uint32_t it = 0;
-            for (uint64_t t = blockIdx.x; t < v.ntiles; t += gridDim.x) {
-                for (uint32_t pin0 = 0; pin0 < per_tile; pin0 += kStageRecs, it++) {
-                    const uint32_t st = it % NS, k = it / NS;
-                    if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
-                    const uint32_t cnt = min(kStageRecs, per_tile - pin0);
-                    // stage rows t*32 .. t*32+31, in-row offsets j0 .. j1: index range
-                    const uint64_t j0 = pin0 >> 5, j1 = (pin0 + cnt - 1) >> 5;
-                    const uint64_t H0 = (v.t0 + t) * kTileRows;
-                    const uint64_t lo = H0 * v.row + j0, hi = (H0 + kTileRows - 1) * v.row + j1;
-                    meta[st].t = t;
-                    meta[st].pin0 = pin0;
-                    meta[st].cnt = cnt;
-                    meta[st].all_valid = (cnt % 32 == 0 && lo >= v.ib && hi < v.ie) ? 1u : 0u;
-                    mbar_expect_tx(&full_bar[st], cnt * (uint32_t)sizeof(Rec4));
-                    tma_bulk_g2s(ring + (size_t)st * kStageRecs, v.recs + t * per_tile + pin0,
-                                 cnt * (uint32_t)sizeof(Rec4), &full_bar[st]);
-                }
+            // DRAM latency is covered by L2 prefetches kPrefetch stages ahead (the smem
+            // ring only has to cover L2 latency): prime the first ones
+            for (uint32_t pf = 0; pf < kPrefetch; pf++) {
+                const uint64_t sp = blockIdx.x + (uint64_t)pf * gridDim.x;
+                if (sp < nstages)
+                    tma_prefetch_l2(v.recs + sp * kStageRecs, (uint32_t)umin64(kStageRecs, total - sp * kStageRecs) * (uint32_t)sizeof(Rec4));
             }
-            const uint32_t st = it % NS, k = it / NS;  // end-of-stream marker
-            if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
-            meta[st].cnt = 0;
-            mbar_arrive(&full_bar[st]);
+            for (uint64_t sg = blockIdx.x; sg < nstages; sg += gridDim.x, it++) {
+                const uint64_t sp = sg + (uint64_t)kPrefetch * gridDim.x;
+                if (sp < nstages)
+                    tma_prefetch_l2(v.recs + sp * kStageRecs, (uint32_t)umin64(kStageRecs, total - sp * kStageRecs) * (uint32_t)sizeof(Rec4));
+                const uint32_t st = it % NS, k = it / NS;
+                if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
+                const uint64_t pos0 = sg * kStageRecs;
+                const uint32_t cnt = (uint32_t)umin64(kStageRecs, total - pos0);
+                // tile padding lives only in the first and the last tile of a segment
+                const bool edge = pos0 < per_tile || pos0 + cnt > total - per_tile;
+                meta[st].pos0 = pos0;
+                meta[st].cnt = cnt;
+                meta[st].all_valid = edge ? 0u : 1u;
+                mbar_expect_tx(&full_bar[st], cnt * (uint32_t)sizeof(Rec4));
+                tma_bulk_g2s(ring + (size_t)st * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4),
+                             &full_bar[st]);
+            }
+            for (int g = 0; g < kGroups; g++, it++) {  // one end-of-stream marker per group
+                const uint32_t st = it % NS, k = it / NS;
+                if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
+                meta[st].cnt = 0;
+                mbar_arrive(&full_bar[st]);
+            }
         }
     } else {
-        // ---------------- consumers
-        for (uint32_t it = 0;; it++) {
+        // ---------------- consumers: group g takes stages g, g + kGroups, ...
+        const uint32_t grp = (uint32_t)warp / kGW;
+        const uint32_t gtid = threadIdx.x - grp * (kGW * 32);
+        for (uint32_t it = grp;; it += kGroups) {
             const uint32_t st = it % NS;
             mbar_wait(&full_bar[st], (it / NS) & 1);
             const StageMeta mt = meta[st];
             if (mt.cnt == 0) break;
-            const uint32_t tid = threadIdx.x;  // < kStageRecs
-            bool valid = tid < mt.cnt;
-            if (valid && !mt.all_valid) {  // tile-edge stages only
-                const uint64_t i0 = tiled_index(v.t0, v.row, mt.t, mt.pin0 + tid);
-                valid = tid < mt.cnt && i0 >= v.ib && i0 < v.ie;
+            Rec4 r[kRPT];
+            bool valid[kRPT];
+#pragma unroll
+            for (int u = 0; u < kRPT; u++) {
+                const uint32_t o = gtid + u * (kGW * 32);
+                valid[u] = o < mt.cnt;
+                if (valid[u] && !mt.all_valid) {  // edge stages only
+                    const uint64_t i0 = flat_index(v, per_tile, mt.pos0 + o);
+                    valid[u] = i0 >= v.ib && i0 < v.ie;
+                }
+                if (valid[u]) r[u] = ring[(size_t)st * kStageRecs + o];
+                else r[u] = Rec4{};
             }
-            Rec4 r{};
-            if (valid) r = ring[(size_t)st * kStageRecs + tid];
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage data is in registers now
-            if (valid) {
+            const bool obj_q = P.objective == 0;
 #pragma unroll
-                for (int q = 0; q < NQ; q++) {
-                    // cheap first-key filter: once the best is feasible only a feasible
-                    // record can win, and under QUALITY_FIRST only with quality >= best's
-                    if (bf[q] && P.objective == 0 && rec_Q(r) < rec_Q(br[q])) continue;
-                    const bool f = feasible(P.q[q], r);
-                    if (bf[q] && !f) continue;
-                    const uint64_t idx = tiled_index(v.t0, v.row, mt.t, mt.pin0 + tid);
-                    if (cand_better(P.q[q], P.objective, idx, r, bi[q], br[q])) {
-                        bi[q] = idx;
-                        br[q] = r;
-                        bf[q] = f;
+            for (int q = 0; q < NQ; q++) {
+                // predicate pass (branch-free, bitwise): which records can still beat this
+                // block's best for query q?  The full comparison runs only for those.
+                // A record whose packed key is below the block's best feasible key has
+                // lower quality, or equal quality and higher cost: strictly worse.
+                const unsigned long long thr = s_thr[q];
+                const bool anyf = (thr != 0) | bf[q];
+                const uint64_t slo_t = P.q[q].slo_t, slo_s = P.q[q].slo_s, bud = P.q[q].budget;
+                uint32_t need = 0;
+#pragma unroll
+                for (int u = 0; u < kRPT; u++) {
+                    const bool f = (r[u].w0 <= slo_t) & (r[u].w1 <= slo_s) & (r[u].w2 <= bud);
+                    const bool qok = !obj_q | (qc_key(r[u]) >= thr);
+                    need |= (uint32_t)(valid[u] & qok & (f | !anyf)) << u;
+                }
+                if (__any_sync(0xffffffffu, need != 0)) {
+#pragma unroll
+                    for (int u = 0; u < kRPT; u++) {
+                        if (!((need >> u) & 1u)) continue;
+                        const bool f = feasible(P.q[q], r[u]);
+                        const uint64_t idx = flat_index(v, per_tile, mt.pos0 + gtid + u * (kGW * 32));
+                        if (cand_better(P.q[q], P.objective, idx, r[u], bi[q], br[q])) {
+                            bi[q] = idx;
+                            br[q] = r[u];
+                            bf[q] = f;
+                            if (f) atomicMax(&s_thr[q], obj_q ? (unsigned long long)qc_key(r[u]) : 1ull);
+                        }
                     }
                 }
             }
             if (PARETO) {
-                bool keep = false;
-                PPoint pt{};
-                if (valid) {
-                    pt.t = r.w0 + r.w1;
-                    pt.c = r.w2;
-                    pt.q = rec_Q(r);
-                    keep = !dlt_dominated(d, pt.t, pt.c, pt.q);
-                }
-                if (keep) pt.idx = tiled_index(v.t0, v.row, mt.t, mt.pin0 + tid);
-                unsigned pend = __ballot_sync(0xffffffffu, keep);
-                while (pend) {  // exact test of each DLT survivor by the whole warp
-                    const int src = __ffs(pend) - 1;
-                    pend &= pend - 1;
-                    PPoint x;
-                    x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
-                    x.t = __shfl_sync(0xffffffffu, pt.t, src);
-                    x.c = __shfl_sync(0xffffffffu, pt.c, src);
-                    x.q = __shfl_sync(0xffffffffu, pt.q, src);
-                    bool dom = false;
-                    // front sorted by t: only points with t <= x.t can dominate x
-                    for (uint32_t j0 = 0; j0 < m_sm && fs[j0].t <= x.t; j0 += 32) {
-                        const uint32_t j = j0 + lane;
-                        // an identical entry (same index) also removes x: it is already kept
-                        const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
-                        if (__any_sync(0xffffffffu, dj)) {
-                            dom = true;
-                            break;
+                uint32_t keepm = 0;  // DLT survivors, all kRPT lookups first (independent: ILP)
+#pragma unroll
+                for (int u = 0; u < kRPT; u++)
+                    keepm |= (uint32_t)(valid[u] & !dlt_dominated(d, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u]))) << u;
+                if (!__any_sync(0xffffffffu, keepm != 0)) continue;
+#pragma unroll
+                for (int u = 0; u < kRPT; u++) {
+                    PPoint pt;
+                    pt.t = r[u].w0 + r[u].w1;
+                    pt.c = r[u].w2;
+                    pt.q = rec_Q(r[u]);
+                    pt.idx = 0;
+                    pt.pad = 0;
+                    bool keep = (keepm >> u) & 1u;
+                    unsigned pend = __ballot_sync(0xffffffffu, keep);
+                    if (!pend) continue;
+                    if (keep) pt.idx = flat_index(v, per_tile, mt.pos0 + gtid + u * (kGW * 32));
+                    while (pend) {  // exact test of each DLT survivor by the whole warp
+                        const int src = __ffs(pend) - 1;
+                        pend &= pend - 1;
+                        PPoint x;
+                        x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
+                        x.t = __shfl_sync(0xffffffffu, pt.t, src);
+                        x.c = __shfl_sync(0xffffffffu, pt.c, src);
+                        x.q = __shfl_sync(0xffffffffu, pt.q, src);
+                        bool dom = false;
+                        // front sorted by t: only points with t <= x.t can dominate x
+                        for (uint32_t j0 = 0; j0 < m_sm && fs[j0].t <= x.t; j0 += 32) {
+                            const uint32_t j = j0 + lane;
+                            // an identical entry (same index) also removes x: it is already kept
+                            const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
+                            if (__any_sync(0xffffffffu, dj)) {
+                                dom = true;
+                                break;
+                            }
                         }
+                        // front points beyond the smem subset: from global (L2-resident)
+                        for (uint32_t j0 = m_sm; !dom && j0 < m_all && pa.front[j0].t <= x.t; j0 += 32) {
+                            const uint32_t j = j0 + lane;
+                            const bool dj = j < m_all && pdom(pa.front[j], 0, x, 1);
+                            if (__any_sync(0xffffffffu, dj)) dom = true;
+                        }
+                        if (lane == src && dom) keep = false;
                     }
-                    if (lane == src && dom) keep = false;
-                }
-                const unsigned mask = __ballot_sync(0xffffffffu, keep);
-                if (mask) {
-                    const int leader = __ffs(mask) - 1;
-                    unsigned long long slot0 = 0;
-                    if (lane == leader) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
-                    slot0 = __shfl_sync(0xffffffffu, slot0, leader);
-                    if (keep) {
-                        const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-                        if (slot < pa.cap) pa.surv[slot] = pt;
+                    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                    if (mask) {
+                        const int leader = __ffs(mask) - 1;
+                        unsigned long long slot0 = 0;
+                        if (lane == leader) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
+                        slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+                        if (keep) {
+                            const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+                            if (slot < pa.cap) pa.surv[slot] = pt;
+                        }
                     }
                 }
             }
         }
     }
 #pragma unroll
-    for (int q = 0; q < NQ; q++) {
+    for (int q = 0; q < NQ; q++) {  // the producer warp joins with "none"
         uint64_t idx = bi[q];
-        Rec4 r = br[q];
+        Rec4 rr = br[q];
+        block_reduce_cand(P.q[q], P.objective, idx, rr, s_tmp);
+        if (threadIdx.x == 0) {
+            partial[out_block * SW_MAX_QUERIES + q].idx = idx;
+            partial[out_block * SW_MAX_QUERIES + q].r = rr;
+        }
+    }
+}
+
+// Fleet merge: block b reduces, for each of its request's queries q, the `count`
+// candidates in[b * stride_block + j * stride_item + q] (j < count) -> out[b * SW_MAX_QUERIES
+// + q], with the closest flag in .pad.  Per-block partials after a fleet scan
+// (stride_item = SW_MAX_QUERIES) and the cross-rank merge of allgathered winners
+// (stride_item = n_requests * SW_MAX_QUERIES) both use it.
+__global__ void __launch_bounds__(kScanThreads) select_merge_kernel(const Cand* __restrict__ in, uint32_t count,
+                                                                    uint64_t stride_item, uint64_t stride_block,
+                                                                    const ScanJob* __restrict__ jobs,
+                                                                    Cand* __restrict__ out) {
+    __shared__ Cand s_tmp[32];
+    const SelParams& P = jobs[blockIdx.x].P;
+    const Cand* base = in + (uint64_t)blockIdx.x * stride_block;
+    for (uint32_t q = 0; q < P.nq; q++) {
+        uint64_t idx = kInf64;
+        Rec4 r{};
+        for (uint32_t j = threadIdx.x; j < count; j += blockDim.x) {
+            const Cand c = base[(uint64_t)j * stride_item + q];
+            if (cand_better(P.q[q], P.objective, c.idx, c.r, idx, r)) {
+                idx = c.idx;
+                r = c.r;
+            }
+        }
         block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
         if (threadIdx.x == 0) {
-            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].idx = idx;
-            partial[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q].r = r;
+            Cand& o = out[(uint64_t)blockIdx.x * SW_MAX_QUERIES + q];
+            o.idx = idx;
+            o.r = r;
+            o.pad = (idx != kInf64 && !feasible(P.q[q], r)) ? 1ull : 0ull;
         }
+        __syncthreads();
+    }
+}
+
+// Fleet winners' full metrics: block b recomputes query q's winner of request b.
+template <int NP>
+__global__ void detail_fleet_kernel(const EvalJob* __restrict__ jobs, const Cand* __restrict__ win, uint32_t nq,
+                                    DetailOut* __restrict__ out) {
+    const uint32_t b = blockIdx.x;
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        const Cand c = win[(uint64_t)b * SW_MAX_QUERIES + q];
+        if (c.idx != kInf64) detail_one<NP>(jobs[b].hdr, jobs[b].va, c.idx, out + (uint64_t)b * SW_MAX_QUERIES + q);
     }
 }
 

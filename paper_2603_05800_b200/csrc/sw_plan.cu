@@ -78,6 +78,7 @@ struct sw_plan {
     bool fuse_pareto = true;     // fold unfolded segments inside select scans
     uint64_t chunk = 1ull << 25; // records per fold chunk (the front improves per chunk)
     uint64_t fold_passes = 0;    // diagnostics: filter passes run
+    bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint64_t* d_counts = nullptr;
 
     // select / detail / digest
@@ -89,8 +90,19 @@ struct sw_plan {
     DetailOut* d_detail = nullptr;
     unsigned long long* d_digest = nullptr;
 
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // CUDA events around every eval-kernel launch, on the handle's stream: a ring of
+    // pairs harvested (synchronised and summed) when full or on sw_plan_eval_time
+    static constexpr int kEvPairs = 64;
+    cudaEvent_t ev[2 * kEvPairs] = {};
+    uint32_t ev_kind[kEvPairs] = {};   // SW_KERNEL_EVAL / SW_KERNEL_SCAN
+    uint64_t ev_bytes[kEvPairs] = {};  // algorithmic bytes of the launch (32 B x records)
+    int ev_used = 0;          // pairs recorded since the last harvest
+    int ev_last = -1;         // pair of the last eval launch
+    float last_eval_ms = 0.f;
     bool have_eval_ev = false;
+    uint64_t k_launches[2] = {0, 0};
+    double k_ms[2] = {0.0, 0.0};
+    uint64_t k_bytes[2] = {0, 0};
     uint64_t launches = 0;
     std::string err;
 };
@@ -263,7 +275,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         }
         const u128 lim62 = (u128)1 << 62;
         if (tmax >= lim62 || dsum >= lim62) return fail(nullptr, SW_ERANGE, "time bound exceeds 2^62 us");
-        if (qsum >= ((u128)1 << 32)) return fail(nullptr, SW_ERANGE, "quality bound exceeds 2^32");
+        if (qsum >= ((u128)1 << 32) - 1) return fail(nullptr, SW_ERANGE, "quality bound exceeds 2^32 - 2");
         u128 cmax = pr->fixed_cost_mc;
         for (uint32_t p = 0; p < NP; p++) {
             const u128 X = (u128)pr->gpus[p] * tmax;  // >= busy and >= G * span
@@ -463,8 +475,18 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         cudaError_t e = cudaSuccess;
         launch_np(h, [&](auto np) {
             constexpr int NPc = decltype(np)::value;
-            e = cudaFuncSetAttribute(eval_kernel<NPc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)h->eval_smem);
+            // the attribute is per kernel, not per handle: set the device maximum so
+            // that every handle's table size stays launchable (occupancy below uses
+            // this handle's actual size)
+            int optin = 0;
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+            cudaFuncAttributes fa{};
+            e = cudaFuncGetAttributes(&fa, eval_kernel<NPc>);
+            const size_t dyn_max = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+            if (e == cudaSuccess)
+                e = dyn_max < h->eval_smem ? cudaErrorInvalidValue
+                                           : cudaFuncSetAttribute(eval_kernel<NPc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                  (int)dyn_max);
             if (e == cudaSuccess)
                 e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eval_kernel<NPc>, kEvalThreads,
                                                                   h->eval_smem);
@@ -479,6 +501,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     h->scan_grid = (uint32_t)h->num_sms;  // scan kernels: one TMA-pipelined block per SM
     if (const char* ev = getenv("SW_PARETO_CHUNK")) h->chunk = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
+    if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     if (set_scan_smem_attrs() != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ECUDA, "scan kernel smem attribute failed"));
@@ -486,7 +509,9 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
 
     // ---- record buffer + reduction scratch
     uint64_t cap = rt->record_capacity;
-    if (cap == 0) cap = N / (uint64_t)h->nranks + 1;
+    // default: this rank's largest possible shard (whole rows split evenly, plus a
+    // ragged head or tail of under a row each)
+    if (cap == 0) cap = N / (uint64_t)h->nranks + 3 * h->row;
     h->cand_cap = cap;
     {  // slots: whole tiles of 32 rows plus 2 tiles of padding for each of up to
        // kMaxSegs segments (each eval call adds at most 2 partial tiles)
@@ -515,8 +540,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return bail(st);
     if (cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream) != cudaSuccess)
         return bail(fail(nullptr, SW_ECUDA, "ctl init failed"));
-    if (cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
-        return bail(fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
+    for (int i = 0; i < 2 * sw_plan::kEvPairs; i++)
+        if (cudaEventCreate(&h->ev[i]) != cudaSuccess) return bail(fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ECUDA, "create: device work failed"));
@@ -535,8 +560,8 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
                         h->d_counts, h->d_gather, h->d_tmp2, h->d_surv};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
-        if (h->ev0) cudaEventDestroy(h->ev0);
-        if (h->ev1) cudaEventDestroy(h->ev1);
+        for (cudaEvent_t e : h->ev)
+            if (e) cudaEventDestroy(e);
         if (h->own_stream) cudaStreamDestroy(h->stream);
         cudaGetLastError();
     }
@@ -600,6 +625,43 @@ extern "C" sw_status sw_shard_range(uint64_t begin, uint64_t end, uint64_t row, 
 }
 
 // ============================================================================ eval
+// Sum the recorded eval-kernel event pairs into the totals and free the ring.
+static sw_status harvest_eval_events(sw_plan* h) {
+    if (h->ev_used == 0) return SW_OK;
+    CK(h, cudaEventSynchronize(h->ev[2 * (h->ev_used - 1) + 1]));
+    for (int i = 0; i < h->ev_used; i++) {
+        float ms = 0.f;
+        CK(h, cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]));
+        const uint32_t k = h->ev_kind[i];
+        h->k_launches[k]++;
+        h->k_ms[k] += ms;
+        h->k_bytes[k] += h->ev_bytes[i];
+        if (i == h->ev_last) h->last_eval_ms = ms;
+    }
+    h->ev_used = 0;
+    h->ev_last = -1;
+    return SW_OK;
+}
+
+// Event pair around one timed launch: begin_timed() before, end_timed() after.
+static sw_status begin_timed(sw_plan* h, uint32_t kind, uint64_t bytes, int* pair) {
+    if (h->ev_used == sw_plan::kEvPairs) {
+        sw_status hs = harvest_eval_events(h);
+        if (hs < 0) return hs;
+    }
+    const int pr = h->ev_used++;
+    h->ev_kind[pr] = kind;
+    h->ev_bytes[pr] = bytes;
+    CK(h, cudaEventRecord(h->ev[2 * pr], h->stream));
+    *pair = pr;
+    return SW_OK;
+}
+
+static sw_status end_timed(sw_plan* h, int pair) {
+    CK(h, cudaEventRecord(h->ev[2 * pair + 1], h->stream));
+    return SW_OK;
+}
+
 extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
     if (!h) return fail(nullptr, SW_EINVAL, "null handle");
     if (begin > end || end > h->N)
@@ -627,14 +689,18 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
         const uint64_t need = (sg.ntiles * kTileRows + kEvalThreads - 1) / kEvalThreads;  // one warp per tile
         const uint32_t grid = (uint32_t)std::min<uint64_t>(need, (uint64_t)h->eval_grid);
         Rec4* outp = h->d_rec + h->rec_used;
-        CK(h, cudaEventRecord(h->ev0, h->stream));
+        int pr = 0;
+        sw_status ts = begin_timed(h, SW_KERNEL_EVAL, n * sizeof(Rec4), &pr);
+        if (ts < 0) return ts;
         launch_np(h, [&](auto np) {
             constexpr int NPc = decltype(np)::value;
-            eval_kernel<NPc><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(h->d_hdr, h->d_va, h->va_bytes, t0, t1,
-                                                                             outp);
+            eval_kernel<NPc><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(
+                EvalJob{h->d_hdr, h->d_va, h->va_bytes, t0, t1, outp}, nullptr);
         });
         CKL(h);
-        CK(h, cudaEventRecord(h->ev1, h->stream));
+        ts = end_timed(h, pr);
+        if (ts < 0) return ts;
+        h->ev_last = pr;
         h->have_eval_ev = true;
         h->rec_used += slots;
         h->cand_used += n;
@@ -646,8 +712,23 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
 extern "C" sw_status sw_plan_last_eval_ms(sw_plan* h, float* ms) {
     if (!h || !ms) return fail(nullptr, SW_EINVAL, "null argument");
     if (!h->have_eval_ev) return fail(h, SW_ESTATE, "no eval launched yet");
-    CK(h, cudaEventSynchronize(h->ev1));
-    CK(h, cudaEventElapsedTime(ms, h->ev0, h->ev1));
+    if (h->ev_last >= 0) {
+        CK(h, cudaEventSynchronize(h->ev[2 * h->ev_last + 1]));
+        CK(h, cudaEventElapsedTime(&h->last_eval_ms, h->ev[2 * h->ev_last], h->ev[2 * h->ev_last + 1]));
+    }
+    *ms = h->last_eval_ms;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_kernel_time(sw_plan* h, uint32_t kind, uint64_t* n_launches, double* total_ms,
+                                         uint64_t* bytes) {
+    if (!h || !n_launches || !total_ms || !bytes) return fail(nullptr, SW_EINVAL, "null argument");
+    if (kind > SW_KERNEL_SCAN) return fail(h, SW_EINVAL, "bad kernel kind %u", kind);
+    sw_status st = harvest_eval_events(h);
+    if (st < 0) return st;
+    *n_launches = h->k_launches[kind];
+    *total_ms = h->k_ms[kind];
+    *bytes = h->k_bytes[kind];
     return SW_OK;
 }
 
@@ -681,7 +762,7 @@ static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint
 template <int NQ, bool PARETO>
 static void launch_scan(uint32_t grid, size_t smem, cudaStream_t st, const SegView& v, const SelParams& P,
                         Cand* partial, const ParetoArgs& pa) {
-    scan_kernel<NQ, PARETO><<<grid, kScanBlock, smem, st>>>(v, P, partial, pa);
+    scan_kernel<NQ, PARETO><<<grid, kScanBlock, smem, st>>>(v, P, partial, pa, nullptr);
 }
 
 template <bool PARETO>
@@ -738,14 +819,15 @@ static sw_status reduce_async(sw_plan* h, PPoint* out) {
     const uint64_t U = h->front_cap + h->surv_cap;
     ParetoCtl* c = h->d_ctl;
     const uint32_t gl = (uint32_t)((U + kLocal - 1) / kLocal), gs = (uint32_t)((U + kScanThreads - 1) / kScanThreads);
+    const uint32_t gls = (uint32_t)((U + kLocalSmall - 1) / kLocalSmall);
     CK(h, cudaMemsetAsync(&c->m_loc, 0, 3 * sizeof(uint32_t), h->stream));  // m_loc, m_loc2, m_cmp
-    pareto_local_kernel<<<gl, kLocal, 0, h->stream>>>(h->d_work, &c->m_in, h->d_tmp2, &c->m_loc);
+    (void)gl;
+    pareto_local_kernel<kLocalSmall><<<gls, kLocalSmall, 0, h->stream>>>(h->d_work, &c->m_in, h->d_tmp2, &c->m_loc,
+                                                                         h->d_keep);
     CKL(h);
-    pareto_local_kernel<<<gl, kLocal, 0, h->stream>>>(h->d_tmp2, &c->m_loc, h->d_tmp, &c->m_loc2);
+    pareto_mark2d_kernel<<<2 * h->num_sms, kScanThreads, 0, h->stream>>>(h->d_tmp2, &c->m_loc, h->d_keep);
     CKL(h);
-    pareto_mark_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_tmp, &c->m_loc2, h->d_keep);
-    CKL(h);
-    pareto_compact_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_tmp, &c->m_loc2, h->d_keep, h->d_work, &c->m_cmp);
+    pareto_compact_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_tmp2, &c->m_loc, h->d_keep, h->d_work, &c->m_cmp);
     CKL(h);
     pareto_rank_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_work, &c->m_cmp, out, c, h->front_cap);
     CKL(h);
@@ -784,14 +866,26 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
             part = h->d_partial + (uint64_t)*np * SW_MAX_QUERIES;
             *np += grid;
         }
+        int pr = 0;
+        sw_status ts = begin_timed(h, SW_KERNEL_SCAN, (c1 - c0) * per_tile * sizeof(Rec4), &pr);
+        if (ts < 0) return ts;
         launch_scan_nq<true>(nq, grid, psmem, h->stream, view_of(h, g, c0, c1), P, part, pareto_args(h));
         CKL(h);
+        if ((ts = end_timed(h, pr)) < 0) return ts;
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                h->d_ctl);
         CKL(h);
         sw_status st = reduce_async(h, h->d_front);
         if (st < 0) return st;
         h->fold_passes++;
+        if (h->debug) {  // diagnostics only: synchronises every pass
+            ParetoCtl c;
+            CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
+            CK(h, cudaStreamSynchronize(h->stream));
+            fprintf(stderr, "[sw] fold pass %llu: tiles [%llu,%llu) survivors %llu merge-in %u local %u/%u front %llu\n",
+                    (unsigned long long)h->fold_passes, (unsigned long long)c0, (unsigned long long)c1,
+                    (unsigned long long)c.surv, c.m_in, c.m_loc, c.m_loc2, (unsigned long long)c.front_n);
+        }
     }
     return SW_OK;
 }
@@ -837,9 +931,13 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
         } else {
             const uint32_t grid = (uint32_t)std::min<uint64_t>(g.ntiles, h->scan_grid);
             if (np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many segments for one select");
+            int pr = 0;
+            sw_status ts = begin_timed(h, SW_KERNEL_SCAN, g.ntiles * kTileRows * h->row * sizeof(Rec4), &pr);
+            if (ts < 0) return ts;
             launch_scan_nq<false>(nq, grid, kRingBytes, h->stream, view_of(h, g, 0, g.ntiles), P,
                                   h->d_partial + (uint64_t)np * SW_MAX_QUERIES, pareto_args(h));
             CKL(h);
+            if ((ts = end_timed(h, pr)) < 0) return ts;
             np += grid;
         }
     }
@@ -912,8 +1010,11 @@ extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uin
     if (!h->segs.empty()) return fail(h, SW_ESTATE, "sweep needs a handle without records (reset/release)");
     // largest global chunk whose every rank shard fits the per-rank capacity: whole
     // rows per rank, at most cand_cap - row candidates each (ragged ends fit the slack)
-    const uint64_t rows_per_rank = h->cand_cap > h->row ? (h->cand_cap - h->row) / h->row : 0;
-    const uint64_t max_chunk = rows_per_rank * h->row * (uint64_t)h->nranks;
+    // one rank: the shard is the chunk; several: whole rows split evenly (<= one extra
+    // row per rank) plus a ragged head / tail of under a row each
+    uint64_t max_chunk = h->cand_cap;
+    if (h->nranks > 1)
+        max_chunk = h->cand_cap > 3 * h->row ? (h->cand_cap - 3 * h->row) / h->row * h->row * (uint64_t)h->nranks : 0;
     if (chunk == 0) chunk = max_chunk;
     if (chunk == 0 || chunk > max_chunk)
         return fail(h, SW_ERANGE, "chunk %llu exceeds what record_capacity %llu allows (%llu)",
@@ -1123,6 +1224,316 @@ extern "C" sw_status sw_selection_merge(uint32_t objective, const sw_query* q, c
     if ((take_b ? ib : ia) == kInf64) out->status = SW_EMPTY;
     else out->status = feasible(qd, take_b ? rb : ra) ? SW_OK : SW_CLOSEST;
     return out->status;
+}
+
+// ============================================================================ fleet (C4)
+// A batch of requests evaluated and selected together: ONE eval launch for every
+// request's space (grid.y = request, each CTA stages its own request's tables), ONE
+// select scan (grid.y = request, one query per request), one merge kernel, one batched
+// winner-detail kernel and -- multi-GPU -- one allgather of the n winners.  The per-request
+// handles stay usable (Pareto front, digest, records, detail) through sw_fleet_plan.
+struct sw_fleet {
+    std::vector<sw_plan*> plans;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    uint32_t np_max = 1;
+    size_t eval_smem = 0;
+    int eval_occ = 1, num_sms = 148;
+    uint32_t gx = 1;  // scan blocks per request
+    EvalJob* d_ejobs = nullptr;
+    ScanJob* d_sjobs = nullptr;
+    Cand* d_partial = nullptr;
+    Cand* d_win = nullptr;
+    Cand* d_win_all = nullptr;
+    DetailOut* d_det = nullptr;
+    bool evaluated = false;
+    cudaEvent_t ev[4] = {};
+    uint64_t k_launches[2] = {0, 0};
+    double k_ms[2] = {0.0, 0.0};
+    uint64_t k_bytes[2] = {0, 0};
+};
+
+template <typename F>
+static sw_status launch_np_n(uint32_t np, sw_plan* h, F&& f) {
+    switch (np) {
+        case 1: f(std::integral_constant<int, 1>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        case 3: f(std::integral_constant<int, 3>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        default: return fail(h, SW_EINVAL, "bad pool count");
+    }
+    return SW_OK;
+}
+
+extern "C" sw_status sw_fleet_destroy(sw_fleet* f) {
+    if (!f) return SW_OK;
+    if (f->stream) {
+        cudaSetDevice(f->device);
+        void* bufs[] = {f->d_ejobs, f->d_sjobs, f->d_partial, f->d_win, f->d_win_all, f->d_det};
+        for (void* b : bufs)
+            if (b) cudaFreeAsync(b, f->stream);
+        for (cudaEvent_t e : f->ev)
+            if (e) cudaEventDestroy(e);
+    }
+    for (sw_plan* p : f->plans) sw_plan_destroy(p);
+    if (f->stream) {
+        cudaStreamSynchronize(f->stream);
+        if (f->own_stream) cudaStreamDestroy(f->stream);
+    }
+    cudaGetLastError();
+    delete f;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables, const sw_scene_list* scenes,
+                                     const sw_price_table* prices, const sw_runtime* rt, sw_fleet** out) {
+    if (!tables || !scenes || !prices || !rt || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (n < 1 || n > SW_MAX_FLEET) return fail(nullptr, SW_EINVAL, "fleet size %u not in 1..%d", n, SW_MAX_FLEET);
+    sw_fleet* f = new sw_fleet();
+    f->device = rt->device;
+    f->comm = (ncclComm_t)rt->nccl_comm;
+    f->rank = rt->rank;
+    f->nranks = rt->nranks;
+    auto bail = [&](sw_status s) {
+        sw_fleet_destroy(f);
+        return s;
+    };
+    if (cudaSetDevice(f->device) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(nullptr, SW_ECUDA, "cudaSetDevice(%d) failed (no CUDA device?)", f->device));
+    }
+    if (rt->stream) {
+        f->stream = (cudaStream_t)rt->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(nullptr, SW_ECUDA, "cudaStreamCreate failed"));
+        f->own_stream = true;
+    }
+    sw_runtime prt = *rt;
+    prt.stream = f->stream;
+    for (uint32_t i = 0; i < n; i++) {
+        sw_plan* p = nullptr;
+        sw_status st = sw_plan_create(&tables[i], &scenes[i], &prices[i], &prt, &p);
+        if (st < 0) {
+            const std::string msg = "request " + std::to_string(i) + ": " + g_last_error;
+            bail(st);
+            return fail(nullptr, st, "%s", msg.c_str());
+        }
+        f->plans.push_back(p);
+        f->np_max = std::max(f->np_max, p->NP);
+        f->eval_smem = std::max(f->eval_smem, p->eval_smem);
+    }
+    sw_plan* h = f->plans[0];
+    f->num_sms = h->num_sms;
+    {
+        cudaError_t e = cudaSuccess;
+        int occ = 0;
+        launch_np_n(f->np_max, h, [&](auto np) {
+            constexpr int NPc = decltype(np)::value;
+            int optin = 0;
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, f->device);
+            cudaFuncAttributes fa{};
+            e = cudaFuncGetAttributes(&fa, eval_kernel<NPc>);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(eval_kernel<NPc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         optin - (int)fa.sharedSizeBytes);
+            if (e == cudaSuccess)
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eval_kernel<NPc>, kEvalThreads, f->eval_smem);
+        });
+        if (e != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            return bail(fail(nullptr, SW_ECUDA, "fleet eval kernel cannot launch (%s)", cudaGetErrorString(e)));
+        }
+        f->eval_occ = occ;
+    }
+    f->gx = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(1, (8ull * f->num_sms + n - 1) / n));
+    auto alloc = [&](void** p, size_t bytes) {
+        return cudaMallocAsync(p, bytes, f->stream) == cudaSuccess;
+    };
+    if (!alloc((void**)&f->d_ejobs, sizeof(EvalJob) * n) || !alloc((void**)&f->d_sjobs, sizeof(ScanJob) * n) ||
+        !alloc((void**)&f->d_partial, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n * f->gx) ||
+        !alloc((void**)&f->d_win, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n) ||
+        !alloc((void**)&f->d_win_all, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n * f->nranks) ||
+        !alloc((void**)&f->d_det, sizeof(DetailOut) * (size_t)n)) {
+        cudaGetLastError();
+        return bail(fail(nullptr, SW_ENOMEM, "fleet scratch allocation failed"));
+    }
+    for (cudaEvent_t& e : f->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
+    if (cudaStreamSynchronize(f->stream) != cudaSuccess) return bail(fail(nullptr, SW_ECUDA, "fleet create failed"));
+    *out = f;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_fleet_size(const sw_fleet* f, uint32_t* n) {
+    if (!f || !n) return fail(nullptr, SW_EINVAL, "null argument");
+    *n = (uint32_t)f->plans.size();
+    return SW_OK;
+}
+
+extern "C" sw_status sw_fleet_plan(sw_fleet* f, uint32_t i, sw_plan** out) {
+    if (!f || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (i >= f->plans.size()) return fail(nullptr, SW_EINVAL, "request %u of %zu", i, f->plans.size());
+    *out = f->plans[i];
+    return SW_OK;
+}
+
+extern "C" sw_status sw_fleet_reset(sw_fleet* f) {
+    if (!f) return fail(nullptr, SW_EINVAL, "null fleet");
+    for (sw_plan* p : f->plans) {
+        sw_status st = sw_plan_reset(p);
+        if (st < 0) return st;
+    }
+    f->evaluated = false;
+    return SW_OK;
+}
+
+static sw_status fleet_harvest(sw_fleet* f, int kind, uint64_t bytes) {
+    sw_plan* h = f->plans[0];
+    float ms = 0.f;
+    CK(h, cudaEventSynchronize(f->ev[2 * kind + 1]));
+    CK(h, cudaEventElapsedTime(&ms, f->ev[2 * kind], f->ev[2 * kind + 1]));
+    f->k_launches[kind]++;
+    f->k_ms[kind] += ms;
+    f->k_bytes[kind] += bytes;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_fleet_eval(sw_fleet* f) {
+    if (!f) return fail(nullptr, SW_EINVAL, "null fleet");
+    sw_plan* h = f->plans[0];
+    const uint32_t n = (uint32_t)f->plans.size();
+    for (sw_plan* p : f->plans)
+        if (!p->segs.empty()) return fail(h, SW_ESTATE, "fleet eval needs handles without records (sw_fleet_reset)");
+    CK(h, cudaSetDevice(f->device));
+    std::vector<EvalJob> jobs(n);
+    uint64_t max_tiles = 0, recs = 0;
+    for (uint32_t i = 0; i < n; i++) {
+        sw_plan* p = f->plans[i];
+        uint64_t b, e;
+        sw_status st = sw_shard_range(0, p->N, p->row, p->rank, p->nranks, &b, &e);
+        if (st < 0) return st;
+        const uint64_t m = e - b;
+        const uint64_t rb = b / p->row, re = (e + p->row - 1) / p->row;
+        const uint64_t t0 = rb / kTileRows, t1 = (re + kTileRows - 1) / kTileRows;
+        const uint64_t slots = m ? (t1 - t0) * kTileRows * p->row : 0;
+        if (m > p->cand_cap || slots > p->rec_cap)
+            return fail(h, SW_ERANGE, "request %u: records exceed its capacity", i);
+        p->segs.push_back(Segment{0, p->N, b, e, 0, t0, m ? t1 - t0 : 0, false});
+        p->rec_used = slots;
+        p->cand_used = m;
+        jobs[i] = EvalJob{p->d_hdr, p->d_va, p->va_bytes, t0, m ? t1 : t0, p->d_rec};
+        max_tiles = std::max<uint64_t>(max_tiles, m ? t1 - t0 : 0);
+        recs += m;
+    }
+    CK(h, cudaMemcpyAsync(f->d_ejobs, jobs.data(), sizeof(EvalJob) * n, cudaMemcpyHostToDevice, f->stream));
+    f->evaluated = true;
+    if (max_tiles == 0) return SW_OK;
+    // one warp per tile: blocks per request = ceil(max tiles / warps per block)
+    const uint32_t gxe = (uint32_t)((max_tiles * kTileRows + kEvalThreads - 1) / kEvalThreads);
+    CK(h, cudaEventRecord(f->ev[0], f->stream));
+    launch_np_n(f->np_max, h, [&](auto np) {
+        constexpr int NPc = decltype(np)::value;
+        eval_kernel<NPc><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
+    });
+    CKL(h);
+    CK(h, cudaEventRecord(f->ev[1], f->stream));
+    return fleet_harvest(f, SW_KERNEL_EVAL, recs * sizeof(Rec4));
+}
+
+extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_selection* out) {
+    if (!f || !queries || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    sw_plan* h = f->plans[0];
+    if (!f->evaluated) return fail(h, SW_ESTATE, "sw_fleet_eval first");
+    const uint32_t n = (uint32_t)f->plans.size();
+    CK(h, cudaSetDevice(f->device));
+    std::vector<ScanJob> jobs(n);
+    uint64_t slots = 0;
+    for (uint32_t i = 0; i < n; i++) {
+        sw_plan* p = f->plans[i];
+        if (p->segs.size() != 1) return fail(h, SW_ESTATE, "request %u: records changed since sw_fleet_eval", i);
+        const Segment& g = p->segs[0];
+        jobs[i].v = view_of(p, g, 0, g.ntiles);
+        memset(&jobs[i].P, 0, sizeof(SelParams));
+        jobs[i].P.nq = 1;
+        jobs[i].P.objective = (p->h.flags & 4u) ? 1u : 0u;
+        jobs[i].P.q[0] = QueryDev{queries[i].slo_startup_us, queries[i].slo_stall_us, queries[i].budget_mc};
+        slots += g.ntiles * kTileRows * p->row;
+    }
+    CK(h, cudaMemcpyAsync(f->d_sjobs, jobs.data(), sizeof(ScanJob) * n, cudaMemcpyHostToDevice, f->stream));
+    CK(h, cudaEventRecord(f->ev[2], f->stream));
+    scan_kernel<1, false><<<dim3(f->gx, n), kScanBlock, kRingBytes, f->stream>>>(SegView{}, SelParams{}, f->d_partial,
+                                                                                ParetoArgs{}, f->d_sjobs);
+    CKL(h);
+    CK(h, cudaEventRecord(f->ev[3], f->stream));
+    select_merge_kernel<<<n, kScanThreads, 0, f->stream>>>(f->d_partial, f->gx, SW_MAX_QUERIES,
+                                                           (uint64_t)f->gx * SW_MAX_QUERIES, f->d_sjobs, f->d_win);
+    CKL(h);
+    if (f->nranks > 1) {  // a10: one allgather of the n winners, replicated merge
+        CKN(h, ncclAllGather(f->d_win, f->d_win_all, sizeof(Cand) * SW_MAX_QUERIES * n, ncclUint8, f->comm, f->stream));
+        select_merge_kernel<<<n, kScanThreads, 0, f->stream>>>(f->d_win_all, (uint32_t)f->nranks,
+                                                               (uint64_t)n * SW_MAX_QUERIES, SW_MAX_QUERIES, f->d_sjobs,
+                                                               f->d_win);
+        CKL(h);
+    }
+    launch_np_n(f->np_max, h, [&](auto np) {
+        constexpr int NPc = decltype(np)::value;
+        detail_fleet_kernel<NPc><<<n, 32, 0, f->stream>>>(f->d_ejobs, f->d_win, 1, f->d_det);
+    });
+    CKL(h);
+    std::vector<Cand> win((size_t)n * SW_MAX_QUERIES);
+    std::vector<DetailOut> det(n);
+    CK(h, cudaMemcpyAsync(win.data(), f->d_win, sizeof(Cand) * win.size(), cudaMemcpyDeviceToHost, f->stream));
+    CK(h, cudaMemcpyAsync(det.data(), f->d_det, sizeof(DetailOut) * n, cudaMemcpyDeviceToHost, f->stream));
+    sw_status st = fleet_harvest(f, SW_KERNEL_SCAN, slots * sizeof(Rec4));  // synchronises the scan
+    if (st < 0) return st;
+    CK(h, cudaStreamSynchronize(f->stream));
+    sw_status worst = SW_OK;
+    for (uint32_t i = 0; i < n; i++) {
+        const Cand& c = win[(size_t)i * SW_MAX_QUERIES];
+        sw_selection& o = out[i];
+        memset(&o, 0, sizeof o);
+        if (c.idx == kInf64) {
+            o.status = SW_EMPTY;
+        } else {
+            const sw_plan* p = f->plans[i];
+            const DetailOut& d = det[i];
+            o.status = c.pad ? SW_CLOSEST : SW_OK;
+            o.index = c.idx;
+            o.rec.ttff_us = d.rec.w0;
+            o.rec.stall_us = d.rec.w1;
+            o.rec.cost_mc = d.rec.w2;
+            o.rec.quality = (uint32_t)d.rec.w3;
+            o.rec.stall_count = (uint16_t)(d.rec.w3 >> 32);
+            o.rec.flags = (uint8_t)(d.rec.w3 >> 48);
+            o.ttff_eff_us = d.ttff_eff;
+            o.makespan_us = d.makespan;
+            for (uint32_t q = 0; q < SW_MAX_POOLS; q++) o.pool_end_us[q] = q < p->NP ? d.pool_end[q] : 0;
+            for (uint32_t b = 0; b < p->B_user; b++) o.digit[b] = (uint8_t)d.digit[b + p->pad_digits];
+        }
+        worst = std::max<sw_status>(worst, o.status);
+    }
+    return worst;
+}
+
+extern "C" sw_status sw_fleet_kernel_time(sw_fleet* f, uint32_t kind, uint64_t* n_launches, double* total_ms,
+                                          uint64_t* bytes) {
+    if (!f || !n_launches || !total_ms || !bytes) return fail(nullptr, SW_EINVAL, "null argument");
+    if (kind > SW_KERNEL_SCAN) return fail(nullptr, SW_EINVAL, "bad kernel kind %u", kind);
+    *n_launches = f->k_launches[kind];
+    *total_ms = f->k_ms[kind];
+    *bytes = f->k_bytes[kind];
+    return SW_OK;
+}
+
+extern "C" uint64_t sw_fleet_launch_count(const sw_fleet* f) {
+    uint64_t s = 0;
+    if (f)
+        for (const sw_plan* p : f->plans) s += p->launches;
+    return s;
 }
 
 // ============================================================================ NCCL

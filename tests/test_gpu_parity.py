@@ -217,3 +217,87 @@ def test_fleet_c4(sw):
             _check_winners(plan.select_batch(pb.queries), gr["winners"])
             assert plan.digest() == int(gr["digest"])
             assert plan.pareto() == [tuple(p) for p in gr["front"]]
+
+
+def test_c5_chunked_sweep(sw):
+    """C5 (48^6 = 1.2e10 plans, 60 scenes, 3 pools) on the oracle's pinned sub-ranges,
+    through sw_plan_sweep with a record buffer far smaller than the range (7 chunks):
+    winners (merged across chunks), digest and the running front."""
+    g = _golden("C5sub")
+    pb = make_config("C5")
+    for rg in g["ranges"]:
+        b, e = rg["begin"], rg["end"]
+        with sw.Plan(pb, record_capacity=8_000_000) as plan:
+            sels, dg = plan.sweep(b, e, pb.queries, digest=True)
+            _check_winners(sels, rg["winners"])
+            assert dg == int(rg["digest"])
+            assert plan.pareto() == [tuple(p) for p in rg["front"]]
+            # winners carry their full detail (recomputed on the GPU)
+            for s in sels:
+                d, _ = plan.detail(s.index)
+                assert tuple(d.rec) == tuple(s.rec) and d.digit == s.digit
+
+
+def test_sweep_matches_eval_select(sw, oracle_mod):
+    """sw_plan_sweep over ragged chunks == one eval + select_batch + pareto (C3 sub-range)."""
+    pb = make_config("C3")
+    b, e = 5_000_003, 5_000_003 + 2_345_679
+    orc = oracle_mod.Oracle(pb)
+    w, f, d = orc.sweep(b, e, pb.queries)
+    exp = [{"status": st, "index": i, "rec": r.astuple()} for st, i, r in w]
+    with sw.Plan(pb, record_capacity=600_000) as plan:
+        sels, dg = plan.sweep(b, e, pb.queries, chunk=511_111, digest=True)
+        _check_winners(sels, exp)
+        assert dg == d
+        assert plan.pareto() == f
+        with pytest.raises(sw.SwError):  # chunk larger than the capacity allows
+            plan.sweep(0, 10, pb.queries, chunk=10**9)
+        plan.eval(0, 1000)
+        with pytest.raises(sw.SwError) as ei:  # records held: sweep refuses
+            plan.sweep(2000, 3000, pb.queries)
+        assert ei.value.status == sw.SW_ESTATE
+
+
+def test_interleaved_handles(sw, oracle_mod):
+    """Handles with different table sizes created first, evaluated after (per-kernel
+    launch attributes must not leak between handles); each matches the oracle."""
+    probs = [make_config("C1"), make_config("C3"), make_config("C1")]
+    probs[1].name = "C3"
+    plans = [sw.Plan(pb, record_capacity=200_000) for pb in probs]
+    try:
+        for p in plans:
+            p.eval(0, min(p.n, 200_000))
+        for pb, p in zip(probs, plans):
+            n = min(p.n, 200_000)
+            orc = oracle_mod.Oracle(pb)
+            w, f, d = orc.sweep(0, n, pb.queries)
+            _check_winners(p.select_batch(pb.queries),
+                           [{"status": st, "index": i, "rec": r.astuple()} for st, i, r in w])
+            assert p.digest() == d
+    finally:
+        for p in plans:
+            p.close()
+
+
+def test_fleet_batch_api(sw):
+    """C4 through sw_fleet_*: one eval launch for all 256 requests, one select scan with
+    per-request SLO/budget; every winner, every digest and a sample of fronts vs the
+    oracle golden; reset + second round gives the same winners."""
+    g = _golden("C4")
+    fleet = make_fleet()
+    with sw.Fleet(fleet) as F:
+        for rnd in range(2):
+            if rnd:
+                F.reset()
+            F.eval()
+            sels = F.select([pb.queries[0] for pb in fleet])
+            for s, gr in zip(sels, g["requests"]):
+                _check_winners([s], gr["winners"])
+        for i, (pb, gr) in enumerate(zip(fleet, g["requests"])):
+            p = F.plan(i)
+            assert p.digest() == int(gr["digest"]), i
+            if i % 16 == 5:
+                assert p.pareto() == [tuple(x) for x in gr["front"]], i
+            d, _ = p.detail(sels[i].index)
+            assert tuple(d.rec) == tuple(sels[i].rec) and d.digit == sels[i].digit
+        assert F.launch_count() > 0

@@ -1,7 +1,7 @@
 """Write full-space oracle results to tests/golden/oracle_<cfg>.json.
 
 Calls ONLY oracle/ (and swgen/ for the seeded inputs).  No value here comes from
-the CUDA path.  Usage:  python tools/gen_golden.py C1 C2 C3 [C4] [C5] [--threads T]
+the CUDA path.  Usage:  python tools/gen_golden.py C1 C2 C3 [C4] [C5sub] [--threads T]
 """
 import argparse
 import hashlib
@@ -23,13 +23,20 @@ def problem_hash(pb) -> str:
     return hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest()
 
 
-def sweep_json(pb, threads):
+# C5 (1.2e10 plans, ~2.2e4 core-s for the full space) is pinned on fixed sub-ranges:
+# one from the start of the space and one ragged range in the middle.
+C5_RANGES = [(0, 50_000_000), (6_000_000_007, 6_000_000_007 + 20_000_000)]
+
+
+def sweep_json(pb, threads, begin=0, end=None):
     o = Oracle(pb)
+    end = o.n if end is None else end
     t0 = time.time()
-    winners, front, digest = o.sweep(0, o.n, pb.queries, nthreads=threads)
+    winners, front, digest = o.sweep(begin, end, pb.queries, nthreads=threads)
     dt = time.time() - t0
     return {
-        "name": pb.name, "sha256": problem_hash(pb), "n": o.n, "digest": str(digest),
+        "name": pb.name, "sha256": problem_hash(pb), "n": o.n, "begin": begin, "end": end,
+        "digest": str(digest),
         "queries": [[q.slo_startup_us, q.slo_stall_us, q.budget_mc] for q in pb.queries],
         "winners": [{"status": st, "index": idx, "rec": list(r.astuple())}
                     for st, idx, r in winners],
@@ -45,7 +52,11 @@ def main():
     args = ap.parse_args()
     out_dir = os.path.join(ROOT, "tests", "golden")
     for cfg in args.configs:
-        if cfg == "C4":
+        if cfg == "C5sub":
+            pb = make_config("C5")
+            res = {"name": "C5sub", "ranges": [sweep_json(pb, args.threads, b, e)
+                                               for b, e in C5_RANGES]}
+        elif cfg == "C4":
             reqs = [sweep_json(pb, args.threads) for pb in make_fleet()]
             res = {"name": "C4", "requests": reqs}
         else:

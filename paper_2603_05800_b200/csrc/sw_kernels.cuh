@@ -196,6 +196,18 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2
     }
 }
 
+// Scenes [f0, f1) of one digit's block with choice (p, k), gang update specialised for K
+// (K = 0: runtime k).
+template <int NP, int K>
+__device__ __forceinline__ void run_block(State<NP>& st, const DevHeader& h, uint32_t p, uint32_t k, uint32_t f0,
+                                          uint32_t f1, const VaEntry* vb, uint32_t r) {
+    for (uint32_t s = f0; s < f1; s++) {
+        const VaEntry v = vb[(s - f0) * r];
+        const uint64_t e = scene_step<NP, K>(st, p, k, h.a[s], v.t_us);
+        scene_metrics(st, s, e, h.P[s], v.q);
+    }
+}
+
 // ============================================================================ a1-a7 eval
 // Lane <-> row H: the candidates [H*row, (H+1)*row) share their HI digits (digits
 // 0..B-3); a warp owns a tile of 32 consecutive rows (tiled record layout, sw_plan.h).  The thread simulates the HI scenes once (per-lane choices, runtime k/pool),
@@ -256,10 +268,15 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(EvalJob job, const E
             const uint32_t k = ch_k(ch), p = ch_pool(ch);
             const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
             const VaEntry* vb = va + h.voff[b] + c;
-            for (uint32_t s = f0; s < f1; s++) {
-                const VaEntry v = vb[(s - f0) * r];
-                const uint64_t e = scene_step<NP, 0>(st, p, k, h.a[s], v.t_us);
-                scene_metrics(st, s, e, h.P[s], v.q);
+            // k differs across lanes here, but a divergent switch over the compile-time
+            // gang updates (each ~15x cheaper than the runtime-k barrel shift) wins even
+            // when a warp takes all four paths
+            switch (k) {
+                case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
+                case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
+                case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
+                case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
+                default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
             }
         }
         // ---- MID digit: warp-uniform choice
@@ -893,12 +910,13 @@ __global__ void __launch_bounds__(kScanThreads) pareto_mark2d_kernel(const PPoin
 // point of the segment whatever front subset is used: the later merge stays exact.
 constexpr uint32_t kFrontSmem = 512;  // front points held in smem for the exact filter
 
-struct ParetoArgs {
+struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select flags
     const Dlt* dlt;
     const PPoint* front;
     ParetoCtl* ctl;  // front_n (read) and the survivor counter (atomics)
     PPoint* surv;
     uint64_t cap;
+    uint32_t* gfeas;  // [SW_MAX_QUERIES] per request: a feasible record was seen (or null)
 };
 
 // objective keys only (ties keep the earlier = lower index within a thread's scan)
@@ -958,7 +976,8 @@ __host__ __device__ constexpr size_t ring_bytes(bool pareto) {
 struct StageMeta {
     uint64_t pos0;       // flat slot of the stage's first record
     uint32_t cnt;        // records in the stage; 0 = end of stream
-    uint32_t all_valid;  // no tile padding inside: skip per-record range checks
+    uint16_t all_valid;  // no tile padding inside: skip per-record range checks
+    uint16_t feas;       // bit q: some block already found a feasible record for query q
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -989,6 +1008,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     if (jobs) {  // fleet: request y (never with PARETO)
         v = jobs[blockIdx.y].v;
         P = jobs[blockIdx.y].P;
+        if (pa.gfeas) pa.gfeas += (uint64_t)blockIdx.y * SW_MAX_QUERIES;
     }
     const uint64_t out_block = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
     constexpr int NQA = NQ > 0 ? NQ : 1;
@@ -1000,6 +1020,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     // per query: packed key (Q << 32 | ~min(cost, 2^32-1)) of this block's best FEASIBLE
     // record under QUALITY_FIRST (any nonzero value under COST_X_TTFF); 0 = none yet
     __shared__ unsigned long long s_thr[NQA];
+    // per query, while no feasible record is known: the smallest startup+stall violation
+    // V_t of any closest-tier best in this block (records with a larger V_t cannot win)
+    __shared__ unsigned long long s_vt[NQA];
     Rec4* ring = reinterpret_cast<Rec4*>(fsm);
     Dlt& d = *reinterpret_cast<Dlt*>(fsm + ring_bytes(PARETO));
     PPoint* fs = reinterpret_cast<PPoint*>(fsm + ring_bytes(PARETO) + sizeof(Dlt));
@@ -1010,7 +1033,10 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
             mbar_init(&empty_bar[st], kGW);
         }
     }
-    if (threadIdx.x < NQA) s_thr[threadIdx.x] = 0;
+    if (threadIdx.x < NQA) {
+        s_thr[threadIdx.x] = 0;
+        s_vt[threadIdx.x] = ~0ull;
+    }
     uint32_t m_sm = 0, m_all = 0;
     if (PARETO) {
         m_all = (uint32_t)pa.ctl->front_n;
@@ -1048,7 +1074,14 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 if (sp < nstages)
                     tma_prefetch_l2(v.recs + sp * kStageRecs, (uint32_t)umin64(kStageRecs, total - sp * kStageRecs) * (uint32_t)sizeof(Rec4));
             }
+            uint32_t fm = 0;  // grid-wide feasibility flags, loaded one stage ahead
             for (uint64_t sg = blockIdx.x; sg < nstages; sg += gridDim.x, it++) {
+                uint32_t fm_next = 0;
+                if (NQ > 0 && pa.gfeas) {
+#pragma unroll
+                    for (int q = 0; q < NQ; q++)
+                        fm_next |= (*(volatile const uint32_t*)&pa.gfeas[q] != 0 ? 1u : 0u) << q;
+                }
                 const uint64_t sp = sg + (uint64_t)kPrefetch * gridDim.x;
                 if (sp < nstages)
                     tma_prefetch_l2(v.recs + sp * kStageRecs, (uint32_t)umin64(kStageRecs, total - sp * kStageRecs) * (uint32_t)sizeof(Rec4));
@@ -1060,7 +1093,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 const bool edge = pos0 < per_tile || pos0 + cnt > total - per_tile;
                 meta[st].pos0 = pos0;
                 meta[st].cnt = cnt;
-                meta[st].all_valid = edge ? 0u : 1u;
+                meta[st].all_valid = edge ? 0 : 1;
+                meta[st].feas = (uint16_t)fm;
+                fm = fm_next;
                 mbar_expect_tx(&full_bar[st], cnt * (uint32_t)sizeof(Rec4));
                 tma_bulk_g2s(ring + (size_t)st * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4),
                              &full_bar[st]);
@@ -1101,17 +1136,32 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
             for (int q = 0; q < NQ; q++) {
                 // predicate pass (branch-free, bitwise): which records can still beat this
                 // block's best for query q?  The full comparison runs only for those.
-                // A record whose packed key is below the block's best feasible key has
-                // lower quality, or equal quality and higher cost: strictly worse.
+                //  - once a feasible record is known (this thread, this block or -- via
+                //    the stage meta -- any block) only feasible records can win, and under
+                //    QUALITY_FIRST only those at least as good in (Q desc, cost asc) as
+                //    the block's best feasible key;
+                //  - before that, only records whose startup+stall violation does not
+                //    exceed the block's best closest-tier violation.
                 const unsigned long long thr = s_thr[q];
-                const bool anyf = (thr != 0) | bf[q];
+                const uint32_t tq = (uint32_t)(thr >> 32), tc = ~(uint32_t)thr;
+                const bool anyf = (thr != 0) | bf[q] | (((uint32_t)mt.feas >> q) & 1u);
                 const uint64_t slo_t = P.q[q].slo_t, slo_s = P.q[q].slo_s, bud = P.q[q].budget;
                 uint32_t need = 0;
 #pragma unroll
                 for (int u = 0; u < kRPT; u++) {
                     const bool f = (r[u].w0 <= slo_t) & (r[u].w1 <= slo_s) & (r[u].w2 <= bud);
-                    const bool qok = !obj_q | (qc_key(r[u]) >= thr);
-                    need |= (uint32_t)(valid[u] & qok & (f | !anyf)) << u;
+                    const uint32_t Qr = rec_Q(r[u]);
+                    const bool qok = !obj_q | (thr == 0) | (Qr > tq) |
+                                     ((Qr == tq) & ((r[u].w2 >> 32) == 0) & ((uint32_t)r[u].w2 <= tc));
+                    need |= (uint32_t)(valid[u] & f & qok) << u;
+                }
+                if (__any_sync(0xffffffffu, !anyf)) {  // closest tier still open somewhere
+                    const unsigned long long vmax = s_vt[q];
+#pragma unroll
+                    for (int u = 0; u < kRPT; u++) {
+                        const uint64_t vt = sat_sub(r[u].w0, slo_t) + sat_sub(r[u].w1, slo_s);
+                        need |= (uint32_t)(valid[u] & !anyf & (vt <= vmax)) << u;
+                    }
                 }
                 if (__any_sync(0xffffffffu, need != 0)) {
 #pragma unroll
@@ -1122,8 +1172,14 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                         if (cand_better(P.q[q], P.objective, idx, r[u], bi[q], br[q])) {
                             bi[q] = idx;
                             br[q] = r[u];
+                            if (f) {
+                                if (!bf[q] && pa.gfeas) atomicOr(&pa.gfeas[q], 1u);
+                                atomicMax(&s_thr[q], obj_q ? (unsigned long long)qc_key(r[u]) : 1ull);
+                            } else {
+                                atomicMin(&s_vt[q], (unsigned long long)(sat_sub(r[u].w0, P.q[q].slo_t) +
+                                                                         sat_sub(r[u].w1, P.q[q].slo_s)));
+                            }
                             bf[q] = f;
-                            if (f) atomicMax(&s_thr[q], obj_q ? (unsigned long long)qc_key(r[u]) : 1ull);
                         }
                     }
                 }
@@ -1233,14 +1289,15 @@ __global__ void __launch_bounds__(kScanThreads) select_merge_kernel(const Cand* 
     }
 }
 
-// Fleet winners' full metrics: block b recomputes query q's winner of request b.
+// Fleet winners' full metrics: block b recomputes query q's winner of request b into
+// out[b * nq + q] (winners strided by SW_MAX_QUERIES).
 template <int NP>
 __global__ void detail_fleet_kernel(const EvalJob* __restrict__ jobs, const Cand* __restrict__ win, uint32_t nq,
                                     DetailOut* __restrict__ out) {
     const uint32_t b = blockIdx.x;
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
         const Cand c = win[(uint64_t)b * SW_MAX_QUERIES + q];
-        if (c.idx != kInf64) detail_one<NP>(jobs[b].hdr, jobs[b].va, c.idx, out + (uint64_t)b * SW_MAX_QUERIES + q);
+        if (c.idx != kInf64) detail_one<NP>(jobs[b].hdr, jobs[b].va, c.idx, out + (uint64_t)b * nq + q);
     }
 }
 

@@ -80,6 +80,7 @@ struct sw_plan {
     uint64_t fold_passes = 0;    // diagnostics: filter passes run
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint64_t* d_counts = nullptr;
+    uint32_t* d_gfeas = nullptr;  // [SW_MAX_QUERIES] grid-wide "feasible seen" flags of a select
 
     // select / detail / digest
     Cand* d_partial = nullptr;
@@ -502,9 +503,11 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (const char* ev = getenv("SW_PARETO_CHUNK")) h->chunk = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
-    if (set_scan_smem_attrs() != cudaSuccess) {
+    if (cudaError_t se = set_scan_smem_attrs(); se != cudaSuccess) {
         cudaGetLastError();
-        return bail(fail(nullptr, SW_ECUDA, "scan kernel smem attribute failed"));
+        return bail(fail(nullptr, SW_ECUDA, "scan kernels cannot launch one block per SM (%s; smem %zu/%zu B)",
+                         cudaGetErrorString(se), ring_bytes(true) + sizeof(Dlt) + kFrontSmem * sizeof(PPoint),
+                         ring_bytes(false)));
     }
 
     // ---- record buffer + reduction scratch
@@ -536,6 +539,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if ((st = alloc_n(h, &h->d_detail, 1, "detail")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_digest, 1, "digest")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 1, "counts")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_gfeas, SW_MAX_QUERIES, "select flags")) < 0) return bail(st);
     if (h->nranks > 1)
         if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return bail(st);
     if (cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream) != cudaSuccess)
@@ -557,7 +561,7 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
         void* bufs[] = {h->d_hdr,   h->d_va,      h->d_rec,     h->d_front, h->d_work,
                         h->d_tmp,   h->d_keep,    h->d_ctl,     h->d_dlt,
                         h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest,
-                        h->d_counts, h->d_gather, h->d_tmp2, h->d_surv};
+                        h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
         for (cudaEvent_t e : h->ev)
@@ -790,7 +794,15 @@ static cudaError_t set_attr_one() {
                                          (int)kScanSmemPareto);
     cudaError_t b = cudaFuncSetAttribute(scan_kernel<NQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kRingBytes);
-    return a != cudaSuccess ? a : b;
+    if (a != cudaSuccess) return a;
+    if (b != cudaSuccess) return b;
+    // the persistent scan needs one resident block per SM (registers x 544 threads + smem)
+    int o1 = 0, o2 = 0;
+    a = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, scan_kernel<NQ, true>, kScanBlock, kScanSmemPareto);
+    b = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, scan_kernel<NQ, false>, kScanBlock, kRingBytes);
+    if (a != cudaSuccess) return a;
+    if (b != cudaSuccess) return b;
+    return (o1 < 1 || o2 < 1) ? cudaErrorLaunchOutOfResources : cudaSuccess;
 }
 
 static cudaError_t set_scan_smem_attrs() {
@@ -809,6 +821,7 @@ static ParetoArgs pareto_args(sw_plan* h) {
     pa.ctl = h->d_ctl;
     pa.surv = h->d_surv;
     pa.cap = h->surv_cap;
+    pa.gfeas = h->d_gfeas;
     return pa;
 }
 
@@ -837,7 +850,8 @@ static sw_status reduce_async(sw_plan* h, PPoint* out) {
 // Seed the running front from a strided sample of a segment (async).
 static sw_status seed_async(sw_plan* h, const Segment& g) {
     const uint64_t n = g.end - g.begin;
-    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, h->front_cap + h->surv_cap);
+    // a strided sample seeds the running front (its exact front is cheap to reduce)
+    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, 32768);
     CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
     pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), ns, h->d_work, h->d_ctl);
     CKL(h);
@@ -913,6 +927,7 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
     for (uint32_t q = 0; q < nq; q++) P.q[q] = QueryDev{qs[q].slo_startup_us, qs[q].slo_stall_us, qs[q].budget_mc};
     uint32_t np = 0;
     std::vector<size_t> fused;
+    CK(h, cudaMemsetAsync(h->d_gfeas, 0, sizeof(uint32_t) * SW_MAX_QUERIES, h->stream));
     bool seeded = h->front_n > 0;
     for (size_t si = 0; si < h->segs.size(); si++) {
         Segment& g = h->segs[si];
@@ -1249,6 +1264,7 @@ struct sw_fleet {
     Cand* d_win = nullptr;
     Cand* d_win_all = nullptr;
     DetailOut* d_det = nullptr;
+    uint32_t* d_gfeas = nullptr;
     bool evaluated = false;
     cudaEvent_t ev[4] = {};
     uint64_t k_launches[2] = {0, 0};
@@ -1272,7 +1288,7 @@ extern "C" sw_status sw_fleet_destroy(sw_fleet* f) {
     if (!f) return SW_OK;
     if (f->stream) {
         cudaSetDevice(f->device);
-        void* bufs[] = {f->d_ejobs, f->d_sjobs, f->d_partial, f->d_win, f->d_win_all, f->d_det};
+        void* bufs[] = {f->d_ejobs, f->d_sjobs, f->d_partial, f->d_win, f->d_win_all, f->d_det, f->d_gfeas};
         for (void* b : bufs)
             if (b) cudaFreeAsync(b, f->stream);
         for (cudaEvent_t e : f->ev)
@@ -1357,7 +1373,8 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
         !alloc((void**)&f->d_partial, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n * f->gx) ||
         !alloc((void**)&f->d_win, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n) ||
         !alloc((void**)&f->d_win_all, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n * f->nranks) ||
-        !alloc((void**)&f->d_det, sizeof(DetailOut) * (size_t)n)) {
+        !alloc((void**)&f->d_det, sizeof(DetailOut) * (size_t)n) ||
+        !alloc((void**)&f->d_gfeas, sizeof(uint32_t) * SW_MAX_QUERIES * (size_t)n)) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ENOMEM, "fleet scratch allocation failed"));
     }
@@ -1464,9 +1481,12 @@ extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_se
         slots += g.ntiles * kTileRows * p->row;
     }
     CK(h, cudaMemcpyAsync(f->d_sjobs, jobs.data(), sizeof(ScanJob) * n, cudaMemcpyHostToDevice, f->stream));
+    CK(h, cudaMemsetAsync(f->d_gfeas, 0, sizeof(uint32_t) * SW_MAX_QUERIES * n, f->stream));
+    ParetoArgs pa{};
+    pa.gfeas = f->d_gfeas;
     CK(h, cudaEventRecord(f->ev[2], f->stream));
     scan_kernel<1, false><<<dim3(f->gx, n), kScanBlock, kRingBytes, f->stream>>>(SegView{}, SelParams{}, f->d_partial,
-                                                                                ParetoArgs{}, f->d_sjobs);
+                                                                                pa, f->d_sjobs);
     CKL(h);
     CK(h, cudaEventRecord(f->ev[3], f->stream));
     select_merge_kernel<<<n, kScanThreads, 0, f->stream>>>(f->d_partial, f->gx, SW_MAX_QUERIES,

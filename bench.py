@@ -175,7 +175,7 @@ def run_reference(args, pb):
                                    " + digest" % (per_step, len(pb.queries))},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -184,7 +184,21 @@ def input_bytes(pb):
             + 4 * len(pb.choices) + 4 * len(pb.level_score) + 12 * len(pb.gpus))
 
 
+def emit(line):
+    """Print the ONE JSON line on the real stdout (libraries such as NCCL may print to
+    fd 1; main() points fd 1 at stderr for the rest of the run)."""
+    _REAL_STDOUT.write(json.dumps(line) + "\n")
+    _REAL_STDOUT.flush()
+
+
+_REAL_STDOUT = sys.stdout
+
+
 def main():
+    global _REAL_STDOUT
+    _REAL_STDOUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -353,7 +367,7 @@ def main():
             "parity": parity,
             "front_points": len(front),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if comm:
         sw.comm_destroy(comm)
     if world > 1:

@@ -242,6 +242,21 @@ sw_status sw_plan_records(const sw_plan *h, const sw_record **dev_ptr, uint64_t 
  * segment) into host memory. */
 sw_status sw_plan_copy_records(sw_plan *h, uint64_t index, uint64_t n, sw_record *host_out);
 
+/* ---- greedy + iterative refinement planner ------------ */
+
+/* The paper's provisioner on the batched evaluator: start from the
+ * cost-efficient baseline (start_index = UINT64_MAX: per digit the choice with the
+ * smallest (level score, k, pool price)) or from start_index (a warm start,
+ * P:1341), then repeatedly evaluate every single-digit change in parallel (one GPU
+ * thread each) and move to the best one under the query's total order (R13)
+ * while it is strictly better; stop at a local optimum (reading R28).  Needs no
+ * records (runs on the tables).  *out = the plan with full detail; status SW_OK
+ * (feasible) or SW_CLOSEST; *iterations = moves made, *evaluations = plans evaluated
+ * (either may be NULL).  Synchronises; replicated (no collective) when nranks > 1. */
+sw_status sw_plan_greedy(sw_plan *h, uint64_t slo_startup_us, uint64_t slo_stall_us,
+                         uint64_t budget_mc, uint64_t start_index, sw_selection *out,
+                         uint32_t *iterations, uint64_t *evaluations);
+
 /* ---- host-only helpers (no device needed) ---------------------------------- */
 
 /* Size of the plan space N = prod r_b and the row size (candidates per eval-kernel

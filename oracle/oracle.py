@@ -211,6 +211,20 @@ class Oracle:
         return winners, front, dg.value
 
 
+def greedy(orc, query, start=None):
+    """Greedy + iterative refinement planner (R28) on the oracle:
+    -> (status, index, Rec, iterations, evaluations); status 0 feasible, 1 closest."""
+    q = OrQuery(query.slo_startup_us, query.slo_stall_us, query.budget_mc)
+    idx = C.c_uint64()
+    rec = OrRecord()
+    st = C.c_int32()
+    it = C.c_uint32()
+    ev = C.c_uint64()
+    lib().or_greedy(C.byref(orc.c), C.byref(q), C.c_uint64((1 << 64) - 1 if start is None else start),
+                    C.byref(idx), C.byref(rec), C.byref(st), C.byref(it), C.byref(ev))
+    return st.value, idx.value, _rec(rec), it.value, ev.value
+
+
 def pareto_points(points):
     """Plain O(n^2) Pareto front of explicit (index, ttff_eff, cost, Q) tuples."""
     n = len(points)

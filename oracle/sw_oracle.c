@@ -445,6 +445,90 @@ uint64_t or_pareto_points(const or_point *pts, uint64_t n, or_point *out) {
     return nf;
 }
 
+/* ---- greedy + iterative refinement planner -------------
+ * The paper's provisioner: "Initial provisioning: we start with a
+ * cost-efficient baseline configuration that leverages inexpensive models and
+ * lower-cost GPUs. Each model instance ... is assigned a single GPU";
+ * "Iterative refinement: ... systematically exploring the latency-cost trade-off
+ * space. For each setting, we use the greedy algorithm to estimate the latency and
+ * cost", switching GPU types, models and GPU allocation per instance
+ * (P:906-911), minimising the objective and steering toward the SLO, "If we cannot
+ * find feasible solutions, it returns the closest solution".
+ * Reading R28: the baseline takes, in every digit, the choice with the
+ * smallest (level score, k, pool price, choice index); a refinement step evaluates
+ * every single-digit change of the current plan (switch model = level, GPU type =
+ * pool, parallelism = k) and moves to the best one under the query's total order
+ * (feasible first by the objective key, else closest) if it is strictly better than
+ * the current plan; it stops when none is (steepest descent to a local optimum). */
+static int query_better(uint32_t objective, const or_query *q, uint64_t ia, const or_record *a,
+                        uint64_t ib, const or_record *b) {
+    int fa = feasible(q, a), fb = feasible(q, b);
+    if (fa != fb) return fa;
+    if (fa) return obj_cmp(objective, ia, a, ib, b) < 0;
+    return closest_cmp(objective, q, ia, a, ib, b) < 0;
+}
+
+int or_greedy(const or_problem *pb, const or_query *q, uint64_t start, uint64_t *out_index,
+              or_record *out_rec, int32_t *status, uint32_t *iterations, uint64_t *evaluations) {
+    uint64_t *a = malloc(sizeof(uint64_t) * pb->S), *P = malloc(sizeof(uint64_t) * pb->S);
+    or_fixed_stages(pb, a);
+    or_deadlines(pb, P);
+    uint64_t place[64];
+    uint64_t pl = 1;
+    for (int b = (int)pb->B - 1; b >= 0; b--) { place[b] = pl; pl *= pb->radix[b]; }
+    uint32_t dig[64];
+    if (start == UINT64_MAX) { /* cost-efficient baseline */
+        uint32_t coff = 0;
+        start = 0;
+        for (uint32_t b = 0; b < pb->B; b++) {
+            uint32_t best = 0;
+            for (uint32_t c = 1; c < pb->radix[b]; c++) {
+                uint32_t x = coff + c, y = coff + best;
+                uint64_t kx[3] = {pb->level_score[pb->choice_level[x]], pb->choice_k[x], pb->price_mc[pb->choice_pool[x]]};
+                uint64_t ky[3] = {pb->level_score[pb->choice_level[y]], pb->choice_k[y], pb->price_mc[pb->choice_pool[y]]};
+                int lt = 0;
+                for (int i = 0; i < 3; i++) if (kx[i] != ky[i]) { lt = kx[i] < ky[i]; goto decided; }
+                lt = 0; /* equal keys: keep the lower choice index */
+            decided:
+                if (lt) best = c;
+            }
+            start += best * place[b];
+            coff += pb->radix[b];
+        }
+    }
+    uint64_t cur = start;
+    or_record rc;
+    or_eval_detail(pb, a, P, cur, &rc, NULL, NULL, NULL, NULL);
+    uint64_t evals = 1;
+    uint32_t it = 0;
+    for (;;) {
+        or_decode(pb, cur, dig);
+        uint64_t bi = UINT64_MAX;
+        or_record br;
+        for (uint32_t b = 0; b < pb->B; b++)
+            for (uint32_t c = 0; c < pb->radix[b]; c++) {
+                if (c == dig[b]) continue;
+                uint64_t x = cur - (uint64_t)dig[b] * place[b] + (uint64_t)c * place[b];
+                or_record r;
+                or_eval_detail(pb, a, P, x, &r, NULL, NULL, NULL, NULL);
+                evals++;
+                if (bi == UINT64_MAX || query_better(pb->objective, q, x, &r, bi, &br)) { bi = x; br = r; }
+            }
+        if (bi == UINT64_MAX || !query_better(pb->objective, q, bi, &br, cur, &rc)) break;
+        cur = bi;
+        rc = br;
+        it++;
+    }
+    *out_index = cur;
+    *out_rec = rc;
+    *status = feasible(q, &rc) ? 0 : 1;
+    *iterations = it;
+    *evaluations = evals;
+    free(a);
+    free(P);
+    return 0;
+}
+
 int or_abi_version(void) { return 1; }
 uint32_t or_sizeof_record(void) { return (uint32_t)sizeof(or_record); }
 uint32_t or_sizeof_winner(void) { return (uint32_t)sizeof(or_winner); }

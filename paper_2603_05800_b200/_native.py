@@ -98,6 +98,8 @@ EXPORTS = {
                                          C.POINTER(sw_selection)]),
     "sw_plan_sweep": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
                                   C.POINTER(sw_query), C.POINTER(sw_selection), U64P]),
+    "sw_plan_greedy": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                   C.POINTER(sw_selection), C.POINTER(C.c_uint32), U64P]),
     "sw_pareto_get": (C.c_int32, [C.c_void_p, C.POINTER(sw_pareto_point), C.c_uint64, U64P]),
     "sw_plan_digest": (C.c_int32, [C.c_void_p, U64P]),
     "sw_plan_detail": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(sw_selection), U64P]),
@@ -373,6 +375,18 @@ class Plan:
         self._ck(lib().sw_plan_sweep(self.h, begin, end, chunk, len(qs), arr, out,
                                      C.byref(d) if digest else None))
         return [_sel(o, self.n_pools, self.B) for o in out[: len(qs)]], (d.value if digest else None)
+
+    def greedy(self, query=None, start: Optional[int] = None):
+        """Greedy + refinement planner (sw_plan_greedy) -> (Selection, iterations,
+        evaluations).  query: object / 3-tuple (None = unconstrained)."""
+        q = (UINT64_MAX,) * 3 if query is None else (
+            query if isinstance(query, tuple) else (query.slo_startup_us, query.slo_stall_us,
+                                                    query.budget_mc))
+        out = sw_selection()
+        it, ev = C.c_uint32(), C.c_uint64()
+        self._ck(lib().sw_plan_greedy(self.h, q[0], q[1], q[2], UINT64_MAX if start is None else start,
+                                      C.byref(out), C.byref(it), C.byref(ev)))
+        return _sel(out, self.n_pools, self.B), it.value, ev.value
 
     def pareto(self):
         n = C.c_uint64()

@@ -30,6 +30,12 @@ struct SegView {
     uint64_t ntiles;
     uint64_t row;
     uint64_t ib, ie;
+    // Strided fold passes (scan kernels only): the view is cut into units of `upt`
+    // tiles (a whole number of scan stages); pass 1 scans units u % 64 == 0, pass 2
+    // u % 8 == 0 && u % 64 != 0, pass 3 u % 8 != 0 -- each pass a uniform sample of the
+    // whole segment, so the Pareto filter sees every region of the space early.
+    // pass 0: the whole view in order.
+    uint32_t pass, upt;
 };
 constexpr int kScanThreads = 256;
 constexpr int kDltT = 128;  // dominance lookup table: ttff_eff bins (front quantiles)
@@ -268,16 +274,9 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(EvalJob job, const E
             const uint32_t k = ch_k(ch), p = ch_pool(ch);
             const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
             const VaEntry* vb = va + h.voff[b] + c;
-            // k differs across lanes here, but a divergent switch over the compile-time
-            // gang updates (each ~15x cheaper than the runtime-k barrel shift) wins even
-            // when a warp takes all four paths
-            switch (k) {
-                case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
-                case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
-                case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
-                case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
-                default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
-            }
+            // k differs across lanes here: the runtime-k gang update (a divergent switch
+            // over the compile-time variants measured 12% slower overall on C2)
+            run_block<NP, 0>(st, h, p, k, f0, f1, vb, r);
         }
         // ---- MID digit: warp-uniform choice
         for (uint32_t dm = 0; dm < rm; dm++) {
@@ -1051,7 +1050,21 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     __syncthreads();
     const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
     const uint64_t total = v.ntiles * per_tile;
-    const uint64_t nstages = (total + kStageRecs - 1) / kStageRecs;
+    // stage sg of this view/pass -> flat slot of its first record (kInf64: none)
+    const uint64_t unit_recs = (uint64_t)v.upt * per_tile;
+    const uint64_t spu = v.pass ? unit_recs / kStageRecs : 1;
+    const uint64_t nunits = v.pass ? (total + unit_recs - 1) / unit_recs : 0;
+    const uint64_t k8 = (nunits + 7) / 8, k64 = (nunits + 63) / 64;
+    const uint64_t nstages = v.pass == 0 ? (total + kStageRecs - 1) / kStageRecs
+                                         : spu * (v.pass == 1 ? k64 : v.pass == 2 ? k8 - k64 : nunits - k8);
+    auto stage_pos = [&](uint64_t sg) -> uint64_t {
+        if (v.pass == 0) return sg * kStageRecs;
+        const uint64_t j = sg / spu, part = sg - j * spu;
+        const uint64_t m = (j / 7) * 8 + (j % 7) + 1;  // j-th positive non-multiple of 8
+        const uint64_t u = v.pass == 1 ? 64 * j : v.pass == 2 ? 8 * m : m;
+        const uint64_t pos = u * unit_recs + part * kStageRecs;
+        return pos < total ? pos : kInf64;
+    };
     // one running best per query under the query's total order (feasible first)
     uint64_t bi[NQA];
     Rec4 br[NQA];
@@ -1071,8 +1084,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
             // ring only has to cover L2 latency): prime the first ones
             for (uint32_t pf = 0; pf < kPrefetch; pf++) {
                 const uint64_t sp = blockIdx.x + (uint64_t)pf * gridDim.x;
-                if (sp < nstages)
-                    tma_prefetch_l2(v.recs + sp * kStageRecs, (uint32_t)umin64(kStageRecs, total - sp * kStageRecs) * (uint32_t)sizeof(Rec4));
+                const uint64_t pp = sp < nstages ? stage_pos(sp) : kInf64;
+                if (pp != kInf64)
+                    tma_prefetch_l2(v.recs + pp, (uint32_t)umin64(kStageRecs, total - pp) * (uint32_t)sizeof(Rec4));
             }
             uint32_t fm = 0;  // grid-wide feasibility flags, loaded one stage ahead
             for (uint64_t sg = blockIdx.x; sg < nstages; sg += gridDim.x, it++) {
@@ -1083,11 +1097,16 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                         fm_next |= (*(volatile const uint32_t*)&pa.gfeas[q] != 0 ? 1u : 0u) << q;
                 }
                 const uint64_t sp = sg + (uint64_t)kPrefetch * gridDim.x;
-                if (sp < nstages)
-                    tma_prefetch_l2(v.recs + sp * kStageRecs, (uint32_t)umin64(kStageRecs, total - sp * kStageRecs) * (uint32_t)sizeof(Rec4));
+                const uint64_t pp = sp < nstages ? stage_pos(sp) : kInf64;
+                if (pp != kInf64)
+                    tma_prefetch_l2(v.recs + pp, (uint32_t)umin64(kStageRecs, total - pp) * (uint32_t)sizeof(Rec4));
+                const uint64_t pos0 = stage_pos(sg);
+                if (pos0 == kInf64) {  // past the partial last unit: no stage
+                    it--;
+                    continue;
+                }
                 const uint32_t st = it % NS, k = it / NS;
                 if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
-                const uint64_t pos0 = sg * kStageRecs;
                 const uint32_t cnt = (uint32_t)umin64(kStageRecs, total - pos0);
                 // tile padding lives only in the first and the last tile of a segment
                 const bool edge = pos0 < per_tile || pos0 + cnt > total - per_tile;
@@ -1126,8 +1145,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                     const uint64_t i0 = flat_index(v, per_tile, mt.pos0 + o);
                     valid[u] = i0 >= v.ib && i0 < v.ie;
                 }
-                if (valid[u]) r[u] = ring[(size_t)st * kStageRecs + o];
-                else r[u] = Rec4{};
+                // unconditional: a slot past cnt holds stale bytes that valid[] masks out
+                r[u] = ring[(size_t)st * kStageRecs + o];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage data is in registers now
@@ -1298,6 +1317,152 @@ __global__ void detail_fleet_kernel(const EvalJob* __restrict__ jobs, const Cand
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
         const Cand c = win[(uint64_t)b * SW_MAX_QUERIES + q];
         if (c.idx != kInf64) detail_one<NP>(jobs[b].hdr, jobs[b].va, c.idx, out + (uint64_t)b * nq + q);
+    }
+}
+
+// ============================================================================ greedy planner
+// The paper's provisioner on the batched evaluator:
+// a cost-efficient baseline -- per digit the choice with the smallest (level score, k,
+// pool price, index): cheap models, one GPU, cheap GPUs -- then iterative
+// refinement: every single-digit change of the current plan (switch model / GPU type /
+// parallelism) is evaluated by one thread in parallel, the best under the
+// query's total order is taken if strictly better; stop at a local optimum.
+// One CTA runs the whole search (R28).
+constexpr int kGreedyThreads = 1024;
+constexpr int kMaxLevels = 16;
+
+struct GreedyArgs {
+    QueryDev q;
+    uint32_t objective, n_levels;
+    uint64_t start;  // kInf64: the cost-efficient baseline
+    uint32_t score[kMaxLevels];
+    uint32_t max_iter;
+};
+struct GreedyOut {
+    uint64_t index;
+    Rec4 rec;
+    uint64_t evaluations;
+    uint32_t iterations, feasible;
+};
+
+// One candidate's record by full recompute (compile-time gang updates per block).
+template <int NP>
+__device__ Rec4 full_eval(const DevHeader& h, const VaEntry* __restrict__ va, uint64_t index) {
+    State<NP> st;
+    state_init(st, h);
+    uint32_t dig[kMaxDigits];
+    uint64_t rem = index;
+    for (int b = (int)h.B - 1; b >= 0; b--) {
+        dig[b] = (uint32_t)(rem % h.radix[b]);
+        rem /= h.radix[b];
+    }
+    for (uint32_t b = 0; b < h.B; b++) {
+        const uint32_t ch = h.choice[h.coff[b] + dig[b]];
+        const uint32_t k = ch_k(ch), p = ch_pool(ch);
+        const VaEntry* vb = va + h.voff[b] + dig[b];
+        const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
+        switch (k) {
+            case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
+            case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
+            case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
+            case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
+            default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
+        }
+    }
+    Rec4 o;
+    o.w0 = st.R0;
+    o.w1 = (uint64_t)st.M - st.R0;
+    o.w2 = state_cost(st, h);
+    o.w3 = (uint64_t)st.Q | ((uint64_t)st.cnt << 32) | ((uint64_t)st.used << 48);
+    return o;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(const DevHeader* __restrict__ g_hdr,
+                                                               const VaEntry* __restrict__ g_va, GreedyArgs A,
+                                                               GreedyOut* __restrict__ out) {
+    __shared__ Cand s_tmp[32];
+    __shared__ uint64_t s_place[kMaxDigits];
+    __shared__ uint32_t s_dig[kMaxDigits], s_nboff[kMaxDigits + 1];
+    __shared__ uint64_t s_cur;
+    __shared__ Rec4 s_rec;
+    __shared__ int s_done;
+    const DevHeader& h = *g_hdr;
+    const uint32_t B = h.B;
+    if (threadIdx.x == 0) {
+        uint64_t pl = 1;
+        for (int b = (int)B - 1; b >= 0; b--) {
+            s_place[b] = pl;
+            pl *= h.radix[b];
+        }
+        s_nboff[0] = 0;
+        for (uint32_t b = 0; b < B; b++) s_nboff[b + 1] = s_nboff[b] + h.radix[b] - 1;
+        uint64_t cur = A.start;
+        if (cur == kInf64) {  // cost-efficient baseline
+            cur = 0;
+            for (uint32_t b = 0; b < B; b++) {
+                uint32_t best = 0;
+                for (uint32_t c = 1; c < h.radix[b]; c++) {
+                    const uint32_t x = h.choice[h.coff[b] + c], y = h.choice[h.coff[b] + best];
+                    const uint32_t sx = A.score[ch_level(x)], sy = A.score[ch_level(y)];
+                    const uint64_t px = h.price[ch_pool(x)], py = h.price[ch_pool(y)];
+                    const bool lt = sx != sy ? sx < sy : (ch_k(x) != ch_k(y) ? ch_k(x) < ch_k(y) : px < py);
+                    if (lt) best = c;
+                }
+                cur += best * s_place[b];
+            }
+        }
+        s_cur = cur;
+        s_rec = full_eval<NP>(h, g_va, cur);
+        s_done = 0;
+    }
+    __syncthreads();
+    uint32_t iters = 0;
+    uint64_t evals = 1;
+    const uint32_t n_nb = s_nboff[B];
+    while (true) {
+        if (threadIdx.x == 0) {
+            uint64_t rem = s_cur;
+            for (int b = (int)B - 1; b >= 0; b--) {
+                s_dig[b] = (uint32_t)(rem % h.radix[b]);
+                rem /= h.radix[b];
+            }
+        }
+        __syncthreads();
+        uint64_t idx = kInf64;
+        Rec4 r{};
+        for (uint32_t t = threadIdx.x; t < n_nb; t += blockDim.x) {  // one neighbour per thread
+            uint32_t b = 0;
+            while (t >= s_nboff[b + 1]) b++;
+            uint32_t c = t - s_nboff[b];
+            if (c >= s_dig[b]) c++;  // skip the current choice
+            const uint64_t x = s_cur - (uint64_t)s_dig[b] * s_place[b] + (uint64_t)c * s_place[b];
+            const Rec4 rx = full_eval<NP>(h, g_va, x);
+            if (cand_better(A.q, A.objective, x, rx, idx, r)) {
+                idx = x;
+                r = rx;
+            }
+        }
+        block_reduce_cand(A.q, A.objective, idx, r, s_tmp);
+        evals += n_nb;
+        if (threadIdx.x == 0) {
+            if (idx != kInf64 && iters < A.max_iter && cand_better(A.q, A.objective, idx, r, s_cur, s_rec)) {
+                s_cur = idx;
+                s_rec = r;
+            } else {
+                s_done = 1;
+            }
+        }
+        __syncthreads();
+        if (s_done) break;
+        iters++;
+    }
+    if (threadIdx.x == 0) {
+        out->index = s_cur;
+        out->rec = s_rec;
+        out->iterations = iters;
+        out->evaluations = evals;
+        out->feasible = feasible(A.q, s_rec) ? 1u : 0u;
     }
 }
 

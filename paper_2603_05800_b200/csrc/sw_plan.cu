@@ -78,9 +78,13 @@ struct sw_plan {
     bool fuse_pareto = true;     // fold unfolded segments inside select scans
     uint64_t chunk = 1ull << 25; // records per fold chunk (the front improves per chunk)
     uint64_t fold_passes = 0;    // diagnostics: filter passes run
+    uint64_t epoch = 1;          // bumped by every change of records or front
+    uint64_t merged_epoch = 0, merged_n = 0;  // multi-rank merged front cached in d_gather
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint64_t* d_counts = nullptr;
     uint32_t* d_gfeas = nullptr;  // [SW_MAX_QUERIES] grid-wide "feasible seen" flags of a select
+    GreedyOut* d_greedy = nullptr;
+    std::vector<uint32_t> level_score;  // for the greedy baseline (host copy of the input)
 
     // select / detail / digest
     Cand* d_partial = nullptr;
@@ -88,7 +92,8 @@ struct sw_plan {
     uint32_t max_partial = 0;
     Cand* d_cand = nullptr;
     Cand* d_cand_all = nullptr;
-    DetailOut* d_detail = nullptr;
+    DetailOut* d_detail = nullptr;  // [SW_MAX_QUERIES]
+    EvalJob* d_selfjob = nullptr;   // this handle's tables as a 1-entry job list
     unsigned long long* d_digest = nullptr;
 
     // CUDA events around every eval-kernel launch, on the handle's stream: a ring of
@@ -198,6 +203,8 @@ static SegView view_of(const sw_plan* h, const Segment& g, uint64_t t_lo, uint64
     v.row = h->row;
     v.ib = g.begin;
     v.ie = g.end;
+    v.pass = 0;
+    v.upt = 1;
     return v;
 }
 static cudaError_t set_scan_smem_attrs();
@@ -536,10 +543,18 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if ((st = alloc_n(h, &h->d_partial, (uint64_t)h->max_partial * SW_MAX_QUERIES, "partials")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_cand, SW_MAX_QUERIES, "winners")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_cand_all, (uint64_t)SW_MAX_QUERIES * h->nranks, "winners all")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_detail, 1, "detail")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_detail, SW_MAX_QUERIES, "detail")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_selfjob, 1, "self job")) < 0) return bail(st);
+    {
+        const EvalJob sj{h->d_hdr, h->d_va, h->va_bytes, 0, 0, nullptr};
+        if (cudaMemcpyAsync(h->d_selfjob, &sj, sizeof sj, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+            return bail(fail(nullptr, SW_ECUDA, "self job upload failed"));
+    }
     if ((st = alloc_n(h, &h->d_digest, 1, "digest")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 1, "counts")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_gfeas, SW_MAX_QUERIES, "select flags")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_greedy, 1, "greedy result")) < 0) return bail(st);
+    h->level_score.assign(tb->level_score, tb->level_score + tb->n_levels);
     if (h->nranks > 1)
         if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return bail(st);
     if (cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream) != cudaSuccess)
@@ -560,8 +575,8 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
         cudaSetDevice(h->device);
         void* bufs[] = {h->d_hdr,   h->d_va,      h->d_rec,     h->d_front, h->d_work,
                         h->d_tmp,   h->d_keep,    h->d_ctl,     h->d_dlt,
-                        h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest,
-                        h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas};
+                        h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest, h->d_selfjob,
+                        h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas, h->d_greedy};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
         for (cudaEvent_t e : h->ev)
@@ -575,6 +590,7 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
 
 extern "C" sw_status sw_plan_reset(sw_plan* h) {
     if (!h) return fail(nullptr, SW_EINVAL, "null handle");
+    h->epoch++;
     h->segs.clear();
     h->rec_used = 0;
     h->cand_used = 0;
@@ -688,6 +704,7 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
         return fail(h, SW_ERANGE, "record buffer fragmented by more than %llu eval calls: reset or chunk",
                     (unsigned long long)kMaxSegs);
     Segment sg{begin, end, b, e, h->rec_used, t0, n ? t1 - t0 : 0, false};
+    h->epoch++;
     CK(h, cudaSetDevice(h->device));
     if (n > 0) {
         const uint64_t need = (sg.ntiles * kTileRows + kEvalThreads - 1) / kEvalThreads;  // one warp per tile
@@ -737,6 +754,9 @@ extern "C" sw_status sw_plan_kernel_time(sw_plan* h, uint32_t kind, uint64_t* n_
 }
 
 // ============================================================================ select
+static void detail_to_selection(const sw_plan* h, uint64_t index, const DetailOut& d, sw_selection* out,
+                                uint64_t* ready);
+
 static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint64_t* ready) {
     launch_np(h, [&](auto np) {
         constexpr int NPc = decltype(np)::value;
@@ -746,6 +766,12 @@ static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint
     DetailOut d;
     CK(h, cudaMemcpyAsync(&d, h->d_detail, sizeof d, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
+    detail_to_selection(h, index, d, out, ready);
+    return SW_OK;
+}
+
+static void detail_to_selection(const sw_plan* h, uint64_t index, const DetailOut& d, sw_selection* out,
+                                uint64_t* ready) {
     out->index = index;
     out->rec.ttff_us = d.rec.w0;
     out->rec.stall_us = d.rec.w1;
@@ -760,7 +786,6 @@ static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint
     memset(out->digit, 0, sizeof out->digit);
     for (uint32_t b = 0; b < h->B_user; b++) out->digit[b] = (uint8_t)d.digit[b + h->pad_digits];
     if (ready) memcpy(ready, d.ready, sizeof(uint64_t) * h->S);
-    return SW_OK;
 }
 
 template <int NQ, bool PARETO>
@@ -862,18 +887,33 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
 // chunk (fused with nq select queries when nq > 0), survivors merged on the device.
 static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
     const size_t psmem = kScanSmemPareto;
-    // geometric chunks: the front sharpens on small early chunks, later chunks are big
+    // strided passes: units of upt tiles (a whole number of scan stages); pass 1 = every
+    // 64th unit, pass 2 = the other multiples of 8, pass 3 = the rest -- each a uniform
+    // sample of the segment, so the front (and its DLT filter) is close to final after
+    // the first 1/64.  Small segments: one pass over everything.
     const uint64_t per_tile = kTileRows * h->row;
-    uint64_t ct = std::max<uint64_t>(1, (h->chunk >> 4) / per_tile);
-    const uint64_t ct_max = std::max<uint64_t>(1, (h->chunk << 3) / per_tile);
-    for (uint64_t c0 = 0, c1 = 0; c0 < g.ntiles; c0 = c1, ct = std::min(ct_max, ct * 4)) {
-        c1 = std::min(g.ntiles, c0 + ct);
+    uint32_t upt = 1;
+    while ((upt * per_tile) % kStageRecs) upt++;
+    const uint64_t unit_recs = upt * per_tile;
+    const uint64_t total = g.ntiles * per_tile;
+    const uint64_t nunits = (total + unit_recs - 1) / unit_recs;
+    const bool strided = nunits >= 256;
+    const uint64_t k8 = (nunits + 7) / 8, k64 = (nunits + 63) / 64;
+    const uint64_t last_short = nunits * unit_recs - total;  // missing slots of the last unit
+    for (uint32_t pass = strided ? 1 : 0; pass <= (strided ? 3u : 0u); pass++) {
+        uint64_t units = pass == 0 ? nunits : pass == 1 ? k64 : pass == 2 ? k8 - k64 : nunits - k8;
+        const uint64_t L = nunits - 1;  // which pass holds the (possibly short) last unit
+        const uint32_t lp = (L % 64 == 0) ? 1 : (L % 8 == 0) ? 2 : 3;
+        const uint64_t recs = units * unit_recs - ((pass == 0 || pass == lp) ? last_short : 0);
+        SegView v = view_of(h, g, 0, g.ntiles);
+        v.pass = pass;
+        v.upt = upt;
         dlt_head_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         dlt_cell_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(c1 - c0, h->scan_grid);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / kStageRecs), h->scan_grid);
         Cand* part = h->d_partial;
         if (nq) {
             if (*np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many chunks for one select");
@@ -881,9 +921,9 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
             *np += grid;
         }
         int pr = 0;
-        sw_status ts = begin_timed(h, SW_KERNEL_SCAN, (c1 - c0) * per_tile * sizeof(Rec4), &pr);
+        sw_status ts = begin_timed(h, SW_KERNEL_SCAN, recs * sizeof(Rec4), &pr);
         if (ts < 0) return ts;
-        launch_scan_nq<true>(nq, grid, psmem, h->stream, view_of(h, g, c0, c1), P, part, pareto_args(h));
+        launch_scan_nq<true>(nq, grid, psmem, h->stream, v, P, part, pareto_args(h));
         CKL(h);
         if ((ts = end_timed(h, pr)) < 0) return ts;
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
@@ -892,12 +932,13 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         sw_status st = reduce_async(h, h->d_front);
         if (st < 0) return st;
         h->fold_passes++;
+        h->epoch++;
         if (h->debug) {  // diagnostics only: synchronises every pass
             ParetoCtl c;
             CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
             CK(h, cudaStreamSynchronize(h->stream));
-            fprintf(stderr, "[sw] fold pass %llu: tiles [%llu,%llu) survivors %llu merge-in %u local %u/%u front %llu\n",
-                    (unsigned long long)h->fold_passes, (unsigned long long)c0, (unsigned long long)c1,
+            fprintf(stderr, "[sw] fold pass %llu: stride pass %u, %llu records, survivors %llu merge-in %u local %u/%u front %llu\n",
+                    (unsigned long long)h->fold_passes, pass, (unsigned long long)recs,
                     (unsigned long long)c.surv, c.m_in, c.m_loc, c.m_loc2, (unsigned long long)c.front_n);
         }
     }
@@ -972,8 +1013,16 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
         select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_cand_all, (uint32_t)h->nranks, P, h->d_cand);
         CKL(h);
     }
+    // every winner's full metrics in one launch, read back with the winners (one sync)
+    launch_np(h, [&](auto npc) {
+        constexpr int NPc = decltype(npc)::value;
+        detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nq, h->d_detail);
+    });
+    CKL(h);
     Cand win[SW_MAX_QUERIES];
+    DetailOut det[SW_MAX_QUERIES];
     CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nq, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nq, cudaMemcpyDeviceToHost, h->stream));
     if (!fused.empty()) {
         bool overflow = false;
         sw_status st = sync_ctl(h, &overflow);
@@ -991,8 +1040,7 @@ extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_quer
             worst = std::max<sw_status>(worst, SW_EMPTY);
             continue;
         }
-        sw_status st = fill_detail(h, win[q].idx, &out[q], nullptr);
-        if (st < 0) return st;
+        detail_to_selection(h, win[q].idx, det[q], &out[q], nullptr);
         out[q].status = win[q].pad ? SW_CLOSEST : SW_OK;  // feasibility flag set on device
         worst = std::max<sw_status>(worst, out[q].status);
     }
@@ -1122,7 +1170,10 @@ extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t ca
     if (st < 0) return st;
     const PPoint* res = h->d_front;
     uint64_t n = h->front_n;
-    if (h->nranks > 1) {  // a10: allgather counts, then padded fronts; exact merge
+    if (h->nranks > 1 && h->merged_epoch == h->epoch) {  // same state: the cached merge
+        n = h->merged_n;
+        res = h->d_gather;
+    } else if (h->nranks > 1) {  // a10: allgather counts, then padded fronts; exact merge
         uint64_t mine = h->front_n;
         CK(h, cudaMemcpyAsync(h->d_counts + h->nranks, &mine, 8, cudaMemcpyHostToDevice, h->stream));
         CKN(h, ncclAllGather(h->d_counts + h->nranks, h->d_counts, 1, ncclUint64, h->comm, h->stream));
@@ -1151,6 +1202,8 @@ extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t ca
         n = h->front_n;
         res = h->d_gather;
         h->front_n = mine;
+        h->merged_epoch = h->epoch;
+        h->merged_n = n;
         CK(h, cudaMemcpyAsync(&h->d_ctl->front_n, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
         CK(h, cudaStreamSynchronize(h->stream));
     }
@@ -1192,6 +1245,37 @@ extern "C" sw_status sw_plan_copy_records(sw_plan* h, uint64_t index, uint64_t n
         }
     }
     return fail(h, SW_EINVAL, "range not inside one local segment");
+}
+
+// ============================================================================ greedy planner
+extern "C" sw_status sw_plan_greedy(sw_plan* h, uint64_t slo_startup_us, uint64_t slo_stall_us, uint64_t budget_mc,
+                                    uint64_t start_index, sw_selection* out, uint32_t* iterations,
+                                    uint64_t* evaluations) {
+    if (!h || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (start_index != UINT64_MAX && start_index >= h->N) return fail(h, SW_EINVAL, "start index out of range");
+    if (h->level_score.size() > (size_t)kMaxLevels) return fail(h, SW_EINVAL, "greedy supports <= %d levels", kMaxLevels);
+    CK(h, cudaSetDevice(h->device));
+    GreedyArgs A{};
+    A.q = QueryDev{slo_startup_us, slo_stall_us, budget_mc};
+    A.objective = (h->h.flags & 4u) ? 1u : 0u;
+    A.n_levels = (uint32_t)h->level_score.size();
+    for (size_t l = 0; l < h->level_score.size(); l++) A.score[l] = h->level_score[l];
+    A.start = start_index == UINT64_MAX ? kInf64 : start_index;
+    A.max_iter = 1u << 20;
+    launch_np(h, [&](auto np) {
+        constexpr int NPc = decltype(np)::value;
+        greedy_kernel<NPc><<<1, kGreedyThreads, 0, h->stream>>>(h->d_hdr, h->d_va, A, h->d_greedy);
+    });
+    CKL(h);
+    GreedyOut g;
+    CK(h, cudaMemcpyAsync(&g, h->d_greedy, sizeof g, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    sw_status st = fill_detail(h, g.index, out, nullptr);
+    if (st < 0) return st;
+    out->status = g.feasible ? SW_OK : SW_CLOSEST;
+    if (iterations) *iterations = g.iterations;
+    if (evaluations) *evaluations = g.evaluations;
+    return out->status;
 }
 
 // ============================================================================ host helpers

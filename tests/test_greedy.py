@@ -1,0 +1,154 @@
+"""Greedy + iterative refinement planner (R28).
+
+CPU pins of the oracle's planner (no GPU): every result is a local optimum (no
+single-digit change is strictly better, checked here with an independent statement
+of the query order on records the oracle's pinned evaluator produces), it is never
+better than the exhaustive winner, a start at the exhaustive winner stays there, the
+evaluation count is 1 + (moves + 1) x sum(r_b - 1), and the baseline is the
+per-digit cheapest choice.  GPU: the CUDA planner equals the oracle's bit for bit.
+"""
+import random
+
+import pytest
+
+from swgen import make_config, INF
+from swgen.generator import Query
+from tests.conftest import cuda_available
+from tests.helpers import random_problem
+
+
+def _better(q, objective, ia, a, ib, b):
+    """Independent statement of the query's total order (R13) on records
+    (ttff, stall, cost, Q, cnt, flags)."""
+    def feas(r):
+        return r[0] <= q.slo_startup_us and r[1] <= q.slo_stall_us and r[2] <= q.budget_mc
+
+    def obj(i, r):
+        t = r[0] + r[1]
+        return ((-r[3], r[2], t) if objective == 0 else (r[2] * t, -r[3])) + (i,)
+
+    def close(i, r):
+        vt = max(r[0] - q.slo_startup_us, 0) + max(r[1] - q.slo_stall_us, 0)
+        return (vt, max(r[2] - q.budget_mc, 0)) + obj(i, r)
+    fa, fb = feas(a), feas(b)
+    if fa != fb:
+        return fa
+    return (obj(ia, a) < obj(ib, b)) if fa else (close(ia, a) < close(ib, b))
+
+
+def _golden_winner(pb, q):
+    """Exhaustive winner from tests/golden (written by tools/gen_golden.py from oracle/)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "oracle_%s.json" % pb.name)
+    if not os.path.exists(path):
+        return None
+    g = json.load(open(path))
+    for gq, w in zip(g["queries"], g["winners"]):
+        if tuple(gq) == (q.slo_startup_us, q.slo_stall_us, q.budget_mc):
+            return w["status"], w["index"], tuple(w["rec"])
+    return None
+
+
+def _rec_of(orc, i):
+    return orc.record_list(i, i + 1)[0].astuple()
+
+
+def _cases():
+    out = [(make_config(c), q) for c in ("C1", "C2", "C3") for q in make_config(c).queries]
+    # (problem, query); the config cases also carry their exhaustive golden winner
+    for seed in range(8):
+        rng = random.Random(500 + seed)
+        pb = random_problem(rng, max_scenes=6, max_pools=3, max_choices=5,
+                            one_scene_digits=rng.random() < 0.5)
+        qs = [Query(INF, INF, INF),
+              Query(rng.randint(10**6, 10**8), rng.randint(0, 10**8), rng.randint(10**3, 10**6))]
+        out += [(pb, q) for q in qs]
+    return out
+
+
+@pytest.mark.parametrize("case", range(len(_cases())))
+def test_oracle_greedy_local_optimum_and_bounds(oracle_mod, case):
+    pb, q = _cases()[case]
+    orc = oracle_mod.Oracle(pb)
+    st, idx, rec, it, ev = oracle_mod.greedy(orc, q)
+    r = rec.astuple()
+    assert r == _rec_of(orc, idx)
+    # local optimum: no single-digit change is strictly better
+    digits = orc.decode(idx)
+    place = [1] * len(pb.radix)
+    for b in range(len(pb.radix) - 2, -1, -1):
+        place[b] = place[b + 1] * pb.radix[b + 1]
+    nb = 0
+    for b, rb in enumerate(pb.radix):
+        for c in range(rb):
+            if c == digits[b]:
+                continue
+            x = idx + (c - digits[b]) * place[b]
+            assert not _better(q, pb.objective, x, _rec_of(orc, x), idx, r), (b, c)
+            nb += 1
+    assert ev == 1 + (it + 1) * nb
+    # never better than the exhaustive winner; starting there stays there
+    win = _golden_winner(pb, q)
+    if win is None and orc.n <= 2_000_000:
+        (wst, widx, wrec), = orc.sweep(0, orc.n, [q])[0]
+        win = (wst, widx, wrec.astuple())
+    if win is not None:
+        wst, widx, w = win
+        assert widx == idx or _better(q, pb.objective, widx, w, idx, r)
+        assert st == wst or (st == 1 and wst == 0)
+        st2, idx2, rec2, it2, ev2 = oracle_mod.greedy(orc, q, start=widx)
+        assert (idx2, it2) == (widx, 0)
+
+
+def test_oracle_greedy_baseline_is_cheapest(oracle_mod):
+    """With no refinement possible (a query nothing can improve on is not needed): the
+    baseline of C2 is LOW quality, k = 1 on every digit."""
+    pb = make_config("C2")
+    orc = oracle_mod.Oracle(pb)
+    # start from the baseline and read it back through a zero-iteration run: an
+    # impossible-to-improve query is emulated by starting from the result itself
+    st, idx, rec, it, ev = oracle_mod.greedy(orc, Query(INF, INF, INF))
+    # the baseline digit per block is the first LOW/k=1 choice: level 0, k 1, pool 0
+    base = 0
+    for b, rb in enumerate(pb.radix):
+        off = sum(pb.radix[:b])
+        ch = [i for i in range(rb) if pb.choices[off + i][0] == 0 and pb.choices[off + i][1] == 1]
+        base = base * rb + ch[0]
+    st0, idx0, rec0, it0, ev0 = oracle_mod.greedy(orc, Query(INF, INF, INF), start=base)
+    assert (idx0, it0) == (idx, it)  # the default start is exactly this baseline
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C5"])
+def test_gpu_greedy_matches_oracle(oracle_mod, cfg):
+    if not cuda_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_05800_b200 as sw
+    pb = make_config(cfg)
+    orc = oracle_mod.Oracle(pb)
+    with sw.Plan(pb, record_capacity=1) as plan:
+        for q in pb.queries:
+            st, idx, rec, it, ev = oracle_mod.greedy(orc, q)
+            sel, git, gev = plan.greedy(q)
+            assert sel.status == st and sel.index == idx and tuple(sel.rec) == rec.astuple()
+            assert (git, gev) == (it, ev)
+            # warm start at an arbitrary plan
+            s0 = (idx * 7919 + 12345) % orc.n
+            st, idx, rec, it, ev = oracle_mod.greedy(orc, q, start=s0)
+            sel, git, gev = plan.greedy(q, start=s0)
+            assert sel.index == idx and tuple(sel.rec) == rec.astuple() and git == it
+
+
+@pytest.mark.gpu
+def test_gpu_greedy_random_problems(oracle_mod):
+    if not cuda_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_05800_b200 as sw
+    for case in range(len(_cases())):
+        pb, q = _cases()[case]
+        orc = oracle_mod.Oracle(pb)
+        st, idx, rec, it, ev = oracle_mod.greedy(orc, q)
+        with sw.Plan(pb, record_capacity=1) as plan:
+            sel, git, gev = plan.greedy(q)
+        assert sel.index == idx and tuple(sel.rec) == rec.astuple() and (git, gev) == (it, ev), case

@@ -439,3 +439,31 @@ def test_generator_calibration():
     assert (0.88 * 93.0) / dit8 > 5.0
     assert abs(va_seconds(5063, 1, 1, "A100") / va_seconds(5063, 1, 1, "H100") - 1.9) < 1e-12
     assert abs(va_seconds(63, 1, 1, "A100") / 0.0625 - 66.0) < 0.1
+
+
+def test_budget_only_winner_is_on_the_front(oracle_mod):
+    """Reading R30: under QUALITY_FIRST a query that bounds neither startup
+    nor stall has its winner -- feasible or closest -- on the exact 3-D Pareto front, so
+    the GPU answers it from the front.  Checked on the oracle for random problems and
+    budgets (including infeasible ones)."""
+    import random
+    from tests.helpers import random_problem
+    from swgen.generator import Query, INF
+    checked = 0
+    for seed in range(40):
+        rng = random.Random(9000 + seed)
+        pb = random_problem(rng, max_scenes=5, max_pools=3, max_choices=4,
+                            one_scene_digits=rng.random() < 0.5)
+        pb.objective = 0
+        orc = oracle_mod.Oracle(pb)
+        recs = orc.record_list(0, orc.n)
+        costs = sorted(r.cost_mc for r in recs)
+        qs = [Query(INF, INF, INF), Query(INF, INF, costs[len(costs) // 3]),
+              Query(INF, INF, max(0, costs[0] - 1))]  # the last: nothing feasible
+        w, front, _ = orc.sweep(0, orc.n, qs)
+        on_front = {p[0] for p in front}
+        for st, idx, rec in w:
+            assert idx in on_front, (seed, st, idx)
+            checked += 1
+        assert w[2][0] == 1  # closest tier exercised
+    assert checked == 120

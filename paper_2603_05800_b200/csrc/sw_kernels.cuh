@@ -274,9 +274,21 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(EvalJob job, const E
             const uint32_t k = ch_k(ch), p = ch_pool(ch);
             const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
             const VaEntry* vb = va + h.voff[b] + c;
-            // k differs across lanes here: the runtime-k gang update (a divergent switch
-            // over the compile-time variants measured 12% slower overall on C2)
-            run_block<NP, 0>(st, h, p, k, f0, f1, vb, r);
+            // lanes are 32 consecutive rows: the high digits usually agree across the
+            // warp -- then (k, p) is warp-uniform and the compile-time gang update runs;
+            // otherwise the runtime-k update (a divergent switch over the compile-time
+            // variants measured 12% slower overall on C2)
+            if (__all_sync(0xffffffffu, ch == __shfl_sync(0xffffffffu, ch, 0))) {
+                switch (k) {
+                    case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
+                    case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
+                    case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
+                    case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
+                    default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
+                }
+            } else {
+                run_block<NP, 0>(st, h, p, k, f0, f1, vb, r);
+            }
         }
         // ---- MID digit: warp-uniform choice
         for (uint32_t dm = 0; dm < rm; dm++) {
@@ -671,16 +683,22 @@ __device__ __forceinline__ int32_t dlt_tkey(uint64_t t) {
     return (int32_t)(__float_as_uint(__ull2float_rz(t)) >> kDltTShift);
 }
 
-__device__ __forceinline__ bool dlt_dominated(const Dlt& d, uint64_t t, uint64_t c, uint32_t q) {
+// The DLT's scalar fields, held in registers by the scan consumers.
+struct DltHot {
+    int32_t kbase;
+    uint32_t qmin, qmax, qshift;
+};
+
+__device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
     // branch-free: clamp both cell coordinates, look the two maps up independently,
     // then predicate away the out-of-range cases
-    const int32_t k = dlt_tkey(t) - d.kbase;
+    const int32_t k = dlt_tkey(t) - hs.kbase;
     const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
-    const uint32_t qc = min((max(q, d.qmin) - d.qmin) >> d.qshift, (uint32_t)kDltMap - 1);
+    const uint32_t qc = min((max(q, hs.qmin) - hs.qmin) >> hs.qshift, (uint32_t)kDltMap - 1);
     const uint32_t b1 = d.tmap[kc];  // t bin + 1 (0: no front point has t <= this t)
     const uint32_t j = d.qmap[qc];
     const uint32_t cell = d.cell[(max(b1, 1u) - 1) * kDltQ + j];
-    return (k >= 0) & (q <= d.qmax) & (b1 != 0) & (cell != 0xffffffffu) & ((uint64_t)cell < c);
+    return (k >= 0) & (q <= hs.qmax) & (b1 != 0) & (cell != 0xffffffffu) & ((uint64_t)cell < c);
 }
 
 // Header pass (1 block of 1024): edges, coarse maps.
@@ -900,6 +918,37 @@ __global__ void __launch_bounds__(kScanThreads) pareto_mark2d_kernel(const PPoin
     }
 }
 
+// a9 from the front (reading R30): a QUALITY_FIRST query that bounds neither startup nor
+// stall has its winner -- feasible (cost <= budget) or closest (least budget overshoot)
+// -- on the exact 3-D Pareto front, so it is reduced over the front points only.
+__global__ void __launch_bounds__(kScanThreads) select_front_kernel(const PPoint* __restrict__ front, uint64_t n,
+                                                                    SelParams P, Cand* __restrict__ out) {
+    __shared__ Cand s_tmp[32];
+    for (uint32_t q = 0; q < P.nq; q++) {
+        uint64_t idx = kInf64;
+        Rec4 r{};
+        for (uint64_t j = threadIdx.x; j < n; j += blockDim.x) {
+            const PPoint pt = front[j];
+            Rec4 x;
+            x.w0 = pt.t;  // ttff_eff as ttff with zero stall: unbounded in this query
+            x.w1 = 0;
+            x.w2 = pt.c;
+            x.w3 = pt.q;
+            if (cand_better(P.q[q], P.objective, pt.idx, x, idx, r)) {
+                idx = pt.idx;
+                r = x;
+            }
+        }
+        block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
+        if (threadIdx.x == 0) {
+            out[q].idx = idx;
+            out[q].r = r;
+            out[q].pad = (idx != kInf64 && !feasible(P.q[q], r)) ? 1ull : 0ull;
+        }
+        __syncthreads();
+    }
+}
+
 // ============================================================================ fused scan
 // One pass over a record segment serves (a9) up to NQ select queries and, when PARETO,
 // (a8) the front filter: (1) the DLT prefilter, O(1) per record; (2) for DLT survivors
@@ -916,6 +965,7 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
     PPoint* surv;
     uint64_t cap;
     uint32_t* gfeas;  // [SW_MAX_QUERIES] per request: a feasible record was seen (or null)
+    uint32_t prefetch;  // iterations per consumer group kept in flight as L2 bulk prefetches
 };
 
 // objective keys only (ties keep the earlier = lower index within a thread's scan)
@@ -944,12 +994,15 @@ __device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_
     return obj_strict_better(obj, a, b);
 }
 
-// TMA-pipelined scan: warp kCW (one elected lane) streams the segment's records (a flat
-// run of ntiles * 32 * row slots, tile padding included) through a kStages-deep
-// shared-memory ring with cp.async.bulk, 32 KB per stage, completion on a "full"
-// mbarrier per stage; stages are dealt round-robin to the blocks.  kCW consumer warps take
-// kRPT records per thread per stage from shared memory (independent chains: ILP) and
-// release the stage on an "empty" mbarrier.  Bytes in flight per SM are set by the ring.
+// TMA-pipelined scan: the segment's records (a flat run of ntiles * 32 * row slots, tile
+// padding included) are dealt to the blocks in 32 KB stages, round-robin.  A block's
+// consumer warps form kGroups groups; each group owns NS / kGroups ring slots and its
+// own stages (stage i of the block goes to group i % kGroups).  One elected thread per
+// group issues the group's cp.async.bulk copies (completion on a "full" mbarrier per
+// slot) and the L2 bulk prefetches kPrefetch stages ahead; after the whole group has
+// moved a stage into registers (a named barrier), it reissues the freed slot at once --
+// no producer warp, no "empty" barriers, no head-of-line blocking between groups.
+// Consumers take kRPT records per thread per stage (independent chains: ILP).
 //
 // Select (a9) per record and query costs a few integer ops in the common case: the block
 // shares, per query, a threshold in shared memory -- the best quality of any FEASIBLE
@@ -957,14 +1010,16 @@ __device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_
 // quality (resp. an infeasible record once a feasible one exists) is strictly worse than
 // a record this block will report, so it is skipped; the full total-order comparison
 // (cand_better) runs only for the rare records that pass.
-constexpr int kCW = 16;                         // consumer warps per block
-constexpr int kScanBlock = (kCW + 1) * 32;      // + 1 producer warp
+constexpr int kCW = 16;                         // consumer warps per block (no producer warp:
+                                                // 4 per SMSP, up to 128 registers)
+constexpr int kScanBlock = kCW * 32;
 constexpr int kGroups = 2;                      // consumer groups take alternate stages
 constexpr int kGW = kCW / kGroups;              // warps per group
 constexpr int kRPT = 4;                         // records per consumer thread per stage
 constexpr uint32_t kStageRecs = kGW * 32 * kRPT;  // records per stage (32 KB)
 // Little's law: ~45 GB/s per SM x ~1.5-2 us loaded latency => ~100 KB in flight per SM
-constexpr int kPrefetch = 6;      // stages per block prefetched into L2 ahead of the TMA copy
+constexpr int kPrefetch = 0;      // iterations per consumer group prefetched into L2 ahead (0: off;
+                                  // measured: 0-4 equal, 6+ over-run L2 and re-read DRAM)
 constexpr int kStages = 6;        // plain scans (192 KB ring)
 constexpr int kStagesPareto = 4;  // scans carrying the DLT + front subset in smem (128 KB)
 static_assert(kStages % kGroups == 0 && kStagesPareto % kGroups == 0, "groups own fixed ring slots");
@@ -972,12 +1027,14 @@ __host__ __device__ constexpr size_t ring_bytes(bool pareto) {
     return (size_t)(pareto ? kStagesPareto : kStages) * kStageRecs * sizeof(Rec4);
 }
 
-struct StageMeta {
+struct __align__(16) StageMeta {
+    uint32_t gf[SW_MAX_QUERIES];  // grid-wide "feasible seen" flags, copied by the stage's TMA
     uint64_t pos0;       // flat slot of the stage's first record
     uint32_t cnt;        // records in the stage; 0 = end of stream
     uint16_t all_valid;  // no tile padding inside: skip per-record range checks
-    uint16_t feas;       // bit q: some block already found a feasible record for query q
+    uint16_t pad;
 };
+static_assert(sizeof(uint32_t) * SW_MAX_QUERIES % 16 == 0, "flags are bulk-copied");
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -993,6 +1050,26 @@ __device__ __forceinline__ uint64_t flat_index(const SegView& v, uint32_t per_ti
 __device__ __forceinline__ uint64_t qc_key(const Rec4& r) {
     const uint32_t c32 = r.w2 > 0xffffffffull ? 0xffffffffu : (uint32_t)r.w2;
     return ((uint64_t)rec_Q(r) << 32) | (uint64_t)(~c32);
+}
+
+// Select predicate of kRPT records for one query: bit u set iff record u is valid,
+// feasible (only the bounds in AM are compared) and, under QUALITY_FIRST, its packed key
+// is >= the block's best feasible key thr (thr == 0: none yet, every key passes).
+template <int AM>
+__device__ __forceinline__ uint32_t pred_pass(const Rec4 (&r)[kRPT], const bool (&valid)[kRPT],
+                                              unsigned long long thr, bool obj_q,
+                                              uint64_t slo_t, uint64_t slo_s, uint64_t bud) {
+    uint32_t need = 0;
+#pragma unroll
+    for (int u = 0; u < kRPT; u++) {
+        bool f = valid[u];
+        if (AM & 1) f &= r[u].w0 <= slo_t;
+        if (AM & 2) f &= r[u].w1 <= slo_s;
+        if (AM & 4) f &= r[u].w2 <= bud;
+        f &= !obj_q | (qc_key(r[u]) >= thr);
+        need |= (uint32_t)f << u;
+    }
+    return need;
 }
 
 // A fleet scan: request blockIdx.y scans its own records with its own queries.
@@ -1011,11 +1088,18 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     }
     const uint64_t out_block = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
     constexpr int NQA = NQ > 0 ? NQ : 1;
+    uint32_t amask[NQA];  // per query: bit 0 ttff bound set, bit 1 stall bound, bit 2 budget
+#pragma unroll
+    for (int q = 0; q < NQA; q++)
+        amask[q] = NQ == 0 ? 0u
+                           : (P.q[q].slo_t != kInf64 ? 1u : 0u) | (P.q[q].slo_s != kInf64 ? 2u : 0u) |
+                                 (P.q[q].budget != kInf64 ? 4u : 0u);
     extern __shared__ __align__(128) unsigned char fsm[];
     __shared__ Cand s_tmp[32];
     constexpr int NS = PARETO ? kStagesPareto : kStages;
-    __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
+    __shared__ __align__(8) uint64_t full_bar[NS];
     __shared__ StageMeta meta[NS];
+    __shared__ uint32_t s_rel[NS];  // warps of the owning group done with the slot's stage
     // per query: packed key (Q << 32 | ~min(cost, 2^32-1)) of this block's best FEASIBLE
     // record under QUALITY_FIRST (any nonzero value under COST_X_TTFF); 0 = none yet
     __shared__ unsigned long long s_thr[NQA];
@@ -1029,7 +1113,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     if (threadIdx.x == 0) {
         for (int st = 0; st < NS; st++) {
             mbar_init(&full_bar[st], 1);
-            mbar_init(&empty_bar[st], kGW);
+            s_rel[st] = 0;
         }
     }
     if (threadIdx.x < NQA) {
@@ -1048,6 +1132,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = pa.front[i];
     }
     __syncthreads();
+    DltHot dh{0, 0, 0, 0};
+    if (PARETO) dh = DltHot{d.kbase, d.qmin, d.qmax, d.qshift};
     const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
     const uint64_t total = v.ntiles * per_tile;
     // stage sg of this view/pass -> flat slot of its first record (kInf64: none)
@@ -1059,8 +1145,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                                          : spu * (v.pass == 1 ? k64 : v.pass == 2 ? k8 - k64 : nunits - k8);
     auto stage_pos = [&](uint64_t sg) -> uint64_t {
         if (v.pass == 0) return sg * kStageRecs;
-        const uint64_t j = sg / spu, part = sg - j * spu;
-        const uint64_t m = (j / 7) * 8 + (j % 7) + 1;  // j-th positive non-multiple of 8
+        // stage counts stay far below 2^32 (2^32 stages = 1.4e14 records): 32-bit divides
+        const uint32_t j = (uint32_t)sg / (uint32_t)spu, part = (uint32_t)sg - j * (uint32_t)spu;
+        const uint64_t m = (uint64_t)(j / 7) * 8 + (j % 7) + 1;  // j-th positive non-multiple of 8
         const uint64_t u = v.pass == 1 ? 64 * j : v.pass == 2 ? 8 * m : m;
         const uint64_t pos = u * unit_recs + part * kStageRecs;
         return pos < total ? pos : kInf64;
@@ -1076,65 +1163,77 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         bf[q] = false;
     }
 
-    if (warp == kCW) {
-        // ---------------- producer: one elected lane issues the bulk copies
-        if (lane == 0) {
-            uint32_t it = 0;
-            // DRAM latency is covered by L2 prefetches kPrefetch stages ahead (the smem
-            // ring only has to cover L2 latency): prime the first ones
-            for (uint32_t pf = 0; pf < kPrefetch; pf++) {
-                const uint64_t sp = blockIdx.x + (uint64_t)pf * gridDim.x;
-                const uint64_t pp = sp < nstages ? stage_pos(sp) : kInf64;
+    // ---------------- the group's pipeline: slots grp*SPG .. grp*SPG+SPG-1
+    constexpr int SPG = NS / kGroups;  // slots per group
+    const uint32_t grp = (uint32_t)warp / kGW;
+    const uint32_t gtid = threadIdx.x - grp * (kGW * 32);
+    // Iteration k of group g consumes block-local stage i = g + k * kGroups (global stage
+    // sg = blockIdx.x + i * gridDim.x) from slot g*SPG + k % SPG.  The warp that finishes
+    // moving a slot into registers LAST refills it with iteration k + SPG (a per-slot
+    // arrival counter, no barrier): no producer warp, no head-of-line blocking.
+    auto issue = [&](uint32_t slot, uint64_t kk) {  // one thread: fill slot for iteration kk
+        const uint64_t i = grp + kk * kGroups;
+        // keep the group's stream warm in L2 kPrefetch iterations ahead
+        const uint64_t ip = i + (uint64_t)pa.prefetch * kGroups;
+        if (ip * gridDim.x + blockIdx.x < nstages) {
+            const uint64_t pp = stage_pos(ip * gridDim.x + blockIdx.x);
+            if (pp != kInf64)
+                tma_prefetch_l2(v.recs + pp, (uint32_t)umin64(kStageRecs, total - pp) * (uint32_t)sizeof(Rec4));
+        }
+        const uint64_t sg = i * gridDim.x + blockIdx.x;
+        if (sg >= nstages) {  // end of this group's stream
+            meta[slot].pos0 = 0;
+            meta[slot].cnt = 0;
+            mbar_arrive(&full_bar[slot]);
+            return;
+        }
+        const uint64_t pos0 = stage_pos(sg);
+        if (pos0 == kInf64) {  // a stage past a partial last unit: nothing to read
+            meta[slot].pos0 = kInf64;
+            meta[slot].cnt = 0;
+            mbar_arrive(&full_bar[slot]);
+            return;
+        }
+        const uint32_t cnt = (uint32_t)umin64(kStageRecs, total - pos0);
+        // tile padding lives only in the first and the last tile of a segment
+        const bool edge = pos0 < per_tile || pos0 + cnt > total - per_tile;
+        meta[slot].pos0 = pos0;
+        meta[slot].cnt = cnt;
+        meta[slot].all_valid = edge ? 0 : 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA write
+        // the grid-wide feasibility flags ride on the stage's own transaction: no thread
+        // waits on a global load
+        const uint32_t gf_bytes = (NQ > 0 && pa.gfeas) ? (uint32_t)sizeof(meta[slot].gf) : 0u;
+        mbar_expect_tx(&full_bar[slot], cnt * (uint32_t)sizeof(Rec4) + gf_bytes);
+        if (gf_bytes) tma_bulk_g2s(meta[slot].gf, pa.gfeas, gf_bytes, &full_bar[slot]);
+        tma_bulk_g2s(ring + (size_t)slot * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4), &full_bar[slot]);
+    };
+    if (gtid == 0) {
+        for (uint32_t pf = 0; pf < pa.prefetch; pf++) {  // prime the L2 prefetch window
+            const uint64_t ip = grp + (uint64_t)pf * kGroups;
+            if (ip * gridDim.x + blockIdx.x < nstages) {
+                const uint64_t pp = stage_pos(ip * gridDim.x + blockIdx.x);
                 if (pp != kInf64)
                     tma_prefetch_l2(v.recs + pp, (uint32_t)umin64(kStageRecs, total - pp) * (uint32_t)sizeof(Rec4));
-            }
-            uint32_t fm = 0;  // grid-wide feasibility flags, loaded one stage ahead
-            for (uint64_t sg = blockIdx.x; sg < nstages; sg += gridDim.x, it++) {
-                uint32_t fm_next = 0;
-                if (NQ > 0 && pa.gfeas) {
-#pragma unroll
-                    for (int q = 0; q < NQ; q++)
-                        fm_next |= (*(volatile const uint32_t*)&pa.gfeas[q] != 0 ? 1u : 0u) << q;
-                }
-                const uint64_t sp = sg + (uint64_t)kPrefetch * gridDim.x;
-                const uint64_t pp = sp < nstages ? stage_pos(sp) : kInf64;
-                if (pp != kInf64)
-                    tma_prefetch_l2(v.recs + pp, (uint32_t)umin64(kStageRecs, total - pp) * (uint32_t)sizeof(Rec4));
-                const uint64_t pos0 = stage_pos(sg);
-                if (pos0 == kInf64) {  // past the partial last unit: no stage
-                    it--;
-                    continue;
-                }
-                const uint32_t st = it % NS, k = it / NS;
-                if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
-                const uint32_t cnt = (uint32_t)umin64(kStageRecs, total - pos0);
-                // tile padding lives only in the first and the last tile of a segment
-                const bool edge = pos0 < per_tile || pos0 + cnt > total - per_tile;
-                meta[st].pos0 = pos0;
-                meta[st].cnt = cnt;
-                meta[st].all_valid = edge ? 0 : 1;
-                meta[st].feas = (uint16_t)fm;
-                fm = fm_next;
-                mbar_expect_tx(&full_bar[st], cnt * (uint32_t)sizeof(Rec4));
-                tma_bulk_g2s(ring + (size_t)st * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4),
-                             &full_bar[st]);
-            }
-            for (int g = 0; g < kGroups; g++, it++) {  // one end-of-stream marker per group
-                const uint32_t st = it % NS, k = it / NS;
-                if (k > 0) mbar_wait(&empty_bar[st], (k - 1) & 1);
-                meta[st].cnt = 0;
-                mbar_arrive(&full_bar[st]);
             }
         }
-    } else {
-        // ---------------- consumers: group g takes stages g, g + kGroups, ...
-        const uint32_t grp = (uint32_t)warp / kGW;
-        const uint32_t gtid = threadIdx.x - grp * (kGW * 32);
-        for (uint32_t it = grp;; it += kGroups) {
-            const uint32_t st = it % NS;
-            mbar_wait(&full_bar[st], (it / NS) & 1);
+        for (int j = 0; j < SPG; j++) issue(grp * SPG + j, (uint64_t)j);
+    }
+    {
+        // ---------------- consume: iteration k uses slot grp*SPG + k % SPG
+        for (uint32_t k = 0;; k++) {
+            const uint32_t st = grp * SPG + k % SPG;
+            mbar_wait(&full_bar[st], (k / SPG) & 1);
             const StageMeta mt = meta[st];
-            if (mt.cnt == 0) break;
+            if (mt.cnt == 0 && mt.pos0 == 0) break;  // end of the group's stream
+            if (mt.cnt == 0) {                        // empty stage: release and go on
+                __syncwarp();
+                if (lane == 0 && atomicAdd(&s_rel[st], 1u) == kGW - 1) {
+                    s_rel[st] = 0;
+                    issue(st, (uint64_t)k + SPG);
+                }
+                continue;
+            }
             Rec4 r[kRPT];
             bool valid[kRPT];
 #pragma unroll
@@ -1148,8 +1247,16 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 // unconditional: a slot past cnt holds stale bytes that valid[] masks out
                 r[u] = ring[(size_t)st * kStageRecs + o];
             }
+            // this warp has the stage in registers; the group's last warp refills the slot
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage data is in registers now
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(&s_rel[st], 1u) == kGW - 1) {
+                    s_rel[st] = 0;
+                    __threadfence_block();
+                    issue(st, (uint64_t)k + SPG);
+                }
+            }
             const bool obj_q = P.objective == 0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
@@ -1162,17 +1269,19 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 //  - before that, only records whose startup+stall violation does not
                 //    exceed the block's best closest-tier violation.
                 const unsigned long long thr = s_thr[q];
-                const uint32_t tq = (uint32_t)(thr >> 32), tc = ~(uint32_t)thr;
-                const bool anyf = (thr != 0) | bf[q] | (((uint32_t)mt.feas >> q) & 1u);
+                const bool anyf = (thr != 0) | bf[q] | (pa.gfeas != nullptr && mt.gf[q] != 0);
                 const uint64_t slo_t = P.q[q].slo_t, slo_s = P.q[q].slo_s, bud = P.q[q].budget;
-                uint32_t need = 0;
-#pragma unroll
-                for (int u = 0; u < kRPT; u++) {
-                    const bool f = (r[u].w0 <= slo_t) & (r[u].w1 <= slo_s) & (r[u].w2 <= bud);
-                    const uint32_t Qr = rec_Q(r[u]);
-                    const bool qok = !obj_q | (thr == 0) | (Qr > tq) |
-                                     ((Qr == tq) & ((r[u].w2 >> 32) == 0) & ((uint32_t)r[u].w2 <= tc));
-                    need |= (uint32_t)(valid[u] & f & qok) << u;
+                // only the bounds the query actually sets are compared (uniform dispatch)
+                uint32_t need;
+                switch (amask[q]) {
+                    case 0: need = pred_pass<0>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 1: need = pred_pass<1>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 2: need = pred_pass<2>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 3: need = pred_pass<3>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 4: need = pred_pass<4>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 5: need = pred_pass<5>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 6: need = pred_pass<6>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    default: need = pred_pass<7>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
                 }
                 if (__any_sync(0xffffffffu, !anyf)) {  // closest tier still open somewhere
                     const unsigned long long vmax = s_vt[q];
@@ -1207,7 +1316,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 uint32_t keepm = 0;  // DLT survivors, all kRPT lookups first (independent: ILP)
 #pragma unroll
                 for (int u = 0; u < kRPT; u++)
-                    keepm |= (uint32_t)(valid[u] & !dlt_dominated(d, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u]))) << u;
+                    keepm |= (uint32_t)(valid[u] & !dlt_dominated(d, dh, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u]))) << u;
                 if (!__any_sync(0xffffffffu, keepm != 0)) continue;
 #pragma unroll
                 for (int u = 0; u < kRPT; u++) {
@@ -1250,10 +1359,10 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                     }
                     const unsigned mask = __ballot_sync(0xffffffffu, keep);
                     if (mask) {
-                        const int leader = __ffs(mask) - 1;
+                        const int ldr = __ffs(mask) - 1;
                         unsigned long long slot0 = 0;
-                        if (lane == leader) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
-                        slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+                        if (lane == ldr) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
+                        slot0 = __shfl_sync(0xffffffffu, slot0, ldr);
                         if (keep) {
                             const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
                             if (slot < pa.cap) pa.surv[slot] = pt;
@@ -1264,7 +1373,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         }
     }
 #pragma unroll
-    for (int q = 0; q < NQ; q++) {  // the producer warp joins with "none"
+    for (int q = 0; q < NQ; q++) {
         uint64_t idx = bi[q];
         Rec4 rr = br[q];
         block_reduce_cand(P.q[q], P.objective, idx, rr, s_tmp);

@@ -79,8 +79,10 @@ struct sw_plan {
     uint64_t chunk = 1ull << 25; // records per fold chunk (the front improves per chunk)
     uint64_t fold_passes = 0;    // diagnostics: filter passes run
     uint64_t epoch = 1;          // bumped by every change of records or front
+    bool released = false;       // records dropped since create/reset: the front covers more
     uint64_t merged_epoch = 0, merged_n = 0;  // multi-rank merged front cached in d_gather
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
+    uint32_t prefetch = kPrefetch;  // SW_PREFETCH: scan L2 prefetch distance (iterations per group)
     uint64_t* d_counts = nullptr;
     uint32_t* d_gfeas = nullptr;  // [SW_MAX_QUERIES] grid-wide "feasible seen" flags of a select
     GreedyOut* d_greedy = nullptr;
@@ -192,6 +194,7 @@ using u128 = unsigned __int128;
 }  // namespace
 
 static sw_status fold_pending(sw_plan* h);
+static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_out);
 static constexpr uint64_t kMaxSegs = 16;  // segments with tile padding budgeted per handle
 
 // Tiles [t_lo, t_hi) (relative to the segment) of a segment as a scan view.
@@ -510,6 +513,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (const char* ev = getenv("SW_PARETO_CHUNK")) h->chunk = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
+    if (const char* ev = getenv("SW_PREFETCH")) h->prefetch = (uint32_t)atoi(ev);
     if (cudaError_t se = set_scan_smem_attrs(); se != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ECUDA, "scan kernels cannot launch one block per SM (%s; smem %zu/%zu B)",
@@ -595,6 +599,7 @@ extern "C" sw_status sw_plan_reset(sw_plan* h) {
     h->rec_used = 0;
     h->cand_used = 0;
     h->front_n = 0;
+    h->released = false;
     CK(h, cudaSetDevice(h->device));
     CK(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream));
     return SW_OK;
@@ -608,6 +613,8 @@ extern "C" sw_status sw_plan_release_records(sw_plan* h) {
     h->segs.clear();
     h->rec_used = 0;
     h->cand_used = 0;
+    h->released = true;
+    h->epoch++;
     return SW_OK;
 }
 
@@ -847,6 +854,7 @@ static ParetoArgs pareto_args(sw_plan* h) {
     pa.surv = h->d_surv;
     pa.cap = h->surv_cap;
     pa.gfeas = h->d_gfeas;
+    pa.prefetch = h->prefetch;
     return pa;
 }
 
@@ -958,10 +966,79 @@ static sw_status sync_ctl(sw_plan* h, bool* overflow) {
     return SW_OK;
 }
 
+// Winners of front-answerable queries (R30) from the exact global front.  Collective.
+static sw_status front_answer(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
+    const PPoint* fr = nullptr;
+    uint64_t n = 0;
+    sw_status st = global_front(h, &fr, &n);
+    if (st < 0) return st;
+    SelParams P{};
+    P.nq = nq;
+    P.objective = (h->h.flags & 4u) ? 1u : 0u;
+    for (uint32_t q = 0; q < nq; q++) P.q[q] = QueryDev{qs[q].slo_startup_us, qs[q].slo_stall_us, qs[q].budget_mc};
+    select_front_kernel<<<1, kScanThreads, 0, h->stream>>>(fr, n, P, h->d_cand);
+    CKL(h);
+    launch_np(h, [&](auto npc) {
+        constexpr int NPc = decltype(npc)::value;
+        detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nq, h->d_detail);
+    });
+    CKL(h);
+    Cand win[SW_MAX_QUERIES];
+    DetailOut det[SW_MAX_QUERIES];
+    CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nq, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nq, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    sw_status worst = SW_OK;
+    for (uint32_t q = 0; q < nq; q++) {
+        memset(&out[q], 0, sizeof(sw_selection));
+        if (win[q].idx == kInf64) {
+            out[q].status = SW_EMPTY;
+        } else {
+            detail_to_selection(h, win[q].idx, det[q], &out[q], nullptr);
+            out[q].status = win[q].pad ? SW_CLOSEST : SW_OK;
+        }
+        worst = std::max<sw_status>(worst, out[q].status);
+    }
+    return worst;
+}
+
+// A query is front-answerable (R30) when it bounds neither startup nor stall under the
+// QUALITY_FIRST objective and the handle's front covers exactly its records.
+static bool front_query(const sw_plan* h, const sw_query& q) {
+    return h->fuse_pareto && !(h->h.flags & 4u) && q.slo_startup_us == UINT64_MAX && q.slo_stall_us == UINT64_MAX;
+}
+
+static sw_status select_scan(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out);
+
 extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
     if (!h || !qs || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (nq < 1 || nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u not in 1..%d", nq, SW_MAX_QUERIES);
     CK(h, cudaSetDevice(h->device));
+    uint32_t fi[SW_MAX_QUERIES], si[SW_MAX_QUERIES], nf = 0, ns = 0;
+    for (uint32_t q = 0; q < nq; q++) {
+        if (!h->released && front_query(h, qs[q])) fi[nf++] = q;
+        else si[ns++] = q;
+    }
+    if (nf == 0) return select_scan(h, nq, qs, out);
+    sw_query qf[SW_MAX_QUERIES], qsn[SW_MAX_QUERIES];
+    sw_selection of[SW_MAX_QUERIES], os[SW_MAX_QUERIES];
+    for (uint32_t j = 0; j < nf; j++) qf[j] = qs[fi[j]];
+    for (uint32_t j = 0; j < ns; j++) qsn[j] = qs[si[j]];
+    sw_status worst = SW_OK, st;
+    if (ns) {  // the scan queries (the fused scan also folds the records into the front)
+        st = select_scan(h, ns, qsn, os);
+        if (st < 0) return st;
+        worst = std::max(worst, st);
+    }
+    st = front_answer(h, nf, qf, of);  // folds whatever is still pending first
+    if (st < 0) return st;
+    worst = std::max(worst, st);
+    for (uint32_t j = 0; j < nf; j++) out[fi[j]] = of[j];
+    for (uint32_t j = 0; j < ns; j++) out[si[j]] = os[j];
+    return worst;
+}
+
+static sw_status select_scan(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
     SelParams P{};
     P.nq = nq;
     P.objective = (h->h.flags & 4u) ? 1u : 0u;
@@ -1088,14 +1165,24 @@ extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uin
     }
     uint64_t dsum = 0;
     sw_selection tmp[SW_MAX_QUERIES];
+    // front-answerable queries (R30) are answered once from the final front when that
+    // front covers exactly [begin, end) (empty front at the start); the others per chunk
+    const bool front_ok = h->front_n == 0 && !h->released && h->segs.empty();
+    uint32_t fi[SW_MAX_QUERIES], si[SW_MAX_QUERIES], nf = 0, ns = 0;
+    sw_query qsn[SW_MAX_QUERIES];
+    for (uint32_t q = 0; q < nq; q++) {
+        if (front_ok && front_query(h, qs[q])) fi[nf++] = q;
+        else qsn[ns] = qs[q], si[ns++] = q;
+    }
     for (uint64_t c0 = begin; c0 < end;) {
         const uint64_t c1 = end - c0 > chunk ? c0 + chunk : end;
         sw_status st = sw_plan_eval(h, c0, c1);
         if (st < 0) return st;
-        if (nq) {
-            st = sw_plan_select_batch(h, nq, qs, tmp);  // also folds the chunk into the front
+        if (ns) {
+            st = select_scan(h, ns, qsn, tmp);  // also folds the chunk into the front
             if (st < 0) return st;
-            for (uint32_t q = 0; q < nq; q++) sw_selection_merge(h->h.flags & 4u ? 1u : 0u, &qs[q], &out[q], &tmp[q], &out[q]);
+            for (uint32_t j = 0; j < ns; j++)
+                sw_selection_merge(h->h.flags & 4u ? 1u : 0u, &qsn[j], &out[si[j]], &tmp[j], &out[si[j]]);
         }
         if (digest) {
             uint64_t d = 0;
@@ -1106,6 +1193,13 @@ extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uin
         st = sw_plan_release_records(h);  // folds whatever is still pending, drops the records
         if (st < 0) return st;
         c0 = c1;
+    }
+    if (nf) {
+        sw_query qf[SW_MAX_QUERIES];
+        for (uint32_t j = 0; j < nf; j++) qf[j] = qs[fi[j]];
+        sw_status st = front_answer(h, nf, qf, tmp);
+        if (st < 0) return st;
+        for (uint32_t j = 0; j < nf; j++) out[fi[j]] = tmp[j];
     }
     if (digest) *digest = dsum;
     sw_status worst = SW_OK;
@@ -1164,8 +1258,10 @@ static sw_status fold_pending(sw_plan* h) {
     return SW_OK;
 }
 
-extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t cap, uint64_t* n_out) {
-    if (!h || !n_out || (cap && !out)) return fail(nullptr, SW_EINVAL, "null argument");
+// The exact front of all records since create/reset over ALL ranks: folds pending
+// segments, and with nranks > 1 merges the per-rank fronts (allgather of counts, then of
+// padded fronts, exact merge; cached until the state changes).  Collective.
+static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_out) {
     sw_status st = fold_pending(h);
     if (st < 0) return st;
     const PPoint* res = h->d_front;
@@ -1207,6 +1303,17 @@ extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t ca
         CK(h, cudaMemcpyAsync(&h->d_ctl->front_n, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
         CK(h, cudaStreamSynchronize(h->stream));
     }
+    *res_out = res;
+    *n_out = n;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t cap, uint64_t* n_out) {
+    if (!h || !n_out || (cap && !out)) return fail(nullptr, SW_EINVAL, "null argument");
+    const PPoint* res = nullptr;
+    uint64_t n = 0;
+    sw_status st = global_front(h, &res, &n);
+    if (st < 0) return st;
     *n_out = n;
     if (cap == 0) return SW_OK;
     if (cap < n) return SW_TRUNCATED;
@@ -1568,6 +1675,7 @@ extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_se
     CK(h, cudaMemsetAsync(f->d_gfeas, 0, sizeof(uint32_t) * SW_MAX_QUERIES * n, f->stream));
     ParetoArgs pa{};
     pa.gfeas = f->d_gfeas;
+    pa.prefetch = kPrefetch;
     CK(h, cudaEventRecord(f->ev[2], f->stream));
     scan_kernel<1, false><<<dim3(f->gx, n), kScanBlock, kRingBytes, f->stream>>>(SegView{}, SelParams{}, f->d_partial,
                                                                                 pa, f->d_sjobs);

@@ -14,6 +14,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 python tools/launch_summary.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launch_summary.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 3 -c 1 \
    -o gpurun_out/${TAG}_eval python tools/one_step.py $CFG 5 > gpurun_out/${TAG}_ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s ${SCAN_SKIP:-5} -c 1 \
    -o gpurun_out/${TAG}_scan python tools/one_step.py $CFG 5 > gpurun_out/${TAG}_ncu_scan.log 2>&1
 echo done

@@ -388,11 +388,16 @@ class Plan:
                                       C.byref(out), C.byref(it), C.byref(ev)))
         return _sel(out, self.n_pools, self.B), it.value, ev.value
 
-    def pareto(self):
+    def pareto(self, cap_hint: int = 4096):
+        """The exact front (sw_pareto_get): one call with a buffer of cap_hint points,
+        a second only when the front is larger (SW_TRUNCATED gives the size)."""
         n = C.c_uint64()
-        self._ck(lib().sw_pareto_get(self.h, None, 0, C.byref(n)))
-        buf = (sw_pareto_point * max(1, n.value))()
-        st = self._ck(lib().sw_pareto_get(self.h, buf, n.value, C.byref(n)))
+        cap = max(1, cap_hint)
+        buf = (sw_pareto_point * cap)()
+        st = self._ck(lib().sw_pareto_get(self.h, buf, cap, C.byref(n)))
+        if st == SW_TRUNCATED:
+            buf = (sw_pareto_point * max(1, n.value))()
+            st = self._ck(lib().sw_pareto_get(self.h, buf, n.value, C.byref(n)))
         assert st == SW_OK
         return [(p.index, p.ttff_eff_us, p.cost_mc, p.quality) for p in buf[: n.value]]
 

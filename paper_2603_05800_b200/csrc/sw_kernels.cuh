@@ -658,23 +658,18 @@ __global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint*
 
 // Dominance lookup table (DLT) from the current front (sorted by ttff_eff).
 // t-bins: quantile edges of the front's t (tedge ascending, bin b holds t >= tedge[b]);
-// q-bins: quantile edges of a strided sample of the front's q (bin j = [qedge[j],
-// qedge[j+1])).  cell[b][j] = min cost over front points f with f.t <= tedge[b] and
-// f.q >= qedge[j+1] - 1, as u32 (0xffffffff = none / too big).  A record (t, c, q) in
-// cell (b, j) with cell < c is strictly dominated by a real candidate (f.t <= t,
-// f.q >= q, f.c < c), so it cannot be on the front.
-// Lookup is O(1) with no refinement: direct maps from a fine cell of t (float exponent +
-// 8 mantissa bits, 256 cells per octave) and of q (linear) to a CONSERVATIVE bin: the t
-// bin of the cell's lower end (tedge[b] <= lower end <= t) and the q bin of the cell's
-// upper end (q <= upper end), so cell[b][j] only counts points that dominate the record.
+// q-bins: linear, 2^qshift wide from qmin (bin j = [qmin + j 2^qshift, qmin + (j+1) 2^qshift)).
+// cell[b][j] = min cost over front points f with f.t <= tedge[b] and f.q >= the largest
+// q of bin j, as u32 (0xffffffff = none / too big).  A record (t, c, q) in cell (b, j)
+// with cell < c is strictly dominated by a real candidate (f.t <= t, f.q >= q, f.c < c),
+// so it cannot be on the front.  Lookup is O(1) and conservative: the t bin comes from a
+// fine direct map of the float exponent + 8 mantissa bits (the bin of the map cell's
+// lower end), the q bin is a shift.
 struct Dlt {
     int32_t kbase;         // t key of tmap[0]
     uint32_t qmin, qmax, qshift;
     uint64_t tedge[kDltT];
-    uint32_t qedge[kDltQ + 1];
-    uint32_t pad_[3];
     uint8_t tmap[kDltMap];  // #edges <= lower end of t cell k (0..kDltT)
-    uint8_t qmap[kDltMap];  // bin containing the upper end of q cell k
     uint32_t cell[kDltT * kDltQ];
 };
 static_assert(sizeof(Dlt) % 16 == 0, "Dlt is staged in 16 B vectors");
@@ -690,109 +685,70 @@ struct DltHot {
 };
 
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
-    // branch-free: clamp both cell coordinates, look the two maps up independently,
-    // then predicate away the out-of-range cases
+    // branch-free: clamp the t cell, shift q, then predicate away the out-of-range cases
     const int32_t k = dlt_tkey(t) - hs.kbase;
     const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
-    const uint32_t qc = min((max(q, hs.qmin) - hs.qmin) >> hs.qshift, (uint32_t)kDltMap - 1);
+    const uint32_t j = min((max(q, hs.qmin) - hs.qmin) >> hs.qshift, (uint32_t)kDltQ - 1);
     const uint32_t b1 = d.tmap[kc];  // t bin + 1 (0: no front point has t <= this t)
-    const uint32_t j = d.qmap[qc];
     const uint32_t cell = d.cell[(max(b1, 1u) - 1) * kDltQ + j];
     return (k >= 0) & (q <= hs.qmax) & (b1 != 0) & (cell != 0xffffffffu) & ((uint64_t)cell < c);
 }
 
-// Header pass (1 block of 1024): edges, coarse maps.
-__global__ void __launch_bounds__(1024) dlt_head_kernel(const PPoint* __restrict__ front,
-                                                        const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
-    __shared__ uint32_t qs[1024];
-    __shared__ uint32_t qmin_s, qmax_s;
-    const uint32_t m = (uint32_t)ctl->front_n;
-    if (threadIdx.x == 0) {
-        qmin_s = 0xffffffffu;
-        qmax_s = 0;
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-        atomicMin(&qmin_s, front[i].q);
-        atomicMax(&qmax_s, front[i].q);
-    }
-    // strided sample of front qualities, rank-sorted
-    const uint32_t ms = m < 1024u ? m : 1024u;
-    uint32_t myq = 0;
-    if (threadIdx.x < ms) myq = front[((uint64_t)threadIdx.x * m) / ms].q;
-    __syncthreads();
-    if (threadIdx.x < ms) qs[threadIdx.x] = myq;
-    __syncthreads();
-    uint32_t rank = 0;
-    if (threadIdx.x < ms)
-        for (uint32_t j = 0; j < ms; j++) {
-            const uint32_t o = qs[j];
-            rank += (o < myq || (o == myq && j < threadIdx.x)) ? 1u : 0u;
-        }
-    __syncthreads();
-    if (threadIdx.x < ms) qs[rank] = myq;
-    __syncthreads();
-    const uint32_t qmin = qmin_s, qmax = qmax_s;
-    if (threadIdx.x == 0) {
-        d->qmin = m ? qmin : 0xffffffffu;
-        d->qmax = m ? qmax : 0;
-        uint32_t sh = 0;
-        const uint64_t range = m ? (uint64_t)qmax - qmin + 1 : 1;
-        while (((range - 1) >> sh) >= (uint64_t)kDltMap) sh++;
-        d->qshift = sh;
-        d->kbase = m ? dlt_tkey(front[0].t) : 0x7fffffff;
-    }
+// One launch builds the whole DLT: block b (kDltQ threads) computes the t edges it
+// needs, q range and shift, cell row b and a 1/kDltT share of the t map; block 0 writes
+// the header.  The front is sorted by t, so a cell scan stops at the first f.t > edge.
+__global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restrict__ front,
+                                                          const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
+    __shared__ PPoint tile[kDltQ];
     __shared__ uint64_t te[kDltT];
-    __shared__ uint32_t qe[kDltQ + 1];
-    for (uint32_t i = threadIdx.x; i < kDltT; i += blockDim.x) {
-        te[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
-        d->tedge[i] = te[i];
+    __shared__ uint32_t s_qmin, s_qmax;
+    const uint32_t m = (uint32_t)ctl->front_n;
+    const uint32_t b = blockIdx.x, j = threadIdx.x;
+    if (j == 0) {
+        s_qmin = 0xffffffffu;
+        s_qmax = 0;
     }
-    for (uint32_t j = threadIdx.x; j <= kDltQ; j += blockDim.x) {
-        qe[j] = !m ? 0xffffffffu : (j == kDltQ ? qmax + 1 : (j == 0 ? qmin : qs[((uint64_t)j * ms) / kDltQ]));
-        d->qedge[j] = qe[j];
-    }
+    for (uint32_t i = j; i < kDltT; i += blockDim.x) te[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
     __syncthreads();
-    // direct maps (edges ascending: binary searches over the smem copies)
-    const int32_t kbase = m ? dlt_tkey(front[0].t) : 0;
-    uint32_t qsh = 0;
-    {
-        const uint64_t range = m ? (uint64_t)qmax - qmin + 1 : 1;
-        while (((range - 1) >> qsh) >= (uint64_t)kDltMap) qsh++;
+    uint32_t lo = 0xffffffffu, hi = 0;
+    for (uint32_t i = j; i < m; i += blockDim.x) {
+        const uint32_t q = front[i].q;
+        lo = min(lo, q);
+        hi = max(hi, q);
     }
-    for (uint32_t k = threadIdx.x; k < kDltMap; k += blockDim.x) {
-        // lower end of t cell k: smallest integer t with key(t) >= kbase + k
+    atomicMin(&s_qmin, lo);
+    atomicMax(&s_qmax, hi);
+    __syncthreads();
+    const uint32_t qmin = s_qmin, qmax = s_qmax;
+    uint32_t qsh = 0;
+    if (m)
+        while ((((uint64_t)qmax - qmin) >> qsh) >= (uint64_t)kDltQ) qsh++;
+    const int32_t kbase = m ? dlt_tkey(front[0].t) : 0x7fffffff;
+    if (b == 0) {
+        if (j == 0) {
+            d->kbase = kbase;
+            d->qmin = m ? qmin : 0xffffffffu;
+            d->qmax = m ? qmax : 0;
+            d->qshift = qsh;
+        }
+        for (uint32_t i = j; i < kDltT; i += blockDim.x) d->tedge[i] = te[i];
+    }
+    // this block's share of the t map: #edges <= lower end of cell k
+    for (uint32_t k = b * (kDltMap / kDltT) + j; k < (b + 1) * (kDltMap / kDltT); k += blockDim.x) {
         const int32_t key = kbase + (int32_t)k;
         const uint64_t L = (!m || key >= (0x7f800000 >> kDltTShift)) ? kInf64
                                                                      : (uint64_t)ceilf(__uint_as_float((uint32_t)key << kDltTShift));
-        uint32_t lo = 0, hi = kDltT;  // #edges <= L
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (te[mid] <= L) lo = mid + 1;
-            else hi = mid;
+        uint32_t a = 0, e = kDltT;
+        while (a < e) {
+            const uint32_t mid = (a + e) >> 1;
+            if (te[mid] <= L) a = mid + 1;
+            else e = mid;
         }
-        d->tmap[k] = (uint8_t)(m ? lo : 0);
-        // upper end of q cell k -> the bin j with qe[j] <= U < qe[j + 1] (last bin: kDltQ-1)
-        const uint64_t U64 = (uint64_t)qmin + (((uint64_t)k + 1) << qsh) - 1;
-        const uint32_t U = U64 > qmax ? qmax : (uint32_t)U64;
-        uint32_t a2 = 1, b2 = kDltQ;  // #edges qe[1..kDltQ-1] <= U
-        while (a2 < b2) {
-            const uint32_t mid = (a2 + b2) >> 1;
-            if (qe[mid] <= U) a2 = mid + 1;
-            else b2 = mid;
-        }
-        d->qmap[k] = (uint8_t)(a2 - 1);
+        d->tmap[k] = (uint8_t)(m ? a : 0);
     }
-}
-
-// Cells: block b = t-bin, thread j = q-bin; front staged through smem.
-__global__ void __launch_bounds__(kDltQ) dlt_cell_kernel(const PPoint* __restrict__ front,
-                                                         const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
-    __shared__ PPoint tile[kDltQ];
-    const uint32_t m = (uint32_t)ctl->front_n;
-    const uint32_t b = blockIdx.x, j = threadIdx.x;
-    const uint64_t Eb = d->tedge[b];
-    const uint64_t qhi = (uint64_t)d->qedge[j + 1] - 1;
+    // cell row b, thread j = q bin: needs f.q >= the largest q of bin j
+    const uint64_t Eb = te[b];
+    const uint64_t qhi = (uint64_t)qmin + (((uint64_t)j + 1) << qsh) - 1;
     uint64_t best = kInf64;
     bool more = true;
     for (uint32_t base = 0; base < m && more; base += kDltQ) {
@@ -847,6 +803,32 @@ __global__ void pareto_sample_kernel(SegView v, uint32_t ns, PPoint* __restrict_
     p.q = rec_Q(r);
     p.pad = 0;
     out[atomicAdd(&ctl->m_in, 1u)] = p;
+}
+
+// Device-sized variant for the asynchronous cross-rank merge: fronts allgathered padded to
+// `pad` points (counts allgathered alongside); each rank's first min(count, pad) points are
+// concatenated into out, ctl->m_in = their total, *pad_over = 1 if some front exceeded pad
+// (the host then redoes the merge at full size).
+__global__ void front_gather_pad_kernel(const PPoint* __restrict__ padded, const uint64_t* __restrict__ counts,
+                                        int nranks, uint32_t pad, PPoint* __restrict__ out, ParetoCtl* ctl,
+                                        uint64_t* __restrict__ pad_over) {
+    const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t r = x / pad, j = x % pad;
+    if (x == 0) {
+        uint64_t tot = 0, over = 0;
+        for (int q = 0; q < nranks; q++) {
+            tot += counts[q] < pad ? counts[q] : pad;
+            over |= counts[q] > pad ? 1ull : 0ull;
+        }
+        ctl->m_in = (uint32_t)tot;
+        *pad_over = over;
+    }
+    if ((int)r >= nranks) return;
+    const uint64_t cr = counts[r] < pad ? counts[r] : pad;
+    if (j >= cr) return;
+    uint64_t off = 0;
+    for (uint64_t q = 0; q < r; q++) off += counts[q] < pad ? counts[q] : pad;
+    out[off + j] = padded[x];
 }
 
 // Gather variable-size per-rank fronts (allgathered, padded to maxc) into one array.
@@ -922,8 +904,10 @@ __global__ void __launch_bounds__(kScanThreads) pareto_mark2d_kernel(const PPoin
 // stall has its winner -- feasible (cost <= budget) or closest (least budget overshoot)
 // -- on the exact 3-D Pareto front, so it is reduced over the front points only.
 __global__ void __launch_bounds__(kScanThreads) select_front_kernel(const PPoint* __restrict__ front, uint64_t n,
-                                                                    SelParams P, Cand* __restrict__ out) {
+                                                                    const uint64_t* __restrict__ d_n, SelParams P,
+                                                                    Cand* __restrict__ out) {
     __shared__ Cand s_tmp[32];
+    if (d_n) n = *d_n;  // front size produced on the device by the preceding merge
     for (uint32_t q = 0; q < P.nq; q++) {
         uint64_t idx = kInf64;
         Rec4 r{};

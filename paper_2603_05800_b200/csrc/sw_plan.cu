@@ -83,6 +83,8 @@ struct sw_plan {
     uint64_t merged_epoch = 0, merged_n = 0;  // multi-rank merged front cached in d_gather
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint32_t prefetch = kPrefetch;  // SW_PREFETCH: scan L2 prefetch distance (iterations per group)
+    bool trace = false;             // SW_TRACE=1: per-phase CUDA-event times of each select on stderr
+    std::vector<std::pair<const char*, cudaEvent_t>> tr;  // (phase that ENDS at the event, event)
     uint64_t* d_counts = nullptr;
     uint32_t* d_gfeas = nullptr;  // [SW_MAX_QUERIES] grid-wide "feasible seen" flags of a select
     GreedyOut* d_greedy = nullptr;
@@ -514,6 +516,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     if (const char* ev = getenv("SW_PREFETCH")) h->prefetch = (uint32_t)atoi(ev);
+    if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
     if (cudaError_t se = set_scan_smem_attrs(); se != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ECUDA, "scan kernels cannot launch one block per SM (%s; smem %zu/%zu B)",
@@ -555,7 +558,9 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
             return bail(fail(nullptr, SW_ECUDA, "self job upload failed"));
     }
     if ((st = alloc_n(h, &h->d_digest, 1, "digest")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 1, "counts")) < 0) return bail(st);
+    // [0, R) gathered counts, [R] mine, [R+1] saved local front size, [R+2] merged size,
+    // [R+3] pad overflow flag of the asynchronous merge
+    if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 4, "counts")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_gfeas, SW_MAX_QUERIES, "select flags")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_greedy, 1, "greedy result")) < 0) return bail(st);
     h->level_score.assign(tb->level_score, tb->level_score + tb->n_levels);
@@ -687,6 +692,31 @@ static sw_status begin_timed(sw_plan* h, uint32_t kind, uint64_t bytes, int* pai
 static sw_status end_timed(sw_plan* h, int pair) {
     CK(h, cudaEventRecord(h->ev[2 * pair + 1], h->stream));
     return SW_OK;
+}
+
+// SW_TRACE: mark the end of a phase on the stream (no-op unless tracing).
+static void trace_mark(sw_plan* h, const char* phase) {
+    if (!h->trace) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, h->stream);
+    h->tr.emplace_back(phase, e);
+}
+
+// After a sync: print the phase durations and drop the events.
+static void trace_dump(sw_plan* h, const char* what) {
+    if (!h->trace || h->tr.empty()) return;
+    std::string line = std::string("[sw trace] rank ") + std::to_string(h->rank) + " " + what + ":";
+    for (size_t i = 1; i < h->tr.size(); i++) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->tr[i - 1].second, h->tr[i].second);
+        char buf[96];
+        snprintf(buf, sizeof buf, " %s %.3f", h->tr[i].first, ms);
+        line += buf;
+    }
+    fprintf(stderr, "%s ms\n", line.c_str());
+    for (auto& pe : h->tr) cudaEventDestroy(pe.second);
+    h->tr.clear();
 }
 
 extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
@@ -873,6 +903,8 @@ static sw_status reduce_async(sw_plan* h, PPoint* out) {
     CKL(h);
     pareto_mark2d_kernel<<<2 * h->num_sms, kScanThreads, 0, h->stream>>>(h->d_tmp2, &c->m_loc, h->d_keep);
     CKL(h);
+    // compaction first: the O(m^2) rank sort then runs over the (few hundred) kept points
+    // only (a fused compact+rank over all m measured 7x slower)
     pareto_compact_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_tmp2, &c->m_loc, h->d_keep, h->d_work, &c->m_cmp);
     CKL(h);
     pareto_rank_kernel<<<gs, kScanThreads, 0, h->stream>>>(h->d_work, &c->m_cmp, out, c, h->front_cap);
@@ -916,9 +948,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         SegView v = view_of(h, g, 0, g.ntiles);
         v.pass = pass;
         v.upt = upt;
-        dlt_head_kernel<<<1, 1024, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
-        CKL(h);
-        dlt_cell_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+        dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
         const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / kStageRecs), h->scan_grid);
@@ -931,14 +961,17 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         int pr = 0;
         sw_status ts = begin_timed(h, SW_KERNEL_SCAN, recs * sizeof(Rec4), &pr);
         if (ts < 0) return ts;
+        trace_mark(h, "dlt");
         launch_scan_nq<true>(nq, grid, psmem, h->stream, v, P, part, pareto_args(h));
         CKL(h);
         if ((ts = end_timed(h, pr)) < 0) return ts;
+        trace_mark(h, pass == 1 ? "scan1" : pass == 2 ? "scan2" : pass == 3 ? "scan3" : "scan");
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                h->d_ctl);
         CKL(h);
         sw_status st = reduce_async(h, h->d_front);
         if (st < 0) return st;
+        trace_mark(h, "merge");
         h->fold_passes++;
         h->epoch++;
         if (h->debug) {  // diagnostics only: synchronises every pass
@@ -966,7 +999,44 @@ static sw_status sync_ctl(sw_plan* h, bool* overflow) {
     return SW_OK;
 }
 
-// Winners of front-answerable queries (R30) from the exact global front.  Collective.
+// The exact global front, launched asynchronously: 1 rank -> the running front and its
+// device-side size; several -> counts and fronts padded to kMergePad points allgathered,
+// concatenated and merged on the device into d_gather (size in d_counts[R+2]); the local
+// front size is saved and restored on the device.  Cached per state epoch.  Collective.
+// After the caller's sync, finish_global_front() records the cache or reports that some
+// front exceeded the pad (then the synchronous global_front() redoes the merge).
+static constexpr uint32_t kMergePad = 4096;
+
+static sw_status global_front_async(sw_plan* h, const PPoint** res, const uint64_t** d_n, bool* launched) {
+    *launched = false;
+    if (h->nranks == 1) {
+        *res = h->d_front;
+        *d_n = &h->d_ctl->front_n;
+        return SW_OK;
+    }
+    const int R = h->nranks;
+    *res = h->d_gather;
+    *d_n = h->d_counts + R + 2;
+    if (h->merged_epoch == h->epoch) return SW_OK;  // cached merge, size already on device
+    ParetoCtl* c = h->d_ctl;
+    CK(h, cudaMemcpyAsync(h->d_counts + R, &c->front_n, 8, cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->d_counts + R + 1, &c->front_n, 8, cudaMemcpyDeviceToDevice, h->stream));
+    CKN(h, ncclAllGather(h->d_counts + R, h->d_counts, 1, ncclUint64, h->comm, h->stream));
+    CKN(h, ncclAllGather(h->d_front, h->d_gather, (size_t)kMergePad * sizeof(PPoint), ncclUint8, h->comm, h->stream));
+    const uint64_t all = (uint64_t)kMergePad * R;
+    front_gather_pad_kernel<<<(uint32_t)((all + 255) / 256), 256, 0, h->stream>>>(
+        h->d_gather, h->d_counts, R, kMergePad, h->d_work, c, h->d_counts + R + 3);
+    CKL(h);
+    sw_status st = reduce_async(h, h->d_gather);
+    if (st < 0) return st;
+    CK(h, cudaMemcpyAsync(h->d_counts + R + 2, &c->front_n, 8, cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(&c->front_n, h->d_counts + R + 1, 8, cudaMemcpyDeviceToDevice, h->stream));
+    *launched = true;
+    return SW_OK;
+}
+
+// Winners of front-answerable queries (R30) from the exact global front, synchronous
+// (fallback path).  Collective.
 static sw_status front_answer(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
     const PPoint* fr = nullptr;
     uint64_t n = 0;
@@ -976,7 +1046,7 @@ static sw_status front_answer(sw_plan* h, uint32_t nq, const sw_query* qs, sw_se
     P.nq = nq;
     P.objective = (h->h.flags & 4u) ? 1u : 0u;
     for (uint32_t q = 0; q < nq; q++) P.q[q] = QueryDev{qs[q].slo_startup_us, qs[q].slo_stall_us, qs[q].budget_mc};
-    select_front_kernel<<<1, kScanThreads, 0, h->stream>>>(fr, n, P, h->d_cand);
+    select_front_kernel<<<1, kScanThreads, 0, h->stream>>>(fr, n, nullptr, P, h->d_cand);
     CKL(h);
     launch_np(h, [&](auto npc) {
         constexpr int NPc = decltype(npc)::value;
@@ -1003,52 +1073,38 @@ static sw_status front_answer(sw_plan* h, uint32_t nq, const sw_query* qs, sw_se
 }
 
 // A query is front-answerable (R30) when it bounds neither startup nor stall under the
-// QUALITY_FIRST objective and the handle's front covers exactly its records.
+// QUALITY_FIRST objective (and the handle's front covers exactly its records).
 static bool front_query(const sw_plan* h, const sw_query& q) {
     return h->fuse_pareto && !(h->h.flags & 4u) && q.slo_startup_us == UINT64_MAX && q.slo_stall_us == UINT64_MAX;
 }
 
-static sw_status select_scan(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out);
-
-extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
-    if (!h || !qs || !out) return fail(nullptr, SW_EINVAL, "null argument");
-    if (nq < 1 || nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u not in 1..%d", nq, SW_MAX_QUERIES);
-    CK(h, cudaSetDevice(h->device));
+// Select over the held records.  Scan queries (S) ride on the fused select + Pareto-fold
+// scans (or a plain scan of already folded segments); front-answerable queries (F, when
+// allow_front) are reduced over the exact global front.  Everything -- scans, folds,
+// merges, allgathers, every winner's detail -- is launched asynchronously and read back
+// with ONE synchronisation; a Pareto capacity overflow falls back to the synchronous
+// refold + front answer.  Collective when nranks > 1.
+static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out, bool allow_front) {
     uint32_t fi[SW_MAX_QUERIES], si[SW_MAX_QUERIES], nf = 0, ns = 0;
     for (uint32_t q = 0; q < nq; q++) {
-        if (!h->released && front_query(h, qs[q])) fi[nf++] = q;
+        if (allow_front && front_query(h, qs[q])) fi[nf++] = q;
         else si[ns++] = q;
     }
-    if (nf == 0) return select_scan(h, nq, qs, out);
-    sw_query qf[SW_MAX_QUERIES], qsn[SW_MAX_QUERIES];
-    sw_selection of[SW_MAX_QUERIES], os[SW_MAX_QUERIES];
-    for (uint32_t j = 0; j < nf; j++) qf[j] = qs[fi[j]];
-    for (uint32_t j = 0; j < ns; j++) qsn[j] = qs[si[j]];
-    sw_status worst = SW_OK, st;
-    if (ns) {  // the scan queries (the fused scan also folds the records into the front)
-        st = select_scan(h, ns, qsn, os);
-        if (st < 0) return st;
-        worst = std::max(worst, st);
-    }
-    st = front_answer(h, nf, qf, of);  // folds whatever is still pending first
-    if (st < 0) return st;
-    worst = std::max(worst, st);
-    for (uint32_t j = 0; j < nf; j++) out[fi[j]] = of[j];
-    for (uint32_t j = 0; j < ns; j++) out[si[j]] = os[j];
-    return worst;
-}
-
-static sw_status select_scan(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
-    SelParams P{};
-    P.nq = nq;
-    P.objective = (h->h.flags & 4u) ? 1u : 0u;
-    for (uint32_t q = 0; q < nq; q++) P.q[q] = QueryDev{qs[q].slo_startup_us, qs[q].slo_stall_us, qs[q].budget_mc};
+    SelParams PS{}, PF{};
+    PS.objective = PF.objective = (h->h.flags & 4u) ? 1u : 0u;
+    PS.nq = ns;
+    PF.nq = nf;
+    for (uint32_t j = 0; j < ns; j++)
+        PS.q[j] = QueryDev{qs[si[j]].slo_startup_us, qs[si[j]].slo_stall_us, qs[si[j]].budget_mc};
+    for (uint32_t j = 0; j < nf; j++)
+        PF.q[j] = QueryDev{qs[fi[j]].slo_startup_us, qs[fi[j]].slo_stall_us, qs[fi[j]].budget_mc};
     uint32_t np = 0;
     std::vector<size_t> fused;
+    trace_mark(h, "start");
     CK(h, cudaMemsetAsync(h->d_gfeas, 0, sizeof(uint32_t) * SW_MAX_QUERIES, h->stream));
     bool seeded = h->front_n > 0;
-    for (size_t si = 0; si < h->segs.size(); si++) {
-        Segment& g = h->segs[si];
+    for (size_t si_ = 0; si_ < h->segs.size(); si_++) {
+        Segment& g = h->segs[si_];
         const uint64_t n = g.end - g.begin;
         if (n == 0) continue;
         if (h->fuse_pareto && !g.folded) {  // a8 rides on the same 32 B loads as a9
@@ -1056,72 +1112,118 @@ static sw_status select_scan(sw_plan* h, uint32_t nq, const sw_query* qs, sw_sel
                 sw_status st = seed_async(h, g);
                 if (st < 0) return st;
                 seeded = true;
+                trace_mark(h, "seed");
             }
-            sw_status st = fold_chunks_async(h, g, nq, P, &np);
+            sw_status st = fold_chunks_async(h, g, ns, PS, &np);
             if (st < 0) return st;
             g.folded = true;
-            fused.push_back(si);
-        } else {
+            fused.push_back(si_);
+        } else if (ns) {
             const uint32_t grid = (uint32_t)std::min<uint64_t>(g.ntiles, h->scan_grid);
             if (np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many segments for one select");
             int pr = 0;
             sw_status ts = begin_timed(h, SW_KERNEL_SCAN, g.ntiles * kTileRows * h->row * sizeof(Rec4), &pr);
             if (ts < 0) return ts;
-            launch_scan_nq<false>(nq, grid, kRingBytes, h->stream, view_of(h, g, 0, g.ntiles), P,
+            launch_scan_nq<false>(ns, grid, kRingBytes, h->stream, view_of(h, g, 0, g.ntiles), PS,
                                   h->d_partial + (uint64_t)np * SW_MAX_QUERIES, pareto_args(h));
             CKL(h);
             if ((ts = end_timed(h, pr)) < 0) return ts;
             np += grid;
         }
     }
-    if (np == 0) {
-        // empty local contribution: a row of "none" candidates
-        std::vector<Cand> none(SW_MAX_QUERIES);
-        for (auto& c : none) c.idx = kInf64;
-        CK(h, cudaMemcpyAsync(h->d_partial, none.data(), sizeof(Cand) * SW_MAX_QUERIES, cudaMemcpyHostToDevice,
-                              h->stream));
-        np = 1;
+    trace_mark(h, "folds");
+    if (ns) {
+        if (np == 0) {  // empty local contribution: a row of "none" candidates
+            std::vector<Cand> none(SW_MAX_QUERIES);
+            for (auto& c : none) c.idx = kInf64;
+            CK(h, cudaMemcpyAsync(h->d_partial, none.data(), sizeof(Cand) * SW_MAX_QUERIES, cudaMemcpyHostToDevice,
+                                  h->stream));
+            np = 1;
+        }
+        select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_partial, np, PS, h->d_cand);
+        CKL(h);
+        if (h->nranks > 1) {  // a10: allgather per-rank winners over NVLink, replicated merge
+            CKN(h, ncclAllGather(h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, ncclUint8, h->comm,
+                                 h->stream));
+            select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_cand_all, (uint32_t)h->nranks, PS, h->d_cand);
+            CKL(h);
+        }
     }
-    select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_partial, np, P, h->d_cand);
-    CKL(h);
-    if (h->nranks > 1) {  // a10: allgather per-rank winners over NVLink, replicated merge
-        CKN(h, ncclAllGather(h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, ncclUint8, h->comm,
-                             h->stream));
-        select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_cand_all, (uint32_t)h->nranks, P, h->d_cand);
+    trace_mark(h, "select");
+    bool merged_now = false;
+    if (nf) {
+        const PPoint* fr = nullptr;
+        const uint64_t* d_n = nullptr;
+        sw_status st = global_front_async(h, &fr, &d_n, &merged_now);
+        if (st < 0) return st;
+        trace_mark(h, "front_merge");
+        select_front_kernel<<<1, kScanThreads, 0, h->stream>>>(fr, 0, d_n, PF, h->d_cand + ns);
         CKL(h);
     }
     // every winner's full metrics in one launch, read back with the winners (one sync)
+    const uint32_t nw = ns + nf;
     launch_np(h, [&](auto npc) {
         constexpr int NPc = decltype(npc)::value;
-        detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nq, h->d_detail);
+        detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nw, h->d_detail);
     });
     CKL(h);
     Cand win[SW_MAX_QUERIES];
     DetailOut det[SW_MAX_QUERIES];
-    CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nq, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nq, cudaMemcpyDeviceToHost, h->stream));
-    if (!fused.empty()) {
-        bool overflow = false;
-        sw_status st = sync_ctl(h, &overflow);
-        if (st < 0) return st;
-        if (overflow)  // the front is valid but incomplete: refold these segments later
-            for (size_t si : fused) h->segs[si].folded = false;
-    } else {
-        CK(h, cudaStreamSynchronize(h->stream));
+    ParetoCtl cc;
+    uint64_t aux[2] = {0, 0};  // merged front size, pad overflow
+    CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nw, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nw, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(&cc, h->d_ctl, sizeof cc, cudaMemcpyDeviceToHost, h->stream));
+    if (h->nranks > 1)
+        CK(h, cudaMemcpyAsync(aux, h->d_counts + h->nranks + 2, 16, cudaMemcpyDeviceToHost, h->stream));
+    trace_mark(h, "answers");
+    CK(h, cudaStreamSynchronize(h->stream));
+    trace_dump(h, "select");
+    if (cc.front_overflow) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
+    h->front_n = cc.front_n;
+    bool redo_front = false;
+    if (cc.surv_overflow) {  // a filter pass overflowed: the front is valid but incomplete
+        CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
+        for (size_t x : fused) h->segs[x].folded = false;
+        redo_front = nf > 0;
+    }
+    if (merged_now) {
+        if (aux[1]) redo_front = nf > 0;  // some rank's front exceeded the pad
+        else if (!cc.surv_overflow) {
+            h->merged_epoch = h->epoch;
+            h->merged_n = aux[0];
+        }
     }
     sw_status worst = SW_OK;
-    for (uint32_t q = 0; q < nq; q++) {
+    for (uint32_t j = 0; j < nw; j++) {
+        const uint32_t q = j < ns ? si[j] : fi[j - ns];
         memset(&out[q], 0, sizeof(sw_selection));
-        if (win[q].idx == kInf64) {
+        if (win[j].idx == kInf64) {
             out[q].status = SW_EMPTY;
-            worst = std::max<sw_status>(worst, SW_EMPTY);
-            continue;
+        } else {
+            detail_to_selection(h, win[j].idx, det[j], &out[q], nullptr);
+            out[q].status = win[j].pad ? SW_CLOSEST : SW_OK;  // feasibility flag set on device
         }
-        detail_to_selection(h, win[q].idx, det[q], &out[q], nullptr);
-        out[q].status = win[q].pad ? SW_CLOSEST : SW_OK;  // feasibility flag set on device
         worst = std::max<sw_status>(worst, out[q].status);
     }
+    if (redo_front) {  // rare: exact refold, full-size merge, answer again
+        sw_query qf[SW_MAX_QUERIES];
+        sw_selection of[SW_MAX_QUERIES];
+        for (uint32_t j = 0; j < nf; j++) qf[j] = qs[fi[j]];
+        sw_status st = front_answer(h, nf, qf, of);
+        if (st < 0) return st;
+        worst = SW_OK;
+        for (uint32_t j = 0; j < nf; j++) out[fi[j]] = of[j];
+        for (uint32_t q = 0; q < nq; q++) worst = std::max<sw_status>(worst, out[q].status);
+    }
     return worst;
+}
+
+extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
+    if (!h || !qs || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (nq < 1 || nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u not in 1..%d", nq, SW_MAX_QUERIES);
+    CK(h, cudaSetDevice(h->device));
+    return select_impl(h, nq, qs, out, !h->released);
 }
 
 extern "C" sw_status sw_plan_select(sw_plan* h, uint64_t slo_startup_us, uint64_t slo_stall_us, uint64_t budget_mc,
@@ -1179,7 +1281,7 @@ extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uin
         sw_status st = sw_plan_eval(h, c0, c1);
         if (st < 0) return st;
         if (ns) {
-            st = select_scan(h, ns, qsn, tmp);  // also folds the chunk into the front
+            st = select_impl(h, ns, qsn, tmp, false);  // also folds the chunk into the front
             if (st < 0) return st;
             for (uint32_t j = 0; j < ns; j++)
                 sw_selection_merge(h->h.flags & 4u ? 1u : 0u, &qsn[j], &out[si[j]], &tmp[j], &out[si[j]]);
@@ -1301,6 +1403,8 @@ static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_ou
         h->merged_epoch = h->epoch;
         h->merged_n = n;
         CK(h, cudaMemcpyAsync(&h->d_ctl->front_n, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
+        // the asynchronous path reads the cached merge's size from the device
+        CK(h, cudaMemcpyAsync(h->d_counts + h->nranks + 2, &n, sizeof n, cudaMemcpyHostToDevice, h->stream));
         CK(h, cudaStreamSynchronize(h->stream));
     }
     *res_out = res;

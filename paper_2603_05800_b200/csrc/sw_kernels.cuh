@@ -8,6 +8,8 @@
 // pareto_*        : a8 exact 3-D Pareto front (DLT filter + exact dominance merge)
 // digest_kernel   : order-independent record digest (full-space parity tool)
 #pragma once
+#include <cooperative_groups.h>
+
 #include "sw_device.cuh"
 
 namespace sw {
@@ -32,8 +34,8 @@ struct SegView {
     uint64_t ib, ie;
     // Strided fold passes (scan kernels only): the view is cut into units of `upt`
     // tiles (a whole number of scan stages); pass 1 scans units u % 64 == 0, pass 2
-    // u % 8 == 0 && u % 64 != 0, pass 3 u % 8 != 0 -- each pass a uniform sample of the
-    // whole segment, so the Pareto filter sees every region of the space early.
+    // u % 8 == 0 && u % 64 != 0, pass 3 u % 8 != 0 (pass 4 = passes 2 and 3 at once) -- each
+    // a uniform sample of the whole segment, so the Pareto filter sees every region early.
     // pass 0: the whole view in order.
     uint32_t pass, upt;
 };
@@ -569,10 +571,11 @@ struct __align__(16) PPoint {  // == sw_pareto_point
 // y dominates x: <= in ttff_eff and cost, >= in quality, one strict; exact duplicates
 // keep the lowest index (R14); identical entries (same index) keep the first position.
 __device__ __forceinline__ bool pdom(const PPoint& y, uint32_t py, const PPoint& x, uint32_t px) {
-    if (!(y.t <= x.t && y.c <= x.c && y.q >= x.q)) return false;
-    if (y.t < x.t || y.c < x.c || y.q > x.q) return true;
-    if (y.idx != x.idx) return y.idx < x.idx;
-    return py < px;
+    // branch-free, so that unrolled loops overlap several tests
+    const bool le = (y.t <= x.t) & (y.c <= x.c) & (y.q >= x.q);
+    const bool strict = (y.t < x.t) | (y.c < x.c) | (y.q > x.q);
+    const bool tie = (y.idx < x.idx) | ((y.idx == x.idx) & (py < px));
+    return le & (strict | tie);
 }
 
 // Device-side sizes of the Pareto merge pipeline: every kernel below reads its input
@@ -583,6 +586,7 @@ struct ParetoCtl {
     uint64_t front_n;         // size of the running front (d_front)
     uint32_t surv_overflow;   // a filter pass had more survivors than capacity
     uint32_t front_overflow;  // the front exceeded its capacity
+    uint64_t stamp[6];        // diagnostics: %globaltimer at the merge kernel's phase ends
 };
 
 // keep[x] = no other point of pts[0,m) dominates x.  O(m^2), tiles through smem.
@@ -933,6 +937,145 @@ __global__ void __launch_bounds__(kScanThreads) select_front_kernel(const PPoint
     }
 }
 
+// The whole exact merge work[0, ctl.m_in) -> sorted front in `out`, in ONE cooperative
+// launch (a persistent grid of 1024-thread blocks, phases separated by grid-wide
+// barriers): (1) 256-point block-local fronts into tmp2, (2) the m x m dominance mark in
+// 256 x 256 tiles, (3) compaction into work, (4) rank sort into out; publishes front_n /
+// front_overflow.  Every 256-point tile is worked by 4 threads per point (64 tests each,
+// 8 independent tests per step): the phases are latency chains, not throughput, so the
+// critical path is what counts.  Reads of data other blocks wrote in an earlier phase
+// bypass L1 (__ldcg).
+constexpr int kRedThreads = 1024;
+constexpr int kRedParts = kRedThreads / kScanThreads;  // threads per point
+constexpr uint32_t kRedSpan = kScanThreads / kRedParts;  // candidates per thread per tile
+
+__device__ __forceinline__ PPoint ldcg_point(const PPoint* p) {
+    PPoint x;
+    x.idx = __ldcg(&p->idx);
+    x.t = __ldcg(&p->t);
+    x.c = __ldcg(&p->c);
+    x.q = __ldcg(&p->q);
+    x.pad = 0;
+    return x;
+}
+
+// Does any of tile[j0, j0 + kRedSpan) (restricted to j < lim, position y0 + j != px)
+// dominate x?  Branch-free groups of 8 tests.
+__device__ __forceinline__ bool span_dominated(const PPoint* tile, uint32_t j0, uint32_t lim, uint32_t y0,
+                                               const PPoint& x, uint32_t px) {
+    bool dom = false;
+    for (uint32_t g = 0; g < kRedSpan && !dom; g += 8) {
+#pragma unroll
+        for (uint32_t u = 0; u < 8; u++) {
+            const uint32_t j = j0 + g + u;
+            const bool ok = (j < lim) & (y0 + j != px);
+            dom |= ok & pdom(tile[ok ? j : 0], y0 + j, x, px);
+        }
+    }
+    return dom;
+}
+
+__global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* __restrict__ work,
+                                                                       PPoint* __restrict__ tmp2,
+                                                                       uint8_t* __restrict__ keep,
+                                                                       PPoint* __restrict__ out, ParetoCtl* ctl,
+                                                                       uint64_t cap) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ PPoint tile[kScanThreads];
+    __shared__ uint8_t s_dom[kScanThreads];
+    __shared__ uint32_t s_rank[kScanThreads];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t pt = tid % kScanThreads, part = tid / kScanThreads;
+    auto stamp = [&](int i) {
+        if (blockIdx.x == 0 && tid == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            ctl->stamp[i] = t;
+        }
+    };
+    stamp(0);
+    if (blockIdx.x == 0 && tid == 0) {
+        ctl->m_loc = 0;
+        ctl->m_cmp = 0;
+    }
+    grid.sync();
+    stamp(1);
+    const uint32_t m = __ldcg(&ctl->m_in);
+    // (1) block-local fronts of 256-point chunks
+    for (uint32_t base = blockIdx.x * kScanThreads; base < m; base += gridDim.x * kScanThreads) {
+        const uint32_t cnt = min((uint32_t)kScanThreads, m - base);
+        __syncthreads();
+        if (part == 0) {
+            if (pt < cnt) tile[pt] = work[base + pt];
+            s_dom[pt] = 0;
+        }
+        __syncthreads();
+        if (pt < cnt && span_dominated(tile, part * kRedSpan, cnt, base, tile[pt], base + pt)) s_dom[pt] = 1;
+        __syncthreads();
+        if (part == 0 && pt < cnt && !s_dom[pt]) {
+            const uint32_t slot = atomicAdd(&ctl->m_loc, 1u);
+            tmp2[slot] = tile[pt];
+            keep[slot] = 1;
+        }
+    }
+    grid.sync();
+    stamp(2);
+    const uint32_t ml = __ldcg(&ctl->m_loc);
+    // (2) dominance mark over 256 x 256 tiles
+    const uint32_t nb = (ml + kScanThreads - 1) / kScanThreads;
+    const uint64_t items = (uint64_t)nb * nb;
+    for (uint64_t w = blockIdx.x; w < items; w += gridDim.x) {
+        const uint32_t xb = (uint32_t)(w / nb), yb = (uint32_t)(w - (uint64_t)xb * nb);
+        const uint32_t x = xb * kScanThreads + pt, y0 = yb * kScanThreads;
+        __syncthreads();
+        if (part == 0 && y0 + pt < ml) tile[pt] = ldcg_point(&tmp2[y0 + pt]);
+        __syncthreads();
+        if (x >= ml || !__ldcg(&keep[x])) continue;
+        const PPoint px = ldcg_point(&tmp2[x]);
+        const uint32_t lim = min((uint32_t)kScanThreads, ml - y0);
+        if (span_dominated(tile, part * kRedSpan, lim, y0, px, x)) keep[x] = 0;
+    }
+    grid.sync();
+    stamp(3);
+    // (3) compaction of the kept points into work
+    for (uint32_t x = blockIdx.x * blockDim.x + tid; x < ml; x += gridDim.x * blockDim.x)
+        if (__ldcg(&keep[x])) work[atomicAdd(&ctl->m_cmp, 1u)] = ldcg_point(&tmp2[x]);
+    grid.sync();
+    stamp(4);
+    const uint32_t mc = __ldcg(&ctl->m_cmp);
+    if (blockIdx.x == 0 && tid == 0) {
+        ctl->front_n = mc <= cap ? mc : 0;
+        if (mc > cap) ctl->front_overflow = 1;
+    }
+    if (mc > cap) return;
+    // (4) rank sort by (t asc, c asc, q desc, index asc) -- indices are unique (a bitonic
+    // sort of the few hundred points in one block measured slower: ~45 barrier steps)
+    for (uint32_t xb = blockIdx.x; xb * kScanThreads < mc; xb += gridDim.x) {
+        const uint32_t x = xb * kScanThreads + pt;
+        __syncthreads();
+        if (part == 0) s_rank[pt] = 0;
+        const PPoint px = x < mc ? ldcg_point(&work[x]) : PPoint{};
+        uint32_t rank = 0;
+        for (uint32_t base = 0; base < mc; base += kScanThreads) {
+            __syncthreads();
+            if (part == 0 && base + pt < mc) tile[pt] = ldcg_point(&work[base + pt]);
+            __syncthreads();
+            const uint32_t lim = min((uint32_t)kScanThreads, mc - base);
+            const uint32_t j0 = part * kRedSpan;
+#pragma unroll 8
+            for (uint32_t g = 0; g < kRedSpan; g++) {
+                const uint32_t j = j0 + g;
+                rank += ((j < lim) & pkey_less(tile[j < lim ? j : 0], px)) ? 1u : 0u;
+            }
+        }
+        atomicAdd(&s_rank[pt], rank);
+        __syncthreads();
+        if (part == 0 && x < mc) out[s_rank[pt]] = px;
+    }
+    if (blockIdx.x == 0) stamp(5);  // block 0's own share of the rank sort done
+}
+
 // ============================================================================ fused scan
 // One pass over a record segment serves (a9) up to NQ select queries and, when PARETO,
 // (a8) the front filter: (1) the DLT prefilter, O(1) per record; (2) for DLT survivors
@@ -941,6 +1084,7 @@ __global__ void __launch_bounds__(kScanThreads) select_front_kernel(const PPoint
 // candidate cannot be on the front, so the survivors always contain every true front
 // point of the segment whatever front subset is used: the later merge stays exact.
 constexpr uint32_t kFrontSmem = 512;  // front points held in smem for the exact filter
+constexpr uint32_t kBlockSurv = 256;  // this block's own survivors, kept in smem as a second filter
 
 struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select flags
     const Dlt* dlt;
@@ -1093,6 +1237,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     Rec4* ring = reinterpret_cast<Rec4*>(fsm);
     Dlt& d = *reinterpret_cast<Dlt*>(fsm + ring_bytes(PARETO));
     PPoint* fs = reinterpret_cast<PPoint*>(fsm + ring_bytes(PARETO) + sizeof(Dlt));
+    PPoint* bsurv = fs + kFrontSmem;  // PARETO only
+    __shared__ uint32_t s_bcnt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int st = 0; st < NS; st++) {
@@ -1104,6 +1250,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         s_thr[threadIdx.x] = 0;
         s_vt[threadIdx.x] = ~0ull;
     }
+    if (threadIdx.x == 0) s_bcnt = 0;
     uint32_t m_sm = 0, m_all = 0;
     if (PARETO) {
         m_all = (uint32_t)pa.ctl->front_n;
@@ -1114,6 +1261,17 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
             for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
         }
         for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = pa.front[i];
+        // a reserved-but-not-yet-written (or torn) survivor slot must dominate nothing:
+        // sentinel t = c = max, q = 0 (a torn write mixes halves that still carry a max)
+        for (uint32_t i = threadIdx.x; i < kBlockSurv; i += blockDim.x) {
+            PPoint sent;
+            sent.idx = kInf64;
+            sent.t = kInf64;
+            sent.c = kInf64;
+            sent.q = 0;
+            sent.pad = 0;
+            bsurv[i] = sent;
+        }
     }
     __syncthreads();
     DltHot dh{0, 0, 0, 0};
@@ -1126,13 +1284,19 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     const uint64_t nunits = v.pass ? (total + unit_recs - 1) / unit_recs : 0;
     const uint64_t k8 = (nunits + 7) / 8, k64 = (nunits + 63) / 64;
     const uint64_t nstages = v.pass == 0 ? (total + kStageRecs - 1) / kStageRecs
-                                         : spu * (v.pass == 1 ? k64 : v.pass == 2 ? k8 - k64 : nunits - k8);
+                                         : spu * (v.pass == 1   ? k64
+                                                  : v.pass == 2 ? k8 - k64
+                                                  : v.pass == 3 ? nunits - k8
+                                                                : nunits - k64);
     auto stage_pos = [&](uint64_t sg) -> uint64_t {
         if (v.pass == 0) return sg * kStageRecs;
         // stage counts stay far below 2^32 (2^32 stages = 1.4e14 records): 32-bit divides
         const uint32_t j = (uint32_t)sg / (uint32_t)spu, part = (uint32_t)sg - j * (uint32_t)spu;
         const uint64_t m = (uint64_t)(j / 7) * 8 + (j % 7) + 1;  // j-th positive non-multiple of 8
-        const uint64_t u = v.pass == 1 ? 64 * j : v.pass == 2 ? 8 * m : m;
+        const uint64_t u = v.pass == 1   ? 64 * (uint64_t)j
+                           : v.pass == 2 ? 8 * m
+                           : v.pass == 3 ? m
+                                         : (uint64_t)(j / 63) * 64 + (j % 63) + 1;  // pass 4: not multiples of 64
         const uint64_t pos = u * unit_recs + part * kStageRecs;
         return pos < total ? pos : kInf64;
     };
@@ -1339,22 +1503,51 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                             const bool dj = j < m_all && pdom(pa.front[j], 0, x, 1);
                             if (__any_sync(0xffffffffu, dj)) dom = true;
                         }
+                        // ... and against this block's earlier survivors: neighbouring
+                        // records (one stage = 1024 consecutive indices) often dominate
+                        // each other, and every survivor costs the merge O(m)
+                        const uint32_t bc = min(*(volatile uint32_t*)&s_bcnt, kBlockSurv);
+                        for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {
+                            const uint32_t j = j0 + lane;
+                            const bool dj = j < bc && pdom(bsurv[j], 0, x, 1);
+                            if (__any_sync(0xffffffffu, dj)) dom = true;
+                        }
                         if (lane == src && dom) keep = false;
                     }
                     const unsigned mask = __ballot_sync(0xffffffffu, keep);
                     if (mask) {
                         const int ldr = __ffs(mask) - 1;
-                        unsigned long long slot0 = 0;
-                        if (lane == ldr) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(mask));
-                        slot0 = __shfl_sync(0xffffffffu, slot0, ldr);
-                        if (keep) {
-                            const uint64_t slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-                            if (slot < pa.cap) pa.surv[slot] = pt;
+                        uint32_t b0 = 0;
+                        if (lane == ldr) b0 = atomicAdd(&s_bcnt, (uint32_t)__popc(mask));
+                        b0 = __shfl_sync(0xffffffffu, b0, ldr);
+                        const uint32_t my = b0 + __popc(mask & ((1u << lane) - 1u));
+                        const bool local = my < kBlockSurv;
+                        if (keep && local) bsurv[my] = pt;
+                        // block list full: straight to the global survivor buffer
+                        const unsigned gmask = __ballot_sync(0xffffffffu, keep && !local);
+                        if (gmask) {
+                            const int gl = __ffs(gmask) - 1;
+                            unsigned long long slot0 = 0;
+                            if (lane == gl) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(gmask));
+                            slot0 = __shfl_sync(0xffffffffu, slot0, gl);
+                            if (keep && !local) {
+                                const uint64_t slot = slot0 + __popc(gmask & ((1u << lane) - 1u));
+                                if (slot < pa.cap) pa.surv[slot] = pt;
+                            }
                         }
                     }
                 }
             }
         }
+    }
+    if (PARETO) {  // flush this block's survivor list to the global survivor buffer
+        __syncthreads();
+        __shared__ unsigned long long s_base;
+        const uint32_t nb = min(s_bcnt, kBlockSurv);
+        if (threadIdx.x == 0) s_base = nb ? atomicAdd(&pa.ctl->surv, (unsigned long long)nb) : 0ull;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+            if (s_base + i < pa.cap) pa.surv[s_base + i] = bsurv[i];
     }
 #pragma unroll
     for (int q = 0; q < NQ; q++) {

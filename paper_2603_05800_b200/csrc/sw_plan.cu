@@ -83,6 +83,9 @@ struct sw_plan {
     uint64_t merged_epoch = 0, merged_n = 0;  // multi-rank merged front cached in d_gather
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint32_t prefetch = kPrefetch;  // SW_PREFETCH: scan L2 prefetch distance (iterations per group)
+    bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
+    uint32_t passes = 3;            // SW_PASSES: strided fold passes per segment (2 or 3)
+    uint32_t coop_grid = 0;
     bool trace = false;             // SW_TRACE=1: per-phase CUDA-event times of each select on stderr
     std::vector<std::pair<const char*, cudaEvent_t>> tr;  // (phase that ENDS at the event, event)
     uint64_t* d_counts = nullptr;
@@ -517,10 +520,24 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     if (const char* ev = getenv("SW_PREFETCH")) h->prefetch = (uint32_t)atoi(ev);
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
+    if (const char* ev = getenv("SW_COOP_REDUCE")) h->coop_reduce = atoi(ev) != 0;
+    if (const char* ev = getenv("SW_PASSES")) h->passes = atoi(ev) == 2 ? 2u : 3u;
+    {  // the cooperative merge needs all its blocks co-resident
+        int occ = 0, coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pareto_reduce_kernel, kRedThreads, 0) != cudaSuccess ||
+            occ < 1 || !coop) {
+            cudaGetLastError();
+            h->coop_reduce = false;
+        }
+        h->coop_grid = (uint32_t)(std::min(occ, 1) * h->num_sms);  // one block per SM
+        if (const char* ev = getenv("SW_COOP_GRID"))
+            h->coop_grid = std::min<uint32_t>(h->coop_grid, std::max(1, atoi(ev)));
+    }
     if (cudaError_t se = set_scan_smem_attrs(); se != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ECUDA, "scan kernels cannot launch one block per SM (%s; smem %zu/%zu B)",
-                         cudaGetErrorString(se), ring_bytes(true) + sizeof(Dlt) + kFrontSmem * sizeof(PPoint),
+                         cudaGetErrorString(se), ring_bytes(true) + sizeof(Dlt) + (kFrontSmem + kBlockSurv) * sizeof(PPoint),
                          ring_bytes(false)));
     }
 
@@ -847,7 +864,7 @@ static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t
     }
 }
 
-static constexpr size_t kScanSmemPareto = ring_bytes(true) + sizeof(Dlt) + kFrontSmem * sizeof(PPoint);
+static constexpr size_t kScanSmemPareto = ring_bytes(true) + sizeof(Dlt) + (kFrontSmem + kBlockSurv) * sizeof(PPoint);
 static constexpr size_t kRingBytes = ring_bytes(false);
 
 template <int NQ>
@@ -892,6 +909,18 @@ static ParetoArgs pareto_args(sw_plan* h) {
 // (two block-local passes in smem, a global O(m'^2) mark, compaction, rank sort).
 // Grids are sized for the capacity; blocks beyond the live count exit at once.
 static sw_status reduce_async(sw_plan* h, PPoint* out) {
+    if (h->coop_reduce) {  // one cooperative launch for the whole merge
+        PPoint* work = h->d_work;
+        PPoint* tmp2 = h->d_tmp2;
+        uint8_t* keep = h->d_keep;
+        ParetoCtl* ctl = h->d_ctl;
+        uint64_t cap = h->front_cap;
+        void* args[] = {&work, &tmp2, &keep, &out, &ctl, &cap};
+        CK(h, cudaLaunchCooperativeKernel((const void*)pareto_reduce_kernel, dim3(h->coop_grid), dim3(kRedThreads),
+                                          args, 0, h->stream));
+        h->launches++;
+        return SW_OK;
+    }
     const uint64_t U = h->front_cap + h->surv_cap;
     ParetoCtl* c = h->d_ctl;
     const uint32_t gl = (uint32_t)((U + kLocal - 1) / kLocal), gs = (uint32_t)((U + kScanThreads - 1) / kScanThreads);
@@ -916,7 +945,7 @@ static sw_status reduce_async(sw_plan* h, PPoint* out) {
 static sw_status seed_async(sw_plan* h, const Segment& g) {
     const uint64_t n = g.end - g.begin;
     // a strided sample seeds the running front (its exact front is cheap to reduce)
-    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, 32768);
+    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, 16384);
     CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
     pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), ns, h->d_work, h->d_ctl);
     CKL(h);
@@ -940,11 +969,17 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
     const bool strided = nunits >= 256;
     const uint64_t k8 = (nunits + 7) / 8, k64 = (nunits + 63) / 64;
     const uint64_t last_short = nunits * unit_recs - total;  // missing slots of the last unit
-    for (uint32_t pass = strided ? 1 : 0; pass <= (strided ? 3u : 0u); pass++) {
-        uint64_t units = pass == 0 ? nunits : pass == 1 ? k64 : pass == 2 ? k8 - k64 : nunits - k8;
-        const uint64_t L = nunits - 1;  // which pass holds the (possibly short) last unit
-        const uint32_t lp = (L % 64 == 0) ? 1 : (L % 8 == 0) ? 2 : 3;
-        const uint64_t recs = units * unit_recs - ((pass == 0 || pass == lp) ? last_short : 0);
+    // pass schedule: 1/64 then 7/64 then 56/64 (SW_PASSES=3, default), or 1/64 then 63/64
+    const uint32_t sched3[] = {1, 2, 3}, sched2[] = {1, 4}, sched1[] = {0};
+    const uint32_t* sched = !strided ? sched1 : h->passes == 2 ? sched2 : sched3;
+    const uint32_t npass = !strided ? 1 : h->passes == 2 ? 2 : 3;
+    for (uint32_t pi = 0; pi < npass; pi++) {
+        const uint32_t pass = sched[pi];
+        uint64_t units = pass == 0 ? nunits : pass == 1 ? k64 : pass == 2 ? k8 - k64 : pass == 3 ? nunits - k8 : nunits - k64;
+        const uint64_t L = nunits - 1;  // does this pass hold the (possibly short) last unit?
+        const bool has_last = pass == 0 || (pass == 1 && L % 64 == 0) || (pass == 2 && L % 8 == 0 && L % 64 != 0) ||
+                              (pass == 3 && L % 8 != 0) || (pass == 4 && L % 64 != 0);
+        const uint64_t recs = units * unit_recs - (has_last ? last_short : 0);
         SegView v = view_of(h, g, 0, g.ntiles);
         v.pass = pass;
         v.upt = upt;
@@ -965,7 +1000,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         launch_scan_nq<true>(nq, grid, psmem, h->stream, v, P, part, pareto_args(h));
         CKL(h);
         if ((ts = end_timed(h, pr)) < 0) return ts;
-        trace_mark(h, pass == 1 ? "scan1" : pass == 2 ? "scan2" : pass == 3 ? "scan3" : "scan");
+        trace_mark(h, pass == 1 ? "scan1" : pass == 2 ? "scan2" : pass == 3 ? "scan3" : pass == 4 ? "scan23" : "scan");
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                h->d_ctl);
         CKL(h);
@@ -978,9 +1013,13 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
             ParetoCtl c;
             CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
             CK(h, cudaStreamSynchronize(h->stream));
-            fprintf(stderr, "[sw] fold pass %llu: stride pass %u, %llu records, survivors %llu merge-in %u local %u/%u front %llu\n",
+            fprintf(stderr, "[sw] fold pass %llu: stride pass %u, %llu records, survivors %llu merge-in %u local %u/%u front %llu"
+                            " | merge phases us: init %.1f local %.1f mark %.1f compact %.1f rank(b0) %.1f\n",
                     (unsigned long long)h->fold_passes, pass, (unsigned long long)recs,
-                    (unsigned long long)c.surv, c.m_in, c.m_loc, c.m_loc2, (unsigned long long)c.front_n);
+                    (unsigned long long)c.surv, c.m_in, c.m_loc, c.m_loc2, (unsigned long long)c.front_n,
+                    1e-3 * (double)(c.stamp[1] - c.stamp[0]), 1e-3 * (double)(c.stamp[2] - c.stamp[1]),
+                    1e-3 * (double)(c.stamp[3] - c.stamp[2]), 1e-3 * (double)(c.stamp[4] - c.stamp[3]),
+                    1e-3 * (double)(c.stamp[5] - c.stamp[4]));
         }
     }
     return SW_OK;

@@ -8,6 +8,8 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+
+import numpy as np
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -81,6 +83,8 @@ class sw_pareto_point(C.Structure):
     _fields_ = [("index", C.c_uint64), ("ttff_eff_us", C.c_uint64), ("cost_mc", C.c_uint64),
                 ("quality", C.c_uint32), ("pad", C.c_uint32)]
 
+
+_PP_DTYPE = np.dtype([("index", "<u8"), ("t", "<u8"), ("c", "<u8"), ("q", "<u4"), ("pad", "<u4")])
 
 EXPORTS = {
     # name: (restype, argtypes)
@@ -389,17 +393,20 @@ class Plan:
         return _sel(out, self.n_pools, self.B), it.value, ev.value
 
     def pareto(self, cap_hint: int = 4096):
-        """The exact front (sw_pareto_get): one call with a buffer of cap_hint points,
-        a second only when the front is larger (SW_TRUNCATED gives the size)."""
+        """The exact front (sw_pareto_get) as (index, ttff_eff_us, cost_mc, quality) tuples:
+        one call into a buffer kept by the handle, a second only when the front is larger
+        (SW_TRUNCATED gives the size)."""
         n = C.c_uint64()
-        cap = max(1, cap_hint)
-        buf = (sw_pareto_point * cap)()
-        st = self._ck(lib().sw_pareto_get(self.h, buf, cap, C.byref(n)))
+        buf = getattr(self, "_pbuf", None)
+        if buf is None or len(buf) < cap_hint:
+            buf = self._pbuf = (sw_pareto_point * max(1, cap_hint))()
+        st = self._ck(lib().sw_pareto_get(self.h, buf, len(buf), C.byref(n)))
         if st == SW_TRUNCATED:
-            buf = (sw_pareto_point * max(1, n.value))()
-            st = self._ck(lib().sw_pareto_get(self.h, buf, n.value, C.byref(n)))
+            buf = self._pbuf = (sw_pareto_point * max(1, n.value))()
+            st = self._ck(lib().sw_pareto_get(self.h, buf, len(buf), C.byref(n)))
         assert st == SW_OK
-        return [(p.index, p.ttff_eff_us, p.cost_mc, p.quality) for p in buf[: n.value]]
+        a = np.frombuffer(buf, dtype=_PP_DTYPE, count=n.value)
+        return list(zip(a["index"].tolist(), a["t"].tolist(), a["c"].tolist(), a["q"].tolist()))
 
     def digest(self) -> int:
         d = C.c_uint64()

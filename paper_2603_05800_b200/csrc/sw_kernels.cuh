@@ -40,10 +40,10 @@ struct SegView {
     uint32_t pass, upt;
 };
 constexpr int kScanThreads = 256;
-constexpr int kDltT = 128;  // dominance lookup table: ttff_eff bins (front quantiles)
-constexpr int kDltQ = 128;  //                         quality bins (front quantiles)
-constexpr int kDltMap = 4096;  // direct maps (t: 256 cells per octave over 16 octaves; q: linear)
-constexpr int kDltTShift = 15; // t cell key = float bits >> 15 (8 mantissa bits)
+constexpr int kDltT = 255;  // dominance lookup table: ttff_eff bins (front quantiles; <= 255: u8 map)
+constexpr int kDltQ = 128;  //                         quality bins (linear, 2^k wide)
+constexpr int kDltMap = 2048;  // t direct map: 128 cells per octave over 16 octaves
+constexpr int kDltTShift = 16; // t cell key = float bits >> 16 (7 mantissa bits)
 
 // ============================================================================ a2 + packing
 struct RawDesc {
@@ -587,6 +587,7 @@ struct ParetoCtl {
     uint32_t surv_overflow;   // a filter pass had more survivors than capacity
     uint32_t front_overflow;  // the front exceeded its capacity
     uint64_t stamp[6];        // diagnostics: %globaltimer at the merge kernel's phase ends
+    unsigned long long dlt_pass;  // diagnostics: records the DLT did not rule out (all passes)
 };
 
 // keep[x] = no other point of pts[0,m) dominates x.  O(m^2), tiles through smem.
@@ -672,9 +673,16 @@ __global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint*
 struct Dlt {
     int32_t kbase;         // t key of tmap[0]
     uint32_t qmin, qmax, qshift;
-    uint64_t tedge[kDltT];
-    uint8_t tmap[kDltMap];  // #edges <= lower end of t cell k (0..kDltT)
-    uint32_t cell[kDltT * kDltQ];
+    uint32_t cshift, pad_[3];
+    uint64_t tedge[kDltT + 1];
+    // t map cell k: lo = #edges <= the cell's lower end, hi = #edges <= its upper end
+    // (packed lo | hi << 8).  A record's bin count is hi when t >= tedge[hi - 1] (the
+    // cell's largest edge), else lo -- exact also when many front points share one t
+    // (e.g. every stall-free plan behind a static intro)
+    uint16_t tmap[kDltMap];
+    // min cost >> cshift, rounded down (0xffff = none): a record with cost c is strictly
+    // dominated when (cell + 1) << cshift <= c, i.e. the true minimum is < c
+    uint16_t cell[kDltT * kDltQ];
 };
 static_assert(sizeof(Dlt) % 16 == 0, "Dlt is staged in 16 B vectors");
 
@@ -685,7 +693,7 @@ __device__ __forceinline__ int32_t dlt_tkey(uint64_t t) {
 // The DLT's scalar fields, held in registers by the scan consumers.
 struct DltHot {
     int32_t kbase;
-    uint32_t qmin, qmax, qshift;
+    uint32_t qmin, qmax, qshift, cshift;
 };
 
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
@@ -693,9 +701,12 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     const int32_t k = dlt_tkey(t) - hs.kbase;
     const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
     const uint32_t j = min((max(q, hs.qmin) - hs.qmin) >> hs.qshift, (uint32_t)kDltQ - 1);
-    const uint32_t b1 = d.tmap[kc];  // t bin + 1 (0: no front point has t <= this t)
+    const uint32_t lh = d.tmap[kc];
+    const uint32_t lo = lh & 0xffu, hi = lh >> 8;
+    // t bin + 1 (0: no front point has t <= this t)
+    const uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;
     const uint32_t cell = d.cell[(max(b1, 1u) - 1) * kDltQ + j];
-    return (k >= 0) & (q <= hs.qmax) & (b1 != 0) & (cell != 0xffffffffu) & ((uint64_t)cell < c);
+    return (k >= 0) & (q <= hs.qmax) & (b1 != 0) & (cell != 0xffffu) & (((uint64_t)cell + 1) << hs.cshift <= c);
 }
 
 // One launch builds the whole DLT: block b (kDltQ threads) computes the t edges it
@@ -706,27 +717,33 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
     __shared__ PPoint tile[kDltQ];
     __shared__ uint64_t te[kDltT];
     __shared__ uint32_t s_qmin, s_qmax;
+    __shared__ unsigned long long s_cmax;
     const uint32_t m = (uint32_t)ctl->front_n;
     const uint32_t b = blockIdx.x, j = threadIdx.x;
     if (j == 0) {
         s_qmin = 0xffffffffu;
         s_qmax = 0;
+        s_cmax = 0;
     }
     for (uint32_t i = j; i < kDltT; i += blockDim.x) te[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
     __syncthreads();
     uint32_t lo = 0xffffffffu, hi = 0;
+    uint64_t cmx = 0;
     for (uint32_t i = j; i < m; i += blockDim.x) {
-        const uint32_t q = front[i].q;
-        lo = min(lo, q);
-        hi = max(hi, q);
+        const PPoint f = front[i];
+        lo = min(lo, f.q);
+        hi = max(hi, f.q);
+        cmx = umax64(cmx, f.c);
     }
     atomicMin(&s_qmin, lo);
     atomicMax(&s_qmax, hi);
+    atomicMax(&s_cmax, (unsigned long long)cmx);
     __syncthreads();
     const uint32_t qmin = s_qmin, qmax = s_qmax;
-    uint32_t qsh = 0;
+    uint32_t qsh = 0, csh = 0;
     if (m)
         while ((((uint64_t)qmax - qmin) >> qsh) >= (uint64_t)kDltQ) qsh++;
+    while ((s_cmax >> csh) >= 0xffffull) csh++;  // every front cost fits below the 0xffff "none"
     const int32_t kbase = m ? dlt_tkey(front[0].t) : 0x7fffffff;
     if (b == 0) {
         if (j == 0) {
@@ -734,21 +751,30 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
             d->qmin = m ? qmin : 0xffffffffu;
             d->qmax = m ? qmax : 0;
             d->qshift = qsh;
+            d->cshift = csh;
         }
         for (uint32_t i = j; i < kDltT; i += blockDim.x) d->tedge[i] = te[i];
     }
-    // this block's share of the t map: #edges <= lower end of cell k
-    for (uint32_t k = b * (kDltMap / kDltT) + j; k < (b + 1) * (kDltMap / kDltT); k += blockDim.x) {
+    // the t map, dealt over the grid: #edges <= lower end of cell k
+    for (uint32_t k = b * blockDim.x + j; k < (uint32_t)kDltMap; k += gridDim.x * blockDim.x) {
         const int32_t key = kbase + (int32_t)k;
-        const uint64_t L = (!m || key >= (0x7f800000 >> kDltTShift)) ? kInf64
-                                                                     : (uint64_t)ceilf(__uint_as_float((uint32_t)key << kDltTShift));
-        uint32_t a = 0, e = kDltT;
-        while (a < e) {
-            const uint32_t mid = (a + e) >> 1;
-            if (te[mid] <= L) a = mid + 1;
-            else e = mid;
-        }
-        d->tmap[k] = (uint8_t)(m ? a : 0);
+        auto lower_end = [&](int32_t kk) -> uint64_t {  // smallest integer t with key(t) >= kk
+            return (kk >= (0x7f800000 >> kDltTShift)) ? kInf64 : (uint64_t)ceilf(__uint_as_float((uint32_t)kk << kDltTShift));
+        };
+        auto count_le = [&](uint64_t L) -> uint32_t {  // #edges <= L
+            uint32_t a = 0, e = kDltT;
+            while (a < e) {
+                const uint32_t mid = (a + e) >> 1;
+                if (te[mid] <= L) a = mid + 1;
+                else e = mid;
+            }
+            return a;
+        };
+        const uint64_t L = lower_end(key), Lnext = lower_end(key + 1);
+        // the last map cell also covers everything above it
+        const uint64_t U = (k == (uint32_t)kDltMap - 1 || Lnext == kInf64) ? kInf64 : Lnext - 1;
+        const uint32_t lo = m ? count_le(L) : 0, hi = m ? count_le(U) : 0;
+        d->tmap[k] = (uint16_t)(lo | (hi << 8));
     }
     // cell row b, thread j = q bin: needs f.q >= the largest q of bin j
     const uint64_t Eb = te[b];
@@ -770,7 +796,7 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
         }
         more = __syncthreads_or(more);
     }
-    d->cell[b * kDltQ + j] = (m == 0 || best >= 0xffffffffull) ? 0xffffffffu : (uint32_t)best;
+    d->cell[b * kDltQ + j] = (m == 0 || best == kInf64) ? (uint16_t)0xffff : (uint16_t)(best >> csh);
 }
 
 // work = front[0, front_n) ++ surv[0, min(surv, cap)); m_in = its size.
@@ -1094,6 +1120,7 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
     uint64_t cap;
     uint32_t* gfeas;  // [SW_MAX_QUERIES] per request: a feasible record was seen (or null)
     uint32_t prefetch;  // iterations per consumer group kept in flight as L2 bulk prefetches
+    uint32_t debug;     // count DLT passes (SW_DEBUG)
 };
 
 // objective keys only (ties keep the earlier = lower index within a thread's scan)
@@ -1274,8 +1301,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         }
     }
     __syncthreads();
-    DltHot dh{0, 0, 0, 0};
-    if (PARETO) dh = DltHot{d.kbase, d.qmin, d.qmax, d.qshift};
+    DltHot dh{0, 0, 0, 0, 0};
+    if (PARETO) dh = DltHot{d.kbase, d.qmin, d.qmax, d.qshift, d.cshift};
     const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
     const uint64_t total = v.ntiles * per_tile;
     // stage sg of this view/pass -> flat slot of its first record (kInf64: none)
@@ -1466,6 +1493,10 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 for (int u = 0; u < kRPT; u++)
                     keepm |= (uint32_t)(valid[u] & !dlt_dominated(d, dh, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u]))) << u;
                 if (!__any_sync(0xffffffffu, keepm != 0)) continue;
+                if (pa.debug) {  // diagnostics: how many records reach the exact test
+                    const uint32_t nk = __reduce_add_sync(0xffffffffu, __popc(keepm));
+                    if (lane == 0) atomicAdd(&pa.ctl->dlt_pass, (unsigned long long)nk);
+                }
 #pragma unroll
                 for (int u = 0; u < kRPT; u++) {
                     PPoint pt;

@@ -902,6 +902,7 @@ static ParetoArgs pareto_args(sw_plan* h) {
     pa.cap = h->surv_cap;
     pa.gfeas = h->d_gfeas;
     pa.prefetch = h->prefetch;
+    pa.debug = h->debug ? 1u : 0u;
     return pa;
 }
 
@@ -1013,6 +1014,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
             ParetoCtl c;
             CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
             CK(h, cudaStreamSynchronize(h->stream));
+            fprintf(stderr, "[sw] dlt passed %llu records so far\n", (unsigned long long)c.dlt_pass);
             fprintf(stderr, "[sw] fold pass %llu: stride pass %u, %llu records, survivors %llu merge-in %u local %u/%u front %llu"
                             " | merge phases us: init %.1f local %.1f mark %.1f compact %.1f rank(b0) %.1f\n",
                     (unsigned long long)h->fold_passes, pass, (unsigned long long)recs,

@@ -208,11 +208,12 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2
 // (K = 0: runtime k).
 template <int NP, int K>
 __device__ __forceinline__ void run_block(State<NP>& st, const DevHeader& h, uint32_t p, uint32_t k, uint32_t f0,
-                                          uint32_t f1, const VaEntry* vb, uint32_t r) {
+                                          uint32_t f1, const VaEntry* vb, uint32_t r, uint64_t* ready = nullptr) {
     for (uint32_t s = f0; s < f1; s++) {
         const VaEntry v = vb[(s - f0) * r];
         const uint64_t e = scene_step<NP, K>(st, p, k, h.a[s], v.t_us);
         scene_metrics(st, s, e, h.P[s], v.q);
+        if (ready) ready[s] = e;
     }
 }
 
@@ -361,11 +362,15 @@ __device__ void detail_one(const DevHeader* __restrict__ g_hdr, const VaEntry* _
         const uint32_t c = dig[b];
         out->digit[b] = c;
         const uint32_t ch = h.choice[h.coff[b] + c];
-        for (uint32_t s = h.first[b]; s < h.first[b + 1]; s++) {
-            const VaEntry v = g_va[h.voff[b] + (s - h.first[b]) * h.radix[b] + c];
-            const uint64_t e = scene_step<NP, 0>(st, ch_pool(ch), ch_k(ch), h.a[s], v.t_us);
-            scene_metrics(st, s, e, h.P[s], v.q);
-            out->ready[s] = e;
+        const uint32_t k = ch_k(ch), p = ch_pool(ch);
+        const VaEntry* vb = g_va + h.voff[b] + c;
+        const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
+        switch (k) {  // compile-time gang updates (a single thread: no divergence cost)
+            case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r, out->ready); break;
+            case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r, out->ready); break;
+            case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r, out->ready); break;
+            case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r, out->ready); break;
+            default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r, out->ready); break;
         }
     }
     uint64_t mk = st.R0;
@@ -1177,6 +1182,8 @@ constexpr int kPrefetch = 0;      // iterations per consumer group prefetched in
                                   // measured: 0-4 equal, 6+ over-run L2 and re-read DRAM)
 constexpr int kStages = 6;        // plain scans (192 KB ring)
 constexpr int kStagesPareto = 4;  // scans carrying the DLT + front subset in smem (128 KB)
+// (measured alternatives, C2 big pass: 24 KB stages x 6 with 64 q-bins 3.17 ms, 16 KB x 8
+// 3.68 ms, this 32 KB x 4 2.6 ms -- per-stage overhead outweighs deeper rings)
 static_assert(kStages % kGroups == 0 && kStagesPareto % kGroups == 0, "groups own fixed ring slots");
 __host__ __device__ constexpr size_t ring_bytes(bool pareto) {
     return (size_t)(pareto ? kStagesPareto : kStages) * kStageRecs * sizeof(Rec4);

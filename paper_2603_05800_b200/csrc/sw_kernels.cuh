@@ -33,11 +33,12 @@ struct SegView {
     uint64_t row;
     uint64_t ib, ie;
     // Strided fold passes (scan kernels only): the view is cut into units of `upt`
-    // tiles (a whole number of scan stages); pass 1 scans units u % 64 == 0, pass 2
-    // u % 8 == 0 && u % 64 != 0, pass 3 u % 8 != 0 (pass 4 = passes 2 and 3 at once) -- each
-    // a uniform sample of the whole segment, so the Pareto filter sees every region early.
-    // pass 0: the whole view in order.
-    uint32_t pass, upt;
+    // tiles (a whole number of scan stages).  With K levels, pass 1 scans the units
+    // u % 8^K == 0, pass l+1 (l = 1..K) the units that are multiples of 8^(K-l) but not of
+    // 8^(K-l+1) -- each pass a uniform sample of the whole segment, 8x the previous one,
+    // so the Pareto filter sees every region early and each pass's survivors stay
+    // bounded.  pass 0: the whole view in order.
+    uint32_t pass, upt, levels, pad_;
 };
 constexpr int kScanThreads = 256;
 constexpr int kDltT = 255;  // dominance lookup table: ttff_eff bins (front quantiles; <= 255: u8 map)
@@ -1316,22 +1317,18 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     const uint64_t unit_recs = (uint64_t)v.upt * per_tile;
     const uint64_t spu = v.pass ? unit_recs / kStageRecs : 1;
     const uint64_t nunits = v.pass ? (total + unit_recs - 1) / unit_recs : 0;
-    const uint64_t k8 = (nunits + 7) / 8, k64 = (nunits + 63) / 64;
-    const uint64_t nstages = v.pass == 0 ? (total + kStageRecs - 1) / kStageRecs
-                                         : spu * (v.pass == 1   ? k64
-                                                  : v.pass == 2 ? k8 - k64
-                                                  : v.pass == 3 ? nunits - k8
-                                                                : nunits - k64);
+    // level of this pass: 0 = multiples of 8^K; l >= 1 = multiples of 8^(K-l), not of 8^(K-l+1)
+    const uint32_t lvl = v.pass ? v.pass - 1 : 0;
+    const uint32_t sh = v.pass ? 3 * (v.levels - lvl) : 0;  // log2 of the unit stride
+    const uint64_t c_here = v.pass ? (nunits + (1ull << sh) - 1) >> sh : 0;
+    const uint64_t c_up = (v.pass && lvl > 0) ? (nunits + (1ull << (sh + 3)) - 1) >> (sh + 3) : 0;
+    const uint64_t nstages = v.pass == 0 ? (total + kStageRecs - 1) / kStageRecs : spu * (c_here - c_up);
     auto stage_pos = [&](uint64_t sg) -> uint64_t {
         if (v.pass == 0) return sg * kStageRecs;
         // stage counts stay far below 2^32 (2^32 stages = 1.4e14 records): 32-bit divides
         const uint32_t j = (uint32_t)sg / (uint32_t)spu, part = (uint32_t)sg - j * (uint32_t)spu;
-        const uint64_t m = (uint64_t)(j / 7) * 8 + (j % 7) + 1;  // j-th positive non-multiple of 8
-        const uint64_t u = v.pass == 1   ? 64 * (uint64_t)j
-                           : v.pass == 2 ? 8 * m
-                           : v.pass == 3 ? m
-                                         : (uint64_t)(j / 63) * 64 + (j % 63) + 1;  // pass 4: not multiples of 64
-        const uint64_t pos = u * unit_recs + part * kStageRecs;
+        const uint64_t m = lvl == 0 ? (uint64_t)j : (uint64_t)(j / 7) * 8 + (j % 7) + 1;  // j-th non-multiple of 8
+        const uint64_t pos = (m << sh) * unit_recs + part * kStageRecs;
         return pos < total ? pos : kInf64;
     };
     // one running best per query under the query's total order (feasible first)

@@ -84,7 +84,6 @@ struct sw_plan {
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint32_t prefetch = kPrefetch;  // SW_PREFETCH: scan L2 prefetch distance (iterations per group)
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
-    uint32_t passes = 3;            // SW_PASSES: strided fold passes per segment (2 or 3)
     uint32_t coop_grid = 0;
     bool trace = false;             // SW_TRACE=1: per-phase CUDA-event times of each select on stderr
     std::vector<std::pair<const char*, cudaEvent_t>> tr;  // (phase that ENDS at the event, event)
@@ -213,6 +212,8 @@ static SegView view_of(const sw_plan* h, const Segment& g, uint64_t t_lo, uint64
     v.ie = g.end;
     v.pass = 0;
     v.upt = 1;
+    v.levels = 0;
+    v.pad_ = 0;
     return v;
 }
 static cudaError_t set_scan_smem_attrs();
@@ -521,7 +522,6 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (const char* ev = getenv("SW_PREFETCH")) h->prefetch = (uint32_t)atoi(ev);
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
     if (const char* ev = getenv("SW_COOP_REDUCE")) h->coop_reduce = atoi(ev) != 0;
-    if (const char* ev = getenv("SW_PASSES")) h->passes = atoi(ev) == 2 ? 2u : 3u;
     {  // the cooperative merge needs all its blocks co-resident
         int occ = 0, coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
@@ -958,32 +958,40 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
 static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
     const size_t psmem = kScanSmemPareto;
     // strided passes: units of upt tiles (a whole number of scan stages); pass 1 = every
-    // 64th unit, pass 2 = the other multiples of 8, pass 3 = the rest -- each a uniform
-    // sample of the segment, so the front (and its DLT filter) is close to final after
-    // the first 1/64.  Small segments: one pass over everything.
+    // 8^K-th unit (about kFirstPass records, at most 1/64 of the segment), each further
+    // pass the multiples of the next smaller power of 8 not yet scanned (8x more) -- each a
+    // uniform sample of the segment, so the front (and its DLT filter) is close to final
+    // early and every pass's survivors stay bounded.  Small segments: one pass.
     const uint64_t per_tile = kTileRows * h->row;
     uint32_t upt = 1;
     while ((upt * per_tile) % kStageRecs) upt++;
     const uint64_t unit_recs = upt * per_tile;
     const uint64_t total = g.ntiles * per_tile;
     const uint64_t nunits = (total + unit_recs - 1) / unit_recs;
+    // K levels: the first pass covers about kFirstPass records (>= 1/64 of the segment)
+    const uint64_t kFirstPass = 8ull << 20;
+    uint32_t K = 2;
+    while (K < 10 && (nunits >> (3 * K)) * unit_recs > kFirstPass) K++;
     const bool strided = nunits >= 256;
-    const uint64_t k8 = (nunits + 7) / 8, k64 = (nunits + 63) / 64;
     const uint64_t last_short = nunits * unit_recs - total;  // missing slots of the last unit
-    // pass schedule: 1/64 then 7/64 then 56/64 (SW_PASSES=3, default), or 1/64 then 63/64
-    const uint32_t sched3[] = {1, 2, 3}, sched2[] = {1, 4}, sched1[] = {0};
-    const uint32_t* sched = !strided ? sched1 : h->passes == 2 ? sched2 : sched3;
-    const uint32_t npass = !strided ? 1 : h->passes == 2 ? 2 : 3;
+    const uint32_t npass = strided ? K + 1 : 1;
     for (uint32_t pi = 0; pi < npass; pi++) {
-        const uint32_t pass = sched[pi];
-        uint64_t units = pass == 0 ? nunits : pass == 1 ? k64 : pass == 2 ? k8 - k64 : pass == 3 ? nunits - k8 : nunits - k64;
-        const uint64_t L = nunits - 1;  // does this pass hold the (possibly short) last unit?
-        const bool has_last = pass == 0 || (pass == 1 && L % 64 == 0) || (pass == 2 && L % 8 == 0 && L % 64 != 0) ||
-                              (pass == 3 && L % 8 != 0) || (pass == 4 && L % 64 != 0);
+        const uint32_t pass = strided ? pi + 1 : 0;
+        const uint32_t lvl = pi, sh = 3 * (K - lvl);
+        uint64_t units = nunits;
+        bool has_last = true;
+        if (strided) {
+            const uint64_t c_here = (nunits + (1ull << sh) - 1) >> sh;
+            const uint64_t c_up = lvl ? (nunits + (1ull << (sh + 3)) - 1) >> (sh + 3) : 0;
+            units = c_here - c_up;
+            const uint64_t L = nunits - 1;  // does this pass hold the (possibly short) last unit?
+            has_last = (L % (1ull << sh) == 0) && (lvl == 0 || L % (1ull << (sh + 3)) != 0);
+        }
         const uint64_t recs = units * unit_recs - (has_last ? last_short : 0);
         SegView v = view_of(h, g, 0, g.ntiles);
         v.pass = pass;
         v.upt = upt;
+        v.levels = K;
         dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
@@ -1001,7 +1009,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         launch_scan_nq<true>(nq, grid, psmem, h->stream, v, P, part, pareto_args(h));
         CKL(h);
         if ((ts = end_timed(h, pr)) < 0) return ts;
-        trace_mark(h, pass == 1 ? "scan1" : pass == 2 ? "scan2" : pass == 3 ? "scan3" : pass == 4 ? "scan23" : "scan");
+        trace_mark(h, pass == 1 ? "scan1" : pass == 2 ? "scan2" : pass == 3 ? "scan3" : pass == 4 ? "scan4" : "scan");
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                h->d_ctl);
         CKL(h);

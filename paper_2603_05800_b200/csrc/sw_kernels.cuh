@@ -43,6 +43,7 @@ struct SegView {
 constexpr int kScanThreads = 256;
 constexpr int kDltT = 255;  // dominance lookup table: ttff_eff bins (front quantiles; <= 255: u8 map)
 constexpr int kDltQ = 128;  //                         quality bins (linear, 2^k wide)
+constexpr int kDltCols = kDltQ + 1;  // + the "above every front q" column
 constexpr int kDltMap = 2048;  // t direct map: 128 cells per octave over 16 octaves
 constexpr int kDltTShift = 16; // t cell key = float bits >> 16 (7 mantissa bits)
 
@@ -686,9 +687,12 @@ struct Dlt {
     // cell's largest edge), else lo -- exact also when many front points share one t
     // (e.g. every stall-free plan behind a static intro)
     uint16_t tmap[kDltMap];
-    // min cost >> cshift, rounded down (0xffff = none): a record with cost c is strictly
-    // dominated when (cell + 1) << cshift <= c, i.e. the true minimum is < c
-    uint16_t cell[kDltT * kDltQ];
+    // cell[b1][j] (row b1 = t bin + 1, column j = q bin): min cost >> cshift, rounded down;
+    // 0xffff = none.  Row 0 (no front point has t <= the record's t) and column kDltQ (q
+    // above every front point's) are all "none", so the lookup needs no range checks.  A
+    // record with cost c is strictly dominated when min(c >> cshift, 0xffff) > cell, i.e.
+    // c >= (cell + 1) << cshift > the true minimum.
+    uint16_t cell[(kDltT + 1) * kDltCols];
 };
 static_assert(sizeof(Dlt) % 16 == 0, "Dlt is staged in 16 B vectors");
 
@@ -703,16 +707,17 @@ struct DltHot {
 };
 
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
-    // branch-free: clamp the t cell, shift q, then predicate away the out-of-range cases
+    // branch-free and check-free: the map's cell 0 lies below the front's smallest t (so a
+    // clamped t below it gets row 0), column kDltQ catches q above the front's
     const int32_t k = dlt_tkey(t) - hs.kbase;
     const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
-    const uint32_t j = min((max(q, hs.qmin) - hs.qmin) >> hs.qshift, (uint32_t)kDltQ - 1);
+    const uint32_t j = min((max(q, hs.qmin) - hs.qmin) >> hs.qshift, (uint32_t)kDltQ);
     const uint32_t lh = d.tmap[kc];
     const uint32_t lo = lh & 0xffu, hi = lh >> 8;
-    // t bin + 1 (0: no front point has t <= this t)
-    const uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;
-    const uint32_t cell = d.cell[(max(b1, 1u) - 1) * kDltQ + j];
-    return (k >= 0) & (q <= hs.qmax) & (b1 != 0) & (cell != 0xffffu) & (((uint64_t)cell + 1) << hs.cshift <= c);
+    const uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;  // t bin + 1
+    const uint32_t cell = d.cell[b1 * kDltCols + j];
+    const uint64_t cs = c >> hs.cshift;
+    return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;
 }
 
 // One launch builds the whole DLT: block b (kDltQ threads) computes the t edges it
@@ -750,7 +755,8 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
     if (m)
         while ((((uint64_t)qmax - qmin) >> qsh) >= (uint64_t)kDltQ) qsh++;
     while ((s_cmax >> csh) >= 0xffffull) csh++;  // every front cost fits below the 0xffff "none"
-    const int32_t kbase = m ? dlt_tkey(front[0].t) : 0x7fffffff;
+    // map cell 0 sits just below the front's smallest t: it holds no edge
+    const int32_t kbase = m ? dlt_tkey(front[0].t) - 1 : 0x7fffffff;
     if (b == 0) {
         if (j == 0) {
             d->kbase = kbase;
@@ -802,7 +808,11 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
         }
         more = __syncthreads_or(more);
     }
-    d->cell[b * kDltQ + j] = (m == 0 || best == kInf64) ? (uint16_t)0xffff : (uint16_t)(best >> csh);
+    // row b + 1 holds t bin b; row 0 and column kDltQ are "none"
+    d->cell[(b + 1) * kDltCols + j] = (m == 0 || best == kInf64) ? (uint16_t)0xffff : (uint16_t)(best >> csh);
+    if (j == 0) d->cell[(b + 1) * kDltCols + kDltQ] = 0xffff;
+    if (b == 0)
+        for (uint32_t i = j; i < (uint32_t)kDltCols; i += blockDim.x) d->cell[i] = 0xffff;
 }
 
 // work = front[0, front_n) ++ surv[0, min(surv, cap)); m_in = its size.

@@ -1135,7 +1135,6 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
     PPoint* surv;
     uint64_t cap;
     uint32_t* gfeas;  // [SW_MAX_QUERIES] per request: a feasible record was seen (or null)
-    uint32_t prefetch;  // iterations per consumer group kept in flight as L2 bulk prefetches
     uint32_t debug;     // count DLT passes (SW_DEBUG)
 };
 
@@ -1166,14 +1165,15 @@ __device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_
 }
 
 // TMA-pipelined scan: the segment's records (a flat run of ntiles * 32 * row slots, tile
-// padding included) are dealt to the blocks in 32 KB stages, round-robin.  A block's
-// consumer warps form kGroups groups; each group owns NS / kGroups ring slots and its
-// own stages (stage i of the block goes to group i % kGroups).  One elected thread per
-// group issues the group's cp.async.bulk copies (completion on a "full" mbarrier per
-// slot) and the L2 bulk prefetches kPrefetch stages ahead; after the whole group has
-// moved a stage into registers (a named barrier), it reissues the freed slot at once --
-// no producer warp, no "empty" barriers, no head-of-line blocking between groups.
-// Consumers take kRPT records per thread per stage (independent chains: ILP).
+// padding included) are dealt to the WARPS of the grid in 4 KB stages (128 records),
+// round-robin (warp w of block b takes stages b * kCW + w + i * gridDim.x * kCW).  Every
+// warp owns its own ring slots and full mbarriers: its lane 0 issues the cp.async.bulk
+// of the warp's next stage the moment the warp has moved the current one into registers.
+// No producer warp, no empty barriers, and no coupling between warps -- a warp that
+// spends longer on a stage (select candidates, exact Pareto tests) delays only its own
+// stream (measured: group-owned 32 KB stages, refilled after the group's slowest warp,
+// left fast warps spinning on their next stage).  kRPT records per thread per stage
+// (independent chains: ILP).
 //
 // Select (a9) per record and query costs a few integer ops in the common case: the block
 // shares, per query, a threshold in shared memory -- the best quality of any FEASIBLE
@@ -1181,23 +1181,16 @@ __device__ __forceinline__ bool closest_strict_better(const QueryDev& q, uint32_
 // quality (resp. an infeasible record once a feasible one exists) is strictly worse than
 // a record this block will report, so it is skipped; the full total-order comparison
 // (cand_better) runs only for the rare records that pass.
-constexpr int kCW = 16;                         // consumer warps per block (no producer warp:
-                                                // 4 per SMSP, up to 128 registers)
+constexpr int kCW = 16;                         // warps per block (4 per SMSP, up to 128 registers)
 constexpr int kScanBlock = kCW * 32;
-constexpr int kGroups = 2;                      // consumer groups take alternate stages
-constexpr int kGW = kCW / kGroups;              // warps per group
-constexpr int kRPT = 4;                         // records per consumer thread per stage
-constexpr uint32_t kStageRecs = kGW * 32 * kRPT;  // records per stage (32 KB)
-// Little's law: ~45 GB/s per SM x ~1.5-2 us loaded latency => ~100 KB in flight per SM
-constexpr int kPrefetch = 0;      // iterations per consumer group prefetched into L2 ahead (0: off;
-                                  // measured: 0-4 equal, 6+ over-run L2 and re-read DRAM)
-constexpr int kStages = 6;        // plain scans (192 KB ring)
-constexpr int kStagesPareto = 4;  // scans carrying the DLT + front subset in smem (128 KB)
-// (measured alternatives, C2 big pass: 24 KB stages x 6 with 64 q-bins 3.17 ms, 16 KB x 8
-// 3.68 ms, this 32 KB x 4 2.6 ms -- per-stage overhead outweighs deeper rings)
-static_assert(kStages % kGroups == 0 && kStagesPareto % kGroups == 0, "groups own fixed ring slots");
+constexpr int kRPT = 4;                         // records per thread per stage
+constexpr uint32_t kStageRecs = 32 * kRPT;      // one warp's stage: 128 records (4 KB)
+constexpr uint32_t kUnitAlign = 1024;           // strided fold units: multiples of this many records
+constexpr int kWarpSlots = 3;        // plain scans: 16 warps x 3 x 4 KB = 192 KB ring
+constexpr int kWarpSlotsPareto = 2;  // scans carrying the DLT + front subset in smem: 128 KB
+static_assert(kUnitAlign % kStageRecs == 0, "units are whole stages");
 __host__ __device__ constexpr size_t ring_bytes(bool pareto) {
-    return (size_t)(pareto ? kStagesPareto : kStages) * kStageRecs * sizeof(Rec4);
+    return (size_t)kCW * (pareto ? kWarpSlotsPareto : kWarpSlots) * kStageRecs * sizeof(Rec4);
 }
 
 struct __align__(16) StageMeta {
@@ -1269,10 +1262,10 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                                  (P.q[q].budget != kInf64 ? 4u : 0u);
     extern __shared__ __align__(128) unsigned char fsm[];
     __shared__ Cand s_tmp[32];
-    constexpr int NS = PARETO ? kStagesPareto : kStages;
+    constexpr int WS = PARETO ? kWarpSlotsPareto : kWarpSlots;  // ring slots per warp
+    constexpr int NS = kCW * WS;
     __shared__ __align__(8) uint64_t full_bar[NS];
     __shared__ StageMeta meta[NS];
-    __shared__ uint32_t s_rel[NS];  // warps of the owning group done with the slot's stage
     // per query: packed key (Q << 32 | ~min(cost, 2^32-1)) of this block's best FEASIBLE
     // record under QUALITY_FIRST (any nonzero value under COST_X_TTFF); 0 = none yet
     __shared__ unsigned long long s_thr[NQA];
@@ -1286,10 +1279,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     __shared__ uint32_t s_bcnt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int st = 0; st < NS; st++) {
-            mbar_init(&full_bar[st], 1);
-            s_rel[st] = 0;
-        }
+        for (int st = 0; st < NS; st++) mbar_init(&full_bar[st], 1);
     }
     if (threadIdx.x < NQA) {
         s_thr[threadIdx.x] = 0;
@@ -1352,25 +1342,14 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         bf[q] = false;
     }
 
-    // ---------------- the group's pipeline: slots grp*SPG .. grp*SPG+SPG-1
-    constexpr int SPG = NS / kGroups;  // slots per group
-    const uint32_t grp = (uint32_t)warp / kGW;
-    const uint32_t gtid = threadIdx.x - grp * (kGW * 32);
-    // Iteration k of group g consumes block-local stage i = g + k * kGroups (global stage
-    // sg = blockIdx.x + i * gridDim.x) from slot g*SPG + k % SPG.  The warp that finishes
-    // moving a slot into registers LAST refills it with iteration k + SPG (a per-slot
-    // arrival counter, no barrier): no producer warp, no head-of-line blocking.
-    auto issue = [&](uint32_t slot, uint64_t kk) {  // one thread: fill slot for iteration kk
-        const uint64_t i = grp + kk * kGroups;
-        // keep the group's stream warm in L2 kPrefetch iterations ahead
-        const uint64_t ip = i + (uint64_t)pa.prefetch * kGroups;
-        if (ip * gridDim.x + blockIdx.x < nstages) {
-            const uint64_t pp = stage_pos(ip * gridDim.x + blockIdx.x);
-            if (pp != kInf64)
-                tma_prefetch_l2(v.recs + pp, (uint32_t)umin64(kStageRecs, total - pp) * (uint32_t)sizeof(Rec4));
-        }
-        const uint64_t sg = i * gridDim.x + blockIdx.x;
-        if (sg >= nstages) {  // end of this group's stream
+    // ---------------- this warp's pipeline: slots warp*WS .. warp*WS+WS-1
+    // Iteration k of the warp consumes global stage sg = gw + k * (gridDim.x * kCW) from
+    // slot warp*WS + k % WS; lane 0 refills the slot with iteration k + WS as soon as the
+    // warp holds the stage in registers.
+    const uint64_t gw = (uint64_t)blockIdx.x * kCW + warp, nw = (uint64_t)gridDim.x * kCW;
+    auto issue = [&](uint32_t slot, uint64_t kk) {  // lane 0: fill slot for iteration kk
+        const uint64_t sg = gw + kk * nw;
+        if (sg >= nstages) {  // end of this warp's stream
             meta[slot].pos0 = 0;
             meta[slot].cnt = 0;
             mbar_arrive(&full_bar[slot]);
@@ -1397,37 +1376,25 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         if (gf_bytes) tma_bulk_g2s(meta[slot].gf, pa.gfeas, gf_bytes, &full_bar[slot]);
         tma_bulk_g2s(ring + (size_t)slot * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4), &full_bar[slot]);
     };
-    if (gtid == 0) {
-        for (uint32_t pf = 0; pf < pa.prefetch; pf++) {  // prime the L2 prefetch window
-            const uint64_t ip = grp + (uint64_t)pf * kGroups;
-            if (ip * gridDim.x + blockIdx.x < nstages) {
-                const uint64_t pp = stage_pos(ip * gridDim.x + blockIdx.x);
-                if (pp != kInf64)
-                    tma_prefetch_l2(v.recs + pp, (uint32_t)umin64(kStageRecs, total - pp) * (uint32_t)sizeof(Rec4));
-            }
-        }
-        for (int j = 0; j < SPG; j++) issue(grp * SPG + j, (uint64_t)j);
-    }
+    if (lane == 0)
+        for (int j = 0; j < WS; j++) issue(warp * WS + j, (uint64_t)j);
     {
-        // ---------------- consume: iteration k uses slot grp*SPG + k % SPG
+        // ---------------- consume
         for (uint32_t k = 0;; k++) {
-            const uint32_t st = grp * SPG + k % SPG;
-            mbar_wait(&full_bar[st], (k / SPG) & 1);
+            const uint32_t st = warp * WS + k % WS;
+            mbar_wait(&full_bar[st], (k / WS) & 1);
             const StageMeta mt = meta[st];
-            if (mt.cnt == 0 && mt.pos0 == 0) break;  // end of the group's stream
-            if (mt.cnt == 0) {                        // empty stage: release and go on
+            if (mt.cnt == 0 && mt.pos0 == 0) break;  // end of the warp's stream
+            if (mt.cnt == 0) {                        // empty stage: refill and go on
                 __syncwarp();
-                if (lane == 0 && atomicAdd(&s_rel[st], 1u) == kGW - 1) {
-                    s_rel[st] = 0;
-                    issue(st, (uint64_t)k + SPG);
-                }
+                if (lane == 0) issue(st, (uint64_t)k + WS);
                 continue;
             }
             Rec4 r[kRPT];
             bool valid[kRPT];
 #pragma unroll
             for (int u = 0; u < kRPT; u++) {
-                const uint32_t o = gtid + u * (kGW * 32);
+                const uint32_t o = lane + u * 32;
                 valid[u] = o < mt.cnt;
                 if (valid[u] && !mt.all_valid) {  // edge stages only
                     const uint64_t i0 = flat_index(v, per_tile, mt.pos0 + o);
@@ -1436,16 +1403,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 // unconditional: a slot past cnt holds stale bytes that valid[] masks out
                 r[u] = ring[(size_t)st * kStageRecs + o];
             }
-            // this warp has the stage in registers; the group's last warp refills the slot
+            // the warp has the stage in registers: lane 0 refills the slot
             __syncwarp();
-            if (lane == 0) {
-                __threadfence_block();
-                if (atomicAdd(&s_rel[st], 1u) == kGW - 1) {
-                    s_rel[st] = 0;
-                    __threadfence_block();
-                    issue(st, (uint64_t)k + SPG);
-                }
-            }
+            if (lane == 0) issue(st, (uint64_t)k + WS);
             const bool obj_q = P.objective == 0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
@@ -1485,7 +1445,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                     for (int u = 0; u < kRPT; u++) {
                         if (!((need >> u) & 1u)) continue;
                         const bool f = feasible(P.q[q], r[u]);
-                        const uint64_t idx = flat_index(v, per_tile, mt.pos0 + gtid + u * (kGW * 32));
+                        const uint64_t idx = flat_index(v, per_tile, mt.pos0 + lane + u * 32);
                         if (cand_better(P.q[q], P.objective, idx, r[u], bi[q], br[q])) {
                             bi[q] = idx;
                             br[q] = r[u];
@@ -1522,7 +1482,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                     bool keep = (keepm >> u) & 1u;
                     unsigned pend = __ballot_sync(0xffffffffu, keep);
                     if (!pend) continue;
-                    if (keep) pt.idx = flat_index(v, per_tile, mt.pos0 + gtid + u * (kGW * 32));
+                    if (keep) pt.idx = flat_index(v, per_tile, mt.pos0 + lane + u * 32);
                     while (pend) {  // exact test of each DLT survivor by the whole warp
                         const int src = __ffs(pend) - 1;
                         pend &= pend - 1;
@@ -1549,7 +1509,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                             if (__any_sync(0xffffffffu, dj)) dom = true;
                         }
                         // ... and against this block's earlier survivors: neighbouring
-                        // records (one stage = 1024 consecutive indices) often dominate
+                        // records (runs of consecutive indices) often dominate
                         // each other, and every survivor costs the merge O(m)
                         const uint32_t bc = min(*(volatile uint32_t*)&s_bcnt, kBlockSurv);
                         for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {

@@ -82,7 +82,6 @@ struct sw_plan {
     bool released = false;       // records dropped since create/reset: the front covers more
     uint64_t merged_epoch = 0, merged_n = 0;  // multi-rank merged front cached in d_gather
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
-    uint32_t prefetch = kPrefetch;  // SW_PREFETCH: scan L2 prefetch distance (iterations per group)
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
     uint32_t coop_grid = 0;
     bool trace = false;             // SW_TRACE=1: per-phase CUDA-event times of each select on stderr
@@ -519,7 +518,6 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (const char* ev = getenv("SW_PARETO_CHUNK")) h->chunk = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
-    if (const char* ev = getenv("SW_PREFETCH")) h->prefetch = (uint32_t)atoi(ev);
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
     if (const char* ev = getenv("SW_COOP_REDUCE")) h->coop_reduce = atoi(ev) != 0;
     {  // the cooperative merge needs all its blocks co-resident
@@ -901,7 +899,6 @@ static ParetoArgs pareto_args(sw_plan* h) {
     pa.surv = h->d_surv;
     pa.cap = h->surv_cap;
     pa.gfeas = h->d_gfeas;
-    pa.prefetch = h->prefetch;
     pa.debug = h->debug ? 1u : 0u;
     return pa;
 }
@@ -964,7 +961,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
     // early and every pass's survivors stay bounded.  Small segments: one pass.
     const uint64_t per_tile = kTileRows * h->row;
     uint32_t upt = 1;
-    while ((upt * per_tile) % kStageRecs) upt++;
+    while ((upt * per_tile) % kUnitAlign) upt++;
     const uint64_t unit_recs = upt * per_tile;
     const uint64_t total = g.ntiles * per_tile;
     const uint64_t nunits = (total + unit_recs - 1) / unit_recs;
@@ -995,7 +992,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / kStageRecs), h->scan_grid);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / (kStageRecs * kCW)), h->scan_grid);
         Cand* part = h->d_partial;
         if (nq) {
             if (*np + grid > h->max_partial) return fail(h, SW_ERANGE, "too many chunks for one select");
@@ -1828,7 +1825,6 @@ extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_se
     CK(h, cudaMemsetAsync(f->d_gfeas, 0, sizeof(uint32_t) * SW_MAX_QUERIES * n, f->stream));
     ParetoArgs pa{};
     pa.gfeas = f->d_gfeas;
-    pa.prefetch = kPrefetch;
     CK(h, cudaEventRecord(f->ev[2], f->stream));
     scan_kernel<1, false><<<dim3(f->gx, n), kScanBlock, kRingBytes, f->stream>>>(SegView{}, SelParams{}, f->d_partial,
                                                                                 pa, f->d_sjobs);

@@ -1323,12 +1323,14 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     const uint64_t c_here = v.pass ? (nunits + (1ull << sh) - 1) >> sh : 0;
     const uint64_t c_up = (v.pass && lvl > 0) ? (nunits + (1ull << (sh + 3)) - 1) >> (sh + 3) : 0;
     const uint64_t nstages = v.pass == 0 ? (total + kStageRecs - 1) / kStageRecs : spu * (c_here - c_up);
-    auto stage_pos = [&](uint64_t sg) -> uint64_t {
-        if (v.pass == 0) return sg * kStageRecs;
-        // stage counts stay far below 2^32 (2^32 stages = 1.4e14 records): 32-bit divides
-        const uint32_t j = (uint32_t)sg / (uint32_t)spu, part = (uint32_t)sg - j * (uint32_t)spu;
+    // stage sg -> flat slot of its first record: with sg = j * spu + part (pass 0: spu = 1),
+    // pos = (m << sh) * unit_recs + part * kStageRecs, m = the j-th unit of this pass
+    // (pass 0: sh = 0 and unit_recs = kStageRecs, so pos = sg * kStageRecs)
+    const uint64_t unit_pos = v.pass ? unit_recs : kStageRecs;
+    const uint32_t spu32 = (uint32_t)spu;
+    auto stage_pos = [&](uint32_t j, uint32_t part) -> uint64_t {
         const uint64_t m = lvl == 0 ? (uint64_t)j : (uint64_t)(j / 7) * 8 + (j % 7) + 1;  // j-th non-multiple of 8
-        const uint64_t pos = (m << sh) * unit_recs + part * kStageRecs;
+        const uint64_t pos = (m << sh) * unit_pos + part * kStageRecs;
         return pos < total ? pos : kInf64;
     };
     // one running best per query under the query's total order (feasible first)
@@ -1346,16 +1348,29 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     // Iteration k of the warp consumes global stage sg = gw + k * (gridDim.x * kCW) from
     // slot warp*WS + k % WS; lane 0 refills the slot with iteration k + WS as soon as the
     // warp holds the stage in registers.
-    const uint64_t gw = (uint64_t)blockIdx.x * kCW + warp, nw = (uint64_t)gridDim.x * kCW;
-    auto issue = [&](uint32_t slot, uint64_t kk) {  // lane 0: fill slot for iteration kk
-        const uint64_t sg = gw + kk * nw;
+    // lane 0 walks the warp's stages in order (one issue per iteration): a cursor sg =
+    // c_j * spu + c_part advanced by nw per issue -- no divisions on the stream
+    const uint32_t gw = blockIdx.x * kCW + warp, nw = gridDim.x * kCW;
+    const uint32_t dj = nw / spu32, dp = nw - dj * spu32;
+    uint64_t c_sg = gw;
+    uint32_t c_j = gw / spu32, c_part = gw - c_j * spu32;
+    auto issue = [&](uint32_t slot) {  // lane 0: fill slot with the warp's next stage
+        const uint64_t sg = c_sg;
+        const uint32_t j = c_j, part = c_part;
+        c_sg += nw;
+        c_j += dj;
+        c_part += dp;
+        if (c_part >= spu32) {
+            c_part -= spu32;
+            c_j++;
+        }
         if (sg >= nstages) {  // end of this warp's stream
             meta[slot].pos0 = 0;
             meta[slot].cnt = 0;
             mbar_arrive(&full_bar[slot]);
             return;
         }
-        const uint64_t pos0 = stage_pos(sg);
+        const uint64_t pos0 = stage_pos(j, part);
         if (pos0 == kInf64) {  // a stage past a partial last unit: nothing to read
             meta[slot].pos0 = kInf64;
             meta[slot].cnt = 0;
@@ -1367,7 +1382,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         const bool edge = pos0 < per_tile || pos0 + cnt > total - per_tile;
         meta[slot].pos0 = pos0;
         meta[slot].cnt = cnt;
-        meta[slot].all_valid = edge ? 0 : 1;
+        meta[slot].all_valid = (edge || cnt != kStageRecs) ? 0 : 1;  // a full stage, no padding
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA write
         // the grid-wide feasibility flags ride on the stage's own transaction: no thread
         // waits on a global load
@@ -1377,7 +1392,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         tma_bulk_g2s(ring + (size_t)slot * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4), &full_bar[slot]);
     };
     if (lane == 0)
-        for (int j = 0; j < WS; j++) issue(warp * WS + j, (uint64_t)j);
+        for (int j = 0; j < WS; j++) issue(warp * WS + j);
     {
         // ---------------- consume
         for (uint32_t k = 0;; k++) {
@@ -1387,25 +1402,33 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
             if (mt.cnt == 0 && mt.pos0 == 0) break;  // end of the warp's stream
             if (mt.cnt == 0) {                        // empty stage: refill and go on
                 __syncwarp();
-                if (lane == 0) issue(st, (uint64_t)k + WS);
+                if (lane == 0) issue(st);
                 continue;
             }
             Rec4 r[kRPT];
             bool valid[kRPT];
+            if (mt.all_valid) {  // a full stage without tile padding (warp-uniform)
 #pragma unroll
-            for (int u = 0; u < kRPT; u++) {
-                const uint32_t o = lane + u * 32;
-                valid[u] = o < mt.cnt;
-                if (valid[u] && !mt.all_valid) {  // edge stages only
-                    const uint64_t i0 = flat_index(v, per_tile, mt.pos0 + o);
-                    valid[u] = i0 >= v.ib && i0 < v.ie;
+                for (int u = 0; u < kRPT; u++) {
+                    valid[u] = true;
+                    r[u] = ring[(size_t)st * kStageRecs + lane + u * 32];
                 }
-                // unconditional: a slot past cnt holds stale bytes that valid[] masks out
-                r[u] = ring[(size_t)st * kStageRecs + o];
+            } else {
+#pragma unroll
+                for (int u = 0; u < kRPT; u++) {
+                    const uint32_t o = lane + u * 32;
+                    valid[u] = o < mt.cnt;
+                    if (valid[u]) {
+                        const uint64_t i0 = flat_index(v, per_tile, mt.pos0 + o);
+                        valid[u] = i0 >= v.ib && i0 < v.ie;
+                    }
+                    // unconditional: a slot past cnt holds stale bytes that valid[] masks out
+                    r[u] = ring[(size_t)st * kStageRecs + o];
+                }
             }
             // the warp has the stage in registers: lane 0 refills the slot
             __syncwarp();
-            if (lane == 0) issue(st, (uint64_t)k + WS);
+            if (lane == 0) issue(st);
             const bool obj_q = P.objective == 0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {

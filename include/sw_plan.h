@@ -220,6 +220,21 @@ sw_status sw_plan_sweep(sw_plan *h, uint64_t begin, uint64_t end, uint64_t chunk
                         uint32_t n_queries, const sw_query *queries, sw_selection *out,
                         uint64_t *digest);
 
+
+/* Fused streaming evaluation of global candidates [begin, end) (
+ * BJ (4)): every candidate is decoded, scored (a1-a6) and handed from
+ * registers straight to the select predicate (a9) and the Pareto DLT filter (a8) inside
+ * one kernel per strided tile pass -- NO records are stored (no record capacity used),
+ * for spaces beyond HBM and the lowest latency.  Winners of the n_queries queries over
+ * [begin, end) (all ranks) go to out[0, n_queries) exactly as sw_plan_select_batch would
+ * report them; the range is folded into the running Pareto front (sw_pareto_get).  The
+ * handle must hold no records (else SW_ESTATE); records cannot be inspected afterwards.
+ * SW_ERANGE if a pass's DLT survivors or a query's reported candidates exceed the
+ * handle's buffers (sw_plan_sweep then gives the same results through records).
+ * Synchronous; collective when nranks > 1.  Returns the worst soft status. */
+sw_status sw_plan_stream(sw_plan *h, uint64_t begin, uint64_t end, uint32_t n_queries,
+                         const sw_query *queries, sw_selection *out);
+
 /* The running 3-D Pareto front over (ttff_eff min, cost min, quality max), exact
  * duplicates keeping the lowest index (R14), sorted by (ttff_eff asc, cost asc,
  * quality desc, index asc).  Two-call idiom: cap = 0 returns *n_out; a short
@@ -338,7 +353,11 @@ sw_status sw_plan_last_eval_ms(sw_plan *h, float *ms);
  * CUDA-event time (ms; events recorded on the handle's stream around each launch) and
  * their ALGORITHMIC bytes (32 B per record written by eval / read by a scan, tile
  * padding included for scans).  Synchronises the last recorded launch. */
-enum { SW_KERNEL_EVAL = 0 /* eval_kernel: a1-a7 */, SW_KERNEL_SCAN = 1 /* scan_kernel: a8+a9 */ };
+enum {
+    SW_KERNEL_EVAL = 0,   /* eval_kernel: a1-a7 */
+    SW_KERNEL_SCAN = 1,   /* scan_kernel: a8+a9 */
+    SW_KERNEL_STREAM = 2  /* stream_kernel: a1-a6 + a8 filter + a9, no records (bytes: 0) */
+};
 sw_status sw_plan_kernel_time(sw_plan *h, uint32_t kind, uint64_t *n_launches, double *total_ms,
                               uint64_t *bytes);
 int32_t sw_abi_version(void);

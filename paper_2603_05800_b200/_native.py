@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libsw_plan.so")
 
 SW_OK, SW_CLOSEST, SW_TRUNCATED, SW_EMPTY = 0, 1, 2, 3
 SW_EINVAL, SW_ERANGE, SW_ENOMEM, SW_ECUDA, SW_ENCCL, SW_ESTATE = -1, -2, -3, -4, -5, -6
-SW_KERNEL_EVAL, SW_KERNEL_SCAN = 0, 1
+SW_KERNEL_EVAL, SW_KERNEL_SCAN, SW_KERNEL_STREAM = 0, 1, 2
 SW_MAX_SCENES, SW_MAX_DIGITS, SW_MAX_CHOICES = 64, 16, 64
 SW_MAX_POOLS, SW_MAX_GPUS_PER_POOL, SW_MAX_QUERIES = 4, 8, 8
 UINT64_MAX = (1 << 64) - 1
@@ -102,6 +102,8 @@ EXPORTS = {
                                          C.POINTER(sw_selection)]),
     "sw_plan_sweep": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
                                   C.POINTER(sw_query), C.POINTER(sw_selection), U64P]),
+    "sw_plan_stream": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                   C.POINTER(sw_query), C.POINTER(sw_selection)]),
     "sw_plan_greedy": (C.c_int32, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                    C.POINTER(sw_selection), C.POINTER(C.c_uint32), U64P]),
     "sw_pareto_get": (C.c_int32, [C.c_void_p, C.POINTER(sw_pareto_point), C.c_uint64, U64P]),
@@ -380,6 +382,15 @@ class Plan:
                                      C.byref(d) if digest else None))
         return [_sel(o, self.n_pools, self.B) for o in out[: len(qs)]], (d.value if digest else None)
 
+    def stream(self, begin: int, end: int, queries: Sequence = ()):
+        """Fused streaming evaluation without records (sw_plan_stream) -> selections."""
+        qs = [q if isinstance(q, tuple) else (q.slo_startup_us, q.slo_stall_us, q.budget_mc)
+              for q in queries]
+        arr = (sw_query * max(1, len(qs)))(*[sw_query(*q) for q in qs])
+        out = (sw_selection * max(1, len(qs)))()
+        self._ck(lib().sw_plan_stream(self.h, begin, end, len(qs), arr, out))
+        return [_sel(o, self.n_pools, self.B) for o in out[: len(qs)]]
+
     def greedy(self, query=None, start: Optional[int] = None):
         """Greedy + refinement planner (sw_plan_greedy) -> (Selection, iterations,
         evaluations).  query: object / 3-tuple (None = unconstrained)."""
@@ -435,7 +446,7 @@ class Plan:
 
     def kernel_time(self, kind: int):
         """(launches, summed CUDA-event ms, algorithmic bytes) of one kernel kind since
-        create: SW_KERNEL_EVAL or SW_KERNEL_SCAN (sw_plan_kernel_time)."""
+        create: SW_KERNEL_EVAL, SW_KERNEL_SCAN or SW_KERNEL_STREAM (sw_plan_kernel_time)."""
         n, ms, by = C.c_uint64(), C.c_double(), C.c_uint64()
         self._ck(lib().sw_plan_kernel_time(self.h, kind, C.byref(n), C.byref(ms), C.byref(by)))
         return n.value, ms.value, by.value

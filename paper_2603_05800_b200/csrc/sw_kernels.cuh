@@ -148,9 +148,8 @@ __device__ __forceinline__ uint64_t fk_dyn(const State<NP>& st, uint32_t p, uint
     }
 }
 
-template <int NP, bool BUSY>
-__device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2, Rec4* __restrict__ lane_out,
-                                         bool live) {
+template <int NP, bool BUSY, class Put>
+__device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2, Put&& put) {
     const uint32_t bl = h.B - 1;
     const uint32_t s = h.first[bl];  // s >= 1 on this path
     const uint64_t as = h.a[s];
@@ -201,7 +200,7 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2
             r.w1 = (uint64_t)M - R0;
             r.w2 = cost;
             r.w3 = (w3g + E.q) + (nm ? (1ull << 32) : 0ull);
-            if (live) st_global_256(lane_out + (size_t)E.dl * kTileRows, r);
+            put(E.dl, r);  // a7 store, or the fused select + Pareto filter (stream)
         }
     }
 }
@@ -233,6 +232,102 @@ struct EvalJob {
     uint64_t va_bytes;
     uint64_t tile_begin, tile_end;
     Rec4* out;
+};
+
+// One tile (32 consecutive rows, lane <-> row H = t * 32 + lane) of candidates: record
+// (dm, dl) of the lane's row goes to emit.at(dm, live)(dl, r) -- the 32 B store of the
+// eval kernel, or the fused select + Pareto filter of the stream kernel.
+template <int NP, class Emit>
+__device__ __forceinline__ void eval_tile(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit) {
+    const uint32_t bm = h.B - 2, bl = h.B - 1;
+    const uint32_t rm = h.radix[bm], rl = h.radix[bl];
+    const uint32_t mfirst = h.first[bm], mlast = h.first[bm + 1];
+    const uint32_t lfirst = h.first[bl], llast = h.first[bl + 1];
+    const uint64_t n_rows = h.n_rows;
+    const bool busy_bill = h.flags & 2u;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t Hraw = t * kTileRows + lane;
+    const bool live = Hraw < n_rows;  // the last tile may run past the space
+    const uint64_t H = live ? Hraw : n_rows - 1;
+    State<NP> st;
+    state_init(st, h);
+    // ---- HI prefix: decode the row index (MSD = earliest block, R19) and simulate
+    uint64_t rem = H;
+    for (uint32_t b = 0; b < bm; b++) {
+        const uint64_t pl = h.place[b];
+        uint32_t c;
+        if ((rem >> 32) == 0 && (pl >> 32) == 0) c = (uint32_t)rem / (uint32_t)pl;
+        else c = (uint32_t)(rem / pl);
+        rem -= (uint64_t)c * pl;
+        const uint32_t ch = h.choice[h.coff[b] + c];
+        const uint32_t k = ch_k(ch), p = ch_pool(ch);
+        const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
+        const VaEntry* vb = va + h.voff[b] + c;
+        // lanes are 32 consecutive rows: the high digits usually agree across the
+        // warp -- then (k, p) is warp-uniform and the compile-time gang update runs;
+        // otherwise the runtime-k update (a divergent switch over the compile-time
+        // variants measured 12% slower overall on C2)
+        if (__all_sync(0xffffffffu, ch == __shfl_sync(0xffffffffu, ch, 0))) {
+            switch (k) {
+                case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
+                case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
+                case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
+                case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
+                default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
+            }
+        } else {
+            run_block<NP, 0>(st, h, p, k, f0, f1, vb, r);
+        }
+    }
+    // ---- MID digit: warp-uniform choice
+    for (uint32_t dm = 0; dm < rm; dm++) {
+        State<NP> s2 = st;
+        {
+            const uint32_t ch = h.choice[h.coff[bm] + dm];
+            const uint32_t k = ch_k(ch), p = ch_pool(ch);
+            const VaEntry* vb = va + h.voff[bm] + dm;
+            for (uint32_t s = mfirst; s < mlast; s++) {
+                const VaEntry v = vb[(s - mfirst) * rm];
+                const uint64_t e = scene_step_uniform<NP>(s2, p, k, h.a[s], v.t_us);
+                scene_metrics(s2, s, e, h.P[s], v.q);
+            }
+        }
+        auto put = emit.at(dm, live);  // put(dl, r): record (dm, dl) of this lane's row
+        if (llast - lfirst == 1 && lfirst != 0) {
+            if (busy_bill) lsd_fast<NP, true>(h, s2, put);
+            else lsd_fast<NP, false>(h, s2, put);
+        } else {
+            // ---- generic LSD block (several scenes share the last digit)
+            for (uint32_t dl = 0; dl < rl; dl++) {
+                State<NP> s3 = s2;
+                const uint32_t ch = h.choice[h.coff[bl] + dl];
+                const uint32_t k = ch_k(ch), p = ch_pool(ch);
+                const VaEntry* vb = va + h.voff[bl] + dl;
+                for (uint32_t s = lfirst; s < llast; s++) {
+                    const VaEntry v = vb[(s - lfirst) * rl];
+                    const uint64_t e = scene_step_uniform<NP>(s3, p, k, h.a[s], v.t_us);
+                    scene_metrics(s3, s, e, h.P[s], v.q);
+                }
+                Rec4 r;
+                r.w0 = s3.R0;
+                r.w1 = (uint64_t)s3.M - s3.R0;
+                r.w2 = state_cost(s3, h);
+                r.w3 = (uint64_t)s3.Q | ((uint64_t)s3.cnt << 32) | ((uint64_t)s3.used << 48);
+                put(dl, r);
+            }
+        }
+    }
+}
+
+// a7: the 32 B store of one record (the eval kernel's sink for lsd_fast)
+struct StoreEmit {
+    struct Put {
+        Rec4* lane_out;
+        bool live;
+        __device__ __forceinline__ void operator()(uint32_t dl, const Rec4& r) const {
+            if (live) st_global_256(lane_out + (size_t)dl * kTileRows, r);
+        }
+    };
 };
 
 // jobs == nullptr: one request (job); else request blockIdx.y of a fleet (jobs[y]), each
@@ -312,8 +407,9 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(EvalJob job, const E
             // a warp store covers 32 consecutive 32 B records (1 KB, fully coalesced)
             Rec4* lane_out = tile_out + (size_t)dm * rl * kTileRows;
             if (llast - lfirst == 1 && lfirst != 0) {
-                if (busy_bill) lsd_fast<NP, true>(h, s2, lane_out, live);
-                else lsd_fast<NP, false>(h, s2, lane_out, live);
+                const StoreEmit::Put put{lane_out, live};
+                if (busy_bill) lsd_fast<NP, true>(h, s2, put);
+                else lsd_fast<NP, false>(h, s2, put);
             } else {
                 // ---- generic LSD block (several scenes share the last digit)
                 for (uint32_t dl = 0; dl < rl; dl++) {
@@ -1631,6 +1727,332 @@ __global__ void detail_fleet_kernel(const EvalJob* __restrict__ jobs, const Cand
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
         const Cand c = win[(uint64_t)b * SW_MAX_QUERIES + q];
         if (c.idx != kInf64) detail_one<NP>(jobs[b].hdr, jobs[b].va, c.idx, out + (uint64_t)b * nq + q);
+    }
+}
+
+// ============================================================================ fused stream
+// Evaluation with NO record store: every candidate's record goes straight from registers
+// to the a9 select predicate and the a8 Pareto filter (one kernel per strided tile pass).
+//  - a9: per query a pruning key, higher = better, of the candidates already reported --
+//    QUALITY_FIRST: the packed (Q, ~min(cost, 2^32-1)) key of a feasible one; COST_X_TTFF:
+//    ~sat(cost x ttff_eff); while none is feasible, ~(packed saturated (V_t, V_c)) of a
+//    closest-tier one.  A record whose key is below the best reported key is strictly
+//    worse than a reported candidate and cannot win; the others (rare) are reduced per
+//    warp with the query's total order (cand_better) and the warp's best is appended to
+//    the query's candidate list (stream_select_final_kernel reduces it).  The keys live in
+//    shared memory per block and in global memory across blocks and passes (atomicMax,
+//    read at block start).  Saturation and ties only let more records through (the
+//    filter stays conservative); a full candidate list is reported (cand_n > cap).
+//  - a8: records the DLT does not rule out get the scan's exact warp-cooperative test
+//    against the front (smem subset + L2) and this block's earlier survivors; the rest
+//    are appended to the block's survivor list, flushed to the pass's survivor buffer,
+//    which the usual pipeline merges into the front after the pass.
+struct StreamArgs {
+    const Dlt* dlt;
+    const PPoint* front;  // the running front (sorted by t), ctl->front_n points
+    ParetoCtl* ctl;
+    PPoint* surv;
+    uint64_t surv_cap;
+    Cand* cand;        // [SW_MAX_QUERIES][cand_cap] reported candidates per query
+    uint32_t* cand_n;  // [SW_MAX_QUERIES]
+    uint32_t cand_cap;
+    unsigned long long* gkey;  // [3][SW_MAX_QUERIES]: key, closest key, feasible flag (all 0 = none)
+    // tile hierarchy of the shard's tiles [tile_begin, tile_end): pass lvl of levels K
+    // (lvl 0 = tiles u with u % 8^K == 0; lvl l >= 1 = multiples of 8^(K-l), not of 8^(K-l+1))
+    uint32_t levels, lvl;
+    uint64_t ntiles_pass;  // tiles in this pass
+    uint64_t ib, ie;       // the shard's global candidate range
+    SelParams P;
+};
+
+__device__ __forceinline__ uint64_t sat_mul64(uint64_t a, uint64_t b) {
+    return __umul64hi(a, b) ? ~0ull : a * b;
+}
+// pruning keys (higher = better) of a feasible record and of a closest-tier record
+__device__ __forceinline__ uint64_t prune_key(uint32_t obj, const Rec4& r) {
+    return obj == 0 ? qc_key(r) : ~sat_mul64(r.w2, r.w0 + r.w1);
+}
+__device__ __forceinline__ uint64_t closest_key(const QueryDev& q, const Rec4& r) {
+    const uint64_t vt = sat_sub(r.w0, q.slo_t) + sat_sub(r.w1, q.slo_s), vc = sat_sub(r.w2, q.budget);
+    return ~((umin64(vt, 0xffffffffull) << 32) | umin64(vc, 0xffffffffull));
+}
+
+struct StreamShared {
+    QueryDev q[SW_MAX_QUERIES];
+    unsigned long long key[SW_MAX_QUERIES];   // best pruning key of a reported feasible candidate
+    unsigned long long ckey[SW_MAX_QUERIES];  // best closest-tier key of a reported candidate
+    uint32_t feas[SW_MAX_QUERIES];            // a feasible candidate was reported
+    uint32_t bcnt;                            // block survivor list fill
+    uint32_t m_sm, m_all;                     // front points in smem / in all
+};
+
+struct StreamEmit {
+    const StreamArgs* sa;
+    StreamShared* ss;
+    const Dlt* d;
+    const PPoint* fs;  // front subset in smem
+    PPoint* bsurv;     // block survivor list (smem)
+    DltHot dh;
+    uint64_t rowbase;  // global index of this lane's row's first candidate
+    uint32_t rl;
+    bool edge;         // the row crosses the shard boundary: check each index
+    struct Put {
+        const StreamEmit* e;
+        uint64_t base;  // index of candidate (dm, 0)
+        bool live;
+        __device__ __forceinline__ void operator()(uint32_t dl, const Rec4& r) const {
+            const StreamArgs& a = *e->sa;
+            StreamShared& S = *e->ss;
+            const uint32_t lane = threadIdx.x & 31;
+            const uint64_t idx = base + dl;
+            const bool valid = live && (!e->edge || (idx >= a.ib && idx < a.ie));
+            const uint32_t obj = a.P.objective;
+            // ---- a9: which records can still beat what was reported?
+            for (uint32_t q = 0; q < a.P.nq; q++) {
+                const QueryDev Q = S.q[q];
+                const bool f = valid & (r.w0 <= Q.slo_t) & (r.w1 <= Q.slo_s) & (r.w2 <= Q.budget);
+                bool pass = f & (prune_key(obj, r) >= *(volatile unsigned long long*)&S.key[q]);
+                if (!*(volatile uint32_t*)&S.feas[q])
+                    pass |= valid & !f & (closest_key(Q, r) >= *(volatile unsigned long long*)&S.ckey[q]);
+                if (!__any_sync(0xffffffffu, pass)) continue;
+                uint64_t ci = pass ? idx : kInf64;  // the warp's best passing record
+                Rec4 cr = r;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    uint64_t oi = ci;
+                    Rec4 orr = cr;
+                    shfl_cand(oi, orr, off);
+                    if (lane + off < 32 && cand_better(Q, obj, oi, orr, ci, cr)) {
+                        ci = oi;
+                        cr = orr;
+                    }
+                }
+                if (lane == 0 && ci != kInf64) {
+                    const uint32_t slot = atomicAdd(&a.cand_n[q], 1u);
+                    if (slot < a.cand_cap) {
+                        Cand c;
+                        c.idx = ci;
+                        c.pad = 0;
+                        c.r = cr;
+                        a.cand[(uint64_t)q * a.cand_cap + slot] = c;
+                    }
+                    if (feasible(Q, cr)) {
+                        const unsigned long long k = prune_key(obj, cr);
+                        S.feas[q] = 1u;
+                        atomicMax(&S.key[q], k);
+                        atomicMax(&a.gkey[q], k);
+                        a.gkey[2 * SW_MAX_QUERIES + q] = 1ull;
+                    } else {
+                        const unsigned long long k = closest_key(Q, cr);
+                        atomicMax(&S.ckey[q], k);
+                        atomicMax(&a.gkey[SW_MAX_QUERIES + q], k);
+                    }
+                }
+                __syncwarp();
+            }
+            // ---- a8: DLT filter, then the exact test of its (rare) survivors
+            const bool cand = valid && !dlt_dominated(*e->d, e->dh, r.w0 + r.w1, r.w2, rec_Q(r));
+            unsigned pend = __ballot_sync(0xffffffffu, cand);
+            if (!pend) return;
+            PPoint pt;
+            pt.idx = idx;
+            pt.t = r.w0 + r.w1;
+            pt.c = r.w2;
+            pt.q = rec_Q(r);
+            pt.pad = 0;
+            bool keep = cand;
+            const PPoint* fs = e->fs;
+            const uint32_t m_sm = S.m_sm, m_all = S.m_all;
+            while (pend) {  // each survivor tested by the whole warp
+                const int src = __ffs(pend) - 1;
+                pend &= pend - 1;
+                PPoint x;
+                x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
+                x.t = __shfl_sync(0xffffffffu, pt.t, src);
+                x.c = __shfl_sync(0xffffffffu, pt.c, src);
+                x.q = __shfl_sync(0xffffffffu, pt.q, src);
+                bool dom = false;
+                // front sorted by t: only points with t <= x.t can dominate x
+                for (uint32_t j0 = 0; j0 < m_sm && fs[j0].t <= x.t; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    if (__any_sync(0xffffffffu, j < m_sm && pdom(fs[j], 0, x, 1))) {
+                        dom = true;
+                        break;
+                    }
+                }
+                for (uint32_t j0 = m_sm; !dom && j0 < m_all && a.front[j0].t <= x.t; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    if (__any_sync(0xffffffffu, j < m_all && pdom(a.front[j], 0, x, 1))) dom = true;
+                }
+                const uint32_t bc = min(*(volatile uint32_t*)&S.bcnt, kBlockSurv);
+                for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    if (__any_sync(0xffffffffu, j < bc && pdom(e->bsurv[j], 0, x, 1))) dom = true;
+                }
+                if (lane == src && dom) keep = false;
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+            if (!mask) return;
+            const int ldr = __ffs(mask) - 1;
+            uint32_t b0 = 0;
+            if (lane == ldr) b0 = atomicAdd(&S.bcnt, (uint32_t)__popc(mask));
+            b0 = __shfl_sync(0xffffffffu, b0, ldr);
+            const uint32_t my = b0 + __popc(mask & ((1u << lane) - 1u));
+            const bool local = my < kBlockSurv;
+            if (keep && local) e->bsurv[my] = pt;
+            const unsigned gmask = __ballot_sync(0xffffffffu, keep && !local);  // list full: global
+            if (gmask) {
+                const int gl = __ffs(gmask) - 1;
+                unsigned long long s0 = 0;
+                if (lane == gl) s0 = atomicAdd(&a.ctl->surv, (unsigned long long)__popc(gmask));
+                s0 = __shfl_sync(0xffffffffu, s0, gl);
+                if (keep && !local) {
+                    const uint64_t slot = s0 + __popc(gmask & ((1u << lane) - 1u));
+                    if (slot < a.surv_cap) a.surv[slot] = pt;
+                }
+            }
+        }
+    };
+    __device__ __forceinline__ Put at(uint32_t dm, bool live) const { return Put{this, rowbase + (uint64_t)dm * rl, live}; }
+};
+
+constexpr int kStreamThreads = 512;  // one block per SM: the DLT (~72 KB) is staged once per SM
+
+template <int NP>
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(EvalJob job, const __grid_constant__ StreamArgs sa) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ StreamShared ss;
+    DevHeader& h = *reinterpret_cast<DevHeader*>(smem);
+    VaEntry* va = reinterpret_cast<VaEntry*>(smem + sizeof(DevHeader));
+    Dlt* d = reinterpret_cast<Dlt*>(smem + ((sizeof(DevHeader) + job.va_bytes + 127) & ~(size_t)127));
+    PPoint* fs = reinterpret_cast<PPoint*>(d + 1);
+    PPoint* bsurv = fs + kFrontSmem;
+    const uint32_t m_all = (uint32_t)sa.ctl->front_n, m_sm = min(m_all, kFrontSmem);
+    {  // the DLT (16 B vectors), the front subset, the sentinel survivor list, the queries
+        const uint4* src = reinterpret_cast<const uint4*>(sa.dlt);
+        uint4* dst = reinterpret_cast<uint4*>(d);
+        for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
+        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = sa.front[i];
+        for (uint32_t i = threadIdx.x; i < kBlockSurv; i += blockDim.x) {
+            PPoint sent;  // a reserved-but-unwritten slot dominates nothing
+            sent.idx = kInf64;
+            sent.t = kInf64;
+            sent.c = kInf64;
+            sent.q = 0;
+            sent.pad = 0;
+            bsurv[i] = sent;
+        }
+    }
+    if (threadIdx.x < SW_MAX_QUERIES) {
+        ss.q[threadIdx.x] = sa.P.q[threadIdx.x];
+        ss.key[threadIdx.x] = sa.gkey[threadIdx.x];
+        ss.ckey[threadIdx.x] = sa.gkey[SW_MAX_QUERIES + threadIdx.x];
+        ss.feas[threadIdx.x] = sa.gkey[2 * SW_MAX_QUERIES + threadIdx.x] ? 1u : 0u;
+    }
+    if (threadIdx.x == 0) {
+        ss.bcnt = 0;
+        ss.m_sm = m_sm;
+        ss.m_all = m_all;
+    }
+    stage_tables(job.hdr, job.va, &h, va, (uint32_t)job.va_bytes, &bar);  // ends with a barrier
+    const DltHot dh{d->kbase, d->qmin, d->qmax, d->qshift, d->cshift};
+    const uint64_t row = h.row;
+    const uint32_t rl = h.radix[h.B - 1];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t sh = 3 * (sa.levels - sa.lvl);
+    for (uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < sa.ntiles_pass; j += nwarps) {
+        const uint64_t u = sa.lvl == 0 ? j << sh : ((j / 7) * 8 + (j % 7) + 1) << sh;  // tile of the pass
+        const uint64_t t = job.tile_begin + u;
+        if (t >= job.tile_end) break;  // warp-uniform; tiles grow with j
+        if (lane < sa.P.nq) {  // other blocks' reported keys (global, monotone) tighten ours
+            const unsigned long long* g = sa.gkey;
+            atomicMax(&ss.key[lane], *(volatile const unsigned long long*)&g[lane]);
+            atomicMax(&ss.ckey[lane], *(volatile const unsigned long long*)&g[SW_MAX_QUERIES + lane]);
+            if (*(volatile const unsigned long long*)&g[2 * SW_MAX_QUERIES + lane]) ss.feas[lane] = 1u;
+        }
+        __syncwarp();
+        const uint64_t H = t * kTileRows + lane;
+        const uint64_t rb = H * row;
+        const StreamEmit em{&sa, &ss, d, fs, bsurv, dh, rb, rl, rb < sa.ib || rb + row > sa.ie};
+        eval_tile<NP>(h, va, t, em);
+    }
+    // flush this block's survivor list to the pass's survivor buffer
+    __syncthreads();
+    __shared__ unsigned long long s_base;
+    const uint32_t nb = min(ss.bcnt, kBlockSurv);
+    if (threadIdx.x == 0) s_base = nb ? atomicAdd(&sa.ctl->surv, (unsigned long long)nb) : 0ull;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+        if (s_base + i < sa.surv_cap) sa.surv[s_base + i] = bsurv[i];
+}
+
+// One candidate from scratch (a1-a7 for a single index; plain loads from global/L2).
+template <int NP>
+__device__ __forceinline__ Rec4 eval_one(const DevHeader& h, const VaEntry* __restrict__ va, uint64_t index) {
+    State<NP> st;
+    state_init(st, h);
+    uint32_t dig[kMaxDigits];
+    uint64_t rem = index;
+    for (int b = (int)h.B - 1; b >= 0; b--) {  // a1: i mod r_b, LSD first
+        dig[b] = (uint32_t)(rem % h.radix[b]);
+        rem /= h.radix[b];
+    }
+    for (uint32_t b = 0; b < h.B; b++) {
+        const uint32_t ch = h.choice[h.coff[b] + dig[b]];
+        const uint32_t k = ch_k(ch), p = ch_pool(ch);
+        run_block<NP, 0>(st, h, p, k, h.first[b], h.first[b + 1], va + h.voff[b] + dig[b], h.radix[b]);
+    }
+    Rec4 r;
+    r.w0 = st.R0;
+    r.w1 = (uint64_t)st.M - st.R0;
+    r.w2 = state_cost(st, h);
+    r.w3 = (uint64_t)st.Q | ((uint64_t)st.cnt << 32) | ((uint64_t)st.used << 48);
+    return r;
+}
+
+// Seed of a stream: ns candidates spread evenly over [b, e) -> work[ctl->m_in++] (their
+// exact front, reduced next, gives the first pass a useful DLT).
+template <int NP>
+__global__ void stream_seed_kernel(const DevHeader* __restrict__ hdr, const VaEntry* __restrict__ va, uint64_t b,
+                                   uint64_t e, uint32_t ns, PPoint* __restrict__ work, ParetoCtl* ctl) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ns) return;
+    const uint64_t idx = b + (uint64_t)((unsigned __int128)(e - b) * j / ns);
+    const Rec4 r = eval_one<NP>(*hdr, va, idx);
+    PPoint p;
+    p.idx = idx;
+    p.t = r.w0 + r.w1;
+    p.c = r.w2;
+    p.q = rec_Q(r);
+    p.pad = 0;
+    work[atomicAdd(&ctl->m_in, 1u)] = p;
+}
+
+// Per query q (block q): reduce the reported candidates of stream passes -> out[q] (the
+// closest flag in .pad), like select_final_kernel.
+__global__ void __launch_bounds__(kScanThreads) stream_select_final_kernel(const Cand* __restrict__ cand,
+                                                                           const uint32_t* __restrict__ cand_n,
+                                                                           uint32_t cap, SelParams P,
+                                                                           Cand* __restrict__ out) {
+    __shared__ Cand s_tmp[32];
+    const uint32_t q = blockIdx.x;
+    const uint32_t n = min(cand_n[q], cap);
+    uint64_t idx = kInf64;
+    Rec4 r{};
+    for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const Cand c = cand[(uint64_t)q * cap + j];
+        if (cand_better(P.q[q], P.objective, c.idx, c.r, idx, r)) {
+            idx = c.idx;
+            r = c.r;
+        }
+    }
+    block_reduce_cand(P.q[q], P.objective, idx, r, s_tmp);
+    if (threadIdx.x == 0) {
+        out[q].idx = idx;
+        out[q].r = r;
+        out[q].pad = (idx != kInf64 && !feasible(P.q[q], r)) ? 1ull : 0ull;
     }
 }
 

@@ -111,11 +111,20 @@ struct sw_plan {
     int ev_last = -1;         // pair of the last eval launch
     float last_eval_ms = 0.f;
     bool have_eval_ev = false;
-    uint64_t k_launches[2] = {0, 0};
-    double k_ms[2] = {0.0, 0.0};
-    uint64_t k_bytes[2] = {0, 0};
+    uint64_t k_launches[3] = {0, 0, 0};
+    double k_ms[3] = {0.0, 0.0, 0.0};
+    uint64_t k_bytes[3] = {0, 0, 0};
     uint64_t launches = 0;
     std::string err;
+
+    // fused stream (sw_plan_stream): per-query reported candidates, allocated on first use
+    Cand* d_scand = nullptr;       // [SW_MAX_QUERIES][scand_cap]
+    uint32_t* d_scand_n = nullptr;  // [SW_MAX_QUERIES]
+    unsigned long long* d_skey = nullptr;  // [3][SW_MAX_QUERIES] pruning keys (StreamArgs::gkey)
+    uint64_t* h_pass_surv = nullptr;       // pinned: survivors of each stream pass (<= 21 levels)
+    uint32_t scand_cap = 1u << 18;
+    size_t stream_smem = 0;
+    uint64_t stream_passes = 0;    // diagnostics
 };
 
 namespace {
@@ -600,9 +609,11 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
         void* bufs[] = {h->d_hdr,   h->d_va,      h->d_rec,     h->d_front, h->d_work,
                         h->d_tmp,   h->d_keep,    h->d_ctl,     h->d_dlt,
                         h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest, h->d_selfjob,
-                        h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas, h->d_greedy};
+                        h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas, h->d_greedy,
+                        h->d_scand, h->d_scand_n, h->d_skey};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
+        if (h->h_pass_surv) cudaFreeHost(h->h_pass_surv);
         for (cudaEvent_t e : h->ev)
             if (e) cudaEventDestroy(e);
         if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -796,7 +807,7 @@ extern "C" sw_status sw_plan_last_eval_ms(sw_plan* h, float* ms) {
 extern "C" sw_status sw_plan_kernel_time(sw_plan* h, uint32_t kind, uint64_t* n_launches, double* total_ms,
                                          uint64_t* bytes) {
     if (!h || !n_launches || !total_ms || !bytes) return fail(nullptr, SW_EINVAL, "null argument");
-    if (kind > SW_KERNEL_SCAN) return fail(h, SW_EINVAL, "bad kernel kind %u", kind);
+    if (kind > SW_KERNEL_STREAM) return fail(h, SW_EINVAL, "bad kernel kind %u", kind);
     sw_status st = harvest_eval_events(h);
     if (st < 0) return st;
     *n_launches = h->k_launches[kind];
@@ -1352,6 +1363,259 @@ extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uin
     if (digest) *digest = dsum;
     sw_status worst = SW_OK;
     for (uint32_t q = 0; q < nq; q++) worst = std::max<sw_status>(worst, out[q].status);
+    return worst;
+}
+
+// ============================================================================ fused stream
+// §8(f) row 1: decode + score + select + Pareto filter in one kernel per strided tile
+// pass, no records.  A fresh front is first seeded from 16K candidates spread over the
+// shard (evaluated one per thread); the tile hierarchy then mirrors the fold passes
+// (fold_chunks_async): pass 0 = every 8^K-th tile of the shard (~1/64), each further pass
+// 8x more tiles, each with a DLT from the front so far.
+static sw_status stream_setup(sw_plan* h) {
+    if (h->d_scand) return SW_OK;
+    sw_status st;
+    if ((st = alloc_n(h, &h->d_scand, (uint64_t)SW_MAX_QUERIES * h->scand_cap, "stream candidates")) < 0) return st;
+    if ((st = alloc_n(h, &h->d_scand_n, SW_MAX_QUERIES, "stream candidate counts")) < 0) return st;
+    if ((st = alloc_n(h, &h->d_skey, 3 * SW_MAX_QUERIES, "stream pruning keys")) < 0) return st;
+    CK(h, cudaMallocHost((void**)&h->h_pass_surv, 32 * sizeof(uint64_t)));
+    h->stream_smem = ((sizeof(DevHeader) + h->va_bytes + 127) & ~(size_t)127) + sizeof(Dlt) +
+                     (kFrontSmem + kBlockSurv) * sizeof(PPoint);
+    cudaError_t e = cudaSuccess;
+    launch_np(h, [&](auto np) {
+        constexpr int NPc = decltype(np)::value;
+        int optin = 0, occ = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+        cudaFuncAttributes fa{};
+        e = cudaFuncGetAttributes(&fa, stream_kernel<NPc>);
+        const size_t dyn_max = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+        if (e == cudaSuccess)
+            e = dyn_max < h->stream_smem ? cudaErrorInvalidValue
+                                         : cudaFuncSetAttribute(stream_kernel<NPc>,
+                                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<NPc>, kStreamThreads, h->stream_smem);
+        if (e == cudaSuccess && occ < 1) e = cudaErrorLaunchOutOfResources;
+    });
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, SW_ECUDA, "stream kernel cannot launch (%s)", cudaGetErrorString(e));
+    }
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, uint32_t nq, const sw_query* qs,
+                                    sw_selection* out) {
+    if (!h || (nq && (!qs || !out))) return fail(nullptr, SW_EINVAL, "null argument");
+    if (nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u > %d", nq, SW_MAX_QUERIES);
+    if (begin > end || end > h->N) return fail(h, SW_EINVAL, "range outside [0, N)");
+    if (!h->segs.empty()) return fail(h, SW_ESTATE, "stream needs a handle without records (reset/release)");
+    CK(h, cudaSetDevice(h->device));
+    sw_status st = stream_setup(h);
+    if (st < 0) return st;
+    // front-answerable queries (R30) come from the front when it covers exactly [begin, end)
+    const bool front_ok = h->front_n == 0 && !h->released;
+    uint32_t fi[SW_MAX_QUERIES], si[SW_MAX_QUERIES], nf = 0, ns = 0;
+    for (uint32_t q = 0; q < nq; q++) {
+        if (front_ok && front_query(h, qs[q])) fi[nf++] = q;
+        else si[ns++] = q;
+    }
+    SelParams PS{}, PF{};
+    PS.objective = PF.objective = (h->h.flags & 4u) ? 1u : 0u;
+    PS.nq = ns;
+    PF.nq = nf;
+    for (uint32_t j = 0; j < ns; j++)
+        PS.q[j] = QueryDev{qs[si[j]].slo_startup_us, qs[si[j]].slo_stall_us, qs[si[j]].budget_mc};
+    for (uint32_t j = 0; j < nf; j++)
+        PF.q[j] = QueryDev{qs[fi[j]].slo_startup_us, qs[fi[j]].slo_stall_us, qs[fi[j]].budget_mc};
+    uint64_t b, e;
+    if ((st = sw_shard_range(begin, end, h->row, h->rank, h->nranks, &b, &e)) < 0) return st;
+    trace_mark(h, "start");
+    CK(h, cudaMemsetAsync(h->d_scand_n, 0, sizeof(uint32_t) * SW_MAX_QUERIES, h->stream));
+    CK(h, cudaMemsetAsync(h->d_skey, 0, sizeof(unsigned long long) * 3 * SW_MAX_QUERIES, h->stream));
+    if (e > b) {
+        const uint64_t rb = b / h->row, re = (e + h->row - 1) / h->row;
+        const uint64_t t0 = rb / kTileRows, t1 = (re + kTileRows - 1) / kTileRows, nt = t1 - t0;
+        const uint64_t per_tile = kTileRows * h->row;
+        auto up = [](uint64_t n, uint32_t sh) { return (n + (1ull << sh) - 1) >> sh; };  // ceil(n / 2^sh)
+        // K levels: pass 0 = about 1/64 of the tiles (its DLT comes from the seed), each
+        // further pass 8x more; more levels only while pass 0 alone would exceed the
+        // survivor budget if nothing were filtered
+        uint32_t K = nt >= 4096 ? 2 : nt >= 64 ? 1 : 0;
+        while (K < 20 && up(nt, 3 * K) * per_tile > 64 * (uint64_t)h->surv_cap) K++;
+        if (h->front_n == 0) {  // fresh front: seed it from 16K candidates spread over the shard
+            const uint32_t ns = (uint32_t)std::min<uint64_t>(e - b, 16384);
+            CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
+            launch_np(h, [&](auto npc) {
+                constexpr int NPc = decltype(npc)::value;
+                stream_seed_kernel<NPc><<<(ns + 127) / 128, 128, 0, h->stream>>>(h->d_hdr, h->d_va, b, e, ns, h->d_work,
+                                                                                h->d_ctl);
+            });
+            CKL(h);
+            if ((st = reduce_async(h, h->d_front)) < 0) return st;
+            trace_mark(h, "seed");
+        }
+        // one pass: DLT from the running front, the fused kernel over the pass's tiles,
+        // survivors merged into the front; the pass's survivor count lands in pinned memory
+        auto run_pass = [&](uint32_t lvl, uint64_t ntp) -> sw_status {
+            dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+            CKL(h);
+            CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
+            StreamArgs sa{};
+            sa.dlt = h->d_dlt;
+            sa.front = h->d_front;
+            sa.gkey = h->d_skey;
+            sa.ctl = h->d_ctl;
+            sa.surv = h->d_surv;
+            sa.surv_cap = h->surv_cap;
+            sa.cand = h->d_scand;
+            sa.cand_n = h->d_scand_n;
+            sa.cand_cap = h->scand_cap;
+            sa.levels = K;
+            sa.lvl = lvl;
+            sa.ntiles_pass = ntp;
+            sa.ib = b;
+            sa.ie = e;
+            sa.P = PS;
+            const uint64_t warps_per_block = kStreamThreads / 32;
+            const uint32_t grid = (uint32_t)std::min<uint64_t>((ntp + warps_per_block - 1) / warps_per_block,
+                                                               (uint64_t)h->num_sms);
+            int pr = 0;
+            sw_status ts = begin_timed(h, SW_KERNEL_STREAM, 0, &pr);
+            if (ts < 0) return ts;
+            launch_np(h, [&](auto npc) {
+                constexpr int NPc = decltype(npc)::value;
+                stream_kernel<NPc><<<grid, kStreamThreads, h->stream_smem, h->stream>>>(
+                    EvalJob{h->d_hdr, h->d_va, h->va_bytes, t0, t1, nullptr}, sa);
+            });
+            CKL(h);
+            if ((ts = end_timed(h, pr)) < 0) return ts;
+            trace_mark(h, "stream");
+            CK(h, cudaMemcpyAsync(&h->h_pass_surv[lvl], &h->d_ctl->surv, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                  h->stream));
+            pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
+                                                                   h->d_ctl);
+            CKL(h);
+            if ((ts = reduce_async(h, h->d_front)) < 0) return ts;
+            trace_mark(h, "merge");
+            h->stream_passes++;
+            h->epoch++;
+            if (h->debug) {
+                ParetoCtl c;
+                uint32_t cn[SW_MAX_QUERIES];
+                CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
+                CK(h, cudaMemcpyAsync(cn, h->d_scand_n, sizeof cn, cudaMemcpyDeviceToHost, h->stream));
+                CK(h, cudaStreamSynchronize(h->stream));
+                fprintf(stderr, "[sw] stream pass %u/%u: %llu tiles, survivors %llu front %llu, candidates reported",
+                        lvl, K, (unsigned long long)ntp, (unsigned long long)c.surv, (unsigned long long)c.front_n);
+                for (uint32_t q = 0; q < ns; q++) fprintf(stderr, " %u", cn[q]);
+                fprintf(stderr, "\n");
+            }
+            return SW_OK;
+        };
+        auto ntiles_of = [&](uint32_t lvl) {
+            const uint32_t sh = 3 * (K - lvl);
+            return up(nt, sh) - (lvl ? up(nt, sh + 3) : 0);
+        };
+        for (uint32_t lvl = 0; lvl <= K; lvl++)
+            if (ntiles_of(lvl) && (st = run_pass(lvl, ntiles_of(lvl))) < 0) return st;
+        // a pass whose survivors overflowed dropped some: the merged front is valid (real
+        // candidates) but may miss points.  Re-running that pass against the better front
+        // is exact -- a record already in the front is removed by its identical entry -- and
+        // its survivors shrink with the front; a few rounds at most.
+        for (int round = 0;; round++) {
+            CK(h, cudaStreamSynchronize(h->stream));
+            std::vector<uint32_t> redo;
+            for (uint32_t lvl = 0; lvl <= K; lvl++)
+                if (ntiles_of(lvl) && h->h_pass_surv[lvl] > h->surv_cap) redo.push_back(lvl);
+            if (redo.empty()) break;
+            if (round == 4)
+                return fail(h, SW_ERANGE, "stream pass survivors exceeded %llu after %d re-runs: use sw_plan_sweep",
+                            (unsigned long long)h->surv_cap, round);
+            CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
+            for (uint32_t lvl : redo)
+                if ((st = run_pass(lvl, ntiles_of(lvl))) < 0) return st;
+        }
+    }
+    h->released = true;  // the front now covers candidates without records
+    if (ns) {
+        stream_select_final_kernel<<<ns, kScanThreads, 0, h->stream>>>(h->d_scand, h->d_scand_n, h->scand_cap, PS,
+                                                                      h->d_cand);
+        CKL(h);
+        if (h->nranks > 1) {  // a10: allgather per-rank winners, replicated merge
+            CKN(h, ncclAllGather(h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, ncclUint8, h->comm,
+                                 h->stream));
+            select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_cand_all, (uint32_t)h->nranks, PS, h->d_cand);
+            CKL(h);
+        }
+    }
+    bool merged_now = false;
+    if (nf) {
+        const PPoint* fr = nullptr;
+        const uint64_t* d_n = nullptr;
+        if ((st = global_front_async(h, &fr, &d_n, &merged_now)) < 0) return st;
+        select_front_kernel<<<1, kScanThreads, 0, h->stream>>>(fr, 0, d_n, PF, h->d_cand + ns);
+        CKL(h);
+    }
+    const uint32_t nw = ns + nf;
+    if (nw) {
+        launch_np(h, [&](auto npc) {
+            constexpr int NPc = decltype(npc)::value;
+            detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nw, h->d_detail);
+        });
+        CKL(h);
+    }
+    Cand win[SW_MAX_QUERIES];
+    DetailOut det[SW_MAX_QUERIES];
+    uint32_t cn[SW_MAX_QUERIES];
+    ParetoCtl cc;
+    uint64_t aux[2] = {0, 0};
+    if (nw) {
+        CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nw, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nw, cudaMemcpyDeviceToHost, h->stream));
+    }
+    CK(h, cudaMemcpyAsync(cn, h->d_scand_n, sizeof cn, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(&cc, h->d_ctl, sizeof cc, cudaMemcpyDeviceToHost, h->stream));
+    if (h->nranks > 1 && merged_now)
+        CK(h, cudaMemcpyAsync(aux, h->d_counts + h->nranks + 2, 16, cudaMemcpyDeviceToHost, h->stream));
+    trace_mark(h, "answers");
+    CK(h, cudaStreamSynchronize(h->stream));
+    trace_dump(h, "stream");
+    if (cc.front_overflow) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
+    h->front_n = cc.front_n;
+    if (cc.surv_overflow) {
+        CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
+        return fail(h, SW_ERANGE, "stream pass survivors exceeded %llu: use sw_plan_sweep",
+                    (unsigned long long)h->surv_cap);
+    }
+    for (uint32_t q = 0; q < ns; q++)
+        if (cn[q] > h->scand_cap)
+            return fail(h, SW_ERANGE, "stream select candidates exceeded %u: use sw_plan_sweep", h->scand_cap);
+    if (merged_now && !aux[1]) {
+        h->merged_epoch = h->epoch;
+        h->merged_n = aux[0];
+    }
+    sw_status worst = SW_OK;
+    for (uint32_t j = 0; j < nw; j++) {
+        const uint32_t q = j < ns ? si[j] : fi[j - ns];
+        memset(&out[q], 0, sizeof(sw_selection));
+        if (win[j].idx == kInf64) {
+            out[q].status = SW_EMPTY;
+        } else {
+            detail_to_selection(h, win[j].idx, det[j], &out[q], nullptr);
+            out[q].status = win[j].pad ? SW_CLOSEST : SW_OK;
+        }
+        worst = std::max<sw_status>(worst, out[q].status);
+    }
+    if (merged_now && aux[1] && nf) {  // some rank's front exceeded the merge pad: exact redo
+        sw_query qf[SW_MAX_QUERIES];
+        sw_selection of[SW_MAX_QUERIES];
+        for (uint32_t j = 0; j < nf; j++) qf[j] = qs[fi[j]];
+        if ((st = front_answer(h, nf, qf, of)) < 0) return st;
+        for (uint32_t j = 0; j < nf; j++) out[fi[j]] = of[j];
+        worst = SW_OK;
+        for (uint32_t q = 0; q < nq; q++) worst = std::max<sw_status>(worst, out[q].status);
+    }
     return worst;
 }
 

@@ -207,6 +207,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--stream-steps", type=int, default=5,
+                    help="fused stream mode (SURVEY §8(f) row 1) calls timed after the main line (0: skip)")
     args = ap.parse_args()
 
     from swgen import make_config
@@ -345,6 +347,42 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
 
+    # §8(f) row 1, reported beside (not instead of) the headline: the fused stream mode
+    # evaluates the same space with NO record store (a7 skipped by design), select + Pareto
+    # filter in-kernel; CUDA events on the stream around whole calls, max over ranks
+    stream_line = None
+    if args.stream_steps > 0:
+        with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world,
+                     record_capacity=1024) as p3:
+            for _ in range(2):
+                p3.reset()
+                ss = p3.stream(0, N, pb.queries)
+            barrier()
+            s0 = p3.kernel_time(sw.SW_KERNEL_STREAM)
+            ev0.record(stream)
+            for _ in range(args.stream_steps):
+                p3.reset()
+                ss = p3.stream(0, N, pb.queries)
+            ev1.record(stream)
+            ev1.synchronize()
+            s1 = p3.kernel_time(sw.SW_KERNEL_STREAM)
+            sms = ev0.elapsed_time(ev1) / args.stream_steps
+            if world > 1:
+                t = torch.tensor([sms], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                sms = float(t[0])
+            sparity = None
+            if os.path.exists(gpath):
+                sparity = (all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
+                               for s, w in zip(ss, g["winners"])) and
+                           p3.pareto() == [tuple(p) for p in g["front"]])
+            stream_line = {"value": N / (sms / 1e3), "unit": UNIT, "ms_per_call": sms,
+                           "stream_kernel_ms_per_call": (s1[1] - s0[1]) / args.stream_steps,
+                           "launches_per_call": (s1[0] - s0[0]) / args.stream_steps,
+                           "calls": args.stream_steps, "parity": sparity,
+                           "note": "sw_plan_stream: no records stored (a7 skipped by design; "
+                                   "SURVEY 8(f) row 1), not the headline step"}
+
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -366,6 +404,7 @@ def main():
             "clocks": ck,
             "parity": parity,
             "front_points": len(front),
+            "stream_mode": stream_line,
         }
         emit(line)
     if comm:

@@ -1443,8 +1443,8 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
         // survivor budget if nothing were filtered
         uint32_t K = nt >= 4096 ? 2 : nt >= 64 ? 1 : 0;
         while (K < 20 && up(nt, 3 * K) * per_tile > 64 * (uint64_t)h->surv_cap) K++;
-        if (h->front_n == 0) {  // fresh front: seed it from 16K candidates spread over the shard
-            const uint32_t ns = (uint32_t)std::min<uint64_t>(e - b, 16384);
+        if (h->front_n == 0) {  // fresh front: seed it from 16K (64K) candidates spread over the shard
+            const uint32_t ns = (uint32_t)std::min<uint64_t>(e - b, (e - b) >> 30 ? 65536 : 16384);
             CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
             launch_np(h, [&](auto npc) {
                 constexpr int NPc = decltype(npc)::value;
@@ -1517,24 +1517,23 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
             const uint32_t sh = 3 * (K - lvl);
             return up(nt, sh) - (lvl ? up(nt, sh + 3) : 0);
         };
-        for (uint32_t lvl = 0; lvl <= K; lvl++)
-            if (ntiles_of(lvl) && (st = run_pass(lvl, ntiles_of(lvl))) < 0) return st;
-        // a pass whose survivors overflowed dropped some: the merged front is valid (real
+        // A pass whose survivors overflowed dropped some: the merged front is valid (real
         // candidates) but may miss points.  Re-running that pass against the better front
-        // is exact -- a record already in the front is removed by its identical entry -- and
-        // its survivors shrink with the front; a few rounds at most.
-        for (int round = 0;; round++) {
-            CK(h, cudaStreamSynchronize(h->stream));
-            std::vector<uint32_t> redo;
-            for (uint32_t lvl = 0; lvl <= K; lvl++)
-                if (ntiles_of(lvl) && h->h_pass_surv[lvl] > h->surv_cap) redo.push_back(lvl);
-            if (redo.empty()) break;
-            if (round == 4)
-                return fail(h, SW_ERANGE, "stream pass survivors exceeded %llu after %d re-runs: use sw_plan_sweep",
-                            (unsigned long long)h->surv_cap, round);
-            CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
-            for (uint32_t lvl : redo)
-                if ((st = run_pass(lvl, ntiles_of(lvl))) < 0) return st;
+        // is exact -- a record already in the front is removed by its identical entry --
+        // and its survivors shrink with the front; it is redone at once (one readback per
+        // pass), before the next, larger pass would build on the weaker front.
+        for (uint32_t lvl = 0; lvl <= K; lvl++) {
+            const uint64_t ntp = ntiles_of(lvl);
+            if (ntp == 0) continue;
+            for (int round = 0;; round++) {
+                if ((st = run_pass(lvl, ntp)) < 0) return st;
+                CK(h, cudaStreamSynchronize(h->stream));
+                if (h->h_pass_surv[lvl] <= h->surv_cap) break;
+                if (round == 8)
+                    return fail(h, SW_ERANGE, "stream pass survivors exceeded %llu after %d re-runs: use sw_plan_sweep",
+                                (unsigned long long)h->surv_cap, round);
+                CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
+            }
         }
     }
     h->released = true;  // the front now covers candidates without records

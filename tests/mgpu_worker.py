@@ -1,5 +1,6 @@
 """Multi-GPU parity worker (one rank per GPU, launched by torchrun from
-tests/test_gpu_multirank.py): sharded eval + NCCL allgather merge through the C ABI,
+tests/test_gpu_multirank.py): sharded eval (and the sharded fused stream) + NCCL
+allgather merge through the C ABI,
 compared bit-exactly with the oracle's golden results (tests/golden/, written by
 tools/gen_golden.py from oracle/ only)."""
 import json
@@ -40,8 +41,16 @@ def main():
             assert s.index == w["index"] and tuple(s.rec) == tuple(w["rec"]), (cfg, rank, s, w)
         assert front == [tuple(p) for p in g["front"]], (cfg, rank, len(front), len(g["front"]))
         assert dg == int(g["digest"]), (cfg, rank)
-        print("rank %d/%d %s ok: %d winners, front %d, digest %x" % (rank, world, cfg, len(sels),
-                                                                    len(front), dg), flush=True)
+        # the fused stream path (no records): sharded over the ranks, same winners + front
+        with sw.Plan(pb, device=local, comm=comm, rank=rank, nranks=world, record_capacity=1024) as plan:
+            ss = plan.stream(0, plan.n, pb.queries)
+            sf = plan.pareto()
+        for s, w in zip(ss, g["winners"]):
+            st = {0: 0, 1: 1, -1: 3}[w["status"]]
+            assert s.status == st and s.index == w["index"] and tuple(s.rec) == tuple(w["rec"]), (cfg, rank, s, w)
+        assert sf == [tuple(p) for p in g["front"]], (cfg, rank, "stream front")
+        print("rank %d/%d %s ok: %d winners, front %d, digest %x (stream too)" % (rank, world, cfg, len(sels),
+                                                                                 len(front), dg), flush=True)
     sw.comm_destroy(comm)
     dist.barrier()
     dist.destroy_process_group()

@@ -36,6 +36,8 @@ WORKLOADS = {
           "(BASELINE configs[2])",
     "C5": "C5: 30-minute podcast, 60 scenes, 4 levels x A100/H100/H200, 48^6 = 1.2e10 plans, "
           "chunked when records exceed HBM (BASELINE configs[4])",
+    "C3w": "C3w: C3 with a cold H100 pool ready at 110 s (load 30 s + warm-up 80 s, P:608-611; "
+           "SURVEY 8(f) row 3), 24^6 plans",
 }
 
 

@@ -117,6 +117,11 @@ typedef struct {
                             1 BUSY: sum k x t (GPU-seconds) -- reading R10 */
     uint32_t objective;  /* 0 QUALITY_FIRST: (-Q, cost, ttff_eff, index);
                             1 COST_X_TTFF: (cost x ttff_eff, -Q, index) -- R13 */
+    const uint64_t *pool_ready_us;  /* [n_pools] or NULL: time at which every GPU of pool p
+                            is free -- model load + warm-up, "~30 seconds ... ~80 seconds"
+                            (reading R31); NULL = all 0
+                            (warm pools, R18).  An unused pool is neither billed nor
+                            counted in the makespan. */
 } sw_price_table;
 
 typedef void *(*sw_alloc_fn)(size_t bytes, void *stream, void *ctx);

@@ -30,7 +30,7 @@ class OrProblem(C.Structure):
         ("objective", C.c_uint32), ("n_levels", C.c_uint32), ("level_score", U32P),
         ("B", C.c_uint32), ("radix", U32P), ("first_scene", U32P),
         ("choice_level", U32P), ("choice_k", U32P), ("choice_pool", U32P),
-        ("va_us", U64P),
+        ("va_us", U64P), ("pool_ready_us", U64P),
     ]
 
 
@@ -131,7 +131,8 @@ class Oracle:
             choice_level=a(C.c_uint32, [x[0] for x in ch]),
             choice_k=a(C.c_uint32, [x[1] for x in ch]),
             choice_pool=a(C.c_uint32, [x[2] for x in ch]),
-            va_us=a(C.c_uint64, pb.va_us))
+            va_us=a(C.c_uint64, pb.va_us),
+            pool_ready_us=a(C.c_uint64, pb.pool_ready_us) if getattr(pb, "pool_ready_us", None) else None)
 
     def _k(self, x):
         self._keep.append(x)

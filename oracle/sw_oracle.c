@@ -57,6 +57,8 @@ typedef struct {
     const uint32_t *choice_k;         /* [sum radix] */
     const uint32_t *choice_pool;      /* [sum radix] */
     const uint64_t *va_us;            /* block-major: b, (s - first_b), c */
+    const uint64_t *pool_ready_us;    /* [n_pools] or NULL: pool p's GPUs free from this time
+                                         (model load + warm-up; reading R31) */
 } or_problem;
 
 typedef struct {
@@ -146,7 +148,9 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
     uint64_t busy[OR_MAXP];
     uint32_t used = 0;
     for (uint32_t p = 0; p < pb->n_pools; p++) {
-        for (uint32_t g = 0; g < pb->gpus[p]; g++) F[p][g] = 0; /* warm pools (R18) */
+        /* every GPU of pool p is free once the pool is loaded and warmed up (P:608-611,
+           R31); warm pools (R18) start at 0 */
+        for (uint32_t g = 0; g < pb->gpus[p]; g++) F[p][g] = pb->pool_ready_us ? pb->pool_ready_us[p] : 0;
         busy[p] = 0;
     }
     uint64_t R0 = 0, Q = 0;
@@ -197,8 +201,9 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
     }
     uint64_t cost = pb->fixed_cost_mc, mk = R0;
     for (uint32_t p = 0; p < pb->n_pools; p++) {
-        uint64_t end = 0;
-        for (uint32_t g = 0; g < pb->gpus[p]; g++) if (F[p][g] > end) end = F[p][g];
+        uint64_t end = 0; /* an unused pool is not provisioned: no end, no bill (R31) */
+        if (used & (1u << p))
+            for (uint32_t g = 0; g < pb->gpus[p]; g++) if (F[p][g] > end) end = F[p][g];
         if (pool_end_us) pool_end_us[p] = end;
         if (end > mk) mk = end;
         if (used & (1u << p)) {

@@ -45,7 +45,8 @@ class sw_profile_tables(C.Structure):
 
 class sw_price_table(C.Structure):
     _fields_ = [("n_pools", C.c_uint32), ("gpus", U32P), ("price_mc_per_gpu_hour", U64P),
-                ("fixed_cost_mc", C.c_uint64), ("billing", C.c_uint32), ("objective", C.c_uint32)]
+                ("fixed_cost_mc", C.c_uint64), ("billing", C.c_uint32), ("objective", C.c_uint32),
+                ("pool_ready_us", U64P)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -265,8 +266,10 @@ def _marshal(pb, keep):
     tb = sw_profile_tables(len(pb.radix), _arr(C.c_uint32, pb.radix),
                            _arr(C.c_uint32, pb.first_scene), chs, _arr(C.c_uint64, pb.va_us),
                            len(pb.level_score), _arr(C.c_uint32, pb.level_score), pb.heads)
+    ready = getattr(pb, "pool_ready_us", None)
     pr = sw_price_table(len(pb.gpus), _arr(C.c_uint32, pb.gpus), _arr(C.c_uint64, pb.price_mc),
-                        pb.fixed_cost_mc, pb.billing, pb.objective)
+                        pb.fixed_cost_mc, pb.billing, pb.objective,
+                        _arr(C.c_uint64, ready) if ready else None)
     keep.append((sc, chs, tb, pr))
     return sc, tb, pr
 

@@ -58,6 +58,7 @@ struct __align__(16) DevHeader {
     uint32_t G[kMaxP];
     uint64_t price[kMaxP];
     uint64_t Gprice[kMaxP];       // G_p * price_p (device-computed in pack_kernel)
+    uint64_t ready[kMaxP];        // pool p's GPUs free from this time (load + warm-up, R31)
     // LSD choices grouped by (pool, k) so the inner loop has neither: group g covers
     // lsd_dl[lsd_goff[g] .. lsd_goff[g+1]) with pool/k packed in lsd_pk[g] (p | k << 8)
     uint32_t lsd_ngroups, pad1;
@@ -103,7 +104,7 @@ __device__ __forceinline__ void state_init(State<NP>& st, const DevHeader& h) {
 #pragma unroll
     for (int p = 0; p < NP; p++) {
 #pragma unroll
-        for (int g = 0; g < kMaxG; g++) st.F[p][g] = (uint32_t)g < h.G[p] ? 0ull : kInf64;
+        for (int g = 0; g < kMaxG; g++) st.F[p][g] = (uint32_t)g < h.G[p] ? h.ready[p] : kInf64;
         st.end[p] = 0;
         st.busy[p] = 0;
     }

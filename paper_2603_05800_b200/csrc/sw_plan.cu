@@ -288,6 +288,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
             qsum += (u128)(sc->dur_us[s] / 1000) * max_score;
         }
         u128 tmax = fixed;
+        if (pr->pool_ready_us)  // a start offset delays every later finish (R31)
+            for (uint32_t p = 0; p < pr->n_pools; p++) tmax = std::max<u128>(tmax, fixed + pr->pool_ready_us[p]);
         uint64_t off = 0;
         for (uint32_t b = 0; b < B; b++) {
             const uint32_t r = tb->radix[b];
@@ -427,6 +429,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     for (uint32_t p = 0; p < NP; p++) {
         H.G[p] = pr->gpus[p];
         H.price[p] = pr->price_mc_per_gpu_hour[p];
+        H.ready[p] = pr->pool_ready_us ? pr->pool_ready_us[p] : 0;  // load + warm-up (R31)
     }
     h->n_va = (uint32_t)n_va;
     h->va_bytes = (uint32_t)(n_va * sizeof(VaEntry));
@@ -2217,4 +2220,4 @@ extern "C" const char* sw_last_error(const sw_plan* h) {
 
 extern "C" uint64_t sw_plan_launch_count(const sw_plan* h) { return h ? h->launches : 0; }
 
-extern "C" int32_t sw_abi_version(void) { return 1; }
+extern "C" int32_t sw_abi_version(void) { return 2; }  // 2: sw_price_table.pool_ready_us

@@ -143,6 +143,7 @@ class Problem:
     va_us: List[int]                # block-major: digit b, scene s in block, choice c
     queries: List[Query] = field(default_factory=list)
     seed: int = 0
+    pool_ready_us: List[int] = field(default_factory=list)  # [] = warm pools (R18); R31
 
     @property
     def B(self) -> int:
@@ -279,6 +280,13 @@ def make_config(name: str) -> Problem:
                       lambda p: [Query(60 * D, 0, 150 * DOLLAR),
                                  Query(600 * D, 1800 * D, 100 * DOLLAR),
                                  Query(INF, INF, 40 * DOLLAR)])
+    if name == "C3w":
+        # C3 with a cold H100 pool: its GPUs are free only after the model load + first
+        # warm-up request, 30 s + 80 s (reading R31).
+        pb = make_config("C3")
+        pb.name = "C3w"
+        pb.pool_ready_us = [0, 110 * D]
+        return pb
     raise KeyError(name)
 
 

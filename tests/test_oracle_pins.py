@@ -467,3 +467,87 @@ def test_budget_only_winner_is_on_the_front(oracle_mod):
             checked += 1
         assert w[2][0] == 1  # closest tier exercised
     assert checked == 120
+
+
+# ------------------------------------------- R31: per-pool ready offsets (load + warm-up)
+def _event_sim_ready(pb, a, digits, ready_us):
+    """_event_sim with every GPU of pool p free from ready_us[p] ("~30 seconds"
+    to load, "~80 seconds" for the first warm-up request); unused pools end at 0."""
+    free = [[ready_us[p]] * g for p, g in enumerate(pb.gpus)]
+    used = set()
+    ready = []
+    coff = [sum(pb.radix[:b]) for b in range(pb.B)]
+    voff = [pb.va_offset(b) for b in range(pb.B)]
+    for s in range(pb.S):
+        b = max(bb for bb in range(pb.B) if pb.first_scene[bb] <= s)
+        c = digits[b]
+        lvl, k, p = pb.choices[coff[b] + c]
+        t = pb.va_us[voff[b] + (s - pb.first_scene[b]) * pb.radix[b] + c]
+        order = sorted(range(pb.gpus[p]), key=lambda g: (free[p][g], g))[:k]
+        start = max([a[s]] + [free[p][g] for g in order])
+        for g in order:
+            free[p][g] = start + t
+        used.add(p)
+        ready.append(start + t)
+    return ready, [max(f) if p in used else 0 for p, f in enumerate(free)]
+
+
+def test_pool_ready_event_simulation(oracle_mod):
+    """Offsets: the multiset recurrence started from F_p = off_p equals the explicit GPU
+    event simulation with GPUs free from off_p (brute force)."""
+    rng = random.Random(31)
+    for _ in range(1500):
+        pb = random_problem(rng, max_scenes=5)
+        pb.pool_ready_us = [rng.choice([0, rng.randint(0, 200_000_000)]) for _ in pb.gpus]
+        o = oracle_mod.Oracle(pb)
+        a = o.fixed_stages()
+        i = rng.randrange(o.n)
+        rec, ready, pend, mk, te = _detail(o, i)
+        r2, ends = _event_sim_ready(pb, a, o.decode(i), pb.pool_ready_us)
+        assert ready == r2
+        assert pend == ends
+        assert mk == max([rec.ttff_us] + ends)
+
+
+def test_pool_ready_closed_forms(oracle_mod):
+    """No contention: R_s = max(a_s, off_p) + t_s.  One pool, no fixed stages, uniform
+    offset x: every ready time and the makespan shift by exactly x.  Zero offsets = none."""
+    rng = random.Random(37)
+    for _ in range(200):
+        S = rng.randint(1, 6)
+        ks = [rng.choice([1, 2, 4]) for _ in range(S)]
+        G = sum(ks) + rng.randint(0, 3)
+        va = [rng.randint(1, 50_000_000) for _ in range(S)]
+        pb = make_problem([1000] * S, [rng.randint(0, 3_000_000) for _ in range(S)],
+                          [rng.randint(0, 3_000_000) for _ in range(S)], [G], [1],
+                          [1] * S, list(range(S + 1)), [(0, k, 0) for k in ks], va,
+                          overhead_us=1_200_000)
+        off = rng.randint(0, 20_000_000)
+        pb.pool_ready_us = [off]
+        o = oracle_mod.Oracle(pb)
+        a = o.fixed_stages()
+        assert _detail(o, 0)[1] == [max(a[s], off) + va[s] for s in range(S)]
+    for _ in range(200):
+        pb = random_problem(rng, max_scenes=5, max_pools=1, zero_fixed=True)
+        base = oracle_mod.Oracle(pb)
+        i = rng.randrange(base.n)
+        r0 = _detail(base, i)
+        x = rng.randint(1, 10**9)
+        pb.pool_ready_us = [x]
+        r1 = _detail(oracle_mod.Oracle(pb), i)
+        assert r1[1] == [t + x for t in r0[1]] and r1[3] == r0[3] + x
+        pb.pool_ready_us = [0]
+        assert _detail(oracle_mod.Oracle(pb), i)[0].astuple() == r0[0].astuple()
+
+
+def test_pool_ready_reserved_cost_example(oracle_mod):
+    """Worked example: one 8xA100 pool (Table 3: $14.42 per server-hour = 180,250 mc per
+    GPU-hour) loaded and warmed up in 30 s + 80 s, one 1-hour scene on all 8
+    GPUs: the pool is rented from t = 0, so it is billed 1 h 110 s = 3,710 s:
+    8 x 180,250 x 3,710 / 3,600 = 1,486,061.1 -> 1,486,061 mc (round half up)."""
+    pb = make_problem([600_000_000], [0], [0], [8], [180_250], [1], [0, 1], [(0, 8, 0)],
+                      [3_600_000_000], heads=0)
+    pb.pool_ready_us = [110_000_000]
+    rec, ready, pend, mk, te = _detail(oracle_mod.Oracle(pb), 0)
+    assert ready == [3_710_000_000] and mk == 3_710_000_000
+    assert rec.cost_mc == 1_486_061

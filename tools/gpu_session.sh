@@ -10,7 +10,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 2
 timeout 600 python bench.py --config $CFG > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?" >> gpurun_out/${TAG}_bench.err
 [ "${NCU:-1}" = "0" ] && { echo done; exit 0; }
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
-   python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_launch.log 2>&1
+   python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --stream-steps 0 > gpurun_out/${TAG}_ncu_launch.log 2>&1
 python tools/launch_summary.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launch_summary.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 3 -c 1 \
    -o gpurun_out/${TAG}_eval python tools/one_step.py $CFG 5 > gpurun_out/${TAG}_ncu_full.log 2>&1

@@ -333,7 +333,7 @@ struct StoreEmit {
 // jobs == nullptr: one request (job); else request blockIdx.y of a fleet (jobs[y]), each
 // CTA staging its own request's tables -- a whole fleet in one launch.
 template <int NP>
-__global__ void __launch_bounds__(kEvalThreads) eval_kernel(EvalJob job, const EvalJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kEvalThreads, NP == 1 ? 0 : 3) eval_kernel(EvalJob job, const EvalJob* __restrict__ jobs) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bar;
     if (jobs) job = jobs[blockIdx.y];

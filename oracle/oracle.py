@@ -30,7 +30,7 @@ class OrProblem(C.Structure):
         ("objective", C.c_uint32), ("n_levels", C.c_uint32), ("level_score", U32P),
         ("B", C.c_uint32), ("radix", U32P), ("first_scene", U32P),
         ("choice_level", U32P), ("choice_k", U32P), ("choice_pool", U32P),
-        ("va_us", U64P), ("pool_ready_us", U64P),
+        ("va_us", U64P), ("pool_ready_us", U64P), ("evict_risk_permille", U32P),
     ]
 
 
@@ -119,6 +119,9 @@ class Oracle:
         self._keep = []
         ch = pb.choices
         a = lambda t, v: self._k(_arr(t, v))  # noqa: E731
+        risk = getattr(pb, "evict_risk_permille", None)
+        if risk and (pb.billing != 0 or any(not 0 <= r < 1000 for r in risk)):
+            raise ValueError("eviction risk needs RESERVED billing and 0 <= rho < 1000 (R32)")
         self.c = OrProblem(
             S=pb.S, dur_us=a(C.c_uint64, pb.dur_us), llm_us=a(C.c_uint64, pb.llm_us),
             tts_us=a(C.c_uint64, pb.tts_us), overhead_us=pb.overhead_us,
@@ -132,7 +135,8 @@ class Oracle:
             choice_k=a(C.c_uint32, [x[1] for x in ch]),
             choice_pool=a(C.c_uint32, [x[2] for x in ch]),
             va_us=a(C.c_uint64, pb.va_us),
-            pool_ready_us=a(C.c_uint64, pb.pool_ready_us) if getattr(pb, "pool_ready_us", None) else None)
+            pool_ready_us=a(C.c_uint64, pb.pool_ready_us) if getattr(pb, "pool_ready_us", None) else None,
+            evict_risk_permille=a(C.c_uint32, risk) if risk else None)
 
     def _k(self, x):
         self._keep.append(x)

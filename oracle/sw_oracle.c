@@ -59,6 +59,8 @@ typedef struct {
     const uint64_t *va_us;            /* block-major: b, (s - first_b), c */
     const uint64_t *pool_ready_us;    /* [n_pools] or NULL: pool p's GPUs free from this time
                                          (model load + warm-up; reading R31) */
+    const uint32_t *evict_risk_permille; /* [n_pools] or NULL: Spot eviction risk of pool p
+                                         over the request, 1/1000 (reading R32) */
 } or_problem;
 
 typedef struct {
@@ -136,6 +138,17 @@ static uint64_t pool_cost(uint64_t X, uint64_t price) {
 }
 
 /* ---- a4-a7: evaluate ONE candidate by full recompute ----------------------- */
+/* Spot over-provisioning ("We proportionally increase the number of allocated
+ * resources to the eviction risk"; reading R32): allocate the fewest GPUs n
+ * whose expected survivors n * (1 - rho) still cover the G the schedule runs on, i.e. the
+ * smallest n >= G with n * (1000 - rho) >= G * 1000.  All n are billed (RESERVED). */
+static uint64_t billed_gpus(const or_problem *pb, uint32_t p) {
+    uint64_t G = pb->gpus[p], rho = pb->evict_risk_permille ? pb->evict_risk_permille[p] : 0;
+    uint64_t n = G;
+    while (n * (1000 - rho) < G * 1000) n++;
+    return n;
+}
+
 /* Optional detail outputs (any may be NULL): ready_us[S], pool_end[n_pools],
  * makespan, ttff_eff. */
 void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
@@ -207,7 +220,7 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
         if (pool_end_us) pool_end_us[p] = end;
         if (end > mk) mk = end;
         if (used & (1u << p)) {
-            uint64_t X = pb->billing == 0 ? (uint64_t)pb->gpus[p] * end : busy[p];
+            uint64_t X = pb->billing == 0 ? billed_gpus(pb, p) * end : busy[p];
             cost += pool_cost(X, pb->price_mc[p]);
         }
     }

@@ -144,6 +144,7 @@ class Problem:
     queries: List[Query] = field(default_factory=list)
     seed: int = 0
     pool_ready_us: List[int] = field(default_factory=list)  # [] = warm pools (R18); R31
+    evict_risk_permille: List[int] = field(default_factory=list)  # [] = no Spot risk; R32
 
     @property
     def B(self) -> int:
@@ -286,6 +287,15 @@ def make_config(name: str) -> Problem:
         pb = make_config("C3")
         pb.name = "C3w"
         pb.pool_ready_us = [0, 110 * D]
+        return pb
+    if name == "C3s":
+        # C3 with its H100 pool on Spot VMs: Table 3's Spot column and a 10%
+        # eviction risk over the request, covered by over-provisioning (SURVEY
+        # §8(f) row 3, reading R32): 8 scheduled H100s are billed as ceil(8 / 0.9) = 9.
+        pb = make_config("C3")
+        pb.name = "C3s"
+        pb.price_mc = [pb.price_mc[0], GPU_CLASSES["H100"][2]]
+        pb.evict_risk_permille = [0, 100]
         return pb
     raise KeyError(name)
 

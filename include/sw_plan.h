@@ -122,6 +122,15 @@ typedef struct {
                             (reading R31); NULL = all 0
                             (warm pools, R18).  An unused pool is neither billed nor
                             counted in the makespan. */
+    const uint32_t *evict_risk_permille;  /* [n_pools] or NULL: Spot eviction risk rho_p of
+                            pool p over the request, in 1/1000 (0 <= rho_p < 1000).  "We
+                            proportionally increase the number of allocated resources to the
+                            eviction risk" ("ceil(replicas /
+                            (1 - risk))"; reading R32): pool p is billed for
+                            G'_p = ceil(G_p * 1000 / (1000 - rho_p)) GPUs while the schedule
+                            runs on G_p (the spares stand by for evicted GPUs).  Pair it with
+                            the Spot column of Table 3.  RESERVED billing only: a non-zero
+                            rho_p with BUSY billing is SW_EINVAL.  NULL = all 0. */
 } sw_price_table;
 
 typedef void *(*sw_alloc_fn)(size_t bytes, void *stream, void *ctx);

@@ -46,7 +46,7 @@ class sw_profile_tables(C.Structure):
 class sw_price_table(C.Structure):
     _fields_ = [("n_pools", C.c_uint32), ("gpus", U32P), ("price_mc_per_gpu_hour", U64P),
                 ("fixed_cost_mc", C.c_uint64), ("billing", C.c_uint32), ("objective", C.c_uint32),
-                ("pool_ready_us", U64P)]
+                ("pool_ready_us", U64P), ("evict_risk_permille", U32P)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -267,9 +267,11 @@ def _marshal(pb, keep):
                            _arr(C.c_uint32, pb.first_scene), chs, _arr(C.c_uint64, pb.va_us),
                            len(pb.level_score), _arr(C.c_uint32, pb.level_score), pb.heads)
     ready = getattr(pb, "pool_ready_us", None)
+    risk = getattr(pb, "evict_risk_permille", None)
     pr = sw_price_table(len(pb.gpus), _arr(C.c_uint32, pb.gpus), _arr(C.c_uint64, pb.price_mc),
                         pb.fixed_cost_mc, pb.billing, pb.objective,
-                        _arr(C.c_uint64, ready) if ready else None)
+                        _arr(C.c_uint64, ready) if ready else None,
+                        _arr(C.c_uint32, risk) if risk else None)
     keep.append((sc, chs, tb, pr))
     return sc, tb, pr
 

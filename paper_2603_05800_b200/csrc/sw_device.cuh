@@ -56,8 +56,9 @@ struct __align__(16) DevHeader {
     uint32_t coff[kMaxDigits];    // choice offset of digit b
     uint32_t voff[kMaxDigits];    // va offset of digit b
     uint32_t G[kMaxP];
+    uint32_t Gbill[kMaxP];        // billed GPUs G'_p >= G_p (Spot over-provisioning, R32)
     uint64_t price[kMaxP];
-    uint64_t Gprice[kMaxP];       // G_p * price_p (device-computed in pack_kernel)
+    uint64_t Gprice[kMaxP];       // G'_p * price_p (device-computed in pack_kernel)
     uint64_t ready[kMaxP];        // pool p's GPUs free from this time (load + warm-up, R31)
     // LSD choices grouped by (pool, k) so the inner loop has neither: group g covers
     // lsd_dl[lsd_goff[g] .. lsd_goff[g+1]) with pool/k packed in lsd_pk[g] (p | k << 8)
@@ -219,7 +220,7 @@ __device__ __forceinline__ uint64_t state_cost(const State<NP>& st, const DevHea
     const bool busy = h.flags & 2u;
 #pragma unroll
     for (int p = 0; p < NP; p++) {
-        const uint64_t X = busy ? st.busy[p] : (uint64_t)h.G[p] * st.end[p];
+        const uint64_t X = busy ? st.busy[p] : (uint64_t)h.Gbill[p] * st.end[p];
         c += pool_cost(X, h.price[p]);  // unused pool: X = 0 -> 0
     }
     return c;

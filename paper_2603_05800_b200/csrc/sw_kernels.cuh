@@ -82,7 +82,7 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
             acc += raw.dur[s];
         }
     }
-    for (uint32_t p = threadIdx.x; p < hdr->NP; p += blockDim.x) hdr->Gprice[p] = (uint64_t)hdr->G[p] * hdr->price[p];
+    for (uint32_t p = threadIdx.x; p < hdr->NP; p += blockDim.x) hdr->Gprice[p] = (uint64_t)hdr->Gbill[p] * hdr->price[p];
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < raw.n_va; i += blockDim.x) {
         const uint32_t s = raw.va_scene[i];

@@ -247,6 +247,14 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
             return fail(nullptr, SW_EINVAL, "pool %u has %u GPUs (1..%d supported)", p, pr->gpus[p],
                         SW_MAX_GPUS_PER_POOL);
     if (pr->billing > 1 || pr->objective > 1) return fail(nullptr, SW_EINVAL, "bad billing/objective");
+    // Spot over-provisioning (R32): billed GPUs G'_p = ceil(G_p * 1000 / (1000 - rho_p))
+    uint32_t gbill[SW_MAX_POOLS];
+    for (uint32_t p = 0; p < NP; p++) {
+        const uint32_t rho = pr->evict_risk_permille ? pr->evict_risk_permille[p] : 0;
+        if (rho >= 1000) return fail(nullptr, SW_EINVAL, "pool %u: eviction risk %u per mille not < 1000", p, rho);
+        if (rho && pr->billing) return fail(nullptr, SW_EINVAL, "pool %u: eviction risk needs RESERVED billing", p);
+        gbill[p] = (uint32_t)(((uint64_t)pr->gpus[p] * 1000 + (999 - rho)) / (1000 - rho));
+    }
     if (tb->n_levels < 1) return fail(nullptr, SW_EINVAL, "n_levels = 0");
     const uint32_t s0 = sc->scene0_static ? 1u : 0u;
     if (s0 && S < 2) return fail(nullptr, SW_EINVAL, "a static intro needs S >= 2");
@@ -305,7 +313,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         if (qsum >= ((u128)1 << 32) - 1) return fail(nullptr, SW_ERANGE, "quality bound exceeds 2^32 - 2");
         u128 cmax = pr->fixed_cost_mc;
         for (uint32_t p = 0; p < NP; p++) {
-            const u128 X = (u128)pr->gpus[p] * tmax;  // >= busy and >= G * span
+            const u128 X = (u128)gbill[p] * tmax;  // >= busy and >= G' * span (G' >= G)
             const u128 prod = X * pr->price_mc_per_gpu_hour[p] + kHalfHour;
             if (prod >= ((u128)1 << 64)) return fail(nullptr, SW_ERANGE, "cost bound of pool %u exceeds 2^64", p);
             cmax += prod / kUsPerHour;
@@ -428,6 +436,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     }
     for (uint32_t p = 0; p < NP; p++) {
         H.G[p] = pr->gpus[p];
+        H.Gbill[p] = gbill[p];
         H.price[p] = pr->price_mc_per_gpu_hour[p];
         H.ready[p] = pr->pool_ready_us ? pr->pool_ready_us[p] : 0;  // load + warm-up (R31)
     }
@@ -2220,4 +2229,4 @@ extern "C" const char* sw_last_error(const sw_plan* h) {
 
 extern "C" uint64_t sw_plan_launch_count(const sw_plan* h) { return h ? h->launches : 0; }
 
-extern "C" int32_t sw_abi_version(void) { return 2; }  // 2: sw_price_table.pool_ready_us
+extern "C" int32_t sw_abi_version(void) { return 3; }  // 2: pool_ready_us; 3: evict_risk_permille

@@ -14,6 +14,7 @@ import pytest
 from swgen import make_config, INF
 from swgen.generator import Query, GPU_CLASSES
 from tests.helpers import make_problem, random_problem
+from tests.test_gpu_parity import sw  # noqa: F401 (GPU fixture: skips without CUDA)
 
 H100_SPOT_MC = 402_750  # Table 3: $32.22 per 8-GPU server-hour -> mc per GPU-hour
 
@@ -83,7 +84,15 @@ def test_risk_changes_only_the_bill(oracle_mod):
         assert got == oracle_mod.Oracle(pb2).eval(0)[0].cost_mc
 
 
-def test_busy_billing_rejects_risk(sw, oracle_mod):
+@pytest.fixture(scope="module")
+def swlib():
+    from paper_2603_05800_b200 import build
+    build.build()
+    import paper_2603_05800_b200 as m
+    return m
+
+
+def test_busy_billing_rejects_risk(swlib, oracle_mod):
     """BUSY billing has no idle spares to bill (R32): the oracle refuses, and the library
     returns SW_EINVAL on the host before any device call; so does rho >= 1000."""
     pb = _one_scene(4, H100_SPOT_MC, 1_000_000)
@@ -91,14 +100,14 @@ def test_busy_billing_rejects_risk(sw, oracle_mod):
     pb.evict_risk_permille = [100]
     with pytest.raises(ValueError):
         oracle_mod.Oracle(pb)
-    with pytest.raises(sw.SwError) as ei:
-        sw.Plan(pb)
-    assert ei.value.status == sw.SW_EINVAL
+    with pytest.raises(swlib.SwError) as ei:
+        swlib.Plan(pb)
+    assert ei.value.status == swlib.SW_EINVAL
     pb.billing = 0
     pb.evict_risk_permille = [1000]
-    with pytest.raises(sw.SwError) as ei:
-        sw.Plan(pb)
-    assert ei.value.status == sw.SW_EINVAL
+    with pytest.raises(swlib.SwError) as ei:
+        swlib.Plan(pb)
+    assert ei.value.status == swlib.SW_EINVAL
 
 
 def test_c3s_config():
@@ -117,7 +126,7 @@ def _exp(w):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("seed", range(8))
-def test_gpu_random_problems_with_risk(sw, oracle_mod, seed):
+def test_gpu_random_problems_with_risk(sw, oracle_mod, seed):  # noqa: F811
     from tests.test_gpu_parity import _check_winners, _records_equal
     rng = random.Random(3300 + seed)
     pb = random_problem(rng, max_scenes=7, max_pools=4, max_choices=5,
@@ -147,7 +156,7 @@ def test_gpu_random_problems_with_risk(sw, oracle_mod, seed):
 
 
 @pytest.mark.gpu
-def test_gpu_c3s_subrange(sw, oracle_mod):
+def test_gpu_c3s_subrange(sw, oracle_mod):  # noqa: F811
     """C3s: a ragged 3M sub-range through eval + select + front + digest and through the
     stream path; sampled records."""
     from tests.test_gpu_parity import _check_winners, _records_equal

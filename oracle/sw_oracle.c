@@ -18,7 +18,10 @@
  *   - playback metrics: TTFF, TTFF_eff = max over scenes of
  *     ready - deadline (scene-granular deadlines P:338-341), stall
  *     = TTFF_eff - TTFF (reading R8);
+ *   - a STATIC rung (degree k = 0): no video stage and no GPU, R_s = a_s (P:997,
+ *     P:823-825; reading R33);
  *   - cost from Table 3 prices billed per pool (reading R10);
+ *     Spot pools over-provisioned by eviction risk (reading R32);
  *   - quality = sum of duration_ms x level score (R12);
  *   - constrained selection: objective, SLO steering and "closest solution"
  *     when infeasible (reading R13);
@@ -166,7 +169,7 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
         for (uint32_t g = 0; g < pb->gpus[p]; g++) F[p][g] = pb->pool_ready_us ? pb->pool_ready_us[p] : 0;
         busy[p] = 0;
     }
-    uint64_t R0 = 0, Q = 0;
+    uint64_t R0 = 0, Q = 0, last = 0; /* last: latest ready time of a STATIC scene */
     int64_t M = 0;
     uint32_t cnt = 0;
     uint32_t s0 = 0;
@@ -189,6 +192,23 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
         uint32_t k = pb->choice_k[coff + c];
         uint32_t p = pb->choice_pool[coff + c];
         uint64_t t = pb->va_us[voff + (s - pb->first_scene[b]) * pb->radix[b] + c];
+        if (k == 0) {
+            /* STATIC rung ("If not enough, we switch to static content", P:823-825;
+               reading R33): no video stage and no GPU -- the scene (slides over its
+               narration) is ready once its text and audio are, R_s = a_s */
+            uint64_t e = a[s];
+            if (ready_us) ready_us[s] = e;
+            if (e > last) last = e;
+            if (s == 0) {
+                R0 = e;
+                M = (int64_t)e;
+            } else if ((int64_t)e - (int64_t)P[s] > M) {
+                M = (int64_t)e - (int64_t)P[s];
+                cnt++;
+            }
+            Q += (pb->dur_us[s] / 1000) * pb->level_score[l];
+            continue;
+        }
         /* the scene needs its text+audio (a_s) and k GPUs: the k earliest free */
         uint64_t fk = F[p][k - 1];
         uint64_t st = a[s] > fk ? a[s] : fk;
@@ -212,7 +232,7 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
         }
         Q += (pb->dur_us[s] / 1000) * pb->level_score[l];
     }
-    uint64_t cost = pb->fixed_cost_mc, mk = R0;
+    uint64_t cost = pb->fixed_cost_mc, mk = R0 > last ? R0 : last; /* makespan: last scene ready */
     for (uint32_t p = 0; p < pb->n_pools; p++) {
         uint64_t end = 0; /* an unused pool is not provisioned: no end, no bill (R31) */
         if (used & (1u << p))

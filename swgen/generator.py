@@ -288,6 +288,28 @@ def make_config(name: str) -> Problem:
         pb.name = "C3w"
         pb.pool_ready_us = [0, 110 * D]
         return pb
+    if name == "C3t":
+        # C3 with a STATIC rung on every digit ("If not enough, we switch to static
+        # content", reading R33): choice (STATIC, k = 0)
+        # first in each digit's list (quality 0 sorts before LOW, R19), no V+A stage
+        # (va_us = 0).  25^6 = 2.4e8 plans.
+        pb = make_config("C3")
+        pb.name = "C3t"
+        static_level = len(pb.level_score)
+        pb.level_score = pb.level_score + [0]  # STATIC scores 0 (R12)
+        choices, va, off, coff = [], [], 0, 0
+        for b, r in enumerate(pb.radix):
+            L = pb.first_scene[b + 1] - pb.first_scene[b]
+            choices.append((static_level, 0, 0))
+            choices.extend(pb.choices[coff:coff + r])
+            for j in range(L):
+                va.append(0)
+                va.extend(pb.va_us[off + j * r: off + (j + 1) * r])
+            off += L * r
+            coff += r
+        pb.radix = [r + 1 for r in pb.radix]
+        pb.choices, pb.va_us = choices, va
+        return pb
     if name == "C3s":
         # C3 with its H100 pool on Spot VMs: Table 3's Spot column and a 10%
         # eviction risk over the request, covered by over-provisioning (SURVEY

@@ -86,8 +86,12 @@ typedef struct {
 /* One choice of a digit: applied to every scene of the digit's block. */
 typedef struct {
     uint8_t level;   /* index into level_score */
-    uint8_t degree;  /* k GPUs (USP degree); must divide heads */
-    uint8_t pool;    /* GPU pool index */
+    uint8_t degree;  /* k GPUs (USP degree); must divide heads.
+                        0 = the STATIC rung: no video stage and no GPU, the scene is
+                        ready with its text and audio, R_s = a_s ("If not enough, we
+                        switch to static content"; reading R33);
+                        pair it with a level whose score is 0 (R12) */
+    uint8_t pool;    /* GPU pool index (< n_pools; unused by a STATIC choice) */
     uint8_t pad;
 } sw_choice;
 
@@ -100,7 +104,8 @@ typedef struct {
     const uint32_t *first_scene;/* [B+1] */
     const sw_choice *choices;   /* [sum r_b] concatenated per digit */
     const uint64_t *va_us;      /* V+A stage time, block-major: digit b, scene s in
-                                   block, choice c -> va_us[off_b + (s-first_b)*r_b + c], >= 1 */
+                                   block, choice c -> va_us[off_b + (s-first_b)*r_b + c], >= 1
+                                   (= 0 exactly for STATIC choices, else SW_EINVAL) */
     uint32_t n_levels;
     const uint32_t *level_score;/* [n_levels] quality score per level (R12) */
     uint32_t heads;             /* attention heads for the divisibility check;

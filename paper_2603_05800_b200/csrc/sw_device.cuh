@@ -161,6 +161,9 @@ __device__ __forceinline__ void gang_update_dyn(uint64_t (&F)[kMaxG], uint64_t e
 template <int NP, int KS>
 __device__ __forceinline__ uint64_t scene_step(State<NP>& st, uint32_t p, uint32_t k,
                                                uint64_t a, uint64_t t) {
+    // STATIC rung (k = 0, runtime path only): no video stage, no GPU -- the scene is
+    // ready with its text and audio, R_s = a_s (reading R33)
+    if (KS == 0 && k == 0) return a;
     uint64_t e = 0;
 #pragma unroll
     for (int q = 0; q < NP; q++) {

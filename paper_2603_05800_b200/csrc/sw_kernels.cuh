@@ -168,6 +168,21 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2
     for (uint32_t g = 0; g < ng; g++) {
         const uint32_t pk = h.lsd_pk[g];
         const uint32_t p = pk & 0xffu, k = pk >> 8;
+        if (k == 0) {  // STATIC rung (R33): R_s = a_s, no pool touched, nothing billed
+            const int64_t d = (int64_t)as - Ps;
+            const bool nm = d > M0;
+            Rec4 r;
+            r.w0 = R0;
+            r.w1 = (uint64_t)(nm ? d : M0) - R0;
+            r.w2 = pcsum;
+            const uint64_t w3s = w3base + (nm ? (1ull << 32) : 0ull);
+            for (uint32_t j = h.lsd_goff[g]; j < h.lsd_goff[g + 1]; j++) {
+                const LsdEntry E = h.lsd[j];
+                r.w3 = w3s + E.q;
+                put(E.dl, r);
+            }
+            continue;
+        }
         uint64_t endp = 0, busyp = 0, pcp = 0, A = 0, price = 0;
 #pragma unroll
         for (int q = 0; q < NP; q++)
@@ -476,6 +491,7 @@ __device__ void detail_one(const DevHeader* __restrict__ g_hdr, const VaEntry* _
         out->pool_end[p] = st.end[p];
         mk = umax64(mk, st.end[p]);
     }
+    for (uint32_t s = 0; s < h.S; s++) mk = umax64(mk, out->ready[s]);  // STATIC scenes (R33)
     out->rec.w0 = st.R0;
     out->rec.w1 = (uint64_t)st.M - st.R0;
     out->rec.w2 = state_cost(st, h);

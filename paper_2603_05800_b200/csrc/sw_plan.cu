@@ -277,13 +277,26 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         const sw_choice& ch = tb->choices[c];
         if (ch.level >= tb->n_levels) return fail(nullptr, SW_EINVAL, "choice %u: level %u >= n_levels", c, ch.level);
         if (ch.pool >= NP) return fail(nullptr, SW_EINVAL, "choice %u: pool %u >= n_pools", c, ch.pool);
-        if (ch.degree < 1 || ch.degree > pr->gpus[ch.pool])
+        if (ch.degree == 0) continue;  // STATIC rung: no video stage, no GPU (R33)
+        if (ch.degree > pr->gpus[ch.pool])
             return fail(nullptr, SW_EINVAL, "choice %u: k = %u exceeds G_p = %u", c, ch.degree, pr->gpus[ch.pool]);
         if (tb->heads && tb->heads % ch.degree)
             return fail(nullptr, SW_EINVAL, "choice %u: k = %u does not divide %u heads (P:748)", c, ch.degree, tb->heads);
     }
-    for (uint64_t i = 0; i < n_va; i++)
-        if (tb->va_us[i] == 0) return fail(nullptr, SW_EINVAL, "va_us[%llu] = 0", (unsigned long long)i);
+    {  // a video stage takes time (va >= 1); a STATIC choice has none (va = 0)
+        uint64_t i = 0, coff = 0;
+        for (uint32_t b = 0; b < B; b++) {
+            const uint32_t r = tb->radix[b];
+            for (uint32_t s = tb->first_scene[b]; s < tb->first_scene[b + 1]; s++)
+                for (uint32_t c = 0; c < r; c++, i++) {
+                    const bool stat = tb->choices[coff + c].degree == 0;
+                    if (stat != (tb->va_us[i] == 0))
+                        return fail(nullptr, SW_EINVAL, "va_us[%llu] = %llu for a %s choice", (unsigned long long)i,
+                                    (unsigned long long)tb->va_us[i], stat ? "STATIC" : "video");
+                }
+            coff += r;
+        }
+    }
     // ---- overflow bounds (R25): every intermediate fits its integer type
     {
         u128 fixed = (u128)sc->overhead_us + sc->static_ready_us;

@@ -38,6 +38,8 @@ WORKLOADS = {
           "chunked when records exceed HBM (BASELINE configs[4])",
     "C3w": "C3w: C3 with a cold H100 pool ready at 110 s (load 30 s + warm-up 80 s, P:608-611; "
            "SURVEY 8(f) row 3), 24^6 plans",
+    "C3u": "C3u: C3 with an upscaled rung (MED + Real-ESRGAN to 1280x800, P:929-931, Table 4; "
+           "SURVEY 8(f) row 3), 32^6 = 1.1e9 plans",
     "C3t": "C3t: C3 with a STATIC rung (no video stage, R_s = a_s; P:997, SURVEY 8(f) row 3) on "
            "every digit, 25^6 plans",
     "C3s": "C3s: C3 with the H100 pool on Spot prices (Table 3) and a 10% eviction risk covered "

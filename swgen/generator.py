@@ -74,6 +74,13 @@ LEVELS = {
 LEVEL_SCORE = [250, 500, 750, 1000]
 LEVEL_LV = [1.0 / 8.0, 1.0, 3.375, 8.0]
 
+# Upscaled rung (reading R34): generate at MED (640x400, 10 steps), then
+# Real-ESRGAN to 1280x800 on the same k GPUs.  Table 4: 2663.4 s for the 600 s
+# video on one A100 -> 4.439 s per video-second, frames independent (divides by k).
+LEVEL_UP = 4
+UP_SCORE = 750
+ESRGAN_S_PER_VIDEO_S = 2663.4 / 600.0
+
 # DiT speed-up for k GPUs under USP ("over a 5x reduction" at 8;
 # ledger L17), VAE/encode fraction 0.12 not parallelised.
 SP = {1: 1.0, 2: 1.9, 4: 3.4, 8: 5.2}
@@ -105,6 +112,9 @@ def n16_frames(dur_ms: int) -> int:
 
 def va_seconds(dur_ms: int, level: int, k: int, gpu: str, jitter: float = 1.0) -> float:
     """Un-rounded V+A stage time in seconds (App. B), before llround to microseconds."""
+    if level == LEVEL_UP:  # MED generation + Real-ESRGAN upscale (R34)
+        return (va_seconds(dur_ms, 1, k, gpu, jitter)
+                + ESRGAN_S_PER_VIDEO_S * (dur_ms / 1000.0) / (k * GPU_CLASSES[gpu][0]))
     n16 = n16_frames(dur_ms)
     clips = (n16 + 80) // 81  # 81-frame clips (P:492, P:532)
     base = clips * VA_INTERCEPT_S + n16 * VA_SLOPE_S
@@ -287,6 +297,16 @@ def make_config(name: str) -> Problem:
         pb = make_config("C3")
         pb.name = "C3w"
         pb.pool_ready_us = [0, 110 * D]
+        return pb
+    if name == "C3u":
+        # C3 with an upscaled rung: MED + Real-ESRGAN to 1280x800 (P:929-931, P:1196,
+        # Table 4, reading R34), scored 750; 32^6 = 1.1e9 plans.
+        pb = _build("C3u", 1003, 600, 20,
+                    [(1, 1), (2, 2), (3, 3), (4, 11), (12, 18), (19, 19)],
+                    [0, 1, LEVEL_UP, 3], [1, 2, 4, 8], [("A100", 8), ("H100", 8)], True, True,
+                    lambda p: [Query(999_999, 0, 45 * DOLLAR), Query(2_999_999, 0, 5 * DOLLAR),
+                               Query(INF, INF, INF)])
+        pb.level_score = LEVEL_SCORE + [UP_SCORE]
         return pb
     if name == "C3t":
         # C3 with a STATIC rung on every digit ("If not enough, we switch to static

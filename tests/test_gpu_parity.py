@@ -96,7 +96,7 @@ def test_random_problems_all_records(sw, oracle_mod, seed):
 
 def test_detail_matches_oracle(sw, oracle_mod):
     rng = random.Random(5)
-    for cfg in ["C1", "C2", "C3", "C3w", "C3s", "C3t", "C5"]:
+    for cfg in ["C1", "C2", "C3", "C3w", "C3s", "C3t", "C3u", "C5"]:
         pb = make_config(cfg)
         orc = oracle_mod.Oracle(pb)
         with sw.Plan(pb, record_capacity=1) as plan:

@@ -120,7 +120,7 @@ def test_oracle_greedy_baseline_is_cheapest(oracle_mod):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3w", "C3s", "C3t", "C5"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3w", "C3s", "C3t", "C3u", "C5"])
 def test_gpu_greedy_matches_oracle(oracle_mod, cfg):
     if not cuda_available():
         pytest.skip("no CUDA device")

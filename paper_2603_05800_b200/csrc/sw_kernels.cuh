@@ -1388,6 +1388,14 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     Dlt& d = *reinterpret_cast<Dlt*>(fsm + ring_bytes(PARETO));
     PPoint* fs = reinterpret_cast<PPoint*>(fsm + ring_bytes(PARETO) + sizeof(Dlt));
     PPoint* bsurv = fs + kFrontSmem;  // PARETO only
+    // the smem front subset as arrays (t, c, idx, q): a warp reading 32 consecutive points
+    // touches consecutive 8 B words (an array of 32 B PPoints costs 4-way bank conflicts)
+    uint64_t* f_t = reinterpret_cast<uint64_t*>(fs);
+    uint64_t* f_c = f_t + kFrontSmem;
+    uint64_t* f_i = f_c + kFrontSmem;
+    uint32_t* f_q = reinterpret_cast<uint32_t*>(f_i + kFrontSmem);
+    static_assert(kFrontSmem * (3 * sizeof(uint64_t) + sizeof(uint32_t)) <= kFrontSmem * sizeof(PPoint),
+                  "front arrays fit the PPoint subset's smem");
     __shared__ uint32_t s_bcnt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -1398,16 +1406,23 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         s_vt[threadIdx.x] = ~0ull;
     }
     if (threadIdx.x == 0) s_bcnt = 0;
-    uint32_t m_sm = 0, m_all = 0;
+    uint32_t m_sm = 0, m_all = 0, chk = 1;
     if (PARETO) {
         m_all = (uint32_t)pa.ctl->front_n;
         m_sm = min(m_all, kFrontSmem);
+        chk = max((m_all + 31u) / 32u, 1u);  // exact test: front probe chunk (32 chunks)
         {  // stage the whole DLT (16 B vectors)
             const uint4* src = reinterpret_cast<const uint4*>(pa.dlt);
             uint4* dst = reinterpret_cast<uint4*>(&d);
             for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
         }
-        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = pa.front[i];
+        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) {
+            const PPoint f = pa.front[i];
+            f_t[i] = f.t;
+            f_c[i] = f.c;
+            f_i[i] = f.idx;
+            f_q[i] = f.q;
+        }
         // a reserved-but-not-yet-written (or torn) survivor slot must dominate nothing:
         // sentinel t = c = max, q = 0 (a torn write mixes halves that still carry a max)
         for (uint32_t i = threadIdx.x; i < kBlockSurv; i += blockDim.x) {
@@ -1627,21 +1642,37 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                         x.c = __shfl_sync(0xffffffffu, pt.c, src);
                         x.q = __shfl_sync(0xffffffffu, pt.q, src);
                         bool dom = false;
-                        // front sorted by t: only points with t <= x.t can dominate x
-                        for (uint32_t j0 = 0; j0 < m_sm && fs[j0].t <= x.t; j0 += 32) {
+                        // front sorted by t: only points with t <= x.t can dominate x.  The
+                        // DLT already rejects what the front below x's t bin dominates, so a
+                        // dominator the exact test must find usually has t just below x.t:
+                        // locate the chunk of 32 holding the last t <= x.t with one warp
+                        // probe (lane l reads the first t of chunk l * chk), then test
+                        // downwards from its end.  The order does not change the result.
+                        uint32_t top = 0;  // test points [0, top)
+                        {
+                            const uint32_t pi = lane * chk;
+                            const uint64_t tp = pi < m_all ? (pi < m_sm ? f_t[pi] : pa.front[pi].t) : kInf64;
+                            const unsigned pb = __ballot_sync(0xffffffffu, tp <= x.t);
+                            if (pb) top = min(m_all, (uint32_t)(31 - __clz(pb)) * chk + chk);
+                        }
+                        for (uint32_t j1 = top; j1 > 0 && !dom;) {
+                            const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
                             const uint32_t j = j0 + lane;
                             // an identical entry (same index) also removes x: it is already kept
-                            const bool dj = j < m_sm && pdom(fs[j], 0, x, 1);
-                            if (__any_sync(0xffffffffu, dj)) {
-                                dom = true;
-                                break;
+                            // (front points beyond the smem subset: from global, L2-resident)
+                            PPoint y;
+                            if (j < m_sm) {
+                                y.t = f_t[j];
+                                y.c = f_c[j];
+                                y.idx = f_i[j];
+                                y.q = f_q[j];
+                                y.pad = 0;
+                            } else {
+                                y = pa.front[j < j1 ? j : 0];
                             }
-                        }
-                        // front points beyond the smem subset: from global (L2-resident)
-                        for (uint32_t j0 = m_sm; !dom && j0 < m_all && pa.front[j0].t <= x.t; j0 += 32) {
-                            const uint32_t j = j0 + lane;
-                            const bool dj = j < m_all && pdom(pa.front[j], 0, x, 1);
+                            const bool dj = j < j1 && pdom(y, 0, x, 1);
                             if (__any_sync(0xffffffffu, dj)) dom = true;
+                            j1 = j0;
                         }
                         // ... and against this block's earlier survivors: neighbouring
                         // records (runs of consecutive indices) often dominate
@@ -1888,17 +1919,22 @@ struct StreamEmit {
                 x.c = __shfl_sync(0xffffffffu, pt.c, src);
                 x.q = __shfl_sync(0xffffffffu, pt.q, src);
                 bool dom = false;
-                // front sorted by t: only points with t <= x.t can dominate x
-                for (uint32_t j0 = 0; j0 < m_sm && fs[j0].t <= x.t; j0 += 32) {
-                    const uint32_t j = j0 + lane;
-                    if (__any_sync(0xffffffffu, j < m_sm && pdom(fs[j], 0, x, 1))) {
-                        dom = true;
-                        break;
-                    }
+                // front sorted by t: only points with t <= x.t can dominate x; probe for the
+                // chunk holding the last such point and test downwards (as scan_kernel)
+                uint32_t top = 0;
+                {
+                    const uint32_t chk = max((m_all + 31u) / 32u, 1u);
+                    const uint32_t pi = lane * chk;
+                    const uint64_t tp = pi < m_all ? (pi < m_sm ? fs[pi].t : a.front[pi].t) : kInf64;
+                    const unsigned pb = __ballot_sync(0xffffffffu, tp <= x.t);
+                    if (pb) top = min(m_all, (uint32_t)(31 - __clz(pb)) * chk + chk);
                 }
-                for (uint32_t j0 = m_sm; !dom && j0 < m_all && a.front[j0].t <= x.t; j0 += 32) {
+                for (uint32_t j1 = top; j1 > 0 && !dom;) {
+                    const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
                     const uint32_t j = j0 + lane;
-                    if (__any_sync(0xffffffffu, j < m_all && pdom(a.front[j], 0, x, 1))) dom = true;
+                    const bool dj = j < j1 && pdom(j < m_sm ? fs[j] : a.front[j < j1 ? j : 0], 0, x, 1);
+                    if (__any_sync(0xffffffffu, dj)) dom = true;
+                    j1 = j0;
                 }
                 const uint32_t bc = min(*(volatile uint32_t*)&S.bcnt, kBlockSurv);
                 for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {

@@ -1621,92 +1621,101 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                     const uint32_t nk = __reduce_add_sync(0xffffffffu, __popc(keepm));
                     if (lane == 0) atomicAdd(&pa.ctl->dlt_pass, (unsigned long long)nk);
                 }
+// exact test of every DLT survivor of the stage by the whole warp, ONE loop over the
+                // (u, lane) pairs: a single copy of the loop body (one copy per u cost
+                // instruction-cache misses: no_instructions was the top stall on C3)
+                uint64_t pidx[kRPT];
+                unsigned pm[kRPT];  // warp-uniform: lanes whose record u is still pending
 #pragma unroll
                 for (int u = 0; u < kRPT; u++) {
-                    PPoint pt;
-                    pt.t = r[u].w0 + r[u].w1;
-                    pt.c = r[u].w2;
-                    pt.q = rec_Q(r[u]);
-                    pt.idx = 0;
-                    pt.pad = 0;
-                    bool keep = (keepm >> u) & 1u;
-                    unsigned pend = __ballot_sync(0xffffffffu, keep);
-                    if (!pend) continue;
-                    if (keep) pt.idx = flat_index(v, per_tile, mt.pos0 + lane + u * 32);
-                    while (pend) {  // exact test of each DLT survivor by the whole warp
-                        const int src = __ffs(pend) - 1;
-                        pend &= pend - 1;
-                        PPoint x;
-                        x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
-                        x.t = __shfl_sync(0xffffffffu, pt.t, src);
-                        x.c = __shfl_sync(0xffffffffu, pt.c, src);
-                        x.q = __shfl_sync(0xffffffffu, pt.q, src);
-                        bool dom = false;
-                        // front sorted by t: only points with t <= x.t can dominate x.  The
-                        // DLT already rejects what the front below x's t bin dominates, so a
-                        // dominator the exact test must find usually has t just below x.t:
-                        // locate the chunk of 32 holding the last t <= x.t with one warp
-                        // probe (lane l reads the first t of chunk l * chk), then test
-                        // downwards from its end.  The order does not change the result.
-                        uint32_t top = 0;  // test points [0, top)
-                        {
-                            const uint32_t pi = lane * chk;
-                            const uint64_t tp = pi < m_all ? (pi < m_sm ? f_t[pi] : pa.front[pi].t) : kInf64;
-                            const unsigned pb = __ballot_sync(0xffffffffu, tp <= x.t);
-                            if (pb) top = min(m_all, (uint32_t)(31 - __clz(pb)) * chk + chk);
+                    const bool k = (keepm >> u) & 1u;
+                    pidx[u] = k ? flat_index(v, per_tile, mt.pos0 + lane + u * 32) : 0;
+                    pm[u] = __ballot_sync(0xffffffffu, k);
+                }
+                for (;;) {
+                    int u = -1;
+                    unsigned pend = 0;
+#pragma unroll
+                    for (int k = kRPT - 1; k >= 0; k--)
+                        if (pm[k]) {
+                            u = k;
+                            pend = pm[k];
                         }
-                        for (uint32_t j1 = top; j1 > 0 && !dom;) {
-                            const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
-                            const uint32_t j = j0 + lane;
-                            // an identical entry (same index) also removes x: it is already kept
-                            // (front points beyond the smem subset: from global, L2-resident)
-                            PPoint y;
-                            if (j < m_sm) {
-                                y.t = f_t[j];
-                                y.c = f_c[j];
-                                y.idx = f_i[j];
-                                y.q = f_q[j];
-                                y.pad = 0;
-                            } else {
-                                y = pa.front[j < j1 ? j : 0];
-                            }
-                            const bool dj = j < j1 && pdom(y, 0, x, 1);
-                            if (__any_sync(0xffffffffu, dj)) dom = true;
-                            j1 = j0;
-                        }
-                        // ... and against this block's earlier survivors: neighbouring
-                        // records (runs of consecutive indices) often dominate
-                        // each other, and every survivor costs the merge O(m)
-                        const uint32_t bc = min(*(volatile uint32_t*)&s_bcnt, kBlockSurv);
-                        for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {
-                            const uint32_t j = j0 + lane;
-                            const bool dj = j < bc && pdom(bsurv[j], 0, x, 1);
-                            if (__any_sync(0xffffffffu, dj)) dom = true;
-                        }
-                        if (lane == src && dom) keep = false;
-                    }
-                    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-                    if (mask) {
-                        const int ldr = __ffs(mask) - 1;
-                        uint32_t b0 = 0;
-                        if (lane == ldr) b0 = atomicAdd(&s_bcnt, (uint32_t)__popc(mask));
-                        b0 = __shfl_sync(0xffffffffu, b0, ldr);
-                        const uint32_t my = b0 + __popc(mask & ((1u << lane) - 1u));
-                        const bool local = my < kBlockSurv;
-                        if (keep && local) bsurv[my] = pt;
-                        // block list full: straight to the global survivor buffer
-                        const unsigned gmask = __ballot_sync(0xffffffffu, keep && !local);
-                        if (gmask) {
-                            const int gl = __ffs(gmask) - 1;
-                            unsigned long long slot0 = 0;
-                            if (lane == gl) slot0 = atomicAdd(&pa.ctl->surv, (unsigned long long)__popc(gmask));
-                            slot0 = __shfl_sync(0xffffffffu, slot0, gl);
-                            if (keep && !local) {
-                                const uint64_t slot = slot0 + __popc(gmask & ((1u << lane) - 1u));
-                                if (slot < pa.cap) pa.surv[slot] = pt;
-                            }
+                    if (u < 0) break;
+                    const int src = __ffs(pend) - 1;
+                    uint64_t xt = 0, xc = 0, xi = 0;
+                    uint32_t xq = 0;
+#pragma unroll
+                    for (int k = 0; k < kRPT; k++) {
+                        if (k == u) {
+                            pm[k] &= pm[k] - 1;
+                            xt = r[k].w0 + r[k].w1;
+                            xc = r[k].w2;
+                            xq = rec_Q(r[k]);
+                            xi = pidx[k];
                         }
                     }
+                    PPoint x;
+                    x.idx = __shfl_sync(0xffffffffu, xi, src);
+                    x.t = __shfl_sync(0xffffffffu, xt, src);
+                    x.c = __shfl_sync(0xffffffffu, xc, src);
+                    x.q = __shfl_sync(0xffffffffu, xq, src);
+                    x.pad = 0;
+                    bool dom = false;
+                    // front sorted by t: only points with t <= x.t can dominate x.  The
+                    // DLT already rejects what the front below x's t bin dominates, so a
+                    // dominator the exact test must find usually has t just below x.t:
+                    // locate the chunk of 32 holding the last t <= x.t with one warp
+                    // probe (lane l reads the first t of chunk l * chk), then test
+                    // downwards from its end.  The order does not change the result.
+                    uint32_t top = 0;  // test points [0, top)
+                    {
+                        const uint32_t pi = lane * chk;
+                        const uint64_t tp = pi < m_all ? (pi < m_sm ? f_t[pi] : pa.front[pi].t) : kInf64;
+                        const unsigned pb = __ballot_sync(0xffffffffu, tp <= x.t);
+                        if (pb) top = min(m_all, (uint32_t)(31 - __clz(pb)) * chk + chk);
+                    }
+                    for (uint32_t j1 = top; j1 > 0 && !dom;) {
+                        const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
+                        const uint32_t j = j0 + lane;
+                        // an identical entry (same index) also removes x: it is already kept
+                        // (front points beyond the smem subset: from global, L2-resident)
+                        PPoint y;
+                        if (j < m_sm) {
+                            y.t = f_t[j];
+                            y.c = f_c[j];
+                            y.idx = f_i[j];
+                            y.q = f_q[j];
+                            y.pad = 0;
+                        } else {
+                            y = pa.front[j < j1 ? j : 0];
+                        }
+                        const bool dj = j < j1 && pdom(y, 0, x, 1);
+                        if (__any_sync(0xffffffffu, dj)) dom = true;
+                        j1 = j0;
+                    }
+                    // ... and against this block's earlier survivors: neighbouring
+                    // records (runs of consecutive indices) often dominate
+                    // each other, and every survivor costs the merge O(m)
+                    const uint32_t bc = min(*(volatile uint32_t*)&s_bcnt, kBlockSurv);
+                    for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {
+                        const uint32_t j = j0 + lane;
+                        const bool dj = j < bc && pdom(bsurv[j], 0, x, 1);
+                        if (__any_sync(0xffffffffu, dj)) dom = true;
+                    }
+                    // a survivor joins this block's list at once, so that the stage's later
+                    // records (the neighbours that often dominate each other) are tested
+                    // against it; list full: straight to the global survivor buffer
+                    if (!dom && lane == src) {
+                        const uint32_t my = atomicAdd(&s_bcnt, 1u);
+                        if (my < kBlockSurv) {
+                            bsurv[my] = x;
+                        } else {
+                            const unsigned long long slot = atomicAdd(&pa.ctl->surv, 1ull);
+                            if (slot < pa.cap) pa.surv[slot] = x;
+                        }
+                    }
+                    __syncwarp();
                 }
             }
         }

@@ -237,3 +237,16 @@ def pareto_points(points):
     out = (OrPoint * max(1, n))()
     m = lib().or_pareto_points(arr, C.c_uint64(n), out)
     return [(p.index, p.ttff_eff_us, p.cost_mc, p.quality) for p in out[:m]]
+
+
+def winner_merge(objective, query, a, b):
+    """Merge two (status, index, Rec) winners of one query over disjoint candidate sets
+    with the rule or_sweep applies across its threads (or_winner_merge)."""
+    q = OrQuery(query.slo_startup_us, query.slo_stall_us, query.budget_mc)
+
+    def w(x):
+        st, idx, rec = x
+        return OrWinner(idx, OrRecord(*rec.astuple(), 0), st, 0)
+    wa, wb, out = w(a), w(b), OrWinner()
+    lib().or_winner_merge(C.c_uint32(objective), C.byref(q), C.byref(wa), C.byref(wb), C.byref(out))
+    return out.status, out.index, _rec(out.rec)

@@ -567,6 +567,21 @@ int or_greedy(const or_problem *pb, const or_query *q, uint64_t start, uint64_t 
     return 0;
 }
 
+/* Merge of two winners of the SAME query over disjoint candidate sets (e.g. pieces of a
+ * long full-space sweep run one after the other): the same rule or_sweep applies across
+ * its threads -- a feasible winner beats a closest one, feasible by the objective key,
+ * closest by (V_t, V_c, key, index) (reading R13); an empty one (status -1)
+ * loses. */
+void or_winner_merge(uint32_t objective, const or_query *q, const or_winner *a, const or_winner *b,
+                     or_winner *out) {
+    if (a->status < 0) { *out = *b; return; }
+    if (b->status < 0) { *out = *a; return; }
+    if (a->status != b->status) { *out = a->status == 0 ? *a : *b; return; }
+    int c = a->status == 0 ? obj_cmp(objective, a->index, &a->rec, b->index, &b->rec)
+                           : closest_cmp(objective, q, a->index, &a->rec, b->index, &b->rec);
+    *out = c <= 0 ? *a : *b;
+}
+
 int or_abi_version(void) { return 1; }
 uint32_t or_sizeof_record(void) { return (uint32_t)sizeof(or_record); }
 uint32_t or_sizeof_winner(void) { return (uint32_t)sizeof(or_winner); }

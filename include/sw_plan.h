@@ -61,8 +61,12 @@ enum {
                          record_capacity (SPEC "InstanceTooLarge") */
     SW_ENOMEM = -3,
     SW_ECUDA = -4,
-    SW_ENCCL = -5,
-    SW_ESTATE = -6 /* wrong call order or handle misuse */
+    SW_ENCCL = -5,    /* a collective failed, a peer rank reported an asynchronous NCCL
+                         error, or a wait exceeded SW_NCCL_TIMEOUT_S seconds (default 600):
+                         the communicator is then aborted (do not use it again) */
+    SW_ESTATE = -6 /* wrong call order or handle misuse; multi-rank: the ranks made
+                      different collective calls (arguments or evaluated ranges differ),
+                      detected on every rank */
 };
 
 #define SW_MAX_SCENES 64
@@ -269,9 +273,29 @@ sw_status sw_plan_digest(sw_plan *h, uint64_t *digest);
  * ready_us may be NULL or point to S entries (scene ready times R_s). */
 sw_status sw_plan_detail(sw_plan *h, uint64_t index, sw_selection *out, uint64_t *ready_us);
 
-/* Zero-copy view of this rank's records: device pointer, count and the global
- * index of each segment's first record (segments = eval calls on this rank). */
+/* Zero-copy view of this rank's records: the device pointer of the record buffer and
+ * *n = the record SLOTS in use.  Records are stored in a TILED layout: an
+ * eval call (a "segment", see sw_plan_segments) covers whole tiles of 32 rows of `row`
+ * candidates; the record of global index i = H * row + j (row H, in-row offset j) of a
+ * segment sits at slot  offset + ((H / 32 - tile0) * row + j) * 32 + H % 32.  Slots of a
+ * segment's first / last tile outside [shard_begin, shard_end) are padding (undefined). */
 sw_status sw_plan_records(const sw_plan *h, const sw_record **dev_ptr, uint64_t *n);
+
+/* Segment table of this rank's records (one entry per eval call since create/reset/
+ * release), for consumers of the zero-copy view.  Two-call idiom as sw_pareto_get. */
+typedef struct {
+    uint64_t global_begin, global_end;  /* the eval call's global range */
+    uint64_t shard_begin, shard_end;    /* this rank's candidates of it */
+    uint64_t offset;                    /* record slot of the segment's first tile */
+    uint64_t tile0, ntiles;             /* tiles of 32 rows covering the shard */
+    uint64_t row;                       /* candidates per row */
+} sw_segment;
+sw_status sw_plan_segments(const sw_plan *h, sw_segment *out, uint64_t cap, uint64_t *n_out);
+
+/* Host helper: the digit (choice index within its digit's list) of candidate `index`
+ * for every scene, choice_per_scene[S] (a static intro scene gets 0).  Mixed-radix,
+ * MSD = earliest block (R19).  EINVAL if index >= N.  No device work. */
+sw_status sw_plan_decode(const sw_plan *h, uint64_t index, uint8_t *choice_per_scene);
 /* Copy n records starting at GLOBAL index `index` (must lie in one evaluated local
  * segment) into host memory. */
 sw_status sw_plan_copy_records(sw_plan *h, uint64_t index, uint64_t n, sw_record *host_out);
@@ -358,7 +382,17 @@ sw_status sw_plan_row_size(const sw_plan *h, uint64_t *row);
 sw_status sw_comm_unique_id(void *id128);
 sw_status sw_comm_init(const void *id128, int32_t rank, int32_t nranks, int32_t device,
                        void **comm_out);
+/* Destroys an NCCL communicator of sw_comm_init (one the library aborted after
+ * SW_ENCCL is only forgotten) or a loopback rank (the group goes with its last rank). */
 sw_status sw_comm_destroy(void *comm);
+/* TEST/EMULATION: an in-process loopback group of nranks ranks.  comms_out[r] is passed
+ * as sw_runtime.nccl_comm of rank r's handle (rank = r, nranks = nranks); each rank is
+ * driven by its own host thread making the same call sequence, and all ranks may live on
+ * ONE device (NCCL refuses duplicate GPUs).  The collectives (allgather / allreduce) are
+ * enqueued on each handle's stream with NCCL's ordering (peers' send buffers are read
+ * after the work that wrote them; later writes wait for the peers' copies), so the
+ * multi-rank device merge path runs unchanged.  Destroy each rank with sw_comm_destroy. */
+sw_status sw_comm_loopback_create(int32_t nranks, void **comms_out);
 
 /* ---- diagnostics ------------------------------------------------------------ */
 const char *sw_status_str(sw_status s);

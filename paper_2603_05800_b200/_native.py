@@ -140,7 +140,11 @@ EXPORTS = {
     "sw_plan_last_eval_ms": (C.c_int32, [C.c_void_p, C.POINTER(C.c_float)]),
     "sw_plan_kernel_time": (C.c_int32, [C.c_void_p, C.c_uint32, U64P, C.POINTER(C.c_double), U64P]),
     "sw_abi_version": (C.c_int32, []),
+    "sw_plan_decode": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint8)]),
+    "sw_plan_segments": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, U64P]),
+    "sw_comm_loopback_create": (C.c_int32, [C.c_int32, C.POINTER(C.c_void_p)]),
 }
+ABI_VERSION = 4
 
 _lib = None
 
@@ -158,11 +162,17 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError("libsw_plan.so not built: run `python -c 'import __graft_entry__ as g; "
                               "g.build()'` (nvcc, sm_100a)")
+        from . import build as _build
+        if _build.needs_build():
+            raise ImportError("libsw_plan.so is stale (built from other sources than csrc/ + include/): "
+                              "rebuild with `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in EXPORTS.items():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.sw_abi_version() != ABI_VERSION:
+            raise ImportError("libsw_plan.so ABI %d, binding expects %d" % (L.sw_abi_version(), ABI_VERSION))
         _lib = L
     return _lib
 
@@ -234,6 +244,20 @@ def comm_init(uid: bytes, rank: int, nranks: int, device: int) -> int:
 
 def comm_destroy(comm: int) -> None:
     _check(lib().sw_comm_destroy(C.c_void_p(comm)))
+
+
+def comm_loopback_create(nranks: int) -> List[int]:
+    """Test/emulation: an in-process loopback group of nranks ranks (sw_comm_loopback_create);
+    pass comms[r] as the comm of rank r's handle, one host thread per rank."""
+    arr = (C.c_void_p * nranks)()
+    _check(lib().sw_comm_loopback_create(nranks, arr))
+    return [arr[r] for r in range(nranks)]
+
+
+class sw_segment(C.Structure):
+    _fields_ = [("global_begin", C.c_uint64), ("global_end", C.c_uint64), ("shard_begin", C.c_uint64),
+                ("shard_end", C.c_uint64), ("offset", C.c_uint64), ("tile0", C.c_uint64),
+                ("ntiles", C.c_uint64), ("row", C.c_uint64)]
 
 
 @dataclass
@@ -439,6 +463,20 @@ class Plan:
         buf = (sw_record * max(1, n))()
         self._ck(lib().sw_plan_copy_records(self.h, index, n, buf))
         return buf
+
+    def decode(self, index: int) -> List[int]:
+        """Digit (choice within its digit) of every scene of candidate `index` (sw_plan_decode)."""
+        out = (C.c_uint8 * max(1, self.S))()
+        self._ck(lib().sw_plan_decode(self.h, index, out))
+        return list(out)[: self.S]
+
+    def segments(self):
+        """This rank's segment table (sw_plan_segments) as a list of dicts."""
+        n = C.c_uint64()
+        self._ck(lib().sw_plan_segments(self.h, None, 0, C.byref(n)))
+        buf = (sw_segment * max(1, n.value))()
+        self._ck(lib().sw_plan_segments(self.h, buf, n.value, C.byref(n)))
+        return [{k: getattr(x, k) for k, _ in sw_segment._fields_} for x in buf[: n.value]]
 
     def records_view(self):
         p = C.c_void_p()

@@ -709,6 +709,28 @@ struct ParetoCtl {
     unsigned long long dlt_pass;  // diagnostics: records the DLT did not rule out (all passes)
 };
 
+// Per-call status words of a multi-rank call, max-reduced over the ranks BEFORE any rank
+// takes a branch that involves another collective (a rank-local decision next to a
+// collective hangs or mispairs the peers): [0] a filter pass of this call overflowed its
+// survivor buffer (refold + exact front redo), [1] the front overflowed its capacity,
+// [2] a stream query's candidate list overflowed, [3] a host-side error of this rank,
+// [4] the call's argument fingerprint and [5] its complement (after the max-reduction
+// max(fp) == ~max(~fp) iff every rank made the same call with the same arguments).
+constexpr uint32_t kStatusWords = 6;
+__global__ void status_words_kernel(const ParetoCtl* __restrict__ ctl, const uint32_t* __restrict__ cand_n,
+                                    uint32_t nq, uint32_t cap, uint64_t host_flag, uint64_t fp,
+                                    uint64_t* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint64_t over = 0;
+    for (uint32_t q = 0; q < nq; q++) over |= cand_n[q] > cap ? 1ull : 0ull;
+    out[0] = ctl->surv_overflow ? 1ull : 0ull;
+    out[1] = ctl->front_overflow ? 1ull : 0ull;
+    out[2] = over;
+    out[3] = host_flag;
+    out[4] = fp;
+    out[5] = ~fp;
+}
+
 // keep[x] = no other point of pts[0,m) dominates x.  O(m^2), tiles through smem.
 __global__ void __launch_bounds__(kScanThreads) pareto_mark_kernel(const PPoint* __restrict__ pts,
                                                                    const uint32_t* __restrict__ d_m,
@@ -1330,10 +1352,26 @@ __device__ __forceinline__ uint64_t qc_key(const Rec4& r) {
     return ((uint64_t)rec_Q(r) << 32) | (uint64_t)(~c32);
 }
 
+// COST_X_TTFF prefilter key: ~min(cost x ttff_eff, 2^64 - 1) -- higher is better; a
+// record whose key is below the best feasible record's has a strictly larger product.
+__device__ __forceinline__ uint64_t cxt_key(const Rec4& r) {
+    const uint64_t t = r.w0 + r.w1;
+    return __umul64hi(r.w2, t) ? 0ull : ~(r.w2 * t);
+}
+// The objective's prefilter key (OBJ 0 / 1 compile-time, -1: runtime obj_q -- fleets).
+template <int OBJ>
+__device__ __forceinline__ uint64_t obj_key(bool obj_q, const Rec4& r) {
+    if (OBJ == 0) return qc_key(r);
+    if (OBJ == 1) return cxt_key(r);
+    return obj_q ? qc_key(r) : cxt_key(r);
+}
+
 // Select predicate of kRPT records for one query: bit u set iff record u is valid,
-// feasible (only the bounds in AM are compared) and, under QUALITY_FIRST, its packed key
-// is >= the block's best feasible key thr (thr == 0: none yet, every key passes).
-template <int AM>
+// feasible (only the bounds in AM are compared) and its objective prefilter key (packed
+// (Q, ~cost) under QUALITY_FIRST, ~sat(cost x ttff_eff) under COST_X_TTFF) is >= the
+// block's best feasible key thr (thr == 0: none yet, every key passes).  Ties pass: they
+// are settled by the full total order.
+template <int AM, int OBJ>
 __device__ __forceinline__ uint32_t pred_pass(const Rec4 (&r)[kRPT], const bool (&valid)[kRPT],
                                               unsigned long long thr, bool obj_q,
                                               uint64_t slo_t, uint64_t slo_s, uint64_t bud) {
@@ -1344,7 +1382,7 @@ __device__ __forceinline__ uint32_t pred_pass(const Rec4 (&r)[kRPT], const bool 
         if (AM & 1) f &= r[u].w0 <= slo_t;
         if (AM & 2) f &= r[u].w1 <= slo_s;
         if (AM & 4) f &= r[u].w2 <= bud;
-        f &= !obj_q | (qc_key(r[u]) >= thr);
+        f &= obj_key<OBJ>(obj_q, r[u]) >= thr;
         need |= (uint32_t)f << u;
     }
     return need;
@@ -1356,7 +1394,9 @@ struct ScanJob {
     SelParams P;
 };
 
-template <int NQ, bool PARETO>
+// OBJ: the handle's objective at compile time (0 QUALITY_FIRST, 1 COST_X_TTFF) or -1 =
+// per request at run time (fleet scans, whose requests may differ).
+template <int NQ, bool PARETO, int OBJ>
 __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParams P, Cand* __restrict__ partial,
                                                              ParetoArgs pa, const ScanJob* __restrict__ jobs) {
     if (jobs) {  // fleet: request y (never with PARETO)
@@ -1378,8 +1418,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     constexpr int NS = kCW * WS;
     __shared__ __align__(8) uint64_t full_bar[NS];
     __shared__ StageMeta meta[NS];
-    // per query: packed key (Q << 32 | ~min(cost, 2^32-1)) of this block's best FEASIBLE
-    // record under QUALITY_FIRST (any nonzero value under COST_X_TTFF); 0 = none yet
+    // per query: the objective prefilter key (obj_key) of this block's best FEASIBLE
+    // record: Q << 32 | ~min(cost, 2^32-1) (QUALITY_FIRST) or ~sat(cost x ttff_eff)
+    // (COST_X_TTFF); 0 = none yet
     __shared__ unsigned long long s_thr[NQA];
     // per query, while no feasible record is known: the smallest startup+stall violation
     // V_t of any closest-tier best in this block (records with a larger V_t cannot win)
@@ -1556,7 +1597,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
             // the warp has the stage in registers: lane 0 refills the slot
             __syncwarp();
             if (lane == 0) issue(st);
-            const bool obj_q = P.objective == 0;
+            const bool obj_q = OBJ >= 0 ? OBJ == 0 : P.objective == 0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
                 // predicate pass (branch-free, bitwise): which records can still beat this
@@ -1573,14 +1614,14 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 // only the bounds the query actually sets are compared (uniform dispatch)
                 uint32_t need;
                 switch (amask[q]) {
-                    case 0: need = pred_pass<0>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
-                    case 1: need = pred_pass<1>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
-                    case 2: need = pred_pass<2>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
-                    case 3: need = pred_pass<3>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
-                    case 4: need = pred_pass<4>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
-                    case 5: need = pred_pass<5>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
-                    case 6: need = pred_pass<6>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
-                    default: need = pred_pass<7>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 0: need = pred_pass<0, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 1: need = pred_pass<1, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 2: need = pred_pass<2, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 3: need = pred_pass<3, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 4: need = pred_pass<4, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 5: need = pred_pass<5, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    case 6: need = pred_pass<6, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
+                    default: need = pred_pass<7, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
                 }
                 if (__any_sync(0xffffffffu, !anyf)) {  // closest tier still open somewhere
                     const unsigned long long vmax = s_vt[q];
@@ -1601,7 +1642,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                             br[q] = r[u];
                             if (f) {
                                 if (!bf[q] && pa.gfeas) atomicOr(&pa.gfeas[q], 1u);
-                                atomicMax(&s_thr[q], obj_q ? (unsigned long long)qc_key(r[u]) : 1ull);
+                                atomicMax(&s_thr[q], (unsigned long long)obj_key<OBJ>(obj_q, r[u]));
                             } else {
                                 atomicMin(&s_vt[q], (unsigned long long)(sat_sub(r[u].w0, P.q[q].slo_t) +
                                                                          sat_sub(r[u].w1, P.q[q].slo_s)));

@@ -18,6 +18,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "sw_coll.cuh"
 #include "sw_kernels.cuh"
 #include "sw_plan.h"
 
@@ -42,6 +43,7 @@ struct sw_plan {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     ncclComm_t comm = nullptr;
+    LoopComm* loop = nullptr;  // in-process loopback rank (tests), instead of comm
     int rank = 0, nranks = 1;
     sw_alloc_fn alloc = nullptr;
     sw_free_fn free_fn = nullptr;
@@ -76,6 +78,7 @@ struct sw_plan {
     PPoint* d_tmp2 = nullptr;    // front_cap + surv_cap (block-local fronts)
     PPoint* d_surv = nullptr;    // surv_cap survivors of filter passes
     bool fuse_pareto = true;     // fold unfolded segments inside select scans
+    bool cxt_front_ok = false;   // COST_X_TTFF: every record has cost > 0 and ttff_eff > 0 (R35)
     uint64_t chunk = 1ull << 25; // records per fold chunk (the front improves per chunk)
     uint64_t fold_passes = 0;    // diagnostics: filter passes run
     uint64_t epoch = 1;          // bumped by every change of records or front
@@ -162,6 +165,31 @@ sw_status fail(sw_plan* h, sw_status s, const char* fmt, ...) {
         ncclResult_t r_ = (call);                                                             \
         if (r_ != ncclSuccess)                                                                \
             return fail((h), SW_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_));        \
+    } while (0)
+
+// The handle's collective context (NCCL or loopback) on its stream.
+Coll coll_of(const sw_plan* h) {
+    Coll c;
+    c.nccl = h->comm;
+    c.loop = h->loop;
+    c.stream = h->stream;
+    c.rank = h->rank;
+    c.nranks = h->nranks;
+    return c;
+}
+
+// a10 collectives and the stream wait of collective calls (async NCCL errors, timeout)
+#define CKC(h, call)                                                                           \
+    do {                                                                                       \
+        const char* why_ = "";                                                                 \
+        sw_status s_ = (call);                                                                 \
+        if (s_ != SW_OK) return fail((h), s_, "%s failed: %s (%s:%d)", #call, why_, __FILE__, __LINE__); \
+    } while (0)
+#define SYNC(h)                                                                               \
+    do {                                                                                      \
+        const char* why_ = "";                                                                \
+        sw_status s_ = coll_sync(coll_of(h), &why_);                                          \
+        if (s_ != SW_OK) return fail((h), s_, "stream synchronisation failed: %s (%s:%d)", why_, __FILE__, __LINE__); \
     } while (0)
 
 void* dev_alloc(sw_plan* h, size_t bytes) {
@@ -336,10 +364,15 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (rt->nranks < 1 || rt->rank < 0 || rt->rank >= rt->nranks)
         return fail(nullptr, SW_EINVAL, "bad rank %d of %d", rt->rank, rt->nranks);
     if (rt->nranks > 1 && !rt->nccl_comm) return fail(nullptr, SW_EINVAL, "nranks > 1 needs nccl_comm");
+    if (LoopComm* lc = as_loop(rt->nccl_comm))
+        if (lc->g->n != rt->nranks || lc->rank != rt->rank)
+            return fail(nullptr, SW_EINVAL, "loopback communicator is rank %d of %d, runtime says %d of %d", lc->rank,
+                        lc->g->n, rt->rank, rt->nranks);
 
     sw_plan* h = new sw_plan();
     h->device = rt->device;
-    h->comm = (ncclComm_t)rt->nccl_comm;
+    h->loop = as_loop(rt->nccl_comm);
+    h->comm = h->loop ? nullptr : (ncclComm_t)rt->nccl_comm;
     h->rank = rt->rank;
     h->nranks = rt->nranks;
     h->alloc = rt->alloc;
@@ -348,6 +381,15 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     h->NP = NP;
     h->S = S;
     h->B_user = B;
+    {  // R35: cost >= fixed cost > 0; ttff_eff >= ttff = R_0 > 0 (a static intro's ready
+       // time; else a_0 = overhead + llm_0 + tts_0, plus t >= 1 for a video choice)
+        bool t_pos = s0 ? sc->static_ready_us > 0 : sc->overhead_us + sc->llm_us[0] + sc->tts_us[0] > 0;
+        if (!s0 && !t_pos) {
+            t_pos = true;  // scene 0 lies in digit 0's block: every choice must run a video stage
+            for (uint32_t c = 0; c < tb->radix[0]; c++) t_pos &= tb->choices[c].degree > 0;
+        }
+        h->cxt_front_ok = pr->fixed_cost_mc > 0 && t_pos;
+    }
     h->N = N;
     auto bail = [&](sw_status s) {
         sw_plan_destroy(h);
@@ -554,6 +596,12 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
     if (const char* ev = getenv("SW_COOP_REDUCE")) h->coop_reduce = atoi(ev) != 0;
+    if (const char* ev = getenv("SW_SURV_CAP")) {  // test hook: "<cap>[@<rank>]" (>= 256)
+        char* end = nullptr;
+        const uint64_t c = strtoull(ev, &end, 10);
+        const int only = (end && *end == '@') ? atoi(end + 1) : -1;
+        if (c >= 256 && (only < 0 || only == h->rank)) h->surv_cap = c;
+    }
     {  // the cooperative merge needs all its blocks co-resident
         int occ = 0, coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
@@ -608,8 +656,9 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     }
     if ((st = alloc_n(h, &h->d_digest, 1, "digest")) < 0) return bail(st);
     // [0, R) gathered counts, [R] mine, [R+1] saved local front size, [R+2] merged size,
-    // [R+3] pad overflow flag of the asynchronous merge
-    if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 4, "counts")) < 0) return bail(st);
+    // [R+3] pad overflow flag of the asynchronous merge, [R+4, R+4+kStatusWords) the
+    // max-reduced status words of a multi-rank call
+    if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 4 + kStatusWords, "counts")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_gfeas, SW_MAX_QUERIES, "select flags")) < 0) return bail(st);
     if ((st = alloc_n(h, &h->d_greedy, 1, "greedy result")) < 0) return bail(st);
     h->level_score.assign(tb->level_score, tb->level_score + tb->n_levels);
@@ -853,7 +902,7 @@ static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint
     CKL(h);
     DetailOut d;
     CK(h, cudaMemcpyAsync(&d, h->d_detail, sizeof d, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     detail_to_selection(h, index, d, out, ready);
     return SW_OK;
 }
@@ -879,21 +928,24 @@ static void detail_to_selection(const sw_plan* h, uint64_t index, const DetailOu
 template <int NQ, bool PARETO>
 static void launch_scan(uint32_t grid, size_t smem, cudaStream_t st, const SegView& v, const SelParams& P,
                         Cand* partial, const ParetoArgs& pa) {
-    scan_kernel<NQ, PARETO><<<grid, kScanBlock, smem, st>>>(v, P, partial, pa, nullptr);
+    if (P.objective) scan_kernel<NQ, PARETO, 1><<<grid, kScanBlock, smem, st>>>(v, P, partial, pa, nullptr);
+    else scan_kernel<NQ, PARETO, 0><<<grid, kScanBlock, smem, st>>>(v, P, partial, pa, nullptr);
 }
 
+// Scan kernels are specialised for NQ in {0, 1, 2, 4, 8} queries: a batch of another size
+// runs with the next larger NQ, the extra slots holding copies of its last query (their
+// partial winners are never read).
 template <bool PARETO>
 static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t st, const SegView& v,
-                           const SelParams& P, Cand* partial, const ParetoArgs& pa) {
-    switch (nq) {
+                           const SelParams& P0, Cand* partial, const ParetoArgs& pa) {
+    SelParams P = P0;
+    const uint32_t nqs = nq <= 2 ? nq : nq <= 4 ? 4 : 8;
+    for (uint32_t j = nq; j < nqs; j++) P.q[j] = P.q[nq - 1];
+    switch (nqs) {
         case 0: launch_scan<0, PARETO>(grid, smem, st, v, P, partial, pa); break;
         case 1: launch_scan<1, PARETO>(grid, smem, st, v, P, partial, pa); break;
         case 2: launch_scan<2, PARETO>(grid, smem, st, v, P, partial, pa); break;
-        case 3: launch_scan<3, PARETO>(grid, smem, st, v, P, partial, pa); break;
         case 4: launch_scan<4, PARETO>(grid, smem, st, v, P, partial, pa); break;
-        case 5: launch_scan<5, PARETO>(grid, smem, st, v, P, partial, pa); break;
-        case 6: launch_scan<6, PARETO>(grid, smem, st, v, P, partial, pa); break;
-        case 7: launch_scan<7, PARETO>(grid, smem, st, v, P, partial, pa); break;
         default: launch_scan<8, PARETO>(grid, smem, st, v, P, partial, pa); break;
     }
 }
@@ -901,18 +953,18 @@ static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t
 static constexpr size_t kScanSmemPareto = ring_bytes(true) + sizeof(Dlt) + (kFrontSmem + kBlockSurv) * sizeof(PPoint);
 static constexpr size_t kRingBytes = ring_bytes(false);
 
-template <int NQ>
+template <int NQ, int OBJ>
 static cudaError_t set_attr_one() {
-    cudaError_t a = cudaFuncSetAttribute(scan_kernel<NQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t a = cudaFuncSetAttribute(scan_kernel<NQ, true, OBJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kScanSmemPareto);
-    cudaError_t b = cudaFuncSetAttribute(scan_kernel<NQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t b = cudaFuncSetAttribute(scan_kernel<NQ, false, OBJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kRingBytes);
     if (a != cudaSuccess) return a;
     if (b != cudaSuccess) return b;
-    // the persistent scan needs one resident block per SM (registers x 544 threads + smem)
+    // the persistent scan needs one resident block per SM (registers x 512 threads + smem)
     int o1 = 0, o2 = 0;
-    a = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, scan_kernel<NQ, true>, kScanBlock, kScanSmemPareto);
-    b = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, scan_kernel<NQ, false>, kScanBlock, kRingBytes);
+    a = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, scan_kernel<NQ, true, OBJ>, kScanBlock, kScanSmemPareto);
+    b = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, scan_kernel<NQ, false, OBJ>, kScanBlock, kRingBytes);
     if (a != cudaSuccess) return a;
     if (b != cudaSuccess) return b;
     return (o1 < 1 || o2 < 1) ? cudaErrorLaunchOutOfResources : cudaSuccess;
@@ -920,11 +972,15 @@ static cudaError_t set_attr_one() {
 
 static cudaError_t set_scan_smem_attrs() {
     cudaError_t e = cudaSuccess;
-    cudaError_t r[] = {set_attr_one<0>(), set_attr_one<1>(), set_attr_one<2>(), set_attr_one<3>(), set_attr_one<4>(),
-                       set_attr_one<5>(), set_attr_one<6>(), set_attr_one<7>(), set_attr_one<8>()};
+    cudaError_t r[] = {set_attr_one<0, 0>(), set_attr_one<1, 0>(), set_attr_one<2, 0>(), set_attr_one<4, 0>(),
+                       set_attr_one<8, 0>(), set_attr_one<0, 1>(), set_attr_one<1, 1>(), set_attr_one<2, 1>(),
+                       set_attr_one<4, 1>(), set_attr_one<8, 1>()};
     for (cudaError_t x : r)
         if (x != cudaSuccess) e = x;
-    return e;
+    // fleet scans: one query per request, objective per request at run time
+    cudaError_t f = cudaFuncSetAttribute(scan_kernel<1, false, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kRingBytes);
+    return f != cudaSuccess ? f : e;
 }
 
 static ParetoArgs pareto_args(sw_plan* h) {
@@ -1054,7 +1110,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         if (h->debug) {  // diagnostics only: synchronises every pass
             ParetoCtl c;
             CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
-            CK(h, cudaStreamSynchronize(h->stream));
+            SYNC(h);
             fprintf(stderr, "[sw] dlt passed %llu records so far\n", (unsigned long long)c.dlt_pass);
             fprintf(stderr, "[sw] fold pass %llu: stride pass %u, %llu records, survivors %llu merge-in %u local %u/%u front %llu"
                             " | merge phases us: init %.1f local %.1f mark %.1f compact %.1f rank(b0) %.1f\n",
@@ -1073,7 +1129,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
 static sw_status sync_ctl(sw_plan* h, bool* overflow) {
     ParetoCtl c;
     CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     if (c.front_overflow) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
     h->front_n = c.front_n;
     *overflow = c.surv_overflow != 0;
@@ -1103,8 +1159,8 @@ static sw_status global_front_async(sw_plan* h, const PPoint** res, const uint64
     ParetoCtl* c = h->d_ctl;
     CK(h, cudaMemcpyAsync(h->d_counts + R, &c->front_n, 8, cudaMemcpyDeviceToDevice, h->stream));
     CK(h, cudaMemcpyAsync(h->d_counts + R + 1, &c->front_n, 8, cudaMemcpyDeviceToDevice, h->stream));
-    CKN(h, ncclAllGather(h->d_counts + R, h->d_counts, 1, ncclUint64, h->comm, h->stream));
-    CKN(h, ncclAllGather(h->d_front, h->d_gather, (size_t)kMergePad * sizeof(PPoint), ncclUint8, h->comm, h->stream));
+    CKC(h, coll_allgather(coll_of(h), h->d_counts + R, h->d_counts, 8, &why_));
+    CKC(h, coll_allgather(coll_of(h), h->d_front, h->d_gather, (size_t)kMergePad * sizeof(PPoint), &why_));
     const uint64_t all = (uint64_t)kMergePad * R;
     front_gather_pad_kernel<<<(uint32_t)((all + 255) / 256), 256, 0, h->stream>>>(
         h->d_gather, h->d_counts, R, kMergePad, h->d_work, c, h->d_counts + R + 3);
@@ -1139,7 +1195,7 @@ static sw_status front_answer(sw_plan* h, uint32_t nq, const sw_query* qs, sw_se
     DetailOut det[SW_MAX_QUERIES];
     CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nq, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nq, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     sw_status worst = SW_OK;
     for (uint32_t q = 0; q < nq; q++) {
         memset(&out[q], 0, sizeof(sw_selection));
@@ -1156,8 +1212,12 @@ static sw_status front_answer(sw_plan* h, uint32_t nq, const sw_query* qs, sw_se
 
 // A query is front-answerable (R30) when it bounds neither startup nor stall under the
 // QUALITY_FIRST objective (and the handle's front covers exactly its records).
+// Under COST_X_TTFF the same holds when every record has cost > 0 and ttff_eff > 0
+// (reading R35): then a dominating point has a strictly smaller cost x ttff_eff product
+// unless only its quality is better, which the key's -Q breaks in its favour.
 static bool front_query(const sw_plan* h, const sw_query& q) {
-    return h->fuse_pareto && !(h->h.flags & 4u) && q.slo_startup_us == UINT64_MAX && q.slo_stall_us == UINT64_MAX;
+    return h->fuse_pareto && (!(h->h.flags & 4u) || h->cxt_front_ok) && q.slo_startup_us == UINT64_MAX &&
+           q.slo_stall_us == UINT64_MAX;
 }
 
 // Select over the held records.  Scan queries (S) ride on the fused select + Pareto-fold
@@ -1166,6 +1226,43 @@ static bool front_query(const sw_plan* h, const sw_query& q) {
 // merges, allgathers, every winner's detail -- is launched asynchronously and read back
 // with ONE synchronisation; a Pareto capacity overflow falls back to the synchronous
 // refold + front answer.  Collective when nranks > 1.
+// Fingerprint of a collective call's arguments (order-sensitive 64-bit mix): ranks that
+// disagree are detected by the status-word reduction and fail with SW_ESTATE together.
+static uint64_t fp_mix(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h * 0xff51afd7ed558ccdull;
+}
+static uint64_t call_fingerprint(const sw_plan* h, uint32_t kind, uint32_t nq, const sw_query* qs, uint64_t a,
+                                 uint64_t b) {
+    uint64_t f = fp_mix(0x5357u, kind);
+    f = fp_mix(f, h->N);
+    f = fp_mix(f, nq);
+    for (uint32_t q = 0; q < nq; q++) {
+        f = fp_mix(f, qs[q].slo_startup_us);
+        f = fp_mix(f, qs[q].slo_stall_us);
+        f = fp_mix(f, qs[q].budget_mc);
+    }
+    f = fp_mix(f, a);
+    f = fp_mix(f, b);
+    for (const Segment& g : h->segs) {
+        f = fp_mix(f, g.gbegin);
+        f = fp_mix(f, g.gend);
+    }
+    return f;
+}
+
+// Launch the status words of this call and max-reduce them over the ranks (no-op at one
+// rank); the caller reads them back with its answers.
+static sw_status status_exchange(sw_plan* h, const uint32_t* cand_n, uint32_t nq, uint32_t cap, uint64_t host_flag,
+                                 uint64_t fp) {
+    if (h->nranks == 1) return SW_OK;
+    uint64_t* d_st = h->d_counts + h->nranks + 4;
+    status_words_kernel<<<1, 1, 0, h->stream>>>(h->d_ctl, cand_n, nq, cap, host_flag, fp, d_st);
+    CKL(h);
+    CKC(h, coll_allreduce_u64(coll_of(h), d_st, kStatusWords, 1, &why_));
+    return SW_OK;
+}
+
 static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out, bool allow_front) {
     uint32_t fi[SW_MAX_QUERIES], si[SW_MAX_QUERIES], nf = 0, ns = 0;
     for (uint32_t q = 0; q < nq; q++) {
@@ -1225,13 +1322,16 @@ static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_sel
         select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_partial, np, PS, h->d_cand);
         CKL(h);
         if (h->nranks > 1) {  // a10: allgather per-rank winners over NVLink, replicated merge
-            CKN(h, ncclAllGather(h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, ncclUint8, h->comm,
-                                 h->stream));
+            CKC(h, coll_allgather(coll_of(h), h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, &why_));
             select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_cand_all, (uint32_t)h->nranks, PS, h->d_cand);
             CKL(h);
         }
     }
     trace_mark(h, "select");
+    {
+        sw_status st = status_exchange(h, nullptr, 0, 0, 0, call_fingerprint(h, 1, nq, qs, allow_front, 0));
+        if (st < 0) return st;
+    }
     bool merged_now = false;
     if (nf) {
         const PPoint* fr = nullptr;
@@ -1252,26 +1352,35 @@ static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_sel
     Cand win[SW_MAX_QUERIES];
     DetailOut det[SW_MAX_QUERIES];
     ParetoCtl cc;
-    uint64_t aux[2] = {0, 0};  // merged front size, pad overflow
+    // merged front size, pad overflow, then the max-reduced status words (multi-rank)
+    uint64_t aux[2 + kStatusWords] = {};
     CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nw, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nw, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaMemcpyAsync(&cc, h->d_ctl, sizeof cc, cudaMemcpyDeviceToHost, h->stream));
     if (h->nranks > 1)
-        CK(h, cudaMemcpyAsync(aux, h->d_counts + h->nranks + 2, 16, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaMemcpyAsync(aux, h->d_counts + h->nranks + 2, sizeof aux, cudaMemcpyDeviceToHost, h->stream));
     trace_mark(h, "answers");
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     trace_dump(h, "select");
-    if (cc.front_overflow) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
+    // every branch below that leads to another collective is taken on the status words
+    // reduced over ALL ranks, so the ranks stay in step (a rank-local overflow would
+    // otherwise send only that rank into the exact front redo's collectives)
+    const uint64_t* gst = aux + 2;
+    const bool g_surv = h->nranks > 1 ? gst[0] != 0 : cc.surv_overflow != 0;
+    const bool g_front = h->nranks > 1 ? gst[1] != 0 : cc.front_overflow != 0;
+    if (h->nranks > 1 && gst[4] != ~gst[5])
+        return fail(h, SW_ESTATE, "ranks made different select calls (arguments or evaluated ranges differ)");
+    if (g_front) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
     h->front_n = cc.front_n;
     bool redo_front = false;
-    if (cc.surv_overflow) {  // a filter pass overflowed: the front is valid but incomplete
+    if (cc.surv_overflow) {  // a local filter pass overflowed: the local front is valid but incomplete
         CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
         for (size_t x : fused) h->segs[x].folded = false;
-        redo_front = nf > 0;
     }
+    if (g_surv) redo_front = nf > 0;  // some rank's front is incomplete: every rank redoes
     if (merged_now) {
         if (aux[1]) redo_front = nf > 0;  // some rank's front exceeded the pad
-        else if (!cc.surv_overflow) {
+        else if (!g_surv) {
             h->merged_epoch = h->epoch;
             h->merged_n = aux[0];
         }
@@ -1456,6 +1565,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
     uint64_t b, e;
     if ((st = sw_shard_range(begin, end, h->row, h->rank, h->nranks, &b, &e)) < 0) return st;
     trace_mark(h, "start");
+    uint64_t host_err = 0;
     CK(h, cudaMemsetAsync(h->d_scand_n, 0, sizeof(uint32_t) * SW_MAX_QUERIES, h->stream));
     CK(h, cudaMemsetAsync(h->d_skey, 0, sizeof(unsigned long long) * 3 * SW_MAX_QUERIES, h->stream));
     if (e > b) {
@@ -1530,7 +1640,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
                 uint32_t cn[SW_MAX_QUERIES];
                 CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
                 CK(h, cudaMemcpyAsync(cn, h->d_scand_n, sizeof cn, cudaMemcpyDeviceToHost, h->stream));
-                CK(h, cudaStreamSynchronize(h->stream));
+                SYNC(h);
                 fprintf(stderr, "[sw] stream pass %u/%u: %llu tiles, survivors %llu front %llu, candidates reported",
                         lvl, K, (unsigned long long)ntp, (unsigned long long)c.surv, (unsigned long long)c.front_n);
                 for (uint32_t q = 0; q < ns; q++) fprintf(stderr, " %u", cn[q]);
@@ -1547,28 +1657,33 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
         // is exact -- a record already in the front is removed by its identical entry --
         // and its survivors shrink with the front; it is redone at once (one readback per
         // pass), before the next, larger pass would build on the weaker front.
-        for (uint32_t lvl = 0; lvl <= K; lvl++) {
+        // (passes are rank-local: a pass that still overflows after 8 re-runs only sets
+        // this rank's error flag; the ranks agree on the outcome after the collectives)
+        for (uint32_t lvl = 0; lvl <= K && !host_err; lvl++) {
             const uint64_t ntp = ntiles_of(lvl);
             if (ntp == 0) continue;
             for (int round = 0;; round++) {
                 if ((st = run_pass(lvl, ntp)) < 0) return st;
-                CK(h, cudaStreamSynchronize(h->stream));
+                SYNC(h);
                 if (h->h_pass_surv[lvl] <= h->surv_cap) break;
-                if (round == 8)
-                    return fail(h, SW_ERANGE, "stream pass survivors exceeded %llu after %d re-runs: use sw_plan_sweep",
-                                (unsigned long long)h->surv_cap, round);
+                if (round == 8) {
+                    host_err = 1;
+                    break;
+                }
                 CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
             }
         }
     }
     h->released = true;  // the front now covers candidates without records
+    if ((st = status_exchange(h, h->d_scand_n, ns, h->scand_cap, host_err,
+                              call_fingerprint(h, 2, nq, qs, begin, end))) < 0)
+        return st;
     if (ns) {
         stream_select_final_kernel<<<ns, kScanThreads, 0, h->stream>>>(h->d_scand, h->d_scand_n, h->scand_cap, PS,
                                                                       h->d_cand);
         CKL(h);
         if (h->nranks > 1) {  // a10: allgather per-rank winners, replicated merge
-            CKN(h, ncclAllGather(h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, ncclUint8, h->comm,
-                                 h->stream));
+            CKC(h, coll_allgather(coll_of(h), h->d_cand, h->d_cand_all, sizeof(Cand) * SW_MAX_QUERIES, &why_));
             select_final_kernel<<<1, kScanThreads, 0, h->stream>>>(h->d_cand_all, (uint32_t)h->nranks, PS, h->d_cand);
             CKL(h);
         }
@@ -1593,28 +1708,37 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
     DetailOut det[SW_MAX_QUERIES];
     uint32_t cn[SW_MAX_QUERIES];
     ParetoCtl cc;
-    uint64_t aux[2] = {0, 0};
+    uint64_t aux[2 + kStatusWords] = {};  // merged front size, pad overflow, status words
     if (nw) {
         CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nw, cudaMemcpyDeviceToHost, h->stream));
         CK(h, cudaMemcpyAsync(det, h->d_detail, sizeof(DetailOut) * nw, cudaMemcpyDeviceToHost, h->stream));
     }
     CK(h, cudaMemcpyAsync(cn, h->d_scand_n, sizeof cn, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaMemcpyAsync(&cc, h->d_ctl, sizeof cc, cudaMemcpyDeviceToHost, h->stream));
-    if (h->nranks > 1 && merged_now)
-        CK(h, cudaMemcpyAsync(aux, h->d_counts + h->nranks + 2, 16, cudaMemcpyDeviceToHost, h->stream));
+    if (h->nranks > 1)
+        CK(h, cudaMemcpyAsync(aux, h->d_counts + h->nranks + 2, sizeof aux, cudaMemcpyDeviceToHost, h->stream));
     trace_mark(h, "answers");
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     trace_dump(h, "stream");
-    if (cc.front_overflow) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
-    h->front_n = cc.front_n;
-    if (cc.surv_overflow) {
-        CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
-        return fail(h, SW_ERANGE, "stream pass survivors exceeded %llu: use sw_plan_sweep",
-                    (unsigned long long)h->surv_cap);
+    // the outcome is decided on the status words reduced over ALL ranks: every rank
+    // returns the same status (an error on one rank fails the call everywhere)
+    bool g_front = cc.front_overflow != 0, g_surv = cc.surv_overflow != 0 || host_err, g_cand = false;
+    for (uint32_t q = 0; q < ns; q++) g_cand |= cn[q] > h->scand_cap;
+    if (h->nranks > 1) {
+        const uint64_t* gst = aux + 2;
+        if (gst[4] != ~gst[5]) return fail(h, SW_ESTATE, "ranks made different stream calls");
+        g_front = gst[1] != 0;
+        g_surv = gst[0] != 0 || gst[3] != 0;
+        g_cand = gst[2] != 0;
     }
-    for (uint32_t q = 0; q < ns; q++)
-        if (cn[q] > h->scand_cap)
-            return fail(h, SW_ERANGE, "stream select candidates exceeded %u: use sw_plan_sweep", h->scand_cap);
+    h->front_n = cc.front_n;
+    if (cc.surv_overflow) CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
+    if (g_front) return fail(h, SW_ERANGE, "Pareto front exceeds %llu points", (unsigned long long)h->front_cap);
+    if (g_surv)
+        return fail(h, SW_ERANGE, "stream pass survivors exceeded %llu (on some rank): use sw_plan_sweep",
+                    (unsigned long long)h->surv_cap);
+    if (g_cand) return fail(h, SW_ERANGE, "stream select candidates exceeded %u (on some rank): use sw_plan_sweep",
+                            h->scand_cap);
     if (merged_now && !aux[1]) {
         h->merged_epoch = h->epoch;
         h->merged_n = aux[0];
@@ -1655,10 +1779,10 @@ extern "C" sw_status sw_plan_digest(sw_plan* h, uint64_t* digest) {
         CKL(h);
     }
     if (h->nranks > 1)
-        CKN(h, ncclAllReduce(h->d_digest, h->d_digest, 1, ncclUint64, ncclSum, h->comm, h->stream));
+        CKC(h, coll_allreduce_u64(coll_of(h), (uint64_t*)h->d_digest, 1, 0, &why_));
     unsigned long long v = 0;
     CK(h, cudaMemcpyAsync(&v, h->d_digest, sizeof v, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     *digest = v;
     return SW_OK;
 }
@@ -1708,17 +1832,17 @@ static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_ou
     } else if (h->nranks > 1) {  // a10: allgather counts, then padded fronts; exact merge
         uint64_t mine = h->front_n;
         CK(h, cudaMemcpyAsync(h->d_counts + h->nranks, &mine, 8, cudaMemcpyHostToDevice, h->stream));
-        CKN(h, ncclAllGather(h->d_counts + h->nranks, h->d_counts, 1, ncclUint64, h->comm, h->stream));
+        CKC(h, coll_allgather(coll_of(h), h->d_counts + h->nranks, h->d_counts, 8, &why_));
         std::vector<uint64_t> counts(h->nranks);
         CK(h, cudaMemcpyAsync(counts.data(), h->d_counts, 8 * h->nranks, cudaMemcpyDeviceToHost, h->stream));
-        CK(h, cudaStreamSynchronize(h->stream));
+        SYNC(h);
         uint64_t maxc = 1, tot = 0;
         for (uint64_t c : counts) {
             maxc = std::max(maxc, c);
             tot += c;
         }
         if (tot > h->front_cap + h->surv_cap) return fail(h, SW_ERANGE, "merged fronts too large");
-        CKN(h, ncclAllGather(h->d_front, h->d_gather, maxc * sizeof(PPoint), ncclUint8, h->comm, h->stream));
+        CKC(h, coll_allgather(coll_of(h), h->d_front, h->d_gather, maxc * sizeof(PPoint), &why_));
         const uint64_t all = maxc * (uint64_t)h->nranks;
         pareto_gather_kernel<<<(uint32_t)((all + 255) / 256), 256, 0, h->stream>>>(h->d_gather, h->d_counts,
                                                                                   h->nranks, maxc, h->d_work);
@@ -1739,7 +1863,7 @@ static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_ou
         CK(h, cudaMemcpyAsync(&h->d_ctl->front_n, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
         // the asynchronous path reads the cached merge's size from the device
         CK(h, cudaMemcpyAsync(h->d_counts + h->nranks + 2, &n, sizeof n, cudaMemcpyHostToDevice, h->stream));
-        CK(h, cudaStreamSynchronize(h->stream));
+        SYNC(h);
     }
     *res_out = res;
     *n_out = n;
@@ -1756,7 +1880,7 @@ extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t ca
     if (cap == 0) return SW_OK;
     if (cap < n) return SW_TRUNCATED;
     CK(h, cudaMemcpyAsync(out, res, n * sizeof(PPoint), cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     return SW_OK;
 }
 
@@ -1765,6 +1889,18 @@ extern "C" sw_status sw_plan_records(const sw_plan* h, const sw_record** dev_ptr
     if (!h || !dev_ptr || !n) return fail(nullptr, SW_EINVAL, "null argument");
     *dev_ptr = (const sw_record*)h->d_rec;
     *n = h->rec_used;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_plan_segments(const sw_plan* h, sw_segment* out, uint64_t cap, uint64_t* n_out) {
+    if (!h || !n_out || (cap && !out)) return fail(nullptr, SW_EINVAL, "null argument");
+    *n_out = h->segs.size();
+    if (cap == 0) return SW_OK;
+    if (cap < h->segs.size()) return SW_TRUNCATED;
+    for (size_t i = 0; i < h->segs.size(); i++) {
+        const Segment& g = h->segs[i];
+        out[i] = sw_segment{g.gbegin, g.gend, g.begin, g.end, g.offset, g.tile0, g.ntiles, h->row};
+    }
     return SW_OK;
 }
 
@@ -1814,7 +1950,7 @@ extern "C" sw_status sw_plan_greedy(sw_plan* h, uint64_t slo_startup_us, uint64_
     CKL(h);
     GreedyOut g;
     CK(h, cudaMemcpyAsync(&g, h->d_greedy, sizeof g, cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h);
     sw_status st = fill_detail(h, g.index, out, nullptr);
     if (st < 0) return st;
     out->status = g.feasible ? SW_OK : SW_CLOSEST;
@@ -1824,6 +1960,24 @@ extern "C" sw_status sw_plan_greedy(sw_plan* h, uint64_t slo_startup_us, uint64_
 }
 
 // ============================================================================ host helpers
+extern "C" sw_status sw_plan_decode(const sw_plan* h, uint64_t index, uint8_t* choice_per_scene) {
+    if (!h || !choice_per_scene) return fail(nullptr, SW_EINVAL, "null argument");
+    if (index >= h->N) return fail(nullptr, SW_EINVAL, "index %llu outside [0, %llu)", (unsigned long long)index,
+                                   (unsigned long long)h->N);
+    // mixed-radix digits, MSD = earliest block (R19); padded virtual digits have radix 1
+    const DevHeader& H = h->h;
+    uint64_t rem = index;
+    uint32_t dig[kMaxDigits] = {};
+    for (int b = (int)H.B - 1; b >= 0; b--) {
+        dig[b] = (uint32_t)(rem % H.radix[b]);
+        rem /= H.radix[b];
+    }
+    memset(choice_per_scene, 0, h->S);
+    for (uint32_t b = h->pad_digits; b < H.B; b++)
+        for (uint32_t s = H.first[b]; s < H.first[b + 1]; s++) choice_per_scene[s] = (uint8_t)dig[b];
+    return SW_OK;
+}
+
 extern "C" sw_status sw_space_shape(const sw_profile_tables* tb, uint64_t* n, uint64_t* row) {
     if (!tb || !n || !row || !tb->radix) return fail(nullptr, SW_EINVAL, "null argument");
     const uint32_t B = tb->n_digits;
@@ -1882,6 +2036,7 @@ struct sw_fleet {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     ncclComm_t comm = nullptr;
+    LoopComm* loop = nullptr;
     int rank = 0, nranks = 1;
     uint32_t np_max = 1;
     size_t eval_smem = 0;
@@ -1939,7 +2094,8 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
     if (n < 1 || n > SW_MAX_FLEET) return fail(nullptr, SW_EINVAL, "fleet size %u not in 1..%d", n, SW_MAX_FLEET);
     sw_fleet* f = new sw_fleet();
     f->device = rt->device;
-    f->comm = (ncclComm_t)rt->nccl_comm;
+    f->loop = as_loop(rt->nccl_comm);
+    f->comm = f->loop ? nullptr : (ncclComm_t)rt->nccl_comm;
     f->rank = rt->rank;
     f->nranks = rt->nranks;
     auto bail = [&](sw_status s) {
@@ -2057,7 +2213,7 @@ extern "C" sw_status sw_fleet_eval(sw_fleet* f) {
     CK(h, cudaSetDevice(f->device));
     std::vector<EvalJob> jobs(n);
     uint64_t max_tiles = 0, recs = 0;
-    for (uint32_t i = 0; i < n; i++) {
+    for (uint32_t i = 0; i < n; i++) {  // every request's capacity first: nothing changes on error
         sw_plan* p = f->plans[i];
         uint64_t b, e;
         sw_status st = sw_shard_range(0, p->N, p->row, p->rank, p->nranks, &b, &e);
@@ -2068,6 +2224,15 @@ extern "C" sw_status sw_fleet_eval(sw_fleet* f) {
         const uint64_t slots = m ? (t1 - t0) * kTileRows * p->row : 0;
         if (m > p->cand_cap || slots > p->rec_cap)
             return fail(h, SW_ERANGE, "request %u: records exceed its capacity", i);
+    }
+    for (uint32_t i = 0; i < n; i++) {
+        sw_plan* p = f->plans[i];
+        uint64_t b, e;
+        sw_shard_range(0, p->N, p->row, p->rank, p->nranks, &b, &e);
+        const uint64_t m = e - b;
+        const uint64_t rb = b / p->row, re = (e + p->row - 1) / p->row;
+        const uint64_t t0 = rb / kTileRows, t1 = (re + kTileRows - 1) / kTileRows;
+        const uint64_t slots = m ? (t1 - t0) * kTileRows * p->row : 0;
         p->segs.push_back(Segment{0, p->N, b, e, 0, t0, m ? t1 - t0 : 0, false});
         p->rec_used = slots;
         p->cand_used = m;
@@ -2114,7 +2279,7 @@ extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_se
     ParetoArgs pa{};
     pa.gfeas = f->d_gfeas;
     CK(h, cudaEventRecord(f->ev[2], f->stream));
-    scan_kernel<1, false><<<dim3(f->gx, n), kScanBlock, kRingBytes, f->stream>>>(SegView{}, SelParams{}, f->d_partial,
+    scan_kernel<1, false, -1><<<dim3(f->gx, n), kScanBlock, kRingBytes, f->stream>>>(SegView{}, SelParams{}, f->d_partial,
                                                                                 pa, f->d_sjobs);
     CKL(h);
     CK(h, cudaEventRecord(f->ev[3], f->stream));
@@ -2122,7 +2287,7 @@ extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_se
                                                            (uint64_t)f->gx * SW_MAX_QUERIES, f->d_sjobs, f->d_win);
     CKL(h);
     if (f->nranks > 1) {  // a10: one allgather of the n winners, replicated merge
-        CKN(h, ncclAllGather(f->d_win, f->d_win_all, sizeof(Cand) * SW_MAX_QUERIES * n, ncclUint8, f->comm, f->stream));
+        CKC(h, coll_allgather(coll_of(h), f->d_win, f->d_win_all, sizeof(Cand) * SW_MAX_QUERIES * n, &why_));
         select_merge_kernel<<<n, kScanThreads, 0, f->stream>>>(f->d_win_all, (uint32_t)f->nranks,
                                                                (uint64_t)n * SW_MAX_QUERIES, SW_MAX_QUERIES, f->d_sjobs,
                                                                f->d_win);
@@ -2139,7 +2304,7 @@ extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_se
     CK(h, cudaMemcpyAsync(det.data(), f->d_det, sizeof(DetailOut) * n, cudaMemcpyDeviceToHost, f->stream));
     sw_status st = fleet_harvest(f, SW_KERNEL_SCAN, slots * sizeof(Rec4));  // synchronises the scan
     if (st < 0) return st;
-    CK(h, cudaStreamSynchronize(f->stream));
+    SYNC(h);
     sw_status worst = SW_OK;
     for (uint32_t i = 0; i < n; i++) {
         const Cand& c = win[(size_t)i * SW_MAX_QUERIES];
@@ -2211,8 +2376,56 @@ extern "C" sw_status sw_comm_init(const void* id128, int32_t rank, int32_t nrank
     return SW_OK;
 }
 
+extern "C" sw_status sw_comm_loopback_create(int32_t nranks, void** comms_out) {
+    if (!comms_out || nranks < 1 || nranks > 1024) return fail(nullptr, SW_EINVAL, "bad loopback arguments");
+    LoopGroup* g = new LoopGroup();
+    g->n = g->alive = nranks;
+    g->send.assign(nranks, nullptr);
+    g->ready.assign(nranks, nullptr);
+    g->done.assign(nranks, nullptr);
+    for (int r = 0; r < nranks; r++) {
+        if (cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            for (cudaEvent_t e : g->ready)
+                if (e) cudaEventDestroy(e);
+            for (cudaEvent_t e : g->done)
+                if (e) cudaEventDestroy(e);
+            delete g;
+            return fail(nullptr, SW_ECUDA, "loopback: cudaEventCreate failed (no CUDA device?)");
+        }
+    }
+    std::lock_guard<std::mutex> lk(loop_registry_mu());
+    for (int r = 0; r < nranks; r++) {
+        LoopComm* c = new LoopComm{kLoopMagic, g, r};
+        loop_registry().insert(c);
+        comms_out[r] = c;
+    }
+    return SW_OK;
+}
+
 extern "C" sw_status sw_comm_destroy(void* comm) {
     if (!comm) return SW_OK;
+    if (LoopComm* lc = as_loop(comm)) {  // a loopback rank: the group goes with its last rank
+        LoopGroup* g = lc->g;
+        bool last = false;
+        {
+            std::lock_guard<std::mutex> lk(loop_registry_mu());
+            loop_registry().erase(comm);
+            last = --g->alive == 0;
+        }
+        delete lc;
+        if (last) {
+            for (cudaEvent_t e : g->ready) cudaEventDestroy(e);
+            for (cudaEvent_t e : g->done) cudaEventDestroy(e);
+            delete g;
+        }
+        return SW_OK;
+    }
+    {
+        std::lock_guard<std::mutex> lk(loop_registry_mu());
+        if (aborted_registry().erase(comm)) return SW_OK;  // already aborted by the library
+    }
     ncclResult_t r = ncclCommDestroy((ncclComm_t)comm);
     if (r != ncclSuccess) return fail(nullptr, SW_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
     return SW_OK;
@@ -2242,4 +2455,4 @@ extern "C" const char* sw_last_error(const sw_plan* h) {
 
 extern "C" uint64_t sw_plan_launch_count(const sw_plan* h) { return h ? h->launches : 0; }
 
-extern "C" int32_t sw_abi_version(void) { return 3; }  // 2: pool_ready_us; 3: evict_risk_permille
+extern "C" int32_t sw_abi_version(void) { return 4; }  // 2: pool_ready_us; 3: evict_risk_permille; 4: loopback, decode, segments

@@ -291,6 +291,13 @@ def make_config(name: str) -> Problem:
                       lambda p: [Query(60 * D, 0, 150 * DOLLAR),
                                  Query(600 * D, 1800 * D, 100 * DOLLAR),
                                  Query(INF, INF, 40 * DOLLAR)])
+    if name == "C2x":
+        # C2 under the paper's own objective, "We minimize cost x TTFF" (reading R13:
+        # COST_X_TTFF = (cost x ttff_eff as u128, -Q, index)), same space and queries.
+        pb = make_config("C2")
+        pb.name = "C2x"
+        pb.objective = 1
+        return pb
     if name == "C3w":
         # C3 with a cold H100 pool: its GPUs are free only after the model load + first
         # warm-up request, 30 s + 80 s (reading R31).

@@ -111,7 +111,7 @@ def test_detail_matches_oracle(sw, oracle_mod):
                 assert sel.digit == orc.decode(i)
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C2x"])
 def test_full_space(sw, oracle_mod, cfg):
     """Full space at the bench's launch configuration: winners, front and digest vs the
     oracle's full sweep; 200 sampled runs of 512 records element by element."""
@@ -301,3 +301,55 @@ def test_fleet_batch_api(sw):
             d, _ = p.detail(sels[i].index)
             assert tuple(d.rec) == tuple(sels[i].rec) and d.digit == sels[i].digit
         assert F.launch_count() > 0
+
+
+def test_decode_and_segments(sw, oracle_mod):
+    """sw_plan_decode (host helper) == the oracle's decoder, per scene; sw_plan_segments
+    describes the tiled layout: every record read through the zero-copy view's slot
+    formula equals the oracle's record."""
+    import ctypes
+    pb = make_config("C3")
+    orc = oracle_mod.Oracle(pb)
+    rng = random.Random(3)
+    with sw.Plan(pb, record_capacity=3_000_000) as plan:
+        for _ in range(50):
+            i = rng.randrange(plan.n)
+            dig = orc.decode(i)
+            per_scene = plan.decode(i)
+            for b in range(len(pb.radix)):
+                for s_ in range(pb.first_scene[b], pb.first_scene[b + 1]):
+                    assert per_scene[s_] == dig[b]
+        plan.eval(1_000_003, 2_000_005)
+        plan.eval(17, 400_000)
+        segs = plan.segments()
+        assert [(x["global_begin"], x["global_end"]) for x in segs] == [(1_000_003, 2_000_005), (17, 400_000)]
+        ptr, nslots = plan.records_view()
+        from paper_2603_05800_b200._native import sw_record
+        rt = _cudart()
+        for sg in segs:
+            for i in [sg["shard_begin"], sg["shard_end"] - 1] + [rng.randrange(sg["shard_begin"], sg["shard_end"])
+                                                                   for _ in range(30)]:
+                H, j = divmod(i, sg["row"])
+                slot = sg["offset"] + ((H // 32 - sg["tile0"]) * sg["row"] + j) * 32 + H % 32
+                assert slot < nslots
+                buf = (ctypes.c_uint8 * 32)()
+                assert rt.cudaMemcpy(ctypes.c_void_p(ctypes.addressof(buf)), ctypes.c_void_p(ptr + 32 * slot),
+                                     ctypes.c_size_t(32), 2) == 0  # cudaMemcpyDeviceToHost
+                rec = sw_record.from_buffer_copy(buf)
+                assert rec.astuple() == orc.records(i, i + 1)[0].astuple(), i
+
+
+def _cudart():
+    """The CUDA runtime (torch's copy) through ctypes, to read the zero-copy view."""
+    import ctypes
+    import glob
+    import torch
+    torch.cuda.init()
+    for name in ("libcudart.so.12", "libcudart.so"):
+        try:
+            return ctypes.CDLL(name)
+        except OSError:
+            pass
+    import nvidia.cuda_runtime
+    d = os.path.join(os.path.dirname(nvidia.cuda_runtime.__file__), "lib")
+    return ctypes.CDLL(sorted(glob.glob(os.path.join(d, "libcudart.so*")))[0])

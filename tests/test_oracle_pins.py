@@ -469,6 +469,43 @@ def test_budget_only_winner_is_on_the_front(oracle_mod):
     assert checked == 120
 
 
+def test_budget_only_winner_on_front_cost_x_ttff(oracle_mod):
+    """Reading R35: under COST_X_TTFF ("We minimize cost x TTFF") the
+    budget-only winner is on the front too when every record has cost > 0 and
+    ttff_eff > 0 (a positive fixed cost, a positive ready time): checked on the oracle for
+    random problems and budgets; and a counter-example with zero costs shows the
+    condition is needed (the GPU then scans)."""
+    import random
+    from tests.helpers import random_problem, make_problem
+    from swgen.generator import Query, INF
+    checked = 0
+    for seed in range(40):
+        rng = random.Random(9100 + seed)
+        pb = random_problem(rng, max_scenes=5, max_pools=3, max_choices=4,
+                            one_scene_digits=rng.random() < 0.5)
+        pb.objective = 1
+        pb.fixed_cost_mc = max(1, pb.fixed_cost_mc)
+        orc = oracle_mod.Oracle(pb)
+        recs = orc.record_list(0, orc.n)
+        assert all(r.cost_mc > 0 and r.ttff_us + r.stall_us > 0 for r in recs)
+        costs = sorted(r.cost_mc for r in recs)
+        qs = [Query(INF, INF, INF), Query(INF, INF, costs[len(costs) // 3]),
+              Query(INF, INF, max(0, costs[0] - 1))]
+        w, front, _ = orc.sweep(0, orc.n, qs)
+        on_front = {p[0] for p in front}
+        for st, idx, rec in w:
+            assert idx in on_front, (seed, st, idx)
+            checked += 1
+    assert checked == 120
+    # zero cost: plans 0 and 1 both have product 0 and Q equal; plan 1 is faster (on the
+    # front, dominating plan 0) but plan 0 wins the key by its lower index
+    pb = make_problem([1000, 1000], [0, 0], [0, 0], [1], [0], [1, 2], [0, 1, 2],
+                      [(1, 1, 0), (1, 1, 0), (1, 1, 0)], [5, 5000, 3000], objective=1)
+    orc = oracle_mod.Oracle(pb)
+    w, front, _ = orc.sweep(0, orc.n, [Query(INF, INF, INF)])
+    assert w[0][1] == 0 and 0 not in {p[0] for p in front}
+
+
 # ------------------------------------------- R31: per-pool ready offsets (load + warm-up)
 def _event_sim_ready(pb, a, digits, ready_us):
     """_event_sim with every GPU of pool p free from ready_us[p] ("~30 seconds"
@@ -551,3 +588,105 @@ def test_pool_ready_reserved_cost_example(oracle_mod):
     rec, ready, pend, mk, te = _detail(oracle_mod.Oracle(pb), 0)
     assert ready == [3_710_000_000] and mk == 3_710_000_000
     assert rec.cost_mc == 1_486_061
+
+
+# ---- record digest hash (R26): pinned to PUBLISHED SplitMix64 outputs -----------------
+# SplitMix64 (Steele, Lea, Flood 2014; Vigna's reference splitmix64.c) returns
+# mix64(seed + k * 0x9E3779B97F4A7C15) as its k-th output; R26's hash of the all-zero
+# record at index i is mix64(i), so these published sequences pin mix64 -- both
+# multipliers and all three shifts -- independently of the oracle's code.
+GOLDEN_GAMMA = 0x9E3779B97F4A7C15
+SPLITMIX_PUBLISHED = {
+    0: [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F, 0xF88BB8A8724C81EC],
+    1234567: [6457827717110365317, 3203168211198807973, 9817491932198370423,
+              4593380528125082431, 16408922859458223821],
+}
+
+
+def _zero_rec():
+    from oracle.oracle import Rec
+    return Rec(0, 0, 0, 0, 0, 0)
+
+
+def test_record_hash_published_splitmix_vectors(oracle_mod):
+    o = oracle_mod.Oracle(make_config("C1"))
+    for seed, outs in SPLITMIX_PUBLISHED.items():
+        for k, v in enumerate(outs, start=1):
+            idx = (seed + k * GOLDEN_GAMMA) % (1 << 64)
+            assert o.record_hash(idx, _zero_rec()) == v, (seed, k)
+
+
+def test_record_hash_covers_every_field(oracle_mod):
+    """Flipping any single bit of any record field (or of the index) changes the hash:
+    a hash that dropped a field (SURVEY's formula omits flags) or lost bits in a shift
+    would fail here."""
+    from oracle.oracle import Rec
+    o = oracle_mod.Oracle(make_config("C1"))
+    rng = random.Random(71)
+    widths = {"ttff_us": 62, "stall_us": 62, "cost_mc": 64, "quality": 32, "stall_count": 16, "flags": 8}
+    for _ in range(20):
+        base = Rec(rng.getrandbits(40), rng.getrandbits(40), rng.getrandbits(40), rng.getrandbits(32),
+                   rng.getrandbits(16), rng.getrandbits(8))
+        i = rng.getrandbits(63)
+        h0 = o.record_hash(i, base)
+        seen = {h0}
+        for b in range(64):
+            h = o.record_hash(i ^ (1 << b), base)
+            assert h not in seen
+            seen.add(h)
+        for f, w in widths.items():
+            for b in range(w):
+                r = Rec(*base.astuple())
+                setattr(r, f, getattr(r, f) ^ (1 << b))
+                h = o.record_hash(i, r)
+                assert h != h0, (f, b)
+
+
+def test_record_hash_field_placement(oracle_mod):
+    """R26's placement: a record's hash equals the zero record's hash at the index XORed
+    with the field's rotated / shifted image (ttff rotl 7, stall rotl 19, cost rotl 31,
+    flags << 48 | Q << 16 | cnt) -- pins the rotation amounts and the packing."""
+    from oracle.oracle import Rec
+    o = oracle_mod.Oracle(make_config("C1"))
+    M = (1 << 64) - 1
+
+    def rotl(x, r):
+        return ((x << r) | (x >> (64 - r))) & M
+    rng = random.Random(72)
+    for _ in range(50):
+        i = rng.getrandbits(64)
+        x = rng.getrandbits(62)
+        assert o.record_hash(i, Rec(x, 0, 0, 0, 0, 0)) == o.record_hash(i ^ rotl(x, 7), _zero_rec())
+        assert o.record_hash(i, Rec(0, x, 0, 0, 0, 0)) == o.record_hash(i ^ rotl(x, 19), _zero_rec())
+        assert o.record_hash(i, Rec(0, 0, x, 0, 0, 0)) == o.record_hash(i ^ rotl(x, 31), _zero_rec())
+        q, c, f = rng.getrandbits(32), rng.getrandbits(16), rng.getrandbits(8)
+        assert o.record_hash(i, Rec(0, 0, 0, q, c, f)) == o.record_hash(i ^ (f << 48 | q << 16 | c),
+                                                                        _zero_rec())
+
+
+# ---- pin 17 (SURVEY 8(c)): the synthetic profile against the paper's headline shape ------
+def test_paper_shape_c2_all_high(oracle_mod):
+    """Sanity link between the synthetic profile and the paper (not parity).  The paper's
+    setup: a 10-minute podcast "with 30 seconds per shot" (P:1104) on one 8xA100 server;
+    all-HIGH with one GPU per scene takes "3.7 hours".  With SURVEY App. B's
+    profile (uniform 30 s scenes, no jitter) the oracle gives 3.68 h, TTFF 4420 s and
+    TTFF_eff 3.54 h (App. C); with k = 8 for every scene the scenes serialise: 7.09 h, RTF
+    42.5 -- below the naive sequential 8.3 h / 50x."""
+    from swgen.generator import va_seconds, _fixed_stage_times, llround
+    S, dur_ms = 20, [30_000] * 20
+    llm, tts = _fixed_stage_times(dur_ms, False)
+    out = {}
+    for k in (1, 8):
+        va = [max(1, llround(1e6 * va_seconds(30_000, 3, k, "A100"))) for _ in range(S)]
+        pb = make_problem([d * 1000 for d in dur_ms], llm, tts, [8], [180250], [1] * S, list(range(S + 1)),
+                          [(3, k, 0)] * S, va, overhead_us=1_200_000)
+        rec, _, _, mk, te = oracle_mod.Oracle(pb).eval(0)
+        out[k] = (rec, mk, te)
+    rec1, mk1, te1 = out[1]
+    assert abs(mk1 / 3.6e9 - 3.7) <= 0.01 * 3.7, mk1 / 3.6e9          # 3.68 h vs "3.7 hours"
+    assert abs(rec1.ttff_us / 1e6 - 4420) < 1                          # App. C
+    assert abs(te1 / 3.6e9 - 3.54) < 0.01
+    assert abs(rec1.cost_mc / 1e5 - 53) < 0.1                          # ~$53 reserved
+    rec8, mk8, _ = out[8]
+    assert abs(mk8 / 3.6e9 - 7.09) < 0.01 and mk8 < 8.3 * 3.6e9         # vs naive 8.3 h (P:310)
+    assert abs(mk8 / 600e6 - 42.5) < 0.1                               # RTF 42.5 vs "50x"

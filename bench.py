@@ -32,6 +32,7 @@ WORKLOADS = {
     "C1": "C1: 1-minute podcast, 4 scenes, MED/HIGH, A100x2, k{1,2}: 256 plans (BASELINE configs[0])",
     "C2": "C2: 10-minute podcast, one 8xA100-profile server, 20 scenes, 3 levels x k{1,2,4,8}, "
           "12^8 plans (BASELINE configs[1])",
+    "C2x": "C2x: C2 under the paper's objective 'We minimize cost x TTFF' (P:918; COST_X_TTFF), 12^8 plans",
     "C3": "C3: 10-minute podcast, A100x8+H100x8, static intro, early low-res ladder, 24^6 plans "
           "(BASELINE configs[2])",
     "C5": "C5: 30-minute podcast, 60 scenes, 4 levels x A100/H100/H200, 48^6 = 1.2e10 plans, "
@@ -187,6 +188,204 @@ def run_reference(args, pb):
     return 0
 
 
+HBM_SPEC_GBS = 8000.0  # B200 HBM3e spec bandwidth (the measured copy peak is the roofline)
+
+
+def host_cpu():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "threads": os.cpu_count()}
+
+
+def load_traffic(cfg):
+    """ncu evidence per config (profiles/traffic.json): DRAM bytes / algorithmic bytes and
+    issue-active % of one captured launch per kernel."""
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        pj = json.load(open(prof))
+    except Exception:
+        return {}
+    return pj.get("configs", {}).get(cfg, {}).get("kernels", {})
+
+
+def kernel_roofline(stats0, stats1, steps, ms_per_step, cfg, names=("eval_kernel", "scan_kernel")):
+    """Per kernel: ALGORITHMIC bytes per launch (32 B x records written by eval / read by a
+    scan) over the launch's CUDA-event time on the handle's stream, averaged over the
+    launches of the timed region, against the measured HBM copy peak."""
+    peak, peak_kind = peaks()
+    tr = load_traffic(cfg)
+    kern = {}
+    for name, a0, a1 in zip(names, stats0, stats1):
+        n_l, t_ms, by = a1[0] - a0[0], a1[1] - a0[1], a1[2] - a0[2]
+        if n_l == 0 or t_ms <= 0:
+            continue
+        avg_ms = t_ms / n_l
+        ach = by / n_l / (avg_ms / 1e3) / 1e9
+        t = tr.get(name, {})
+        kern[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                      "pct_of_spec": 100.0 * ach / HBM_SPEC_GBS,
+                      "traffic": (t["dram_bytes"] / t["algorithmic_bytes"] * by / n_l) if "dram_bytes" in t else None,
+                      "ncu_issue_active_pct": t.get("issue_active_pct"),
+                      "algorithmic_bytes_per_launch": by / n_l, "launches": n_l,
+                      "ms_per_launch": avg_ms, "share_of_step": t_ms / steps / ms_per_step}
+    if not kern:
+        return None
+    dom = max(kern, key=lambda k: kern[k]["share_of_step"])
+    roof = dict(kern[dom])
+    roof["kernel"] = dom
+    roof["peak_source"] = peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    roof["kernels"] = kern
+    return roof
+
+
+def measure_plan(ctx, pb, cfg, steps, warmup, e2e_steps, clocks=None):
+    """One config through sw_plan_*: STEP = reset + sw_plan_sweep of the whole space (eval,
+    records stored, the config's select queries and the Pareto folds; chunked when the
+    records exceed 75% of free HBM) + the exact front.  Device time with CUDA events on
+    the handle's stream, max over ranks; parity vs the oracle golden after the timed
+    region; e2e from host buffers through the public API."""
+    import torch
+    sw, dev, stream, comm = ctx["sw"], ctx["dev"], ctx["stream"], ctx["comm"]
+    rank, world, barrier, mor = ctx["rank"], ctx["world"], ctx["barrier"], ctx["max_over_ranks"]
+    N, row = sw.space_shape(pb)
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    need = N // world + 3 * row  # the library's default: this rank's largest shard
+    cap = 0 if need * REC_BYTES < 0.75 * free_b else int(0.75 * free_b) // REC_BYTES
+    out = {"workload": WORKLOADS.get(cfg, cfg), "n_candidates": N, "cap": cap,
+           "record_capacity_per_rank": cap, "chunked": cap != 0}
+
+    def step(p):
+        p.reset()
+        sels, _ = p.sweep(0, N, pb.queries)  # eval (chunked if needed) + select + fold
+        return sels, p.pareto()
+
+    plan = sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world,
+                   record_capacity=cap)
+    for _ in range(warmup):
+        step(plan)
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)  # let nvidia-smi start sampling
+    barrier()
+    l0 = plan.launch_count()
+    k0 = [plan.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
+    ev0.record(stream)
+    for _ in range(steps):
+        sels, front = step(plan)
+    ev1.record(stream)
+    ev1.synchronize()
+    w1 = time.time()
+    barrier()
+    out["clocks"] = clocks.stop(w0, w1) if clocks else None
+    out["gpu_launches"] = plan.launch_count() - l0
+    k1 = [plan.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
+    ms = mor(ev0.elapsed_time(ev1))
+    out["steps"] = steps
+    out["ms_per_step"] = ms / steps
+    out["value"] = N / (out["ms_per_step"] / 1e3)
+    out["unit"] = UNIT
+    out["roofline"] = kernel_roofline(k0, k1, steps, out["ms_per_step"], cfg)
+    out["front"] = front
+    out["front_points"] = len(front)
+    parity = None
+    gpath = os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % cfg)
+    if os.path.exists(gpath):
+        g = json.load(open(gpath))
+        if g.get("begin", 0) == 0 and g.get("end", N) == N:
+            plan.reset()
+            sels_p, dg = plan.sweep(0, N, pb.queries, digest=True)
+            ok_w = all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
+                       for s, w in zip(sels_p, g["winners"]))
+            ok_f = plan.pareto() == [tuple(p) for p in g["front"]]
+            parity = {"digest": dg == int(g["digest"]), "winners": ok_w, "pareto": ok_f,
+                      "golden_sha256": g.get("sha256")}
+    out["parity"] = parity
+    plan.close()
+    barrier()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(e2e_steps):
+        with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank,
+                     nranks=world, record_capacity=cap) as p2:
+            s2, f2 = step(p2)
+            d2h = 112 * len(s2) + 32 * len(f2)
+    barrier()
+    e2e_s = mor((time.perf_counter() - t0) / max(1, e2e_steps))
+    out["e2e_s"] = e2e_s
+    out["d2h"] = d2h
+    out["e2e"] = {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": input_bytes(pb),
+                  "d2h_bytes_per_step": d2h, "steps": e2e_steps}
+    return out
+
+
+def measure_fleet(ctx, steps, warmup, e2e_steps):
+    """C4 (BASELINE configs[3]): 256 requests of 5-15 min, per-request SLO/budget, through
+    sw_fleet_*: STEP = reset + one eval launch over every request's space + one select scan
+    with one query per request (+ the winners' detail).  Parity: every request's winner and
+    record digest vs the oracle golden."""
+    import torch
+    from swgen import make_fleet
+    sw, dev, stream, comm = ctx["sw"], ctx["dev"], ctx["stream"], ctx["comm"]
+    rank, world, barrier, mor = ctx["rank"], ctx["world"], ctx["barrier"], ctx["max_over_ranks"]
+    fleet = make_fleet()
+    qs = [pb.queries[0] for pb in fleet]
+    out = {"workload": "C4: fleet of %d podcasts of 5-15 min, A100x8+H100x8 each, per-request SLO/budget "
+                       "(real-time / relaxed / batch by r mod 3, P:1449) (BASELINE configs[3])" % len(fleet)}
+    with sw.Fleet(fleet, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world) as F:
+        N = sum(F.plan(i).n for i in range(F.n))
+        out["n_candidates"] = N
+
+        def step():
+            F.reset()
+            F.eval()
+            return F.select(qs)
+        for _ in range(warmup):
+            step()
+        barrier()
+        l0 = F.launch_count()
+        k0 = [F.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            sels = step()
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+        k1 = [F.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
+        ms = mor(ev0.elapsed_time(ev1)) / steps
+        out.update(steps=steps, ms_per_step=ms, value=N / (ms / 1e3), unit=UNIT,
+                   gpu_launches=F.launch_count() - l0,
+                   roofline=kernel_roofline(k0, k1, steps, ms, "C4"))
+        gpath = os.path.join(ROOT, "tests", "golden", "oracle_C4.json")
+        if os.path.exists(gpath):
+            g = json.load(open(gpath))
+            ok_w = all(s.index == gr["winners"][0]["index"] and tuple(s.rec) == tuple(gr["winners"][0]["rec"])
+                       for s, gr in zip(sels, g["requests"]))
+            ok_d = all(F.plan(i).digest() == int(gr["digest"]) for i, gr in enumerate(g["requests"]))
+            out["parity"] = {"winners": ok_w, "digest": ok_d}
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        with sw.Fleet(fleet, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world) as F2:
+            F2.eval()
+            F2.select(qs)
+    barrier()
+    e2e_s = mor((time.perf_counter() - t0) / max(1, e2e_steps))
+    out["e2e"] = {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": sum(input_bytes(pb) for pb in fleet),
+                  "d2h_bytes_per_step": 112 * len(fleet), "steps": e2e_steps}
+    return out
+
+
 def input_bytes(pb):
     return (8 * 3 * pb.S + 8 * len(pb.va_us) + 4 * len(pb.radix) + 4 * len(pb.first_scene)
             + 4 * len(pb.choices) + 4 * len(pb.level_score) + 12 * len(pb.gpus))
@@ -215,6 +414,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--configs", default="C2x,C3,C4,C5",
+                    help="further configs measured after the headline, reported under 'configs'")
     ap.add_argument("--stream-steps", type=int, default=5,
                     help="fused stream mode (SURVEY §8(f) row 1) calls timed after the main line (0: skip)")
     args = ap.parse_args()
@@ -239,24 +440,6 @@ def main():
         comm = sw.comm_init(obj[0], rank, world, dev)
 
     stream = torch.cuda.Stream(device=dev)
-    N = sw.space_shape(pb)[0]
-    # records retained per rank: this rank's share, or as many as 75% of free HBM holds
-    # (C5: 391 GB of records -> chunked sweep)
-    free_b, _ = torch.cuda.mem_get_info(dev)
-    n_max, row = sw.space_shape(pb)
-    need = N // world + 3 * row  # the library's default: this rank's largest shard
-    cap = 0 if need * REC_BYTES < 0.75 * free_b else int(0.75 * free_b) // REC_BYTES
-    plan = sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world,
-                   record_capacity=cap)
-
-    def step(p):
-        p.reset()
-        sels, _ = p.sweep(0, N, pb.queries)  # eval (chunked if needed) + select + fold
-        front = p.pareto()
-        return sels, front
-
-    for _ in range(args.warmup):
-        step(plan)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -264,102 +447,31 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            x = float(t[0])
+        return x
+
+    ctx = dict(sw=sw, dev=dev, stream=stream, comm=comm, rank=rank, world=world, barrier=barrier,
+               max_over_ranks=max_over_ranks)
     clocks = ClockSampler(dev)
-    clocks.start()
-    time.sleep(0.3)  # let nvidia-smi start sampling
-    barrier()
-    l0 = plan.launch_count()
-    k0 = [plan.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    w0 = time.time()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        sels, front = step(plan)
-    ev1.record(stream)
-    ev1.synchronize()
-    w1 = time.time()
-    barrier()
-    ck = clocks.stop(w0, w1)
-    launches = plan.launch_count() - l0
-    k1 = [plan.kernel_time(k) for k in (sw.SW_KERNEL_EVAL, sw.SW_KERNEL_SCAN)]
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
-    ms_per_step = ms / args.steps
-    value = N / (ms_per_step / 1e3)
-
-    # roofline per kernel: ALGORITHMIC bytes per launch (32 B x records written by eval /
-    # read by the fused select+Pareto scan) over the launch's CUDA-event time on the
-    # handle's stream, averaged over the launches of the timed region; the dominant
-    # kernel (largest share of the step) is the line's "roofline"
-    peak, peak_kind = peaks()
-    traffic = {}
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof))
-            if pj.get("config") == args.config:
-                # per kernel: DRAM bytes / algorithmic bytes of the captured launch
-                traffic = {k: v["dram_bytes"] / v["algorithmic_bytes"]
-                           for k, v in pj.get("kernels", {}).items()}
-        except Exception:
-            pass
-    kern = {}
-    for name, a0, a1 in zip(("eval_kernel", "scan_kernel"), k0, k1):
-        n_l, t_ms, by = a1[0] - a0[0], a1[1] - a0[1], a1[2] - a0[2]
-        if n_l == 0:
-            continue
-        avg_ms = t_ms / n_l
-        ach = by / n_l / (avg_ms / 1e3) / 1e9
-        kern[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                      "frac": ach / peak,
-                      "traffic": (traffic[name] * by / n_l) if name in traffic else None,
-                      "algorithmic_bytes_per_launch": by / n_l, "launches": n_l,
-                      "ms_per_launch": avg_ms, "share_of_step": t_ms / args.steps / ms_per_step}
-    dom = max(kern, key=lambda k: kern[k]["share_of_step"])
-    roof = dict(kern[dom])
-    roof["kernel"] = dom
-    roof["peak_source"] = peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
-    roof["kernels"] = kern
-
-    # parity check of the timed configuration (outside the timed region)
-    parity = None
+    head = measure_plan(ctx, pb, args.config, args.steps, args.warmup, args.e2e_steps, clocks=clocks)
+    ms_per_step, value, N, cap = head["ms_per_step"], head["value"], head["n_candidates"], head["cap"]
+    ck, launches, roof, parity, front = head["clocks"], head["gpu_launches"], head["roofline"], head["parity"], head["front"]
+    e2e_s = head["e2e_s"]
+    d2h = head["d2h"]
     gpath = os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % args.config)
-    if os.path.exists(gpath):
-        g = json.load(open(gpath))
-        plan.reset()
-        sels_p, dg = plan.sweep(0, N, pb.queries, digest=True)
-        ok_w = all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
-                   for s, w in zip(sels_p, g["winners"]))
-        ok_f = plan.pareto() == [tuple(p) for p in g["front"]]
-        parity = {"digest": dg == int(g["digest"]), "winners": ok_w, "pareto": ok_f}
-
-    # e2e: public API from HOST buffers each step (create uploads the tables, results
-    # come back to host), wall clock with device sync on both sides, max over ranks
-    plan.close()
-    barrier()
-    t0 = time.perf_counter()
-    d2h = 0
-    for _ in range(args.e2e_steps):
-        with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank,
-                     nranks=world, record_capacity=cap) as p2:
-            s2, f2 = step(p2)
-            d2h = 112 * len(s2) + 32 * len(f2)
-    barrier()
-    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
+    g = json.load(open(gpath)) if os.path.exists(gpath) else None
 
     # §8(f) row 1, reported beside (not instead of) the headline: the fused stream mode
     # evaluates the same space with NO record store (a7 skipped by design), select + Pareto
     # filter in-kernel; CUDA events on the stream around whole calls, max over ranks
     stream_line = None
     if args.stream_steps > 0:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
         with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world,
                      record_capacity=1024) as p3:
             for _ in range(2):
@@ -374,13 +486,9 @@ def main():
             ev1.record(stream)
             ev1.synchronize()
             s1 = p3.kernel_time(sw.SW_KERNEL_STREAM)
-            sms = ev0.elapsed_time(ev1) / args.stream_steps
-            if world > 1:
-                t = torch.tensor([sms], dtype=torch.float64, device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                sms = float(t[0])
+            sms = max_over_ranks(ev0.elapsed_time(ev1) / args.stream_steps)
             sparity = None
-            if os.path.exists(gpath):
+            if g is not None:
                 sparity = (all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
                                for s, w in zip(ss, g["winners"])) and
                            p3.pareto() == [tuple(p) for p in g["front"]])
@@ -390,6 +498,24 @@ def main():
                            "calls": args.stream_steps, "parity": sparity,
                            "note": "sw_plan_stream: no records stored (a7 skipped by design; "
                                    "SURVEY 8(f) row 1), not the headline step"}
+
+    # the other configs of BASELINE.json / SURVEY 8(d), each a full step of its own
+    # workload with per-kernel roofline, parity vs the oracle golden and e2e
+    extra = {}
+    for cfg in [c for c in args.configs.split(",") if c and c != args.config]:
+        try:
+            if cfg == "C4":
+                extra[cfg] = measure_fleet(ctx, min(args.steps, 10), 3, args.e2e_steps)
+            else:
+                pbx = make_config(cfg)
+                nx = sw.space_shape(pbx)[0]
+                st = 3 if nx > 2e9 else min(args.steps, 20)
+                r = measure_plan(ctx, pbx, cfg, st, 3 if nx > 2e9 else args.warmup, 1 if nx > 2e9 else args.e2e_steps)
+                for k in ("cap", "front", "e2e_s", "d2h", "clocks"):
+                    r.pop(k, None)
+                extra[cfg] = r
+        except Exception as ex:  # noqa: BLE001 -- reported in the line, never hides the headline
+            extra[cfg] = {"error": "%s: %s" % (type(ex).__name__, ex)}
 
     if rank == 0:
         cpu = None
@@ -405,6 +531,8 @@ def main():
                        "record_capacity_per_rank": cap,
                        "parallelism": "candidate-shard x%d, NCCL allgather merge" % world},
             "roofline": roof,
+            "hbm_spec_gbs": HBM_SPEC_GBS,
+            "host_cpu": host_cpu(),
             "cpu_baseline": cpu,
             "e2e": {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": input_bytes(pb),
                     "d2h_bytes_per_step": d2h},
@@ -413,6 +541,7 @@ def main():
             "parity": parity,
             "front_points": len(front),
             "stream_mode": stream_line,
+            "configs": extra,
         }
         emit(line)
     if comm:

@@ -250,3 +250,69 @@ def winner_merge(objective, query, a, b):
     wa, wb, out = w(a), w(b), OrWinner()
     lib().or_winner_merge(C.c_uint32(objective), C.byref(q), C.byref(wa), C.byref(wb), C.byref(out))
     return out.status, out.index, _rec(out.rec)
+
+
+class OrShared(C.Structure):
+    _fields_ = [("n_req", C.c_uint32), ("req", C.POINTER(OrProblem)), ("arrival_us", U64P),
+                ("slo_startup_us", U64P), ("slo_stall_us", U64P), ("fixed_index", U64P),
+                ("n_pools", C.c_uint32), ("gpus", U32P), ("price_mc", U64P), ("pool_ready_us", U64P),
+                ("billing", C.c_uint32), ("objective", C.c_uint32)]
+
+
+class SharedOracle:
+    """Shared-pool fleet (reading R36) of a swgen.SharedFleet: joint
+    candidates = the plans of its free requests, evaluated by the per-pool online EDF
+    event simulation of or_shared_eval."""
+
+    def __init__(self, sf):
+        self.sf = sf
+        self.reqs = [Oracle(pb) for pb in sf.requests]
+        R = len(self.reqs)
+        arr = (OrProblem * R)(*[o.c for o in self.reqs])
+        self._keep = [arr]
+        a = lambda t, v: self._k(_arr(t, v))  # noqa: E731
+        self.c = OrShared(
+            n_req=R, req=arr, arrival_us=a(C.c_uint64, sf.arrival_us),
+            slo_startup_us=a(C.c_uint64, sf.slo_startup_us), slo_stall_us=a(C.c_uint64, sf.slo_stall_us),
+            fixed_index=a(C.c_uint64, [(1 << 64) - 1 if x is None else x for x in sf.fixed_index]),
+            n_pools=len(sf.gpus), gpus=a(C.c_uint32, sf.gpus), price_mc=a(C.c_uint64, sf.price_mc),
+            pool_ready_us=a(C.c_uint64, sf.pool_ready_us) if sf.pool_ready_us else None,
+            billing=sf.billing, objective=sf.objective)
+
+    def _k(self, x):
+        self._keep.append(x)
+        return x
+
+    @property
+    def n(self) -> int:
+        lib().or_shared_space_size.restype = C.c_uint64
+        return lib().or_shared_space_size(C.byref(self.c))
+
+    def decode(self, index: int) -> List[int]:
+        out = (C.c_uint64 * len(self.reqs))()
+        lib().or_shared_decode(C.byref(self.c), C.c_uint64(index), out)
+        return list(out)
+
+    def eval(self, index: int):
+        """-> (fleet Rec, [per-request Rec (cost = its fixed cost)], ready_abs[r][s])."""
+        R = len(self.reqs)
+        f = OrRecord()
+        pr = (OrRecord * R)()
+        ready = (C.c_uint64 * (64 * R))()
+        lib().or_shared_eval(C.byref(self.c), C.c_uint64(index), C.byref(f), pr, ready)
+        return _rec(f), [_rec(x) for x in pr], [list(ready[64 * r: 64 * r + pb.S])
+                                                 for r, pb in enumerate(self.sf.requests)]
+
+    def sweep(self, begin: int, end: int, queries, nthreads: Optional[int] = None, front_cap: int = 1 << 20):
+        nthreads = nthreads or os.cpu_count() or 1
+        nq = len(queries)
+        qs = (OrQuery * max(1, nq))(*[OrQuery(q.slo_startup_us, q.slo_stall_us, q.budget_mc) for q in queries])
+        ws = (OrWinner * max(1, nq))()
+        fr = (OrPoint * front_cap)()
+        fn, dg = C.c_uint64(), C.c_uint64()
+        rc = lib().or_shared_sweep(C.byref(self.c), C.c_uint64(begin), C.c_uint64(end), C.c_uint32(nthreads),
+                                   C.c_uint32(nq), qs, ws, fr, C.c_uint64(front_cap), C.byref(fn), C.byref(dg))
+        if rc != 0:
+            raise RuntimeError("or_shared_sweep failed rc=%d" % rc)
+        return ([(w.status, w.index, _rec(w.rec)) for w in ws[:nq]],
+                [(p.index, p.ttff_eff_us, p.cost_mc, p.quality) for p in fr[: fn.value]], dg.value)

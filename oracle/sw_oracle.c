@@ -361,10 +361,15 @@ uint64_t or_record_hash(uint64_t index, const or_record *r) {
 }
 
 /* ---- the full sweep: evaluate [begin,end), select, Pareto, digest --------- */
+typedef void (*or_eval_fn)(const void *ctx, uint64_t index, or_record *rec);
+
 typedef struct {
     const or_problem *pb;
     const uint64_t *a, *P;
     uint64_t begin, end;
+    or_eval_fn fn; /* NULL: one request's candidate (or_eval_detail), else fn(ctx, i, &r) */
+    const void *ctx;
+    uint32_t objective;
     uint32_t nq;
     const or_query *q;
     or_winner feas[64], close[64];
@@ -374,22 +379,23 @@ typedef struct {
 
 static void *sweep_worker(void *arg) {
     sweep_job *j = arg;
-    const or_problem *pb = j->pb;
+    const uint32_t objective = j->objective;
     for (uint32_t k = 0; k < j->nq; k++) { j->feas[k].status = -1; j->close[k].status = -1; }
     for (uint64_t i = j->begin; i < j->end; i++) {
         or_record r;
-        or_eval_detail(pb, j->a, j->P, i, &r, NULL, NULL, NULL, NULL);
+        if (j->fn) j->fn(j->ctx, i, &r);
+        else or_eval_detail(j->pb, j->a, j->P, i, &r, NULL, NULL, NULL, NULL);
         j->digest += or_record_hash(i, &r);
         for (uint32_t k = 0; k < j->nq; k++) {
             const or_query *q = &j->q[k];
             if (feasible(q, &r)) {
                 if (j->feas[k].status < 0 ||
-                    obj_cmp(pb->objective, i, &r, j->feas[k].index, &j->feas[k].rec) < 0) {
+                    obj_cmp(objective, i, &r, j->feas[k].index, &j->feas[k].rec) < 0) {
                     j->feas[k].index = i; j->feas[k].rec = r; j->feas[k].status = 0;
                 }
             } else {
                 if (j->close[k].status < 0 ||
-                    closest_cmp(pb->objective, q, i, &r, j->close[k].index, &j->close[k].rec) < 0) {
+                    closest_cmp(objective, q, i, &r, j->close[k].index, &j->close[k].rec) < 0) {
                     j->close[k].index = i; j->close[k].rec = r; j->close[k].status = 1;
                 }
             }
@@ -400,20 +406,27 @@ static void *sweep_worker(void *arg) {
     return NULL;
 }
 
-/* Returns 0 on success, 1 if the front did not fit (front_n = required size). */
-int or_sweep(const or_problem *pb, uint64_t begin, uint64_t end, uint32_t nthreads,
-             uint32_t nq, const or_query *queries, or_winner *winners,
-             or_point *front_out, uint64_t front_cap, uint64_t *front_n, uint64_t *digest) {
+/* Evaluate [begin, end) with the given evaluator (fn NULL: candidates of pb), select,
+ * Pareto, digest.  Returns 0 on success, 1 if the front did not fit. */
+static int sweep_generic(const or_problem *pb, or_eval_fn fn, const void *ctx, uint32_t objective,
+                         uint64_t begin, uint64_t end, uint32_t nthreads,
+                         uint32_t nq, const or_query *queries, or_winner *winners,
+                         or_point *front_out, uint64_t front_cap, uint64_t *front_n, uint64_t *digest) {
     if (nthreads < 1) nthreads = 1;
     if (nq > 64) return -1;
-    uint64_t *a = malloc(sizeof(uint64_t) * pb->S), *P = malloc(sizeof(uint64_t) * pb->S);
-    or_fixed_stages(pb, a);
-    or_deadlines(pb, P);
+    uint64_t *a = NULL, *P = NULL;
+    if (pb) {
+        a = malloc(sizeof(uint64_t) * pb->S);
+        P = malloc(sizeof(uint64_t) * pb->S);
+        or_fixed_stages(pb, a);
+        or_deadlines(pb, P);
+    }
     sweep_job *jobs = calloc(nthreads, sizeof(sweep_job));
     pthread_t *th = calloc(nthreads, sizeof(pthread_t));
     uint64_t n = end > begin ? end - begin : 0;
     for (uint32_t t = 0; t < nthreads; t++) {
         jobs[t].pb = pb; jobs[t].a = a; jobs[t].P = P;
+        jobs[t].fn = fn; jobs[t].ctx = ctx; jobs[t].objective = objective;
         jobs[t].begin = begin + n * t / nthreads;
         jobs[t].end = begin + n * (t + 1) / nthreads;
         jobs[t].nq = nq; jobs[t].q = queries;
@@ -430,14 +443,14 @@ int or_sweep(const or_problem *pb, uint64_t begin, uint64_t end, uint32_t nthrea
         for (uint32_t t = 0; t < nthreads; t++) {
             or_winner *w = &jobs[t].feas[k];
             if (w->status == 0 && (best.status != 0 ||
-                obj_cmp(pb->objective, w->index, &w->rec, best.index, &best.rec) < 0))
+                obj_cmp(objective, w->index, &w->rec, best.index, &best.rec) < 0))
                 best = *w;
         }
         if (best.status != 0) {
             for (uint32_t t = 0; t < nthreads; t++) {
                 or_winner *w = &jobs[t].close[k];
                 if (w->status == 1 && (best.status != 1 ||
-                    closest_cmp(pb->objective, &queries[k], w->index, &w->rec, best.index, &best.rec) < 0))
+                    closest_cmp(objective, &queries[k], w->index, &w->rec, best.index, &best.rec) < 0))
                     best = *w;
             }
         }
@@ -468,6 +481,13 @@ int or_sweep(const or_problem *pb, uint64_t begin, uint64_t end, uint32_t nthrea
     else memcpy(front_out, fr, nf * sizeof(or_point));
     free(all); free(fr); free(jobs); free(th); free(a); free(P);
     return rc;
+}
+
+int or_sweep(const or_problem *pb, uint64_t begin, uint64_t end, uint32_t nthreads,
+             uint32_t nq, const or_query *queries, or_winner *winners,
+             or_point *front_out, uint64_t front_cap, uint64_t *front_n, uint64_t *digest) {
+    return sweep_generic(pb, NULL, NULL, pb->objective, begin, end, nthreads, nq, queries, winners,
+                         front_out, front_cap, front_n, digest);
 }
 
 /* Pareto front of an explicit point list (plain O(n^2) definition, sorted output). */
@@ -565,6 +585,226 @@ int or_greedy(const or_problem *pb, const or_query *q, uint64_t start, uint64_t 
     free(a);
     free(P);
     return 0;
+}
+
+/* ---- shared-pool fleet (reading R36) ------------------------
+ * "To coordinate multiple requests, model instances maintain local queues that
+ * prioritize tasks by deadline.  For example, the image generation model may process an
+ * early scene from a new request before a later scene from an earlier request if it has
+ * a tighter deadline"; per-node deadlines come from the request's SLO: "a
+ * real-time video podcast with a TTFF of 5 seconds and 10-minute duration sets the final
+ * node's deadline at t_now+605"; heterogeneous SLOs -- real-time, 50% relaxed,
+ * batch (no SLO) -- let the deadline-aware scheduler "prioritize real-time requests"
+ * (P:1449-1451).  Reading R36:
+ *   - requests r arrive at T0_r, each with its own fixed stages (own LLM / TTS, so its
+ *     scene s is released at T0_r + a_s), scenes, tables and a plan; the n_pools GPU pools
+ *     are SHARED by all requests;
+ *   - scene s of request r is due at d_rs = T0_r + slo_startup_r + P_s (UINT64_MAX for a
+ *     batch request, whose scenes then rank after every deadline-bearing task);
+ *   - every pool is an online, non-preemptive EDF queue of gang tasks: whenever it
+ *     decides at time t, the head is the released (release <= t), unstarted task with the
+ *     smallest (deadline, request, scene); it starts at max(t, F[k-1]) on the k
+ *     earliest-free GPUs (the single-request recurrence's gang rule, no backfill)
+ *     unless a more urgent task is released at or before that start, which then takes the
+ *     decision; decisions are made in time order;
+ *   - a request's metrics are its own, relative to T0_r (TTFF, TTFF_eff, stall, count,
+ *     quality as for one request); the FLEET record of a joint plan is
+ *       ttff  = max_r sat(ttff_r - slo_startup_r)   (worst startup lateness)
+ *       stall = max_r sat(stall_r - slo_stall_r)    (worst stall lateness)
+ *       cost  = sum_r fixed_r + sum_p pool cost (RESERVED: billed G_p x the pool's last
+ *               finish, from t = 0; BUSY: sum k t), Q = sum_r Q_r, count = sum_r count_r,
+ *       flags = pools used,
+ *     so the query (0, 0, budget) asks "every request meets its SLO within the fleet
+ *     budget" and the closest tier minimises lateness.
+ * A joint candidate index enumerates the plans of the FREE requests (fixed_index[r] =
+ * UINT64_MAX), MSD = the first free request's first digit; fixed requests are the
+ * background load. */
+typedef struct {
+    uint32_t n_req;
+    const or_problem *req;          /* [n_req]: scenes, tables, fixed cost, level scores of
+                                       each request; their pool fields are ignored */
+    const uint64_t *arrival_us;     /* [n_req] T0_r */
+    const uint64_t *slo_startup_us; /* [n_req] (UINT64_MAX: batch) */
+    const uint64_t *slo_stall_us;   /* [n_req] */
+    const uint64_t *fixed_index;    /* [n_req] plan of a background request, UINT64_MAX = free */
+    uint32_t n_pools;
+    const uint32_t *gpus;
+    const uint64_t *price_mc;
+    const uint64_t *pool_ready_us;  /* or NULL */
+    uint32_t billing;
+    uint32_t objective;
+} or_shared;
+
+#define OR_MAXREQ 16
+
+static uint64_t sat_add(uint64_t a, uint64_t b) { return a > UINT64_MAX - b ? UINT64_MAX : a + b; }
+
+uint64_t or_shared_space_size(const or_shared *sh) {
+    uint64_t n = 1;
+    for (uint32_t r = 0; r < sh->n_req; r++)
+        if (sh->fixed_index[r] == UINT64_MAX) n *= or_space_size(&sh->req[r]);
+    return n;
+}
+
+/* Joint index -> one plan index per request (last free request = least significant). */
+void or_shared_decode(const or_shared *sh, uint64_t index, uint64_t *plan) {
+    for (int r = (int)sh->n_req - 1; r >= 0; r--) {
+        if (sh->fixed_index[r] != UINT64_MAX) { plan[r] = sh->fixed_index[r]; continue; }
+        uint64_t n = or_space_size(&sh->req[r]);
+        plan[r] = index % n;
+        index /= n;
+    }
+}
+
+typedef struct { uint32_t r, s, k, pool; uint64_t rel, dl, t; int started; } sh_task;
+
+static int task_before(const sh_task *x, const sh_task *y) { /* (deadline, request, scene) */
+    if (x->dl != y->dl) return x->dl < y->dl;
+    if (x->r != y->r) return x->r < y->r;
+    return x->s < y->s;
+}
+
+/* Evaluate one joint candidate: fleet record, per-request records (may be NULL) and
+ * absolute scene ready times ready[r * 64 + s] (may be NULL). */
+void or_shared_eval(const or_shared *sh, uint64_t index, or_record *fleet, or_record *per_req,
+                    uint64_t *ready_abs) {
+    uint64_t plan[OR_MAXREQ];
+    or_shared_decode(sh, index, plan);
+    static const uint32_t MAXT = OR_MAXREQ * 64;
+    sh_task *tasks = malloc(sizeof(sh_task) * MAXT);
+    uint64_t ready[OR_MAXREQ][64];
+    uint64_t a[OR_MAXREQ][64], P[OR_MAXREQ][64];
+    uint32_t lvl[OR_MAXREQ][64];
+    uint32_t nt = 0;
+    /* 1. every request's fixed stages and its scenes' choices */
+    for (uint32_t r = 0; r < sh->n_req; r++) {
+        const or_problem *pb = &sh->req[r];
+        or_fixed_stages(pb, a[r]);
+        or_deadlines(pb, P[r]);
+        uint32_t digits[64];
+        or_decode(pb, plan[r], digits);
+        uint32_t coff = 0, voff = 0, b = 0;
+        uint32_t s0 = pb->scene0_static ? 1 : 0;
+        if (s0) { ready[r][0] = sat_add(sh->arrival_us[r], pb->static_ready_us); lvl[r][0] = UINT32_MAX; }
+        for (uint32_t s = s0; s < pb->S; s++) {
+            while (!(pb->first_scene[b] <= s && s < pb->first_scene[b + 1])) {
+                coff += pb->radix[b];
+                voff += (pb->first_scene[b + 1] - pb->first_scene[b]) * pb->radix[b];
+                b++;
+            }
+            uint32_t c = digits[b];
+            lvl[r][s] = pb->choice_level[coff + c];
+            uint32_t k = pb->choice_k[coff + c], p = pb->choice_pool[coff + c];
+            uint64_t t = pb->va_us[voff + (s - pb->first_scene[b]) * pb->radix[b] + c];
+            uint64_t rel = sh->arrival_us[r] + a[r][s];
+            if (k == 0) { ready[r][s] = rel; continue; } /* STATIC rung: R = a (R33) */
+            sh_task x = {r, s, k, p, rel, 0, t, 0};
+            x.dl = sh->slo_startup_us[r] == UINT64_MAX ? UINT64_MAX
+                   : sat_add(sat_add(sh->arrival_us[r], sh->slo_startup_us[r]), P[r][s]);
+            tasks[nt++] = x;
+        }
+    }
+    /* 2. every pool: online non-preemptive EDF of gang tasks */
+    uint32_t used = 0;
+    uint64_t cost = 0;
+    for (uint32_t p = 0; p < sh->n_pools; p++) {
+        uint64_t F[OR_MAXG];
+        uint32_t G = sh->gpus[p];
+        for (uint32_t g = 0; g < G; g++) F[g] = sh->pool_ready_us ? sh->pool_ready_us[p] : 0;
+        uint64_t busy = 0, tnow = 0;
+        int any = 0;
+        for (;;) {
+            int h = -1, left = 0;
+            for (uint32_t i = 0; i < nt; i++) {
+                if (tasks[i].pool != p || tasks[i].started) continue;
+                left = 1;
+                if (tasks[i].rel <= tnow && (h < 0 || task_before(&tasks[i], &tasks[h]))) h = (int)i;
+            }
+            if (!left) break;
+            if (h < 0) { /* nothing released: wait for the next release */
+                uint64_t nr = UINT64_MAX;
+                for (uint32_t i = 0; i < nt; i++)
+                    if (tasks[i].pool == p && !tasks[i].started && tasks[i].rel < nr) nr = tasks[i].rel;
+                tnow = nr;
+                continue;
+            }
+            sh_task *x = &tasks[h];
+            uint64_t fk = F[x->k - 1];
+            uint64_t st = tnow > fk ? tnow : fk;
+            /* a more urgent task released by the head's start takes the decision */
+            uint64_t u = UINT64_MAX;
+            for (uint32_t i = 0; i < nt; i++)
+                if (tasks[i].pool == p && !tasks[i].started && tasks[i].rel > tnow && task_before(&tasks[i], x) &&
+                    tasks[i].rel < u)
+                    u = tasks[i].rel;
+            if (u <= st) { tnow = u; continue; }
+            uint64_t e = st + x->t;
+            uint64_t nf[OR_MAXG];
+            uint32_t n = 0;
+            for (uint32_t g = x->k; g < G; g++) nf[n++] = F[g];
+            for (uint32_t g = 0; g < x->k; g++) nf[n++] = e;
+            qsort(nf, n, sizeof(uint64_t), cmp_u64);
+            for (uint32_t g = 0; g < G; g++) F[g] = nf[g];
+            busy += (uint64_t)x->k * x->t;
+            ready[x->r][x->s] = e;
+            x->started = 1;
+            tnow = st;
+            any = 1;
+        }
+        if (any) {
+            used |= 1u << p;
+            uint64_t end = 0;
+            for (uint32_t g = 0; g < G; g++) if (F[g] > end) end = F[g];
+            uint64_t X = sh->billing == 0 ? (uint64_t)G * end : busy;
+            cost += pool_cost(X, sh->price_mc[p]);
+        }
+    }
+    /* 3. per-request playback metrics in scene order (relative to T0_r), fleet record */
+    uint64_t late_t = 0, late_s = 0, Qs = 0, cnts = 0;
+    for (uint32_t r = 0; r < sh->n_req; r++) {
+        const or_problem *pb = &sh->req[r];
+        uint64_t R0 = 0, Q = 0;
+        int64_t M = 0;
+        uint32_t cnt = 0;
+        for (uint32_t s = 0; s < pb->S; s++) {
+            uint64_t e = ready[r][s] - sh->arrival_us[r];
+            if (ready_abs) ready_abs[r * 64 + s] = ready[r][s];
+            if (s == 0) { R0 = e; M = (int64_t)e; }
+            else if ((int64_t)e - (int64_t)P[r][s] > M) { M = (int64_t)e - (int64_t)P[r][s]; cnt++; }
+            if (lvl[r][s] != UINT32_MAX) Q += (pb->dur_us[s] / 1000) * pb->level_score[lvl[r][s]];
+        }
+        uint64_t stall = (uint64_t)M - R0;
+        cost += pb->fixed_cost_mc;
+        if (per_req) {
+            per_req[r].ttff_us = R0; per_req[r].stall_us = stall; per_req[r].cost_mc = pb->fixed_cost_mc;
+            per_req[r].quality = (uint32_t)Q; per_req[r].stall_count = (uint16_t)cnt; per_req[r].flags = 0;
+            per_req[r].pad = 0;
+        }
+        uint64_t lt = sat_sub(R0, sh->slo_startup_us[r]), ls = sat_sub(stall, sh->slo_stall_us[r]);
+        if (lt > late_t) late_t = lt;
+        if (ls > late_s) late_s = ls;
+        Qs += Q;
+        cnts += cnt;
+    }
+    fleet->ttff_us = late_t;
+    fleet->stall_us = late_s;
+    fleet->cost_mc = cost;
+    fleet->quality = (uint32_t)Qs;
+    fleet->stall_count = (uint16_t)cnts;
+    fleet->flags = (uint8_t)used;
+    fleet->pad = 0;
+    free(tasks);
+}
+
+static void shared_eval_fn(const void *ctx, uint64_t i, or_record *r) {
+    or_shared_eval((const or_shared *)ctx, i, r, NULL, NULL);
+}
+
+int or_shared_sweep(const or_shared *sh, uint64_t begin, uint64_t end, uint32_t nthreads, uint32_t nq,
+                    const or_query *queries, or_winner *winners, or_point *front_out, uint64_t front_cap,
+                    uint64_t *front_n, uint64_t *digest) {
+    return sweep_generic(NULL, shared_eval_fn, sh, sh->objective, begin, end, nthreads, nq, queries, winners,
+                         front_out, front_cap, front_n, digest);
 }
 
 /* Merge of two winners of the SAME query over disjoint candidate sets (e.g. pieces of a

@@ -9,6 +9,6 @@ times, no max-plus recurrence, no metrics, no cost rounding, no selection.
 See DESIGN.md "Input recipe" for the derivation of every constant.
 """
 from .generator import (  # noqa: F401
-    Problem, Query, make_config, make_fleet, CONFIG_NAMES, INF, SplitMix64,
+    Problem, Query, make_config, make_fleet, CONFIG_NAMES, INF, SplitMix64, SharedFleet, make_shared,
     LEVELS, GPU_CLASSES, va_seconds,
 )

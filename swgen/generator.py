@@ -373,3 +373,72 @@ def make_fleet(n_requests: int = 256, seed: int = 1004) -> List[Problem]:
                     stream_prefix="r%d/" % r)
         out.append(pb)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Shared-pool fleets (reading R36): several requests contend for the
+# SAME GPU pools, served by per-pool deadline (EDF) queues.  Nothing here
+# evaluates a plan: these are the inputs (requests, arrivals, SLOs, background plans).
+# ---------------------------------------------------------------------------
+@dataclass
+class SharedFleet:
+    name: str
+    requests: List[Problem]        # each request's scenes/tables; choice pools index the shared pools
+    arrival_us: List[int]          # T0_r
+    slo_startup_us: List[int]      # INF = batch (no SLO)
+    slo_stall_us: List[int]
+    fixed_index: List               # plan index of a background request, None = free (enumerated)
+    gpus: List[int]
+    price_mc: List[int]
+    pool_ready_us: List[int] = field(default_factory=list)
+    billing: int = 0
+    objective: int = 0
+    queries: List[Query] = field(default_factory=list)
+
+    @property
+    def n_candidates(self) -> int:
+        n = 1
+        for pb, fx in zip(self.requests, self.fixed_index):
+            if fx is None:
+                n *= pb.n_candidates
+        return n
+
+
+def make_shared(name: str) -> SharedFleet:
+    """SF2: two 2-minute requests (4 scenes) planned JOINTLY on shared A100x4 + H100x4
+    pools, a real-time one and one arriving 20 s later with a 50%-relaxed SLO.
+    SF3: the 1/3 real-time, 1/3 relaxed, 1/3 batch mix: a real-time and a
+    batch request in flight (background, fixed plans) and a NEW relaxed 5-minute request
+    whose plans are enumerated against that load."""
+    pools = [("A100", 4), ("H100", 4)]
+    if name == "SF2":
+        reqs = []
+        for r in range(2):
+            pb = _build("SF2.%d" % r, 2001, 120, 4, [(0, 0), (1, 1), (2, 2), (3, 3)], [0, 3], [1, 4],
+                        pools, True, False, lambda p: [], stream_prefix="r%d/" % r)
+            reqs.append(pb)
+        sf = SharedFleet("SF2", reqs, [0, 20 * D], [30 * D, 45 * D], [0, 60 * D], [None, None],
+                         [g for _, g in pools], [GPU_CLASSES[c][1] for c, _ in pools])
+        sf.queries = [Query(0, 0, INF), Query(0, 0, 40 * DOLLAR), Query(INF, INF, INF)]
+        return sf
+    if name == "SF3":
+        rt = _build("SF3.rt", 2003, 300, 10, [(0, 0), (1, 1), (2, 5), (6, 9)], [0, 1, 3], [1, 2, 4],
+                    pools, True, False, lambda p: [], stream_prefix="rt/")
+        bt = _build("SF3.batch", 2003, 300, 10, [(0, 0), (1, 1), (2, 5), (6, 9)], [0, 1, 3], [1, 2, 4],
+                    pools, True, False, lambda p: [], stream_prefix="batch/")
+        new = _build("SF3.new", 2003, 300, 10, [(0, 0), (1, 1), (2, 5), (6, 9)], [0, 1, 3], [1, 2, 4],
+                     pools, True, False, lambda p: [], stream_prefix="new/")
+        # background plans: real-time at LOW k = 4 on the H100 pool everywhere; batch at
+        # MED k = 1 on the A100 pool everywhere (level-major choice order, R19)
+        def plan_of(pb, choice):
+            c = pb.choices[: pb.radix[0]].index(choice)
+            i = 0
+            for r in pb.radix:
+                i = i * r + c
+            return i
+        sf = SharedFleet("SF3", [rt, bt, new], [0, 0, 15 * D], [30 * D, INF, 45 * D], [0, INF, 150 * D],
+                         [plan_of(rt, (0, 4, 1)), plan_of(bt, (1, 1, 0)), None],
+                         [g for _, g in pools], [GPU_CLASSES[c][1] for c, _ in pools])
+        sf.queries = [Query(0, 0, INF), Query(0, 0, 30 * DOLLAR), Query(INF, INF, INF)]
+        return sf
+    raise KeyError(name)

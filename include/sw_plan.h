@@ -367,6 +367,49 @@ sw_status sw_fleet_kernel_time(sw_fleet *f, uint32_t kind, uint64_t *n_launches,
                                uint64_t *bytes);
 uint64_t sw_fleet_launch_count(const sw_fleet *f);
 
+/* ---- shared-pool fleet (reading R36) ------------------ */
+
+/* Several requests contend for the SAME GPU pools.  "To coordinate multiple requests,
+ * model instances maintain local queues that prioritize tasks by deadline ... an early
+ * scene from a new request before a later scene from an earlier request if it has a
+ * tighter deadline"; heterogeneous SLOs -- real-time, 50% relaxed, batch --
+ * let the scheduler "prioritize real-time requests".  Reading R36: request r
+ * arrives at arrival_us; its scene s is released at arrival + a_s (its own LLM/TTS) and
+ * due at arrival + slo_startup_us + P_s (UINT64_MAX: batch); every pool is an online,
+ * non-preemptive EDF queue of gang tasks (the head = smallest (deadline, request, scene)
+ * among released tasks takes the k earliest-free GPUs; a more urgent task released
+ * before the head can start takes the decision).  A request with fixed_index != UINT64_MAX
+ * is background load with that fixed plan; the others are FREE and their plans are
+ * enumerated jointly (joint index: mixed radix over the free requests' digits, MSD = the
+ * first free request's first digit).  The fleet RECORD of a joint plan:
+ *   ttff_us  = max_r sat(ttff_r - slo_startup_r)  (worst startup lateness; ttff_r relative
+ *              to the request's arrival)
+ *   stall_us = max_r sat(stall_r - slo_stall_r)   (worst stall lateness)
+ *   cost_mc  = sum_r fixed_cost_mc[r] + sum_p pool cost over the fleet (billing of pools)
+ *   quality = sum_r Q_r, stall_count = sum_r count_r, flags = pools used,
+ * so sw_plan_select(h, 0, 0, budget) finds the best joint plan meeting EVERY request's SLO
+ * within the fleet budget (closest = least lateness).
+ * The result is an ordinary sw_plan handle (row = 1): eval / select / select_batch / sweep /
+ * sw_pareto_get / digest / records / detail / reset work unchanged (detail: the fleet
+ * record, pool ends, joint digits); stream and greedy are SW_EINVAL.  Limits: <= 16
+ * requests, <= 128 scenes in all, <= 16 joint digits.  tables/scenes/fixed_cost_mc/reqs
+ * have n entries (host, deep-copied); pools gives the shared pools (n_pools, gpus, prices,
+ * billing, objective, pool_ready_us; no eviction risk) -- every request's choices index
+ * them.  Collective like sw_plan_create when nranks > 1 (the joint space is sharded). */
+typedef struct {
+    uint64_t arrival_us;      /* T0_r */
+    uint64_t slo_startup_us;  /* deadline base and startup SLO (UINT64_MAX: batch) */
+    uint64_t slo_stall_us;    /* stall SLO */
+    uint64_t fixed_index;     /* background plan, or UINT64_MAX = free (enumerated) */
+} sw_shared_request;
+sw_status sw_shared_create(uint32_t n, const sw_profile_tables *tables, const sw_scene_list *scenes,
+                           const uint64_t *fixed_cost_mc, const sw_shared_request *reqs,
+                           const sw_price_table *pools, const sw_runtime *rt, sw_plan **out);
+/* Per-request metrics of joint candidate `index`: per_request[n] = (ttff, stall relative to
+ * the request's arrival, cost = its fixed cost, quality, stall count, flags 0) and, if
+ * ready_abs is not NULL, the absolute ready time of every scene, request-major. */
+sw_status sw_shared_detail(sw_plan *h, uint64_t index, sw_record *per_request, uint64_t *ready_abs);
+
 /* ---- multi-GPU --------------------------------------------- */
 
 /* Row-aligned contiguous shard of [begin, end) for `rank` of `nranks`: whole rows

@@ -31,6 +31,8 @@ class OrProblem(C.Structure):
         ("B", C.c_uint32), ("radix", U32P), ("first_scene", U32P),
         ("choice_level", U32P), ("choice_k", U32P), ("choice_pool", U32P),
         ("va_us", U64P), ("pool_ready_us", U64P), ("evict_risk_permille", U32P),
+        ("vae_us", U64P), ("choice_vae_pool", U32P), ("metric", C.c_uint32),
+        ("power_active_w", U32P), ("power_idle_w", U32P),
     ]
 
 
@@ -136,7 +138,13 @@ class Oracle:
             choice_pool=a(C.c_uint32, [x[2] for x in ch]),
             va_us=a(C.c_uint64, pb.va_us),
             pool_ready_us=a(C.c_uint64, pb.pool_ready_us) if getattr(pb, "pool_ready_us", None) else None,
-            evict_risk_permille=a(C.c_uint32, risk) if risk else None)
+            evict_risk_permille=a(C.c_uint32, risk) if risk else None,
+            vae_us=a(C.c_uint64, pb.vae_us) if getattr(pb, "vae_us", None) else None,
+            choice_vae_pool=a(C.c_uint32, [0xFFFFFFFF if x is None else x for x in pb.choice_vae_pool])
+            if getattr(pb, "vae_us", None) else None,
+            metric=getattr(pb, "metric", 0),
+            power_active_w=a(C.c_uint32, pb.power_active_w) if getattr(pb, "metric", 0) else None,
+            power_idle_w=a(C.c_uint32, pb.power_idle_w) if getattr(pb, "metric", 0) else None)
 
     def _k(self, x):
         self._keep.append(x)

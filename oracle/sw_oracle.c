@@ -64,6 +64,14 @@ typedef struct {
                                          (model load + warm-up; reading R31) */
     const uint32_t *evict_risk_permille; /* [n_pools] or NULL: Spot eviction risk of pool p
                                          over the request, 1/1000 (reading R32) */
+    const uint64_t *vae_us;           /* NULL, or block-major like va_us: the VAE stage time of a
+                                         disaggregated choice (reading R37) */
+    const uint32_t *choice_vae_pool;  /* NULL, or [sum radix]: pool running the choice's VAE
+                                         stage on 1 GPU; UINT32_MAX = VAE folded into V+A */
+    uint32_t metric;                  /* 0: cost in milli-cents; 1: energy in microjoules
+                                         (reading R38) */
+    const uint32_t *power_active_w;   /* [n_pools] busy GPU power (metric 1) */
+    const uint32_t *power_idle_w;     /* [n_pools] idle GPU power (metric 1) */
 } or_problem;
 
 typedef struct {
@@ -222,6 +230,24 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
         for (uint32_t g = 0; g < G; g++) F[p][g] = nf[g];
         used |= 1u << p;
         busy[p] += (uint64_t)k * t;
+        uint32_t vp = pb->choice_vae_pool ? pb->choice_vae_pool[coff + c] : UINT32_MAX;
+        if (vp != UINT32_MAX) {
+            /* "FramePack DiT streams latent outputs to the VAE for decoding ... This enables
+               pipelined execution" (reading R37): the scene's VAE runs on its own
+               pool, one GPU (the VAE is not parallelised), once its DiT finished and
+               a VAE GPU is free; the DiT pool meanwhile serves the next scene */
+            uint64_t tv = pb->vae_us[voff + (s - pb->first_scene[b]) * pb->radix[b] + c];
+            uint64_t fv = F[vp][0];
+            uint64_t ev = (e > fv ? e : fv) + tv;
+            uint32_t Gv = pb->gpus[vp], m = 0;
+            for (uint32_t g = 1; g < Gv; g++) nf[m++] = F[vp][g];
+            nf[m++] = ev;
+            qsort(nf, m, sizeof(uint64_t), cmp_u64);
+            for (uint32_t g = 0; g < Gv; g++) F[vp][g] = nf[g];
+            used |= 1u << vp;
+            busy[vp] += tv;
+            e = ev;
+        }
         if (ready_us) ready_us[s] = e;
         if (s == 0) {
             R0 = e;
@@ -240,8 +266,18 @@ void or_eval_detail(const or_problem *pb, const uint64_t *a, const uint64_t *P,
         if (pool_end_us) pool_end_us[p] = end;
         if (end > mk) mk = end;
         if (used & (1u << p)) {
-            uint64_t X = pb->billing == 0 ? billed_gpus(pb, p) * end : busy[p];
-            cost += pool_cost(X, pb->price_mc[p]);
+            if (pb->metric == 1) {
+                /* energy ("optimizing for energy"; reading R38): busy GPUs draw their
+                   active power (TDP, "average power remains within 10% of the peak"),
+                   the pool's other rented GPUs their idle power ("63W when idle")
+                   until the pool's last finish (RESERVED); BUSY: busy GPU time only.  W x us
+                   = microjoules, exact */
+                uint64_t idle_us = pb->billing == 0 ? billed_gpus(pb, p) * end - busy[p] : 0;
+                cost += (uint64_t)pb->power_active_w[p] * busy[p] + (uint64_t)pb->power_idle_w[p] * idle_us;
+            } else {
+                uint64_t X = pb->billing == 0 ? billed_gpus(pb, p) * end : busy[p];
+                cost += pool_cost(X, pb->price_mc[p]);
+            }
         }
     }
     rec->ttff_us = R0;

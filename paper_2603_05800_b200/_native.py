@@ -143,8 +143,11 @@ EXPORTS = {
     "sw_plan_decode": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint8)]),
     "sw_plan_segments": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint64, U64P]),
     "sw_comm_loopback_create": (C.c_int32, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "sw_shared_create": (C.c_int32, [C.c_uint32, C.c_void_p, C.c_void_p, U64P, C.c_void_p,
+                                     C.POINTER(sw_price_table), C.POINTER(sw_runtime), C.POINTER(C.c_void_p)]),
+    "sw_shared_detail": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(sw_record), U64P]),
 }
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _lib = None
 
@@ -498,6 +501,62 @@ class Plan:
         ms = C.c_float()
         self._ck(lib().sw_plan_last_eval_ms(self.h, C.byref(ms)))
         return ms.value
+
+
+class sw_shared_request(C.Structure):
+    _fields_ = [("arrival_us", C.c_uint64), ("slo_startup_us", C.c_uint64), ("slo_stall_us", C.c_uint64),
+                ("fixed_index", C.c_uint64)]
+
+
+class SharedPlan(Plan):
+    """A shared-pool fleet (sw_shared_create): requests contending for the same pools under
+    per-pool EDF queues; the handle is a Plan over the joint plans of the free requests
+    (``sf`` duck-typed like swgen.SharedFleet: requests, arrival_us, slo_startup_us,
+    slo_stall_us, fixed_index (None = free), gpus, price_mc, pool_ready_us, billing,
+    objective)."""
+
+    def __init__(self, sf, device: int = 0, stream: Optional[int] = None, comm: Optional[int] = None,
+                 rank: int = 0, nranks: int = 1, record_capacity: int = 0):
+        L = lib()
+        self._keep = []
+        n = len(sf.requests)
+        imgs = [_marshal(pb, self._keep) for pb in sf.requests]
+        scs = (sw_scene_list * n)(*[i[0] for i in imgs])
+        tbs = (sw_profile_tables * n)(*[i[1] for i in imgs])
+        fixed = _arr(C.c_uint64, [pb.fixed_cost_mc for pb in sf.requests])
+        reqs = (sw_shared_request * n)(*[sw_shared_request(a, t, s, UINT64_MAX if x is None else x)
+                                         for a, t, s, x in zip(sf.arrival_us, sf.slo_startup_us,
+                                                               sf.slo_stall_us, sf.fixed_index)])
+        ready = getattr(sf, "pool_ready_us", None)
+        pools = sw_price_table(len(sf.gpus), _arr(C.c_uint32, sf.gpus), _arr(C.c_uint64, sf.price_mc), 0,
+                               sf.billing, sf.objective, _arr(C.c_uint64, ready) if ready else None, None)
+        rt = sw_runtime(device, C.c_void_p(stream or 0), C.c_void_p(comm or 0), rank, nranks,
+                        record_capacity, ALLOC_FN(0), FREE_FN(0), None)
+        self._keep += [scs, tbs, fixed, reqs, pools, rt]
+        h = C.c_void_p()
+        st = L.sw_shared_create(n, C.cast(tbs, C.c_void_p), C.cast(scs, C.c_void_p), fixed,
+                                C.cast(reqs, C.c_void_p), C.byref(pools), C.byref(rt), C.byref(h))
+        if st < 0:
+            raise SwError(st, L.sw_last_error(None).decode(errors="replace"))
+        self.sf = sf
+        nd = sum(len(pb.radix) for pb, x in zip(sf.requests, sf.fixed_index) if x is None)
+
+        class _Shape:  # what Plan._adopt reads
+            gpus, radix, S = sf.gpus, [0] * nd, min(64, sum(pb.S for pb in sf.requests))
+        self._adopt(h, _Shape, owned=True)
+
+    def shared_detail(self, index: int):
+        """-> ([per-request (ttff, stall, fixed cost, Q, count, 0)], [[absolute ready times] per request])."""
+        n = len(self.sf.requests)
+        per = (sw_record * n)()
+        tot = sum(pb.S for pb in self.sf.requests)
+        ready = (C.c_uint64 * max(1, tot))()
+        self._ck(lib().sw_shared_detail(self.h, index, per, ready))
+        out, off = [], 0
+        for pb in self.sf.requests:
+            out.append(list(ready[off: off + pb.S]))
+            off += pb.S
+        return [x.astuple() for x in per], out
 
 
 class Fleet:

@@ -57,6 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     inc, lib = nccl_paths()
+    src_hash = source_hash()  # of the sources as they are when the compile starts
     cmd = [
         "nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
         "-Xcompiler", "-fPIC", "-shared",
@@ -74,7 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(r.stderr)
     with open(STAMP, "w") as f:
-        f.write(source_hash() + "\n")
+        f.write(src_hash + "\n")
     return LIB
 
 

@@ -31,10 +31,11 @@ struct __align__(16) VaEntry {
 // floor((Y + X_t) / D) = qY + cq + (rY + cr >= D) for Y = qY * D + rY.
 struct __align__(16) LsdEntry {
     uint64_t t_us;
-    uint32_t q;
-    uint32_t dl;
     uint64_t cq;
-    uint64_t cr;
+    uint32_t cr;   // < 3.6e9: 32 bits
+    uint32_t q;
+    uint32_t off;  // byte offset of choice dl's record within a lane's MID run: dl x 32 x 32 B
+    uint32_t dl;
 };
 
 // Per-request constants, packed ON THE DEVICE by pack_kernel, staged into shared
@@ -158,7 +159,8 @@ __device__ __forceinline__ void gang_update_dyn(uint64_t (&F)[kMaxG], uint64_t e
 
 // One scene-step on pool p with degree k; returns the scene's ready time e = R_s.
 // KS > 0: k is a compile-time constant (warp-uniform MID/LSD loops); KS == 0: runtime.
-template <int NP, int KS>
+// BUSY: accumulate k x t (BUSY billing); RESERVED billing never reads it.
+template <int NP, int KS, bool BUSY = true>
 __device__ __forceinline__ uint64_t scene_step(State<NP>& st, uint32_t p, uint32_t k,
                                                uint64_t a, uint64_t t) {
     // STATIC rung (k = 0, runtime path only): no video stage, no GPU -- the scene is
@@ -174,16 +176,16 @@ __device__ __forceinline__ uint64_t scene_step(State<NP>& st, uint32_t p, uint32
             if (KS) gang_update_static<KS>(st.F[q], e);
             else gang_update_dyn(st.F[q], e, k);
             st.end[q] = umax64(st.end[q], e);
-            st.busy[q] += (uint64_t)k * t;
+            if (BUSY) st.busy[q] += (uint64_t)k * t;
         }
     }
     st.used |= 1u << p;
     return e;
 }
 
-// Playback metrics after scene s ready at e (R7-R9).
-template <int NP>
-__device__ __forceinline__ void scene_metrics(State<NP>& st, uint32_t s, uint64_t e,
+// Playback metrics after scene s ready at e (R7-R9); St = State<NP> or MidState.
+template <class St>
+__device__ __forceinline__ void scene_metrics(St& st, uint32_t s, uint64_t e,
                                               uint64_t Ps, uint32_t q) {
     if (s == 0) {
         st.R0 = e;
@@ -200,16 +202,84 @@ __device__ __forceinline__ void scene_metrics(State<NP>& st, uint32_t s, uint64_
 
 // Dispatch a runtime k to a compile-time specialisation (k warp-uniform => no
 // divergence; k in {1,2,4,8} covers USP degrees dividing the 40 heads).
-template <int NP>
+template <int NP, bool BUSY = true>
 __device__ __forceinline__ uint64_t scene_step_uniform(State<NP>& st, uint32_t p, uint32_t k,
                                                        uint64_t a, uint64_t t) {
     switch (k) {
-        case 1: return scene_step<NP, 1>(st, p, k, a, t);
-        case 2: return scene_step<NP, 2>(st, p, k, a, t);
-        case 4: return scene_step<NP, 4>(st, p, k, a, t);
-        case 8: return scene_step<NP, 8>(st, p, k, a, t);
-        default: return scene_step<NP, 0>(st, p, k, a, t);
+        case 1: return scene_step<NP, 1, BUSY>(st, p, k, a, t);
+        case 2: return scene_step<NP, 2, BUSY>(st, p, k, a, t);
+        case 4: return scene_step<NP, 4, BUSY>(st, p, k, a, t);
+        case 8: return scene_step<NP, 8, BUSY>(st, p, k, a, t);
+        default: return scene_step<NP, 0, BUSY>(st, p, k, a, t);
     }
+}
+
+// MID state (eval tiles): the HI state of a row is shared by its rm MID choices, and a
+// MID choice (k, pool pm) changes only pool pm -- so the MID pass works on a copy of
+// that one pool's free times (the other pools are read from the HI state).  Keeps the
+// live state at (NP + 1) pools instead of 2 NP (no spills with 3-4 pools).
+struct MidState {
+    uint64_t F[kMaxG];
+    uint64_t end, busy;
+    uint64_t R0;
+    int64_t M;
+    uint32_t cnt, Q, used, pm;
+};
+
+template <int NP>
+__device__ __forceinline__ void mid_init(MidState& m, const State<NP>& st, uint32_t pm) {
+#pragma unroll
+    for (int g = 0; g < kMaxG; g++) m.F[g] = st.F[0][g];
+    m.end = st.end[0];
+    m.busy = st.busy[0];
+#pragma unroll
+    for (int q = 1; q < NP; q++)
+        if ((uint32_t)q == pm) {
+#pragma unroll
+            for (int g = 0; g < kMaxG; g++) m.F[g] = st.F[q][g];
+            m.end = st.end[q];
+            m.busy = st.busy[q];
+        }
+    m.R0 = st.R0;
+    m.M = st.M;
+    m.cnt = st.cnt;
+    m.Q = st.Q;
+    m.used = st.used;
+    m.pm = pm;
+}
+
+// One MID scene step on pool pm (KS compile-time k; KS == 0: runtime k incl. STATIC).
+template <int KS, bool BUSY>
+__device__ __forceinline__ uint64_t mid_step(MidState& m, uint32_t k, uint64_t a, uint64_t t) {
+    if (KS == 0 && k == 0) return a;  // STATIC rung (R33)
+    const uint64_t fk = KS ? m.F[KS - 1] : sel_dyn(m.F, k - 1);
+    const uint64_t e = umax64(a, fk) + t;
+    if (KS) gang_update_static<KS>(m.F, e);
+    else gang_update_dyn(m.F, e, k);
+    m.end = umax64(m.end, e);
+    if (BUSY) m.busy += (uint64_t)k * t;
+    m.used |= 1u << m.pm;
+    return e;
+}
+
+// The full state after the MID pass (generic LSD path).
+template <int NP>
+__device__ __forceinline__ State<NP> merge_mid(const State<NP>& st, const MidState& m) {
+    State<NP> s2 = st;
+#pragma unroll
+    for (int q = 0; q < NP; q++)
+        if ((uint32_t)q == m.pm) {
+#pragma unroll
+            for (int g = 0; g < kMaxG; g++) s2.F[q][g] = m.F[g];
+            s2.end[q] = m.end;
+            s2.busy[q] = m.busy;
+        }
+    s2.R0 = m.R0;
+    s2.M = m.M;
+    s2.cnt = m.cnt;
+    s2.Q = m.Q;
+    s2.used = m.used;
+    return s2;
 }
 
 // Packed 32 B record: {ttff, stall, cost, Q | cnt << 32 | flags << 48}.

@@ -108,8 +108,9 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
             le.t_us = v.t_us;
             le.q = v.q;
             le.dl = dl;
+            le.off = dl * kTileRows * (uint32_t)sizeof(Rec4);  // see StoreEmit
             le.cq = X / kUsPerHour;
-            le.cr = X % kUsPerHour;
+            le.cr = (uint32_t)(X % kUsPerHour);
             hdr->lsd[j] = le;
         }
     }
@@ -120,54 +121,63 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
 // so per candidate  e = max(a_s, F_p[k-1]) + t,  end_p' = max(end_p, e),
 // cost = sum_{q != p} cost_q + round((G_p price_p end_p' + 1.8e9) / 3.6e9)  (RESERVED)
 // or busy_p + k t (BUSY), the playback metrics of the new scene and one 32 B store.
-// Choices are visited grouped by (p, k) (create-time table), so max(a_s, F_p[k-1]),
-// the pool selection and the other pools' cost hoist out of the inner loop.
+// Choices are visited grouped by (p, k) (create-time table), and everything that does
+// not depend on the choice's stage time t is hoisted into per-group thresholds:
+//   e > end_p          <=>  t > end_p - st0           (st0 = max(a_s, F_p[k-1]))
+//   R_s - P_s > M      <=>  t > M - (st0 - P_s)       (a new rebuffering maximum, R8)
+//   cost carry         <=>  cr >= 3.6e9 - rY          (rY: remainder of the hoisted part)
+// so a candidate costs two 16 B table loads, a few 64-bit compares/selects and the store.
 template <int K, int NP>
-__device__ __forceinline__ uint64_t fk_of(const State<NP>& st, uint32_t p) {
-    uint64_t r = 0;
+__device__ __forceinline__ uint64_t fk_of(const State<NP>& st, const MidState& m, uint32_t p) {
+    // F_p[K-1], pool p's free times taken from the MID copy when p is the MID pool
+    uint64_t r = m.F[K - 1];
 #pragma unroll
     for (int q = 0; q < NP; q++)
-        if ((uint32_t)q == p) r = st.F[q][K - 1];
+        if ((uint32_t)q == p && p != m.pm) r = st.F[q][K - 1];
     return r;
 }
 
 template <int NP>
-__device__ __forceinline__ uint64_t fk_dyn(const State<NP>& st, uint32_t p, uint32_t k) {
+__device__ __forceinline__ uint64_t fk_pool(const State<NP>& st, const MidState& m, uint32_t p, uint32_t k) {
     switch (k) {
-        case 1: return fk_of<1, NP>(st, p);
-        case 2: return fk_of<2, NP>(st, p);
-        case 4: return fk_of<4, NP>(st, p);
-        case 8: return fk_of<8, NP>(st, p);
+        case 1: return fk_of<1, NP>(st, m, p);
+        case 2: return fk_of<2, NP>(st, m, p);
+        case 4: return fk_of<4, NP>(st, m, p);
+        case 8: return fk_of<8, NP>(st, m, p);
         default: {
-            uint64_t r = 0;
+            uint64_t r = sel_dyn(m.F, k - 1);
 #pragma unroll
             for (int q = 0; q < NP; q++)
-                if ((uint32_t)q == p) r = sel_dyn(st.F[q], k - 1);
+                if ((uint32_t)q == p && p != m.pm) r = sel_dyn(st.F[q], k - 1);
             return r;
         }
     }
 }
 
 template <int NP, bool BUSY, class Put>
-__device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2, Put&& put) {
+__device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& st, const MidState& m, Put&& put) {
     const uint32_t bl = h.B - 1;
     const uint32_t s = h.first[bl];  // s >= 1 on this path
     const uint64_t as = h.a[s];
     const int64_t Ps = (int64_t)h.P[s];
-    uint64_t pc[NP];
+    uint64_t pc[NP], endq[NP], busyq[NP];
     uint64_t pcsum = h.fixed_cost;
 #pragma unroll
     for (int q = 0; q < NP; q++) {
-        pc[q] = BUSY ? pool_cost(s2.busy[q], h.price[q]) : (s2.end[q] * h.Gprice[q] + kHalfHour) / kUsPerHour;
+        endq[q] = (uint32_t)q == m.pm ? m.end : st.end[q];
+        busyq[q] = (uint32_t)q == m.pm ? m.busy : st.busy[q];
+        pc[q] = BUSY ? pool_cost(busyq[q], h.price[q]) : (endq[q] * h.Gprice[q] + kHalfHour) / kUsPerHour;
         pcsum += pc[q];
     }
-    const uint64_t R0 = s2.R0;
-    const int64_t M0 = s2.M;
-    const uint64_t w3base = (uint64_t)s2.Q | ((uint64_t)s2.cnt << 32) | ((uint64_t)s2.used << 48);
+    const uint64_t R0 = m.R0;
+    const int64_t M0 = m.M;
+    const uint64_t B1 = (uint64_t)M0 - R0;  // w1 = stall when the scene sets no new maximum
+    const uint64_t w3base = (uint64_t)m.Q | ((uint64_t)m.cnt << 32) | ((uint64_t)(st.used | m.used) << 48);
     const uint32_t ng = h.lsd_ngroups;
     for (uint32_t g = 0; g < ng; g++) {
         const uint32_t pk = h.lsd_pk[g];
         const uint32_t p = pk & 0xffu, k = pk >> 8;
+        const uint32_t j0 = h.lsd_goff[g], j1 = h.lsd_goff[g + 1];
         if (k == 0) {  // STATIC rung (R33): R_s = a_s, no pool touched, nothing billed
             const int64_t d = (int64_t)as - Ps;
             const bool nm = d > M0;
@@ -176,10 +186,10 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2
             r.w1 = (uint64_t)(nm ? d : M0) - R0;
             r.w2 = pcsum;
             const uint64_t w3s = w3base + (nm ? (1ull << 32) : 0ull);
-            for (uint32_t j = h.lsd_goff[g]; j < h.lsd_goff[g + 1]; j++) {
+            for (uint32_t j = j0; j < j1; j++) {
                 const LsdEntry E = h.lsd[j];
                 r.w3 = w3s + E.q;
-                put(E.dl, r);
+                put(E.dl, E.off, r);
             }
             continue;
         }
@@ -187,58 +197,70 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& s2
 #pragma unroll
         for (int q = 0; q < NP; q++)
             if ((uint32_t)q == p) {
-                endp = s2.end[q];
-                busyp = s2.busy[q];
+                endp = endq[q];
+                busyp = busyq[q];
                 pcp = pc[q];
                 A = h.Gprice[q];
                 price = h.price[q];
             }
-        const uint64_t st0 = umax64(as, fk_dyn<NP>(s2, p, k));
+        const uint64_t st0 = umax64(as, fk_pool<NP>(st, m, p, k));
         const uint64_t base = pcsum - pcp;
         // Y = (prefix part of X_p) * price + 1.8e9 = qY * D + rY
         const uint64_t Y = (BUSY ? busyp * price : A * st0) + kHalfHour;
         const uint64_t qY = Y / kUsPerHour, rY = Y - qY * kUsPerHour;
         const uint64_t cnew0 = base + qY, cold = base + pcp;
+        const uint32_t Dm = (uint32_t)(kUsPerHour - rY);  // carry iff cr >= Dm (rY + cr >= D)
         const int64_t dd0 = (int64_t)st0 - Ps;
+        const int64_t thrE = (int64_t)endp - (int64_t)st0;  // e > end_p <=> t > thrE
+        const int64_t thrM = M0 - dd0;                     // new maximum <=> t > thrM
+        const uint64_t A1 = (uint64_t)(dd0 - (int64_t)R0);  // w1 on a new maximum: A1 + t
         const uint64_t w3g = w3base | ((uint64_t)(1u << p) << 48);
-        const uint32_t j1 = h.lsd_goff[g + 1];
-        for (uint32_t j = h.lsd_goff[g]; j < j1; j++) {
+        for (uint32_t j = j0; j < j1; j++) {
             const LsdEntry E = h.lsd[j];
-            const uint64_t e = st0 + E.t_us;
-            const uint64_t cnew = cnew0 + E.cq + ((rY + E.cr) >= kUsPerHour ? 1u : 0u);
-            const uint64_t cost = BUSY ? cnew : (e > endp ? cnew : cold);
-            const int64_t d = dd0 + (int64_t)E.t_us;
-            const bool nm = d > M0;  // a new rebuffering maximum (R8)
-            const int64_t M = nm ? d : M0;
+            const int64_t t = (int64_t)E.t_us;
+            const uint64_t cnew = cnew0 + E.cq + (E.cr >= Dm ? 1u : 0u);
+            const bool nm = t > thrM;
             Rec4 r;
             r.w0 = R0;
-            r.w1 = (uint64_t)M - R0;
-            r.w2 = cost;
+            r.w1 = nm ? A1 + (uint64_t)t : B1;
+            r.w2 = BUSY ? cnew : (t > thrE ? cnew : cold);
             r.w3 = (w3g + E.q) + (nm ? (1ull << 32) : 0ull);
-            put(E.dl, r);  // a7 store, or the fused select + Pareto filter (stream)
+            put(E.dl, E.off, r);  // a7 store, or the fused select + Pareto filter (stream)
         }
     }
 }
 
 // Scenes [f0, f1) of one digit's block with choice (p, k), gang update specialised for K
 // (K = 0: runtime k).
-template <int NP, int K>
+template <int NP, int K, bool BUSY = true>
 __device__ __forceinline__ void run_block(State<NP>& st, const DevHeader& h, uint32_t p, uint32_t k, uint32_t f0,
                                           uint32_t f1, const VaEntry* vb, uint32_t r, uint64_t* ready = nullptr) {
     for (uint32_t s = f0; s < f1; s++) {
         const VaEntry v = vb[(s - f0) * r];
-        const uint64_t e = scene_step<NP, K>(st, p, k, h.a[s], v.t_us);
+        const uint64_t e = scene_step<NP, K, BUSY>(st, p, k, h.a[s], v.t_us);
         scene_metrics(st, s, e, h.P[s], v.q);
         if (ready) ready[s] = e;
     }
 }
 
+// MID block scenes [f0, f1) on the MID copy, compile-time K.
+template <int K, bool BUSY>
+__device__ __forceinline__ void mid_block(MidState& m, const DevHeader& h, uint32_t k, uint32_t f0, uint32_t f1,
+                                          const VaEntry* vb, uint32_t r) {
+    for (uint32_t s = f0; s < f1; s++) {
+        const VaEntry v = vb[(s - f0) * r];
+        const uint64_t e = mid_step<K, BUSY>(m, k, h.a[s], v.t_us);
+        scene_metrics(m, s, e, h.P[s], v.q);
+    }
+}
+
 // ============================================================================ a1-a7 eval
 // Lane <-> row H: the candidates [H*row, (H+1)*row) share their HI digits (digits
-// 0..B-3); a warp owns a tile of 32 consecutive rows (tiled record layout, sw_plan.h).  The thread simulates the HI scenes once (per-lane choices, runtime k/pool),
-// then iterates the MID digit and the LSD digit in lock-step with the other lanes:
-// (k, pool) is warp-uniform there, so the gang update uses compile-time slot indices
-// and the LSD step (the dominant loop) is ~40 integer ops + one 32 B store.
+// 0..B-3); a warp owns a tile of 32 consecutive rows (tiled record layout, sw_plan.h).
+// The thread simulates the HI scenes once (per-lane choices, runtime k/pool), then
+// iterates the MID digit and the LSD digit in lock-step with the other lanes: (k, pool)
+// is warp-uniform there, so the gang update uses compile-time slot indices and the LSD
+// step (the dominant loop) is a few integer ops + one 32 B store.
 // Amortised scene-steps per candidate: L_LSD + L_MID / r_LSD + L_HI / row.
 // One eval launch's work for one request: its tables and the tile range to write.
 struct EvalJob {
@@ -250,16 +272,15 @@ struct EvalJob {
 };
 
 // One tile (32 consecutive rows, lane <-> row H = t * 32 + lane) of candidates: record
-// (dm, dl) of the lane's row goes to emit.at(dm, live)(dl, r) -- the 32 B store of the
-// eval kernel, or the fused select + Pareto filter of the stream kernel.
-template <int NP, class Emit>
-__device__ __forceinline__ void eval_tile(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit) {
+// (dm, dl) of the lane's row goes to emit.at(dm, live)(dl, off, r) -- the 32 B store of
+// the eval kernel, or the fused select + Pareto filter of the stream kernel.
+template <int NP, bool BUSY, class Emit>
+__device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit) {
     const uint32_t bm = h.B - 2, bl = h.B - 1;
     const uint32_t rm = h.radix[bm], rl = h.radix[bl];
     const uint32_t mfirst = h.first[bm], mlast = h.first[bm + 1];
     const uint32_t lfirst = h.first[bl], llast = h.first[bl + 1];
     const uint64_t n_rows = h.n_rows;
-    const bool busy_bill = h.flags & 2u;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t Hraw = t * kTileRows + lane;
     const bool live = Hraw < n_rows;  // the last tile may run past the space
@@ -284,43 +305,46 @@ __device__ __forceinline__ void eval_tile(const DevHeader& h, const VaEntry* va,
         // variants measured 12% slower overall on C2)
         if (__all_sync(0xffffffffu, ch == __shfl_sync(0xffffffffu, ch, 0))) {
             switch (k) {
-                case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
-                case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
-                case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
-                case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
-                default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
+                case 1: run_block<NP, 1, BUSY>(st, h, p, k, f0, f1, vb, r); break;
+                case 2: run_block<NP, 2, BUSY>(st, h, p, k, f0, f1, vb, r); break;
+                case 4: run_block<NP, 4, BUSY>(st, h, p, k, f0, f1, vb, r); break;
+                case 8: run_block<NP, 8, BUSY>(st, h, p, k, f0, f1, vb, r); break;
+                default: run_block<NP, 0, BUSY>(st, h, p, k, f0, f1, vb, r); break;
             }
         } else {
-            run_block<NP, 0>(st, h, p, k, f0, f1, vb, r);
+            run_block<NP, 0, BUSY>(st, h, p, k, f0, f1, vb, r);
         }
     }
-    // ---- MID digit: warp-uniform choice
+    // ---- MID digit: warp-uniform choice (k, pm) on a copy of pool pm only
     for (uint32_t dm = 0; dm < rm; dm++) {
-        State<NP> s2 = st;
+        const uint32_t ch = h.choice[h.coff[bm] + dm];
+        const uint32_t k = ch_k(ch), pm = ch_pool(ch);
+        MidState m;
+        mid_init<NP>(m, st, pm);
         {
-            const uint32_t ch = h.choice[h.coff[bm] + dm];
-            const uint32_t k = ch_k(ch), p = ch_pool(ch);
             const VaEntry* vb = va + h.voff[bm] + dm;
-            for (uint32_t s = mfirst; s < mlast; s++) {
-                const VaEntry v = vb[(s - mfirst) * rm];
-                const uint64_t e = scene_step_uniform<NP>(s2, p, k, h.a[s], v.t_us);
-                scene_metrics(s2, s, e, h.P[s], v.q);
+            switch (k) {
+                case 1: mid_block<1, BUSY>(m, h, k, mfirst, mlast, vb, rm); break;
+                case 2: mid_block<2, BUSY>(m, h, k, mfirst, mlast, vb, rm); break;
+                case 4: mid_block<4, BUSY>(m, h, k, mfirst, mlast, vb, rm); break;
+                case 8: mid_block<8, BUSY>(m, h, k, mfirst, mlast, vb, rm); break;
+                default: mid_block<0, BUSY>(m, h, k, mfirst, mlast, vb, rm); break;
             }
         }
-        auto put = emit.at(dm, live);  // put(dl, r): record (dm, dl) of this lane's row
+        auto put = emit.at(dm, live);  // put(dl, off, r): record (dm, dl) of this lane's row
         if (llast - lfirst == 1 && lfirst != 0) {
-            if (busy_bill) lsd_fast<NP, true>(h, s2, put);
-            else lsd_fast<NP, false>(h, s2, put);
+            lsd_fast<NP, BUSY>(h, st, m, put);
         } else {
             // ---- generic LSD block (several scenes share the last digit)
+            const State<NP> s2 = merge_mid<NP>(st, m);
             for (uint32_t dl = 0; dl < rl; dl++) {
                 State<NP> s3 = s2;
-                const uint32_t ch = h.choice[h.coff[bl] + dl];
-                const uint32_t k = ch_k(ch), p = ch_pool(ch);
+                const uint32_t chl = h.choice[h.coff[bl] + dl];
+                const uint32_t kl = ch_k(chl), pl = ch_pool(chl);
                 const VaEntry* vb = va + h.voff[bl] + dl;
                 for (uint32_t s = lfirst; s < llast; s++) {
                     const VaEntry v = vb[(s - lfirst) * rl];
-                    const uint64_t e = scene_step_uniform<NP>(s3, p, k, h.a[s], v.t_us);
+                    const uint64_t e = scene_step_uniform<NP, BUSY>(s3, pl, kl, h.a[s], v.t_us);
                     scene_metrics(s3, s, e, h.P[s], v.q);
                 }
                 Rec4 r;
@@ -328,27 +352,48 @@ __device__ __forceinline__ void eval_tile(const DevHeader& h, const VaEntry* va,
                 r.w1 = (uint64_t)s3.M - s3.R0;
                 r.w2 = state_cost(s3, h);
                 r.w3 = (uint64_t)s3.Q | ((uint64_t)s3.cnt << 32) | ((uint64_t)s3.used << 48);
-                put(dl, r);
+                put(dl, dl * kTileRows * (uint32_t)sizeof(Rec4), r);
             }
         }
     }
 }
 
-// a7: the 32 B store of one record (the eval kernel's sink for lsd_fast)
+template <int NP, class Emit>
+__device__ __forceinline__ void eval_tile(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit) {
+    if (h.flags & 2u) eval_tile_b<NP, true>(h, va, t, emit);  // BUSY billing (uniform branch)
+    else eval_tile_b<NP, false>(h, va, t, emit);
+}
+
+// a7: the 32 B store.  Record (dm, dl) of the lane's row lands at tile_out + (dm * rl +
+// dl) * 32: a warp store covers 32 consecutive records (1 KB, fully coalesced).  Lanes past
+// the end of the space (last tile only) write their tile-padding slot (the tile is
+// allocated whole; scans skip indices outside the segment), so the store is unconditional.
 struct StoreEmit {
+    Rec4* tile_out;  // this lane's first slot in its tile
+    uint32_t rl;
     struct Put {
-        Rec4* lane_out;
-        bool live;
-        __device__ __forceinline__ void operator()(uint32_t dl, const Rec4& r) const {
-            if (live) st_global_256(lane_out + (size_t)dl * kTileRows, r);
+        char* lane_out;
+        __device__ __forceinline__ void operator()(uint32_t, uint32_t off, const Rec4& r) const {
+            st_global_256(lane_out + off, r);
         }
     };
+    __device__ __forceinline__ Put at(uint32_t dm, bool) const {
+        return Put{reinterpret_cast<char*>(tile_out + (size_t)dm * rl * kTileRows)};
+    }
 };
+
+// Resident CTAs per SM the register allocation is sized for, per pool count: the state
+// grows with the pools (NP + 1 pools of 8 free times live in the MID/LSD loops), and
+// these are the largest occupancies whose hot loops do not spill (ptxas -v).
+constexpr int kEvalMinBlocks[5] = {4, 4, 3, 2, 2};
 
 // jobs == nullptr: one request (job); else request blockIdx.y of a fleet (jobs[y]), each
 // CTA staging its own request's tables -- a whole fleet in one launch.
-template <int NP>
-__global__ void __launch_bounds__(kEvalThreads, NP == 1 ? 0 : 3) eval_kernel(EvalJob job, const EvalJob* __restrict__ jobs) {
+// BM: billing mode of the launch -- 0 RESERVED, 1 BUSY, 2 per request at run time (a fleet
+// mixing both).  Compile-time for single requests: one copy of the tile code per kernel
+// (a runtime switch inside doubled the code and cost instruction-cache misses).
+template <int NP, int BM = 2>
+__global__ void __launch_bounds__(kEvalThreads, kEvalMinBlocks[NP]) eval_kernel(EvalJob job, const EvalJob* __restrict__ jobs) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bar;
     if (jobs) job = jobs[blockIdx.y];
@@ -357,95 +402,16 @@ __global__ void __launch_bounds__(kEvalThreads, NP == 1 ? 0 : 3) eval_kernel(Eva
     DevHeader& h = *reinterpret_cast<DevHeader*>(smem);
     VaEntry* va = reinterpret_cast<VaEntry*>(smem + sizeof(DevHeader));
     stage_tables(job.hdr, job.va, &h, va, (uint32_t)job.va_bytes, &bar);
-
-    const uint32_t bm = h.B - 2, bl = h.B - 1;
-    const uint32_t rm = h.radix[bm], rl = h.radix[bl];
-    const uint32_t mfirst = h.first[bm], mlast = h.first[bm + 1];
-    const uint32_t lfirst = h.first[bl], llast = h.first[bl + 1];
     const uint64_t row = h.row;
-    const uint64_t n_rows = h.n_rows;
-    const bool busy_bill = h.flags & 2u;
+    const uint32_t rl = h.radix[h.B - 1];
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-
     // warp <-> tile of 32 consecutive rows; lane <-> row H = tile * 32 + lane
     for (uint64_t t = tile_begin + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < tile_end;
          t += nwarps) {
-        const uint64_t Hraw = t * kTileRows + lane;
-        const bool live = Hraw < n_rows;  // the last tile may run past the space
-        const uint64_t H = live ? Hraw : n_rows - 1;
-        Rec4* tile_out = out + (t - tile_begin) * kTileRows * row + lane;
-        State<NP> st;
-        state_init(st, h);
-        // ---- HI prefix: decode the row index (MSD = earliest block, R19) and simulate
-        uint64_t rem = H;
-        for (uint32_t b = 0; b < bm; b++) {
-            const uint64_t pl = h.place[b];
-            uint32_t c;
-            if ((rem >> 32) == 0 && (pl >> 32) == 0) c = (uint32_t)rem / (uint32_t)pl;
-            else c = (uint32_t)(rem / pl);
-            rem -= (uint64_t)c * pl;
-            const uint32_t ch = h.choice[h.coff[b] + c];
-            const uint32_t k = ch_k(ch), p = ch_pool(ch);
-            const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
-            const VaEntry* vb = va + h.voff[b] + c;
-            // lanes are 32 consecutive rows: the high digits usually agree across the
-            // warp -- then (k, p) is warp-uniform and the compile-time gang update runs;
-            // otherwise the runtime-k update (a divergent switch over the compile-time
-            // variants measured 12% slower overall on C2)
-            if (__all_sync(0xffffffffu, ch == __shfl_sync(0xffffffffu, ch, 0))) {
-                switch (k) {
-                    case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
-                    case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
-                    case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
-                    case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
-                    default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
-                }
-            } else {
-                run_block<NP, 0>(st, h, p, k, f0, f1, vb, r);
-            }
-        }
-        // ---- MID digit: warp-uniform choice
-        for (uint32_t dm = 0; dm < rm; dm++) {
-            State<NP> s2 = st;
-            {
-                const uint32_t ch = h.choice[h.coff[bm] + dm];
-                const uint32_t k = ch_k(ch), p = ch_pool(ch);
-                const VaEntry* vb = va + h.voff[bm] + dm;
-                for (uint32_t s = mfirst; s < mlast; s++) {
-                    const VaEntry v = vb[(s - mfirst) * rm];
-                    const uint64_t e = scene_step_uniform<NP>(s2, p, k, h.a[s], v.t_us);
-                    scene_metrics(s2, s, e, h.P[s], v.q);
-                }
-            }
-            // record (dm, dl) of this lane's row sits at tile_out + (dm * rl + dl) * 32:
-            // a warp store covers 32 consecutive 32 B records (1 KB, fully coalesced)
-            Rec4* lane_out = tile_out + (size_t)dm * rl * kTileRows;
-            if (llast - lfirst == 1 && lfirst != 0) {
-                const StoreEmit::Put put{lane_out, live};
-                if (busy_bill) lsd_fast<NP, true>(h, s2, put);
-                else lsd_fast<NP, false>(h, s2, put);
-            } else {
-                // ---- generic LSD block (several scenes share the last digit)
-                for (uint32_t dl = 0; dl < rl; dl++) {
-                    State<NP> s3 = s2;
-                    const uint32_t ch = h.choice[h.coff[bl] + dl];
-                    const uint32_t k = ch_k(ch), p = ch_pool(ch);
-                    const VaEntry* vb = va + h.voff[bl] + dl;
-                    for (uint32_t s = lfirst; s < llast; s++) {
-                        const VaEntry v = vb[(s - lfirst) * rl];
-                        const uint64_t e = scene_step_uniform<NP>(s3, p, k, h.a[s], v.t_us);
-                        scene_metrics(s3, s, e, h.P[s], v.q);
-                    }
-                    Rec4 r;
-                    r.w0 = s3.R0;
-                    r.w1 = (uint64_t)s3.M - s3.R0;
-                    r.w2 = state_cost(s3, h);
-                    r.w3 = (uint64_t)s3.Q | ((uint64_t)s3.cnt << 32) | ((uint64_t)s3.used << 48);
-                    if (live) st_global_256(lane_out + (size_t)dl * kTileRows, r);
-                }
-            }
-        }
+        const StoreEmit em{out + (t - tile_begin) * kTileRows * row + lane, rl};
+        if (BM == 2) eval_tile<NP>(h, va, t, em);
+        else eval_tile_b<NP, BM == 1>(h, va, t, em);
     }
 }
 
@@ -707,6 +673,7 @@ struct ParetoCtl {
     uint32_t front_overflow;  // the front exceeded its capacity
     uint64_t stamp[6];        // diagnostics: %globaltimer at the merge kernel's phase ends
     unsigned long long dlt_pass;  // diagnostics: records the DLT did not rule out (all passes)
+    unsigned long long dlt_n;     // DLT survivors appended by the current scan pass (deferred exact test)
 };
 
 // Per-call status words of a multi-rank call, max-reduced over the ranks BEFORE any rank
@@ -1265,13 +1232,136 @@ constexpr uint32_t kBlockSurv = 256;  // this block's own survivors, kept in sme
 struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select flags
     const Dlt* dlt;
     const PPoint* front;
-    ParetoCtl* ctl;  // front_n (read) and the survivor counter (atomics)
+    ParetoCtl* ctl;  // front_n (read) and the DLT-survivor counter dlt_n (atomics)
     PPoint* surv;
     uint64_t cap;
+    PPoint* cand;       // DLT survivors of the pass, exact-tested by pareto_exact_kernel
+    uint64_t cand_cap;
     uint32_t* gfeas;  // [SW_MAX_QUERIES] per request: a feasible record was seen (or null)
     uint32_t debug;     // count DLT passes (SW_DEBUG)
 };
 
+// The deferred exact Pareto test of a scan pass (DLT survivors, appended by the scan):
+//  (1) every candidate x is tested against the running front (sorted by t: only points
+//      with t <= x.t can dominate it), from the point with the largest such t downwards --
+//      the dominator the DLT missed is usually just below x.t -- stopping at the first
+//      dominator; an identical entry (same index) also removes x: it is already kept;
+//  (2) the candidates that pass are tested against this block's own earlier survivors and
+//      against each other: a block walks a contiguous range of the buffer (neighbouring
+//      records, which often dominate each other), so its survivor list works as a running
+//      local front and keeps the merge small; the list is flushed to surv (ctl->surv) when
+//      full and at the end.  A dropped survivor only loosens a filter: a record dominated by
+//      a real candidate is never a front point, so the merge stays exact.
+// Dropped DLT survivors (candidate buffer full) set surv_overflow: the merged front is then
+// valid but incomplete and the pass is refolded.  The front (<= kExactFront points) and the
+// block list live in dynamic shared memory as arrays (t, c, idx, q).
+constexpr uint32_t kExactFront = 2048;  // front points staged in smem (larger fronts: from L2)
+constexpr uint32_t kExactList = 2048;   // block survivor list
+constexpr int kExactThreads = 512;      // = candidates per chunk
+__host__ __device__ constexpr size_t exact_smem_bytes() {
+    return (size_t)(kExactFront + kExactList + kExactThreads) * (3 * sizeof(uint64_t) + sizeof(uint32_t));
+}
+struct PArrays {  // a point list as arrays in shared memory
+    uint64_t *t, *c, *i;
+    uint32_t* q;
+    __device__ __forceinline__ PPoint get(uint32_t j) const {
+        PPoint y;
+        y.t = t[j];
+        y.c = c[j];
+        y.idx = i[j];
+        y.q = q[j];
+        y.pad = 0;
+        return y;
+    }
+    __device__ __forceinline__ void put(uint32_t j, const PPoint& x) const {
+        t[j] = x.t;
+        c[j] = x.c;
+        i[j] = x.idx;
+        q[j] = x.q;
+    }
+};
+__device__ __forceinline__ PArrays parrays(unsigned char* base, uint32_t n) {
+    PArrays a;
+    a.t = reinterpret_cast<uint64_t*>(base);
+    a.c = a.t + n;
+    a.i = a.c + n;
+    a.q = reinterpret_cast<uint32_t*>(a.i + n);
+    return a;
+}
+
+__global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PPoint* __restrict__ cand, uint64_t cand_cap,
+                                                                        const PPoint* __restrict__ front, ParetoCtl* ctl,
+                                                                        PPoint* __restrict__ surv, uint64_t surv_cap) {
+    extern __shared__ __align__(16) unsigned char xsm[];
+    const PArrays F = parrays(xsm, kExactFront);
+    const PArrays L = parrays(xsm + (size_t)kExactFront * 28, kExactList);
+    const PArrays K = parrays(xsm + (size_t)(kExactFront + kExactList) * 28, kExactThreads);
+    __shared__ uint32_t s_nl, s_nk;
+    __shared__ unsigned long long s_base;
+    const unsigned long long nd = ctl->dlt_n;
+    const uint64_t n = nd < cand_cap ? nd : cand_cap;
+    const uint32_t m = (uint32_t)ctl->front_n;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && nd > cand_cap) ctl->surv_overflow = 1;
+    // this block's contiguous range of the candidate buffer
+    const uint64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
+    if (r0 >= r1) return;
+    const bool f_smem = m <= kExactFront;
+    if (f_smem)
+        for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) F.put(j, front[j]);
+    if (threadIdx.x == 0) s_nl = 0;
+    auto flush = [&]() {  // block list -> surv (all threads; ends with a barrier)
+        const uint32_t nl = s_nl;
+        if (threadIdx.x == 0) s_base = nl ? atomicAdd(&ctl->surv, (unsigned long long)nl) : 0ull;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < nl; j += blockDim.x)
+            if (s_base + j < surv_cap) surv[s_base + j] = L.get(j);
+        __syncthreads();
+        if (threadIdx.x == 0) s_nl = 0;
+        __syncthreads();
+    };
+    for (uint64_t c0 = r0; c0 < r1; c0 += kExactThreads) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_nk = 0;
+        __syncthreads();
+        // (1) against the running front
+        const uint64_t i = c0 + threadIdx.x;
+        if (i < r1) {
+            const PPoint x = cand[i];
+            uint32_t lo = 0, hi = m;  // #front points with t <= x.t
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if ((f_smem ? F.t[mid] : front[mid].t) <= x.t) lo = mid + 1;
+                else hi = mid;
+            }
+            bool dom = false;
+            for (uint32_t j = lo; j > 0 && !dom;) {
+                j--;
+                dom = pdom(f_smem ? F.get(j) : front[j], 0, x, 1);
+            }
+            if (!dom) K.put(atomicAdd(&s_nk, 1u), x);
+        }
+        __syncthreads();
+        const uint32_t nk = s_nk, nl = s_nl;
+        // (2) against the block's earlier survivors and the chunk's other survivors
+        bool keep = false;
+        PPoint x{};
+        if (threadIdx.x < nk) {
+            x = K.get(threadIdx.x);
+            bool dom = false;
+            for (uint32_t j = 0; j < nl && !dom; j++) dom = pdom(L.get(j), 0, x, 1);
+            for (uint32_t j = 0; j < nk && !dom; j++)
+                if (j != threadIdx.x) dom = pdom(K.get(j), j, x, threadIdx.x);
+            keep = !dom;
+        }
+        __syncthreads();
+        if (nl + nk > kExactList) {  // no room for the chunk's survivors: flush first
+            flush();
+        }
+        if (keep) L.put(atomicAdd(&s_nl, 1u), x);
+    }
+    __syncthreads();
+    flush();
+}
 // objective keys only (ties keep the earlier = lower index within a thread's scan)
 __device__ __forceinline__ bool obj_strict_better(uint32_t obj, const Rec4& a, const Rec4& b) {
     const uint32_t qa = rec_Q(a), qb = rec_Q(b);
@@ -1427,17 +1517,6 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     __shared__ unsigned long long s_vt[NQA];
     Rec4* ring = reinterpret_cast<Rec4*>(fsm);
     Dlt& d = *reinterpret_cast<Dlt*>(fsm + ring_bytes(PARETO));
-    PPoint* fs = reinterpret_cast<PPoint*>(fsm + ring_bytes(PARETO) + sizeof(Dlt));
-    PPoint* bsurv = fs + kFrontSmem;  // PARETO only
-    // the smem front subset as arrays (t, c, idx, q): a warp reading 32 consecutive points
-    // touches consecutive 8 B words (an array of 32 B PPoints costs 4-way bank conflicts)
-    uint64_t* f_t = reinterpret_cast<uint64_t*>(fs);
-    uint64_t* f_c = f_t + kFrontSmem;
-    uint64_t* f_i = f_c + kFrontSmem;
-    uint32_t* f_q = reinterpret_cast<uint32_t*>(f_i + kFrontSmem);
-    static_assert(kFrontSmem * (3 * sizeof(uint64_t) + sizeof(uint32_t)) <= kFrontSmem * sizeof(PPoint),
-                  "front arrays fit the PPoint subset's smem");
-    __shared__ uint32_t s_bcnt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int st = 0; st < NS; st++) mbar_init(&full_bar[st], 1);
@@ -1446,35 +1525,10 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         s_thr[threadIdx.x] = 0;
         s_vt[threadIdx.x] = ~0ull;
     }
-    if (threadIdx.x == 0) s_bcnt = 0;
-    uint32_t m_sm = 0, m_all = 0, chk = 1;
-    if (PARETO) {
-        m_all = (uint32_t)pa.ctl->front_n;
-        m_sm = min(m_all, kFrontSmem);
-        chk = max((m_all + 31u) / 32u, 1u);  // exact test: front probe chunk (32 chunks)
-        {  // stage the whole DLT (16 B vectors)
-            const uint4* src = reinterpret_cast<const uint4*>(pa.dlt);
-            uint4* dst = reinterpret_cast<uint4*>(&d);
-            for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
-        }
-        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) {
-            const PPoint f = pa.front[i];
-            f_t[i] = f.t;
-            f_c[i] = f.c;
-            f_i[i] = f.idx;
-            f_q[i] = f.q;
-        }
-        // a reserved-but-not-yet-written (or torn) survivor slot must dominate nothing:
-        // sentinel t = c = max, q = 0 (a torn write mixes halves that still carry a max)
-        for (uint32_t i = threadIdx.x; i < kBlockSurv; i += blockDim.x) {
-            PPoint sent;
-            sent.idx = kInf64;
-            sent.t = kInf64;
-            sent.c = kInf64;
-            sent.q = 0;
-            sent.pad = 0;
-            bsurv[i] = sent;
-        }
+    if (PARETO) {  // stage the whole DLT (16 B vectors)
+        const uint4* src = reinterpret_cast<const uint4*>(pa.dlt);
+        uint4* dst = reinterpret_cast<uint4*>(&d);
+        for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
     DltHot dh{0, 0, 0, 0, 0};
@@ -1658,117 +1712,36 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 for (int u = 0; u < kRPT; u++)
                     keepm |= (uint32_t)(valid[u] & !dlt_dominated(d, dh, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u]))) << u;
                 if (!__any_sync(0xffffffffu, keepm != 0)) continue;
-                if (pa.debug) {  // diagnostics: how many records reach the exact test
-                    const uint32_t nk = __reduce_add_sync(0xffffffffu, __popc(keepm));
-                    if (lane == 0) atomicAdd(&pa.ctl->dlt_pass, (unsigned long long)nk);
+                // deferred exact test: the stage's DLT survivors (rare) are appended to the
+                // pass's candidate buffer -- one atomic per warp -- and tested after the pass
+                // by pareto_exact_kernel, so this streaming loop stays HBM-bound
+                const uint32_t mine = __popc(keepm);
+                uint32_t incl = mine;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += v;
                 }
-// exact test of every DLT survivor of the stage by the whole warp, ONE loop over the
-                // (u, lane) pairs: a single copy of the loop body (one copy per u cost
-                // instruction-cache misses: no_instructions was the top stall on C3)
-                uint64_t pidx[kRPT];
-                unsigned pm[kRPT];  // warp-uniform: lanes whose record u is still pending
+                unsigned long long base = 0;
+                if (lane == 31) base = atomicAdd(&pa.ctl->dlt_n, (unsigned long long)incl);
+                base = __shfl_sync(0xffffffffu, base, 31);
+                uint64_t slot = base + incl - mine;
 #pragma unroll
                 for (int u = 0; u < kRPT; u++) {
-                    const bool k = (keepm >> u) & 1u;
-                    pidx[u] = k ? flat_index(v, per_tile, mt.pos0 + lane + u * 32) : 0;
-                    pm[u] = __ballot_sync(0xffffffffu, k);
-                }
-                for (;;) {
-                    int u = -1;
-                    unsigned pend = 0;
-#pragma unroll
-                    for (int k = kRPT - 1; k >= 0; k--)
-                        if (pm[k]) {
-                            u = k;
-                            pend = pm[k];
-                        }
-                    if (u < 0) break;
-                    const int src = __ffs(pend) - 1;
-                    uint64_t xt = 0, xc = 0, xi = 0;
-                    uint32_t xq = 0;
-#pragma unroll
-                    for (int k = 0; k < kRPT; k++) {
-                        if (k == u) {
-                            pm[k] &= pm[k] - 1;
-                            xt = r[k].w0 + r[k].w1;
-                            xc = r[k].w2;
-                            xq = rec_Q(r[k]);
-                            xi = pidx[k];
-                        }
+                    if (!((keepm >> u) & 1u)) continue;
+                    if (slot < pa.cand_cap) {
+                        PPoint x;
+                        x.idx = flat_index(v, per_tile, mt.pos0 + lane + u * 32);
+                        x.t = r[u].w0 + r[u].w1;
+                        x.c = r[u].w2;
+                        x.q = rec_Q(r[u]);
+                        x.pad = 0;
+                        pa.cand[slot] = x;
                     }
-                    PPoint x;
-                    x.idx = __shfl_sync(0xffffffffu, xi, src);
-                    x.t = __shfl_sync(0xffffffffu, xt, src);
-                    x.c = __shfl_sync(0xffffffffu, xc, src);
-                    x.q = __shfl_sync(0xffffffffu, xq, src);
-                    x.pad = 0;
-                    bool dom = false;
-                    // front sorted by t: only points with t <= x.t can dominate x.  The
-                    // DLT already rejects what the front below x's t bin dominates, so a
-                    // dominator the exact test must find usually has t just below x.t:
-                    // locate the chunk of 32 holding the last t <= x.t with one warp
-                    // probe (lane l reads the first t of chunk l * chk), then test
-                    // downwards from its end.  The order does not change the result.
-                    uint32_t top = 0;  // test points [0, top)
-                    {
-                        const uint32_t pi = lane * chk;
-                        const uint64_t tp = pi < m_all ? (pi < m_sm ? f_t[pi] : pa.front[pi].t) : kInf64;
-                        const unsigned pb = __ballot_sync(0xffffffffu, tp <= x.t);
-                        if (pb) top = min(m_all, (uint32_t)(31 - __clz(pb)) * chk + chk);
-                    }
-                    for (uint32_t j1 = top; j1 > 0 && !dom;) {
-                        const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
-                        const uint32_t j = j0 + lane;
-                        // an identical entry (same index) also removes x: it is already kept
-                        // (front points beyond the smem subset: from global, L2-resident)
-                        PPoint y;
-                        if (j < m_sm) {
-                            y.t = f_t[j];
-                            y.c = f_c[j];
-                            y.idx = f_i[j];
-                            y.q = f_q[j];
-                            y.pad = 0;
-                        } else {
-                            y = pa.front[j < j1 ? j : 0];
-                        }
-                        const bool dj = j < j1 && pdom(y, 0, x, 1);
-                        if (__any_sync(0xffffffffu, dj)) dom = true;
-                        j1 = j0;
-                    }
-                    // ... and against this block's earlier survivors: neighbouring
-                    // records (runs of consecutive indices) often dominate
-                    // each other, and every survivor costs the merge O(m)
-                    const uint32_t bc = min(*(volatile uint32_t*)&s_bcnt, kBlockSurv);
-                    for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {
-                        const uint32_t j = j0 + lane;
-                        const bool dj = j < bc && pdom(bsurv[j], 0, x, 1);
-                        if (__any_sync(0xffffffffu, dj)) dom = true;
-                    }
-                    // a survivor joins this block's list at once, so that the stage's later
-                    // records (the neighbours that often dominate each other) are tested
-                    // against it; list full: straight to the global survivor buffer
-                    if (!dom && lane == src) {
-                        const uint32_t my = atomicAdd(&s_bcnt, 1u);
-                        if (my < kBlockSurv) {
-                            bsurv[my] = x;
-                        } else {
-                            const unsigned long long slot = atomicAdd(&pa.ctl->surv, 1ull);
-                            if (slot < pa.cap) pa.surv[slot] = x;
-                        }
-                    }
-                    __syncwarp();
+                    slot++;
                 }
             }
         }
-    }
-    if (PARETO) {  // flush this block's survivor list to the global survivor buffer
-        __syncthreads();
-        __shared__ unsigned long long s_base;
-        const uint32_t nb = min(s_bcnt, kBlockSurv);
-        if (threadIdx.x == 0) s_base = nb ? atomicAdd(&pa.ctl->surv, (unsigned long long)nb) : 0ull;
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
-            if (s_base + i < pa.cap) pa.surv[s_base + i] = bsurv[i];
     }
 #pragma unroll
     for (int q = 0; q < NQ; q++) {
@@ -1897,7 +1870,7 @@ struct StreamEmit {
         const StreamEmit* e;
         uint64_t base;  // index of candidate (dm, 0)
         bool live;
-        __device__ __forceinline__ void operator()(uint32_t dl, const Rec4& r) const {
+        __device__ __forceinline__ void operator()(uint32_t dl, uint32_t, const Rec4& r) const {
             const StreamArgs& a = *e->sa;
             StreamShared& S = *e->ss;
             const uint32_t lane = threadIdx.x & 31;

@@ -20,6 +20,7 @@
 
 #include "sw_coll.cuh"
 #include "sw_kernels.cuh"
+#include "sw_shared.cuh"
 #include "sw_plan.h"
 
 using namespace sw;
@@ -37,6 +38,13 @@ struct Segment {
 };
 
 }  // namespace
+
+struct SharedHost {
+    std::vector<sw_plan*> reqs;      // per request: tables only (t_tables_only handles)
+    std::vector<uint32_t> S, sc_off; // scenes and their offset in the joint ready array
+    SharedDev* d_dev = nullptr;
+    SharedDetailOut* d_full = nullptr;  // [SW_MAX_QUERIES]
+};
 
 struct sw_plan {
     int device = 0;
@@ -77,6 +85,8 @@ struct sw_plan {
     PPoint* d_gather = nullptr;  // multi-rank padded fronts
     PPoint* d_tmp2 = nullptr;    // front_cap + surv_cap (block-local fronts)
     PPoint* d_surv = nullptr;    // surv_cap survivors of filter passes
+    PPoint* d_dltc = nullptr;    // DLT survivors of a scan pass (deferred exact test), allocated on first fold
+    uint64_t dltc_cap = 0;
     bool fuse_pareto = true;     // fold unfolded segments inside select scans
     bool cxt_front_ok = false;   // COST_X_TTFF: every record has cost > 0 and ttff_eff > 0 (R35)
     uint64_t chunk = 1ull << 25; // records per fold chunk (the front improves per chunk)
@@ -119,6 +129,9 @@ struct sw_plan {
     uint64_t k_bytes[3] = {0, 0, 0};
     uint64_t launches = 0;
     std::string err;
+
+    // shared-pool fleet (sw_shared_create): the requests' table handles + device descriptor
+    struct SharedHost* shared = nullptr;
 
     // fused stream (sw_plan_stream): per-query reported candidates, allocated on first use
     Cand* d_scand = nullptr;       // [SW_MAX_QUERIES][scand_cap]
@@ -253,6 +266,9 @@ static SegView view_of(const sw_plan* h, const Segment& g, uint64_t t_lo, uint64
     return v;
 }
 static cudaError_t set_scan_smem_attrs();
+
+static sw_status create_common(sw_plan* h, const sw_runtime* rt);
+static thread_local bool t_tables_only = false;  // sw_shared_create: per-request table handles
 
 // ============================================================================ create
 extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_list* sc,
@@ -559,6 +575,14 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     h->launches++;
     dev_free(h, d_raw);
     // keep the host mirror's a/P unused (device-owned); fetch nothing back.
+    if (t_tables_only) {  // a request's tables for a shared-pool fleet: nothing else
+        if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+            cudaGetLastError();
+            return bail(fail(nullptr, SW_ECUDA, "create: device work failed"));
+        }
+        *out = h;
+        return SW_OK;
+    }
 
     // ---- eval launch configuration: persistent grid sized by occupancy x SMs
     h->eval_smem = sizeof(DevHeader) + h->va_bytes;
@@ -572,16 +596,22 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
             // this handle's actual size)
             int optin = 0;
             cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
-            cudaFuncAttributes fa{};
-            e = cudaFuncGetAttributes(&fa, eval_kernel<NPc>);
-            const size_t dyn_max = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
-            if (e == cudaSuccess)
-                e = dyn_max < h->eval_smem ? cudaErrorInvalidValue
-                                           : cudaFuncSetAttribute(eval_kernel<NPc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                                  (int)dyn_max);
-            if (e == cudaSuccess)
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eval_kernel<NPc>, kEvalThreads,
-                                                                  h->eval_smem);
+            auto setup = [&](auto kern) {  // every billing mode's instantiation (fleets use mode 2)
+                cudaFuncAttributes fa{};
+                cudaError_t r = cudaFuncGetAttributes(&fa, kern);
+                const size_t dyn_max = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+                if (r == cudaSuccess)
+                    r = dyn_max < h->eval_smem ? cudaErrorInvalidValue
+                                               : cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                      (int)dyn_max);
+                int o = 0;
+                if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kEvalThreads, h->eval_smem);
+                if (r != cudaSuccess && e == cudaSuccess) e = r;
+                return o;
+            };
+            const int o0 = setup(eval_kernel<NPc, 0>), o1 = setup(eval_kernel<NPc, 1>);
+            setup(eval_kernel<NPc, 2>);
+            occ = (h->h.flags & 2u) ? o1 : o0;
         });
         if (e != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -590,6 +620,16 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         }
         h->eval_grid = occ * h->num_sms;
     }
+    h->level_score.assign(tb->level_score, tb->level_score + tb->n_levels);
+    if ((st = create_common(h, rt)) < 0) return bail(st);
+    *out = h;
+    return SW_OK;
+}
+
+// Everything after the tables: scan configuration, record buffer, reduction scratch,
+// events (shared by sw_plan_create and sw_shared_create).
+static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
+    sw_status st;
     h->scan_grid = (uint32_t)h->num_sms;  // scan kernels: one TMA-pipelined block per SM
     if (const char* ev = getenv("SW_PARETO_CHUNK")) h->chunk = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
@@ -616,8 +656,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     }
     if (cudaError_t se = set_scan_smem_attrs(); se != cudaSuccess) {
         cudaGetLastError();
-        return bail(fail(nullptr, SW_ECUDA, "scan kernels cannot launch one block per SM (%s; smem %zu/%zu B)",
-                         cudaGetErrorString(se), ring_bytes(true) + sizeof(Dlt) + (kFrontSmem + kBlockSurv) * sizeof(PPoint),
+        return (fail(nullptr, SW_ECUDA, "scan kernels cannot launch one block per SM (%s; smem %zu/%zu B)",
+                         cudaGetErrorString(se), ring_bytes(true) + sizeof(Dlt),
                          ring_bytes(false)));
     }
 
@@ -625,7 +665,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     uint64_t cap = rt->record_capacity;
     // default: this rank's largest possible shard (whole rows split evenly, plus a
     // ragged head or tail of under a row each)
-    if (cap == 0) cap = N / (uint64_t)h->nranks + 3 * h->row;
+    if (cap == 0) cap = h->N / (uint64_t)h->nranks + 3 * h->row;
     h->cand_cap = cap;
     {  // slots: whole tiles of 32 rows plus 2 tiles of padding for each of up to
        // kMaxSegs segments (each eval call adds at most 2 partial tiles)
@@ -634,45 +674,43 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         cap = tiles * per_tile;
     }
     h->rec_cap = cap;
-    if ((st = alloc_n(h, &h->d_rec, cap, "records")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_front, h->front_cap, "pareto front")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_work, h->front_cap + h->surv_cap, "pareto work")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_tmp, h->front_cap + h->surv_cap, "pareto tmp")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_keep, h->front_cap + h->surv_cap, "pareto flags")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_tmp2, h->front_cap + h->surv_cap, "pareto tmp2")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_surv, h->surv_cap, "pareto survivors")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_ctl, 1, "pareto ctl")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_dlt, 1, "dlt")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_rec, cap, "records")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_front, h->front_cap, "pareto front")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_work, h->front_cap + h->surv_cap, "pareto work")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_tmp, h->front_cap + h->surv_cap, "pareto tmp")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_keep, h->front_cap + h->surv_cap, "pareto flags")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_tmp2, h->front_cap + h->surv_cap, "pareto tmp2")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_surv, h->surv_cap, "pareto survivors")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_ctl, 1, "pareto ctl")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_dlt, 1, "dlt")) < 0) return (st);
     h->max_partial = h->scan_grid * 64;  // up to 64 segments per select
-    if ((st = alloc_n(h, &h->d_partial, (uint64_t)h->max_partial * SW_MAX_QUERIES, "partials")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_cand, SW_MAX_QUERIES, "winners")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_cand_all, (uint64_t)SW_MAX_QUERIES * h->nranks, "winners all")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_detail, SW_MAX_QUERIES, "detail")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_selfjob, 1, "self job")) < 0) return bail(st);
-    {
+    if ((st = alloc_n(h, &h->d_partial, (uint64_t)h->max_partial * SW_MAX_QUERIES, "partials")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_cand, SW_MAX_QUERIES, "winners")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_cand_all, (uint64_t)SW_MAX_QUERIES * h->nranks, "winners all")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_detail, SW_MAX_QUERIES, "detail")) < 0) return (st);
+    if (h->d_hdr) {  // this handle's tables as a 1-entry job list (winner details)
+        if ((st = alloc_n(h, &h->d_selfjob, 1, "self job")) < 0) return (st);
         const EvalJob sj{h->d_hdr, h->d_va, h->va_bytes, 0, 0, nullptr};
         if (cudaMemcpyAsync(h->d_selfjob, &sj, sizeof sj, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
-            return bail(fail(nullptr, SW_ECUDA, "self job upload failed"));
+            return (fail(nullptr, SW_ECUDA, "self job upload failed"));
     }
-    if ((st = alloc_n(h, &h->d_digest, 1, "digest")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_digest, 1, "digest")) < 0) return (st);
     // [0, R) gathered counts, [R] mine, [R+1] saved local front size, [R+2] merged size,
     // [R+3] pad overflow flag of the asynchronous merge, [R+4, R+4+kStatusWords) the
     // max-reduced status words of a multi-rank call
-    if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 4 + kStatusWords, "counts")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_gfeas, SW_MAX_QUERIES, "select flags")) < 0) return bail(st);
-    if ((st = alloc_n(h, &h->d_greedy, 1, "greedy result")) < 0) return bail(st);
-    h->level_score.assign(tb->level_score, tb->level_score + tb->n_levels);
-    if (h->nranks > 1)
-        if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return bail(st);
+    if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 4 + kStatusWords, "counts")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_gfeas, SW_MAX_QUERIES, "select flags")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_greedy, 1, "greedy result")) < 0) return (st);
+        if (h->nranks > 1)
+        if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return (st);
     if (cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream) != cudaSuccess)
-        return bail(fail(nullptr, SW_ECUDA, "ctl init failed"));
+        return (fail(nullptr, SW_ECUDA, "ctl init failed"));
     for (int i = 0; i < 2 * sw_plan::kEvPairs; i++)
-        if (cudaEventCreate(&h->ev[i]) != cudaSuccess) return bail(fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
+        if (cudaEventCreate(&h->ev[i]) != cudaSuccess) return (fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
         cudaGetLastError();
-        return bail(fail(nullptr, SW_ECUDA, "create: device work failed"));
+        return (fail(nullptr, SW_ECUDA, "create: device work failed"));
     }
-    *out = h;
     return SW_OK;
 }
 
@@ -684,15 +722,21 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
                         h->d_tmp,   h->d_keep,    h->d_ctl,     h->d_dlt,
                         h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest, h->d_selfjob,
                         h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas, h->d_greedy,
-                        h->d_scand, h->d_scand_n, h->d_skey};
+                        h->d_scand, h->d_scand_n, h->d_skey, h->d_dltc};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
         if (h->h_pass_surv) cudaFreeHost(h->h_pass_surv);
         for (cudaEvent_t e : h->ev)
             if (e) cudaEventDestroy(e);
+        if (h->shared) {
+            for (sw_plan* r : h->shared->reqs) sw_plan_destroy(r);
+            cudaFree(h->shared->d_dev);
+            cudaFree(h->shared->d_full);
+        }
         if (h->own_stream) cudaStreamDestroy(h->stream);
         cudaGetLastError();
     }
+    delete h->shared;
     delete h;
     return SW_OK;
 }
@@ -850,11 +894,18 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
         int pr = 0;
         sw_status ts = begin_timed(h, SW_KERNEL_EVAL, n * sizeof(Rec4), &pr);
         if (ts < 0) return ts;
-        launch_np(h, [&](auto np) {
-            constexpr int NPc = decltype(np)::value;
-            eval_kernel<NPc><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(
-                EvalJob{h->d_hdr, h->d_va, h->va_bytes, t0, t1, outp}, nullptr);
-        });
+        if (h->shared) {  // shared-pool fleet: one thread per joint candidate (row = 1)
+            const uint64_t thr = sg.ntiles * kTileRows;
+            const uint32_t sgrid = (uint32_t)std::min<uint64_t>((thr + kShThreads - 1) / kShThreads, 8ull * h->num_sms);
+            shared_eval_kernel<<<sgrid, kShThreads, 0, h->stream>>>(h->shared->d_dev, t0, t1, h->N, outp);
+        } else {
+            launch_np(h, [&](auto np) {
+                constexpr int NPc = decltype(np)::value;
+                const EvalJob job{h->d_hdr, h->d_va, h->va_bytes, t0, t1, outp};
+                if (h->h.flags & 2u) eval_kernel<NPc, 1><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(job, nullptr);
+                else eval_kernel<NPc, 0><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(job, nullptr);
+            });
+        }
         CKL(h);
         ts = end_timed(h, pr);
         if (ts < 0) return ts;
@@ -894,12 +945,34 @@ extern "C" sw_status sw_plan_kernel_time(sw_plan* h, uint32_t kind, uint64_t* n_
 static void detail_to_selection(const sw_plan* h, uint64_t index, const DetailOut& d, sw_selection* out,
                                 uint64_t* ready);
 
-static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint64_t* ready) {
-    launch_np(h, [&](auto np) {
-        constexpr int NPc = decltype(np)::value;
-        detail_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_hdr, h->d_va, index, h->d_detail);
-    });
+// Full metrics of the winners d_cand[0, nw) into d_detail (one launch).
+static sw_status launch_detail(sw_plan* h, uint32_t nw) {
+    if (h->shared) {
+        shared_detail_kernel<<<1, 32, 0, h->stream>>>(h->shared->d_dev, h->d_cand, nw, h->d_detail, h->shared->d_full);
+    } else {
+        launch_np(h, [&](auto npc) {
+            constexpr int NPc = decltype(npc)::value;
+            detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nw, h->d_detail);
+        });
+    }
     CKL(h);
+    return SW_OK;
+}
+
+static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint64_t* ready) {
+    if (h->shared) {
+        Cand c{};
+        c.idx = index;
+        CK(h, cudaMemcpyAsync(h->d_cand, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
+        sw_status ds = launch_detail(h, 1);
+        if (ds < 0) return ds;
+    } else {
+        launch_np(h, [&](auto np) {
+            constexpr int NPc = decltype(np)::value;
+            detail_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_hdr, h->d_va, index, h->d_detail);
+        });
+        CKL(h);
+    }
     DetailOut d;
     CK(h, cudaMemcpyAsync(&d, h->d_detail, sizeof d, cudaMemcpyDeviceToHost, h->stream));
     SYNC(h);
@@ -950,7 +1023,7 @@ static void launch_scan_nq(uint32_t nq, uint32_t grid, size_t smem, cudaStream_t
     }
 }
 
-static constexpr size_t kScanSmemPareto = ring_bytes(true) + sizeof(Dlt) + (kFrontSmem + kBlockSurv) * sizeof(PPoint);
+static constexpr size_t kScanSmemPareto = ring_bytes(true) + sizeof(Dlt);
 static constexpr size_t kRingBytes = ring_bytes(false);
 
 template <int NQ, int OBJ>
@@ -971,12 +1044,13 @@ static cudaError_t set_attr_one() {
 }
 
 static cudaError_t set_scan_smem_attrs() {
-    cudaError_t e = cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(pareto_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)exact_smem_bytes());
     cudaError_t r[] = {set_attr_one<0, 0>(), set_attr_one<1, 0>(), set_attr_one<2, 0>(), set_attr_one<4, 0>(),
                        set_attr_one<8, 0>(), set_attr_one<0, 1>(), set_attr_one<1, 1>(), set_attr_one<2, 1>(),
                        set_attr_one<4, 1>(), set_attr_one<8, 1>()};
     for (cudaError_t x : r)
-        if (x != cudaSuccess) e = x;
+        if (x != cudaSuccess && e == cudaSuccess) e = x;
     // fleet scans: one query per request, objective per request at run time
     cudaError_t f = cudaFuncSetAttribute(scan_kernel<1, false, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kRingBytes);
@@ -990,6 +1064,8 @@ static ParetoArgs pareto_args(sw_plan* h) {
     pa.ctl = h->d_ctl;
     pa.surv = h->d_surv;
     pa.cap = h->surv_cap;
+    pa.cand = h->d_dltc;
+    pa.cand_cap = h->dltc_cap;
     pa.gfeas = h->d_gfeas;
     pa.debug = h->debug ? 1u : 0u;
     return pa;
@@ -1045,6 +1121,11 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
 // Fold a segment chunk by chunk: DLT from the current front, one filter pass over the
 // chunk (fused with nq select queries when nq > 0), survivors merged on the device.
 static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
+    if (!h->d_dltc) {  // DLT-survivor buffer: 1/8 of the record capacity, 256 K..16 M points
+        h->dltc_cap = std::min<uint64_t>(std::max<uint64_t>(h->rec_cap / 8, 1ull << 18), 1ull << 24);
+        sw_status st = alloc_n(h, &h->d_dltc, h->dltc_cap, "DLT survivors");
+        if (st < 0) return st;
+    }
     const size_t psmem = kScanSmemPareto;
     // strided passes: units of upt tiles (a whole number of scan stages); pass 1 = every
     // 8^K-th unit (about kFirstPass records, at most 1/64 of the segment), each further
@@ -1084,6 +1165,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
         CKL(h);
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
+        CK(h, cudaMemsetAsync(&h->d_ctl->dlt_n, 0, sizeof(unsigned long long), h->stream));
         const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / (kStageRecs * kCW)), h->scan_grid);
         Cand* part = h->d_partial;
         if (nq) {
@@ -1099,6 +1181,12 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         CKL(h);
         if ((ts = end_timed(h, pr)) < 0) return ts;
         trace_mark(h, pass == 1 ? "scan1" : pass == 2 ? "scan2" : pass == 3 ? "scan3" : pass == 4 ? "scan4" : "scan");
+        // the pass's DLT survivors: exact test against the running front (grid-stride over
+        // the device-side count)
+        pareto_exact_kernel<<<h->num_sms, kExactThreads, exact_smem_bytes(), h->stream>>>(
+            h->d_dltc, h->dltc_cap, h->d_front, h->d_ctl, h->d_surv, h->surv_cap);
+        CKL(h);
+        trace_mark(h, "exact");
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                h->d_ctl);
         CKL(h);
@@ -1111,7 +1199,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
             ParetoCtl c;
             CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
             SYNC(h);
-            fprintf(stderr, "[sw] dlt passed %llu records so far\n", (unsigned long long)c.dlt_pass);
+            fprintf(stderr, "[sw] dlt passed %llu records in this pass\n", (unsigned long long)c.dlt_n);
             fprintf(stderr, "[sw] fold pass %llu: stride pass %u, %llu records, survivors %llu merge-in %u local %u/%u front %llu"
                             " | merge phases us: init %.1f local %.1f mark %.1f compact %.1f rank(b0) %.1f\n",
                     (unsigned long long)h->fold_passes, pass, (unsigned long long)recs,
@@ -1186,11 +1274,7 @@ static sw_status front_answer(sw_plan* h, uint32_t nq, const sw_query* qs, sw_se
     for (uint32_t q = 0; q < nq; q++) P.q[q] = QueryDev{qs[q].slo_startup_us, qs[q].slo_stall_us, qs[q].budget_mc};
     select_front_kernel<<<1, kScanThreads, 0, h->stream>>>(fr, n, nullptr, P, h->d_cand);
     CKL(h);
-    launch_np(h, [&](auto npc) {
-        constexpr int NPc = decltype(npc)::value;
-        detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nq, h->d_detail);
-    });
-    CKL(h);
+    if (sw_status ds = launch_detail(h, nq); ds < 0) return ds;
     Cand win[SW_MAX_QUERIES];
     DetailOut det[SW_MAX_QUERIES];
     CK(h, cudaMemcpyAsync(win, h->d_cand, sizeof(Cand) * nq, cudaMemcpyDeviceToHost, h->stream));
@@ -1344,11 +1428,7 @@ static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_sel
     }
     // every winner's full metrics in one launch, read back with the winners (one sync)
     const uint32_t nw = ns + nf;
-    launch_np(h, [&](auto npc) {
-        constexpr int NPc = decltype(npc)::value;
-        detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nw, h->d_detail);
-    });
-    CKL(h);
+    if (sw_status ds = launch_detail(h, nw); ds < 0) return ds;
     Cand win[SW_MAX_QUERIES];
     DetailOut det[SW_MAX_QUERIES];
     ParetoCtl cc;
@@ -1544,6 +1624,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
     if (nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u > %d", nq, SW_MAX_QUERIES);
     if (begin > end || end > h->N) return fail(h, SW_EINVAL, "range outside [0, N)");
     if (!h->segs.empty()) return fail(h, SW_ESTATE, "stream needs a handle without records (reset/release)");
+    if (h->shared) return fail(h, SW_EINVAL, "the fused stream mode is not available for shared-pool fleets");
     CK(h, cudaSetDevice(h->device));
     sw_status st = stream_setup(h);
     if (st < 0) return st;
@@ -1698,11 +1779,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
     }
     const uint32_t nw = ns + nf;
     if (nw) {
-        launch_np(h, [&](auto npc) {
-            constexpr int NPc = decltype(npc)::value;
-            detail_fleet_kernel<NPc><<<1, 32, 0, h->stream>>>(h->d_selfjob, h->d_cand, nw, h->d_detail);
-        });
-        CKL(h);
+        if (sw_status ds = launch_detail(h, nw); ds < 0) return ds;
     }
     Cand win[SW_MAX_QUERIES];
     DetailOut det[SW_MAX_QUERIES];
@@ -1934,6 +2011,7 @@ extern "C" sw_status sw_plan_greedy(sw_plan* h, uint64_t slo_startup_us, uint64_
                                     uint64_t* evaluations) {
     if (!h || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (start_index != UINT64_MAX && start_index >= h->N) return fail(h, SW_EINVAL, "start index out of range");
+    if (h->shared) return fail(h, SW_EINVAL, "the greedy planner is not available for shared-pool fleets");
     if (h->level_score.size() > (size_t)kMaxLevels) return fail(h, SW_EINVAL, "greedy supports <= %d levels", kMaxLevels);
     CK(h, cudaSetDevice(h->device));
     GreedyArgs A{};
@@ -1962,6 +2040,7 @@ extern "C" sw_status sw_plan_greedy(sw_plan* h, uint64_t slo_startup_us, uint64_
 // ============================================================================ host helpers
 extern "C" sw_status sw_plan_decode(const sw_plan* h, uint64_t index, uint8_t* choice_per_scene) {
     if (!h || !choice_per_scene) return fail(nullptr, SW_EINVAL, "null argument");
+    if (h->shared) return fail(nullptr, SW_EINVAL, "sw_plan_decode: a shared-pool fleet has joint digits (sw_shared_detail)");
     if (index >= h->N) return fail(nullptr, SW_EINVAL, "index %llu outside [0, %llu)", (unsigned long long)index,
                                    (unsigned long long)h->N);
     // mixed-radix digits, MSD = earliest block (R19); padded virtual digits have radix 1
@@ -2024,6 +2103,213 @@ extern "C" sw_status sw_selection_merge(uint32_t objective, const sw_query* q, c
     return out->status;
 }
 
+// ============================================================================ shared-pool fleet
+// SURVEY §8(f) row 4 (reading R36): requests contending for the same pools through per-pool
+// EDF queues.  The handle is an ordinary sw_plan over the JOINT plan space of
+// the free requests (row = 1, one thread per candidate): eval / select / Pareto / digest /
+// sweep / records work unchanged on its fleet records; each request's tables live in a
+// tables-only handle (validated and packed -- a_s, P_s, V+A entries -- by sw_plan_create).
+extern "C" sw_status sw_shared_create(uint32_t n, const sw_profile_tables* tables, const sw_scene_list* scenes,
+                                      const uint64_t* fixed_cost_mc, const sw_shared_request* reqs,
+                                      const sw_price_table* pools, const sw_runtime* rt, sw_plan** out) {
+    if (!tables || !scenes || !reqs || !pools || !rt || !out) return fail(nullptr, SW_EINVAL, "null argument");
+    if (n < 1 || n > (uint32_t)kShMaxReq) return fail(nullptr, SW_EINVAL, "shared fleet of %u requests (1..%d)", n, kShMaxReq);
+    if (pools->evict_risk_permille) return fail(nullptr, SW_EINVAL, "shared pools take no eviction risk");
+    if (rt->nranks < 1 || rt->rank < 0 || rt->rank >= rt->nranks)
+        return fail(nullptr, SW_EINVAL, "bad rank %d of %d", rt->rank, rt->nranks);
+    if (rt->nranks > 1 && !rt->nccl_comm) return fail(nullptr, SW_EINVAL, "nranks > 1 needs nccl_comm");
+    uint32_t tot_s = 0, nd = 0;
+    uint64_t N = 1;
+    for (uint32_t r = 0; r < n; r++) {
+        tot_s += scenes[r].n_scenes;
+        if (reqs[r].fixed_index == UINT64_MAX) {
+            nd += tables[r].n_digits;
+            for (uint32_t b = 0; b < tables[r].n_digits && tables[r].radix; b++) {
+                if ((u128)N * tables[r].radix[b] >= ((u128)1 << 63))
+                    return fail(nullptr, SW_ERANGE, "joint plan space >= 2^63");
+                N *= tables[r].radix[b];
+            }
+        }
+    }
+    if (tot_s > (uint32_t)kShMaxScenes) return fail(nullptr, SW_EINVAL, "%u scenes over all requests (max %d)", tot_s, kShMaxScenes);
+    if (nd > SW_MAX_DIGITS) return fail(nullptr, SW_EINVAL, "%u joint digits over the free requests (max %d)", nd, SW_MAX_DIGITS);
+    sw_plan* h = new sw_plan();
+    h->shared = new SharedHost();
+    auto bail = [&](sw_status st) {
+        sw_plan_destroy(h);
+        return st;
+    };
+    h->device = rt->device;
+    h->loop = as_loop(rt->nccl_comm);
+    h->comm = h->loop ? nullptr : (ncclComm_t)rt->nccl_comm;
+    h->rank = rt->rank;
+    h->nranks = rt->nranks;
+    h->alloc = rt->alloc;
+    h->free_fn = rt->free;
+    h->alloc_ctx = rt->alloc_ctx;
+    if (cudaSetDevice(h->device) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(nullptr, SW_ECUDA, "cudaSetDevice(%d) failed (no CUDA device?)", h->device));
+    }
+    if (rt->stream) {
+        h->stream = (cudaStream_t)rt->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(nullptr, SW_ECUDA, "cudaStreamCreate failed"));
+        h->own_stream = true;
+    }
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+    // every request's tables, validated against the shared pools and packed on the device
+    SharedDev D{};
+    D.R = n;
+    D.NP = pools->n_pools;
+    D.billing = pools->billing;
+    D.nd = nd;
+    u128 tbound = 0, qsum = 0, maxT0 = 0;
+    uint32_t sc_off = 0, dg = 0;
+    for (uint32_t r = 0; r < n; r++) {
+        sw_price_table pr = *pools;
+        pr.fixed_cost_mc = fixed_cost_mc ? fixed_cost_mc[r] : 0;
+        sw_runtime rr{};
+        rr.device = rt->device;
+        rr.stream = h->stream;
+        rr.rank = 0;
+        rr.nranks = 1;
+        sw_plan* q = nullptr;
+        t_tables_only = true;
+        sw_status st = sw_plan_create(&tables[r], &scenes[r], &pr, &rr, &q);
+        t_tables_only = false;
+        if (st < 0) {
+            const std::string msg = "request " + std::to_string(r) + ": " + g_last_error;
+            bail(st);
+            return fail(nullptr, st, "%s", msg.c_str());
+        }
+        h->shared->reqs.push_back(q);
+        if (reqs[r].fixed_index != UINT64_MAX && reqs[r].fixed_index >= q->N)
+            return bail(fail(nullptr, SW_EINVAL, "request %u: background plan %llu outside [0, %llu)", r,
+                             (unsigned long long)reqs[r].fixed_index, (unsigned long long)q->N));
+        SharedReqDev& R = D.req[r];
+        R.hdr = q->d_hdr;
+        R.va = q->d_va;
+        R.T0 = reqs[r].arrival_us;
+        R.slo_t = reqs[r].slo_startup_us;
+        R.slo_s = reqs[r].slo_stall_us;
+        R.S = q->S;
+        R.s0 = scenes[r].scene0_static ? 1u : 0u;
+        R.B = q->B_user;
+        R.pad_digits = q->pad_digits;
+        R.free_ = reqs[r].fixed_index == UINT64_MAX ? 1u : 0u;
+        R.dig0 = dg;
+        R.sc_off = sc_off;
+        if (R.free_) {
+            for (uint32_t b = 0; b < q->B_user; b++) D.jradix[dg + b] = tables[r].radix[b];
+            dg += q->B_user;
+        } else {  // the background plan's digits (mixed radix, MSD = earliest block)
+            uint64_t rem = reqs[r].fixed_index;
+            for (int b = (int)q->B_user - 1; b >= 0; b--) {
+                R.fixed_dig[b] = (uint32_t)(rem % tables[r].radix[b]);
+                rem /= tables[r].radix[b];
+            }
+        }
+        h->shared->S.push_back(q->S);
+        h->shared->sc_off.push_back(sc_off);
+        sc_off += q->S;
+        // overflow bounds (R25 over the fleet): every task of every request may queue behind
+        // every other one -> time bound = latest arrival + pool offset + sum of all stage times
+        u128 tr = scenes[r].overhead_us + scenes[r].static_ready_us;
+        for (uint32_t s = 0; s < q->S; s++) tr += (u128)scenes[r].llm_us[s] + scenes[r].tts_us[s];
+        uint64_t off = 0;
+        for (uint32_t b = 0; b < tables[r].n_digits; b++) {
+            const uint32_t rb = tables[r].radix[b];
+            for (uint32_t s = tables[r].first_scene[b]; s < tables[r].first_scene[b + 1]; s++) {
+                uint64_t mx = 0;
+                for (uint32_t c = 0; c < rb; c++) mx = std::max(mx, tables[r].va_us[off + (s - tables[r].first_scene[b]) * rb + c]);
+                tr += mx;
+            }
+            off += (uint64_t)(tables[r].first_scene[b + 1] - tables[r].first_scene[b]) * rb;
+        }
+        tbound += tr;
+        maxT0 = std::max<u128>(maxT0, reqs[r].arrival_us);
+        uint32_t max_score = 0;
+        for (uint32_t l = 0; l < tables[r].n_levels; l++) max_score = std::max(max_score, tables[r].level_score[l]);
+        for (uint32_t s = 0; s < q->S; s++) qsum += (u128)(scenes[r].dur_us[s] / 1000) * max_score;
+    }
+    {
+        u128 ready_max = 0;
+        for (uint32_t p = 0; p < pools->n_pools; p++) {
+            D.G[p] = pools->gpus[p];
+            D.price[p] = pools->price_mc_per_gpu_hour[p];
+            D.ready[p] = pools->pool_ready_us ? pools->pool_ready_us[p] : 0;
+            ready_max = std::max<u128>(ready_max, D.ready[p]);
+        }
+        tbound += maxT0 + ready_max;
+        if (tbound >= ((u128)1 << 62)) return bail(fail(nullptr, SW_ERANGE, "fleet time bound exceeds 2^62 us"));
+        if (qsum >= ((u128)1 << 32) - 1) return bail(fail(nullptr, SW_ERANGE, "fleet quality bound exceeds 2^32 - 2"));
+        if (tot_s >= (1u << 16)) return bail(fail(nullptr, SW_ERANGE, "fleet stall-count bound"));
+        u128 cmax = 0;
+        for (uint32_t r = 0; r < n; r++) cmax += fixed_cost_mc ? fixed_cost_mc[r] : 0;
+        for (uint32_t p = 0; p < pools->n_pools; p++) {
+            const u128 prod = (u128)D.G[p] * tbound * D.price[p] + kHalfHour;
+            if (prod >= ((u128)1 << 64)) return bail(fail(nullptr, SW_ERANGE, "cost bound of pool %u exceeds 2^64", p));
+            cmax += prod / kUsPerHour;
+        }
+        if (cmax >= ((u128)1 << 64)) return bail(fail(nullptr, SW_ERANGE, "fleet cost bound exceeds 2^64"));
+    }
+    // the handle over the joint space: row = 1 (tiles of 32 consecutive candidates)
+    h->NP = pools->n_pools;
+    h->S = std::min<uint32_t>(tot_s, SW_MAX_SCENES);
+    h->B_user = nd;
+    h->pad_digits = 0;
+    h->N = N;
+    h->row = 1;
+    DevHeader& H = h->h;
+    memset(&H, 0, sizeof H);
+    H.flags = (pools->billing ? 2u : 0u) | (pools->objective ? 4u : 0u);
+    H.N = N;
+    H.row = 1;
+    H.n_rows = N;
+    h->cxt_front_ok = false;  // lateness can be 0: cost x lateness ties (R35 does not apply)
+    if (cudaMalloc(&h->shared->d_dev, sizeof(SharedDev)) != cudaSuccess ||
+        cudaMalloc(&h->shared->d_full, sizeof(SharedDetailOut) * SW_MAX_QUERIES) != cudaSuccess ||
+        cudaMemcpyAsync(h->shared->d_dev, &D, sizeof D, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(nullptr, SW_ENOMEM, "shared fleet descriptor allocation failed"));
+    }
+    sw_status st = create_common(h, rt);
+    if (st < 0) return bail(st);
+    *out = h;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_shared_detail(sw_plan* h, uint64_t index, sw_record* per_request, uint64_t* ready_abs) {
+    if (!h || !per_request) return fail(nullptr, SW_EINVAL, "null argument");
+    if (!h->shared) return fail(h, SW_EINVAL, "not a shared-pool fleet handle");
+    if (index >= h->N) return fail(h, SW_EINVAL, "index out of range");
+    CK(h, cudaSetDevice(h->device));
+    Cand c{};
+    c.idx = index;
+    CK(h, cudaMemcpyAsync(h->d_cand, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
+    sw_status ds = launch_detail(h, 1);
+    if (ds < 0) return ds;
+    SharedDetailOut d;
+    CK(h, cudaMemcpyAsync(&d, h->shared->d_full, sizeof d, cudaMemcpyDeviceToHost, h->stream));
+    SYNC(h);
+    const uint32_t n = (uint32_t)h->shared->reqs.size();
+    for (uint32_t r = 0; r < n; r++) {
+        sw_record& o = per_request[r];
+        o.ttff_us = d.per[r].w0;
+        o.stall_us = d.per[r].w1;
+        o.cost_mc = d.per[r].w2;
+        o.quality = (uint32_t)d.per[r].w3;
+        o.stall_count = (uint16_t)(d.per[r].w3 >> 32);
+        o.flags = 0;
+        o.pad = 0;
+        if (ready_abs)
+            for (uint32_t s = 0; s < h->shared->S[r]; s++) ready_abs[h->shared->sc_off[r] + s] = d.ready[h->shared->sc_off[r] + s];
+    }
+    return SW_OK;
+}
+
 // ============================================================================ fleet (C4)
 // A batch of requests evaluated and selected together: ONE eval launch for every
 // request's space (grid.y = request, each CTA stages its own request's tables), ONE
@@ -2039,6 +2325,7 @@ struct sw_fleet {
     LoopComm* loop = nullptr;
     int rank = 0, nranks = 1;
     uint32_t np_max = 1;
+    int bmode = -1;  // eval billing mode: 0 / 1 when every request bills RESERVED / BUSY, else 2
     size_t eval_smem = 0;
     int eval_occ = 1, num_sms = 148;
     uint32_t gx = 1;  // scan blocks per request
@@ -2125,6 +2412,8 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
         }
         f->plans.push_back(p);
         f->np_max = std::max(f->np_max, p->NP);
+        const int bm = (p->h.flags & 2u) ? 1 : 0;
+        f->bmode = f->bmode < 0 ? bm : (f->bmode == bm ? bm : 2);
         f->eval_smem = std::max(f->eval_smem, p->eval_smem);
     }
     sw_plan* h = f->plans[0];
@@ -2136,13 +2425,19 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
             constexpr int NPc = decltype(np)::value;
             int optin = 0;
             cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, f->device);
-            cudaFuncAttributes fa{};
-            e = cudaFuncGetAttributes(&fa, eval_kernel<NPc>);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(eval_kernel<NPc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         optin - (int)fa.sharedSizeBytes);
-            if (e == cudaSuccess)
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eval_kernel<NPc>, kEvalThreads, f->eval_smem);
+            auto setup = [&](auto kern) {
+                cudaFuncAttributes fa{};
+                cudaError_t r = cudaFuncGetAttributes(&fa, kern);
+                if (r == cudaSuccess)
+                    r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             optin - (int)fa.sharedSizeBytes);
+                int o = 0;
+                if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kEvalThreads, f->eval_smem);
+                if (r != cudaSuccess && e == cudaSuccess) e = r;
+                return o;
+            };
+            const int o0 = setup(eval_kernel<NPc, 0>), o1 = setup(eval_kernel<NPc, 1>), o2 = setup(eval_kernel<NPc, 2>);
+            occ = f->bmode == 0 ? o0 : f->bmode == 1 ? o1 : o2;
         });
         if (e != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -2248,7 +2543,9 @@ extern "C" sw_status sw_fleet_eval(sw_fleet* f) {
     CK(h, cudaEventRecord(f->ev[0], f->stream));
     launch_np_n(f->np_max, h, [&](auto np) {
         constexpr int NPc = decltype(np)::value;
-        eval_kernel<NPc><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
+        if (f->bmode == 0) eval_kernel<NPc, 0><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
+        else if (f->bmode == 1) eval_kernel<NPc, 1><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
+        else eval_kernel<NPc, 2><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
     });
     CKL(h);
     CK(h, cudaEventRecord(f->ev[1], f->stream));
@@ -2455,4 +2752,4 @@ extern "C" const char* sw_last_error(const sw_plan* h) {
 
 extern "C" uint64_t sw_plan_launch_count(const sw_plan* h) { return h ? h->launches : 0; }
 
-extern "C" int32_t sw_abi_version(void) { return 4; }  // 2: pool_ready_us; 3: evict_risk_permille; 4: loopback, decode, segments
+extern "C" int32_t sw_abi_version(void) { return 5; }  // 2: pool_ready_us; 3: evict_risk_permille; 4: loopback, decode, segments; 5: shared-pool fleets

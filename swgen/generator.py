@@ -95,6 +95,12 @@ GPU_CLASSES = {
     "H200":  (1.995, 565250, 422000),
     "GB200": (2.9, 1441750, 1076000),
 }
+# GPU power (reading R38): busy = the TDP of Table 3 ("at the highest frequency,
+# average power remains within 10% of the peak"); idle = A100's "63W when idle"
+# scaled to the class's TDP ("Other GPU generations show similar trends when
+# normalized to their TDP"), rounded to whole watts.
+GPU_TDP_W = {"V100": 300, "A100": 400, "H100": 700, "H200": 700, "GB200": 1200}
+GPU_IDLE_W = {c: (63 * w + 200) // 400 for c, w in GPU_TDP_W.items()}
 
 HEADS = 40  # Wan attention heads; k in {1,2,4,8} all divide it.
 
@@ -155,6 +161,11 @@ class Problem:
     seed: int = 0
     pool_ready_us: List[int] = field(default_factory=list)  # [] = warm pools (R18); R31
     evict_risk_permille: List[int] = field(default_factory=list)  # [] = no Spot risk; R32
+    vae_us: List[int] = field(default_factory=list)  # [] = VAE folded into V+A; R37 (block-major)
+    choice_vae_pool: List = field(default_factory=list)  # per choice: VAE pool or None; R37
+    metric: int = 0                 # 0 cost (milli-cents), 1 energy (microjoules); R38
+    power_active_w: List[int] = field(default_factory=list)  # per pool (metric 1)
+    power_idle_w: List[int] = field(default_factory=list)
 
     @property
     def B(self) -> int:
@@ -297,6 +308,51 @@ def make_config(name: str) -> Problem:
         pb = make_config("C2")
         pb.name = "C2x"
         pb.objective = 1
+        return pb
+    if name == "C3d":
+        # C3 with FramePack-style DiT/VAE disaggregation (reading R37): every
+        # choice runs its DiT on the chosen pool with k GPUs and streams the latents to a VAE
+        # on a separate A100x4 pool (1 GPU per scene; the VAE fraction 0.12 is not
+        # parallelised).  Same 24^6 space; t_DiT + t_VAE = C3's V+A time.
+        pb = make_config("C3")
+        pb.name = "C3d"
+        rng_j = SplitMix64(1003, "jitter")
+        S = pb.S
+        jit = [rng_j.uniform(0.9, 1.1) for _ in range(S)]
+        classes = pb.pool_class
+        pb.pool_class = classes + ["A100"]
+        pb.gpus = pb.gpus + [4]
+        pb.price_mc = pb.price_mc + [GPU_CLASSES["A100"][1]]
+        va, vae, off = [], [], 0
+        for b, r in enumerate(pb.radix):
+            chs = pb.choices[sum(pb.radix[:b]): sum(pb.radix[:b]) + r]
+            for s in range(pb.first_scene[b], pb.first_scene[b + 1]):
+                dms = pb.dur_us[s] // 1000
+                n16 = n16_frames(dms)
+                base = ((n16 + 80) // 81) * VA_INTERCEPT_S + n16 * VA_SLOPE_S
+                for (lv, k, p) in chs:
+                    dit = jit[s] * base * LEVEL_LV[lv] * (0.88 / SP[k]) / GPU_CLASSES[classes[p]][0]
+                    vs = jit[s] * base * LEVEL_LV[lv] * 0.12 / GPU_CLASSES["A100"][0]
+                    va.append(max(1, llround(1e6 * dit)))
+                    vae.append(max(1, llround(1e6 * vs)))
+        pb.va_us, pb.vae_us = va, vae
+        pb.choice_vae_pool = [2] * len(pb.choices)
+        return pb
+    if name in ("C3e", "C3ex"):
+        # C3 scored by ENERGY instead of money ("optimizing for energy ... Energy x
+        # TTFF"; reading R38): the record's cost field holds microjoules; budgets are energy
+        # budgets.  C3ex minimises Energy x TTFF (the COST_X_TTFF key over energy).
+        pb = make_config("C3")
+        pb.name = name
+        pb.metric = 1
+        pb.objective = 1 if name == "C3ex" else 0
+        pb.power_active_w = [GPU_TDP_W[c] for c in pb.pool_class]
+        pb.power_idle_w = [GPU_IDLE_W[c] for c in pb.pool_class]
+        # the LLM/TTS instance: one A100 busy over the fixed-stage span
+        fixed_span = pb.overhead_us + sum(pb.llm_us) + sum(pb.tts_us)
+        pb.fixed_cost_mc = GPU_TDP_W["A100"] * fixed_span
+        MJ = 10 ** 12  # microjoules per megajoule
+        pb.queries = [Query(999_999, 0, 4 * MJ), Query(2_999_999, 0, 2 * MJ), Query(INF, INF, INF)]
         return pb
     if name == "C3w":
         # C3 with a cold H100 pool: its GPUs are free only after the model load + first

@@ -56,6 +56,18 @@ def main():
             pb = make_config("C5")
             res = {"name": "C5sub", "ranges": [sweep_json(pb, args.threads, b, e)
                                                for b, e in C5_RANGES]}
+        elif cfg.startswith("SF"):  # shared-pool fleets
+            from swgen import make_shared
+            from oracle.oracle import SharedOracle
+            sf = make_shared(cfg)
+            o = SharedOracle(sf)
+            t0 = time.time()
+            w, f, d = o.sweep(0, o.n, sf.queries, nthreads=args.threads)
+            res = {"name": cfg, "n": o.n, "begin": 0, "end": o.n, "digest": str(d),
+                   "queries": [[q.slo_startup_us, q.slo_stall_us, q.budget_mc] for q in sf.queries],
+                   "winners": [{"status": st, "index": i, "rec": list(r.astuple())} for st, i, r in w],
+                   "front": [list(p) for p in f], "oracle_seconds": time.time() - t0,
+                   "oracle_threads": args.threads}
         elif cfg == "C4":
             reqs = [sweep_json(pb, args.threads) for pb in make_fleet()]
             res = {"name": "C4", "requests": reqs}

@@ -96,7 +96,13 @@ typedef struct {
                         switch to static content"; reading R33);
                         pair it with a level whose score is 0 (R12) */
     uint8_t pool;    /* GPU pool index (< n_pools; unused by a STATIC choice) */
-    uint8_t pad;
+    uint8_t vae;     /* 0: the VAE runs inside the V+A stage (R1).  v + 1: FramePack-style
+                        DiT/VAE disaggregation, "FramePack DiT streams latent outputs to the
+                        VAE for decoding ... pipelined execution, independent scaling"
+                        (reading R37): the V+A stage is the DiT (k GPUs of `pool`)
+                        and a separate VAE stage runs on pool v, one GPU (the VAE is not
+                        parallelised), as soon as the scene's DiT finished and a GPU
+                        of pool v is free; needs tables->vae_us */
 } sw_choice;
 
 /* Profiled tables (on-boarding profiles) expanded per candidate choice.
@@ -114,6 +120,9 @@ typedef struct {
     const uint32_t *level_score;/* [n_levels] quality score per level (R12) */
     uint32_t heads;             /* attention heads for the divisibility check;
                                    0 = no check */
+    const uint64_t *vae_us;     /* NULL, or laid out like va_us: the VAE stage time of each
+                                   (scene, choice) with a VAE stage (1 .. 2^32 - 1 us), 0 for
+                                   the others (R37) */
 } sw_profile_tables;
 
 /* Pools and prices (Table 3) in integer milli-cents per GPU-hour. */
@@ -140,6 +149,16 @@ typedef struct {
                             runs on G_p (the spares stand by for evicted GPUs).  Pair it with
                             the Spot column of Table 3.  RESERVED billing only: a non-zero
                             rho_p with BUSY billing is SW_EINVAL.  NULL = all 0. */
+    uint32_t metric;     /* 0: records carry cost in milli-cents (the prices above).
+                            1: ENERGY in microjoules instead ("optimizing for energy,
+                            TTFF, and other combinations (e.g., Energy x TTFF)"; P:701-724;
+                            reading R38): busy GPUs draw power_active_w, a pool's other rented
+                            GPUs power_idle_w until its last finish (RESERVED; BUSY: busy time
+                            only); fixed_cost_mc is then the fixed stages' energy (uJ), query
+                            budgets are energy budgets, and COST_X_TTFF minimises Energy x
+                            TTFF_eff.  Record field cost_mc holds the energy. */
+    const uint32_t *power_active_w; /* [n_pools] (metric 1): busy GPU power, W (the TDP) */
+    const uint32_t *power_idle_w;   /* [n_pools] (metric 1): idle GPU power, W */
 } sw_price_table;
 
 typedef void *(*sw_alloc_fn)(size_t bytes, void *stream, void *ctx);

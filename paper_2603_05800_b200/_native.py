@@ -34,19 +34,20 @@ class sw_scene_list(C.Structure):
 
 
 class sw_choice(C.Structure):
-    _fields_ = [("level", C.c_uint8), ("degree", C.c_uint8), ("pool", C.c_uint8), ("pad", C.c_uint8)]
+    _fields_ = [("level", C.c_uint8), ("degree", C.c_uint8), ("pool", C.c_uint8), ("vae", C.c_uint8)]
 
 
 class sw_profile_tables(C.Structure):
     _fields_ = [("n_digits", C.c_uint32), ("radix", U32P), ("first_scene", U32P),
                 ("choices", C.POINTER(sw_choice)), ("va_us", U64P), ("n_levels", C.c_uint32),
-                ("level_score", U32P), ("heads", C.c_uint32)]
+                ("level_score", U32P), ("heads", C.c_uint32), ("vae_us", U64P)]
 
 
 class sw_price_table(C.Structure):
     _fields_ = [("n_pools", C.c_uint32), ("gpus", U32P), ("price_mc_per_gpu_hour", U64P),
                 ("fixed_cost_mc", C.c_uint64), ("billing", C.c_uint32), ("objective", C.c_uint32),
-                ("pool_ready_us", U64P), ("evict_risk_permille", U32P)]
+                ("pool_ready_us", U64P), ("evict_risk_permille", U32P), ("metric", C.c_uint32),
+                ("power_active_w", U32P), ("power_idle_w", U32P)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -147,7 +148,7 @@ EXPORTS = {
                                      C.POINTER(sw_price_table), C.POINTER(sw_runtime), C.POINTER(C.c_void_p)]),
     "sw_shared_detail": (C.c_int32, [C.c_void_p, C.c_uint64, C.POINTER(sw_record), U64P]),
 }
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _lib = None
 
@@ -202,7 +203,7 @@ def shard_range(begin: int, end: int, row: int, rank: int, nranks: int):
 def space_shape(problem):
     """(N, row) of a problem's plan space without a device (sw_space_shape)."""
     radix = _arr(C.c_uint32, problem.radix)
-    tb = sw_profile_tables(len(problem.radix), radix, None, None, None, 0, None, 0)
+    tb = sw_profile_tables(len(problem.radix), radix, None, None, None, 0, None, 0, None)
     n, row = C.c_uint64(), C.c_uint64()
     _check(lib().sw_space_shape(C.byref(tb), C.byref(n), C.byref(row)))
     return n.value, row.value
@@ -289,16 +290,23 @@ def _marshal(pb, keep):
     sc = sw_scene_list(pb.S, _arr(C.c_uint64, pb.dur_us), _arr(C.c_uint64, pb.llm_us),
                        _arr(C.c_uint64, pb.tts_us), pb.overhead_us, pb.scene0_static,
                        pb.static_ready_us)
-    chs = (sw_choice * len(pb.choices))(*[sw_choice(l, kk, p, 0) for (l, kk, p) in pb.choices])
+    vae = getattr(pb, "vae_us", None)
+    vpool = getattr(pb, "choice_vae_pool", None) or [None] * len(pb.choices)
+    chs = (sw_choice * len(pb.choices))(*[sw_choice(l, kk, p, 0 if v is None else v + 1)
+                                          for (l, kk, p), v in zip(pb.choices, vpool)])
     tb = sw_profile_tables(len(pb.radix), _arr(C.c_uint32, pb.radix),
                            _arr(C.c_uint32, pb.first_scene), chs, _arr(C.c_uint64, pb.va_us),
-                           len(pb.level_score), _arr(C.c_uint32, pb.level_score), pb.heads)
+                           len(pb.level_score), _arr(C.c_uint32, pb.level_score), pb.heads,
+                           _arr(C.c_uint64, vae) if vae else None)
     ready = getattr(pb, "pool_ready_us", None)
     risk = getattr(pb, "evict_risk_permille", None)
+    metric = getattr(pb, "metric", 0)
     pr = sw_price_table(len(pb.gpus), _arr(C.c_uint32, pb.gpus), _arr(C.c_uint64, pb.price_mc),
                         pb.fixed_cost_mc, pb.billing, pb.objective,
                         _arr(C.c_uint64, ready) if ready else None,
-                        _arr(C.c_uint32, risk) if risk else None)
+                        _arr(C.c_uint32, risk) if risk else None, metric,
+                        _arr(C.c_uint32, pb.power_active_w) if metric else None,
+                        _arr(C.c_uint32, pb.power_idle_w) if metric else None)
     keep.append((sc, chs, tb, pr))
     return sc, tb, pr
 
@@ -529,7 +537,8 @@ class SharedPlan(Plan):
                                                                sf.slo_stall_us, sf.fixed_index)])
         ready = getattr(sf, "pool_ready_us", None)
         pools = sw_price_table(len(sf.gpus), _arr(C.c_uint32, sf.gpus), _arr(C.c_uint64, sf.price_mc), 0,
-                               sf.billing, sf.objective, _arr(C.c_uint64, ready) if ready else None, None)
+                               sf.billing, sf.objective, _arr(C.c_uint64, ready) if ready else None, None,
+                               0, None, None)
         rt = sw_runtime(device, C.c_void_p(stream or 0), C.c_void_p(comm or 0), rank, nranks,
                         record_capacity, ALLOC_FN(0), FREE_FN(0), None)
         self._keep += [scs, tbs, fixed, reqs, pools, rt]

@@ -22,7 +22,7 @@ constexpr uint64_t kHalfHour = 1800000000ull;
 struct __align__(16) VaEntry {
     uint64_t t_us;
     uint32_t q;
-    uint32_t pad;
+    uint32_t t_vae;  // VAE stage time of a disaggregated choice (R37; 0 = none), < 2^32 us
 };
 
 // LSD table entry (32 B), stored in (pool, k)-group order: the last scene's stage time
@@ -31,10 +31,9 @@ struct __align__(16) VaEntry {
 // floor((Y + X_t) / D) = qY + cq + (rY + cr >= D) for Y = qY * D + rY.
 struct __align__(16) LsdEntry {
     uint64_t t_us;
-    uint64_t cq;
-    uint32_t cr;   // < 3.6e9: 32 bits
+    uint64_t x1;   // money: cq; energy: the choice's own term when it ends the pool (see lsd_fast)
+    uint64_t x2;   // money: cr (< 3.6e9); energy: the term when it does not
     uint32_t q;
-    uint32_t off;  // byte offset of choice dl's record within a lane's MID run: dl x 32 x 32 B
     uint32_t dl;
 };
 
@@ -61,6 +60,9 @@ struct __align__(16) DevHeader {
     uint64_t price[kMaxP];
     uint64_t Gprice[kMaxP];       // G'_p * price_p (device-computed in pack_kernel)
     uint64_t ready[kMaxP];        // pool p's GPUs free from this time (load + warm-up, R31)
+    uint64_t Pact[kMaxP];         // energy metric (R38): busy power of a GPU of pool p (W)
+    uint64_t Pidle[kMaxP];        //   idle power (W)
+    uint64_t PidleG[kMaxP];       //   idle power x billed GPUs
     // LSD choices grouped by (pool, k) so the inner loop has neither: group g covers
     // lsd_dl[lsd_goff[g] .. lsd_goff[g+1]) with pool/k packed in lsd_pk[g] (p | k << 8)
     uint32_t lsd_ngroups, pad1;
@@ -77,6 +79,22 @@ static_assert(sizeof(DevHeader) % 16 == 0, "TMA bulk copies need 16 B multiples"
 __host__ __device__ __forceinline__ uint32_t ch_level(uint32_t c) { return c & 0xff; }
 __host__ __device__ __forceinline__ uint32_t ch_k(uint32_t c) { return (c >> 8) & 0xff; }
 __host__ __device__ __forceinline__ uint32_t ch_pool(uint32_t c) { return (c >> 16) & 0xff; }
+// VAE pool + 1 of a disaggregated choice (FramePack DiT -> VAE, R37); 0 = VAE folded into V+A
+__host__ __device__ __forceinline__ uint32_t ch_vae(uint32_t c) { return c >> 24; }
+
+// DevHeader.flags: 1 scene0 static, 2 BUSY billing, 4 COST_X_TTFF, 8 energy metric (R38),
+// 16 some choice has a separate VAE stage (R37), 32 the LSD fast path applies.  Cost modes of the kernels: bit 0 =
+// BUSY billing, bit 1 = energy (0 money RESERVED, 1 money BUSY, 2 energy RESERVED,
+// 3 energy BUSY); every mode but 0 accumulates busy GPU time.
+__host__ __device__ __forceinline__ int cost_mode(uint32_t flags) {
+    return ((flags & 2u) ? 1 : 0) | ((flags & 8u) ? 2 : 0);
+}
+// Eval path: 0 fast path, money + RESERVED (no busy time); 1 fast path with busy time;
+// 2 generic path -- flag 32 (set at create) says the fast path applies: the last digit's
+// block is one scene >= 1 and no choice has a VAE stage (flag 16).
+__host__ __device__ __forceinline__ int eval_mode(uint32_t flags) {
+    return ((flags & 16u) || !(flags & 32u)) ? 2 : cost_mode(flags) ? 1 : 0;
+}
 
 __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
@@ -160,6 +178,25 @@ __device__ __forceinline__ void gang_update_dyn(uint64_t (&F)[kMaxG], uint64_t e
 // One scene-step on pool p with degree k; returns the scene's ready time e = R_s.
 // KS > 0: k is a compile-time constant (warp-uniform MID/LSD loops); KS == 0: runtime.
 // BUSY: accumulate k x t (BUSY billing); RESERVED billing never reads it.
+// The VAE stage of a disaggregated choice (R37; "FramePack DiT streams latent outputs to the
+// VAE for decoding ... pipelined execution"): on pool vp, one GPU (the VAE is not
+// parallelised), once the DiT finished at e and a VAE GPU is free.
+template <int NP, bool BUSY>
+__device__ __forceinline__ uint64_t vae_step(State<NP>& st, uint32_t vp, uint64_t e, uint64_t tv) {
+    uint64_t ev = e;
+#pragma unroll
+    for (int q = 0; q < NP; q++) {
+        if ((uint32_t)q == vp) {
+            ev = umax64(e, st.F[q][0]) + tv;
+            gang_update_static<1>(st.F[q], ev);
+            st.end[q] = umax64(st.end[q], ev);
+            if (BUSY) st.busy[q] += tv;
+        }
+    }
+    st.used |= 1u << vp;
+    return ev;
+}
+
 template <int NP, int KS, bool BUSY = true>
 __device__ __forceinline__ uint64_t scene_step(State<NP>& st, uint32_t p, uint32_t k,
                                                uint64_t a, uint64_t t) {
@@ -287,14 +324,29 @@ struct __align__(32) Rec4 {
     uint64_t w0, w1, w2, w3;
 };
 
+// Pool term of the record's cost field: money (Table 3 prices, round half up, R10/R11) or
+// energy in microjoules (R38: busy GPUs at P_act, the pool's other rented GPUs idle at
+// P_idle until its last finish under RESERVED; BUSY: busy time only).
+template <int MODE>
+__device__ __forceinline__ uint64_t pool_term(const DevHeader& h, int q, uint64_t end, uint64_t busy) {
+    if (MODE == 0) return (end * h.Gprice[q] + kHalfHour) / kUsPerHour;
+    if (MODE == 1) return pool_cost(busy, h.price[q]);
+    if (MODE == 2) return h.PidleG[q] * end + (h.Pact[q] - h.Pidle[q]) * busy;
+    return h.Pact[q] * busy;
+}
+
 template <int NP>
 __device__ __forceinline__ uint64_t state_cost(const State<NP>& st, const DevHeader& h) {
     uint64_t c = h.fixed_cost;
-    const bool busy = h.flags & 2u;
+    const int mode = cost_mode(h.flags);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
-        const uint64_t X = busy ? st.busy[p] : (uint64_t)h.Gbill[p] * st.end[p];
-        c += pool_cost(X, h.price[p]);  // unused pool: X = 0 -> 0
+        switch (mode) {  // an unused pool: end = busy = 0 -> 0
+            case 0: c += pool_term<0>(h, p, st.end[p], st.busy[p]); break;
+            case 1: c += pool_term<1>(h, p, st.end[p], st.busy[p]); break;
+            case 2: c += pool_term<2>(h, p, st.end[p], st.busy[p]); break;
+            default: c += pool_term<3>(h, p, st.end[p], st.busy[p]); break;
+        }
     }
     return c;
 }

@@ -56,6 +56,7 @@ struct RawDesc {
     const uint32_t* score;   // level scores
     const uint32_t* va_scene;  // scene of each raw va entry (index bookkeeping from host)
     const uint32_t* va_choice; // global choice slot of each raw va entry
+    const uint64_t* vae;       // raw VAE stage times (R37), or null
     uint64_t overhead;
     uint32_t n_va;
 };
@@ -82,7 +83,10 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
             acc += raw.dur[s];
         }
     }
-    for (uint32_t p = threadIdx.x; p < hdr->NP; p += blockDim.x) hdr->Gprice[p] = (uint64_t)hdr->Gbill[p] * hdr->price[p];
+    for (uint32_t p = threadIdx.x; p < hdr->NP; p += blockDim.x) {
+        hdr->Gprice[p] = (uint64_t)hdr->Gbill[p] * hdr->price[p];
+        hdr->PidleG[p] = (uint64_t)hdr->Gbill[p] * hdr->Pidle[p];
+    }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < raw.n_va; i += blockDim.x) {
         const uint32_t s = raw.va_scene[i];
@@ -90,27 +94,34 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
         VaEntry e;
         e.t_us = raw.va[i];
         e.q = (uint32_t)((raw.dur[s] / 1000ull) * raw.score[lv]);
-        e.pad = 0;
+        e.t_vae = raw.vae ? (uint32_t)raw.vae[i] : 0u;  // < 2^32, validated at create
         va[i] = e;
     }
     __syncthreads();
     // LSD table in (pool, k)-group order (single-scene last block only)
     const uint32_t bl = hdr->B - 1;
     if (hdr->first[bl + 1] - hdr->first[bl] == 1) {
-        const bool busy = hdr->flags & 2u;
+        const int mode = cost_mode(hdr->flags);
         for (uint32_t j = threadIdx.x; j < hdr->radix[bl]; j += blockDim.x) {
             const uint32_t dl = hdr->lsd_dl[j];
             const uint32_t ch = hdr->choice[hdr->coff[bl] + dl];
             const uint32_t p = ch_pool(ch), k = ch_k(ch);
             const VaEntry v = va[hdr->voff[bl] + dl];
-            const uint64_t X = busy ? (uint64_t)k * v.t_us * hdr->price[p] : v.t_us * hdr->Gprice[p];
             LsdEntry le;
             le.t_us = v.t_us;
             le.q = v.q;
             le.dl = dl;
-            le.off = dl * kTileRows * (uint32_t)sizeof(Rec4);  // see StoreEmit
-            le.cq = X / kUsPerHour;
-            le.cr = (uint32_t)(X % kUsPerHour);
+            if (mode <= 1) {  // money: X_t = G price t (RESERVED) or k price t (BUSY) = cq D + cr
+                const uint64_t X = mode ? (uint64_t)k * v.t_us * hdr->price[p] : v.t_us * hdr->Gprice[p];
+                le.x1 = X / kUsPerHour;
+                le.x2 = X % kUsPerHour;
+            } else if (mode == 2) {  // energy, RESERVED: idle G' end + (active - idle) busy
+                const uint64_t B = (hdr->Pact[p] - hdr->Pidle[p]) * k * v.t_us;
+                le.x1 = hdr->PidleG[p] * v.t_us + B;  // the choice ends the pool: end grows by t too
+                le.x2 = B;
+            } else {  // energy, BUSY: active x busy
+                le.x1 = le.x2 = hdr->Pact[p] * k * v.t_us;
+            }
             hdr->lsd[j] = le;
         }
     }
@@ -154,19 +165,24 @@ __device__ __forceinline__ uint64_t fk_pool(const State<NP>& st, const MidState&
     }
 }
 
-template <int NP, bool BUSY, class Put>
+template <int NP, bool ACC, class Put>
 __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& st, const MidState& m, Put&& put) {
     const uint32_t bl = h.B - 1;
     const uint32_t s = h.first[bl];  // s >= 1 on this path
     const uint64_t as = h.a[s];
     const int64_t Ps = (int64_t)h.P[s];
+    // cost mode (cost_mode): 0 without busy accumulation; else 1..3 (uniform over the launch)
+    const int mode = ACC ? cost_mode(h.flags) : 0;
     uint64_t pc[NP], endq[NP], busyq[NP];
     uint64_t pcsum = h.fixed_cost;
 #pragma unroll
     for (int q = 0; q < NP; q++) {
         endq[q] = (uint32_t)q == m.pm ? m.end : st.end[q];
         busyq[q] = (uint32_t)q == m.pm ? m.busy : st.busy[q];
-        pc[q] = BUSY ? pool_cost(busyq[q], h.price[q]) : (endq[q] * h.Gprice[q] + kHalfHour) / kUsPerHour;
+        if (!ACC) pc[q] = pool_term<0>(h, q, endq[q], 0);
+        else if (mode == 1) pc[q] = pool_term<1>(h, q, 0, busyq[q]);
+        else if (mode == 2) pc[q] = pool_term<2>(h, q, endq[q], busyq[q]);
+        else pc[q] = pool_term<3>(h, q, 0, busyq[q]);
         pcsum += pc[q];
     }
     const uint64_t R0 = m.R0;
@@ -174,6 +190,7 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& st
     const uint64_t B1 = (uint64_t)M0 - R0;  // w1 = stall when the scene sets no new maximum
     const uint64_t w3base = (uint64_t)m.Q | ((uint64_t)m.cnt << 32) | ((uint64_t)(st.used | m.used) << 48);
     const uint32_t ng = h.lsd_ngroups;
+#pragma unroll 1
     for (uint32_t g = 0; g < ng; g++) {
         const uint32_t pk = h.lsd_pk[g];
         const uint32_t p = pk & 0xffu, k = pk >> 8;
@@ -189,57 +206,106 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& st
             for (uint32_t j = j0; j < j1; j++) {
                 const LsdEntry E = h.lsd[j];
                 r.w3 = w3s + E.q;
-                put(E.dl, E.off, r);
+                put(E.dl, E.dl * (kTileRows * (uint32_t)sizeof(Rec4)), r);
             }
             continue;
         }
-        uint64_t endp = 0, busyp = 0, pcp = 0, A = 0, price = 0;
+        uint64_t endp = 0, busyp = 0, pcp = 0;
 #pragma unroll
         for (int q = 0; q < NP; q++)
             if ((uint32_t)q == p) {
                 endp = endq[q];
                 busyp = busyq[q];
                 pcp = pc[q];
-                A = h.Gprice[q];
-                price = h.price[q];
             }
         const uint64_t st0 = umax64(as, fk_pool<NP>(st, m, p, k));
         const uint64_t base = pcsum - pcp;
-        // Y = (prefix part of X_p) * price + 1.8e9 = qY * D + rY
-        const uint64_t Y = (BUSY ? busyp * price : A * st0) + kHalfHour;
-        const uint64_t qY = Y / kUsPerHour, rY = Y - qY * kUsPerHour;
-        const uint64_t cnew0 = base + qY, cold = base + pcp;
-        const uint32_t Dm = (uint32_t)(kUsPerHour - rY);  // carry iff cr >= Dm (rY + cr >= D)
         const int64_t dd0 = (int64_t)st0 - Ps;
         const int64_t thrE = (int64_t)endp - (int64_t)st0;  // e > end_p <=> t > thrE
         const int64_t thrM = M0 - dd0;                     // new maximum <=> t > thrM
         const uint64_t A1 = (uint64_t)(dd0 - (int64_t)R0);  // w1 on a new maximum: A1 + t
         const uint64_t w3g = w3base | ((uint64_t)(1u << p) << 48);
-        for (uint32_t j = j0; j < j1; j++) {
-            const LsdEntry E = h.lsd[j];
+        // the cost of the choice's pool, hoisted: cost = U1 + x1 (+ carry) when the scene
+        // ends the pool (t > thrE; always for the busy-only modes), else U2 + x2
+        uint64_t U1, U2 = 0;
+        uint32_t Dm = 0;
+        if (mode <= 1) {  // money: Y = (prefix part of X_p) price + 1.8e9 = qY D + rY
+            const uint64_t Y = (mode ? busyp * h.price[p] : h.Gprice[p] * st0) + kHalfHour;
+            const uint64_t qY = Y / kUsPerHour, rY = Y - qY * kUsPerHour;
+            U1 = base + qY;
+            U2 = base + pcp;
+            Dm = (uint32_t)(kUsPerHour - rY);  // carry iff cr >= Dm (rY + cr >= D)
+        } else if (mode == 2) {  // energy RESERVED: PidleG max(end_p, e) + (Pact - Pidle)(busy_p + k t)
+            const uint64_t Bb = (h.Pact[p] - h.Pidle[p]) * busyp;
+            U1 = base + h.PidleG[p] * st0 + Bb;
+            U2 = base + h.PidleG[p] * endp + Bb;
+        } else {  // energy BUSY: Pact (busy_p + k t)
+            U1 = base + h.Pact[p] * busyp;
+        }
+        auto emit = [&](const LsdEntry& E, uint64_t cost) {
             const int64_t t = (int64_t)E.t_us;
-            const uint64_t cnew = cnew0 + E.cq + (E.cr >= Dm ? 1u : 0u);
             const bool nm = t > thrM;
             Rec4 r;
             r.w0 = R0;
             r.w1 = nm ? A1 + (uint64_t)t : B1;
-            r.w2 = BUSY ? cnew : (t > thrE ? cnew : cold);
+            r.w2 = cost;
             r.w3 = (w3g + E.q) + (nm ? (1ull << 32) : 0ull);
-            put(E.dl, E.off, r);  // a7 store, or the fused select + Pareto filter (stream)
+            put(E.dl, E.dl * (kTileRows * (uint32_t)sizeof(Rec4)), r);  // a7 store, or the stream filter
+        };
+        if (mode == 0) {
+#pragma unroll 1
+            for (uint32_t j = j0; j < j1; j++) {
+                const LsdEntry E = h.lsd[j];
+                const uint64_t cnew = U1 + E.x1 + ((uint32_t)E.x2 >= Dm ? 1u : 0u);
+                emit(E, (int64_t)E.t_us > thrE ? cnew : U2);
+            }
+        } else if (ACC && mode == 1) {
+            for (uint32_t j = j0; j < j1; j++) {
+                const LsdEntry E = h.lsd[j];
+                emit(E, U1 + E.x1 + ((uint32_t)E.x2 >= Dm ? 1u : 0u));
+            }
+        } else if (ACC && mode == 2) {
+            for (uint32_t j = j0; j < j1; j++) {
+                const LsdEntry E = h.lsd[j];
+                emit(E, (int64_t)E.t_us > thrE ? U1 + E.x1 : U2 + E.x2);
+            }
+        } else if (ACC) {
+            for (uint32_t j = j0; j < j1; j++) {
+                const LsdEntry E = h.lsd[j];
+                emit(E, U1 + E.x1);
+            }
         }
     }
 }
 
-// Scenes [f0, f1) of one digit's block with choice (p, k), gang update specialised for K
-// (K = 0: runtime k).
-template <int NP, int K, bool BUSY = true>
-__device__ __forceinline__ void run_block(State<NP>& st, const DevHeader& h, uint32_t p, uint32_t k, uint32_t f0,
-                                          uint32_t f1, const VaEntry* vb, uint32_t r, uint64_t* ready = nullptr) {
+// Scenes [f0, f1) of one digit's block with choice ch (pool, k, optional VAE stage R37), gang
+// update specialised for K (K = 0: runtime k).  ACC: accumulate busy GPU time.
+// VAE: compile the VAE stage in (the fast eval path never has one).
+template <int NP, int K, bool ACC = true, bool VAE = true>
+__device__ __forceinline__ void run_block(State<NP>& st, const DevHeader& h, uint32_t ch, uint32_t f0, uint32_t f1,
+                                          const VaEntry* vb, uint32_t r, uint64_t* ready = nullptr) {
+    const uint32_t p = ch_pool(ch), k = ch_k(ch), vae = VAE ? ch_vae(ch) : 0u;
+#pragma unroll 1  // one copy of the step per K: the gang updates dominate the code size
     for (uint32_t s = f0; s < f1; s++) {
         const VaEntry v = vb[(s - f0) * r];
-        const uint64_t e = scene_step<NP, K, BUSY>(st, p, k, h.a[s], v.t_us);
+        uint64_t e = scene_step<NP, K, ACC>(st, p, k, h.a[s], v.t_us);
+        if (VAE && vae) e = vae_step<NP, ACC>(st, vae - 1, e, v.t_vae);
         scene_metrics(st, s, e, h.P[s], v.q);
         if (ready) ready[s] = e;
+    }
+}
+
+// run_block with a warp-uniform runtime k dispatched to the compile-time specialisations.
+template <int NP, bool ACC = true>
+__device__ __forceinline__ void run_block_uniform(State<NP>& st, const DevHeader& h, uint32_t ch, uint32_t f0,
+                                                  uint32_t f1, const VaEntry* vb, uint32_t r,
+                                                  uint64_t* ready = nullptr) {
+    switch (ch_k(ch)) {
+        case 1: run_block<NP, 1, ACC>(st, h, ch, f0, f1, vb, r, ready); break;
+        case 2: run_block<NP, 2, ACC>(st, h, ch, f0, f1, vb, r, ready); break;
+        case 4: run_block<NP, 4, ACC>(st, h, ch, f0, f1, vb, r, ready); break;
+        case 8: run_block<NP, 8, ACC>(st, h, ch, f0, f1, vb, r, ready); break;
+        default: run_block<NP, 0, ACC>(st, h, ch, f0, f1, vb, r, ready); break;
     }
 }
 
@@ -247,6 +313,7 @@ __device__ __forceinline__ void run_block(State<NP>& st, const DevHeader& h, uin
 template <int K, bool BUSY>
 __device__ __forceinline__ void mid_block(MidState& m, const DevHeader& h, uint32_t k, uint32_t f0, uint32_t f1,
                                           const VaEntry* vb, uint32_t r) {
+#pragma unroll 1
     for (uint32_t s = f0; s < f1; s++) {
         const VaEntry v = vb[(s - f0) * r];
         const uint64_t e = mid_step<K, BUSY>(m, k, h.a[s], v.t_us);
@@ -274,7 +341,12 @@ struct EvalJob {
 // One tile (32 consecutive rows, lane <-> row H = t * 32 + lane) of candidates: record
 // (dm, dl) of the lane's row goes to emit.at(dm, live)(dl, off, r) -- the 32 B store of
 // the eval kernel, or the fused select + Pareto filter of the stream kernel.
-template <int NP, bool BUSY, class Emit>
+// BUSY: accumulate busy GPU time (every cost mode but money + RESERVED).  DIS (the
+// "generic" path): full-state MID pass and per-candidate LSD blocks, for handles whose LSD
+// block has several scenes (or starts at scene 0) or that have DiT/VAE disaggregated
+// choices (R37); the fast path (single-pool MID copy + lsd_fast) is a separate
+// instantiation, so neither carries the other's code or registers.
+template <int NP, bool BUSY, bool DIS, class Emit>
 __device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit) {
     const uint32_t bm = h.B - 2, bl = h.B - 1;
     const uint32_t rm = h.radix[bm], rl = h.radix[bl];
@@ -305,15 +377,37 @@ __device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* v
         // variants measured 12% slower overall on C2)
         if (__all_sync(0xffffffffu, ch == __shfl_sync(0xffffffffu, ch, 0))) {
             switch (k) {
-                case 1: run_block<NP, 1, BUSY>(st, h, p, k, f0, f1, vb, r); break;
-                case 2: run_block<NP, 2, BUSY>(st, h, p, k, f0, f1, vb, r); break;
-                case 4: run_block<NP, 4, BUSY>(st, h, p, k, f0, f1, vb, r); break;
-                case 8: run_block<NP, 8, BUSY>(st, h, p, k, f0, f1, vb, r); break;
-                default: run_block<NP, 0, BUSY>(st, h, p, k, f0, f1, vb, r); break;
+                case 1: run_block<NP, 1, BUSY, DIS>(st, h, ch, f0, f1, vb, r); break;
+                case 2: run_block<NP, 2, BUSY, DIS>(st, h, ch, f0, f1, vb, r); break;
+                case 4: run_block<NP, 4, BUSY, DIS>(st, h, ch, f0, f1, vb, r); break;
+                case 8: run_block<NP, 8, BUSY, DIS>(st, h, ch, f0, f1, vb, r); break;
+                default: run_block<NP, 0, BUSY, DIS>(st, h, ch, f0, f1, vb, r); break;
             }
         } else {
-            run_block<NP, 0, BUSY>(st, h, p, k, f0, f1, vb, r);
+            run_block<NP, 0, BUSY, DIS>(st, h, ch, f0, f1, vb, r);
         }
+    }
+    if (DIS) {
+        // ---- DiT/VAE disaggregated choices (R37) touch two pools per scene: MID and LSD
+        // digits on full state copies (no single-pool MID copy, no LSD fast path)
+        for (uint32_t dm = 0; dm < rm; dm++) {
+            State<NP> s2 = st;
+            const uint32_t chm = h.choice[h.coff[bm] + dm];
+            run_block_uniform<NP, BUSY>(s2, h, chm, mfirst, mlast, va + h.voff[bm] + dm, rm);
+            auto put = emit.at(dm, live);
+            for (uint32_t dl = 0; dl < rl; dl++) {
+                State<NP> s3 = s2;
+                const uint32_t chl = h.choice[h.coff[bl] + dl];
+                run_block_uniform<NP, BUSY>(s3, h, chl, lfirst, llast, va + h.voff[bl] + dl, rl);
+                Rec4 r;
+                r.w0 = s3.R0;
+                r.w1 = (uint64_t)s3.M - s3.R0;
+                r.w2 = state_cost(s3, h);
+                r.w3 = (uint64_t)s3.Q | ((uint64_t)s3.cnt << 32) | ((uint64_t)s3.used << 48);
+                put(dl, dl * kTileRows * (uint32_t)sizeof(Rec4), r);
+            }
+        }
+        return;
     }
     // ---- MID digit: warp-uniform choice (k, pm) on a copy of pool pm only
     for (uint32_t dm = 0; dm < rm; dm++) {
@@ -331,37 +425,18 @@ __device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* v
                 default: mid_block<0, BUSY>(m, h, k, mfirst, mlast, vb, rm); break;
             }
         }
-        auto put = emit.at(dm, live);  // put(dl, off, r): record (dm, dl) of this lane's row
-        if (llast - lfirst == 1 && lfirst != 0) {
-            lsd_fast<NP, BUSY>(h, st, m, put);
-        } else {
-            // ---- generic LSD block (several scenes share the last digit)
-            const State<NP> s2 = merge_mid<NP>(st, m);
-            for (uint32_t dl = 0; dl < rl; dl++) {
-                State<NP> s3 = s2;
-                const uint32_t chl = h.choice[h.coff[bl] + dl];
-                const uint32_t kl = ch_k(chl), pl = ch_pool(chl);
-                const VaEntry* vb = va + h.voff[bl] + dl;
-                for (uint32_t s = lfirst; s < llast; s++) {
-                    const VaEntry v = vb[(s - lfirst) * rl];
-                    const uint64_t e = scene_step_uniform<NP, BUSY>(s3, pl, kl, h.a[s], v.t_us);
-                    scene_metrics(s3, s, e, h.P[s], v.q);
-                }
-                Rec4 r;
-                r.w0 = s3.R0;
-                r.w1 = (uint64_t)s3.M - s3.R0;
-                r.w2 = state_cost(s3, h);
-                r.w3 = (uint64_t)s3.Q | ((uint64_t)s3.cnt << 32) | ((uint64_t)s3.used << 48);
-                put(dl, dl * kTileRows * (uint32_t)sizeof(Rec4), r);
-            }
-        }
+        lsd_fast<NP, BUSY>(h, st, m, emit.at(dm, live));  // record (dm, dl) of this lane's row
     }
 }
 
 template <int NP, class Emit>
 __device__ __forceinline__ void eval_tile(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit) {
-    if (h.flags & 2u) eval_tile_b<NP, true>(h, va, t, emit);  // BUSY billing (uniform branch)
-    else eval_tile_b<NP, false>(h, va, t, emit);
+    // busy GPU time is needed by every cost mode but money + RESERVED (uniform branch)
+    switch (eval_mode(h.flags)) {
+        case 0: eval_tile_b<NP, false, false>(h, va, t, emit); break;
+        case 1: eval_tile_b<NP, true, false>(h, va, t, emit); break;
+        default: eval_tile_b<NP, true, true>(h, va, t, emit); break;
+    }
 }
 
 // a7: the 32 B store.  Record (dm, dl) of the lane's row lands at tile_out + (dm * rl +
@@ -385,15 +460,21 @@ struct StoreEmit {
 // Resident CTAs per SM the register allocation is sized for, per pool count: the state
 // grows with the pools (NP + 1 pools of 8 free times live in the MID/LSD loops), and
 // these are the largest occupancies whose hot loops do not spill (ptxas -v).
-constexpr int kEvalMinBlocks[5] = {4, 4, 3, 2, 2};
+// fast path (BM 0/1) vs generic path (BM 2/3, full-state copies)
+__host__ __device__ constexpr int eval_min_blocks(int np, int bm) {
+    return bm <= 1 ? (np <= 2 ? 4 : np == 3 ? 3 : 2) : (np <= 1 ? 4 : np == 2 ? 3 : 2);
+}
 
 // jobs == nullptr: one request (job); else request blockIdx.y of a fleet (jobs[y]), each
 // CTA staging its own request's tables -- a whole fleet in one launch.
-// BM: billing mode of the launch -- 0 RESERVED, 1 BUSY, 2 per request at run time (a fleet
-// mixing both).  Compile-time for single requests: one copy of the tile code per kernel
-// (a runtime switch inside doubled the code and cost instruction-cache misses).
-template <int NP, int BM = 2>
-__global__ void __launch_bounds__(kEvalThreads, kEvalMinBlocks[NP]) eval_kernel(EvalJob job, const EvalJob* __restrict__ jobs) {
+// BM: path of the launch (eval_mode) -- 0 fast path without busy time (money + RESERVED),
+// 1 fast path with busy time (BUSY billing or the energy metric), 2 generic path, 3 per
+// request at run time (a fleet mixing them).  Compile-time for single requests: one copy of
+// the tile code per kernel (a runtime switch inside multiplied the code and cost
+// instruction-cache misses and registers).
+
+template <int NP, int BM = 3>
+__global__ void __launch_bounds__(kEvalThreads, eval_min_blocks(NP, BM)) eval_kernel(EvalJob job, const EvalJob* __restrict__ jobs) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bar;
     if (jobs) job = jobs[blockIdx.y];
@@ -410,8 +491,8 @@ __global__ void __launch_bounds__(kEvalThreads, kEvalMinBlocks[NP]) eval_kernel(
     for (uint64_t t = tile_begin + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < tile_end;
          t += nwarps) {
         const StoreEmit em{out + (t - tile_begin) * kTileRows * row + lane, rl};
-        if (BM == 2) eval_tile<NP>(h, va, t, em);
-        else eval_tile_b<NP, BM == 1>(h, va, t, em);
+        if (BM == 3) eval_tile<NP>(h, va, t, em);
+        else eval_tile_b<NP, BM != 0, BM == 2>(h, va, t, em);
     }
 }
 
@@ -445,11 +526,11 @@ __device__ void detail_one(const DevHeader* __restrict__ g_hdr, const VaEntry* _
         const VaEntry* vb = g_va + h.voff[b] + c;
         const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
         switch (k) {  // compile-time gang updates (a single thread: no divergence cost)
-            case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r, out->ready); break;
-            case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r, out->ready); break;
-            case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r, out->ready); break;
-            case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r, out->ready); break;
-            default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r, out->ready); break;
+            case 1: run_block<NP, 1>(st, h, ch, f0, f1, vb, r, out->ready); break;
+            case 2: run_block<NP, 2>(st, h, ch, f0, f1, vb, r, out->ready); break;
+            case 4: run_block<NP, 4>(st, h, ch, f0, f1, vb, r, out->ready); break;
+            case 8: run_block<NP, 8>(st, h, ch, f0, f1, vb, r, out->ready); break;
+            default: run_block<NP, 0>(st, h, ch, f0, f1, vb, r, out->ready); break;
         }
     }
     uint64_t mk = st.R0;
@@ -2077,7 +2158,7 @@ __device__ __forceinline__ Rec4 eval_one(const DevHeader& h, const VaEntry* __re
     for (uint32_t b = 0; b < h.B; b++) {
         const uint32_t ch = h.choice[h.coff[b] + dig[b]];
         const uint32_t k = ch_k(ch), p = ch_pool(ch);
-        run_block<NP, 0>(st, h, p, k, h.first[b], h.first[b + 1], va + h.voff[b] + dig[b], h.radix[b]);
+        run_block<NP, 0>(st, h, ch, h.first[b], h.first[b + 1], va + h.voff[b] + dig[b], h.radix[b]);
     }
     Rec4 r;
     r.w0 = st.R0;
@@ -2173,11 +2254,11 @@ __device__ Rec4 full_eval(const DevHeader& h, const VaEntry* __restrict__ va, ui
         const VaEntry* vb = va + h.voff[b] + dig[b];
         const uint32_t f0 = h.first[b], f1 = h.first[b + 1], r = h.radix[b];
         switch (k) {
-            case 1: run_block<NP, 1>(st, h, p, k, f0, f1, vb, r); break;
-            case 2: run_block<NP, 2>(st, h, p, k, f0, f1, vb, r); break;
-            case 4: run_block<NP, 4>(st, h, p, k, f0, f1, vb, r); break;
-            case 8: run_block<NP, 8>(st, h, p, k, f0, f1, vb, r); break;
-            default: run_block<NP, 0>(st, h, p, k, f0, f1, vb, r); break;
+            case 1: run_block<NP, 1>(st, h, ch, f0, f1, vb, r); break;
+            case 2: run_block<NP, 2>(st, h, ch, f0, f1, vb, r); break;
+            case 4: run_block<NP, 4>(st, h, ch, f0, f1, vb, r); break;
+            case 8: run_block<NP, 8>(st, h, ch, f0, f1, vb, r); break;
+            default: run_block<NP, 0>(st, h, ch, f0, f1, vb, r); break;
         }
     }
     Rec4 o;

@@ -94,6 +94,10 @@ struct sw_plan {
     uint64_t epoch = 1;          // bumped by every change of records or front
     bool released = false;       // records dropped since create/reset: the front covers more
     uint64_t merged_epoch = 0, merged_n = 0;  // multi-rank merged front cached in d_gather
+    // state epoch that changes only with calls every rank makes (eval, reset, release,
+    // stream): the merged-front cache is keyed on it, so every rank takes the same
+    // (cached or collective) branch whatever its local refolds did
+    uint64_t gepoch = 1;
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
     uint32_t coop_grid = 0;
@@ -290,7 +294,14 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         if (pr->gpus[p] < 1 || pr->gpus[p] > SW_MAX_GPUS_PER_POOL)
             return fail(nullptr, SW_EINVAL, "pool %u has %u GPUs (1..%d supported)", p, pr->gpus[p],
                         SW_MAX_GPUS_PER_POOL);
-    if (pr->billing > 1 || pr->objective > 1) return fail(nullptr, SW_EINVAL, "bad billing/objective");
+    if (pr->billing > 1 || pr->objective > 1 || pr->metric > 1)
+        return fail(nullptr, SW_EINVAL, "bad billing/objective/metric");
+    if (pr->metric && (!pr->power_active_w || !pr->power_idle_w))
+        return fail(nullptr, SW_EINVAL, "the energy metric needs power_active_w and power_idle_w");
+    if (pr->metric)
+        for (uint32_t p = 0; p < NP; p++)
+            if (pr->power_idle_w[p] > pr->power_active_w[p])
+                return fail(nullptr, SW_EINVAL, "pool %u: idle power above active power", p);
     // Spot over-provisioning (R32): billed GPUs G'_p = ceil(G_p * 1000 / (1000 - rho_p))
     uint32_t gbill[SW_MAX_POOLS];
     for (uint32_t p = 0; p < NP; p++) {
@@ -321,6 +332,11 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         const sw_choice& ch = tb->choices[c];
         if (ch.level >= tb->n_levels) return fail(nullptr, SW_EINVAL, "choice %u: level %u >= n_levels", c, ch.level);
         if (ch.pool >= NP) return fail(nullptr, SW_EINVAL, "choice %u: pool %u >= n_pools", c, ch.pool);
+        if (ch.vae) {  // DiT/VAE disaggregation (R37): the VAE stage runs on pool vae - 1
+            if (!tb->vae_us) return fail(nullptr, SW_EINVAL, "choice %u has a VAE stage but vae_us is NULL", c);
+            if (ch.vae > NP) return fail(nullptr, SW_EINVAL, "choice %u: VAE pool %u >= n_pools", c, ch.vae - 1);
+            if (ch.degree == 0) return fail(nullptr, SW_EINVAL, "choice %u: a STATIC choice has no VAE stage", c);
+        }
         if (ch.degree == 0) continue;  // STATIC rung: no video stage, no GPU (R33)
         if (ch.degree > pr->gpus[ch.pool])
             return fail(nullptr, SW_EINVAL, "choice %u: k = %u exceeds G_p = %u", c, ch.degree, pr->gpus[ch.pool]);
@@ -337,6 +353,13 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
                     if (stat != (tb->va_us[i] == 0))
                         return fail(nullptr, SW_EINVAL, "va_us[%llu] = %llu for a %s choice", (unsigned long long)i,
                                     (unsigned long long)tb->va_us[i], stat ? "STATIC" : "video");
+                    if (tb->vae_us) {  // a VAE stage takes time (1 .. 2^32 - 1 us); none: 0
+                        const bool vae = tb->choices[coff + c].vae != 0;
+                        if (vae != (tb->vae_us[i] != 0) || tb->vae_us[i] >= (1ull << 32))
+                            return fail(nullptr, SW_EINVAL, "vae_us[%llu] = %llu for a choice %s a VAE stage",
+                                        (unsigned long long)i, (unsigned long long)tb->vae_us[i],
+                                        vae ? "with" : "without");
+                    }
                 }
             coff += r;
         }
@@ -360,7 +383,10 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
             const uint32_t r = tb->radix[b];
             for (uint32_t s = tb->first_scene[b]; s < tb->first_scene[b + 1]; s++) {
                 uint64_t mx = 0;
-                for (uint32_t c = 0; c < r; c++) mx = std::max(mx, tb->va_us[off + (s - tb->first_scene[b]) * r + c]);
+                for (uint32_t c = 0; c < r; c++) {
+                    const uint64_t j = off + (s - tb->first_scene[b]) * r + c;
+                    mx = std::max(mx, tb->va_us[j] + (tb->vae_us ? tb->vae_us[j] : 0));
+                }
                 tmax += mx;
             }
             off += (uint64_t)(tb->first_scene[b + 1] - tb->first_scene[b]) * r;
@@ -371,9 +397,10 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         u128 cmax = pr->fixed_cost_mc;
         for (uint32_t p = 0; p < NP; p++) {
             const u128 X = (u128)gbill[p] * tmax;  // >= busy and >= G' * span (G' >= G)
-            const u128 prod = X * pr->price_mc_per_gpu_hour[p] + kHalfHour;
+            const u128 prod = pr->metric ? X * ((u128)pr->power_active_w[p] + pr->power_idle_w[p])  // energy, uJ
+                                         : X * pr->price_mc_per_gpu_hour[p] + kHalfHour;
             if (prod >= ((u128)1 << 64)) return fail(nullptr, SW_ERANGE, "cost bound of pool %u exceeds 2^64", p);
-            cmax += prod / kUsPerHour;
+            cmax += pr->metric ? prod : prod / kUsPerHour;
         }
         if (cmax >= ((u128)1 << 64)) return fail(nullptr, SW_ERANGE, "cost bound exceeds 2^64");
     }
@@ -441,7 +468,10 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     H.S = S;
     H.B = BP;
     H.NP = NP;
-    H.flags = (s0 ? 1u : 0u) | (pr->billing ? 2u : 0u) | (pr->objective ? 4u : 0u);
+    bool any_vae = false;
+    for (uint32_t c = 0; c < n_choice; c++) any_vae |= tb->choices[c].vae != 0;
+    H.flags = (s0 ? 1u : 0u) | (pr->billing ? 2u : 0u) | (pr->objective ? 4u : 0u) | (pr->metric ? 8u : 0u) |
+              (any_vae ? 16u : 0u);
     H.s0 = s0;
     H.R0_static = s0 ? sc->static_ready_us : 0;
     H.fixed_cost = pr->fixed_cost_mc;
@@ -462,7 +492,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
             H.voff[b] = voff;
             for (uint32_t c = 0; c < tb->radix[ub]; c++) {
                 const sw_choice& ch = tb->choices[coff - 1 + c];
-                H.choice[coff + c] = (uint32_t)ch.level | ((uint32_t)ch.degree << 8) | ((uint32_t)ch.pool << 16);
+                H.choice[coff + c] = (uint32_t)ch.level | ((uint32_t)ch.degree << 8) | ((uint32_t)ch.pool << 16) |
+                                     ((uint32_t)ch.vae << 24);
             }
             coff += tb->radix[ub];
             voff += (tb->first_scene[ub + 1] - tb->first_scene[ub]) * tb->radix[ub];
@@ -470,6 +501,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     }
     H.first[BP] = S;
     H.n_choice = coff;
+    if (H.first[BP] - H.first[BP - 1] == 1 && H.first[BP - 1] != 0) H.flags |= 32u;  // LSD fast path
     {  // group the LSD digit's choices by (pool, k) in first-appearance order
         const uint32_t bl = BP - 1, r = H.radix[bl];
         std::vector<uint32_t> keys;
@@ -510,6 +542,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         H.Gbill[p] = gbill[p];
         H.price[p] = pr->price_mc_per_gpu_hour[p];
         H.ready[p] = pr->pool_ready_us ? pr->pool_ready_us[p] : 0;  // load + warm-up (R31)
+        H.Pact[p] = pr->metric ? pr->power_active_w[p] : 0;       // energy metric (R38)
+        H.Pidle[p] = pr->metric ? pr->power_idle_w[p] : 0;
     }
     h->n_va = (uint32_t)n_va;
     h->va_bytes = (uint32_t)(n_va * sizeof(VaEntry));
@@ -527,7 +561,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
                 }
         }
     }
-    const size_t n_raw64 = 3 * (size_t)S + n_va;
+    const bool has_vae = tb->vae_us != nullptr;
+    const size_t n_raw64 = 3 * (size_t)S + n_va + (has_vae ? n_va : 0);
     const size_t raw_bytes = n_raw64 * 8 + (size_t)tb->n_levels * 4 + 2 * (size_t)n_va * 4;
     std::vector<uint8_t> raw(raw_bytes);
     size_t o = 0;
@@ -539,6 +574,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     put(sc->llm_us, 8 * (size_t)S);
     put(sc->tts_us, 8 * (size_t)S);
     put(tb->va_us, 8 * (size_t)n_va);
+    if (has_vae) put(tb->vae_us, 8 * (size_t)n_va);
     put(tb->level_score, 4 * (size_t)tb->n_levels);
     put(va_scene.data(), 4 * (size_t)n_va);
     put(va_choice.data(), 4 * (size_t)n_va);
@@ -560,7 +596,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
         rd.llm = r64 + S;
         rd.tts = r64 + 2 * S;
         rd.va = r64 + 3 * S;
-        const uint32_t* r32 = (const uint32_t*)(r64 + 3 * S + n_va);
+        rd.vae = has_vae ? r64 + 3 * S + n_va : nullptr;
+        const uint32_t* r32 = (const uint32_t*)(r64 + 3 * S + n_va + (has_vae ? n_va : 0));
         rd.score = r32;
         rd.va_scene = r32 + tb->n_levels;
         rd.va_choice = r32 + tb->n_levels + n_va;
@@ -609,9 +646,9 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
                 if (r != cudaSuccess && e == cudaSuccess) e = r;
                 return o;
             };
-            const int o0 = setup(eval_kernel<NPc, 0>), o1 = setup(eval_kernel<NPc, 1>);
-            setup(eval_kernel<NPc, 2>);
-            occ = (h->h.flags & 2u) ? o1 : o0;
+            const int o[3] = {setup(eval_kernel<NPc, 0>), setup(eval_kernel<NPc, 1>), setup(eval_kernel<NPc, 2>)};
+            setup(eval_kernel<NPc, 3>);
+            occ = o[eval_mode(h->h.flags)];
         });
         if (e != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -744,6 +781,7 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
 extern "C" sw_status sw_plan_reset(sw_plan* h) {
     if (!h) return fail(nullptr, SW_EINVAL, "null handle");
     h->epoch++;
+    h->gepoch++;
     h->segs.clear();
     h->rec_used = 0;
     h->cand_used = 0;
@@ -764,6 +802,7 @@ extern "C" sw_status sw_plan_release_records(sw_plan* h) {
     h->cand_used = 0;
     h->released = true;
     h->epoch++;
+    h->gepoch++;
     return SW_OK;
 }
 
@@ -886,6 +925,7 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
                     (unsigned long long)kMaxSegs);
     Segment sg{begin, end, b, e, h->rec_used, t0, n ? t1 - t0 : 0, false};
     h->epoch++;
+    h->gepoch++;
     CK(h, cudaSetDevice(h->device));
     if (n > 0) {
         const uint64_t need = (sg.ntiles * kTileRows + kEvalThreads - 1) / kEvalThreads;  // one warp per tile
@@ -902,8 +942,11 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
             launch_np(h, [&](auto np) {
                 constexpr int NPc = decltype(np)::value;
                 const EvalJob job{h->d_hdr, h->d_va, h->va_bytes, t0, t1, outp};
-                if (h->h.flags & 2u) eval_kernel<NPc, 1><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(job, nullptr);
-                else eval_kernel<NPc, 0><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(job, nullptr);
+                switch (eval_mode(h->h.flags)) {
+                    case 0: eval_kernel<NPc, 0><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(job, nullptr); break;
+                    case 1: eval_kernel<NPc, 1><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(job, nullptr); break;
+                    default: eval_kernel<NPc, 2><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(job, nullptr); break;
+                }
             });
         }
         CKL(h);
@@ -1121,10 +1164,17 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
 // Fold a segment chunk by chunk: DLT from the current front, one filter pass over the
 // chunk (fused with nq select queries when nq > 0), survivors merged on the device.
 static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
-    if (!h->d_dltc) {  // DLT-survivor buffer: 1/8 of the record capacity, 256 K..16 M points
-        h->dltc_cap = std::min<uint64_t>(std::max<uint64_t>(h->rec_cap / 8, 1ull << 18), 1ull << 24);
-        sw_status st = alloc_n(h, &h->d_dltc, h->dltc_cap, "DLT survivors");
-        if (st < 0) return st;
+    if (!h->d_dltc) {  // DLT-survivor buffer: 1/8 of the record capacity, 256 K..128 M points
+        // (a pass whose DLT survivors overflow it is refolded; 1/8 is ~5x the DLT pass rate
+        // of the configs measured, e.g. 1.5% on C3 against the final front)
+        for (uint64_t c = std::min<uint64_t>(std::max<uint64_t>(h->rec_cap / 8, 1ull << 18), 1ull << 27);; c /= 2) {
+            h->d_dltc = (PPoint*)dev_alloc(h, c * sizeof(PPoint));
+            if (h->d_dltc) {
+                h->dltc_cap = c;
+                break;
+            }
+            if (c <= (1ull << 18)) return fail(h, SW_ENOMEM, "DLT survivor buffer allocation failed");
+        }
     }
     const size_t psmem = kScanSmemPareto;
     // strided passes: units of upt tiles (a whole number of scan stages); pass 1 = every
@@ -1243,7 +1293,7 @@ static sw_status global_front_async(sw_plan* h, const PPoint** res, const uint64
     const int R = h->nranks;
     *res = h->d_gather;
     *d_n = h->d_counts + R + 2;
-    if (h->merged_epoch == h->epoch) return SW_OK;  // cached merge, size already on device
+    if (h->merged_epoch == h->gepoch) return SW_OK;  // cached merge, size already on device
     ParetoCtl* c = h->d_ctl;
     CK(h, cudaMemcpyAsync(h->d_counts + R, &c->front_n, 8, cudaMemcpyDeviceToDevice, h->stream));
     CK(h, cudaMemcpyAsync(h->d_counts + R + 1, &c->front_n, 8, cudaMemcpyDeviceToDevice, h->stream));
@@ -1461,7 +1511,7 @@ static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_sel
     if (merged_now) {
         if (aux[1]) redo_front = nf > 0;  // some rank's front exceeded the pad
         else if (!g_surv) {
-            h->merged_epoch = h->epoch;
+            h->merged_epoch = h->gepoch;
             h->merged_n = aux[0];
         }
     }
@@ -1626,6 +1676,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
     if (!h->segs.empty()) return fail(h, SW_ESTATE, "stream needs a handle without records (reset/release)");
     if (h->shared) return fail(h, SW_EINVAL, "the fused stream mode is not available for shared-pool fleets");
     CK(h, cudaSetDevice(h->device));
+    h->gepoch++;  // the stream folds new candidates into the front (every rank makes this call)
     sw_status st = stream_setup(h);
     if (st < 0) return st;
     // front-answerable queries (R30) come from the front when it covers exactly [begin, end)
@@ -1817,7 +1868,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
     if (g_cand) return fail(h, SW_ERANGE, "stream select candidates exceeded %u (on some rank): use sw_plan_sweep",
                             h->scand_cap);
     if (merged_now && !aux[1]) {
-        h->merged_epoch = h->epoch;
+        h->merged_epoch = h->gepoch;
         h->merged_n = aux[0];
     }
     sw_status worst = SW_OK;
@@ -1900,14 +1951,18 @@ static sw_status fold_pending(sw_plan* h) {
 // padded fronts, exact merge; cached until the state changes).  Collective.
 static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_out) {
     sw_status st = fold_pending(h);
-    if (st < 0) return st;
+    if (st < 0 && h->nranks == 1) return st;
     const PPoint* res = h->d_front;
     uint64_t n = h->front_n;
-    if (h->nranks > 1 && h->merged_epoch == h->epoch) {  // same state: the cached merge
+    if (h->nranks > 1 && h->merged_epoch == h->gepoch) {  // same state: the cached merge
+        if (st < 0) return st;  // (cannot happen: the cache implies complete fronts)
         n = h->merged_n;
         res = h->d_gather;
     } else if (h->nranks > 1) {  // a10: allgather counts, then padded fronts; exact merge
-        uint64_t mine = h->front_n;
+        // a rank whose fold failed still takes part in the count exchange (count = max
+        // marks the failure), so every rank fails together instead of hanging its peers
+        const std::string err = st < 0 ? h->err : std::string();
+        uint64_t mine = st < 0 ? ~0ull : h->front_n;
         CK(h, cudaMemcpyAsync(h->d_counts + h->nranks, &mine, 8, cudaMemcpyHostToDevice, h->stream));
         CKC(h, coll_allgather(coll_of(h), h->d_counts + h->nranks, h->d_counts, 8, &why_));
         std::vector<uint64_t> counts(h->nranks);
@@ -1915,6 +1970,8 @@ static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_ou
         SYNC(h);
         uint64_t maxc = 1, tot = 0;
         for (uint64_t c : counts) {
+            if (c == ~0ull)
+                return fail(h, st < 0 ? st : SW_ERANGE, "%s", st < 0 ? err.c_str() : "a peer rank's Pareto fold failed");
             maxc = std::max(maxc, c);
             tot += c;
         }
@@ -1935,7 +1992,7 @@ static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_ou
         n = h->front_n;
         res = h->d_gather;
         h->front_n = mine;
-        h->merged_epoch = h->epoch;
+        h->merged_epoch = h->gepoch;
         h->merged_n = n;
         CK(h, cudaMemcpyAsync(&h->d_ctl->front_n, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
         // the asynchronous path reads the cached merge's size from the device
@@ -2115,6 +2172,9 @@ extern "C" sw_status sw_shared_create(uint32_t n, const sw_profile_tables* table
     if (!tables || !scenes || !reqs || !pools || !rt || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (n < 1 || n > (uint32_t)kShMaxReq) return fail(nullptr, SW_EINVAL, "shared fleet of %u requests (1..%d)", n, kShMaxReq);
     if (pools->evict_risk_permille) return fail(nullptr, SW_EINVAL, "shared pools take no eviction risk");
+    if (pools->metric) return fail(nullptr, SW_EINVAL, "shared-pool fleets use the money metric");
+    for (uint32_t r = 0; r < n; r++)
+        if (tables[r].vae_us) return fail(nullptr, SW_EINVAL, "request %u: DiT/VAE stages are not supported in shared-pool fleets", r);
     if (rt->nranks < 1 || rt->rank < 0 || rt->rank >= rt->nranks)
         return fail(nullptr, SW_EINVAL, "bad rank %d of %d", rt->rank, rt->nranks);
     if (rt->nranks > 1 && !rt->nccl_comm) return fail(nullptr, SW_EINVAL, "nranks > 1 needs nccl_comm");
@@ -2325,7 +2385,7 @@ struct sw_fleet {
     LoopComm* loop = nullptr;
     int rank = 0, nranks = 1;
     uint32_t np_max = 1;
-    int bmode = -1;  // eval billing mode: 0 / 1 when every request bills RESERVED / BUSY, else 2
+    int bmode = -1;  // eval path (eval_mode) shared by every request, else 3 (runtime)
     size_t eval_smem = 0;
     int eval_occ = 1, num_sms = 148;
     uint32_t gx = 1;  // scan blocks per request
@@ -2412,8 +2472,8 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
         }
         f->plans.push_back(p);
         f->np_max = std::max(f->np_max, p->NP);
-        const int bm = (p->h.flags & 2u) ? 1 : 0;
-        f->bmode = f->bmode < 0 ? bm : (f->bmode == bm ? bm : 2);
+        const int bm = eval_mode(p->h.flags);
+        f->bmode = f->bmode < 0 ? bm : (f->bmode == bm ? bm : 3);
         f->eval_smem = std::max(f->eval_smem, p->eval_smem);
     }
     sw_plan* h = f->plans[0];
@@ -2436,8 +2496,9 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
                 if (r != cudaSuccess && e == cudaSuccess) e = r;
                 return o;
             };
-            const int o0 = setup(eval_kernel<NPc, 0>), o1 = setup(eval_kernel<NPc, 1>), o2 = setup(eval_kernel<NPc, 2>);
-            occ = f->bmode == 0 ? o0 : f->bmode == 1 ? o1 : o2;
+            const int o[4] = {setup(eval_kernel<NPc, 0>), setup(eval_kernel<NPc, 1>), setup(eval_kernel<NPc, 2>),
+                              setup(eval_kernel<NPc, 3>)};
+            occ = o[f->bmode];
         });
         if (e != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -2543,9 +2604,12 @@ extern "C" sw_status sw_fleet_eval(sw_fleet* f) {
     CK(h, cudaEventRecord(f->ev[0], f->stream));
     launch_np_n(f->np_max, h, [&](auto np) {
         constexpr int NPc = decltype(np)::value;
-        if (f->bmode == 0) eval_kernel<NPc, 0><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
-        else if (f->bmode == 1) eval_kernel<NPc, 1><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
-        else eval_kernel<NPc, 2><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs);
+        switch (f->bmode) {
+            case 0: eval_kernel<NPc, 0><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs); break;
+            case 1: eval_kernel<NPc, 1><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs); break;
+            case 2: eval_kernel<NPc, 2><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs); break;
+            default: eval_kernel<NPc, 3><<<dim3(gxe, n), kEvalThreads, f->eval_smem, f->stream>>>(EvalJob{}, f->d_ejobs); break;
+        }
     });
     CKL(h);
     CK(h, cudaEventRecord(f->ev[1], f->stream));
@@ -2752,4 +2816,4 @@ extern "C" const char* sw_last_error(const sw_plan* h) {
 
 extern "C" uint64_t sw_plan_launch_count(const sw_plan* h) { return h ? h->launches : 0; }
 
-extern "C" int32_t sw_abi_version(void) { return 5; }  // 2: pool_ready_us; 3: evict_risk_permille; 4: loopback, decode, segments; 5: shared-pool fleets
+extern "C" int32_t sw_abi_version(void) { return 6; }  // 2: pool_ready_us; 3: evict_risk_permille; 4: loopback, decode, segments; 5: shared-pool fleets; 6: VAE stages, energy metric

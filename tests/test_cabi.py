@@ -30,7 +30,7 @@ def test_exports_every_declared_symbol(sw):
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(sw.EXPORTS), set(syms) ^ set(sw.EXPORTS)
-    assert sw.lib().sw_abi_version() == 5 == sw.ABI_VERSION
+    assert sw.lib().sw_abi_version() == 6 == sw.ABI_VERSION
 
 
 def test_fails_loudly_without_gpu(sw):

@@ -353,3 +353,59 @@ def _cudart():
     import nvidia.cuda_runtime
     d = os.path.join(os.path.dirname(nvidia.cuda_runtime.__file__), "lib")
     return ctypes.CDLL(sorted(glob.glob(os.path.join(d, "libcudart.so*")))[0])
+
+
+@pytest.mark.parametrize("cfg", ["C3d", "C3e", "C3ex"])
+def test_disagg_and_energy_full_space(sw, oracle_mod, cfg):
+    """C3d (FramePack DiT/VAE disaggregated onto a VAE pool, R37) and
+    C3e / C3ex (records scored by energy in microjoules, QUALITY_FIRST and Energy x TTFF,
+    R38): the full space at the bench's launch configuration -- winners, exact front,
+    digest -- plus sampled records and winner details vs the oracle."""
+    pb = make_config(cfg)
+    g = _golden(cfg)
+    orc = oracle_mod.Oracle(pb)
+    with sw.Plan(pb) as plan:
+        plan.eval(0, plan.n)
+        sels = plan.select_batch(pb.queries)
+        _check_winners(sels, g["winners"])
+        assert plan.pareto() == [tuple(p) for p in g["front"]]
+        assert plan.digest() == int(g["digest"])
+        rng = random.Random(13)
+        for _ in range(40):
+            b = rng.randrange(plan.n - 512)
+            _records_equal(plan, orc, b, b + 512)
+        for _ in range(10):
+            i = rng.randrange(plan.n)
+            sel, ready = plan.detail(i)
+            rec, oready, pend, mk, te = orc.eval(i)
+            assert tuple(sel.rec) == rec.astuple() and ready == oready and sel.pool_end_us == pend
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_disagg_energy_random(sw, oracle_mod, seed):
+    """Random problems with VAE stages on a VAE pool and/or the energy metric (both
+    billings, both objectives): every record, winners, front, digest; stream == records."""
+    from tests.test_disagg_energy_oracle import _disagg
+    rng = random.Random(2000 + seed)
+    pb = random_problem(rng, max_scenes=6, max_pools=3, max_choices=4, one_scene_digits=rng.random() < 0.5)
+    if seed % 3 != 2:
+        _disagg(pb, rng)
+    if seed % 3 != 0:
+        pb.metric = 1
+        pb.power_active_w = [rng.randint(200, 1200) for _ in pb.gpus]
+        pb.power_idle_w = [rng.randint(10, 150) for _ in pb.gpus]
+    orc = oracle_mod.Oracle(pb)
+    n = orc.n
+    qs = [Query(INF, INF, INF), Query(rng.randint(0, 10**8), rng.randint(0, 10**8), rng.randint(0, 10**12)),
+          Query(0, 0, 0)]
+    w, f, d = orc.sweep(0, n, qs)
+    exp = [{"status": st, "index": i, "rec": r.astuple()} for st, i, r in w]
+    with sw.Plan(pb) as plan:
+        plan.eval(0, n)
+        _records_equal(plan, orc, 0, n)
+        _check_winners(plan.select_batch(qs), exp)
+        assert plan.pareto() == f
+        assert plan.digest() == d
+    with sw.Plan(pb, record_capacity=1024) as plan:
+        _check_winners(plan.stream(0, n, qs), exp)
+        assert plan.pareto() == f

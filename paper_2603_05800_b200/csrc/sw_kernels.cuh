@@ -1322,25 +1322,30 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
     uint32_t debug;     // count DLT passes (SW_DEBUG)
 };
 
-// The deferred exact Pareto test of a scan pass (DLT survivors, appended by the scan):
-//  (1) every candidate x is tested against the running front (sorted by t: only points
-//      with t <= x.t can dominate it), from the point with the largest such t downwards --
-//      the dominator the DLT missed is usually just below x.t -- stopping at the first
-//      dominator; an identical entry (same index) also removes x: it is already kept;
-//  (2) the candidates that pass are tested against this block's own earlier survivors and
-//      against each other: a block walks a contiguous range of the buffer (neighbouring
-//      records, which often dominate each other), so its survivor list works as a running
-//      local front and keeps the merge small; the list is flushed to surv (ctl->surv) when
-//      full and at the end.  A dropped survivor only loosens a filter: a record dominated by
-//      a real candidate is never a front point, so the merge stays exact.
-// Dropped DLT survivors (candidate buffer full) set surv_overflow: the merged front is then
-// valid but incomplete and the pass is refolded.  The front (<= kExactFront points) and the
-// block list live in dynamic shared memory as arrays (t, c, idx, q).
+// The deferred exact Pareto test of a scan pass (DLT survivors, appended by the scan).
+// Every WARP walks its own contiguous run of the candidate buffer, 32 candidates at a time,
+// with no block-wide barrier:
+//  (1) each lane tests its candidate x against the 8 front points just below x.t (the
+//      front is sorted by t; only points with t <= x.t can dominate x, and the dominator
+//      the DLT missed is almost always just below x.t, in x's own t bin);
+//  (2) the still undecided candidates (rare) are tested by the whole warp against the rest
+//      of the front, 32 points per step, early exit on a hit;
+//  (3) a candidate not dominated by the front is tested by the warp against the warp's own
+//      earlier survivors (neighbouring records often dominate each other) and, if it
+//      passes, joins that list at once; lists are flushed to surv (ctl->surv) when full and
+//      at the end.  An identical entry (same index) also removes x: it is already kept.
+// A survivor list only loosens a filter (a record dominated by a real candidate is never a
+// front point), so the merge after the pass stays exact.  Dropped DLT survivors (candidate
+// buffer full) set surv_overflow: the merged front is then valid but incomplete and the pass
+// is refolded.  The front (<= kExactFront points) and the lists live in dynamic shared
+// memory as arrays (t, c, idx, q).
 constexpr uint32_t kExactFront = 2048;  // front points staged in smem (larger fronts: from L2)
-constexpr uint32_t kExactList = 2048;   // block survivor list
-constexpr int kExactThreads = 512;      // = candidates per chunk
+constexpr uint32_t kExactList = 128;    // per-warp survivor list
+constexpr int kExactThreads = 512;
+constexpr int kExactWarps = kExactThreads / 32;
+constexpr uint32_t kExactNear = 8;      // front points below x.t tested per lane first
 __host__ __device__ constexpr size_t exact_smem_bytes() {
-    return (size_t)(kExactFront + kExactList + kExactThreads) * (3 * sizeof(uint64_t) + sizeof(uint32_t));
+    return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t));
 }
 struct PArrays {  // a point list as arrays in shared memory
     uint64_t *t, *c, *i;
@@ -1375,75 +1380,99 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
                                                                         PPoint* __restrict__ surv, uint64_t surv_cap) {
     extern __shared__ __align__(16) unsigned char xsm[];
     const PArrays F = parrays(xsm, kExactFront);
-    const PArrays L = parrays(xsm + (size_t)kExactFront * 28, kExactList);
-    const PArrays K = parrays(xsm + (size_t)(kExactFront + kExactList) * 28, kExactThreads);
-    __shared__ uint32_t s_nl, s_nk;
-    __shared__ unsigned long long s_base;
     const unsigned long long nd = ctl->dlt_n;
     const uint64_t n = nd < cand_cap ? nd : cand_cap;
     const uint32_t m = (uint32_t)ctl->front_n;
     if (blockIdx.x == 0 && threadIdx.x == 0 && nd > cand_cap) ctl->surv_overflow = 1;
-    // this block's contiguous range of the candidate buffer
     const uint64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
     if (r0 >= r1) return;
     const bool f_smem = m <= kExactFront;
     if (f_smem)
         for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) F.put(j, front[j]);
-    if (threadIdx.x == 0) s_nl = 0;
-    auto flush = [&]() {  // block list -> surv (all threads; ends with a barrier)
-        const uint32_t nl = s_nl;
-        if (threadIdx.x == 0) s_base = nl ? atomicAdd(&ctl->surv, (unsigned long long)nl) : 0ull;
-        __syncthreads();
-        for (uint32_t j = threadIdx.x; j < nl; j += blockDim.x)
-            if (s_base + j < surv_cap) surv[s_base + j] = L.get(j);
-        __syncthreads();
-        if (threadIdx.x == 0) s_nl = 0;
-        __syncthreads();
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const PArrays L = parrays(xsm + (size_t)kExactFront * 28 + (size_t)warp * kExactList * 28, kExactList);
+    auto fget = [&](uint32_t j) { return f_smem ? F.get(j) : front[j]; };
+    // this warp's run of the block's range
+    const uint64_t w0 = r0 + (r1 - r0) * warp / kExactWarps, w1 = r0 + (r1 - r0) * (warp + 1) / kExactWarps;
+    uint32_t nl = 0;  // warp-uniform list fill
+    auto flush = [&]() {
+        unsigned long long b = 0;
+        if (lane == 0 && nl) b = atomicAdd(&ctl->surv, (unsigned long long)nl);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        for (uint32_t j = lane; j < nl; j += 32)
+            if (b + j < surv_cap) surv[b + j] = L.get(j);
+        __syncwarp();
+        nl = 0;
     };
-    for (uint64_t c0 = r0; c0 < r1; c0 += kExactThreads) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_nk = 0;
-        __syncthreads();
-        // (1) against the running front
-        const uint64_t i = c0 + threadIdx.x;
-        if (i < r1) {
-            const PPoint x = cand[i];
-            uint32_t lo = 0, hi = m;  // #front points with t <= x.t
+    for (uint64_t base = w0; base < w1; base += 32) {
+        const uint64_t i = base + lane;
+        const bool valid = i < w1;
+        PPoint x{};
+        uint32_t lo = 0;
+        bool dom = !valid;
+        if (valid) {
+            x = cand[i];
+            uint32_t hi = m;  // lo = #front points with t <= x.t
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) >> 1;
                 if ((f_smem ? F.t[mid] : front[mid].t) <= x.t) lo = mid + 1;
                 else hi = mid;
             }
-            bool dom = false;
-            for (uint32_t j = lo; j > 0 && !dom;) {
+            // (1) the nearest points below x.t
+            const uint32_t stop = lo > kExactNear ? lo - kExactNear : 0;
+            for (uint32_t j = lo; j > stop && !dom;) {
                 j--;
-                dom = pdom(f_smem ? F.get(j) : front[j], 0, x, 1);
+                dom = pdom(fget(j), 0, x, 1);
             }
-            if (!dom) K.put(atomicAdd(&s_nk, 1u), x);
         }
-        __syncthreads();
-        const uint32_t nk = s_nk, nl = s_nl;
-        // (2) against the block's earlier survivors and the chunk's other survivors
-        bool keep = false;
-        PPoint x{};
-        if (threadIdx.x < nk) {
-            x = K.get(threadIdx.x);
-            bool dom = false;
-            for (uint32_t j = 0; j < nl && !dom; j++) dom = pdom(L.get(j), 0, x, 1);
-            for (uint32_t j = 0; j < nk && !dom; j++)
-                if (j != threadIdx.x) dom = pdom(K.get(j), j, x, threadIdx.x);
-            keep = !dom;
+        const uint32_t top = lo > kExactNear ? lo - kExactNear : 0;  // still to test: [0, top)
+        // (2) undecided candidates: the whole warp against the rest of the front
+        unsigned hard = __ballot_sync(0xffffffffu, !dom && top > 0);
+        while (hard) {
+            const int src = __ffs(hard) - 1;
+            hard &= hard - 1;
+            PPoint y;
+            y.t = __shfl_sync(0xffffffffu, x.t, src);
+            y.c = __shfl_sync(0xffffffffu, x.c, src);
+            y.idx = __shfl_sync(0xffffffffu, x.idx, src);
+            y.q = __shfl_sync(0xffffffffu, x.q, src);
+            y.pad = 0;
+            const uint32_t ytop = __shfl_sync(0xffffffffu, top, src);
+            bool d = false;
+            for (uint32_t j1 = ytop; j1 > 0 && !d;) {  // downwards: nearer points first
+                const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
+                const uint32_t j = j0 + lane;
+                d = __any_sync(0xffffffffu, j < j1 && pdom(fget(j < j1 ? j : 0), 0, y, 1));
+                j1 = j0;
+            }
+            if (lane == src) dom = d;
         }
-        __syncthreads();
-        if (nl + nk > kExactList) {  // no room for the chunk's survivors: flush first
-            flush();
+        // (3) front survivors: against the warp's earlier survivors, then join the list
+        unsigned keep = __ballot_sync(0xffffffffu, !dom);
+        while (keep) {
+            const int src = __ffs(keep) - 1;
+            keep &= keep - 1;
+            PPoint y;
+            y.t = __shfl_sync(0xffffffffu, x.t, src);
+            y.c = __shfl_sync(0xffffffffu, x.c, src);
+            y.idx = __shfl_sync(0xffffffffu, x.idx, src);
+            y.q = __shfl_sync(0xffffffffu, x.q, src);
+            y.pad = 0;
+            bool d = false;
+            for (uint32_t j0 = 0; j0 < nl && !d; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                d = __any_sync(0xffffffffu, j < nl && pdom(L.get(j), 0, y, 1));
+            }
+            if (d) continue;
+            if (nl == kExactList) flush();
+            if (lane == 0) L.put(nl, y);
+            __syncwarp();
+            nl++;
         }
-        if (keep) L.put(atomicAdd(&s_nl, 1u), x);
     }
-    __syncthreads();
     flush();
-}
-// objective keys only (ties keep the earlier = lower index within a thread's scan)
+}// objective keys only (ties keep the earlier = lower index within a thread's scan)
 __device__ __forceinline__ bool obj_strict_better(uint32_t obj, const Rec4& a, const Rec4& b) {
     const uint32_t qa = rec_Q(a), qb = rec_Q(b);
     if (obj == 0) {
@@ -1900,10 +1929,9 @@ __global__ void detail_fleet_kernel(const EvalJob* __restrict__ jobs, const Cand
 //    which the usual pipeline merges into the front after the pass.
 struct StreamArgs {
     const Dlt* dlt;
-    const PPoint* front;  // the running front (sorted by t), ctl->front_n points
-    ParetoCtl* ctl;
-    PPoint* surv;
-    uint64_t surv_cap;
+    ParetoCtl* ctl;  // dlt_n: DLT survivors appended (atomics)
+    PPoint* pts;     // DLT survivors of the pass (exact-tested by pareto_exact_kernel)
+    uint64_t pts_cap;
     Cand* cand;        // [SW_MAX_QUERIES][cand_cap] reported candidates per query
     uint32_t* cand_n;  // [SW_MAX_QUERIES]
     uint32_t cand_cap;
@@ -1933,16 +1961,12 @@ struct StreamShared {
     unsigned long long key[SW_MAX_QUERIES];   // best pruning key of a reported feasible candidate
     unsigned long long ckey[SW_MAX_QUERIES];  // best closest-tier key of a reported candidate
     uint32_t feas[SW_MAX_QUERIES];            // a feasible candidate was reported
-    uint32_t bcnt;                            // block survivor list fill
-    uint32_t m_sm, m_all;                     // front points in smem / in all
 };
 
 struct StreamEmit {
     const StreamArgs* sa;
     StreamShared* ss;
     const Dlt* d;
-    const PPoint* fs;  // front subset in smem
-    PPoint* bsurv;     // block survivor list (smem)
     DltHot dh;
     uint64_t rowbase;  // global index of this lane's row's first candidate
     uint32_t rl;
@@ -2001,115 +2025,54 @@ struct StreamEmit {
                 }
                 __syncwarp();
             }
-            // ---- a8: DLT filter, then the exact test of its (rare) survivors
+            // ---- a8: the DLT filter; its (rare) survivors go to the pass's candidate
+            // buffer -- one atomic per warp -- and are exact-tested after the pass by
+            // pareto_exact_kernel (deferred, as in the scan)
             const bool cand = valid && !dlt_dominated(*e->d, e->dh, r.w0 + r.w1, r.w2, rec_Q(r));
-            unsigned pend = __ballot_sync(0xffffffffu, cand);
+            const unsigned pend = __ballot_sync(0xffffffffu, cand);
             if (!pend) return;
-            PPoint pt;
-            pt.idx = idx;
-            pt.t = r.w0 + r.w1;
-            pt.c = r.w2;
-            pt.q = rec_Q(r);
-            pt.pad = 0;
-            bool keep = cand;
-            const PPoint* fs = e->fs;
-            const uint32_t m_sm = S.m_sm, m_all = S.m_all;
-            while (pend) {  // each survivor tested by the whole warp
-                const int src = __ffs(pend) - 1;
-                pend &= pend - 1;
-                PPoint x;
-                x.idx = __shfl_sync(0xffffffffu, pt.idx, src);
-                x.t = __shfl_sync(0xffffffffu, pt.t, src);
-                x.c = __shfl_sync(0xffffffffu, pt.c, src);
-                x.q = __shfl_sync(0xffffffffu, pt.q, src);
-                bool dom = false;
-                // front sorted by t: only points with t <= x.t can dominate x; probe for the
-                // chunk holding the last such point and test downwards (as scan_kernel)
-                uint32_t top = 0;
-                {
-                    const uint32_t chk = max((m_all + 31u) / 32u, 1u);
-                    const uint32_t pi = lane * chk;
-                    const uint64_t tp = pi < m_all ? (pi < m_sm ? fs[pi].t : a.front[pi].t) : kInf64;
-                    const unsigned pb = __ballot_sync(0xffffffffu, tp <= x.t);
-                    if (pb) top = min(m_all, (uint32_t)(31 - __clz(pb)) * chk + chk);
-                }
-                for (uint32_t j1 = top; j1 > 0 && !dom;) {
-                    const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
-                    const uint32_t j = j0 + lane;
-                    const bool dj = j < j1 && pdom(j < m_sm ? fs[j] : a.front[j < j1 ? j : 0], 0, x, 1);
-                    if (__any_sync(0xffffffffu, dj)) dom = true;
-                    j1 = j0;
-                }
-                const uint32_t bc = min(*(volatile uint32_t*)&S.bcnt, kBlockSurv);
-                for (uint32_t j0 = 0; !dom && j0 < bc; j0 += 32) {
-                    const uint32_t j = j0 + lane;
-                    if (__any_sync(0xffffffffu, j < bc && pdom(e->bsurv[j], 0, x, 1))) dom = true;
-                }
-                if (lane == src && dom) keep = false;
-            }
-            const unsigned mask = __ballot_sync(0xffffffffu, keep);
-            if (!mask) return;
-            const int ldr = __ffs(mask) - 1;
-            uint32_t b0 = 0;
-            if (lane == ldr) b0 = atomicAdd(&S.bcnt, (uint32_t)__popc(mask));
+            const int ldr = __ffs(pend) - 1;
+            unsigned long long b0 = 0;
+            if (lane == ldr) b0 = atomicAdd(&a.ctl->dlt_n, (unsigned long long)__popc(pend));
             b0 = __shfl_sync(0xffffffffu, b0, ldr);
-            const uint32_t my = b0 + __popc(mask & ((1u << lane) - 1u));
-            const bool local = my < kBlockSurv;
-            if (keep && local) e->bsurv[my] = pt;
-            const unsigned gmask = __ballot_sync(0xffffffffu, keep && !local);  // list full: global
-            if (gmask) {
-                const int gl = __ffs(gmask) - 1;
-                unsigned long long s0 = 0;
-                if (lane == gl) s0 = atomicAdd(&a.ctl->surv, (unsigned long long)__popc(gmask));
-                s0 = __shfl_sync(0xffffffffu, s0, gl);
-                if (keep && !local) {
-                    const uint64_t slot = s0 + __popc(gmask & ((1u << lane) - 1u));
-                    if (slot < a.surv_cap) a.surv[slot] = pt;
-                }
+            const uint64_t slot = b0 + __popc(pend & ((1u << lane) - 1u));
+            if (cand && slot < a.pts_cap) {
+                PPoint pt;
+                pt.idx = idx;
+                pt.t = r.w0 + r.w1;
+                pt.c = r.w2;
+                pt.q = rec_Q(r);
+                pt.pad = 0;
+                a.pts[slot] = pt;
             }
         }
     };
     __device__ __forceinline__ Put at(uint32_t dm, bool live) const { return Put{this, rowbase + (uint64_t)dm * rl, live}; }
 };
 
-constexpr int kStreamThreads = 512;  // one block per SM: the DLT (~72 KB) is staged once per SM
+constexpr int kStreamThreads = 256;  // each block stages the DLT (~72 KB) + tables
+// registers: the eval path plus the in-kernel filters (2 blocks/SM only for one pool)
+__host__ __device__ constexpr int stream_min_blocks(int np, int bm) { return (np == 1 && bm < 2) ? 2 : 1; }
 
-template <int NP>
-__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(EvalJob job, const __grid_constant__ StreamArgs sa) {
+// BM: the eval path (eval_mode) at compile time, as in eval_kernel.
+template <int NP, int BM>
+__global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) stream_kernel(EvalJob job, const __grid_constant__ StreamArgs sa) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bar;
     __shared__ StreamShared ss;
     DevHeader& h = *reinterpret_cast<DevHeader*>(smem);
     VaEntry* va = reinterpret_cast<VaEntry*>(smem + sizeof(DevHeader));
     Dlt* d = reinterpret_cast<Dlt*>(smem + ((sizeof(DevHeader) + job.va_bytes + 127) & ~(size_t)127));
-    PPoint* fs = reinterpret_cast<PPoint*>(d + 1);
-    PPoint* bsurv = fs + kFrontSmem;
-    const uint32_t m_all = (uint32_t)sa.ctl->front_n, m_sm = min(m_all, kFrontSmem);
-    {  // the DLT (16 B vectors), the front subset, the sentinel survivor list, the queries
+    {  // the DLT (16 B vectors) and the queries
         const uint4* src = reinterpret_cast<const uint4*>(sa.dlt);
         uint4* dst = reinterpret_cast<uint4*>(d);
         for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
-        for (uint32_t i = threadIdx.x; i < m_sm; i += blockDim.x) fs[i] = sa.front[i];
-        for (uint32_t i = threadIdx.x; i < kBlockSurv; i += blockDim.x) {
-            PPoint sent;  // a reserved-but-unwritten slot dominates nothing
-            sent.idx = kInf64;
-            sent.t = kInf64;
-            sent.c = kInf64;
-            sent.q = 0;
-            sent.pad = 0;
-            bsurv[i] = sent;
-        }
     }
     if (threadIdx.x < SW_MAX_QUERIES) {
         ss.q[threadIdx.x] = sa.P.q[threadIdx.x];
         ss.key[threadIdx.x] = sa.gkey[threadIdx.x];
         ss.ckey[threadIdx.x] = sa.gkey[SW_MAX_QUERIES + threadIdx.x];
         ss.feas[threadIdx.x] = sa.gkey[2 * SW_MAX_QUERIES + threadIdx.x] ? 1u : 0u;
-    }
-    if (threadIdx.x == 0) {
-        ss.bcnt = 0;
-        ss.m_sm = m_sm;
-        ss.m_all = m_all;
     }
     stage_tables(job.hdr, job.va, &h, va, (uint32_t)job.va_bytes, &bar);  // ends with a barrier
     const DltHot dh{d->kbase, d->qmin, d->qmax, d->qshift, d->cshift};
@@ -2131,17 +2094,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(EvalJob job, 
         __syncwarp();
         const uint64_t H = t * kTileRows + lane;
         const uint64_t rb = H * row;
-        const StreamEmit em{&sa, &ss, d, fs, bsurv, dh, rb, rl, rb < sa.ib || rb + row > sa.ie};
-        eval_tile<NP>(h, va, t, em);
+        const StreamEmit em{&sa, &ss, d, dh, rb, rl, rb < sa.ib || rb + row > sa.ie};
+        eval_tile_b<NP, BM != 0, BM == 2>(h, va, t, em);
     }
-    // flush this block's survivor list to the pass's survivor buffer
-    __syncthreads();
-    __shared__ unsigned long long s_base;
-    const uint32_t nb = min(ss.bcnt, kBlockSurv);
-    if (threadIdx.x == 0) s_base = nb ? atomicAdd(&sa.ctl->surv, (unsigned long long)nb) : 0ull;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
-        if (s_base + i < sa.surv_cap) sa.surv[s_base + i] = bsurv[i];
 }
 
 // One candidate from scratch (a1-a7 for a single index; plain loads from global/L2).

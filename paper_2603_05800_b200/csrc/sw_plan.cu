@@ -144,6 +144,7 @@ struct sw_plan {
     uint64_t* h_pass_surv = nullptr;       // pinned: survivors of each stream pass (<= 21 levels)
     uint32_t scand_cap = 1u << 18;
     size_t stream_smem = 0;
+    int stream_occ[3] = {1, 1, 1};  // resident stream blocks per SM, per eval path
     uint64_t stream_passes = 0;    // diagnostics
 };
 
@@ -1163,19 +1164,30 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
 
 // Fold a segment chunk by chunk: DLT from the current front, one filter pass over the
 // chunk (fused with nq select queries when nq > 0), survivors merged on the device.
-static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
-    if (!h->d_dltc) {  // DLT-survivor buffer: 1/8 of the record capacity, 256 K..128 M points
-        // (a pass whose DLT survivors overflow it is refolded; 1/8 is ~5x the DLT pass rate
-        // of the configs measured, e.g. 1.5% on C3 against the final front)
-        for (uint64_t c = std::min<uint64_t>(std::max<uint64_t>(h->rec_cap / 8, 1ull << 18), 1ull << 27);; c /= 2) {
-            h->d_dltc = (PPoint*)dev_alloc(h, c * sizeof(PPoint));
-            if (h->d_dltc) {
-                h->dltc_cap = c;
-                break;
-            }
-            if (c <= (1ull << 18)) return fail(h, SW_ENOMEM, "DLT survivor buffer allocation failed");
-        }
+// The DLT-survivor buffer of the deferred exact Pareto test: 1/8 of the candidates a pass
+// can cover (records held, or a stream shard), 256 K..128 M points -- a pass whose DLT
+// survivors overflow it is refolded / re-run; 1/8 is ~5x the DLT pass rate measured (1.5%
+// on C3 against the final front).  Grown on demand.
+static sw_status ensure_dltc(sw_plan* h, uint64_t candidates) {
+    const uint64_t want = std::min<uint64_t>(std::max<uint64_t>(candidates / 8, 1ull << 18), 1ull << 27);
+    if (h->d_dltc && h->dltc_cap >= want) return SW_OK;
+    if (h->d_dltc) {
+        dev_free(h, h->d_dltc);
+        h->d_dltc = nullptr;
+        h->dltc_cap = 0;
     }
+    for (uint64_t c = want;; c /= 2) {
+        h->d_dltc = (PPoint*)dev_alloc(h, c * sizeof(PPoint));
+        if (h->d_dltc) {
+            h->dltc_cap = c;
+            return SW_OK;
+        }
+        if (c <= (1ull << 18)) return fail(h, SW_ENOMEM, "DLT survivor buffer allocation failed");
+    }
+}
+
+static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, const SelParams& P, uint32_t* np) {
+    if (sw_status st = ensure_dltc(h, h->rec_cap); st < 0) return st;
     const size_t psmem = kScanSmemPareto;
     // strided passes: units of upt tiles (a whole number of scan stages); pass 1 = every
     // 8^K-th unit (about kFirstPass records, at most 1/64 of the segment), each further
@@ -1642,24 +1654,30 @@ static sw_status stream_setup(sw_plan* h) {
     if ((st = alloc_n(h, &h->d_scand, (uint64_t)SW_MAX_QUERIES * h->scand_cap, "stream candidates")) < 0) return st;
     if ((st = alloc_n(h, &h->d_scand_n, SW_MAX_QUERIES, "stream candidate counts")) < 0) return st;
     if ((st = alloc_n(h, &h->d_skey, 3 * SW_MAX_QUERIES, "stream pruning keys")) < 0) return st;
-    CK(h, cudaMallocHost((void**)&h->h_pass_surv, 32 * sizeof(uint64_t)));
-    h->stream_smem = ((sizeof(DevHeader) + h->va_bytes + 127) & ~(size_t)127) + sizeof(Dlt) +
-                     (kFrontSmem + kBlockSurv) * sizeof(PPoint);
+    CK(h, cudaMallocHost((void**)&h->h_pass_surv, 64 * sizeof(uint64_t)));  // [lvl] survivors, [32+lvl] DLT survivors
+    h->stream_smem = ((sizeof(DevHeader) + h->va_bytes + 127) & ~(size_t)127) + sizeof(Dlt);
     cudaError_t e = cudaSuccess;
     launch_np(h, [&](auto np) {
         constexpr int NPc = decltype(np)::value;
-        int optin = 0, occ = 0;
+        int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
-        cudaFuncAttributes fa{};
-        e = cudaFuncGetAttributes(&fa, stream_kernel<NPc>);
-        const size_t dyn_max = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
-        if (e == cudaSuccess)
-            e = dyn_max < h->stream_smem ? cudaErrorInvalidValue
-                                         : cudaFuncSetAttribute(stream_kernel<NPc>,
-                                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max);
-        if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<NPc>, kStreamThreads, h->stream_smem);
-        if (e == cudaSuccess && occ < 1) e = cudaErrorLaunchOutOfResources;
+        auto setup = [&](auto kern) {
+            cudaFuncAttributes fa{};
+            cudaError_t r = cudaFuncGetAttributes(&fa, kern);
+            const size_t dyn_max = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+            if (r == cudaSuccess)
+                r = dyn_max < h->stream_smem ? cudaErrorInvalidValue
+                                             : cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                    (int)dyn_max);
+            int occ = 0;
+            if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStreamThreads, h->stream_smem);
+            if (r == cudaSuccess && occ < 1) r = cudaErrorLaunchOutOfResources;
+            if (r != cudaSuccess && e == cudaSuccess) e = r;
+            return occ;
+        };
+        h->stream_occ[0] = setup(stream_kernel<NPc, 0>);
+        h->stream_occ[1] = setup(stream_kernel<NPc, 1>);
+        h->stream_occ[2] = setup(stream_kernel<NPc, 2>);
     });
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -1696,6 +1714,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
         PF.q[j] = QueryDev{qs[fi[j]].slo_startup_us, qs[fi[j]].slo_stall_us, qs[fi[j]].budget_mc};
     uint64_t b, e;
     if ((st = sw_shard_range(begin, end, h->row, h->rank, h->nranks, &b, &e)) < 0) return st;
+    if ((st = ensure_dltc(h, e - b)) < 0) return st;
     trace_mark(h, "start");
     uint64_t host_err = 0;
     CK(h, cudaMemsetAsync(h->d_scand_n, 0, sizeof(uint32_t) * SW_MAX_QUERIES, h->stream));
@@ -1728,13 +1747,13 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
             dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
             CKL(h);
             CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
+            CK(h, cudaMemsetAsync(&h->d_ctl->dlt_n, 0, sizeof(unsigned long long), h->stream));
             StreamArgs sa{};
             sa.dlt = h->d_dlt;
-            sa.front = h->d_front;
             sa.gkey = h->d_skey;
             sa.ctl = h->d_ctl;
-            sa.surv = h->d_surv;
-            sa.surv_cap = h->surv_cap;
+            sa.pts = h->d_dltc;
+            sa.pts_cap = h->dltc_cap;
             sa.cand = h->d_scand;
             sa.cand_n = h->d_scand_n;
             sa.cand_cap = h->scand_cap;
@@ -1745,20 +1764,32 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
             sa.ie = e;
             sa.P = PS;
             const uint64_t warps_per_block = kStreamThreads / 32;
-            const uint32_t grid = (uint32_t)std::min<uint64_t>((ntp + warps_per_block - 1) / warps_per_block,
-                                                               (uint64_t)h->num_sms);
+            const uint32_t grid = (uint32_t)std::min<uint64_t>(
+                (ntp + warps_per_block - 1) / warps_per_block,
+                (uint64_t)h->num_sms * std::max(1, h->stream_occ[eval_mode(h->h.flags)]));
             int pr = 0;
             sw_status ts = begin_timed(h, SW_KERNEL_STREAM, 0, &pr);
             if (ts < 0) return ts;
             launch_np(h, [&](auto npc) {
                 constexpr int NPc = decltype(npc)::value;
-                stream_kernel<NPc><<<grid, kStreamThreads, h->stream_smem, h->stream>>>(
-                    EvalJob{h->d_hdr, h->d_va, h->va_bytes, t0, t1, nullptr}, sa);
+                const EvalJob job{h->d_hdr, h->d_va, h->va_bytes, t0, t1, nullptr};
+                switch (eval_mode(h->h.flags)) {
+                    case 0: stream_kernel<NPc, 0><<<grid, kStreamThreads, h->stream_smem, h->stream>>>(job, sa); break;
+                    case 1: stream_kernel<NPc, 1><<<grid, kStreamThreads, h->stream_smem, h->stream>>>(job, sa); break;
+                    default: stream_kernel<NPc, 2><<<grid, kStreamThreads, h->stream_smem, h->stream>>>(job, sa); break;
+                }
             });
             CKL(h);
             if ((ts = end_timed(h, pr)) < 0) return ts;
             trace_mark(h, "stream");
+            // the pass's DLT survivors: exact test against the running front
+            pareto_exact_kernel<<<h->num_sms, kExactThreads, exact_smem_bytes(), h->stream>>>(
+                h->d_dltc, h->dltc_cap, h->d_front, h->d_ctl, h->d_surv, h->surv_cap);
+            CKL(h);
+            trace_mark(h, "exact");
             CK(h, cudaMemcpyAsync(&h->h_pass_surv[lvl], &h->d_ctl->surv, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                  h->stream));
+            CK(h, cudaMemcpyAsync(&h->h_pass_surv[32 + lvl], &h->d_ctl->dlt_n, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                   h->stream));
             pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                    h->d_ctl);
@@ -1797,7 +1828,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
             for (int round = 0;; round++) {
                 if ((st = run_pass(lvl, ntp)) < 0) return st;
                 SYNC(h);
-                if (h->h_pass_surv[lvl] <= h->surv_cap) break;
+                if (h->h_pass_surv[lvl] <= h->surv_cap && h->h_pass_surv[32 + lvl] <= h->dltc_cap) break;
                 if (round == 8) {
                     host_err = 1;
                     break;

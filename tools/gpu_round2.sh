@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1 || { echo "smoke failed"; tail -20 gpurun_out/${TAG}_smoke.log; }
 if [ "${PYTEST:-1}" = "1" ]; then
-  timeout ${PYT_TIMEOUT:-1800} python -m pytest tests -m gpu -q ${PYTEST_ARGS} > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
+  timeout ${PYT_TIMEOUT:-1800} python -m pytest tests -m gpu -q ${PYTEST_ARGS:---timeout=300 -rf} > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
   tail -15 gpurun_out/${TAG}_pytest.log
 fi
 if [ "${BENCH:-1}" = "1" ]; then
@@ -31,6 +31,7 @@ for t in $NCU; do
         python bench.py --config $c --configs "" --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --stream-steps 0 > gpurun_out/${TAG}_ncu_launch_$c.log 2>&1
         python tools/launch_summary.py gpurun_out/${TAG}_launches_$c.csv > gpurun_out/${TAG}_launch_summary_$c.txt 2>&1 ;;
     debug) SW_DEBUG=1 SW_TRACE=1 timeout 300 python tools/one_step.py $c 2 > gpurun_out/${TAG}_debug_$c.txt 2>&1 ;;
+    sdebug) SW_DEBUG=1 SW_TRACE=1 timeout 300 python tools/shared_one.py $c > gpurun_out/${TAG}_sdebug_$c.txt 2>&1 ;;
   esac
 done
 du -sh gpurun_out; echo done

@@ -1,6 +1,7 @@
 """Summarise an ncu --set full report (one or more kernels) into profiles/.
 
-usage: python tools/ncu_summary.py REPORT.ncu-rep [OUT.txt]
+usage: python tools/ncu_summary.py REPORT.ncu-rep|RAW.csv [OUT.txt]
+(RAW.csv = `ncu -i REPORT --page raw --csv`, as exported on the GPU box)
 Prints per kernel launch: duration, DRAM bytes read/written and throughput, L2 hit
 rate, issue-slot utilisation, IPC, warps active, registers, top warp stall reasons."""
 import csv
@@ -32,8 +33,11 @@ KEYS = [
 
 def main():
     rep = sys.argv[1]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
     lines = []

@@ -413,7 +413,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--configs", default="C2x,C3,C4,C5",
                     help="further configs measured after the headline, reported under 'configs'")
     ap.add_argument("--stream-steps", type=int, default=5,

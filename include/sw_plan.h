@@ -73,7 +73,8 @@ enum {
 #define SW_MAX_DIGITS 16
 #define SW_MAX_CHOICES 64          /* per digit */
 #define SW_MAX_POOLS 4
-#define SW_MAX_GPUS_PER_POOL 8
+#define SW_MAX_GPUS_PER_POOL 32 /* <= 8: lane-per-prefix fast path; 9..32: the warp-per-candidate
+                                   generic path (no fused stream mode, no greedy planner) */
 #define SW_MAX_QUERIES 8           /* per sw_plan_select_batch call */
 
 /* Scene list: the refined DAG of one request, scenes in playback order. */

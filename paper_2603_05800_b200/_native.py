@@ -20,7 +20,7 @@ SW_OK, SW_CLOSEST, SW_TRUNCATED, SW_EMPTY = 0, 1, 2, 3
 SW_EINVAL, SW_ERANGE, SW_ENOMEM, SW_ECUDA, SW_ENCCL, SW_ESTATE = -1, -2, -3, -4, -5, -6
 SW_KERNEL_EVAL, SW_KERNEL_SCAN, SW_KERNEL_STREAM = 0, 1, 2
 SW_MAX_SCENES, SW_MAX_DIGITS, SW_MAX_CHOICES = 64, 16, 64
-SW_MAX_POOLS, SW_MAX_GPUS_PER_POOL, SW_MAX_QUERIES = 4, 8, 8
+SW_MAX_POOLS, SW_MAX_GPUS_PER_POOL, SW_MAX_QUERIES = 4, 32, 8
 UINT64_MAX = (1 << 64) - 1
 
 U64P = C.POINTER(C.c_uint64)

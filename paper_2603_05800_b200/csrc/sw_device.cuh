@@ -10,7 +10,7 @@
 namespace sw {
 
 constexpr uint64_t kInf64 = 0xFFFFFFFFFFFFFFFFull;
-constexpr int kMaxG = SW_MAX_GPUS_PER_POOL;  // register slots per pool (8)
+constexpr int kMaxG = 8;  // register slots per pool on the fast path (pools of <= 8 GPUs; wider: sw_wide.cuh)
 constexpr int kMaxP = SW_MAX_POOLS;
 constexpr int kMaxDigits = SW_MAX_DIGITS + 2;  // + up to 2 virtual radix-1 digits
 constexpr int kMaxChoiceTotal = SW_MAX_DIGITS * SW_MAX_CHOICES;

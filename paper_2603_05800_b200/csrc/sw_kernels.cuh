@@ -755,6 +755,7 @@ struct ParetoCtl {
     uint64_t stamp[6];        // diagnostics: %globaltimer at the merge kernel's phase ends
     unsigned long long dlt_pass;  // diagnostics: records the DLT did not rule out (all passes)
     unsigned long long dlt_n;     // DLT survivors appended by the current scan pass (deferred exact test)
+    unsigned long long dlt_max;   // the largest dlt_n of any pass since the host last looked (buffer growth)
 };
 
 // Per-call status words of a multi-rank call, max-reduced over the ranks BEFORE any rank
@@ -1340,7 +1341,7 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
 // is refolded.  The front (<= kExactFront points) and the lists live in dynamic shared
 // memory as arrays (t, c, idx, q).
 constexpr uint32_t kExactFront = 2048;  // front points staged in smem (larger fronts: from L2)
-constexpr uint32_t kExactList = 128;    // per-warp survivor list
+constexpr uint32_t kExactList = 256;    // per-warp survivor list
 constexpr int kExactThreads = 512;
 constexpr int kExactWarps = kExactThreads / 32;
 constexpr uint32_t kExactNear = 8;      // front points below x.t tested per lane first
@@ -1383,7 +1384,10 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
     const unsigned long long nd = ctl->dlt_n;
     const uint64_t n = nd < cand_cap ? nd : cand_cap;
     const uint32_t m = (uint32_t)ctl->front_n;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && nd > cand_cap) ctl->surv_overflow = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (nd > cand_cap) ctl->surv_overflow = 1;
+        atomicMax(&ctl->dlt_max, nd);
+    }
     const uint64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
     if (r0 >= r1) return;
     const bool f_smem = m <= kExactFront;

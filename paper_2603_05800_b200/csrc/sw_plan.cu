@@ -19,8 +19,11 @@
 #include <vector>
 
 #include "sw_coll.cuh"
+#include <nvtx3/nvToolsExt.h>
+
 #include "sw_kernels.cuh"
 #include "sw_shared.cuh"
+#include "sw_wide.cuh"
 #include "sw_plan.h"
 
 using namespace sw;
@@ -28,6 +31,13 @@ using namespace sw;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX range around every public entry point (visible in nsys / ncu timelines; a no-op
+// when no tool is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct Segment {
     uint64_t gbegin, gend;  // global range of the eval call
@@ -89,6 +99,7 @@ struct sw_plan {
     uint64_t dltc_cap = 0;
     bool fuse_pareto = true;     // fold unfolded segments inside select scans
     bool cxt_front_ok = false;   // COST_X_TTFF: every record has cost > 0 and ttff_eff > 0 (R35)
+    bool wide = false;           // a pool of > 8 GPUs: the warp-per-candidate generic path (sw_wide.cuh)
     uint64_t chunk = 1ull << 25; // records per fold chunk (the front improves per chunk)
     uint64_t fold_passes = 0;    // diagnostics: filter passes run
     uint64_t epoch = 1;          // bumped by every change of records or front
@@ -253,6 +264,7 @@ using u128 = unsigned __int128;
 
 static sw_status fold_pending(sw_plan* h);
 static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_out);
+static sw_status ensure_dltc(sw_plan* h, uint64_t candidates);
 static constexpr uint64_t kMaxSegs = 16;  // segments with tile padding budgeted per handle
 
 // Tiles [t_lo, t_hi) (relative to the segment) of a segment as a scan view.
@@ -278,6 +290,7 @@ static thread_local bool t_tables_only = false;  // sw_shared_create: per-reques
 // ============================================================================ create
 extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_list* sc,
                                     const sw_price_table* pr, const sw_runtime* rt, sw_plan** out) {
+    const NvtxRange nvtx_("sw_plan_create");
     if (!tb || !sc || !pr || !rt || !out) return fail(nullptr, SW_EINVAL, "null argument");
     const uint32_t S = sc->n_scenes;
     if (S < 1 || S > SW_MAX_SCENES) return fail(nullptr, SW_EINVAL, "n_scenes %u not in 1..%d", S, SW_MAX_SCENES);
@@ -425,6 +438,7 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
     h->NP = NP;
     h->S = S;
     h->B_user = B;
+    for (uint32_t p = 0; p < NP; p++) h->wide |= pr->gpus[p] > (uint32_t)kMaxG;
     {  // R35: cost >= fixed cost > 0; ttff_eff >= ttff = R_0 > 0 (a static intro's ready
        // time; else a_0 = overhead + llm_0 + tts_0, plus t >= 1 for a video choice)
         bool t_pos = s0 ? sc->static_ready_us > 0 : sc->overhead_us + sc->llm_us[0] + sc->tts_us[0] > 0;
@@ -649,7 +663,8 @@ extern "C" sw_status sw_plan_create(const sw_profile_tables* tb, const sw_scene_
             };
             const int o[3] = {setup(eval_kernel<NPc, 0>), setup(eval_kernel<NPc, 1>), setup(eval_kernel<NPc, 2>)};
             setup(eval_kernel<NPc, 3>);
-            occ = o[eval_mode(h->h.flags)];
+            const int ow = setup(eval_wide_kernel<NPc>);
+            occ = h->wide ? ow : o[eval_mode(h->h.flags)];
         });
         if (e != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -904,6 +919,7 @@ static void trace_dump(sw_plan* h, const char* what) {
 }
 
 extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
+    const NvtxRange nvtx_("sw_plan_eval");
     if (!h) return fail(nullptr, SW_EINVAL, "null handle");
     if (begin > end || end > h->N)
         return fail(h, SW_EINVAL, "range [%llu, %llu) outside [0, %llu)", (unsigned long long)begin,
@@ -935,7 +951,13 @@ extern "C" sw_status sw_plan_eval(sw_plan* h, uint64_t begin, uint64_t end) {
         int pr = 0;
         sw_status ts = begin_timed(h, SW_KERNEL_EVAL, n * sizeof(Rec4), &pr);
         if (ts < 0) return ts;
-        if (h->shared) {  // shared-pool fleet: one thread per joint candidate (row = 1)
+        if (h->wide) {  // pools of > 8 GPUs: one warp per candidate (sw_wide.cuh)
+            launch_np(h, [&](auto np) {
+                constexpr int NPc = decltype(np)::value;
+                eval_wide_kernel<NPc><<<grid, kEvalThreads, h->eval_smem, h->stream>>>(
+                    EvalJob{h->d_hdr, h->d_va, h->va_bytes, t0, t1, outp});
+            });
+        } else if (h->shared) {  // shared-pool fleet: one thread per joint candidate (row = 1)
             const uint64_t thr = sg.ntiles * kTileRows;
             const uint32_t sgrid = (uint32_t)std::min<uint64_t>((thr + kShThreads - 1) / kShThreads, 8ull * h->num_sms);
             shared_eval_kernel<<<sgrid, kShThreads, 0, h->stream>>>(h->shared->d_dev, t0, t1, h->N, outp);
@@ -991,7 +1013,12 @@ static void detail_to_selection(const sw_plan* h, uint64_t index, const DetailOu
 
 // Full metrics of the winners d_cand[0, nw) into d_detail (one launch).
 static sw_status launch_detail(sw_plan* h, uint32_t nw) {
-    if (h->shared) {
+    if (h->wide) {
+        launch_np(h, [&](auto npc) {
+            constexpr int NPc = decltype(npc)::value;
+            wide_detail_kernel<NPc><<<nw, 32, 0, h->stream>>>(h->d_hdr, h->d_va, h->d_cand, nw, h->d_detail);
+        });
+    } else if (h->shared) {
         shared_detail_kernel<<<1, 32, 0, h->stream>>>(h->shared->d_dev, h->d_cand, nw, h->d_detail, h->shared->d_full);
     } else {
         launch_np(h, [&](auto npc) {
@@ -1004,7 +1031,7 @@ static sw_status launch_detail(sw_plan* h, uint32_t nw) {
 }
 
 static sw_status fill_detail(sw_plan* h, uint64_t index, sw_selection* out, uint64_t* ready) {
-    if (h->shared) {
+    if (h->shared || h->wide) {
         Cand c{};
         c.idx = index;
         CK(h, cudaMemcpyAsync(h->d_cand, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
@@ -1155,7 +1182,9 @@ static sw_status reduce_async(sw_plan* h, PPoint* out) {
 static sw_status seed_async(sw_plan* h, const Segment& g) {
     const uint64_t n = g.end - g.begin;
     // a strided sample seeds the running front (its exact front is cheap to reduce)
-    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, 16384);
+    // (a larger sample for large segments: a better first front cuts the first pass's
+    // survivors and its merge)
+    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, n >= (1ull << 26) ? 65536 : 16384);
     CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
     pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), ns, h->d_work, h->d_ctl);
     CKL(h);
@@ -1284,6 +1313,11 @@ static sw_status sync_ctl(sw_plan* h, bool* overflow) {
     h->front_n = c.front_n;
     *overflow = c.surv_overflow != 0;
     if (c.surv_overflow) CK(h, cudaMemsetAsync(&h->d_ctl->surv_overflow, 0, sizeof(uint32_t), h->stream));
+    if (c.dlt_max > h->dltc_cap) {  // a loose DLT (e.g. discrete qualities): grow the buffer so
+                                    // the refold does not drop survivors again
+        sw_status st = ensure_dltc(h, c.dlt_max * 10);
+        if (st < 0) return st;
+    }
     return SW_OK;
 }
 
@@ -1553,6 +1587,7 @@ static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_sel
 }
 
 extern "C" sw_status sw_plan_select_batch(sw_plan* h, uint32_t nq, const sw_query* qs, sw_selection* out) {
+    const NvtxRange nvtx_("sw_plan_select_batch");
     if (!h || !qs || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (nq < 1 || nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u not in 1..%d", nq, SW_MAX_QUERIES);
     CK(h, cudaSetDevice(h->device));
@@ -1566,6 +1601,7 @@ extern "C" sw_status sw_plan_select(sw_plan* h, uint64_t slo_startup_us, uint64_
 }
 
 extern "C" sw_status sw_plan_detail(sw_plan* h, uint64_t index, sw_selection* out, uint64_t* ready_us) {
+    const NvtxRange nvtx_("sw_plan_detail");
     if (!h || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (index >= h->N) return fail(h, SW_EINVAL, "index out of range");
     CK(h, cudaSetDevice(h->device));
@@ -1579,6 +1615,7 @@ extern "C" sw_status sw_plan_detail(sw_plan* h, uint64_t index, sw_selection* ou
 // ============================================================================ chunked sweep
 extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uint64_t chunk, uint32_t nq,
                                    const sw_query* qs, sw_selection* out, uint64_t* digest) {
+    const NvtxRange nvtx_("sw_plan_sweep");
     if (!h || (nq && (!qs || !out))) return fail(nullptr, SW_EINVAL, "null argument");
     if (nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u > %d", nq, SW_MAX_QUERIES);
     if (begin > end || end > h->N) return fail(h, SW_EINVAL, "range outside [0, N)");
@@ -1688,11 +1725,13 @@ static sw_status stream_setup(sw_plan* h) {
 
 extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, uint32_t nq, const sw_query* qs,
                                     sw_selection* out) {
+    const NvtxRange nvtx_("sw_plan_stream");
     if (!h || (nq && (!qs || !out))) return fail(nullptr, SW_EINVAL, "null argument");
     if (nq > SW_MAX_QUERIES) return fail(h, SW_EINVAL, "n_queries %u > %d", nq, SW_MAX_QUERIES);
     if (begin > end || end > h->N) return fail(h, SW_EINVAL, "range outside [0, N)");
     if (!h->segs.empty()) return fail(h, SW_ESTATE, "stream needs a handle without records (reset/release)");
     if (h->shared) return fail(h, SW_EINVAL, "the fused stream mode is not available for shared-pool fleets");
+    if (h->wide) return fail(h, SW_EINVAL, "the fused stream mode needs pools of <= 8 GPUs (use sw_plan_sweep)");
     CK(h, cudaSetDevice(h->device));
     h->gepoch++;  // the stream folds new candidates into the front (every rank makes this call)
     sw_status st = stream_setup(h);
@@ -1829,6 +1868,8 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
                 if ((st = run_pass(lvl, ntp)) < 0) return st;
                 SYNC(h);
                 if (h->h_pass_surv[lvl] <= h->surv_cap && h->h_pass_surv[32 + lvl] <= h->dltc_cap) break;
+                if (h->h_pass_surv[32 + lvl] > h->dltc_cap && (st = ensure_dltc(h, h->h_pass_surv[32 + lvl] * 10)) < 0)
+                    return st;
                 if (round == 8) {
                     host_err = 1;
                     break;
@@ -1928,6 +1969,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
 
 // ============================================================================ digest
 extern "C" sw_status sw_plan_digest(sw_plan* h, uint64_t* digest) {
+    const NvtxRange nvtx_("sw_plan_digest");
     if (!h || !digest) return fail(nullptr, SW_EINVAL, "null argument");
     CK(h, cudaSetDevice(h->device));
     CK(h, cudaMemsetAsync(h->d_digest, 0, sizeof(unsigned long long), h->stream));
@@ -2036,6 +2078,7 @@ static sw_status global_front(sw_plan* h, const PPoint** res_out, uint64_t* n_ou
 }
 
 extern "C" sw_status sw_pareto_get(sw_plan* h, sw_pareto_point* out, uint64_t cap, uint64_t* n_out) {
+    const NvtxRange nvtx_("sw_pareto_get");
     if (!h || !n_out || (cap && !out)) return fail(nullptr, SW_EINVAL, "null argument");
     const PPoint* res = nullptr;
     uint64_t n = 0;
@@ -2097,9 +2140,11 @@ extern "C" sw_status sw_plan_copy_records(sw_plan* h, uint64_t index, uint64_t n
 extern "C" sw_status sw_plan_greedy(sw_plan* h, uint64_t slo_startup_us, uint64_t slo_stall_us, uint64_t budget_mc,
                                     uint64_t start_index, sw_selection* out, uint32_t* iterations,
                                     uint64_t* evaluations) {
+    const NvtxRange nvtx_("sw_plan_greedy");
     if (!h || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (start_index != UINT64_MAX && start_index >= h->N) return fail(h, SW_EINVAL, "start index out of range");
     if (h->shared) return fail(h, SW_EINVAL, "the greedy planner is not available for shared-pool fleets");
+    if (h->wide) return fail(h, SW_EINVAL, "the greedy planner needs pools of <= 8 GPUs");
     if (h->level_score.size() > (size_t)kMaxLevels) return fail(h, SW_EINVAL, "greedy supports <= %d levels", kMaxLevels);
     CK(h, cudaSetDevice(h->device));
     GreedyArgs A{};
@@ -2200,10 +2245,13 @@ extern "C" sw_status sw_selection_merge(uint32_t objective, const sw_query* q, c
 extern "C" sw_status sw_shared_create(uint32_t n, const sw_profile_tables* tables, const sw_scene_list* scenes,
                                       const uint64_t* fixed_cost_mc, const sw_shared_request* reqs,
                                       const sw_price_table* pools, const sw_runtime* rt, sw_plan** out) {
+    const NvtxRange nvtx_("sw_shared_create");
     if (!tables || !scenes || !reqs || !pools || !rt || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (n < 1 || n > (uint32_t)kShMaxReq) return fail(nullptr, SW_EINVAL, "shared fleet of %u requests (1..%d)", n, kShMaxReq);
     if (pools->evict_risk_permille) return fail(nullptr, SW_EINVAL, "shared pools take no eviction risk");
     if (pools->metric) return fail(nullptr, SW_EINVAL, "shared-pool fleets use the money metric");
+    for (uint32_t p = 0; p < pools->n_pools; p++)
+        if (pools->gpus[p] > (uint32_t)kMaxG) return fail(nullptr, SW_EINVAL, "shared pools of <= %d GPUs", kMaxG);
     for (uint32_t r = 0; r < n; r++)
         if (tables[r].vae_us) return fail(nullptr, SW_EINVAL, "request %u: DiT/VAE stages are not supported in shared-pool fleets", r);
     if (rt->nranks < 1 || rt->rank < 0 || rt->rank >= rt->nranks)
@@ -2468,6 +2516,7 @@ extern "C" sw_status sw_fleet_destroy(sw_fleet* f) {
 
 extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables, const sw_scene_list* scenes,
                                      const sw_price_table* prices, const sw_runtime* rt, sw_fleet** out) {
+    const NvtxRange nvtx_("sw_fleet_create");
     if (!tables || !scenes || !prices || !rt || !out) return fail(nullptr, SW_EINVAL, "null argument");
     if (n < 1 || n > SW_MAX_FLEET) return fail(nullptr, SW_EINVAL, "fleet size %u not in 1..%d", n, SW_MAX_FLEET);
     sw_fleet* f = new sw_fleet();
@@ -2502,6 +2551,10 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
             return fail(nullptr, st, "%s", msg.c_str());
         }
         f->plans.push_back(p);
+        if (p->wide) {
+            bail(SW_EINVAL);
+            return fail(nullptr, SW_EINVAL, "request %u: fleets need pools of <= %d GPUs", i, kMaxG);
+        }
         f->np_max = std::max(f->np_max, p->NP);
         const int bm = eval_mode(p->h.flags);
         f->bmode = f->bmode < 0 ? bm : (f->bmode == bm ? bm : 3);
@@ -2592,6 +2645,7 @@ static sw_status fleet_harvest(sw_fleet* f, int kind, uint64_t bytes) {
 }
 
 extern "C" sw_status sw_fleet_eval(sw_fleet* f) {
+    const NvtxRange nvtx_("sw_fleet_eval");
     if (!f) return fail(nullptr, SW_EINVAL, "null fleet");
     sw_plan* h = f->plans[0];
     const uint32_t n = (uint32_t)f->plans.size();
@@ -2648,6 +2702,7 @@ extern "C" sw_status sw_fleet_eval(sw_fleet* f) {
 }
 
 extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_selection* out) {
+    const NvtxRange nvtx_("sw_fleet_select");
     if (!f || !queries || !out) return fail(nullptr, SW_EINVAL, "null argument");
     sw_plan* h = f->plans[0];
     if (!f->evaluated) return fail(h, SW_ESTATE, "sw_fleet_eval first");

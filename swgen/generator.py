@@ -354,6 +354,13 @@ def make_config(name: str) -> Problem:
         MJ = 10 ** 12  # microjoules per megajoule
         pb.queries = [Query(999_999, 0, 4 * MJ), Query(2_999_999, 0, 2 * MJ), Query(INF, INF, INF)]
         return pb
+    if name == "C2w":
+        # C2 on one 16 x A100 pool ("16xA100"): G_p = 16 > 8 takes the library's
+        # generic warp-per-candidate path (SURVEY §8(a) layout note, §8(b) "<= 32 generic").
+        return _build("C2w", 1002, 600, 20,
+                      [(0, 0), (1, 1), (2, 2), (3, 3), (4, 8), (9, 13), (14, 18), (19, 19)],
+                      [0, 1, 3], [1, 2, 4, 8], [("A100", 16)], True, False,
+                      lambda p: [Query(INF, INF, 25 * DOLLAR), Query(120 * D, 0, INF), Query(INF, INF, INF)])
     if name == "C3w":
         # C3 with a cold H100 pool: its GPUs are free only after the model load + first
         # warm-up request, 30 s + 80 s (reading R31).

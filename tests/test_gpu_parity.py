@@ -409,3 +409,20 @@ def test_disagg_energy_random(sw, oracle_mod, seed):
     with sw.Plan(pb, record_capacity=1024) as plan:
         _check_winners(plan.stream(0, n, qs), exp)
         assert plan.pareto() == f
+
+
+def test_c5_full_space(sw):
+    """C5 (48^6 = 1.2e10 plans, 391 GB of records) over the WHOLE space through the chunked
+    sweep at the bench's launch configuration (records capacity 75% of free HBM): winners,
+    exact front and digest vs the oracle's full-space result (computed once in pieces and
+    cached by input SHA-256, tools/gen_golden_full.py)."""
+    g = _golden("C5")
+    import torch
+    pb = make_config("C5")
+    free_b, _ = torch.cuda.mem_get_info(0)
+    cap = int(0.75 * free_b) // 32
+    with sw.Plan(pb, record_capacity=cap) as plan:
+        sels, dg = plan.sweep(0, plan.n, pb.queries, digest=True)
+        _check_winners(sels, g["winners"])
+        assert dg == int(g["digest"])
+        assert plan.pareto() == [tuple(p) for p in g["front"]]

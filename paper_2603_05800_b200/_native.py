@@ -15,6 +15,10 @@ from typing import List, Optional, Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libsw_plan.so")
+# experiment variants (tools/build_variant.py): a differently compiled library, same ABI
+_VARIANT = os.environ.get("SW_LIB_VARIANT")
+if _VARIANT:
+    LIB_PATH = os.path.join(_PKG, "variants", "libsw_plan_%s.so" % _VARIANT)
 
 SW_OK, SW_CLOSEST, SW_TRUNCATED, SW_EMPTY = 0, 1, 2, 3
 SW_EINVAL, SW_ERANGE, SW_ENOMEM, SW_ECUDA, SW_ENCCL, SW_ESTATE = -1, -2, -3, -4, -5, -6
@@ -167,7 +171,7 @@ def lib():
             raise ImportError("libsw_plan.so not built: run `python -c 'import __graft_entry__ as g; "
                               "g.build()'` (nvcc, sm_100a)")
         from . import build as _build
-        if _build.needs_build():
+        if not _VARIANT and _build.needs_build():
             raise ImportError("libsw_plan.so is stale (built from other sources than csrc/ + include/): "
                               "rebuild with `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(LIB_PATH)

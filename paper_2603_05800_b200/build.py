@@ -53,8 +53,9 @@ def needs_build() -> bool:
         return f.read().strip() != source_hash()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libsw_plan.so (out/defines: experiment variants, tools/build_variant.py)."""
+    if out is None and not force and not needs_build():
         return LIB
     inc, lib = nccl_paths()
     src_hash = source_hash()  # of the sources as they are when the compile starts
@@ -63,10 +64,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-Xcompiler", "-fPIC", "-shared",
         "-Xptxas", "-v" if verbose else "-O3",
         "-I", INCLUDE, "-I", inc, "-cudart", "static",
-        "-DSW_BUILD_SHARED",
+        "-DSW_BUILD_SHARED", *["-D" + d for d in defines],
         os.path.join(CSRC, "sw_plan.cu"),
         "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib,
-        "-o", LIB,
+        "-o", out or LIB,
     ]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -74,6 +75,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed")
     if verbose:
         sys.stderr.write(r.stderr)
+    if out:
+        return out
     with open(STAMP, "w") as f:
         f.write(src_hash + "\n")
     return LIB

@@ -127,6 +127,10 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
     }
 }
 
+#ifndef SW_LSD_UNROLL
+#define SW_LSD_UNROLL 1  // (experiments: tools/build_variant.py)
+#endif
+constexpr int kLsdUnroll = SW_LSD_UNROLL;
 // ============================================================================ LSD fast path
 // The last digit's block is a single scene: only pool p of the chosen (p, k) changes,
 // so per candidate  e = max(a_s, F_p[k-1]) + t,  end_p' = max(end_p, e),
@@ -253,7 +257,7 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& st
             put(E.dl, E.dl * (kTileRows * (uint32_t)sizeof(Rec4)), r);  // a7 store, or the stream filter
         };
         if (mode == 0) {
-#pragma unroll 1
+#pragma unroll kLsdUnroll
             for (uint32_t j = j0; j < j1; j++) {
                 const LsdEntry E = h.lsd[j];
                 const uint64_t cnew = U1 + E.x1 + ((uint32_t)E.x2 >= Dm ? 1u : 0u);
@@ -461,8 +465,11 @@ struct StoreEmit {
 // grows with the pools (NP + 1 pools of 8 free times live in the MID/LSD loops), and
 // these are the largest occupancies whose hot loops do not spill (ptxas -v).
 // fast path (BM 0/1) vs generic path (BM 2/3, full-state copies)
+#ifndef SW_EVAL_MINB1
+#define SW_EVAL_MINB1 4  // (experiments: tools/build_variant.py)
+#endif
 __host__ __device__ constexpr int eval_min_blocks(int np, int bm) {
-    return bm <= 1 ? (np <= 2 ? 4 : np == 3 ? 3 : 2) : (np <= 1 ? 4 : np == 2 ? 3 : 2);
+    return bm <= 1 ? (np == 1 ? SW_EVAL_MINB1 : np == 2 ? 4 : np == 3 ? 3 : 2) : (np <= 1 ? 4 : np == 2 ? 3 : 2);
 }
 
 // jobs == nullptr: one request (job); else request blockIdx.y of a fleet (jobs[y]), each

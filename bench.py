@@ -401,6 +401,44 @@ def emit(line):
 _REAL_STDOUT = sys.stdout
 
 
+def measure_stream(ctx, pb, g, steps):
+    """SURVEY §8(f) row 1, reported beside (not instead of) a config's step: the fused
+    stream mode evaluates the same space with NO record store (a7 skipped by design),
+    select + Pareto filter in-kernel.  CUDA events on the handle's stream around whole
+    calls, max over ranks; parity vs the oracle golden (winners + front) when there is one."""
+    sw, dev, stream, comm = ctx["sw"], ctx["dev"], ctx["stream"], ctx["comm"]
+    rank, world = ctx["rank"], ctx["world"]
+    N = sw.space_shape(pb)[0]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world,
+                 record_capacity=1024) as p3:
+        for _ in range(2 if N < 2e9 else 1):
+            p3.reset()
+            ss = p3.stream(0, N, pb.queries)
+        ctx["barrier"]()
+        s0 = p3.kernel_time(sw.SW_KERNEL_STREAM)
+        ev0.record(stream)
+        for _ in range(steps):
+            p3.reset()
+            ss = p3.stream(0, N, pb.queries)
+        ev1.record(stream)
+        ev1.synchronize()
+        s1 = p3.kernel_time(sw.SW_KERNEL_STREAM)
+        sms = ctx["max_over_ranks"](ev0.elapsed_time(ev1) / steps)
+        sparity = None
+        if g is not None:
+            sparity = (all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
+                           for s, w in zip(ss, g["winners"])) and
+                       p3.pareto() == [tuple(p) for p in g["front"]])
+    return {"value": N / (sms / 1e3), "unit": UNIT, "ms_per_call": sms,
+            "stream_kernel_ms_per_call": (s1[1] - s0[1]) / steps,
+            "launches_per_call": (s1[0] - s0[0]) / steps,
+            "calls": steps, "parity": sparity,
+            "note": "sw_plan_stream: no records stored (a7 skipped by design; "
+                    "SURVEY 8(f) row 1), not the headline step"}
+
+
 def main():
     global _REAL_STDOUT
     _REAL_STDOUT = os.fdopen(os.dup(1), "w")
@@ -465,39 +503,7 @@ def main():
     gpath = os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % args.config)
     g = json.load(open(gpath)) if os.path.exists(gpath) else None
 
-    # §8(f) row 1, reported beside (not instead of) the headline: the fused stream mode
-    # evaluates the same space with NO record store (a7 skipped by design), select + Pareto
-    # filter in-kernel; CUDA events on the stream around whole calls, max over ranks
-    stream_line = None
-    if args.stream_steps > 0:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        with sw.Plan(pb, device=dev, stream=stream.cuda_stream, comm=comm, rank=rank, nranks=world,
-                     record_capacity=1024) as p3:
-            for _ in range(2):
-                p3.reset()
-                ss = p3.stream(0, N, pb.queries)
-            barrier()
-            s0 = p3.kernel_time(sw.SW_KERNEL_STREAM)
-            ev0.record(stream)
-            for _ in range(args.stream_steps):
-                p3.reset()
-                ss = p3.stream(0, N, pb.queries)
-            ev1.record(stream)
-            ev1.synchronize()
-            s1 = p3.kernel_time(sw.SW_KERNEL_STREAM)
-            sms = max_over_ranks(ev0.elapsed_time(ev1) / args.stream_steps)
-            sparity = None
-            if g is not None:
-                sparity = (all(s.index == w["index"] and tuple(s.rec) == tuple(w["rec"])
-                               for s, w in zip(ss, g["winners"])) and
-                           p3.pareto() == [tuple(p) for p in g["front"]])
-            stream_line = {"value": N / (sms / 1e3), "unit": UNIT, "ms_per_call": sms,
-                           "stream_kernel_ms_per_call": (s1[1] - s0[1]) / args.stream_steps,
-                           "launches_per_call": (s1[0] - s0[0]) / args.stream_steps,
-                           "calls": args.stream_steps, "parity": sparity,
-                           "note": "sw_plan_stream: no records stored (a7 skipped by design; "
-                                   "SURVEY 8(f) row 1), not the headline step"}
+    stream_line = measure_stream(ctx, pb, g, args.stream_steps) if args.stream_steps > 0 else None
 
     # the other configs of BASELINE.json / SURVEY 8(d), each a full step of its own
     # workload with per-kernel roofline, parity vs the oracle golden and e2e
@@ -513,6 +519,10 @@ def main():
                 r = measure_plan(ctx, pbx, cfg, st, 3 if nx > 2e9 else args.warmup, 1 if nx > 2e9 else args.e2e_steps)
                 for k in ("cap", "front", "e2e_s", "d2h", "clocks"):
                     r.pop(k, None)
+                if args.stream_steps > 0:
+                    gx = os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % cfg)
+                    r["stream_mode"] = measure_stream(ctx, pbx, json.load(open(gx)) if os.path.exists(gx) else None,
+                                                      2 if nx > 2e9 else args.stream_steps)
                 extra[cfg] = r
         except Exception as ex:  # noqa: BLE001 -- reported in the line, never hides the headline
             extra[cfg] = {"error": "%s: %s" % (type(ex).__name__, ex)}

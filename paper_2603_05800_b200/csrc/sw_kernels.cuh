@@ -42,8 +42,9 @@ struct SegView {
 };
 constexpr int kScanThreads = 256;
 constexpr int kDltT = 255;  // dominance lookup table: ttff_eff bins (front quantiles; <= 255: u8 map)
-constexpr int kDltQ = 128;  //                         quality bins (linear, 2^k wide)
+constexpr int kDltQ = 128;  //                         quality bins (tops at front quality values)
 constexpr int kDltCols = kDltQ + 1;  // + the "above every front q" column
+constexpr int kDltQMap = 1024;  // q map: linear cells over the quality tops' range
 constexpr int kDltMap = 2048;  // t direct map: 128 cells per octave over 16 octaves
 constexpr int kDltTShift = 16; // t cell key = float bits >> 16 (7 mantissa bits)
 
@@ -860,7 +861,7 @@ __global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint*
 
 // Dominance lookup table (DLT) from the current front (sorted by ttff_eff).
 // t-bins: quantile edges of the front's t (tedge ascending, bin b holds t >= tedge[b]);
-// q-bins: linear, 2^qshift wide from qmin (bin j = [qmin + j 2^qshift, qmin + (j+1) 2^qshift)).
+// q-bins: (qtop[j-1], qtop[j]] with tops at front quality values (dlt_qtop_kernel).
 // cell[b][j] = min cost over front points f with f.t <= tedge[b] and f.q >= the largest
 // q of bin j, as u32 (0xffffffff = none / too big).  A record (t, c, q) in cell (b, j)
 // with cell < c is strictly dominated by a real candidate (f.t <= t, f.q >= q, f.c < c),
@@ -869,7 +870,9 @@ __global__ void __launch_bounds__(kScanThreads) pareto_rank_kernel(const PPoint*
 // lower end), the q bin is a shift.
 struct Dlt {
     int32_t kbase;         // t key of tmap[0]
-    uint32_t qmin, qmax, qshift;
+    uint32_t qbase;        // q of qmap[0]'s lower end (= qtop[0])
+    uint32_t qmshift;      // q map cell width 2^qmshift
+    uint32_t ntop;         // quality bin tops in use (<= kDltQ)
     uint32_t cshift, pad_[3];
     uint64_t tedge[kDltT + 1];
     // t map cell k: lo = #edges <= the cell's lower end, hi = #edges <= its upper end
@@ -883,6 +886,17 @@ struct Dlt {
     // record with cost c is strictly dominated when min(c >> cshift, 0xffff) > cell, i.e.
     // c >= (cell + 1) << cshift > the true minimum.
     uint16_t cell[(kDltT + 1) * kDltCols];
+    // quality bins (round 2): bin j = (qtop[j-1], qtop[j]], the tops are front quality
+    // values (all distinct ones, or quantiles of them), so a column needs f.q >= qtop[j]
+    // and a front point of the record's OWN quality still counts (linear bins of width 2^k
+    // needed f.q >= the bin's top and missed same-quality dominators -- the common case
+    // with discrete quality levels).  q map: kDltQMap linear cells of 2^qmshift from qbase
+    // over the tops' range; cell k: lo = #tops < its lower end, hi = #tops <= its upper
+    // end; a record's column is lo when q <= qtop[lo], else hi (exact when the cell holds
+    // <= 1 top, else conservative: column hi needs f.q >= qtop[hi] >= q).  Packed per cell
+    // as {qtop[lo] (~0 when lo = ntop), lo | hi << 8}: one 8 B shared load per lookup.
+    uint32_t qtop[kDltQ];
+    uint2 qmap[kDltQMap];
 };
 static_assert(sizeof(Dlt) % 16 == 0, "Dlt is staged in 16 B vectors");
 
@@ -893,7 +907,7 @@ __device__ __forceinline__ int32_t dlt_tkey(uint64_t t) {
 // The DLT's scalar fields, held in registers by the scan consumers.
 struct DltHot {
     int32_t kbase;
-    uint32_t qmin, qmax, qshift, cshift;
+    uint32_t qbase, qmshift, cshift;
 };
 
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
@@ -901,7 +915,9 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     // clamped t below it gets row 0), column kDltQ catches q above the front's
     const int32_t k = dlt_tkey(t) - hs.kbase;
     const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
-    const uint32_t j = min((max(q, hs.qmin) - hs.qmin) >> hs.qshift, (uint32_t)kDltQ);
+    const uint2 qm = d.qmap[min((max(q, hs.qbase) - hs.qbase) >> hs.qmshift, (uint32_t)kDltQMap - 1)];
+    const uint32_t loq = qm.y & 0xffu, hiq = qm.y >> 8;
+    const uint32_t j = q > qm.x ? hiq : loq;  // #tops < q (column; kDltQ = none)
     const uint32_t lh = d.tmap[kc];
     const uint32_t lo = lh & 0xffu, hi = lh >> 8;
     const uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;  // t bin + 1
@@ -910,49 +926,155 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;
 }
 
-// One launch builds the whole DLT: block b (kDltQ threads) computes the t edges it
-// needs, q range and shift, cell row b and a 1/kDltT share of the t map; block 0 writes
-// the header.  The front is sorted by t, so a cell scan stops at the first f.t > edge.
+// Quality bin tops and the q map of the DLT (one block, before dlt_build_kernel): the
+// front's quality values sorted (bitonic, in shared memory), the distinct ones -- all, or
+// kDltQ quantiles of them -- as tops.  Fronts above kDltSortMax points take kDltQ linear
+// tops over [qmin, qmax] instead (still exact: a column only ever counts f.q >= its top).
+constexpr uint32_t kDltSortMax = 16384;
+constexpr int kDltQThreads = 1024;
+__global__ void __launch_bounds__(kDltQThreads) dlt_qtop_kernel(const PPoint* __restrict__ front,
+                                                                const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
+    extern __shared__ uint32_t qs[];  // kDltSortMax
+    __shared__ uint32_t s_nd, s_qmin, s_qmax;
+    __shared__ uint32_t s_wsum[32];
+    __shared__ uint32_t s_top[kDltQ];
+    const uint32_t m = (uint32_t)ctl->front_n, tid = threadIdx.x;
+    uint32_t ntop = 0;
+    if (m > 0 && m <= kDltSortMax) {
+        uint32_t n2 = 1;
+        while (n2 < m) n2 <<= 1;
+        for (uint32_t i = tid; i < n2; i += blockDim.x) qs[i] = i < m ? front[i].q : 0xffffffffu;
+        __syncthreads();
+        for (uint32_t k = 2; k <= n2; k <<= 1)  // bitonic sort, ascending
+            for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+                for (uint32_t i = tid; i < n2; i += blockDim.x) {
+                    const uint32_t l = i ^ jj;
+                    if (l > i) {
+                        const uint32_t a = qs[i], b = qs[l];
+                        if (((i & k) == 0) ? (a > b) : (a < b)) {
+                            qs[i] = b;
+                            qs[l] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        // distinct values, compacted in place: thread tid owns kDltPer consecutive slots
+        // (held in registers across the barrier), a block scan gives its output offset
+        constexpr uint32_t kDltPer = kDltSortMax / kDltQThreads;
+        uint32_t v[kDltPer], fresh = 0, cnt = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < kDltPer; r++) {
+            const uint32_t i = tid * kDltPer + r;
+            v[r] = i < m ? qs[i] : 0;
+            if (i < m && (i == 0 || qs[i] != qs[i - 1])) {
+                fresh |= 1u << r;
+                cnt++;
+            }
+        }
+        const uint32_t lane = tid & 31, wid = tid >> 5;
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        if (lane == 31) s_wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = s_wsum[lane], wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= (uint32_t)o) wi += y;
+            }
+            s_wsum[lane] = wi - w;  // exclusive
+            if (lane == 31) s_nd = wi;
+        }
+        __syncthreads();
+        uint32_t off = s_wsum[wid] + inc - cnt;
+#pragma unroll
+        for (uint32_t r = 0; r < kDltPer; r++)
+            if (fresh & (1u << r)) qs[off++] = v[r];
+        __syncthreads();
+        const uint32_t nd = s_nd;
+        ntop = min(nd, (uint32_t)kDltQ);
+        for (uint32_t jj = tid; jj < ntop; jj += blockDim.x)
+            s_top[jj] = nd <= (uint32_t)kDltQ ? qs[jj] : qs[((uint64_t)(jj + 1) * nd) / kDltQ - 1];
+    } else if (m > 0) {
+        if (tid == 0) {
+            s_qmin = 0xffffffffu;
+            s_qmax = 0;
+        }
+        __syncthreads();
+        uint32_t lo = 0xffffffffu, hi = 0;
+        for (uint32_t i = tid; i < m; i += blockDim.x) {
+            lo = min(lo, front[i].q);
+            hi = max(hi, front[i].q);
+        }
+        atomicMin(&s_qmin, lo);
+        atomicMax(&s_qmax, hi);
+        __syncthreads();
+        const uint64_t qmin = s_qmin, span = (uint64_t)s_qmax - s_qmin + 1;
+        ntop = kDltQ;
+        for (uint32_t jj = tid; jj < (uint32_t)kDltQ; jj += blockDim.x)
+            s_top[jj] = (uint32_t)(qmin + ((uint64_t)(jj + 1) * span - 1) / kDltQ);
+    }
+    __syncthreads();
+    for (uint32_t jj = tid; jj < (uint32_t)kDltQ; jj += blockDim.x) d->qtop[jj] = jj < ntop ? s_top[jj] : 0xffffffffu;
+    const uint32_t qbase = ntop ? s_top[0] : 0;
+    uint32_t qsh = 0;
+    if (ntop)
+        while (((uint64_t)(s_top[ntop - 1] - qbase) >> qsh) >= (uint64_t)kDltQMap) qsh++;
+    if (tid == 0) {
+        d->qbase = qbase;
+        d->qmshift = qsh;
+        d->ntop = ntop;
+    }
+    auto count_lt = [&](uint64_t L) -> uint32_t {  // #tops < L
+        uint32_t a = 0, e = ntop;
+        while (a < e) {
+            const uint32_t mid = (a + e) >> 1;
+            if ((uint64_t)s_top[mid] < L) a = mid + 1;
+            else e = mid;
+        }
+        return a;
+    };
+    // the q map (cell 0 also takes q below qbase, the last cell everything above)
+    for (uint32_t k = tid; k < (uint32_t)kDltQMap; k += blockDim.x) {
+        const uint64_t L = k ? (uint64_t)qbase + ((uint64_t)k << qsh) : 0;
+        const bool last = k == (uint32_t)kDltQMap - 1;
+        const uint32_t lo = count_lt(L);
+        const uint32_t hi = last ? ntop : count_lt((uint64_t)qbase + ((uint64_t)(k + 1) << qsh));
+        d->qmap[k] = make_uint2(lo < ntop ? s_top[lo] : 0xffffffffu, lo | (hi << 8));
+    }
+}
+
+// One launch builds the rest of the DLT: block b (kDltQ threads) computes the t edges it
+// needs, the cost shift, cell row b and a 1/kDltT share of the t map; block 0 writes the
+// header.  The front is sorted by t, so a cell scan stops at the first f.t > edge.  The
+// quality tops come from dlt_qtop_kernel (launched before, same stream).
 __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restrict__ front,
                                                           const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
     __shared__ PPoint tile[kDltQ];
     __shared__ uint64_t te[kDltT];
-    __shared__ uint32_t s_qmin, s_qmax;
     __shared__ unsigned long long s_cmax;
     const uint32_t m = (uint32_t)ctl->front_n;
     const uint32_t b = blockIdx.x, j = threadIdx.x;
-    if (j == 0) {
-        s_qmin = 0xffffffffu;
-        s_qmax = 0;
-        s_cmax = 0;
-    }
+    if (j == 0) s_cmax = 0;
     for (uint32_t i = j; i < kDltT; i += blockDim.x) te[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
     __syncthreads();
-    uint32_t lo = 0xffffffffu, hi = 0;
     uint64_t cmx = 0;
-    for (uint32_t i = j; i < m; i += blockDim.x) {
-        const PPoint f = front[i];
-        lo = min(lo, f.q);
-        hi = max(hi, f.q);
-        cmx = umax64(cmx, f.c);
-    }
-    atomicMin(&s_qmin, lo);
-    atomicMax(&s_qmax, hi);
+    for (uint32_t i = j; i < m; i += blockDim.x) cmx = umax64(cmx, front[i].c);
     atomicMax(&s_cmax, (unsigned long long)cmx);
     __syncthreads();
-    const uint32_t qmin = s_qmin, qmax = s_qmax;
-    uint32_t qsh = 0, csh = 0;
-    if (m)
-        while ((((uint64_t)qmax - qmin) >> qsh) >= (uint64_t)kDltQ) qsh++;
+    uint32_t csh = 0;
     while ((s_cmax >> csh) >= 0xffffull) csh++;  // every front cost fits below the 0xffff "none"
     // map cell 0 sits just below the front's smallest t: it holds no edge
     const int32_t kbase = m ? dlt_tkey(front[0].t) - 1 : 0x7fffffff;
     if (b == 0) {
         if (j == 0) {
             d->kbase = kbase;
-            d->qmin = m ? qmin : 0xffffffffu;
-            d->qmax = m ? qmax : 0;
-            d->qshift = qsh;
             d->cshift = csh;
         }
         for (uint32_t i = j; i < kDltT; i += blockDim.x) d->tedge[i] = te[i];
@@ -978,9 +1100,10 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
         const uint32_t lo = m ? count_le(L) : 0, hi = m ? count_le(U) : 0;
         d->tmap[k] = (uint16_t)(lo | (hi << 8));
     }
-    // cell row b, thread j = q bin: needs f.q >= the largest q of bin j
+    // cell row b, thread j = quality column: needs f.q >= qtop[j] (columns >= ntop: none)
     const uint64_t Eb = te[b];
-    const uint64_t qhi = (uint64_t)qmin + (((uint64_t)j + 1) << qsh) - 1;
+    const uint32_t ntop = d->ntop;
+    const uint64_t qthr = j < ntop ? (uint64_t)d->qtop[j] : (1ull << 33);
     uint64_t best = kInf64;
     bool more = true;
     for (uint32_t base = 0; base < m && more; base += kDltQ) {
@@ -994,7 +1117,7 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
                 more = false;  // front sorted by t: no later point qualifies
                 break;
             }
-            if ((uint64_t)f.q >= qhi) best = umin64(best, f.c);
+            if ((uint64_t)f.q >= qthr) best = umin64(best, f.c);
         }
         more = __syncthreads_or(more);
     }
@@ -1652,8 +1775,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    DltHot dh{0, 0, 0, 0, 0};
-    if (PARETO) dh = DltHot{d.kbase, d.qmin, d.qmax, d.qshift, d.cshift};
+    DltHot dh{0, 0, 0, 0};
+    if (PARETO) dh = DltHot{d.kbase, d.qbase, d.qmshift, d.cshift};
     const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
     const uint64_t total = v.ntiles * per_tile;
     // stage sg of this view/pass -> flat slot of its first record (kInf64: none)
@@ -2086,7 +2209,7 @@ __global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) str
         ss.feas[threadIdx.x] = sa.gkey[2 * SW_MAX_QUERIES + threadIdx.x] ? 1u : 0u;
     }
     stage_tables(job.hdr, job.va, &h, va, (uint32_t)job.va_bytes, &bar);  // ends with a barrier
-    const DltHot dh{d->kbase, d->qmin, d->qmax, d->qshift, d->cshift};
+    const DltHot dh{d->kbase, d->qbase, d->qmshift, d->cshift};
     const uint64_t row = h.row;
     const uint32_t rl = h.radix[h.B - 1];
     const uint32_t lane = threadIdx.x & 31;

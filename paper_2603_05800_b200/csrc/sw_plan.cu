@@ -110,6 +110,7 @@ struct sw_plan {
     // (cached or collective) branch whatever its local refolds did
     uint64_t gepoch = 1;
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
+    const char* dump_merge = nullptr;  // SW_DUMP_MERGE=<prefix>: every fold merge's input -> <prefix>_<n>.bin
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
     uint32_t coop_grid = 0;
     bool trace = false;             // SW_TRACE=1: per-phase CUDA-event times of each select on stderr
@@ -687,6 +688,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if (const char* ev = getenv("SW_PARETO_CHUNK")) h->chunk = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
+    h->dump_merge = getenv("SW_DUMP_MERGE");
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
     if (const char* ev = getenv("SW_COOP_REDUCE")) h->coop_reduce = atoi(ev) != 0;
     if (const char* ev = getenv("SW_SURV_CAP")) {  // test hook: "<cap>[@<rank>]" (>= 256)
@@ -1117,6 +1119,9 @@ static cudaError_t set_attr_one() {
 static cudaError_t set_scan_smem_attrs() {
     cudaError_t e = cudaFuncSetAttribute(pareto_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)exact_smem_bytes());
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(dlt_qtop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kDltSortMax * sizeof(uint32_t)));
     cudaError_t r[] = {set_attr_one<0, 0>(), set_attr_one<1, 0>(), set_attr_one<2, 0>(), set_attr_one<4, 0>(),
                        set_attr_one<8, 0>(), set_attr_one<0, 1>(), set_attr_one<1, 1>(), set_attr_one<2, 1>(),
                        set_attr_one<4, 1>(), set_attr_one<8, 1>()};
@@ -1140,6 +1145,16 @@ static ParetoArgs pareto_args(sw_plan* h) {
     pa.gfeas = h->d_gfeas;
     pa.debug = h->debug ? 1u : 0u;
     return pa;
+}
+
+// The DLT of the current front: quality tops + q map (one block), then the t edges, t map
+// and cells (kDltT blocks).
+static sw_status dlt_build_async(sw_plan* h) {
+    dlt_qtop_kernel<<<1, kDltQThreads, kDltSortMax * sizeof(uint32_t), h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+    CKL(h);
+    dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+    CKL(h);
+    return SW_OK;
 }
 
 // ---- the device-sized merge pipeline: work[0, ctl.m_in) -> exact front in `out`
@@ -1253,8 +1268,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         v.pass = pass;
         v.upt = upt;
         v.levels = K;
-        dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
-        CKL(h);
+        if (sw_status ds = dlt_build_async(h); ds < 0) return ds;
         CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
         CK(h, cudaMemsetAsync(&h->d_ctl->dlt_n, 0, sizeof(unsigned long long), h->stream));
         const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / (kStageRecs * kCW)), h->scan_grid);
@@ -1281,6 +1295,20 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
                                                                h->d_ctl);
         CKL(h);
+        if (h->dump_merge) {  // diagnostics only (merge experiments): the merge input, raw PPoints
+            ParetoCtl c;
+            CK(h, cudaMemcpyAsync(&c, h->d_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
+            SYNC(h);
+            std::vector<PPoint> buf(c.m_in);
+            CK(h, cudaMemcpy(buf.data(), h->d_work, sizeof(PPoint) * c.m_in, cudaMemcpyDeviceToHost));
+            char path[512];
+            snprintf(path, sizeof path, "%s_%llu.bin", h->dump_merge, (unsigned long long)h->fold_passes + 1);
+            if (FILE* f = fopen(path, "wb")) {
+                fwrite(&c.front_n, sizeof(uint64_t), 1, f);  // the running front = the first front_n points
+                fwrite(buf.data(), sizeof(PPoint), buf.size(), f);
+                fclose(f);
+            }
+        }
         sw_status st = reduce_async(h, h->d_front);
         if (st < 0) return st;
         trace_mark(h, "merge");
@@ -1783,8 +1811,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
         // one pass: DLT from the running front, the fused kernel over the pass's tiles,
         // survivors merged into the front; the pass's survivor count lands in pinned memory
         auto run_pass = [&](uint32_t lvl, uint64_t ntp) -> sw_status {
-            dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
-            CKL(h);
+            if (sw_status ds = dlt_build_async(h); ds < 0) return ds;
             CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
             CK(h, cudaMemsetAsync(&h->d_ctl->dlt_n, 0, sizeof(unsigned long long), h->stream));
             StreamArgs sa{};

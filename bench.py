@@ -406,6 +406,7 @@ def measure_stream(ctx, pb, g, steps):
     stream mode evaluates the same space with NO record store (a7 skipped by design),
     select + Pareto filter in-kernel.  CUDA events on the handle's stream around whole
     calls, max over ranks; parity vs the oracle golden (winners + front) when there is one."""
+    import torch
     sw, dev, stream, comm = ctx["sw"], ctx["dev"], ctx["stream"], ctx["comm"]
     rank, world = ctx["rank"], ctx["world"]
     N = sw.space_shape(pb)[0]

@@ -764,6 +764,7 @@ struct ParetoCtl {
     unsigned long long dlt_pass;  // diagnostics: records the DLT did not rule out (all passes)
     unsigned long long dlt_n;     // DLT survivors appended by the current scan pass (deferred exact test)
     unsigned long long dlt_max;   // the largest dlt_n of any pass since the host last looked (buffer growth)
+    uint32_t rkmin, rkmax;        // merge: range of the t sort keys (bucket sort before the local fronts)
 };
 
 // Per-call status words of a multi-rank call, max-reduced over the ranks BEFORE any rank
@@ -1294,7 +1295,13 @@ __global__ void __launch_bounds__(kScanThreads) select_front_kernel(const PPoint
 
 // The whole exact merge work[0, ctl.m_in) -> sorted front in `out`, in ONE cooperative
 // launch (a persistent grid of 1024-thread blocks, phases separated by grid-wide
-// barriers): (1) 256-point block-local fronts into tmp2, (2) the m x m dominance mark in
+// barriers): (0) a bucket sort of the input by ttff_eff into `sorted` (kRedBuckets
+// buckets of the float key of t over its range: counts, one block's scan, scatter) -- a
+// point's dominators mostly have about its t, so (1) the 256-point block-local fronts of
+// t-sorted chunks keep ~4x fewer points than chunks in arrival order (measured on the C3
+// merges: 30 K in -> 3.9 K vs 16.9 K kept), which cuts the quadratic mark ~19x; the order
+// only affects speed, every phase is exact whatever it is; (1) local fronts into tmp2,
+// (2) the m x m dominance mark in
 // 256 x 256 tiles, (3) compaction into work, (4) rank sort into out; publishes front_n /
 // front_overflow.  Every 256-point tile is worked by 4 threads per point (64 tests each,
 // 8 independent tests per step): the phases are latency chains, not throughput, so the
@@ -1330,11 +1337,15 @@ __device__ __forceinline__ bool span_dominated(const PPoint* tile, uint32_t j0, 
     return dom;
 }
 
+constexpr uint32_t kRedBuckets = 4096;
+__device__ __forceinline__ uint32_t red_tkey(uint64_t t) { return __float_as_uint(__ull2float_rz(t)); }
+
 __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* __restrict__ work,
                                                                        PPoint* __restrict__ tmp2,
                                                                        uint8_t* __restrict__ keep,
                                                                        PPoint* __restrict__ out, ParetoCtl* ctl,
-                                                                       uint64_t cap) {
+                                                                       uint64_t cap, PPoint* __restrict__ sorted,
+                                                                       uint32_t* __restrict__ hist) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ PPoint tile[kScanThreads];
@@ -1350,19 +1361,86 @@ __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* _
         }
     };
     stamp(0);
-    if (blockIdx.x == 0 && tid == 0) {
-        ctl->m_loc = 0;
-        ctl->m_cmp = 0;
+    if (blockIdx.x == 0) {
+        if (tid == 0) {
+            ctl->m_loc = 0;
+            ctl->m_cmp = 0;
+            ctl->rkmin = 0xffffffffu;
+            ctl->rkmax = 0;
+        }
+        for (uint32_t i = tid; i < kRedBuckets; i += blockDim.x) hist[i] = 0;
     }
     grid.sync();
-    stamp(1);
     const uint32_t m = __ldcg(&ctl->m_in);
-    // (1) block-local fronts of 256-point chunks
+    const uint32_t gsz = gridDim.x * blockDim.x, gid = blockIdx.x * blockDim.x + tid;
+    {  // (0) bucket sort by t: key range, counts, scan (block 0), scatter
+        uint32_t lo = 0xffffffffu, hi = 0;
+        for (uint32_t x = gid; x < m; x += gsz) {
+            const uint32_t k = red_tkey(work[x].t);
+            lo = min(lo, k);
+            hi = max(hi, k);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if ((tid & 31) == 0 && hi >= lo) {
+            atomicMin(&ctl->rkmin, lo);
+            atomicMax(&ctl->rkmax, hi);
+        }
+        grid.sync();
+        const uint32_t kmin = __ldcg(&ctl->rkmin), kmax = __ldcg(&ctl->rkmax);
+        uint32_t sh = 0;
+        while (kmax > kmin && ((kmax - kmin) >> sh) >= kRedBuckets) sh++;
+        for (uint32_t x = gid; x < m; x += gsz) atomicAdd(&hist[(red_tkey(work[x].t) - kmin) >> sh], 1u);
+        grid.sync();
+        if (blockIdx.x == 0) {  // exclusive scan of the counts, kRedBuckets / 1024 per thread
+            constexpr uint32_t kPer = kRedBuckets / kRedThreads;
+            uint32_t v[kPer], sum = 0;
+#pragma unroll
+            for (uint32_t r = 0; r < kPer; r++) {
+                v[r] = __ldcg(&hist[tid * kPer + r]);
+                sum += v[r];
+            }
+            uint32_t inc = sum;
+            const uint32_t lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= (uint32_t)o) inc += y;
+            }
+            if (lane == 31) s_rank[wid] = inc;
+            __syncthreads();
+            if (wid == 0) {
+                const uint32_t w = s_rank[lane];
+                uint32_t wi = w;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                    if (lane >= (uint32_t)o) wi += y;
+                }
+                s_rank[lane] = wi - w;
+            }
+            __syncthreads();
+            uint32_t off = s_rank[wid] + inc - sum;
+#pragma unroll
+            for (uint32_t r = 0; r < kPer; r++) {
+                hist[tid * kPer + r] = off;
+                off += v[r];
+            }
+        }
+        grid.sync();
+        for (uint32_t x = gid; x < m; x += gsz) {
+            const PPoint p = work[x];
+            sorted[atomicAdd(&hist[(red_tkey(p.t) - kmin) >> sh], 1u)] = p;
+        }
+        grid.sync();
+    }
+    stamp(1);
+    // (1) block-local fronts of 256-point chunks of the t-sorted input
     for (uint32_t base = blockIdx.x * kScanThreads; base < m; base += gridDim.x * kScanThreads) {
         const uint32_t cnt = min((uint32_t)kScanThreads, m - base);
         __syncthreads();
         if (part == 0) {
-            if (pt < cnt) tile[pt] = work[base + pt];
+            if (pt < cnt) tile[pt] = ldcg_point(&sorted[base + pt]);
             s_dom[pt] = 0;
         }
         __syncthreads();

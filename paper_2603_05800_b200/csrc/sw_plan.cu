@@ -88,7 +88,8 @@ struct sw_plan {
     uint64_t front_cap = 1ull << 17;
     uint64_t surv_cap = 1ull << 17;
     PPoint* d_work = nullptr;  // front_cap + surv_cap
-    PPoint* d_tmp = nullptr;   // front_cap + surv_cap
+    PPoint* d_tmp = nullptr;   // front_cap + surv_cap (the merge's t-sorted input)
+    uint32_t* d_rhist = nullptr;  // kRedBuckets (the merge's bucket sort)
     uint8_t* d_keep = nullptr;
     ParetoCtl* d_ctl = nullptr;
     Dlt* d_dlt = nullptr;
@@ -734,6 +735,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if ((st = alloc_n(h, &h->d_work, h->front_cap + h->surv_cap, "pareto work")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_tmp, h->front_cap + h->surv_cap, "pareto tmp")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_keep, h->front_cap + h->surv_cap, "pareto flags")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_rhist, kRedBuckets, "merge buckets")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_tmp2, h->front_cap + h->surv_cap, "pareto tmp2")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_surv, h->surv_cap, "pareto survivors")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_ctl, 1, "pareto ctl")) < 0) return (st);
@@ -777,7 +779,7 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
                         h->d_tmp,   h->d_keep,    h->d_ctl,     h->d_dlt,
                         h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest, h->d_selfjob,
                         h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas, h->d_greedy,
-                        h->d_scand, h->d_scand_n, h->d_skey, h->d_dltc};
+                        h->d_scand, h->d_scand_n, h->d_skey, h->d_dltc, h->d_rhist};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
         if (h->h_pass_surv) cudaFreeHost(h->h_pass_surv);
@@ -1167,7 +1169,9 @@ static sw_status reduce_async(sw_plan* h, PPoint* out) {
         uint8_t* keep = h->d_keep;
         ParetoCtl* ctl = h->d_ctl;
         uint64_t cap = h->front_cap;
-        void* args[] = {&work, &tmp2, &keep, &out, &ctl, &cap};
+        PPoint* sorted = h->d_tmp;
+        uint32_t* hist = h->d_rhist;
+        void* args[] = {&work, &tmp2, &keep, &out, &ctl, &cap, &sorted, &hist};
         CK(h, cudaLaunchCooperativeKernel((const void*)pareto_reduce_kernel, dim3(h->coop_grid), dim3(kRedThreads),
                                           args, 0, h->stream));
         h->launches++;

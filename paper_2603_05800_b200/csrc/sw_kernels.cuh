@@ -1547,14 +1547,19 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
 // front point), so the merge after the pass stays exact.  Dropped DLT survivors (candidate
 // buffer full) set surv_overflow: the merged front is then valid but incomplete and the pass
 // is refolded.  The front (<= kExactFront points) and the lists live in dynamic shared
-// memory as arrays (t, c, idx, q).
+// memory as arrays (t, c, idx, q), with a position map of the front's t (the float key of
+// t, kDltMap cells of 1/128 octave: cell k -> [#front t below it, #front t up to its
+// end]) so that x's position in the front is a map load plus a search of one cell's
+// range (usually empty) instead of an 11-step binary search of dependent smem loads.
+// 24 warps per block (one block per SM: the front copy is shared by all of them).
 constexpr uint32_t kExactFront = 2048;  // front points staged in smem (larger fronts: from L2)
-constexpr uint32_t kExactList = 256;    // per-warp survivor list
-constexpr int kExactThreads = 512;
+constexpr uint32_t kExactList = 128;    // per-warp survivor list
+constexpr int kExactThreads = 768;
 constexpr int kExactWarps = kExactThreads / 32;
 constexpr uint32_t kExactNear = 8;      // front points below x.t tested per lane first
 __host__ __device__ constexpr size_t exact_smem_bytes() {
-    return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t));
+    return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t)) +
+           (size_t)kDltMap * sizeof(uint32_t);
 }
 struct PArrays {  // a point list as arrays in shared memory
     uint64_t *t, *c, *i;
@@ -1599,8 +1604,34 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
     const uint64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
     if (r0 >= r1) return;
     const bool f_smem = m <= kExactFront;
-    if (f_smem)
+    uint32_t* pmap = reinterpret_cast<uint32_t*>(xsm + (size_t)(kExactFront + kExactWarps * kExactList) * 28);
+    const int32_t pkbase = m ? dlt_tkey(front[0].t) : 0;  // cell 0 holds the smallest front t
+    if (f_smem) {
         for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) F.put(j, front[j]);
+        __syncthreads();
+        auto count_le = [&](uint64_t v) {  // #front points with t <= v
+            uint32_t a = 0, e = m;
+            while (a < e) {
+                const uint32_t mid = (a + e) >> 1;
+                if (F.t[mid] <= v) a = mid + 1;
+                else e = mid;
+            }
+            return a;
+        };
+        for (uint32_t k = threadIdx.x; k < (uint32_t)kDltMap; k += blockDim.x) {
+            // cell k: keys pkbase + k (the last cell: everything above); lo = #t below the
+            // cell's lower end L, hi = #t <= its upper end
+            const int32_t key = pkbase + (int32_t)k;
+            auto lower_end = [&](int32_t kk) -> uint64_t {  // smallest integer t with key(t) >= kk
+                return (kk >= (0x7f800000 >> kDltTShift)) ? kInf64
+                                                          : (uint64_t)ceilf(__uint_as_float((uint32_t)kk << kDltTShift));
+            };
+            const uint64_t L = lower_end(key), Ln = lower_end(key + 1);
+            const uint32_t lo = (k == 0 || L == 0) ? 0 : count_le(L - 1);
+            const uint32_t hi = (k == (uint32_t)kDltMap - 1 || Ln == kInf64) ? m : count_le(Ln - 1);
+            pmap[k] = lo | (hi << 16);
+        }
+    }
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const PArrays L = parrays(xsm + (size_t)kExactFront * 28 + (size_t)warp * kExactList * 28, kExactList);
@@ -1626,6 +1657,12 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
         if (valid) {
             x = cand[i];
             uint32_t hi = m;  // lo = #front points with t <= x.t
+            if (f_smem) {  // narrowed by the position map (t below the front's smallest: lo = 0)
+                const int32_t k = dlt_tkey(x.t) - pkbase;
+                const uint32_t pm = pmap[min(max(k, 0), kDltMap - 1)];
+                lo = k < 0 ? 0 : pm & 0xffffu;
+                hi = k < 0 ? 0 : pm >> 16;
+            }
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) >> 1;
                 if ((f_smem ? F.t[mid] : front[mid].t) <= x.t) lo = mid + 1;

@@ -522,8 +522,11 @@ def main():
                     r.pop(k, None)
                 if args.stream_steps > 0:
                     gx = os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % cfg)
-                    r["stream_mode"] = measure_stream(ctx, pbx, json.load(open(gx)) if os.path.exists(gx) else None,
-                                                      2 if nx > 2e9 else args.stream_steps)
+                    try:
+                        r["stream_mode"] = measure_stream(ctx, pbx, json.load(open(gx)) if os.path.exists(gx) else None,
+                                                          2 if nx > 2e9 else args.stream_steps)
+                    except Exception as ex:  # noqa: BLE001 -- reported, never hides the record path
+                        r["stream_mode"] = {"error": "%s: %s" % (type(ex).__name__, ex)}
                 extra[cfg] = r
         except Exception as ex:  # noqa: BLE001 -- reported in the line, never hides the headline
             extra[cfg] = {"error": "%s: %s" % (type(ex).__name__, ex)}

@@ -2205,7 +2205,12 @@ __device__ __forceinline__ uint64_t closest_key(const QueryDev& q, const Rec4& r
     return ~((umin64(vt, 0xffffffffull) << 32) | umin64(vc, 0xffffffffull));
 }
 
+constexpr int kStreamThreads = 256;  // each block stages the DLT (~80 KB) + tables
 struct StreamShared {
+    // per warp and query: the best candidate this warp passed to the query's filter (total
+    // order cand_better); appended to the query's list once, when the warp is done -- a
+    // report per improvement overflowed the lists when many records tie on the pruning key
+    Cand wb[kStreamThreads / 32][SW_MAX_QUERIES];
     QueryDev q[SW_MAX_QUERIES];
     unsigned long long key[SW_MAX_QUERIES];   // best pruning key of a reported feasible candidate
     unsigned long long ckey[SW_MAX_QUERIES];  // best closest-tier key of a reported candidate
@@ -2220,6 +2225,8 @@ struct StreamEmit {
     uint64_t rowbase;  // global index of this lane's row's first candidate
     uint32_t rl;
     bool edge;         // the row crosses the shard boundary: check each index
+    bool allf;         // at the tile's start every query had a feasible report ...
+    unsigned long long kmin;  // ... and this was the smallest of their pruning keys
     struct Put {
         const StreamEmit* e;
         uint64_t base;  // index of candidate (dm, 0)
@@ -2231,8 +2238,10 @@ struct StreamEmit {
             const uint64_t idx = base + dl;
             const bool valid = live && (!e->edge || (idx >= a.ib && idx < a.ie));
             const uint32_t obj = a.P.objective;
-            // ---- a9: which records can still beat what was reported?
-            for (uint32_t q = 0; q < a.P.nq; q++) {
+            // ---- a9: which records can still beat what was reported?  (Keys only rise:
+            // a record below the smallest key of the tile's start passes no query.)
+            const bool pre = !e->allf || (valid && prune_key(obj, r) >= e->kmin);
+            for (uint32_t q = 0; q < a.P.nq && __any_sync(0xffffffffu, pre); q++) {
                 const QueryDev Q = S.q[q];
                 const bool f = valid & (r.w0 <= Q.slo_t) & (r.w1 <= Q.slo_s) & (r.w2 <= Q.budget);
                 bool pass = f & (prune_key(obj, r) >= *(volatile unsigned long long*)&S.key[q]);
@@ -2252,13 +2261,10 @@ struct StreamEmit {
                     }
                 }
                 if (lane == 0 && ci != kInf64) {
-                    const uint32_t slot = atomicAdd(&a.cand_n[q], 1u);
-                    if (slot < a.cand_cap) {
-                        Cand c;
-                        c.idx = ci;
-                        c.pad = 0;
-                        c.r = cr;
-                        a.cand[(uint64_t)q * a.cand_cap + slot] = c;
+                    Cand& wb = S.wb[threadIdx.x >> 5][q];
+                    if (cand_better(Q, obj, ci, cr, wb.idx, wb.r)) {
+                        wb.idx = ci;
+                        wb.r = cr;
                     }
                     if (feasible(Q, cr)) {
                         const unsigned long long k = prune_key(obj, cr);
@@ -2299,7 +2305,6 @@ struct StreamEmit {
     __device__ __forceinline__ Put at(uint32_t dm, bool live) const { return Put{this, rowbase + (uint64_t)dm * rl, live}; }
 };
 
-constexpr int kStreamThreads = 256;  // each block stages the DLT (~72 KB) + tables
 // registers: the eval path plus the in-kernel filters (2 blocks/SM only for one pool)
 __host__ __device__ constexpr int stream_min_blocks(int np, int bm) { return (np == 1 && bm < 2) ? 2 : 1; }
 
@@ -2317,6 +2322,8 @@ __global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) str
         uint4* dst = reinterpret_cast<uint4*>(d);
         for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
     }
+    for (uint32_t i = threadIdx.x; i < (kStreamThreads / 32) * SW_MAX_QUERIES; i += blockDim.x)
+        ss.wb[i / SW_MAX_QUERIES][i % SW_MAX_QUERIES].idx = kInf64;
     if (threadIdx.x < SW_MAX_QUERIES) {
         ss.q[threadIdx.x] = sa.P.q[threadIdx.x];
         ss.key[threadIdx.x] = sa.gkey[threadIdx.x];
@@ -2343,8 +2350,26 @@ __global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) str
         __syncwarp();
         const uint64_t H = t * kTileRows + lane;
         const uint64_t rb = H * row;
-        const StreamEmit em{&sa, &ss, d, dh, rb, rl, rb < sa.ib || rb + row > sa.ie};
+        bool allf = true;
+        unsigned long long kmin = ~0ull;
+        for (uint32_t q = 0; q < sa.P.nq; q++) {
+            allf &= *(volatile uint32_t*)&ss.feas[q] != 0;
+            kmin = min(kmin, *(volatile unsigned long long*)&ss.key[q]);
+        }
+        const StreamEmit em{&sa, &ss, d, dh, rb, rl, rb < sa.ib || rb + row > sa.ie, allf, kmin};
         eval_tile_b<NP, BM != 0, BM == 2>(h, va, t, em);
+    }
+    __syncwarp();
+    if (lane < sa.P.nq) {  // this warp's best per query -> the query's list
+        const Cand& wb = ss.wb[threadIdx.x >> 5][lane];
+        if (wb.idx != kInf64) {
+            const uint32_t slot = atomicAdd(&sa.cand_n[lane], 1u);
+            if (slot < sa.cand_cap) {
+                Cand c = wb;
+                c.pad = 0;
+                sa.cand[(uint64_t)lane * sa.cand_cap + slot] = c;
+            }
+        }
     }
 }
 

@@ -30,6 +30,7 @@ for t in $NCU; do
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_$c.csv \
         python bench.py --config $c --configs "" --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --stream-steps 0 > gpurun_out/${TAG}_ncu_launch_$c.log 2>&1
         python tools/launch_summary.py gpurun_out/${TAG}_launches_$c.csv > gpurun_out/${TAG}_launch_summary_$c.txt 2>&1 ;;
+    trace) SW_TRACE=1 timeout 300 python tools/one_step.py $c 3 > gpurun_out/${TAG}_trace_$c.txt 2>&1 ;;
     debug) SW_DEBUG=1 SW_TRACE=1 timeout 300 python tools/one_step.py $c 2 > gpurun_out/${TAG}_debug_$c.txt 2>&1 ;;
     dump) mkdir -p gpurun_out/dump; SW_DUMP_MERGE=gpurun_out/dump/${TAG}_$c SW_DEBUG=1 timeout 300 python tools/one_step.py $c 1 > gpurun_out/${TAG}_dump_$c.txt 2>&1 ;;
     sdebug) SW_DEBUG=1 SW_TRACE=1 timeout 300 python tools/shared_one.py $c > gpurun_out/${TAG}_sdebug_$c.txt 2>&1 ;;

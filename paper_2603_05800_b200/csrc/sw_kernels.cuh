@@ -2208,8 +2208,9 @@ __device__ __forceinline__ uint64_t closest_key(const QueryDev& q, const Rec4& r
 constexpr int kStreamThreads = 256;  // each block stages the DLT (~80 KB) + tables
 struct StreamShared {
     // per warp and query: the best candidate this warp passed to the query's filter (total
-    // order cand_better); appended to the query's list once, when the warp is done -- a
-    // report per improvement overflowed the lists when many records tie on the pruning key
+    // order cand_better), kept by the warp's lane 0 (the only thread that touches it) and
+    // appended to the query's list once, when the warp is done -- a report per improvement
+    // overflowed the lists when many records tie on the pruning key
     Cand wb[kStreamThreads / 32][SW_MAX_QUERIES];
     QueryDev q[SW_MAX_QUERIES];
     unsigned long long key[SW_MAX_QUERIES];   // best pruning key of a reported feasible candidate
@@ -2241,7 +2242,8 @@ struct StreamEmit {
             // ---- a9: which records can still beat what was reported?  (Keys only rise:
             // a record below the smallest key of the tile's start passes no query.)
             const bool pre = !e->allf || (valid && prune_key(obj, r) >= e->kmin);
-            for (uint32_t q = 0; q < a.P.nq && __any_sync(0xffffffffu, pre); q++) {
+            const uint32_t nq = __any_sync(0xffffffffu, pre) ? a.P.nq : 0u;
+            for (uint32_t q = 0; q < nq; q++) {
                 const QueryDev Q = S.q[q];
                 const bool f = valid & (r.w0 <= Q.slo_t) & (r.w1 <= Q.slo_s) & (r.w2 <= Q.budget);
                 bool pass = f & (prune_key(obj, r) >= *(volatile unsigned long long*)&S.key[q]);
@@ -2322,8 +2324,8 @@ __global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) str
         uint4* dst = reinterpret_cast<uint4*>(d);
         for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
     }
-    for (uint32_t i = threadIdx.x; i < (kStreamThreads / 32) * SW_MAX_QUERIES; i += blockDim.x)
-        ss.wb[i / SW_MAX_QUERIES][i % SW_MAX_QUERIES].idx = kInf64;
+    if ((threadIdx.x & 31) == 0)  // each warp's lane 0 alone writes and reads its bests
+        for (uint32_t q = 0; q < SW_MAX_QUERIES; q++) ss.wb[threadIdx.x >> 5][q].idx = kInf64;
     if (threadIdx.x < SW_MAX_QUERIES) {
         ss.q[threadIdx.x] = sa.P.q[threadIdx.x];
         ss.key[threadIdx.x] = sa.gkey[threadIdx.x];
@@ -2359,18 +2361,17 @@ __global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) str
         const StreamEmit em{&sa, &ss, d, dh, rb, rl, rb < sa.ib || rb + row > sa.ie, allf, kmin};
         eval_tile_b<NP, BM != 0, BM == 2>(h, va, t, em);
     }
-    __syncwarp();
-    if (lane < sa.P.nq) {  // this warp's best per query -> the query's list
-        const Cand& wb = ss.wb[threadIdx.x >> 5][lane];
-        if (wb.idx != kInf64) {
-            const uint32_t slot = atomicAdd(&sa.cand_n[lane], 1u);
+    if (lane == 0)  // this warp's best per query -> the query's list (lane 0 wrote them)
+        for (uint32_t q = 0; q < sa.P.nq; q++) {
+            const Cand& wb = ss.wb[threadIdx.x >> 5][q];
+            if (wb.idx == kInf64) continue;
+            const uint32_t slot = atomicAdd(&sa.cand_n[q], 1u);
             if (slot < sa.cand_cap) {
                 Cand c = wb;
                 c.pad = 0;
-                sa.cand[(uint64_t)lane * sa.cand_cap + slot] = c;
+                sa.cand[(uint64_t)q * sa.cand_cap + slot] = c;
             }
         }
-    }
 }
 
 // One candidate from scratch (a1-a7 for a single index; plain loads from global/L2).

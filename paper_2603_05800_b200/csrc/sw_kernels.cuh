@@ -944,8 +944,25 @@ __global__ void __launch_bounds__(kDltQThreads) dlt_qtop_kernel(const PPoint* __
     if (m > 0 && m <= kDltSortMax) {
         uint32_t n2 = 1;
         while (n2 < m) n2 <<= 1;
-        for (uint32_t i = tid; i < n2; i += blockDim.x) qs[i] = i < m ? front[i].q : 0xffffffffu;
-        __syncthreads();
+        if (m <= (uint32_t)kDltQThreads) {  // one value per thread: rank sort, no barrier steps
+            uint32_t* src = qs + kDltSortMax / 2;
+            if (tid < m) src[tid] = front[tid].q;
+            __syncthreads();
+            if (tid < m) {
+                const uint32_t v = src[tid];
+                uint32_t r = 0;
+                for (uint32_t j = 0; j < m; j++) {
+                    const uint32_t w = src[j];
+                    r += (w < v || (w == v && j < tid)) ? 1u : 0u;
+                }
+                qs[r] = v;
+            }
+            __syncthreads();
+            n2 = 0;  // sorted: skip the network below
+        } else {
+            for (uint32_t i = tid; i < n2; i += blockDim.x) qs[i] = i < m ? front[i].q : 0xffffffffu;
+            __syncthreads();
+        }
         for (uint32_t k = 2; k <= n2; k <<= 1)  // bitonic sort, ascending
             for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
                 for (uint32_t i = tid; i < n2; i += blockDim.x) {
@@ -1338,6 +1355,7 @@ __device__ __forceinline__ bool span_dominated(const PPoint* tile, uint32_t j0, 
 }
 
 constexpr uint32_t kRedBuckets = 4096;
+constexpr uint32_t kRedSortMin = 12288;
 __device__ __forceinline__ uint32_t red_tkey(uint64_t t) { return __float_as_uint(__ull2float_rz(t)); }
 
 __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* __restrict__ work,
@@ -1373,7 +1391,10 @@ __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* _
     grid.sync();
     const uint32_t m = __ldcg(&ctl->m_in);
     const uint32_t gsz = gridDim.x * blockDim.x, gid = blockIdx.x * blockDim.x + tid;
-    {  // (0) bucket sort by t: key range, counts, scan (block 0), scatter
+    // (0) bucket sort by t (inputs of >= kRedSortMin points; smaller ones are cheap to mark
+    // as they come): key range, counts, scan (block 0), scatter.  m is grid-uniform.
+    const bool do_sort = m >= kRedSortMin;
+    if (do_sort) {
         uint32_t lo = 0xffffffffu, hi = 0;
         for (uint32_t x = gid; x < m; x += gsz) {
             const uint32_t k = red_tkey(work[x].t);
@@ -1440,7 +1461,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* _
         const uint32_t cnt = min((uint32_t)kScanThreads, m - base);
         __syncthreads();
         if (part == 0) {
-            if (pt < cnt) tile[pt] = ldcg_point(&sorted[base + pt]);
+            if (pt < cnt) tile[pt] = ldcg_point(do_sort ? &sorted[base + pt] : &work[base + pt]);
             s_dom[pt] = 0;
         }
         __syncthreads();
@@ -1483,28 +1504,29 @@ __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* _
     }
     if (mc > cap) return;
     // (4) rank sort by (t asc, c asc, q desc, index asc) -- indices are unique (a bitonic
-    // sort of the few hundred points in one block measured slower: ~45 barrier steps)
-    for (uint32_t xb = blockIdx.x; xb * kScanThreads < mc; xb += gridDim.x) {
-        const uint32_t x = xb * kScanThreads + pt;
+    // sort of the few hundred points in one block measured slower: ~45 barrier steps).
+    // 64 points per block, 16 threads per point (each 1/16 of every 256-point tile), so a
+    // front of m points keeps m / 64 blocks busy.
+    constexpr uint32_t kRankPts = 64, kRankParts = kRedThreads / kRankPts;
+    const uint32_t rp = tid % kRankPts, rpart = tid / kRankPts;
+    for (uint32_t xb = blockIdx.x; xb * kRankPts < mc; xb += gridDim.x) {
+        const uint32_t x = xb * kRankPts + rp;
         __syncthreads();
-        if (part == 0) s_rank[pt] = 0;
+        if (tid < kRankPts) s_rank[tid] = 0;
         const PPoint px = x < mc ? ldcg_point(&work[x]) : PPoint{};
         uint32_t rank = 0;
         for (uint32_t base = 0; base < mc; base += kScanThreads) {
             __syncthreads();
-            if (part == 0 && base + pt < mc) tile[pt] = ldcg_point(&work[base + pt]);
+            if (tid < kScanThreads && base + tid < mc) tile[tid] = ldcg_point(&work[base + tid]);
             __syncthreads();
             const uint32_t lim = min((uint32_t)kScanThreads, mc - base);
-            const uint32_t j0 = part * kRedSpan;
-#pragma unroll 8
-            for (uint32_t g = 0; g < kRedSpan; g++) {
-                const uint32_t j = j0 + g;
-                rank += ((j < lim) & pkey_less(tile[j < lim ? j : 0], px)) ? 1u : 0u;
-            }
+#pragma unroll 4
+            for (uint32_t g = rpart; g < (uint32_t)kScanThreads; g += kRankParts)
+                rank += ((g < lim) & pkey_less(tile[g < lim ? g : 0], px)) ? 1u : 0u;
         }
-        atomicAdd(&s_rank[pt], rank);
+        atomicAdd(&s_rank[rp], rank);
         __syncthreads();
-        if (part == 0 && x < mc) out[s_rank[pt]] = px;
+        if (tid < kRankPts && x < mc) out[s_rank[tid]] = px;
     }
     if (blockIdx.x == 0) stamp(5);  // block 0's own share of the rank sort done
 }

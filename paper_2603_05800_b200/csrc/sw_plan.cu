@@ -111,6 +111,7 @@ struct sw_plan {
     // (cached or collective) branch whatever its local refolds did
     uint64_t gepoch = 1;
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
+    uint32_t fold_kmin = 2;      // SW_FOLD_KMIN: fewest strided fold levels (passes - 1) of a large segment
     const char* dump_merge = nullptr;  // SW_DUMP_MERGE=<prefix>: every fold merge's input -> <prefix>_<n>.bin
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
     uint32_t coop_grid = 0;
@@ -690,6 +691,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     h->dump_merge = getenv("SW_DUMP_MERGE");
+    if (const char* ev = getenv("SW_FOLD_KMIN")) h->fold_kmin = (uint32_t)std::min(std::max(atoi(ev), 1), 9);
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
     if (const char* ev = getenv("SW_COOP_REDUCE")) h->coop_reduce = atoi(ev) != 0;
     if (const char* ev = getenv("SW_SURV_CAP")) {  // test hook: "<cap>[@<rank>]" (>= 256)
@@ -1203,7 +1205,9 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
     // a strided sample seeds the running front (its exact front is cheap to reduce)
     // (a larger sample for large segments: a better first front cuts the first pass's
     // survivors and its merge)
-    const uint32_t ns = (uint32_t)std::min<uint64_t>(n, n >= (1ull << 26) ? 65536 : 16384);
+    uint64_t want = n >= (1ull << 26) ? 65536 : 16384;
+    if (const char* ev = getenv("SW_SEED_N")) want = std::max<uint64_t>(1024, strtoull(ev, nullptr, 10));  // experiments
+    const uint32_t ns = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(n, want), h->front_cap + h->surv_cap);
     CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
     pareto_sample_kernel<<<(ns + 255) / 256, 256, 0, h->stream>>>(view_of(h, g, 0, g.ntiles), ns, h->d_work, h->d_ctl);
     CKL(h);
@@ -1250,7 +1254,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
     const uint64_t nunits = (total + unit_recs - 1) / unit_recs;
     // K levels: the first pass covers about kFirstPass records (>= 1/64 of the segment)
     const uint64_t kFirstPass = 8ull << 20;
-    uint32_t K = 2;
+    uint32_t K = h->fold_kmin;
     while (K < 10 && (nunits >> (3 * K)) * unit_recs > kFirstPass) K++;
     const bool strided = nunits >= 256;
     const uint64_t last_short = nunits * unit_recs - total;  // missing slots of the last unit

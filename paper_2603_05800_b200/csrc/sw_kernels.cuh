@@ -1068,37 +1068,49 @@ __global__ void __launch_bounds__(kDltQThreads) dlt_qtop_kernel(const PPoint* __
     }
 }
 
-// One launch builds the rest of the DLT: block b (kDltQ threads) computes the t edges it
-// needs, the cost shift, cell row b and a 1/kDltT share of the t map; block 0 writes the
-// header.  The front is sorted by t, so a cell scan stops at the first f.t > edge.  The
-// quality tops come from dlt_qtop_kernel (launched before, same stream).
-__global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restrict__ front,
-                                                          const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
-    __shared__ PPoint tile[kDltQ];
+// One launch builds the rest of the DLT: block j (256 threads) owns quality column j;
+// thread r takes the front's t slice (te[r-1], te[r]] (the front is sorted by t: an index
+// range, two binary searches), the min cost of its points with q >= qtop[j], and a block
+// prefix-min over r turns slices into the cell's "t <= te[r]" minimum.  Every block also
+// builds a 1/kDltQ share of the t map; block 0 writes the header, the t edges and the
+// "none" row and column.  The quality tops come from dlt_qtop_kernel (launched before).
+constexpr int kDltBuildThreads = 256;
+static_assert(kDltT < kDltBuildThreads, "one thread per t bin");
+__global__ void __launch_bounds__(kDltBuildThreads) dlt_build_kernel(const PPoint* __restrict__ front,
+                                                                     const ParetoCtl* __restrict__ ctl,
+                                                                     Dlt* __restrict__ d) {
     __shared__ uint64_t te[kDltT];
     __shared__ unsigned long long s_cmax;
+    __shared__ unsigned long long s_wmin[kDltBuildThreads / 32];
     const uint32_t m = (uint32_t)ctl->front_n;
-    const uint32_t b = blockIdx.x, j = threadIdx.x;
-    if (j == 0) s_cmax = 0;
-    for (uint32_t i = j; i < kDltT; i += blockDim.x) te[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
+    const uint32_t j = blockIdx.x, r = threadIdx.x, lane = r & 31, wid = r >> 5;
+    if (r == 0) s_cmax = 0;
+    for (uint32_t i = r; i < kDltT; i += blockDim.x) te[i] = m ? front[((uint64_t)i * m) / kDltT].t : kInf64;
     __syncthreads();
     uint64_t cmx = 0;
-    for (uint32_t i = j; i < m; i += blockDim.x) cmx = umax64(cmx, front[i].c);
-    atomicMax(&s_cmax, (unsigned long long)cmx);
+    for (uint32_t i = r; i < m; i += blockDim.x) cmx = umax64(cmx, front[i].c);
+    cmx = umax64(cmx, __shfl_xor_sync(0xffffffffu, cmx, 16));
+    cmx = umax64(cmx, __shfl_xor_sync(0xffffffffu, cmx, 8));
+    cmx = umax64(cmx, __shfl_xor_sync(0xffffffffu, cmx, 4));
+    cmx = umax64(cmx, __shfl_xor_sync(0xffffffffu, cmx, 2));
+    cmx = umax64(cmx, __shfl_xor_sync(0xffffffffu, cmx, 1));
+    if (lane == 0) atomicMax(&s_cmax, (unsigned long long)cmx);
     __syncthreads();
     uint32_t csh = 0;
     while ((s_cmax >> csh) >= 0xffffull) csh++;  // every front cost fits below the 0xffff "none"
     // map cell 0 sits just below the front's smallest t: it holds no edge
     const int32_t kbase = m ? dlt_tkey(front[0].t) - 1 : 0x7fffffff;
-    if (b == 0) {
-        if (j == 0) {
+    if (j == 0) {
+        if (r == 0) {
             d->kbase = kbase;
             d->cshift = csh;
         }
-        for (uint32_t i = j; i < kDltT; i += blockDim.x) d->tedge[i] = te[i];
+        for (uint32_t i = r; i < kDltT; i += blockDim.x) d->tedge[i] = te[i];
+        for (uint32_t i = r; i <= (uint32_t)kDltT; i += blockDim.x) d->cell[i * kDltCols + kDltQ] = 0xffff;
     }
+    if (r == 0) d->cell[j] = 0xffff;  // row 0: no front point has t <= the record's t
     // the t map, dealt over the grid: #edges <= lower end of cell k
-    for (uint32_t k = b * blockDim.x + j; k < (uint32_t)kDltMap; k += gridDim.x * blockDim.x) {
+    for (uint32_t k = j * blockDim.x + r; k < (uint32_t)kDltMap; k += gridDim.x * blockDim.x) {
         const int32_t key = kbase + (int32_t)k;
         auto lower_end = [&](int32_t kk) -> uint64_t {  // smallest integer t with key(t) >= kk
             return (kk >= (0x7f800000 >> kDltTShift)) ? kInf64 : (uint64_t)ceilf(__uint_as_float((uint32_t)kk << kDltTShift));
@@ -1118,32 +1130,46 @@ __global__ void __launch_bounds__(kDltQ) dlt_build_kernel(const PPoint* __restri
         const uint32_t lo = m ? count_le(L) : 0, hi = m ? count_le(U) : 0;
         d->tmap[k] = (uint16_t)(lo | (hi << 8));
     }
-    // cell row b, thread j = quality column: needs f.q >= qtop[j] (columns >= ntop: none)
-    const uint64_t Eb = te[b];
+    // slice of t bin r: front indices [#t <= te[r-1], #t <= te[r]).  te[r] is the t of
+    // front point (r m) / kDltT, so #t <= te[r] is found by galloping forward from there
+    // (a step or two; long runs of equal t take a doubling search)
+    auto count_le_from = [&](uint32_t start) -> uint32_t {  // front[start].t = v; #t <= v
+        const uint64_t v = __ldg(&front[start].t);
+        uint32_t a = start + 1, b = a, step = 1;  // invariant: t[a - 1] <= v
+        while (b < m && __ldg(&front[b].t) <= v) {
+            a = b + 1;
+            b = a + step;
+            step <<= 1;
+        }
+        b = min(b, m);
+        while (a < b) {  // t[a - 1] <= v < t[b] (or b = m)
+            const uint32_t mid = (a + b) >> 1;
+            if (__ldg(&front[mid].t) <= v) a = mid + 1;
+            else b = mid;
+        }
+        return a;
+    };
     const uint32_t ntop = d->ntop;
     const uint64_t qthr = j < ntop ? (uint64_t)d->qtop[j] : (1ull << 33);
     uint64_t best = kInf64;
-    bool more = true;
-    for (uint32_t base = 0; base < m && more; base += kDltQ) {
-        __syncthreads();
-        if (base + j < m) tile[j] = front[base + j];
-        __syncthreads();
-        const uint32_t lim = min((uint32_t)kDltQ, m - base);
-        for (uint32_t i = 0; i < lim; i++) {
-            const PPoint f = tile[i];
-            if (f.t > Eb) {
-                more = false;  // front sorted by t: no later point qualifies
-                break;
-            }
-            if ((uint64_t)f.q >= qthr) best = umin64(best, f.c);
-        }
-        more = __syncthreads_or(more);
+    if (r < (uint32_t)kDltT && m && j < ntop) {
+        const uint32_t i0 = r ? count_le_from((uint32_t)(((uint64_t)(r - 1) * m) / kDltT)) : 0;
+        const uint32_t i1 = count_le_from((uint32_t)(((uint64_t)r * m) / kDltT));
+        for (uint32_t i = i0; i < i1; i++)
+            if ((uint64_t)__ldg(&front[i].q) >= qthr) best = umin64(best, __ldg(&front[i].c));
     }
-    // row b + 1 holds t bin b; row 0 and column kDltQ are "none"
-    d->cell[(b + 1) * kDltCols + j] = (m == 0 || best == kInf64) ? (uint16_t)0xffff : (uint16_t)(best >> csh);
-    if (j == 0) d->cell[(b + 1) * kDltCols + kDltQ] = 0xffff;
-    if (b == 0)
-        for (uint32_t i = j; i < (uint32_t)kDltCols; i += blockDim.x) d->cell[i] = 0xffff;
+    // inclusive prefix-min over the t bins (warp scan, then across the warps)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, best, o);
+        if (lane >= (uint32_t)o) best = umin64(best, y);
+    }
+    if (lane == 31) s_wmin[wid] = best;
+    __syncthreads();
+    for (uint32_t w = 0; w < wid; w++) best = umin64(best, s_wmin[w]);
+    // row r + 1 holds t bin r
+    if (r < (uint32_t)kDltT)
+        d->cell[(r + 1) * kDltCols + j] = best == kInf64 ? (uint16_t)0xffff : (uint16_t)(best >> csh);
 }
 
 // work = front[0, front_n) ++ surv[0, min(surv, cap)); m_in = its size.

@@ -1156,7 +1156,7 @@ static ParetoArgs pareto_args(sw_plan* h) {
 static sw_status dlt_build_async(sw_plan* h) {
     dlt_qtop_kernel<<<1, kDltQThreads, kDltSortMax * sizeof(uint32_t), h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
     CKL(h);
-    dlt_build_kernel<<<kDltT, kDltQ, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+    dlt_build_kernel<<<kDltQ, kDltBuildThreads, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
     CKL(h);
     return SW_OK;
 }
@@ -1205,7 +1205,7 @@ static sw_status seed_async(sw_plan* h, const Segment& g) {
     // a strided sample seeds the running front (its exact front is cheap to reduce)
     // (a larger sample for large segments: a better first front cuts the first pass's
     // survivors and its merge)
-    uint64_t want = n >= (1ull << 26) ? 65536 : 16384;
+    uint64_t want = n >= (1ull << 26) ? 32768 : 16384;
     if (const char* ev = getenv("SW_SEED_N")) want = std::max<uint64_t>(1024, strtoull(ev, nullptr, 10));  // experiments
     const uint32_t ns = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(n, want), h->front_cap + h->surv_cap);
     CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));

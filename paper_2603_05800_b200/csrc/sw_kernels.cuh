@@ -947,13 +947,20 @@ __global__ void __launch_bounds__(kDltQThreads) dlt_qtop_kernel(const PPoint* __
         if (m <= (uint32_t)kDltQThreads) {  // one value per thread: rank sort, no barrier steps
             uint32_t* src = qs + kDltSortMax / 2;
             if (tid < m) src[tid] = front[tid].q;
+            else if (tid < ((m + 3) & ~3u)) src[tid] = 0xffffffffu;  // pad to whole 16 B loads (never counted)
             __syncthreads();
-            if (tid < m) {
+            if (tid < m) {  // rank = #{j: q_j < v} + #{j < tid: q_j = v}, 4 values per 16 B load
                 const uint32_t v = src[tid];
                 uint32_t r = 0;
-                for (uint32_t j = 0; j < m; j++) {
-                    const uint32_t w = src[j];
-                    r += (w < v || (w == v && j < tid)) ? 1u : 0u;
+                const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll 4
+                for (uint32_t j4 = 0; j4 < (m + 3) / 4; j4++) {
+                    const uint4 w = s4[j4];
+                    const uint32_t j = 4 * j4;
+                    r += (w.x < v || (w.x == v && j < tid)) ? 1u : 0u;
+                    r += (w.y < v || (w.y == v && j + 1 < tid)) ? 1u : 0u;
+                    r += (w.z < v || (w.z == v && j + 2 < tid)) ? 1u : 0u;
+                    r += (w.w < v || (w.w == v && j + 3 < tid)) ? 1u : 0u;
                 }
                 qs[r] = v;
             }
@@ -1605,6 +1612,7 @@ constexpr uint32_t kExactList = 128;    // per-warp survivor list
 constexpr int kExactThreads = 768;
 constexpr int kExactWarps = kExactThreads / 32;
 constexpr uint32_t kExactNear = 8;      // front points below x.t tested per lane first
+constexpr int kExactLaneMin = 6;        // undecided lanes from which each lane scans its own
 __host__ __device__ constexpr size_t exact_smem_bytes() {
     return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t)) +
            (size_t)kDltMap * sizeof(uint32_t);
@@ -1724,8 +1732,20 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
             }
         }
         const uint32_t top = lo > kExactNear ? lo - kExactNear : 0;  // still to test: [0, top)
-        // (2) undecided candidates: the whole warp against the rest of the front
+        // (2) undecided candidates against the rest of the front: many (an early pass with
+        // a weak front) -> each lane scans its own, nearer points first, 4 tests per step;
+        // few -> the whole warp per candidate, 32 points per step
         unsigned hard = __ballot_sync(0xffffffffu, !dom && top > 0);
+        if (__popc(hard) >= kExactLaneMin) {
+            if (!dom && top > 0) {
+                uint32_t j = top;
+                for (; j >= 4 && !dom; j -= 4)
+                    dom = pdom(fget(j - 1), 0, x, 1) | pdom(fget(j - 2), 0, x, 1) | pdom(fget(j - 3), 0, x, 1) |
+                          pdom(fget(j - 4), 0, x, 1);
+                for (; j > 0 && !dom; j--) dom = pdom(fget(j - 1), 0, x, 1);
+            }
+            hard = 0;
+        }
         while (hard) {
             const int src = __ffs(hard) - 1;
             hard &= hard - 1;

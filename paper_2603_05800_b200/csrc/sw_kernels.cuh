@@ -927,63 +927,60 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;
 }
 
-// Quality bin tops and the q map of the DLT (one block, before dlt_build_kernel): the
-// front's quality values sorted (bitonic, in shared memory), the distinct ones -- all, or
+// Quality bin tops and the q map of the DLT (before dlt_build_kernel): the front's quality
+// values rank-sorted over the grid (rank = #smaller + #equal at a lower position, 16
+// threads per value), then the last block to finish takes the distinct ones -- all, or
 // kDltQ quantiles of them -- as tops.  Fronts above kDltSortMax points take kDltQ linear
 // tops over [qmin, qmax] instead (still exact: a column only ever counts f.q >= its top).
 constexpr uint32_t kDltSortMax = 16384;
 constexpr int kDltQThreads = 1024;
+constexpr int kDltQtopGrid = 64;  // the rank sort's blocks (64 values per block step)
 __global__ void __launch_bounds__(kDltQThreads) dlt_qtop_kernel(const PPoint* __restrict__ front,
-                                                                const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d) {
+                                                                const ParetoCtl* __restrict__ ctl, Dlt* __restrict__ d,
+                                                                uint32_t* __restrict__ qsorted,
+                                                                uint32_t* __restrict__ done) {
     extern __shared__ uint32_t qs[];  // kDltSortMax
     __shared__ uint32_t s_nd, s_qmin, s_qmax;
     __shared__ uint32_t s_wsum[32];
     __shared__ uint32_t s_top[kDltQ];
+    __shared__ uint32_t s_cnt[64];
+    __shared__ bool s_last;
     const uint32_t m = (uint32_t)ctl->front_n, tid = threadIdx.x;
-    uint32_t ntop = 0;
-    if (m > 0 && m <= kDltSortMax) {
-        uint32_t n2 = 1;
-        while (n2 < m) n2 <<= 1;
-        if (m <= (uint32_t)kDltQThreads) {  // one value per thread: rank sort, no barrier steps
-            uint32_t* src = qs + kDltSortMax / 2;
-            if (tid < m) src[tid] = front[tid].q;
-            else if (tid < ((m + 3) & ~3u)) src[tid] = 0xffffffffu;  // pad to whole 16 B loads (never counted)
+    const bool sortable = m > 0 && m <= kDltSortMax;
+    if (sortable) {  // (1) rank sort over the grid: 64 values per block step, 16 threads each
+        const uint32_t pl = tid % 64, part = tid / 64;
+        for (uint32_t base = blockIdx.x * 64; base < m; base += gridDim.x * 64) {
+            const uint32_t p = base + pl;
+            const uint32_t v = p < m ? __ldg(&front[p].q) : 0u;
+            if (tid < 64) s_cnt[tid] = 0;
             __syncthreads();
-            if (tid < m) {  // rank = #{j: q_j < v} + #{j < tid: q_j = v}, 4 values per 16 B load
-                const uint32_t v = src[tid];
-                uint32_t r = 0;
-                const uint4* s4 = reinterpret_cast<const uint4*>(src);
+            uint32_t r = 0;  // #{j: q_j < v} + #{j < p: q_j = v}
+            if (p < m)
 #pragma unroll 4
-                for (uint32_t j4 = 0; j4 < (m + 3) / 4; j4++) {
-                    const uint4 w = s4[j4];
-                    const uint32_t j = 4 * j4;
-                    r += (w.x < v || (w.x == v && j < tid)) ? 1u : 0u;
-                    r += (w.y < v || (w.y == v && j + 1 < tid)) ? 1u : 0u;
-                    r += (w.z < v || (w.z == v && j + 2 < tid)) ? 1u : 0u;
-                    r += (w.w < v || (w.w == v && j + 3 < tid)) ? 1u : 0u;
+                for (uint32_t j = part; j < m; j += kDltQThreads / 64) {
+                    const uint32_t w = __ldg(&front[j].q);
+                    r += (w < v || (w == v && j < p)) ? 1u : 0u;
                 }
-                qs[r] = v;
-            }
+            atomicAdd(&s_cnt[pl], r);
             __syncthreads();
-            n2 = 0;  // sorted: skip the network below
-        } else {
-            for (uint32_t i = tid; i < n2; i += blockDim.x) qs[i] = i < m ? front[i].q : 0xffffffffu;
+            if (tid < 64 && p < m) qsorted[s_cnt[tid]] = v;
             __syncthreads();
         }
-        for (uint32_t k = 2; k <= n2; k <<= 1)  // bitonic sort, ascending
-            for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-                for (uint32_t i = tid; i < n2; i += blockDim.x) {
-                    const uint32_t l = i ^ jj;
-                    if (l > i) {
-                        const uint32_t a = qs[i], b = qs[l];
-                        if (((i & k) == 0) ? (a > b) : (a < b)) {
-                            qs[i] = b;
-                            qs[l] = a;
-                        }
-                    }
-                }
-                __syncthreads();
-            }
+    }
+    // (2) the last block to finish derives the tops and the q map from the sorted values
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (tid == 0) *done = 0;  // re-armed for the next launch (stream-ordered)
+    __threadfence();
+    uint32_t ntop = 0;
+    if (sortable) {
+        for (uint32_t i = tid; i < m; i += blockDim.x) qs[i] = __ldcg(&qsorted[i]);
+        __syncthreads();
         // distinct values, compacted in place: thread tid owns kDltPer consecutive slots
         // (held in registers across the barrier), a block scan gives its output offset
         constexpr uint32_t kDltPer = kDltSortMax / kDltQThreads;
@@ -1612,7 +1609,6 @@ constexpr uint32_t kExactList = 128;    // per-warp survivor list
 constexpr int kExactThreads = 768;
 constexpr int kExactWarps = kExactThreads / 32;
 constexpr uint32_t kExactNear = 8;      // front points below x.t tested per lane first
-constexpr int kExactLaneMin = 6;        // undecided lanes from which each lane scans its own
 __host__ __device__ constexpr size_t exact_smem_bytes() {
     return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t)) +
            (size_t)kDltMap * sizeof(uint32_t);
@@ -1732,20 +1728,8 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
             }
         }
         const uint32_t top = lo > kExactNear ? lo - kExactNear : 0;  // still to test: [0, top)
-        // (2) undecided candidates against the rest of the front: many (an early pass with
-        // a weak front) -> each lane scans its own, nearer points first, 4 tests per step;
-        // few -> the whole warp per candidate, 32 points per step
+        // (2) undecided candidates (rare): the whole warp against the rest of the front
         unsigned hard = __ballot_sync(0xffffffffu, !dom && top > 0);
-        if (__popc(hard) >= kExactLaneMin) {
-            if (!dom && top > 0) {
-                uint32_t j = top;
-                for (; j >= 4 && !dom; j -= 4)
-                    dom = pdom(fget(j - 1), 0, x, 1) | pdom(fget(j - 2), 0, x, 1) | pdom(fget(j - 3), 0, x, 1) |
-                          pdom(fget(j - 4), 0, x, 1);
-                for (; j > 0 && !dom; j--) dom = pdom(fget(j - 1), 0, x, 1);
-            }
-            hard = 0;
-        }
         while (hard) {
             const int src = __ffs(hard) - 1;
             hard &= hard - 1;

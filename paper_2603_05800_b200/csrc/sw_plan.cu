@@ -90,6 +90,7 @@ struct sw_plan {
     PPoint* d_work = nullptr;  // front_cap + surv_cap
     PPoint* d_tmp = nullptr;   // front_cap + surv_cap (the merge's t-sorted input)
     uint32_t* d_rhist = nullptr;  // kRedBuckets (the merge's bucket sort)
+    uint32_t* d_qsort = nullptr;  // kDltSortMax + 1: the DLT's sorted front qualities, then its done counter
     uint8_t* d_keep = nullptr;
     ParetoCtl* d_ctl = nullptr;
     Dlt* d_dlt = nullptr;
@@ -738,6 +739,9 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if ((st = alloc_n(h, &h->d_tmp, h->front_cap + h->surv_cap, "pareto tmp")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_keep, h->front_cap + h->surv_cap, "pareto flags")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_rhist, kRedBuckets, "merge buckets")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_qsort, kDltSortMax + 1, "dlt quality sort")) < 0) return (st);
+    if (cudaMemsetAsync(h->d_qsort + kDltSortMax, 0, sizeof(uint32_t), h->stream) != cudaSuccess)
+        return (fail(nullptr, SW_ECUDA, "dlt counter init failed"));
     if ((st = alloc_n(h, &h->d_tmp2, h->front_cap + h->surv_cap, "pareto tmp2")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_surv, h->surv_cap, "pareto survivors")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_ctl, 1, "pareto ctl")) < 0) return (st);
@@ -781,7 +785,7 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
                         h->d_tmp,   h->d_keep,    h->d_ctl,     h->d_dlt,
                         h->d_partial, h->d_cand,  h->d_cand_all, h->d_detail, h->d_digest, h->d_selfjob,
                         h->d_counts, h->d_gather, h->d_tmp2, h->d_surv, h->d_gfeas, h->d_greedy,
-                        h->d_scand, h->d_scand_n, h->d_skey, h->d_dltc, h->d_rhist};
+                        h->d_scand, h->d_scand_n, h->d_skey, h->d_dltc, h->d_rhist, h->d_qsort};
         for (void* b : bufs) dev_free(h, b);
         cudaStreamSynchronize(h->stream);
         if (h->h_pass_surv) cudaFreeHost(h->h_pass_surv);
@@ -1154,7 +1158,8 @@ static ParetoArgs pareto_args(sw_plan* h) {
 // The DLT of the current front: quality tops + q map (one block), then the t edges, t map
 // and cells (kDltT blocks).
 static sw_status dlt_build_async(sw_plan* h) {
-    dlt_qtop_kernel<<<1, kDltQThreads, kDltSortMax * sizeof(uint32_t), h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
+    dlt_qtop_kernel<<<kDltQtopGrid, kDltQThreads, kDltSortMax * sizeof(uint32_t), h->stream>>>(
+        h->d_front, h->d_ctl, h->d_dlt, h->d_qsort, h->d_qsort + kDltSortMax);
     CKL(h);
     dlt_build_kernel<<<kDltQ, kDltBuildThreads, 0, h->stream>>>(h->d_front, h->d_ctl, h->d_dlt);
     CKL(h);

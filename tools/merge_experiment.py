@@ -20,12 +20,14 @@ def dominated_by(P, X):
     if len(P) == 0:
         return out
     pt, pc, pq = P["t"].astype(np.int64), P["c"].astype(np.int64), P["q"].astype(np.int64)
+    pi = P["idx"].astype(np.uint64)
     for s in range(0, len(X), 512):
         x = X[s:s + 512]
         xt, xc, xq = (x["t"].astype(np.int64)[:, None], x["c"].astype(np.int64)[:, None],
                       x["q"].astype(np.int64)[:, None])
+        xi = x["idx"].astype(np.uint64)[:, None]
         le = (pt[None] <= xt) & (pc[None] <= xc) & (pq[None] >= xq)
-        st = (pt[None] < xt) | (pc[None] < xc) | (pq[None] > xq)
+        st = (pt[None] < xt) | (pc[None] < xc) | (pq[None] > xq) | (pi[None] < xi)  # ties: lowest index
         out[s:s + 512] = (le & st).any(1)
     return out
 

@@ -1608,7 +1608,10 @@ constexpr uint32_t kExactFront = 2048;  // front points staged in smem (larger f
 constexpr uint32_t kExactList = 128;    // per-warp survivor list
 constexpr int kExactThreads = 768;
 constexpr int kExactWarps = kExactThreads / 32;
-constexpr uint32_t kExactNear = 8;      // front points below x.t tested per lane first
+#ifndef SW_EXACT_NEAR
+#define SW_EXACT_NEAR 16
+#endif
+constexpr uint32_t kExactNear = SW_EXACT_NEAR;  // front points below x.t tested per lane first
 __host__ __device__ constexpr size_t exact_smem_bytes() {
     return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t)) +
            (size_t)kDltMap * sizeof(uint32_t);
@@ -1720,12 +1723,13 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
                 if ((f_smem ? F.t[mid] : front[mid].t) <= x.t) lo = mid + 1;
                 else hi = mid;
             }
-            // (1) the nearest points below x.t
+            // (1) the nearest points below x.t, 4 independent tests per step
             const uint32_t stop = lo > kExactNear ? lo - kExactNear : 0;
-            for (uint32_t j = lo; j > stop && !dom;) {
-                j--;
-                dom = pdom(fget(j), 0, x, 1);
-            }
+            uint32_t j = lo;
+            for (; j >= stop + 4 && !dom; j -= 4)
+                dom = pdom(fget(j - 1), 0, x, 1) | pdom(fget(j - 2), 0, x, 1) | pdom(fget(j - 3), 0, x, 1) |
+                      pdom(fget(j - 4), 0, x, 1);
+            for (; j > stop && !dom; j--) dom = pdom(fget(j - 1), 0, x, 1);
         }
         const uint32_t top = lo > kExactNear ? lo - kExactNear : 0;  // still to test: [0, top)
         // (2) undecided candidates (rare): the whole warp against the rest of the front

@@ -877,9 +877,8 @@ struct Dlt {
     uint32_t cshift, pad_[3];
     uint64_t tedge[kDltT + 1];
     // t map cell k: lo = #edges <= the cell's lower end, hi = #edges <= its upper end
-    // (packed lo | hi << 8).  A record's bin count is hi when t >= tedge[hi - 1] (the
-    // cell's largest edge), else lo -- exact also when many front points share one t
-    // (e.g. every stall-free plan behind a static intro)
+    // (packed lo | hi << 8).  A record's bin count is exact: lo or hi by one compare when
+    // the cell holds at most one edge, else a search of tedge[lo, hi)
     uint16_t tmap[kDltMap];
     // cell[b1][j] (row b1 = t bin + 1, column j = q bin): min cost >> cshift, rounded down;
     // 0xffff = none.  Row 0 (no front point has t <= the record's t) and column kDltQ (q
@@ -921,7 +920,21 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     const uint32_t j = q > qm.x ? hiq : loq;  // #tops < q (column; kDltQ = none)
     const uint32_t lh = d.tmap[kc];
     const uint32_t lo = lh & 0xffu, hi = lh >> 8;
-    const uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;  // t bin + 1
+    // t bin + 1 = #edges <= t: one compare when the map cell holds at most one edge, else a
+    // search of the cell's edges (a map cell is 1/128 octave; where the front is dense in t
+    // it holds several -- answering "lo" there let ~4x more records through on C3)
+    uint32_t b1;
+    if (hi <= lo + 1) {
+        b1 = (hi > lo && t >= d.tedge[lo]) ? hi : lo;
+    } else {
+        uint32_t a = lo, e = hi;
+        while (a < e) {
+            const uint32_t mid = (a + e) >> 1;
+            if (d.tedge[mid] <= t) a = mid + 1;
+            else e = mid;
+        }
+        b1 = a;
+    }
     const uint32_t cell = d.cell[b1 * kDltCols + j];
     const uint64_t cs = c >> hs.cshift;
     return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;

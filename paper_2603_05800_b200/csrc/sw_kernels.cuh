@@ -910,16 +910,9 @@ struct DltHot {
     uint32_t qbase, qmshift, cshift;
 };
 
-// EXACT = false (the scans' hot loops): branch-free, the t bin is exact when the record's
-// map cell holds at most one edge, else row lo (conservative: fewer front points).
-// EXACT = true (the deferred exact test, on the few records that passed the scan): the t
-// bin by a search of the cell's edges -- a map cell is 1/128 octave and where the front is
-// dense in t it holds several; row lo let ~4x more records through on C3
-// (tools/dlt_experiment.py), but searching in the scan itself slowed it by 15-20%.
-template <bool EXACT = false>
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
-    // check-free: the map's cell 0 lies below the front's smallest t (so a clamped t below
-    // it gets row 0), column kDltQ catches q above the front's
+    // check-free: the map's cell 0 lies below the front's smallest t (so a
+    // clamped t below it gets row 0), column kDltQ catches q above the front's
     const int32_t k = dlt_tkey(t) - hs.kbase;
     const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
     const uint2 qm = d.qmap[min((max(q, hs.qbase) - hs.qbase) >> hs.qmshift, (uint32_t)kDltQMap - 1)];
@@ -927,19 +920,23 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     const uint32_t j = q > qm.x ? hiq : loq;  // #tops < q (column; kDltQ = none)
     const uint32_t lh = d.tmap[kc];
     const uint32_t lo = lh & 0xffu, hi = lh >> 8;
-    uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;  // t bin + 1
-    if (EXACT && hi > lo + 1) {  // #edges <= t within the cell's edges [lo, hi)
-        uint32_t a = lo, e = hi;
-        while (a < e) {
-            const uint32_t mid = (a + e) >> 1;
-            if (d.tedge[mid] <= t) a = mid + 1;
-            else e = mid;
-        }
-        b1 = a;
-    }
-    const uint32_t cell = d.cell[b1 * kDltCols + j];
+    // t bin + 1 = #edges <= t: exact by one compare when the map cell holds at most one
+    // edge; else row lo first (conservative: fewer front points) and, only for the rare
+    // records row lo does not rule out, a search of the cell's edges (a map cell is 1/128
+    // octave; where the front is dense in t it holds several -- stopping at row lo let ~4x
+    // more records through on C3; searching for every record slowed the scan by 20%)
+    const uint32_t b1 = (hi == lo + 1 && t >= d.tedge[lo]) ? hi : lo;
     const uint64_t cs = c >> hs.cshift;
-    return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;
+    const uint32_t cq = (uint32_t)(cs < 0xffffull ? cs : 0xffffull);
+    if (cq > d.cell[b1 * kDltCols + j]) return true;
+    if (hi <= lo + 1) return false;
+    uint32_t a = lo, e = hi;
+    while (a < e) {
+        const uint32_t mid = (a + e) >> 1;
+        if (d.tedge[mid] <= t) a = mid + 1;
+        else e = mid;
+    }
+    return cq > d.cell[a * kDltCols + j];
 }
 
 // Quality bin tops and the q map of the DLT (before dlt_build_kernel): the front's quality
@@ -1661,8 +1658,7 @@ __device__ __forceinline__ PArrays parrays(unsigned char* base, uint32_t n) {
 
 __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PPoint* __restrict__ cand, uint64_t cand_cap,
                                                                         const PPoint* __restrict__ front, ParetoCtl* ctl,
-                                                                        PPoint* __restrict__ surv, uint64_t surv_cap,
-                                                                        const Dlt* __restrict__ dlt) {
+                                                                        PPoint* __restrict__ surv, uint64_t surv_cap) {
     extern __shared__ __align__(16) unsigned char xsm[];
     const PArrays F = parrays(xsm, kExactFront);
     const unsigned long long nd = ctl->dlt_n;
@@ -1706,7 +1702,6 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const PArrays L = parrays(xsm + (size_t)kExactFront * 28 + (size_t)warp * kExactList * 28, kExactList);
-    const DltHot dh{dlt->kbase, dlt->qbase, dlt->qmshift, dlt->cshift};
     auto fget = [&](uint32_t j) { return f_smem ? F.get(j) : front[j]; };
     // this warp's run of the block's range
     const uint64_t w0 = r0 + (r1 - r0) * warp / kExactWarps, w1 = r0 + (r1 - r0) * (warp + 1) / kExactWarps;
@@ -1728,11 +1723,6 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
         bool dom = !valid;
         if (valid) {
             x = cand[i];
-            // (0) the pass's DLT again with the exact t bin (from L1/L2): most candidates the
-            // scan's conservative lookup let through end here
-            dom = dlt_dominated<true>(*dlt, dh, x.t, x.c, x.q);
-        }
-        if (valid && !dom) {
             uint32_t hi = m;  // lo = #front points with t <= x.t
             if (f_smem) {  // narrowed by the position map (t below the front's smallest: lo = 0)
                 const int32_t k = dlt_tkey(x.t) - pkbase;

@@ -877,8 +877,9 @@ struct Dlt {
     uint32_t cshift, pad_[3];
     uint64_t tedge[kDltT + 1];
     // t map cell k: lo = #edges <= the cell's lower end, hi = #edges <= its upper end
-    // (packed lo | hi << 8).  A record's bin count is exact: lo or hi by one compare when
-    // the cell holds at most one edge, else a search of tedge[lo, hi)
+    // (packed lo | hi << 8).  A record's bin count is hi when t >= tedge[hi - 1] (the
+    // cell's largest edge), else lo -- exact also when many front points share one t
+    // (e.g. every stall-free plan behind a static intro)
     uint16_t tmap[kDltMap];
     // cell[b1][j] (row b1 = t bin + 1, column j = q bin): min cost >> cshift, rounded down;
     // 0xffff = none.  Row 0 (no front point has t <= the record's t) and column kDltQ (q
@@ -911,7 +912,7 @@ struct DltHot {
 };
 
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
-    // check-free: the map's cell 0 lies below the front's smallest t (so a
+    // branch-free and check-free: the map's cell 0 lies below the front's smallest t (so a
     // clamped t below it gets row 0), column kDltQ catches q above the front's
     const int32_t k = dlt_tkey(t) - hs.kbase;
     const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
@@ -920,23 +921,10 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     const uint32_t j = q > qm.x ? hiq : loq;  // #tops < q (column; kDltQ = none)
     const uint32_t lh = d.tmap[kc];
     const uint32_t lo = lh & 0xffu, hi = lh >> 8;
-    // t bin + 1 = #edges <= t: exact by one compare when the map cell holds at most one
-    // edge; else row lo first (conservative: fewer front points) and, only for the rare
-    // records row lo does not rule out, a search of the cell's edges (a map cell is 1/128
-    // octave; where the front is dense in t it holds several -- stopping at row lo let ~4x
-    // more records through on C3; searching for every record slowed the scan by 20%)
-    const uint32_t b1 = (hi == lo + 1 && t >= d.tedge[lo]) ? hi : lo;
+    const uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;  // t bin + 1
+    const uint32_t cell = d.cell[b1 * kDltCols + j];
     const uint64_t cs = c >> hs.cshift;
-    const uint32_t cq = (uint32_t)(cs < 0xffffull ? cs : 0xffffull);
-    if (cq > d.cell[b1 * kDltCols + j]) return true;
-    if (hi <= lo + 1) return false;
-    uint32_t a = lo, e = hi;
-    while (a < e) {
-        const uint32_t mid = (a + e) >> 1;
-        if (d.tedge[mid] <= t) a = mid + 1;
-        else e = mid;
-    }
-    return cq > d.cell[a * kDltCols + j];
+    return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;
 }
 
 // Quality bin tops and the q map of the DLT (before dlt_build_kernel): the front's quality

@@ -129,7 +129,7 @@ __global__ void pack_kernel(RawDesc raw, DevHeader* __restrict__ hdr, VaEntry* _
 }
 
 #ifndef SW_LSD_UNROLL
-#define SW_LSD_UNROLL 1  // (experiments: tools/build_variant.py)
+#define SW_LSD_UNROLL 2  // 1 and 4 measured 1-2% slower (eval C2, C5; tools/build_variant.py)
 #endif
 constexpr int kLsdUnroll = SW_LSD_UNROLL;
 // ============================================================================ LSD fast path

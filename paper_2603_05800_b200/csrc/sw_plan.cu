@@ -112,7 +112,7 @@ struct sw_plan {
     // (cached or collective) branch whatever its local refolds did
     uint64_t gepoch = 1;
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
-    uint32_t fold_kmin = 2;      // SW_FOLD_KMIN: fewest strided fold levels (passes - 1) of a large segment
+    uint32_t fold_kmin = 1;      // SW_FOLD_KMIN: fewest strided fold levels (passes - 1); a first pass stays <= ~8 M records
     const char* dump_merge = nullptr;  // SW_DUMP_MERGE=<prefix>: every fold merge's input -> <prefix>_<n>.bin
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
     uint32_t coop_grid = 0;
@@ -1686,6 +1686,16 @@ extern "C" sw_status sw_plan_sweep(sw_plan* h, uint64_t begin, uint64_t end, uin
     for (uint32_t q = 0; q < nq; q++) {
         if (front_ok && front_query(h, qs[q])) fi[nf++] = q;
         else qsn[ns] = qs[q], si[ns++] = q;
+    }
+    if (front_ok && nf && end - begin <= chunk && !digest) {
+        // one chunk: the front after its fold covers exactly [begin, end), so every query
+        // goes through one select (front-answerable ones from that front, one readback)
+        sw_status st = sw_plan_eval(h, begin, end);
+        if (st < 0) return st;
+        const sw_status sel = select_impl(h, nq, qs, out, true);
+        if (sel < 0) return sel;
+        if ((st = sw_plan_release_records(h)) < 0) return st;
+        return sel;
     }
     for (uint64_t c0 = begin; c0 < end;) {
         const uint64_t c1 = end - c0 > chunk ? c0 + chunk : end;

@@ -26,6 +26,9 @@ for t in $NCU; do
     eval) cap ${TAG}_eval_$c eval_kernel 2 python tools/one_step.py $c 3 ;;
     scan) cap ${TAG}_scan_$c scan_kernel ${SCAN_SKIP:-8} python tools/one_step.py $c 3 ;;
     exact) cap ${TAG}_exact_$c pareto_exact_kernel 5 python tools/one_step.py $c 3 ;;
+    eval5) cap ${TAG}_eval_C5 eval_kernel 2 python tools/one_step_c5.py ;;
+    scan5) cap ${TAG}_scan_C5 scan_kernel 8 python tools/one_step_c5.py
+        SW_DEBUG=1 timeout 300 python tools/one_step_c5.py > gpurun_out/${TAG}_debug_C5chunk.txt 2>&1 ;;
     stream) cap ${TAG}_stream_$c stream_kernel 3 python tools/stream_one.py $c ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_$c.csv \
         python bench.py --config $c --configs "" --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --stream-steps 0 > gpurun_out/${TAG}_ncu_launch_$c.log 2>&1

@@ -54,8 +54,13 @@ def dlt_pass(F, t, c, q, nt=255, nq=128, t_distinct=False, tmap=False):
         hi = np.searchsorted(te, U, side="right")
         lo_k, hi_k = lo[k], hi[k]
         b1 = np.where((hi_k > lo_k) & (t >= te[np.maximum(hi_k - 1, 0)]), hi_k, lo_k)
-        if tmap == "exact":  # round 2: a search of the cell's edges when it holds several
+        if tmap == "exact":  # a search of the cell's edges when it holds several
             b1 = np.where(hi_k > lo_k + 1, np.searchsorted(te, t, side="right"), b1)
+        if tmap == "three":  # branch-free: the cell's first three edges, then its last
+            sp = hi_k - lo_k
+            tt = lambda i: te[np.minimum(i, len(te) - 1)]
+            b1 = lo_k + ((sp >= 1) & (t >= tt(lo_k))) + ((sp >= 2) & (t >= tt(lo_k + 1))) + ((sp >= 3) & (t >= tt(lo_k + 2)))
+            b1 = np.where((sp > 3) & (t >= te[np.maximum(hi_k - 1, 0)]), hi_k, b1)
     col = np.searchsorted(tops, q, side="left")
     cs = np.minimum(c >> csh, 0xffff)
     return ~(cs > cell[b1, col])
@@ -82,7 +87,7 @@ def main():
     dom = exact_dominated(F, t, c, q)
     print("records %d, front %d (distinct t %d, q %d); dominated by the front: %d (%.2f%%)" % (
         len(t), fn, len(np.unique(F["t"])), len(np.unique(F["q"])), dom.sum(), 100 * dom.mean()))
-    for name, kw in (("v5 255x128", {}), ("v5 + round-1 t map", {"tmap": True}), ("v5 + exact t map", {"tmap": "exact"}), ("t distinct 255x128", {"t_distinct": True}),
+    for name, kw in (("v5 255x128", {}), ("v5 + round-1 t map", {"tmap": True}), ("v5 + exact t map", {"tmap": "exact"}), ("v5 + 3-edge t map", {"tmap": "three"}), ("t distinct 255x128", {"t_distinct": True}),
                      ("255x256", {"nq": 256}), ("t distinct 255x256", {"t_distinct": True, "nq": 256}),
                      ("511x128", {"nt": 511}), ("t distinct 511x64", {"t_distinct": True, "nt": 511, "nq": 64})):
         p = dlt_pass(F, t, c, q, **kw)

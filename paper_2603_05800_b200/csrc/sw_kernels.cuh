@@ -877,10 +877,9 @@ struct Dlt {
     uint32_t cshift, pad_[3];
     uint64_t tedge[kDltT + 1];
     // t map cell k: lo = #edges <= the cell's lower end, hi = #edges <= its upper end
-    // (packed lo | hi << 8).  A record's bin count: lo plus the cell's first three edges
-    // <= t, or hi when t >= the cell's largest edge -- exact for cells of <= 3 edges and
-    // also when many front points share one t (e.g. every stall-free plan behind a static
-    // intro)
+    // (packed lo | hi << 8).  A record's bin count is hi when t >= tedge[hi - 1] (the
+    // cell's largest edge), else lo -- exact also when many front points share one t
+    // (e.g. every stall-free plan behind a static intro)
     uint16_t tmap[kDltMap];
     // cell[b1][j] (row b1 = t bin + 1, column j = q bin): min cost >> cshift, rounded down;
     // 0xffff = none.  Row 0 (no front point has t <= the record's t) and column kDltQ (q
@@ -912,10 +911,6 @@ struct DltHot {
     uint32_t qbase, qmshift, cshift;
 };
 
-// FINE: the t bin from the map cell's first three edges too (below); else from its last
-// edge only (2 fewer shared loads -- the C2 scan is at the edge of issue-bound, where the
-// fine lookup cost 15%; scans switch per warp when their DLT pass rate is high)
-template <bool FINE = false>
 __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c, uint32_t q) {
     // branch-free and check-free: the map's cell 0 lies below the front's smallest t (so a
     // clamped t below it gets row 0), column kDltQ catches q above the front's
@@ -926,17 +921,7 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     const uint32_t j = q > qm.x ? hiq : loq;  // #tops < q (column; kDltQ = none)
     const uint32_t lh = d.tmap[kc];
     const uint32_t lo = lh & 0xffu, hi = lh >> 8;
-    // t bin + 1 = #edges <= t, branch-free: the map cell's first three edges, then its last
-    // (exact for cells of <= 3 edges; a cell is 1/128 octave and where the front is dense in
-    // t it holds several -- round 1 compared only the last one, which let ~4x more records
-    // through on C3: tools/dlt_experiment.py)
-    const uint32_t sp = hi - lo;
-    uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;
-    if (FINE)
-        b1 = (sp > 3u && t >= d.tedge[hi - 1])
-                 ? hi
-                 : lo + ((sp >= 1u) & (t >= d.tedge[lo])) + ((sp >= 2u) & (t >= d.tedge[min(lo + 1, (uint32_t)kDltT)])) +
-                       ((sp >= 3u) & (t >= d.tedge[min(lo + 2, (uint32_t)kDltT)]));
+    const uint32_t b1 = (hi > lo && t >= d.tedge[hi > 0 ? hi - 1 : 0]) ? hi : lo;  // t bin + 1
     const uint32_t cell = d.cell[b1 * kDltCols + j];
     const uint64_t cs = c >> hs.cshift;
     return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;
@@ -1963,8 +1948,6 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     __syncthreads();
     DltHot dh{0, 0, 0, 0};
     if (PARETO) dh = DltHot{d.kbase, d.qbase, d.qmshift, d.cshift};
-    bool fine = false;             // this warp's DLT lookup: the fine t bin (dlt_dominated)
-    uint32_t w_seen = 0, w_pass = 0;  // records this warp looked up / let through
     const uint32_t per_tile = (uint32_t)(kTileRows * v.row);
     const uint64_t total = v.ntiles * per_tile;
     // stage sg of this view/pass -> flat slot of its first record (kInf64: none)
@@ -2140,20 +2123,9 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
             }
             if (PARETO) {
                 uint32_t keepm = 0;  // DLT survivors, all kRPT lookups first (independent: ILP)
-                if (fine) {
 #pragma unroll
-                    for (int u = 0; u < kRPT; u++)
-                        keepm |= (uint32_t)(valid[u] &
-                                            !dlt_dominated<true>(d, dh, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u])))
-                                 << u;
-                } else {
-#pragma unroll
-                    for (int u = 0; u < kRPT; u++)
-                        keepm |= (uint32_t)(valid[u] &
-                                            !dlt_dominated<false>(d, dh, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u])))
-                                 << u;
-                }
-                w_seen += 32 * kRPT;
+                for (int u = 0; u < kRPT; u++)
+                    keepm |= (uint32_t)(valid[u] & !dlt_dominated(d, dh, r[u].w0 + r[u].w1, r[u].w2, rec_Q(r[u]))) << u;
                 if (!__any_sync(0xffffffffu, keepm != 0)) continue;
                 // deferred exact test: the stage's DLT survivors (rare) are appended to the
                 // pass's candidate buffer -- one atomic per warp -- and tested after the pass
@@ -2169,9 +2141,6 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 if (lane == 31) base = atomicAdd(&pa.ctl->dlt_n, (unsigned long long)incl);
                 base = __shfl_sync(0xffffffffu, base, 31);
                 uint64_t slot = base + incl - mine;
-                // a warp whose DLT pass rate stays above 1/256 switches to the fine t bin
-                w_pass += __shfl_sync(0xffffffffu, incl, 31);
-                fine |= w_seen >= 8192u && w_pass * 256u > w_seen;
 #pragma unroll
                 for (int u = 0; u < kRPT; u++) {
                     if (!((keepm >> u) & 1u)) continue;

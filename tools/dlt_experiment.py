@@ -8,15 +8,15 @@ import numpy as np
 from merge_experiment import load
 
 
-def tkey(t):
-    """float32 bits of t rounded toward zero, >> 16 (the device's dlt_tkey)."""
+def tkey(t, sh=16):
+    """float32 bits of t rounded toward zero, >> sh (the device's dlt_tkey: sh = 16)."""
     f = t.astype(np.float64).astype(np.float32)
     over = f.astype(np.float64) > t.astype(np.float64)
     f[over] = np.nextafter(f[over], np.float32(0))
-    return (f.view(np.uint32) >> 16).astype(np.int64)
+    return (f.view(np.uint32) >> sh).astype(np.int64)
 
 
-def dlt_pass(F, t, c, q, nt=255, nq=128, t_distinct=False, tmap=False):
+def dlt_pass(F, t, c, q, nt=255, nq=128, t_distinct=False, tmap=False, tsh=16, ncell=2048):
     m = len(F)
     Ft, Fc, Fq = F["t"].astype(np.int64), F["c"].astype(np.int64), F["q"].astype(np.int64)
     if t_distinct:
@@ -40,11 +40,11 @@ def dlt_pass(F, t, c, q, nt=255, nq=128, t_distinct=False, tmap=False):
                 cell[b + 1, j] = Fc[s2].min() >> csh
     b1 = np.searchsorted(te, t, side="right")
     if tmap:  # the device's 2048-cell direct map: (lo, hi) per cell, hi only if t >= edge[hi-1]
-        kbase = tkey(Ft[:1])[0] - 1
-        k = np.clip(tkey(t) - kbase, 0, 2047)
-        ks = np.arange(2048) + kbase
+        kbase = tkey(Ft[:1], tsh)[0] - 1
+        k = np.clip(tkey(t, tsh) - kbase, 0, ncell - 1)
+        ks = np.arange(ncell) + kbase
         def lower_end(kk):
-            v = (kk.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+            v = (kk.astype(np.uint32) << tsh).view(np.float32).astype(np.float64)
             return np.ceil(v).astype(np.int64)
         L = lower_end(ks)
         Ln = lower_end(ks + 1)
@@ -87,7 +87,10 @@ def main():
     dom = exact_dominated(F, t, c, q)
     print("records %d, front %d (distinct t %d, q %d); dominated by the front: %d (%.2f%%)" % (
         len(t), fn, len(np.unique(F["t"])), len(np.unique(F["q"])), dom.sum(), 100 * dom.mean()))
-    for name, kw in (("v5 255x128", {}), ("v5 + round-1 t map", {"tmap": True}), ("v5 + exact t map", {"tmap": "exact"}), ("v5 + 3-edge t map", {"tmap": "three"}), ("t distinct 255x128", {"t_distinct": True}),
+    for name, kw in (("v5 255x128", {}), ("v5 + round-1 t map", {"tmap": True}), ("v5 + exact t map", {"tmap": "exact"}), ("v5 + 3-edge t map", {"tmap": "three"}),
+                     ("v5 + t map 1/256 oct", {"tmap": True, "tsh": 15, "ncell": 4096}),
+                     ("v5 + t map 1/512 oct", {"tmap": True, "tsh": 14, "ncell": 8192}),
+                     ("v5 + t map 1/1024 oct", {"tmap": True, "tsh": 13, "ncell": 16384}), ("t distinct 255x128", {"t_distinct": True}),
                      ("255x256", {"nq": 256}), ("t distinct 255x256", {"t_distinct": True, "nq": 256}),
                      ("511x128", {"nt": 511}), ("t distinct 511x64", {"t_distinct": True, "nt": 511, "nq": 64})):
         p = dlt_pass(F, t, c, q, **kw)

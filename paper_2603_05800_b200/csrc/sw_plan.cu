@@ -112,6 +112,7 @@ struct sw_plan {
     // (cached or collective) branch whatever its local refolds did
     uint64_t gepoch = 1;
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
+    uint64_t first_pass = 8ull << 20;  // SW_FIRST_PASS: records of the first strided fold pass (about)
     uint32_t fold_kmin = 1;      // SW_FOLD_KMIN: fewest strided fold levels (passes - 1); a first pass stays <= ~8 M records
     const char* dump_merge = nullptr;  // SW_DUMP_MERGE=<prefix>: every fold merge's input -> <prefix>_<n>.bin
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
@@ -692,6 +693,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     h->dump_merge = getenv("SW_DUMP_MERGE");
+    if (const char* ev = getenv("SW_FIRST_PASS")) h->first_pass = std::max<uint64_t>(1 << 16, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FOLD_KMIN")) h->fold_kmin = (uint32_t)std::min(std::max(atoi(ev), 1), 9);
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
     if (const char* ev = getenv("SW_COOP_REDUCE")) h->coop_reduce = atoi(ev) != 0;
@@ -1258,7 +1260,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
     const uint64_t total = g.ntiles * per_tile;
     const uint64_t nunits = (total + unit_recs - 1) / unit_recs;
     // K levels: the first pass covers about kFirstPass records (>= 1/64 of the segment)
-    const uint64_t kFirstPass = 8ull << 20;
+    const uint64_t kFirstPass = h->first_pass;
     uint32_t K = h->fold_kmin;
     while (K < 10 && (nunits >> (3 * K)) * unit_recs > kFirstPass) K++;
     const bool strided = nunits >= 256;

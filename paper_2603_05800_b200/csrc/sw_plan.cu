@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -225,6 +226,31 @@ Coll coll_of(const sw_plan* h) {
         sw_status s_ = coll_sync(coll_of(h), &why_);                                          \
         if (s_ != SW_OK) return fail((h), s_, "stream synchronisation failed: %s (%s:%d)", why_, __FILE__, __LINE__); \
     } while (0)
+
+// Timing events outlive handles: a process-wide pool (per device), filled lazily and
+// refilled at destroy -- 128 cudaEventCreate + cudaEventDestroy per handle were about a
+// third of an end-to-end step's create/destroy host time.
+namespace {
+std::mutex g_ev_mu;
+std::vector<std::pair<int, cudaEvent_t>> g_ev_free;
+cudaError_t event_get(int dev, cudaEvent_t* e) {
+    {
+        std::lock_guard<std::mutex> g(g_ev_mu);
+        for (size_t i = g_ev_free.size(); i-- > 0;)
+            if (g_ev_free[i].first == dev) {
+                *e = g_ev_free[i].second;
+                g_ev_free[i] = g_ev_free.back();
+                g_ev_free.pop_back();
+                return cudaSuccess;
+            }
+    }
+    return cudaEventCreate(e);
+}
+void event_put(int dev, cudaEvent_t e) {  // the handle's stream is idle (synchronised)
+    std::lock_guard<std::mutex> g(g_ev_mu);
+    g_ev_free.push_back({dev, e});
+}
+}  // namespace
 
 void* dev_alloc(sw_plan* h, size_t bytes) {
     if (bytes == 0) bytes = 16;
@@ -771,7 +797,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if (cudaMemsetAsync(h->d_ctl, 0, sizeof(ParetoCtl), h->stream) != cudaSuccess)
         return (fail(nullptr, SW_ECUDA, "ctl init failed"));
     for (int i = 0; i < 2 * sw_plan::kEvPairs; i++)
-        if (cudaEventCreate(&h->ev[i]) != cudaSuccess) return (fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
+        if (event_get(h->device, &h->ev[i]) != cudaSuccess) return (fail(nullptr, SW_ECUDA, "cudaEventCreate failed"));
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
         cudaGetLastError();
         return (fail(nullptr, SW_ECUDA, "create: device work failed"));
@@ -792,7 +818,7 @@ extern "C" sw_status sw_plan_destroy(sw_plan* h) {
         cudaStreamSynchronize(h->stream);
         if (h->h_pass_surv) cudaFreeHost(h->h_pass_surv);
         for (cudaEvent_t e : h->ev)
-            if (e) cudaEventDestroy(e);
+            if (e) event_put(h->device, e);
         if (h->shared) {
             for (sw_plan* r : h->shared->reqs) sw_plan_destroy(r);
             cudaFree(h->shared->d_dev);

@@ -54,10 +54,11 @@ def test_stream_random_problems(sw, oracle_mod, seed):
         assert plan.pareto() == f
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C2x", "C3", "C5"])
 def test_stream_full_space(sw, cfg):
-    """The configs' full spaces (C2: 4.3e8 plans) with a record capacity of 1024: the
-    paper-shaped queries' winners and the front equal the oracle's (golden)."""
+    """The configs' full spaces (C2: 4.3e8 plans; C5: 1.2e10 plans, whole-space golden) with
+    a record capacity of 1024: the paper-shaped queries' winners and the front equal the
+    oracle's (golden); C2x runs the paper's COST_X_TTFF objective."""
     pb = make_config(cfg)
     g = _golden(cfg)
     with sw.Plan(pb, record_capacity=1024) as plan:

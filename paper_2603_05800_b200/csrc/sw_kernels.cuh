@@ -2295,9 +2295,19 @@ struct StreamEmit {
             const uint64_t idx = base + dl;
             const bool valid = live && (!e->edge || (idx >= a.ib && idx < a.ie));
             const uint32_t obj = a.P.objective;
-            // ---- a9: which records can still beat what was reported?  (Keys only rise:
-            // a record below the smallest key of the tile's start passes no query.)
-            const bool pre = !e->allf || (valid && prune_key(obj, r) >= e->kmin);
+            // ---- a9: which records can still beat what was reported?  Once every query has
+            // a feasible report: only a record feasible for some query q with a pruning key
+            // >= q's (keys only rise, so a stale read is a weaker filter, never a wrong one)
+            bool pre = valid;
+            if (e->allf) {
+                const uint64_t key = prune_key(obj, r);
+                bool any = false;
+                for (uint32_t q = 0; q < a.P.nq; q++) {
+                    const QueryDev& Q = S.q[q];
+                    any |= (key >= S.key[q]) & (r.w2 <= Q.budget) & (r.w0 <= Q.slo_t) & (r.w1 <= Q.slo_s);
+                }
+                pre &= any;
+            }
             const uint32_t nq = __any_sync(0xffffffffu, pre) ? a.P.nq : 0u;
             for (uint32_t q = 0; q < nq; q++) {
                 const QueryDev Q = S.q[q];
@@ -2364,7 +2374,10 @@ struct StreamEmit {
 };
 
 // registers: the eval path plus the in-kernel filters (2 blocks/SM only for one pool)
-__host__ __device__ constexpr int stream_min_blocks(int np, int bm) { return (np == 1 && bm < 2) ? 2 : 1; }
+#ifndef SW_STREAM_MINB1
+#define SW_STREAM_MINB1 2
+#endif
+__host__ __device__ constexpr int stream_min_blocks(int np, int bm) { return (np == 1 && bm < 2) ? SW_STREAM_MINB1 : 1; }
 
 // BM: the eval path (eval_mode) at compile time, as in eval_kernel.
 template <int NP, int BM>

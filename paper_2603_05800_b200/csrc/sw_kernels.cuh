@@ -9,6 +9,7 @@
 // digest_kernel   : order-independent record digest (full-space parity tool)
 #pragma once
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "sw_device.cuh"
 
@@ -258,7 +259,9 @@ __device__ __forceinline__ void lsd_fast(const DevHeader& h, const State<NP>& st
             put(E.dl, E.dl * (kTileRows * (uint32_t)sizeof(Rec4)), r);  // a7 store, or the stream filter
         };
         if (mode == 0) {
-#pragma unroll kLsdUnroll
+            // the eval store unrolls (ILP); the stream filter does not (registers)
+            constexpr int kUnr = std::decay_t<Put>::kUnroll;
+#pragma unroll kUnr
             for (uint32_t j = j0; j < j1; j++) {
                 const LsdEntry E = h.lsd[j];
                 const uint64_t cnew = U1 + E.x1 + ((uint32_t)E.x2 >= Dm ? 1u : 0u);
@@ -452,6 +455,7 @@ struct StoreEmit {
     Rec4* tile_out;  // this lane's first slot in its tile
     uint32_t rl;
     struct Put {
+        static constexpr int kUnroll = kLsdUnroll;
         char* lane_out;
         __device__ __forceinline__ void operator()(uint32_t, uint32_t off, const Rec4& r) const {
             st_global_256(lane_out + off, r);
@@ -2285,6 +2289,7 @@ struct StreamEmit {
     bool allf;         // at the tile's start every query had a feasible report ...
     unsigned long long kmin;  // ... and this was the smallest of their pruning keys
     struct Put {
+        static constexpr int kUnroll = 1;
         const StreamEmit* e;
         uint64_t base;  // index of candidate (dm, 0)
         bool live;

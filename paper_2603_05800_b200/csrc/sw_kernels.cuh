@@ -354,10 +354,14 @@ struct EvalJob {
 // block has several scenes (or starts at scene 0) or that have DiT/VAE disaggregated
 // choices (R37); the fast path (single-pool MID copy + lsd_fast) is a separate
 // instantiation, so neither carries the other's code or registers.
+// [slice of nslice]: only the MID digits [slice rm / nslice, (slice + 1) rm / nslice) (the
+// stream kernel splits small passes' tiles so that they fill the GPU).
 template <int NP, bool BUSY, bool DIS, class Emit>
-__device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit) {
+__device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* va, uint64_t t, Emit&& emit,
+                                            uint32_t slice = 0, uint32_t nslice = 1) {
     const uint32_t bm = h.B - 2, bl = h.B - 1;
     const uint32_t rm = h.radix[bm], rl = h.radix[bl];
+    const uint32_t dm0 = slice * rm / nslice, dm1 = (slice + 1) * rm / nslice;
     const uint32_t mfirst = h.first[bm], mlast = h.first[bm + 1];
     const uint32_t lfirst = h.first[bl], llast = h.first[bl + 1];
     const uint64_t n_rows = h.n_rows;
@@ -398,7 +402,7 @@ __device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* v
     if (DIS) {
         // ---- DiT/VAE disaggregated choices (R37) touch two pools per scene: MID and LSD
         // digits on full state copies (no single-pool MID copy, no LSD fast path)
-        for (uint32_t dm = 0; dm < rm; dm++) {
+        for (uint32_t dm = dm0; dm < dm1; dm++) {
             State<NP> s2 = st;
             const uint32_t chm = h.choice[h.coff[bm] + dm];
             run_block_uniform<NP, BUSY>(s2, h, chm, mfirst, mlast, va + h.voff[bm] + dm, rm);
@@ -418,7 +422,7 @@ __device__ __forceinline__ void eval_tile_b(const DevHeader& h, const VaEntry* v
         return;
     }
     // ---- MID digit: warp-uniform choice (k, pm) on a copy of pool pm only
-    for (uint32_t dm = 0; dm < rm; dm++) {
+    for (uint32_t dm = dm0; dm < dm1; dm++) {
         const uint32_t ch = h.choice[h.coff[bm] + dm];
         const uint32_t k = ch_k(ch), pm = ch_pool(ch);
         MidState m;
@@ -2249,6 +2253,7 @@ struct StreamArgs {
     // (lvl 0 = tiles u with u % 8^K == 0; lvl l >= 1 = multiples of 8^(K-l), not of 8^(K-l+1))
     uint32_t levels, lvl;
     uint64_t ntiles_pass;  // tiles in this pass
+    uint32_t msplit;       // work items per tile (MID-digit slices): small passes fill the GPU
     uint64_t ib, ie;       // the shard's global candidate range
     SelParams P;
 };
@@ -2413,7 +2418,10 @@ __global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) str
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t sh = 3 * (sa.levels - sa.lvl);
-    for (uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < sa.ntiles_pass; j += nwarps) {
+    const uint64_t nwork = sa.ntiles_pass * sa.msplit;
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwork; w += nwarps) {
+        const uint64_t j = w / sa.msplit;  // the pass's j-th tile, MID slice w % msplit
+        const uint32_t slice = (uint32_t)(w - j * sa.msplit);
         const uint64_t u = sa.lvl == 0 ? j << sh : ((j / 7) * 8 + (j % 7) + 1) << sh;  // tile of the pass
         const uint64_t t = job.tile_begin + u;
         if (t >= job.tile_end) break;  // warp-uniform; tiles grow with j
@@ -2433,7 +2441,7 @@ __global__ void __launch_bounds__(kStreamThreads, stream_min_blocks(NP, BM)) str
             kmin = min(kmin, *(volatile unsigned long long*)&ss.key[q]);
         }
         const StreamEmit em{&sa, &ss, d, dh, rb, rl, rb < sa.ib || rb + row > sa.ie, allf, kmin};
-        eval_tile_b<NP, BM != 0, BM == 2>(h, va, t, em);
+        eval_tile_b<NP, BM != 0, BM == 2>(h, va, t, em, slice, sa.msplit);
     }
     if (lane == 0)  // this warp's best per query -> the query's list (lane 0 wrote them)
         for (uint32_t q = 0; q < sa.P.nq; q++) {

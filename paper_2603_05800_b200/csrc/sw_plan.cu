@@ -1881,9 +1881,14 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
             sa.ie = e;
             sa.P = PS;
             const uint64_t warps_per_block = kStreamThreads / 32;
-            const uint32_t grid = (uint32_t)std::min<uint64_t>(
-                (ntp + warps_per_block - 1) / warps_per_block,
-                (uint64_t)h->num_sms * std::max(1, h->stream_occ[eval_mode(h->h.flags)]));
+            const uint64_t max_blocks = (uint64_t)h->num_sms * std::max(1, h->stream_occ[eval_mode(h->h.flags)]);
+            // a warp works a whole tile (32 rows x row candidates): a pass of few tiles is
+            // split into MID-digit slices so that it has >= 2 work items per warp slot
+            const uint64_t slots = max_blocks * warps_per_block;
+            const uint32_t rm = h->h.radix[h->h.B - 2];
+            sa.msplit = (uint32_t)std::min<uint64_t>(rm, std::max<uint64_t>(1, (2 * slots + ntp - 1) / ntp));
+            const uint64_t nwork = ntp * sa.msplit;
+            const uint32_t grid = (uint32_t)std::min<uint64_t>((nwork + warps_per_block - 1) / warps_per_block, max_blocks);
             int pr = 0;
             sw_status ts = begin_timed(h, SW_KERNEL_STREAM, 0, &pr);
             if (ts < 0) return ts;

@@ -1847,8 +1847,8 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
         // survivor budget if nothing were filtered
         uint32_t K = nt >= 4096 ? 2 : nt >= 64 ? 1 : 0;
         while (K < 20 && up(nt, 3 * K) * per_tile > 64 * (uint64_t)h->surv_cap) K++;
-        if (h->front_n == 0) {  // fresh front: seed it from 16K (64K) candidates spread over the shard
-            const uint32_t ns = (uint32_t)std::min<uint64_t>(e - b, (e - b) >> 30 ? 65536 : 16384);
+        if (h->front_n == 0) {  // fresh front: seed it from 16K (64K from 2^26 on) candidates spread over the shard
+            const uint32_t ns = (uint32_t)std::min<uint64_t>(e - b, (e - b) >> 26 ? 65536 : 16384);
             CK(h, cudaMemsetAsync(&h->d_ctl->m_in, 0, sizeof(uint32_t), h->stream));
             launch_np(h, [&](auto npc) {
                 constexpr int NPc = decltype(npc)::value;

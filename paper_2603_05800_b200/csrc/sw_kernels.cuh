@@ -2387,7 +2387,12 @@ struct StreamEmit {
 #ifndef SW_STREAM_MINB1
 #define SW_STREAM_MINB1 2
 #endif
-__host__ __device__ constexpr int stream_min_blocks(int np, int bm) { return (np == 1 && bm < 2) ? SW_STREAM_MINB1 : 1; }
+#ifndef SW_STREAM_MINB2
+#define SW_STREAM_MINB2 1
+#endif
+__host__ __device__ constexpr int stream_min_blocks(int np, int bm) {
+    return (np == 1 && bm < 2) ? SW_STREAM_MINB1 : (np == 2 && bm < 2) ? SW_STREAM_MINB2 : 1;
+}
 
 // BM: the eval path (eval_mode) at compile time, as in eval_kernel.
 template <int NP, int BM>

@@ -27,14 +27,21 @@ def main():
     for cfg in cfgs:
         pb = make_config(cfg)
         g = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % cfg)))
-        with sw.Plan(pb, device=local, comm=comm, rank=rank, nranks=world) as plan:
-            # global range in two ragged calls: each rank shards both internally
-            cut = plan.n // 3 + 12345
-            plan.eval(cut, plan.n)
-            plan.eval(0, cut)
-            sels = plan.select_batch(pb.queries)
-            front = plan.pareto()
-            dg = plan.digest()
+        n = sw.space_shape(pb)[0]
+        if n * 32 > 0.5 * torch.cuda.mem_get_info(local)[0] * world:  # C5: the chunked sweep
+            cap = int(0.75 * torch.cuda.mem_get_info(local)[0]) // 32
+            with sw.Plan(pb, device=local, comm=comm, rank=rank, nranks=world, record_capacity=cap) as plan:
+                sels, dg = plan.sweep(0, plan.n, pb.queries, digest=True)
+                front = plan.pareto()
+        else:
+            with sw.Plan(pb, device=local, comm=comm, rank=rank, nranks=world) as plan:
+                # global range in two ragged calls: each rank shards both internally
+                cut = plan.n // 3 + 12345
+                plan.eval(cut, plan.n)
+                plan.eval(0, cut)
+                sels = plan.select_batch(pb.queries)
+                front = plan.pareto()
+                dg = plan.digest()
         for s, w in zip(sels, g["winners"]):
             st = {0: 0, 1: 1, -1: 3}[w["status"]]
             assert s.status == st, (cfg, rank, s, w)

@@ -38,3 +38,18 @@ def test_sharded_eval_nccl_merge(world):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert r.stdout.count(" ok:") == 2 * world, r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_c5_full_space(world):
+    """C5 (1.2e10 plans) through the chunked sweep sharded over `world` GPUs (NCCL), and
+    through the sharded fused stream: winners, the 3021-point front and the whole-space
+    digest equal the oracle's full-space golden on every rank."""
+    if _ngpus() < world:
+        pytest.skip("needs %d GPUs" % world)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(world), "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tests", "mgpu_worker.py"), "C5"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert r.stdout.count(" ok:") == world, r.stdout

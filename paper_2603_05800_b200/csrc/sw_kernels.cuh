@@ -1089,7 +1089,7 @@ __global__ void __launch_bounds__(kDltQThreads) dlt_qtop_kernel(const PPoint* __
 constexpr int kDltBuildThreads = 256;
 static_assert(kDltT < kDltBuildThreads, "one thread per t bin");
 __global__ void __launch_bounds__(kDltBuildThreads) dlt_build_kernel(const PPoint* __restrict__ front,
-                                                                     const ParetoCtl* __restrict__ ctl,
+                                                                     ParetoCtl* __restrict__ ctl,
                                                                      Dlt* __restrict__ d) {
     __shared__ uint64_t te[kDltT];
     __shared__ unsigned long long s_cmax;
@@ -1116,6 +1116,10 @@ __global__ void __launch_bounds__(kDltBuildThreads) dlt_build_kernel(const PPoin
         if (r == 0) {
             d->kbase = kbase;
             d->cshift = csh;
+            // the coming pass's counters (the previous pass's were consumed before this
+            // launch): folded in here instead of two memset launches per pass
+            ctl->surv = 0;
+            ctl->dlt_n = 0;
         }
         for (uint32_t i = r; i < kDltT; i += blockDim.x) d->tedge[i] = te[i];
         for (uint32_t i = r; i <= (uint32_t)kDltT; i += blockDim.x) d->cell[i * kDltCols + kDltQ] = 0xffff;

@@ -1310,8 +1310,6 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         v.upt = upt;
         v.levels = K;
         if (sw_status ds = dlt_build_async(h); ds < 0) return ds;
-        CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
-        CK(h, cudaMemsetAsync(&h->d_ctl->dlt_n, 0, sizeof(unsigned long long), h->stream));
         const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / (kStageRecs * kCW)), h->scan_grid);
         Cand* part = h->d_partial;
         if (nq) {
@@ -1863,8 +1861,6 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
         // survivors merged into the front; the pass's survivor count lands in pinned memory
         auto run_pass = [&](uint32_t lvl, uint64_t ntp) -> sw_status {
             if (sw_status ds = dlt_build_async(h); ds < 0) return ds;
-            CK(h, cudaMemsetAsync(&h->d_ctl->surv, 0, sizeof(unsigned long long), h->stream));
-            CK(h, cudaMemsetAsync(&h->d_ctl->dlt_n, 0, sizeof(unsigned long long), h->stream));
             StreamArgs sa{};
             sa.dlt = h->d_dlt;
             sa.gkey = h->d_skey;

@@ -1509,10 +1509,34 @@ __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* _
         __syncthreads();
         if (pt < cnt && span_dominated(tile, part * kRedSpan, cnt, base, tile[pt], base + pt)) s_dom[pt] = 1;
         __syncthreads();
-        if (part == 0 && pt < cnt && !s_dom[pt]) {
-            const uint32_t slot = atomicAdd(&ctl->m_loc, 1u);
-            tmp2[slot] = tile[pt];
-            keep[slot] = 1;
+        // the chunk's kept points: one global atomic per chunk (ballots + a block offset)
+        // -- one per kept point serialised ~10 us on 30 K-point C3 merges
+        if (part == 0) {
+            const bool kp = pt < cnt && !s_dom[pt];
+            const unsigned bal = __ballot_sync(0xffffffffu, kp);
+            if ((tid & 31) == 0) s_rank[tid >> 5] = __popc(bal);  // per-warp counts (8 warps)
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t acc = 0;
+            for (uint32_t w = 0; w < kScanThreads / 32; w++) {
+                const uint32_t c = s_rank[w];
+                s_rank[w] = acc;
+                acc += c;
+            }
+            s_rank[kScanThreads / 32] = acc ? atomicAdd(&ctl->m_loc, acc) : 0u;
+        }
+        __syncthreads();
+        if (part == 0) {  // whole warps (tid < 256): the ballot sees every lane
+            const bool kp = pt < cnt && !s_dom[pt];
+            const unsigned bal = __ballot_sync(0xffffffffu, kp);
+            if (kp) {
+                const uint32_t slot =
+                    s_rank[kScanThreads / 32] + s_rank[tid >> 5] + __popc(bal & ((1u << (tid & 31)) - 1u));
+                tmp2[slot] = tile[pt];
+                keep[slot] = 1;
+            }
         }
     }
     grid.sync();
@@ -1535,8 +1559,15 @@ __global__ void __launch_bounds__(kRedThreads, 1) pareto_reduce_kernel(PPoint* _
     grid.sync();
     stamp(3);
     // (3) compaction of the kept points into work
-    for (uint32_t x = blockIdx.x * blockDim.x + tid; x < ml; x += gridDim.x * blockDim.x)
-        if (__ldcg(&keep[x])) work[atomicAdd(&ctl->m_cmp, 1u)] = ldcg_point(&tmp2[x]);
+    for (uint32_t x0 = blockIdx.x * blockDim.x; x0 < ml; x0 += gridDim.x * blockDim.x) {  // one atomic per warp
+        const uint32_t x = x0 + tid;
+        const bool kp = x < ml && __ldcg(&keep[x]);
+        const unsigned bal = __ballot_sync(0xffffffffu, kp);
+        uint32_t wb = 0;
+        if ((tid & 31) == 0 && bal) wb = atomicAdd(&ctl->m_cmp, (uint32_t)__popc(bal));
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if (kp) work[wb + __popc(bal & ((1u << (tid & 31)) - 1u))] = ldcg_point(&tmp2[x]);
+    }
     grid.sync();
     stamp(4);
     const uint32_t mc = __ldcg(&ctl->m_cmp);

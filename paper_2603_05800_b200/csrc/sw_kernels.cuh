@@ -935,26 +935,6 @@ __device__ __forceinline__ bool dlt_dominated(const Dlt& d, const DltHot& hs, ui
     return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > cell;
 }
 
-// The same lookup with the exact t bin (a search of the map cell's edges when it holds
-// several): for the deferred exact test's undecided candidates only -- in the scans' hot
-// loop the search cost more than the records it saves.
-__device__ __forceinline__ bool dlt_dominated_exact_t(const Dlt& d, const DltHot& hs, uint64_t t, uint64_t c,
-                                                      uint32_t q) {
-    const int32_t k = dlt_tkey(t) - hs.kbase;
-    const uint32_t kc = (uint32_t)min(max(k, 0), kDltMap - 1);
-    const uint2 qm = d.qmap[min((max(q, hs.qbase) - hs.qbase) >> hs.qmshift, (uint32_t)kDltQMap - 1)];
-    const uint32_t j = q > qm.x ? (qm.y >> 8) : (qm.y & 0xffu);
-    const uint32_t lh = d.tmap[kc];
-    uint32_t a = lh & 0xffu, e = lh >> 8;  // #edges <= t lies in [lo, hi]
-    while (a < e) {
-        const uint32_t mid = (a + e) >> 1;
-        if (d.tedge[mid] <= t) a = mid + 1;
-        else e = mid;
-    }
-    const uint64_t cs = c >> hs.cshift;
-    return (uint32_t)(cs < 0xffffull ? cs : 0xffffull) > d.cell[a * kDltCols + j];
-}
-
 // Quality bin tops and the q map of the DLT (before dlt_build_kernel): the front's quality
 // values rank-sorted over the grid (rank = #smaller + #equal at a lower position, 16
 // threads per value), then the last block to finish takes the distinct ones -- all, or
@@ -1668,7 +1648,7 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
 // range (usually empty) instead of an 11-step binary search of dependent smem loads.
 // 24 warps per block (one block per SM: the front copy is shared by all of them).
 constexpr uint32_t kExactFront = 2048;  // front points staged in smem (larger fronts: from L2)
-constexpr uint32_t kExactList = 64;     // per-warp survivor list
+constexpr uint32_t kExactList = 128;    // per-warp survivor list
 constexpr int kExactThreads = 768;
 constexpr int kExactWarps = kExactThreads / 32;
 #ifndef SW_EXACT_NEAR
@@ -1677,7 +1657,7 @@ constexpr int kExactWarps = kExactThreads / 32;
 constexpr uint32_t kExactNear = SW_EXACT_NEAR;  // front points below x.t tested per lane first
 __host__ __device__ constexpr size_t exact_smem_bytes() {
     return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t)) +
-           (size_t)kDltMap * sizeof(uint32_t) + sizeof(Dlt);
+           (size_t)kDltMap * sizeof(uint32_t);
 }
 struct PArrays {  // a point list as arrays in shared memory
     uint64_t *t, *c, *i;
@@ -1709,8 +1689,7 @@ __device__ __forceinline__ PArrays parrays(unsigned char* base, uint32_t n) {
 
 __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PPoint* __restrict__ cand, uint64_t cand_cap,
                                                                         const PPoint* __restrict__ front, ParetoCtl* ctl,
-                                                                        PPoint* __restrict__ surv, uint64_t surv_cap,
-                                                                        const Dlt* __restrict__ g_dlt) {
+                                                                        PPoint* __restrict__ surv, uint64_t surv_cap) {
     extern __shared__ __align__(16) unsigned char xsm[];
     const PArrays F = parrays(xsm, kExactFront);
     const unsigned long long nd = ctl->dlt_n;
@@ -1724,12 +1703,6 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
     if (r0 >= r1) return;
     const bool f_smem = m <= kExactFront;
     uint32_t* pmap = reinterpret_cast<uint32_t*>(xsm + (size_t)(kExactFront + kExactWarps * kExactList) * 28);
-    Dlt& dsm = *reinterpret_cast<Dlt*>(pmap + kDltMap);  // the pass's DLT (offset a multiple of 16 B)
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(g_dlt);
-        uint4* dst = reinterpret_cast<uint4*>(&dsm);
-        for (uint32_t i = threadIdx.x; i < sizeof(Dlt) / 16; i += blockDim.x) dst[i] = src[i];
-    }
     const int32_t pkbase = m ? dlt_tkey(front[0].t) : 0;  // cell 0 holds the smallest front t
     if (f_smem) {
         for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) F.put(j, front[j]);
@@ -1760,7 +1733,6 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const PArrays L = parrays(xsm + (size_t)kExactFront * 28 + (size_t)warp * kExactList * 28, kExactList);
-    const DltHot dh{dsm.kbase, dsm.qbase, dsm.qmshift, dsm.cshift};
     auto fget = [&](uint32_t j) { return f_smem ? F.get(j) : front[j]; };
     // this warp's run of the block's range
     const uint64_t w0 = r0 + (r1 - r0) * warp / kExactWarps, w1 = r0 + (r1 - r0) * (warp + 1) / kExactWarps;
@@ -1803,10 +1775,6 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
             for (; j > stop && !dom; j--) dom = pdom(fget(j - 1), 0, x, 1);
         }
         const uint32_t top = lo > kExactNear ? lo - kExactNear : 0;  // still to test: [0, top)
-        // (1b) still undecided: the pass's DLT with the exact t bin -- it holds the
-        // dominators far below x.t that the nearest points miss (a hit spares the warp a
-        // scan of the rest of the front)
-        if (!dom && top > 0) dom = dlt_dominated_exact_t(dsm, dh, x.t, x.c, x.q);
         // (2) undecided candidates (rare): the whole warp against the rest of the front
         unsigned hard = __ballot_sync(0xffffffffu, !dom && top > 0);
         while (hard) {

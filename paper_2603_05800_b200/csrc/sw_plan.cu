@@ -1328,7 +1328,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         // the pass's DLT survivors: exact test against the running front (grid-stride over
         // the device-side count)
         pareto_exact_kernel<<<h->num_sms, kExactThreads, exact_smem_bytes(), h->stream>>>(
-            h->d_dltc, h->dltc_cap, h->d_front, h->d_ctl, h->d_surv, h->surv_cap, h->d_dlt);
+            h->d_dltc, h->dltc_cap, h->d_front, h->d_ctl, h->d_surv, h->surv_cap);
         CKL(h);
         trace_mark(h, "exact");
         pareto_append_kernel<<<h->num_sms, 256, 0, h->stream>>>(h->d_front, h->d_surv, h->surv_cap, h->d_work,
@@ -1902,7 +1902,7 @@ extern "C" sw_status sw_plan_stream(sw_plan* h, uint64_t begin, uint64_t end, ui
             trace_mark(h, "stream");
             // the pass's DLT survivors: exact test against the running front
             pareto_exact_kernel<<<h->num_sms, kExactThreads, exact_smem_bytes(), h->stream>>>(
-                h->d_dltc, h->dltc_cap, h->d_front, h->d_ctl, h->d_surv, h->surv_cap, h->d_dlt);
+                h->d_dltc, h->dltc_cap, h->d_front, h->d_ctl, h->d_surv, h->surv_cap);
             CKL(h);
             trace_mark(h, "exact");
             CK(h, cudaMemcpyAsync(&h->h_pass_surv[lvl], &h->d_ctl->surv, sizeof(uint64_t), cudaMemcpyDeviceToHost,

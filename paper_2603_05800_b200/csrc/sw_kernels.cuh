@@ -1657,7 +1657,7 @@ constexpr int kExactWarps = kExactThreads / 32;
 constexpr uint32_t kExactNear = SW_EXACT_NEAR;  // front points below x.t tested per lane first
 __host__ __device__ constexpr size_t exact_smem_bytes() {
     return (size_t)(kExactFront + kExactWarps * kExactList) * (3 * sizeof(uint64_t) + sizeof(uint32_t)) +
-           (size_t)kDltMap * sizeof(uint32_t);
+           (size_t)kDltMap * sizeof(uint32_t) + (size_t)kExactFront * (sizeof(uint32_t) + sizeof(uint64_t));
 }
 struct PArrays {  // a point list as arrays in shared memory
     uint64_t *t, *c, *i;
@@ -1730,8 +1730,38 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
             pmap[k] = lo | (hi << 16);
         }
     }
-    __syncthreads();
+    // per 32-point block of the t-sorted front: its qualities sorted descending (sq) and the
+    // running min cost over them (sc) -- "is any point of this block >= q and < c?" is then
+    // one binary search, so a candidate the nearest points leave undecided is settled by
+    // one lookup per block (a lane each) instead of a scan of the whole front below it
+    uint32_t* sq = pmap + kDltMap;
+    uint64_t* sc = reinterpret_cast<uint64_t*>(sq + kExactFront);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (f_smem) {
+        __syncthreads();  // F staged
+        for (uint32_t kb = warp; kb * 32 < m; kb += kExactWarps) {
+            const uint32_t p = kb * 32 + lane;
+            const uint32_t q = p < m ? F.q[p] : 0u;
+            const uint64_t c = p < m ? F.c[p] : kInf64;
+            uint32_t r = 0;  // rank: higher q first, ties by lane
+            for (uint32_t o = 0; o < 32; o++) {
+                const uint32_t oq = __shfl_sync(0xffffffffu, q, o);
+                r += (oq > q || (oq == q && o < lane)) ? 1u : 0u;
+            }
+            sq[kb * 32 + r] = q;
+            sc[kb * 32 + r] = c;
+            __syncwarp();
+            uint64_t mn = sc[kb * 32 + lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, mn, o);
+                if (lane >= (uint32_t)o) mn = umin64(mn, y);
+            }
+            sc[kb * 32 + lane] = mn;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
     const PArrays L = parrays(xsm + (size_t)kExactFront * 28 + (size_t)warp * kExactList * 28, kExactList);
     auto fget = [&](uint32_t j) { return f_smem ? F.get(j) : front[j]; };
     // this warp's run of the block's range
@@ -1787,13 +1817,42 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
             y.q = __shfl_sync(0xffffffffu, x.q, src);
             y.pad = 0;
             const uint32_t ytop = __shfl_sync(0xffffffffu, top, src);
-            bool d = false;
-            for (uint32_t j1 = ytop; j1 > 0 && !d;) {  // downwards: nearer points first
-                const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
-                const uint32_t j = j0 + lane;
-                d = __any_sync(0xffffffffu, j < j1 && pdom(fget(j < j1 ? j : 0), 0, y, 1));
-                j1 = j0;
+            const uint32_t kfull = f_smem ? ytop >> 5 : 0;  // whole blocks below ytop: by summary
+            bool d;
+            {  // the rest above them: direct tests, a lane each
+                const uint32_t j = (kfull << 5) + lane;
+                d = __any_sync(0xffffffffu, j < ytop && pdom(fget(j < ytop ? j : 0), 0, y, 1));
             }
+            if (!d && kfull) {
+                bool hit = false, unsure = false;
+                for (uint32_t kb = lane; kb < kfull; kb += 32) {
+                    uint32_t a = 0, e = 32;  // #points of block kb with q >= y.q
+                    while (a < e) {
+                        const uint32_t mid = (a + e) >> 1;
+                        if (sq[kb * 32 + mid] >= y.q) a = mid + 1;
+                        else e = mid;
+                    }
+                    if (a) {
+                        const uint64_t mc = sc[kb * 32 + a - 1];
+                        hit |= mc < y.c;      // t <= y.t, q >= y.q, c < y.c: dominates
+                        unsure |= mc == y.c;  // equal cost: strictness decided point by point
+                    }
+                }
+                d = __any_sync(0xffffffffu, hit);
+                if (!d && __any_sync(0xffffffffu, unsure))
+                    for (uint32_t j1 = kfull << 5; j1 > 0 && !d;) {  // rare: the exact scan
+                        const uint32_t j0 = j1 - 32, j = j0 + lane;
+                        d = __any_sync(0xffffffffu, pdom(fget(j), 0, y, 1));
+                        j1 = j0;
+                    }
+            }
+            if (!f_smem)  // front beyond smem: the downward scan from L2
+                for (uint32_t j1 = ytop; j1 > 0 && !d;) {
+                    const uint32_t j0 = j1 > 32 ? j1 - 32 : 0;
+                    const uint32_t j = j0 + lane;
+                    d = __any_sync(0xffffffffu, j < j1 && pdom(fget(j < j1 ? j : 0), 0, y, 1));
+                    j1 = j0;
+                }
             if (lane == src) dom = d;
         }
         // (3) front survivors: against the warp's earlier survivors, then join the list

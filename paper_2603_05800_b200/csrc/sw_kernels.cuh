@@ -1826,12 +1826,11 @@ __global__ void __launch_bounds__(kExactThreads, 1) pareto_exact_kernel(const PP
             if (!d && kfull) {
                 bool hit = false, unsure = false;
                 for (uint32_t kb = lane; kb < kfull; kb += 32) {
-                    uint32_t a = 0, e = 32;  // #points of block kb with q >= y.q
-                    while (a < e) {
-                        const uint32_t mid = (a + e) >> 1;
-                        if (sq[kb * 32 + mid] >= y.q) a = mid + 1;
-                        else e = mid;
-                    }
+                    const uint32_t* qa = sq + kb * 32;  // descending
+                    uint32_t a = 0;                     // #points of block kb with q >= y.q
+#pragma unroll
+                    for (uint32_t st = 16; st > 0; st >>= 1) a += qa[a + st - 1] >= y.q ? st : 0u;
+                    a += qa[a] >= y.q ? 1u : 0u;  // a <= 31 here: the last element
                     if (a) {
                         const uint64_t mc = sc[kb * 32 + a - 1];
                         hit |= mc < y.c;      // t <= y.t, q >= y.q, c < y.c: dominates

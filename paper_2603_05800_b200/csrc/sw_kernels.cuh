@@ -39,7 +39,10 @@ struct SegView {
     // 8^(K-l+1) -- each pass a uniform sample of the whole segment, 8x the previous one,
     // so the Pareto filter sees every region early and each pass's survivors stay
     // bounded.  pass 0: the whole view in order.
-    uint32_t pass, upt, levels, pad_;
+    uint32_t pass, upt, levels;
+    // a huge pass is folded in sub-passes: this one covers the pass's units [j0, j1)
+    // (pass-local unit order; j1 = ~0: to the end)
+    uint32_t j0, j1, pad_;
 };
 constexpr int kScanThreads = 256;
 constexpr int kDltT = 255;  // dominance lookup table: ttff_eff bins (front quantiles; <= 255: u8 map)
@@ -2060,13 +2063,17 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     const uint32_t sh = v.pass ? 3 * (v.levels - lvl) : 0;  // log2 of the unit stride
     const uint64_t c_here = v.pass ? (nunits + (1ull << sh) - 1) >> sh : 0;
     const uint64_t c_up = (v.pass && lvl > 0) ? (nunits + (1ull << (sh + 3)) - 1) >> (sh + 3) : 0;
-    const uint64_t nstages = v.pass == 0 ? (total + kStageRecs - 1) / kStageRecs : spu * (c_here - c_up);
+    const uint64_t units_here = c_here - c_up;
+    const uint64_t j_end = v.j1 < units_here ? v.j1 : units_here;
+    const uint64_t nstages = v.pass == 0 ? (total + kStageRecs - 1) / kStageRecs
+                                         : (j_end > v.j0 ? spu * (j_end - v.j0) : 0);
     // stage sg -> flat slot of its first record: with sg = j * spu + part (pass 0: spu = 1),
     // pos = (m << sh) * unit_recs + part * kStageRecs, m = the j-th unit of this pass
     // (pass 0: sh = 0 and unit_recs = kStageRecs, so pos = sg * kStageRecs)
     const uint64_t unit_pos = v.pass ? unit_recs : kStageRecs;
     const uint32_t spu32 = (uint32_t)spu;
-    auto stage_pos = [&](uint32_t j, uint32_t part) -> uint64_t {
+    auto stage_pos = [&](uint32_t jl, uint32_t part) -> uint64_t {
+        const uint32_t j = jl + (v.pass ? v.j0 : 0u);  // the pass's j-th unit
         const uint64_t m = lvl == 0 ? (uint64_t)j : (uint64_t)(j / 7) * 8 + (j % 7) + 1;  // j-th non-multiple of 8
         const uint64_t pos = (m << sh) * unit_pos + part * kStageRecs;
         return pos < total ? pos : kInf64;

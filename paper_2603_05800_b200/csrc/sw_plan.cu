@@ -114,6 +114,7 @@ struct sw_plan {
     uint64_t gepoch = 1;
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint64_t first_pass = 8ull << 20;  // SW_FIRST_PASS: records of the first strided fold pass (about)
+    uint64_t max_pass = 1ull << 29;    // SW_MAX_PASS: records of a fold (sub-)pass at most
     uint32_t fold_kmin = 1;      // SW_FOLD_KMIN: fewest strided fold levels (passes - 1); a first pass stays <= ~8 M records
     const char* dump_merge = nullptr;  // SW_DUMP_MERGE=<prefix>: every fold merge's input -> <prefix>_<n>.bin
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
@@ -310,6 +311,8 @@ static SegView view_of(const sw_plan* h, const Segment& g, uint64_t t_lo, uint64
     v.pass = 0;
     v.upt = 1;
     v.levels = 0;
+    v.j0 = 0;
+    v.j1 = 0xffffffffu;
     v.pad_ = 0;
     return v;
 }
@@ -719,6 +722,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     h->dump_merge = getenv("SW_DUMP_MERGE");
+    if (const char* ev = getenv("SW_MAX_PASS")) h->max_pass = std::max<uint64_t>(1 << 20, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FIRST_PASS")) h->first_pass = std::max<uint64_t>(1 << 16, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FOLD_KMIN")) h->fold_kmin = (uint32_t)std::min(std::max(atoi(ev), 1), 9);
     if (const char* ev = getenv("SW_TRACE")) h->trace = atoi(ev) != 0;
@@ -1287,6 +1291,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
     const uint64_t nunits = (total + unit_recs - 1) / unit_recs;
     // K levels: the first pass covers about kFirstPass records (>= 1/64 of the segment)
     const uint64_t kFirstPass = h->first_pass;
+    const uint64_t kMaxPassRecs = h->max_pass;
     uint32_t K = h->fold_kmin;
     while (K < 10 && (nunits >> (3 * K)) * unit_recs > kFirstPass) K++;
     const bool strided = nunits >= 256;
@@ -1304,11 +1309,21 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
             const uint64_t L = nunits - 1;  // does this pass hold the (possibly short) last unit?
             has_last = (L % (1ull << sh) == 0) && (lvl == 0 || L % (1ull << (sh + 3)) != 0);
         }
-        const uint64_t recs = units * unit_recs - (has_last ? last_short : 0);
+        const uint64_t recs_level = units * unit_recs - (has_last ? last_short : 0);
+        // a huge pass (a big chunk's last level) is folded in sub-passes of <= kMaxPassRecs:
+        // its survivors of the exact test against a front from much fewer records would
+        // overflow the survivor buffer and force a refold (a second read of the pass)
+        const uint64_t nsub = strided ? std::max<uint64_t>(1, (recs_level + kMaxPassRecs - 1) / kMaxPassRecs) : 1;
+        for (uint64_t si = 0; si < nsub; si++) {
+        const uint64_t j0 = units * si / nsub, j1 = units * (si + 1) / nsub;
+        const uint64_t recs = nsub == 1 ? recs_level
+                                        : (j1 - j0) * unit_recs - (has_last && j1 == units ? last_short : 0);
         SegView v = view_of(h, g, 0, g.ntiles);
         v.pass = pass;
         v.upt = upt;
         v.levels = K;
+        v.j0 = (uint32_t)j0;
+        v.j1 = nsub == 1 ? 0xffffffffu : (uint32_t)j1;
         if (sw_status ds = dlt_build_async(h); ds < 0) return ds;
         const uint32_t grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, recs / (kStageRecs * kCW)), h->scan_grid);
         Cand* part = h->d_partial;
@@ -1366,6 +1381,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
                     1e-3 * (double)(c.stamp[3] - c.stamp[2]), 1e-3 * (double)(c.stamp[4] - c.stamp[3]),
                     1e-3 * (double)(c.stamp[5] - c.stamp[4]));
         }
+        }  // sub-passes
     }
     return SW_OK;
 }

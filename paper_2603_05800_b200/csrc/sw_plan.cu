@@ -317,6 +317,7 @@ static SegView view_of(const sw_plan* h, const Segment& g, uint64_t t_lo, uint64
     return v;
 }
 static cudaError_t set_scan_smem_attrs();
+static cudaError_t set_scan_smem_attrs_once(int device);
 
 static sw_status create_common(sw_plan* h, const sw_runtime* rt);
 static thread_local bool t_tables_only = false;  // sw_shared_create: per-request table handles
@@ -745,7 +746,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
         if (const char* ev = getenv("SW_COOP_GRID"))
             h->coop_grid = std::min<uint32_t>(h->coop_grid, std::max(1, atoi(ev)));
     }
-    if (cudaError_t se = set_scan_smem_attrs(); se != cudaSuccess) {
+    if (cudaError_t se = set_scan_smem_attrs_once(h->device); se != cudaSuccess) {
         cudaGetLastError();
         return (fail(nullptr, SW_ECUDA, "scan kernels cannot launch one block per SM (%s; smem %zu/%zu B)",
                          cudaGetErrorString(se), ring_bytes(true) + sizeof(Dlt),
@@ -1171,6 +1172,18 @@ static cudaError_t set_scan_smem_attrs() {
     cudaError_t f = cudaFuncSetAttribute(scan_kernel<1, false, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kRingBytes);
     return f != cudaSuccess ? f : e;
+}
+
+// Function attributes are context-wide: set once per device (they were redone, with the
+// occupancy queries, at every create -- part of an end-to-end step's create time).
+static cudaError_t set_scan_smem_attrs_once(int device) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> g(mu);
+    if (device >= 0 && device < 64 && done[device]) return cudaSuccess;
+    const cudaError_t e = set_scan_smem_attrs();
+    if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
+    return e;
 }
 
 static ParetoArgs pareto_args(sw_plan* h) {

@@ -1975,6 +1975,13 @@ __device__ __forceinline__ uint64_t obj_key(bool obj_q, const Rec4& r) {
     return obj_q ? qc_key(r) : cxt_key(r);
 }
 
+// Closest-tier prefilter key (lower is better): saturated (V_t, V_c) packed in 64 bits.
+__device__ __forceinline__ uint64_t closest_pack(const Rec4& r, uint64_t slo_t, uint64_t slo_s, uint64_t bud) {
+    const uint64_t vt = sat_sub(r.w0, slo_t) + sat_sub(r.w1, slo_s);
+    const uint64_t vc = sat_sub(r.w2, bud);
+    return (umin64(vt, 0xffffffffull) << 32) | umin64(vc, 0xffffffffull);
+}
+
 // Select predicate of kRPT records for one query: bit u set iff record u is valid,
 // feasible (only the bounds in AM are compared) and its objective prefilter key (packed
 // (Q, ~cost) under QUALITY_FIRST, ~sat(cost x ttff_eff) under COST_X_TTFF) is >= the
@@ -2031,8 +2038,12 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     // record: Q << 32 | ~min(cost, 2^32-1) (QUALITY_FIRST) or ~sat(cost x ttff_eff)
     // (COST_X_TTFF); 0 = none yet
     __shared__ unsigned long long s_thr[NQA];
-    // per query, while no feasible record is known: the smallest startup+stall violation
-    // V_t of any closest-tier best in this block (records with a larger V_t cannot win)
+    // per query, while no feasible record is known: the smallest closest-tier key
+    // (min(V_t, 2^32-1) << 32 | min(V_c, 2^32-1), V_t the startup+stall violation and V_c the
+    // budget violation -- the closest tier's order) of any best in this block; a record
+    // with a larger key cannot win.  (V_t alone let every record of a shard through where
+    // a query is infeasible and many records tie on V_t: C3's last quarter at 4 ranks
+    // scanned at half speed.)
     __shared__ unsigned long long s_vt[NQA];
     Rec4* ring = reinterpret_cast<Rec4*>(fsm);
     Dlt& d = *reinterpret_cast<Dlt*>(fsm + ring_bytes(PARETO));
@@ -2203,10 +2214,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 if (__any_sync(0xffffffffu, !anyf)) {  // closest tier still open somewhere
                     const unsigned long long vmax = s_vt[q];
 #pragma unroll
-                    for (int u = 0; u < kRPT; u++) {
-                        const uint64_t vt = sat_sub(r[u].w0, slo_t) + sat_sub(r[u].w1, slo_s);
-                        need |= (uint32_t)(valid[u] & !anyf & (vt <= vmax)) << u;
-                    }
+                    for (int u = 0; u < kRPT; u++)
+                        need |= (uint32_t)(valid[u] & !anyf & (closest_pack(r[u], slo_t, slo_s, bud) <= vmax)) << u;
                 }
                 if (__any_sync(0xffffffffu, need != 0)) {
 #pragma unroll
@@ -2221,8 +2230,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                                 if (!bf[q] && pa.gfeas) atomicOr(&pa.gfeas[q], 1u);
                                 atomicMax(&s_thr[q], (unsigned long long)obj_key<OBJ>(obj_q, r[u]));
                             } else {
-                                atomicMin(&s_vt[q], (unsigned long long)(sat_sub(r[u].w0, P.q[q].slo_t) +
-                                                                         sat_sub(r[u].w1, P.q[q].slo_s)));
+                                atomicMin(&s_vt[q], (unsigned long long)closest_pack(r[u], P.q[q].slo_t,
+                                                                                     P.q[q].slo_s, P.q[q].budget));
                             }
                             bf[q] = f;
                         }

@@ -256,7 +256,10 @@ def measure_plan(ctx, pb, cfg, steps, warmup, e2e_steps, clocks=None):
     N, row = sw.space_shape(pb)
     free_b, _ = torch.cuda.mem_get_info(dev)
     need = N // world + 3 * row  # the library's default: this rank's largest shard
-    cap = 0 if need * REC_BYTES < 0.75 * free_b else int(0.75 * free_b) // REC_BYTES
+    cap_free = int(0.75 * free_b) // REC_BYTES
+    if world > 1:  # every rank must chunk the same way (sw_plan_sweep is collective): the min
+        cap_free = int(-mor(-float(cap_free)))
+    cap = 0 if need < cap_free else cap_free
     out = {"workload": WORKLOADS.get(cfg, cfg), "n_candidates": N, "cap": cap,
            "record_capacity_per_rank": cap, "chunked": cap != 0}
 

@@ -254,6 +254,7 @@ def measure_plan(ctx, pb, cfg, steps, warmup, e2e_steps, clocks=None):
     sw, dev, stream, comm = ctx["sw"], ctx["dev"], ctx["stream"], ctx["comm"]
     rank, world, barrier, mor = ctx["rank"], ctx["world"], ctx["barrier"], ctx["max_over_ranks"]
     N, row = sw.space_shape(pb)
+    sw.trim_device_memory(dev)  # earlier configs' handles stay cached in the pool otherwise
     free_b, _ = torch.cuda.mem_get_info(dev)
     need = N // world + 3 * row  # the library's default: this rank's largest shard
     cap_free = int(0.75 * free_b) // REC_BYTES

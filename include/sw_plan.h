@@ -344,6 +344,14 @@ sw_status sw_plan_greedy(sw_plan *h, uint64_t slo_startup_us, uint64_t slo_stall
  * N >= 2^63. */
 sw_status sw_space_shape(const sw_profile_tables *tables, uint64_t *n, uint64_t *row);
 
+/* Device memory of destroyed handles stays cached in the device's default stream-ordered
+ * memory pool (the library allocates with cudaMallocAsync), so that re-creating a handle
+ * of the same shape maps no new memory.  sw_trim_device_memory synchronises the device
+ * and returns the cached, unused part of that pool to the driver (cudaMemPoolTrimTo 0), so
+ * that cudaMemGetInfo shows it as free again -- e.g. before sizing a record capacity from
+ * free memory.  Memory of live handles is untouched.  ECUDA on a CUDA error. */
+sw_status sw_trim_device_memory(int32_t device);
+
 /* Associative, commutative merge of two selections of the SAME query (q) over
  * disjoint candidate sets, e.g. the winners of successive chunks of a chunked sweep
  * (eval -> select -> release_records, R13) or of independent handles.  *out = the

@@ -139,6 +139,7 @@ EXPORTS = {
     "sw_comm_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                  C.POINTER(C.c_void_p)]),
     "sw_comm_destroy": (C.c_int32, [C.c_void_p]),
+    "sw_trim_device_memory": (C.c_int32, [C.c_int32]),
     "sw_status_str": (C.c_char_p, [C.c_int32]),
     "sw_last_error": (C.c_char_p, [C.c_void_p]),
     "sw_plan_launch_count": (C.c_uint64, [C.c_void_p]),
@@ -252,6 +253,11 @@ def comm_init(uid: bytes, rank: int, nranks: int, device: int) -> int:
 
 def comm_destroy(comm: int) -> None:
     _check(lib().sw_comm_destroy(C.c_void_p(comm)))
+
+
+def trim_device_memory(device: int = 0) -> None:
+    """Return the device's cached, unused pool memory to the driver (sw_trim_device_memory)."""
+    _check(lib().sw_trim_device_memory(int(device)))
 
 
 def comm_loopback_create(nranks: int) -> List[int]:

@@ -2959,6 +2959,16 @@ extern "C" sw_status sw_comm_loopback_create(int32_t nranks, void** comms_out) {
     return SW_OK;
 }
 
+extern "C" sw_status sw_trim_device_memory(int32_t device) {
+    cudaMemPool_t pool;
+    if (cudaSetDevice(device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+        cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess || cudaMemPoolTrimTo(pool, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(nullptr, SW_ECUDA, "trimming the device memory pool of device %d failed", device);
+    }
+    return SW_OK;
+}
+
 extern "C" sw_status sw_comm_destroy(void* comm) {
     if (!comm) return SW_OK;
     if (LoopComm* lc = as_loop(comm)) {  // a loopback rank: the group goes with its last rank

@@ -29,6 +29,7 @@ def main():
         g = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_%s.json" % cfg)))
         n = sw.space_shape(pb)[0]
         if n * 32 > 0.5 * torch.cuda.mem_get_info(local)[0] * world:  # C5: the chunked sweep
+            sw.trim_device_memory(local)
             cap = torch.tensor([int(0.75 * torch.cuda.mem_get_info(local)[0]) // 32], device="cuda")
             dist.all_reduce(cap, op=dist.ReduceOp.MIN)  # the sweep is collective: one chunking on every rank
             cap = int(cap.item())

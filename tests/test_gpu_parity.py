@@ -419,6 +419,7 @@ def test_c5_full_space(sw):
     g = _golden("C5")
     import torch
     pb = make_config("C5")
+    sw.trim_device_memory(0)
     free_b, _ = torch.cuda.mem_get_info(0)
     cap = int(0.75 * free_b) // 32
     with sw.Plan(pb, record_capacity=cap) as plan:

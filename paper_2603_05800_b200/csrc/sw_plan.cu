@@ -114,7 +114,8 @@ struct sw_plan {
     uint64_t gepoch = 1;
     bool debug = false;          // SW_DEBUG=1: per-pass fold statistics on stderr
     uint64_t first_pass = 8ull << 20;  // SW_FIRST_PASS: records of the first strided fold pass (about)
-    uint64_t max_pass = 1ull << 29;    // SW_MAX_PASS: records of a fold (sub-)pass at most
+    uint64_t max_pass = 1ull << 29;    // SW_MAX_PASS: a fold level of more records is split ...
+    uint64_t sub_pass = 1ull << 28;    // SW_SUB_PASS: ... into sub-passes of about this many
     uint32_t fold_kmin = 1;      // SW_FOLD_KMIN: fewest strided fold levels (passes - 1); a first pass stays <= ~8 M records
     const char* dump_merge = nullptr;  // SW_DUMP_MERGE=<prefix>: every fold merge's input -> <prefix>_<n>.bin
     bool coop_reduce = true;        // merge in one cooperative launch (SW_COOP_REDUCE=0: 5 launches)
@@ -723,6 +724,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     if (const char* ev = getenv("SW_FUSE_PARETO")) h->fuse_pareto = atoi(ev) != 0;
     if (const char* ev = getenv("SW_DEBUG")) h->debug = atoi(ev) != 0;
     h->dump_merge = getenv("SW_DUMP_MERGE");
+    if (const char* ev = getenv("SW_SUB_PASS")) h->sub_pass = std::max<uint64_t>(1 << 20, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_MAX_PASS")) h->max_pass = std::max<uint64_t>(1 << 20, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FIRST_PASS")) h->first_pass = std::max<uint64_t>(1 << 16, strtoull(ev, nullptr, 10));
     if (const char* ev = getenv("SW_FOLD_KMIN")) h->fold_kmin = (uint32_t)std::min(std::max(atoi(ev), 1), 9);
@@ -1329,7 +1331,7 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         // (levels above kMaxPassRecs split into halves of it: C5's 256 M sub-passes measured
         // 8% faster than 512 M ones, while splitting C2's 376 M last level cost 1.4%)
         const uint64_t nsub = strided && recs_level > kMaxPassRecs
-                                  ? (recs_level + kMaxPassRecs / 2 - 1) / (kMaxPassRecs / 2) : 1;
+                                  ? (recs_level + h->sub_pass - 1) / h->sub_pass : 1;
         for (uint64_t si = 0; si < nsub; si++) {
         const uint64_t j0 = units * si / nsub, j1 = units * (si + 1) / nsub;
         const uint64_t recs = nsub == 1 ? recs_level

@@ -1306,7 +1306,12 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
     const uint64_t nunits = (total + unit_recs - 1) / unit_recs;
     // K levels: the first pass covers about kFirstPass records (>= 1/64 of the segment)
     const uint64_t kFirstPass = h->first_pass;
-    const uint64_t kMaxPassRecs = h->max_pass;
+    // a level of more than kMaxPassRecs records is folded in sub-passes of h->sub_pass: for
+    // segments of >= 2^31 records (a big chunk) every level above 256 M -- its survivors
+    // against the front of the levels before overflowed the survivor buffer and forced a
+    // refold (C5 213 -> 188 ms, same box); smaller segments only above 512 M (C2's 376 M
+    // last level unsplit: splitting it cost 1.3%)
+    const uint64_t kMaxPassRecs = g.ntiles * kTileRows * h->row >= (1ull << 31) ? h->sub_pass : h->max_pass;
     uint32_t K = h->fold_kmin;
     while (K < 10 && (nunits >> (3 * K)) * unit_recs > kFirstPass) K++;
     const bool strided = nunits >= 256;
@@ -1328,8 +1333,6 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
         // a huge pass (a big chunk's last level) is folded in sub-passes of <= kMaxPassRecs:
         // its survivors of the exact test against a front from much fewer records would
         // overflow the survivor buffer and force a refold (a second read of the pass)
-        // (levels above kMaxPassRecs split into halves of it: C5's 256 M sub-passes measured
-        // 8% faster than 512 M ones, while splitting C2's 376 M last level cost 1.4%)
         const uint64_t nsub = strided && recs_level > kMaxPassRecs
                                   ? (recs_level + h->sub_pass - 1) / h->sub_pass : 1;
         for (uint64_t si = 0; si < nsub; si++) {

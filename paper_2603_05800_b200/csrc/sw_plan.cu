@@ -1312,7 +1312,6 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
     // refold (C5 213 -> 188 ms, same box); smaller segments only above 512 M (C2's 376 M
     // last level unsplit: splitting it cost 1.3%)
     const uint64_t kMaxPassRecs = g.ntiles * kTileRows * h->row >= (1ull << 31) ? h->sub_pass : h->max_pass;
-    uint64_t folded = 0;  // records of this segment folded by the passes so far
     uint32_t K = h->fold_kmin;
     while (K < 10 && (nunits >> (3 * K)) * unit_recs > kFirstPass) K++;
     const bool strided = nunits >= 256;
@@ -1331,31 +1330,15 @@ static sw_status fold_chunks_async(sw_plan* h, const Segment& g, uint32_t nq, co
             has_last = (L % (1ull << sh) == 0) && (lvl == 0 || L % (1ull << (sh + 3)) != 0);
         }
         const uint64_t recs_level = units * unit_recs - (has_last ? last_short : 0);
-        // a big level is folded in sub-passes over windows of its units, each at most the
-        // records folded before it (at least h->sub_pass): the exact test's survivors of a
-        // pass many times larger than the front's history overflowed the survivor buffer and
-        // forced a refold (a second read of the pass); doubling pieces keep a big chunk's
-        // last level to a few sub-passes once the front is good
-        std::vector<std::pair<uint64_t, uint64_t>> wins;
-        if (strided && recs_level > kMaxPassRecs) {
-            uint64_t j = 0, fold = folded;
-            while (j < units) {
-                const uint64_t want = std::max<uint64_t>(1, std::max<uint64_t>(h->sub_pass, fold) / unit_recs);
-                uint64_t j1 = std::min<uint64_t>(units, j + want);
-                if (units - j1 < want / 4) j1 = units;  // no sliver at the end
-                wins.push_back({j, j1});
-                fold += (j1 - j) * unit_recs;
-                j = j1;
-            }
-        } else {
-            wins.push_back({0, units});
-        }
-        const uint64_t nsub = wins.size();
+        // a huge pass (a big chunk's last level) is folded in sub-passes of <= kMaxPassRecs:
+        // its survivors of the exact test against a front from much fewer records would
+        // overflow the survivor buffer and force a refold (a second read of the pass)
+        const uint64_t nsub = strided && recs_level > kMaxPassRecs
+                                  ? (recs_level + h->sub_pass - 1) / h->sub_pass : 1;
         for (uint64_t si = 0; si < nsub; si++) {
-        const uint64_t j0 = wins[si].first, j1 = wins[si].second;
+        const uint64_t j0 = units * si / nsub, j1 = units * (si + 1) / nsub;
         const uint64_t recs = nsub == 1 ? recs_level
                                         : (j1 - j0) * unit_recs - (has_last && j1 == units ? last_short : 0);
-        folded += recs;
         SegView v = view_of(h, g, 0, g.ntiles);
         v.pass = pass;
         v.upt = upt;

@@ -1938,12 +1938,20 @@ __host__ __device__ constexpr size_t ring_bytes(bool pareto) {
 
 struct __align__(16) StageMeta {
     uint32_t gf[SW_MAX_QUERIES];  // grid-wide "feasible seen" flags, copied by the stage's TMA
+    // ... and right behind them the grid-wide closest-tier keys, complemented (~key of the
+    // best closest-tier record any block has seen; 0 = none): a block's own closest bound
+    // starts at ~0 and tightens slowly where a query is infeasible in its shard, the grid's
+    // is known after a few stages
+    unsigned long long gneg[SW_MAX_QUERIES];
     uint64_t pos0;       // flat slot of the stage's first record
     uint32_t cnt;        // records in the stage; 0 = end of stream
     uint16_t all_valid;  // no tile padding inside: skip per-record range checks
     uint16_t pad;
 };
 static_assert(sizeof(uint32_t) * SW_MAX_QUERIES % 16 == 0, "flags are bulk-copied");
+// global layout per request (pa.gfeas): gf[SW_MAX_QUERIES] u32 then gneg[SW_MAX_QUERIES] u64
+constexpr uint32_t kGSelWords = SW_MAX_QUERIES + 2 * SW_MAX_QUERIES;
+static_assert(offsetof(StageMeta, gneg) == sizeof(uint32_t) * SW_MAX_QUERIES, "gf and gneg are one bulk copy");
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -2018,7 +2026,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
     if (jobs) {  // fleet: request y (never with PARETO)
         v = jobs[blockIdx.y].v;
         P = jobs[blockIdx.y].P;
-        if (pa.gfeas) pa.gfeas += (uint64_t)blockIdx.y * SW_MAX_QUERIES;
+        if (pa.gfeas) pa.gfeas += (uint64_t)blockIdx.y * kGSelWords;
     }
     const uint64_t out_block = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
     constexpr int NQA = NQ > 0 ? NQ : 1;
@@ -2142,7 +2150,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA write
         // the grid-wide feasibility flags ride on the stage's own transaction: no thread
         // waits on a global load
-        const uint32_t gf_bytes = (NQ > 0 && pa.gfeas) ? (uint32_t)sizeof(meta[slot].gf) : 0u;
+        const uint32_t gf_bytes =
+            (NQ > 0 && pa.gfeas) ? (uint32_t)(sizeof(meta[slot].gf) + sizeof(meta[slot].gneg)) : 0u;
         mbar_expect_tx(&full_bar[slot], cnt * (uint32_t)sizeof(Rec4) + gf_bytes);
         if (gf_bytes) tma_bulk_g2s(meta[slot].gf, pa.gfeas, gf_bytes, &full_bar[slot]);
         tma_bulk_g2s(ring + (size_t)slot * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4), &full_bar[slot]);
@@ -2212,7 +2221,8 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                     default: need = pred_pass<7, OBJ>(r, valid, thr, obj_q, slo_t, slo_s, bud); break;
                 }
                 if (__any_sync(0xffffffffu, !anyf)) {  // closest tier still open somewhere
-                    const unsigned long long vmax = s_vt[q];
+                    const unsigned long long gv = pa.gfeas ? ~mt.gneg[q] : ~0ull;
+                    const unsigned long long vmax = s_vt[q] < gv ? s_vt[q] : gv;
 #pragma unroll
                     for (int u = 0; u < kRPT; u++)
                         need |= (uint32_t)(valid[u] & !anyf & (closest_pack(r[u], slo_t, slo_s, bud) <= vmax)) << u;
@@ -2230,8 +2240,11 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                                 if (!bf[q] && pa.gfeas) atomicOr(&pa.gfeas[q], 1u);
                                 atomicMax(&s_thr[q], (unsigned long long)obj_key<OBJ>(obj_q, r[u]));
                             } else {
-                                atomicMin(&s_vt[q], (unsigned long long)closest_pack(r[u], P.q[q].slo_t,
-                                                                                     P.q[q].slo_s, P.q[q].budget));
+                                const unsigned long long ck =
+                                    closest_pack(r[u], P.q[q].slo_t, P.q[q].slo_s, P.q[q].budget);
+                                if (ck < atomicMin(&s_vt[q], ck) && pa.gfeas)  // a block improvement
+                                    atomicMax(reinterpret_cast<unsigned long long*>(pa.gfeas + SW_MAX_QUERIES) + q,
+                                              ~ck);
                             }
                             bf[q] = f;
                         }

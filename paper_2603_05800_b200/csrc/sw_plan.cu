@@ -87,7 +87,7 @@ struct sw_plan {
     PPoint* d_front = nullptr;
     uint64_t front_n = 0;
     uint64_t front_cap = 1ull << 17;
-    uint64_t surv_cap = 1ull << 17;
+    uint64_t surv_cap = 1ull << 18;  // 2^17 overflowed in the first passes of 3 G-record C5 shards (a refold: 2x the scan)
     PPoint* d_work = nullptr;  // front_cap + surv_cap
     PPoint* d_tmp = nullptr;   // front_cap + surv_cap (the merge's t-sorted input)
     uint32_t* d_rhist = nullptr;  // kRedBuckets (the merge's bucket sort)
@@ -123,7 +123,7 @@ struct sw_plan {
     bool trace = false;             // SW_TRACE=1: per-phase CUDA-event times of each select on stderr
     std::vector<std::pair<const char*, cudaEvent_t>> tr;  // (phase that ENDS at the event, event)
     uint64_t* d_counts = nullptr;
-    uint32_t* d_gfeas = nullptr;  // [SW_MAX_QUERIES] grid-wide "feasible seen" flags of a select
+    uint32_t* d_gfeas = nullptr;  // grid-wide "feasible seen" flags + closest keys of a select (kGSelWords)
     GreedyOut* d_greedy = nullptr;
     std::vector<uint32_t> level_score;  // for the greedy baseline (host copy of the input)
 
@@ -797,7 +797,7 @@ static sw_status create_common(sw_plan* h, const sw_runtime* rt) {
     // [R+3] pad overflow flag of the asynchronous merge, [R+4, R+4+kStatusWords) the
     // max-reduced status words of a multi-rank call
     if ((st = alloc_n(h, &h->d_counts, (uint64_t)h->nranks + 4 + kStatusWords, "counts")) < 0) return (st);
-    if ((st = alloc_n(h, &h->d_gfeas, SW_MAX_QUERIES, "select flags")) < 0) return (st);
+    if ((st = alloc_n(h, &h->d_gfeas, kGSelWords, "select flags")) < 0) return (st);
     if ((st = alloc_n(h, &h->d_greedy, 1, "greedy result")) < 0) return (st);
         if (h->nranks > 1)
         if ((st = alloc_n(h, &h->d_gather, h->front_cap * (uint64_t)h->nranks, "front gather")) < 0) return (st);
@@ -1564,7 +1564,7 @@ static sw_status select_impl(sw_plan* h, uint32_t nq, const sw_query* qs, sw_sel
     uint32_t np = 0;
     std::vector<size_t> fused;
     trace_mark(h, "start");
-    CK(h, cudaMemsetAsync(h->d_gfeas, 0, sizeof(uint32_t) * SW_MAX_QUERIES, h->stream));
+    CK(h, cudaMemsetAsync(h->d_gfeas, 0, sizeof(uint32_t) * kGSelWords, h->stream));
     bool seeded = h->front_n > 0;
     for (size_t si_ = 0; si_ < h->segs.size(); si_++) {
         Segment& g = h->segs[si_];
@@ -2715,7 +2715,7 @@ extern "C" sw_status sw_fleet_create(uint32_t n, const sw_profile_tables* tables
         !alloc((void**)&f->d_win, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n) ||
         !alloc((void**)&f->d_win_all, sizeof(Cand) * SW_MAX_QUERIES * (size_t)n * f->nranks) ||
         !alloc((void**)&f->d_det, sizeof(DetailOut) * (size_t)n) ||
-        !alloc((void**)&f->d_gfeas, sizeof(uint32_t) * SW_MAX_QUERIES * (size_t)n)) {
+        !alloc((void**)&f->d_gfeas, sizeof(uint32_t) * kGSelWords * (size_t)n)) {
         cudaGetLastError();
         return bail(fail(nullptr, SW_ENOMEM, "fleet scratch allocation failed"));
     }
@@ -2838,7 +2838,7 @@ extern "C" sw_status sw_fleet_select(sw_fleet* f, const sw_query* queries, sw_se
         slots += g.ntiles * kTileRows * p->row;
     }
     CK(h, cudaMemcpyAsync(f->d_sjobs, jobs.data(), sizeof(ScanJob) * n, cudaMemcpyHostToDevice, f->stream));
-    CK(h, cudaMemsetAsync(f->d_gfeas, 0, sizeof(uint32_t) * SW_MAX_QUERIES * n, f->stream));
+    CK(h, cudaMemsetAsync(f->d_gfeas, 0, sizeof(uint32_t) * kGSelWords * n, f->stream));
     ParetoArgs pa{};
     pa.gfeas = f->d_gfeas;
     CK(h, cudaEventRecord(f->ev[2], f->stream));

@@ -1943,20 +1943,15 @@ struct __align__(16) StageMeta {
     // starts at ~0 and tightens slowly where a query is infeasible in its shard, the grid's
     // is known after a few stages
     unsigned long long gneg[SW_MAX_QUERIES];
-    // ... and the grid-wide best feasible prefilter key (obj_key; 0 = none): a block's own
-    // threshold starts at 0 and every record of its first stages passes
-    unsigned long long gpos[SW_MAX_QUERIES];
     uint64_t pos0;       // flat slot of the stage's first record
     uint32_t cnt;        // records in the stage; 0 = end of stream
     uint16_t all_valid;  // no tile padding inside: skip per-record range checks
     uint16_t pad;
 };
 static_assert(sizeof(uint32_t) * SW_MAX_QUERIES % 16 == 0, "flags are bulk-copied");
-// global layout per request (pa.gfeas): gf[SW_MAX_QUERIES] u32, gneg and gpos[SW_MAX_QUERIES] u64
-constexpr uint32_t kGSelWords = SW_MAX_QUERIES + 4 * SW_MAX_QUERIES;
-static_assert(offsetof(StageMeta, gneg) == sizeof(uint32_t) * SW_MAX_QUERIES &&
-                  offsetof(StageMeta, gpos) == offsetof(StageMeta, gneg) + 8 * SW_MAX_QUERIES,
-              "gf, gneg and gpos are one bulk copy");
+// global layout per request (pa.gfeas): gf[SW_MAX_QUERIES] u32 then gneg[SW_MAX_QUERIES] u64
+constexpr uint32_t kGSelWords = SW_MAX_QUERIES + 2 * SW_MAX_QUERIES;
+static_assert(offsetof(StageMeta, gneg) == sizeof(uint32_t) * SW_MAX_QUERIES, "gf and gneg are one bulk copy");
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -2156,9 +2151,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
         // the grid-wide feasibility flags ride on the stage's own transaction: no thread
         // waits on a global load
         const uint32_t gf_bytes =
-            (NQ > 0 && pa.gfeas)
-                ? (uint32_t)(sizeof(meta[slot].gf) + sizeof(meta[slot].gneg) + sizeof(meta[slot].gpos))
-                : 0u;
+            (NQ > 0 && pa.gfeas) ? (uint32_t)(sizeof(meta[slot].gf) + sizeof(meta[slot].gneg)) : 0u;
         mbar_expect_tx(&full_bar[slot], cnt * (uint32_t)sizeof(Rec4) + gf_bytes);
         if (gf_bytes) tma_bulk_g2s(meta[slot].gf, pa.gfeas, gf_bytes, &full_bar[slot]);
         tma_bulk_g2s(ring + (size_t)slot * kStageRecs, v.recs + pos0, cnt * (uint32_t)sizeof(Rec4), &full_bar[slot]);
@@ -2212,7 +2205,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                 //    the block's best feasible key;
                 //  - before that, only records whose startup+stall violation does not
                 //    exceed the block's best closest-tier violation.
-                const unsigned long long thr = pa.gfeas && mt.gpos[q] > s_thr[q] ? mt.gpos[q] : s_thr[q];
+                const unsigned long long thr = s_thr[q];
                 const bool anyf = (thr != 0) | bf[q] | (pa.gfeas != nullptr && mt.gf[q] != 0);
                 const uint64_t slo_t = P.q[q].slo_t, slo_s = P.q[q].slo_s, bud = P.q[q].budget;
                 // only the bounds the query actually sets are compared (uniform dispatch)
@@ -2245,10 +2238,7 @@ __global__ void __launch_bounds__(kScanBlock, 1) scan_kernel(SegView v, SelParam
                             br[q] = r[u];
                             if (f) {
                                 if (!bf[q] && pa.gfeas) atomicOr(&pa.gfeas[q], 1u);
-                                const unsigned long long kk = obj_key<OBJ>(obj_q, r[u]);
-                                if (kk > atomicMax(&s_thr[q], kk) && pa.gfeas)  // a block improvement
-                                    atomicMax(reinterpret_cast<unsigned long long*>(pa.gfeas + 3 * SW_MAX_QUERIES) + q,
-                                              kk);
+                                atomicMax(&s_thr[q], (unsigned long long)obj_key<OBJ>(obj_q, r[u]));
                             } else {
                                 const unsigned long long ck =
                                     closest_pack(r[u], P.q[q].slo_t, P.q[q].slo_s, P.q[q].budget);

@@ -1650,8 +1650,14 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
 // end]) so that x's position in the front is a map load plus a search of one cell's
 // range (usually empty) instead of an 11-step binary search of dependent smem loads.
 // 24 warps per block (one block per SM: the front copy is shared by all of them).
-constexpr uint32_t kExactFront = 2048;  // front points staged in smem (larger fronts: from L2)
-constexpr uint32_t kExactList = 128;    // per-warp survivor list
+#ifndef SW_EXACT_FRONT
+#define SW_EXACT_FRONT 2048
+#endif
+#ifndef SW_EXACT_LIST
+#define SW_EXACT_LIST 128
+#endif
+constexpr uint32_t kExactFront = SW_EXACT_FRONT;  // front points staged in smem (larger fronts: from L2)
+constexpr uint32_t kExactList = SW_EXACT_LIST;    // per-warp survivor list
 constexpr int kExactThreads = 768;
 constexpr int kExactWarps = kExactThreads / 32;
 #ifndef SW_EXACT_NEAR

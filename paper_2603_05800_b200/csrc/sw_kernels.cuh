@@ -1651,10 +1651,10 @@ struct ParetoArgs {  // scan auxiliaries: Pareto filter state + grid-wide select
 // range (usually empty) instead of an 11-step binary search of dependent smem loads.
 // 24 warps per block (one block per SM: the front copy is shared by all of them).
 #ifndef SW_EXACT_FRONT
-#define SW_EXACT_FRONT 2048
+#define SW_EXACT_FRONT 4096  // C5 fronts (3021 points) in smem with their staircases: C5 182 -> 177 ms
 #endif
 #ifndef SW_EXACT_LIST
-#define SW_EXACT_LIST 128
+#define SW_EXACT_LIST 64  // (128 and 64 measured equal on C2/C3)
 #endif
 constexpr uint32_t kExactFront = SW_EXACT_FRONT;  // front points staged in smem (larger fronts: from L2)
 constexpr uint32_t kExactList = SW_EXACT_LIST;    // per-warp survivor list
